@@ -1,0 +1,486 @@
+// C entry points over the UNMODIFIED reference sources — TEST INFRASTRUCTURE.
+//
+// Built by oracle/Makefile together with /root/reference/proj/src/{geometry,
+// accel_tree,tracer,emission,air_absorption,image_sources,rir,mesh_gen,
+// shoebox}.cpp (compiled in place, against the from-scratch Eigen subset in
+// oracle/eigen_shim) into oracle/_ref/libroomray_ref.so.  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+// load it.  Every function below only marshals plain arrays into the
+// reference's own types and calls the reference's public API:
+//   build_tree            accel_tree.hpp:38
+//   nearest_hit(_brute)   accel_tree.hpp:50-55
+//   trace / step          tracer.hpp:43-52   (strided subsets: the trace()
+//                         loop of tracer.cpp:108-132 driven over a subset)
+//   build_image_sources   image_sources.hpp:58-61
+//   build_pulse_trains / synthesize / design_band_filter  rir.hpp:33-45
+//   air_beta_bands        air_absorption.hpp:30
+//   enumerate_images      shoebox.hpp:43
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "roomray/accel_tree.hpp"
+#include "roomray/air_absorption.hpp"
+#include "roomray/emission.hpp"
+#include "roomray/image_sources.hpp"
+#include "roomray/mesh_gen.hpp"
+#include "roomray/rir.hpp"
+#include "roomray/shoebox.hpp"
+#include "roomray/tracer.hpp"
+
+using namespace roomray;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+TriangleMesh make_mesh(const double* verts, int64_t nv, const int32_t* tris,
+                       int64_t nf, const double* alpha, int32_t nmat) {
+  TriangleMesh mesh;
+  mesh.vertices.resize(nv);
+  for (int64_t i = 0; i < nv; ++i)
+    mesh.vertices[i] = Vec3(verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]);
+  mesh.faces.resize(nf);
+  for (int64_t f = 0; f < nf; ++f)
+    mesh.faces[f] = {tris[4 * f], tris[4 * f + 1], tris[4 * f + 2],
+                     tris[4 * f + 3]};
+  mesh.materials.resize(nmat);
+  for (int32_t m = 0; m < nmat; ++m) {
+    mesh.materials[m].name = "m" + std::to_string(m);
+    for (int b = 0; b < kNumBands; ++b)
+      mesh.materials[m].absorption[b] = alpha[kNumBands * m + b];
+  }
+  return mesh;
+}
+
+struct RefScene {
+  TriangleMesh mesh;
+  AccelTree tree;
+};
+
+struct RefTrace {
+  TraceResult result;
+  int64_t total_hist = 0;
+  int64_t ray_bounces = 0;
+};
+
+struct RefImages {
+  std::vector<ImageSource> images;
+  int64_t total_path = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* rref_last_error() { return g_err.c_str(); }
+
+// Scene = mesh + reference tree (build_tree, accel_tree.cpp:70-87).
+void* rref_scene_create(const double* verts, int64_t nv, const int32_t* tris,
+                        int64_t nf, const double* alpha, int32_t nmat,
+                        int validate) {
+  RefScene* s = nullptr;
+  int rc = guarded([&] {
+    auto scene = std::make_unique<RefScene>();
+    scene->mesh = make_mesh(verts, nv, tris, nf, alpha, nmat);
+    if (validate) scene->mesh.validate();
+    scene->tree = build_tree(scene->mesh);
+    s = scene.release();
+  });
+  return rc == 0 ? s : nullptr;
+}
+
+void rref_scene_destroy(void* h) { delete static_cast<RefScene*>(h); }
+
+int64_t rref_tree_size(void* h, int32_t* root, int32_t* depth) {
+  auto* s = static_cast<RefScene*>(h);
+  *root = s->tree.root;
+  *depth = s->tree.depth();
+  return static_cast<int64_t>(s->tree.nodes.size());
+}
+
+void rref_tree_nodes(void* h, int32_t* left, int32_t* right, int32_t* face,
+                     double* lo, double* hi) {
+  auto* s = static_cast<RefScene*>(h);
+  for (size_t i = 0; i < s->tree.nodes.size(); ++i) {
+    const TreeNode& n = s->tree.nodes[i];
+    left[i] = n.left;
+    right[i] = n.right;
+    face[i] = n.face_index;
+    for (int k = 0; k < 3; ++k) {
+      lo[3 * i + k] = n.box.min[k];
+      hi[3 * i + k] = n.box.max[k];
+    }
+  }
+}
+
+int rref_empty_tree_throws() {
+  TriangleMesh mesh;
+  return guarded([&] { build_tree(mesh); });
+}
+
+// nearest_hit (tree) or nearest_hit_brute for n rays.
+int rref_nearest_hit(void* h, const double* o, const double* d, int64_t n,
+                     int brute, int32_t* face, double* delta, double* point) {
+  auto* s = static_cast<RefScene*>(h);
+  return guarded([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      const Vec3 org(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+      const Vec3 dir(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+      const auto hit = brute ? nearest_hit_brute(s->mesh, org, dir)
+                             : nearest_hit(s->tree, s->mesh, org, dir);
+      face[i] = hit ? hit->face_index : -1;
+      delta[i] = hit ? hit->delta : 0.0;
+      for (int k = 0; k < 3; ++k) point[3 * i + k] = hit ? hit->point[k] : 0.0;
+    }
+  });
+}
+
+int rref_intersect_sphere(const double* o, const double* d, const double* c,
+                          double r, double* out) {
+  const auto s = intersect_sphere(Vec3(o[0], o[1], o[2]), Vec3(d[0], d[1], d[2]),
+                                  Vec3(c[0], c[1], c[2]), r);
+  *out = s ? *s : -1.0;
+  return s ? 1 : 0;
+}
+
+void rref_fibonacci(int n, double* out) {
+  const auto dirs = fibonacci_directions(n);
+  for (int k = 0; k < n; ++k)
+    for (int a = 0; a < 3; ++a) out[3 * k + a] = dirs[k][a];
+}
+
+// trace(): tracer.cpp:108-149.  When stride > 1, the same loop is driven over
+// the ray subset k = first + i*stride (i < count) of the full-N Fibonacci
+// lattice, with max_range resolved against the full N (tracer.cpp:117-118).
+// stride <= 0 calls trace() itself; stride >= 1 runs the subset driver, which
+// also counts ray-bounces (one per step_ray call on a live ray).
+// Capture ray indices are reported as global lattice indices.
+void* rref_trace(void* h, const double* src, int32_t ray_count,
+                 const double* recv, double radius, int32_t max_iterations,
+                 double max_range, int32_t threads, int64_t first,
+                 int64_t stride, int64_t count) {
+  auto* s = static_cast<RefScene*>(h);
+  RefTrace* out = nullptr;
+  int rc = guarded([&] {
+    auto t = std::make_unique<RefTrace>();
+    SourceConfig source;
+    source.position = Vec3(src[0], src[1], src[2]);
+    source.ray_count = ray_count;
+    Receiver receiver{Vec3(recv[0], recv[1], recv[2]), radius};
+    TraceConfig config;
+    config.max_iterations = max_iterations;
+    config.max_range = max_range;
+    config.thread_count = threads;
+    if (stride <= 0) {
+      t->result = trace(s->mesh, s->tree, source, receiver, config);
+    } else {
+      if (receiver.radius <= 0.0)
+        throw std::invalid_argument("receiver radius must be > 0");
+      source.validate();
+      const auto all = emit(source);
+      std::vector<Ray> rays;
+      std::vector<int> global;
+      for (int64_t i = 0; i < count; ++i) {
+        const int64_t k = first + i * stride;
+        if (k >= ray_count) break;
+        rays.push_back(all[k]);
+        global.push_back(static_cast<int>(k));
+      }
+      TraceConfig resolved = config;
+      resolved.max_range = config.resolved_max_range(receiver, ray_count);
+      TraceResult& result = t->result;
+      result.max_range = resolved.max_range;
+      size_t live = rays.size();
+      while (live > 0 && result.iterations < config.max_iterations) {
+        auto caps = step(rays, s->mesh, &s->tree, receiver, resolved);
+        for (auto& c : caps) {
+          c.ray_index = global[c.ray_index];
+          result.captures.push_back(std::move(c));
+        }
+        ++result.iterations;
+        live = 0;
+        for (const Ray& r : rays) live += r.alive ? 1 : 0;
+      }
+      result.truncated = live > 0;
+      for (const Ray& r : rays) {
+        if (!r.alive && r.path_length > resolved.max_range)
+          ++result.out_of_range;
+        else if (!r.alive)
+          ++result.escaped;
+        t->ray_bounces += static_cast<int64_t>(r.face_history.size());
+      }
+      t->ray_bounces += static_cast<int64_t>(result.escaped);
+      std::sort(result.captures.begin(), result.captures.end(),
+                [](const Capture& a, const Capture& b) {
+                  if (a.ray_index != b.ray_index)
+                    return a.ray_index < b.ray_index;
+                  return a.path_length < b.path_length;
+                });
+    }
+    for (const Capture& c : t->result.captures)
+      t->total_hist += static_cast<int64_t>(c.face_history.size());
+    out = t.release();
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void rref_trace_info(void* h, int32_t* iterations, int32_t* truncated,
+                     int64_t* escaped, int64_t* out_of_range,
+                     double* max_range, int64_t* n_captures,
+                     int64_t* total_hist, int64_t* ray_bounces) {
+  auto* t = static_cast<RefTrace*>(h);
+  *iterations = t->result.iterations;
+  *truncated = t->result.truncated ? 1 : 0;
+  *escaped = static_cast<int64_t>(t->result.escaped);
+  *out_of_range = static_cast<int64_t>(t->result.out_of_range);
+  *max_range = t->result.max_range;
+  *n_captures = static_cast<int64_t>(t->result.captures.size());
+  *total_hist = t->total_hist;
+  *ray_bounces = t->ray_bounces;
+}
+
+void rref_trace_captures(void* h, int32_t* ray, double* point, double* dir,
+                         double* path, double* mult, int64_t* hist_off,
+                         int32_t* hist) {
+  auto* t = static_cast<RefTrace*>(h);
+  int64_t off = 0;
+  for (size_t i = 0; i < t->result.captures.size(); ++i) {
+    const Capture& c = t->result.captures[i];
+    ray[i] = c.ray_index;
+    for (int k = 0; k < 3; ++k) {
+      point[3 * i + k] = c.point[k];
+      dir[3 * i + k] = c.incoming_dir[k];
+    }
+    path[i] = c.path_length;
+    for (int b = 0; b < kNumBands; ++b) mult[kNumBands * i + b] = c.band_multiplier[b];
+    hist_off[i] = off;
+    for (int f : c.face_history) hist[off++] = f;
+  }
+  hist_off[t->result.captures.size()] = off;
+}
+
+void rref_trace_free(void* h) { delete static_cast<RefTrace*>(h); }
+
+// build_image_sources over captures given as arrays (image_sources.cpp:154).
+void* rref_image_sources(void* hs, int64_t n, const int32_t* ray,
+                         const double* point, const double* dir,
+                         const double* path, const double* mult,
+                         const int64_t* hist_off, const int32_t* hist,
+                         int32_t total_rays, const double* air4,
+                         const double* recv, double tol_scale,
+                         int merge_coplanar) {
+  auto* s = static_cast<RefScene*>(hs);
+  RefImages* out = nullptr;
+  int rc = guarded([&] {
+    std::vector<Capture> caps(n);
+    for (int64_t i = 0; i < n; ++i) {
+      Capture& c = caps[i];
+      c.ray_index = ray[i];
+      c.point = Vec3(point[3 * i], point[3 * i + 1], point[3 * i + 2]);
+      c.incoming_dir = Vec3(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]);
+      c.path_length = path[i];
+      for (int b = 0; b < kNumBands; ++b) c.band_multiplier[b] = mult[kNumBands * i + b];
+      c.face_history.assign(hist + hist_off[i], hist + hist_off[i + 1]);
+    }
+    AirModel air;
+    air.enabled = air4[0] != 0.0;
+    air.temperature_c = air4[1];
+    air.relative_humidity = air4[2];
+    air.pressure_kpa = air4[3];
+    ClusterOptions opt;
+    opt.tol_scale = tol_scale;
+    opt.merge_coplanar = merge_coplanar != 0;
+    auto r = std::make_unique<RefImages>();
+    r->images = build_image_sources(caps, total_rays, air,
+                                    Vec3(recv[0], recv[1], recv[2]), s->mesh,
+                                    s->tree, opt);
+    for (const auto& im : r->images) r->total_path += im.face_path.size();
+    out = r.release();
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void rref_images_info(void* h, int64_t* n, int64_t* total_path) {
+  auto* r = static_cast<RefImages*>(h);
+  *n = static_cast<int64_t>(r->images.size());
+  *total_path = r->total_path;
+}
+
+void rref_images_get(void* h, double* pos, double* dist, double* energy,
+                     double* mult, int32_t* ray_count, int32_t* order,
+                     int32_t* has_proj, double* proj, int64_t* path_off,
+                     int32_t* path) {
+  auto* r = static_cast<RefImages*>(h);
+  int64_t off = 0;
+  for (size_t i = 0; i < r->images.size(); ++i) {
+    const ImageSource& im = r->images[i];
+    for (int k = 0; k < 3; ++k) pos[3 * i + k] = im.position[k];
+    dist[i] = im.distance;
+    for (int b = 0; b < kNumBands; ++b) {
+      energy[kNumBands * i + b] = im.band_energy[b];
+      mult[kNumBands * i + b] = im.band_multiplier[b];
+    }
+    ray_count[i] = im.ray_count;
+    order[i] = im.order;
+    has_proj[i] = im.projection ? 1 : 0;
+    for (int k = 0; k < 3; ++k) proj[3 * i + k] = im.projection ? (*im.projection)[k] : 0.0;
+    path_off[i] = off;
+    for (int f : im.face_path) path[off++] = f;
+  }
+  path_off[r->images.size()] = off;
+}
+
+void rref_images_free(void* h) { delete static_cast<RefImages*>(h); }
+
+void rref_air_beta_bands(const double* air4, double* beta) {
+  AirModel air;
+  air.enabled = air4[0] != 0.0;
+  air.temperature_c = air4[1];
+  air.relative_humidity = air4[2];
+  air.pressure_kpa = air4[3];
+  const BandArray b = air_beta_bands(air);
+  for (int i = 0; i < kNumBands; ++i) beta[i] = b[i];
+}
+
+double rref_air_alpha(const double* air4, double f) {
+  AirModel air;
+  air.enabled = air4[0] != 0.0;
+  air.temperature_c = air4[1];
+  air.relative_humidity = air4[2];
+  air.pressure_kpa = air4[3];
+  return air_alpha_db_per_m(air, f);
+}
+
+int rref_band_filter(int band, double fs, double* taps) {
+  return guarded([&] {
+    const auto k = design_band_filter(band, fs);
+    std::memcpy(taps, k.data(), sizeof(double) * k.size());
+  });
+}
+
+// build_pulse_trains + synthesize (rir.cpp:9-96) from image distances and
+// band energies; writes the broadband response, returns its length.
+// If out == nullptr only the length is computed.  band_mask selects which
+// bands' trains are populated (the per-band trick of tests/test_rir.cpp:44).
+int64_t rref_synthesize(int64_t n, const double* dist, const double* energy,
+                        double c, double fs, int32_t band_mask, double* out,
+                        int64_t cap) {
+  int64_t len = -1;
+  int rc = guarded([&] {
+    std::vector<ImageSource> images(n);
+    for (int64_t i = 0; i < n; ++i) {
+      images[i].distance = dist[i];
+      for (int b = 0; b < kNumBands; ++b)
+        images[i].band_energy[b] = energy[kNumBands * i + b];
+    }
+    PulseTrains trains = build_pulse_trains(images, c);
+    for (int b = 0; b < kNumBands; ++b)
+      if (!(band_mask & (1 << b))) trains[b].events.clear();
+    const auto rir = synthesize(trains, fs);
+    len = static_cast<int64_t>(rir.samples.size());
+    if (out) {
+      const int64_t m = std::min(len, cap);
+      std::memcpy(out, rir.samples.data(), sizeof(double) * m);
+    }
+  });
+  return rc == 0 ? len : -1;
+}
+
+// Shoebox lattice oracle (shoebox.cpp:43-116): count, then fetch.
+void* rref_lattice(const double* dims, const double* walls_alpha /*6x8*/,
+                   const double* src, const double* recv, double max_distance,
+                   double radius, const double* air4, int64_t* n) {
+  std::vector<OracleImageSource>* out = nullptr;
+  int rc = guarded([&] {
+    ShoeBox box;
+    box.dimensions = Vec3(dims[0], dims[1], dims[2]);
+    for (int w = 0; w < 6; ++w)
+      for (int b = 0; b < kNumBands; ++b)
+        box.walls[w].absorption[b] = walls_alpha[kNumBands * w + b];
+    AirModel air;
+    air.enabled = air4[0] != 0.0;
+    air.temperature_c = air4[1];
+    air.relative_humidity = air4[2];
+    air.pressure_kpa = air4[3];
+    out = new std::vector<OracleImageSource>(enumerate_images(
+        box, Vec3(src[0], src[1], src[2]), Vec3(recv[0], recv[1], recv[2]),
+        max_distance, radius, air));
+    *n = static_cast<int64_t>(out->size());
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void rref_lattice_get(void* h, double* pos, double* dist, int32_t* order,
+                      double* energy) {
+  auto* v = static_cast<std::vector<OracleImageSource>*>(h);
+  for (size_t i = 0; i < v->size(); ++i) {
+    const auto& im = (*v)[i];
+    for (int k = 0; k < 3; ++k) pos[3 * i + k] = im.position[k];
+    dist[i] = im.distance;
+    order[i] = im.order;
+    for (int b = 0; b < kNumBands; ++b) energy[kNumBands * i + b] = im.band_energy[b];
+  }
+}
+
+void rref_lattice_free(void* h) {
+  delete static_cast<std::vector<OracleImageSource>*>(h);
+}
+
+// Reference mesh generators (mesh_gen.cpp) — used to pin scene fixtures.
+// kind 0: box(dims=p[0..2]); 1: icosphere(level); 2: tetra(log2 faces).
+void* rref_mesh_gen(int kind, const double* p, int level, int64_t* nv,
+                    int64_t* nf) {
+  TriangleMesh* out = nullptr;
+  int rc = guarded([&] {
+    Material m;
+    m.name = "g";
+    TriangleMesh mesh;
+    if (kind == 0) mesh = make_box_mesh(Vec3(p[0], p[1], p[2]), m);
+    else if (kind == 1) mesh = make_icosphere(level, m);
+    else mesh = make_subdivided_tetrahedron(level, m);
+    out = new TriangleMesh(std::move(mesh));
+    *nv = static_cast<int64_t>(out->vertices.size());
+    *nf = static_cast<int64_t>(out->faces.size());
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void rref_mesh_get(void* h, double* verts, int32_t* tris) {
+  auto* m = static_cast<TriangleMesh*>(h);
+  for (size_t i = 0; i < m->vertices.size(); ++i)
+    for (int k = 0; k < 3; ++k) verts[3 * i + k] = m->vertices[i][k];
+  for (size_t f = 0; f < m->faces.size(); ++f) {
+    tris[4 * f] = m->faces[f].a;
+    tris[4 * f + 1] = m->faces[f].b;
+    tris[4 * f + 2] = m->faces[f].c;
+    tris[4 * f + 3] = m->faces[f].material_id;
+  }
+}
+
+void rref_mesh_free(void* h) { delete static_cast<TriangleMesh*>(h); }
+
+int rref_hardware_threads() {
+  return static_cast<int>(std::thread::hardware_concurrency());
+}
+
+}  // extern "C"
