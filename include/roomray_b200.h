@@ -1,0 +1,210 @@
+/* roomray_b200 — C ABI of the B200-native specular ray / image-source engine.
+ *
+ * Drop-in boundary for the reference's hot path (reference = roomray, C++20,
+ * /root/reference/proj).  Every entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; all host buffers are caller-owned.
+ * Calls are synchronous with respect to the host unless the name ends in
+ * _async; a context owns one CUDA stream and is not thread-safe (use one
+ * context per thread/GPU).  Errors: every call returns an rr_status; the
+ * message of the last failure on the calling thread is rr_last_error().
+ * RR_INVALID_ARGUMENT corresponds to the reference's std::invalid_argument.
+ */
+#ifndef ROOMRAY_B200_H
+#define ROOMRAY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RR_NUM_BANDS 8
+
+typedef enum {
+  RR_OK = 0,
+  RR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  RR_RUNTIME = 2,          /* reference: other std::exception */
+  RR_CUDA = 3,
+  RR_NCCL = 4
+} rr_status;
+
+typedef struct rr_ctx rr_ctx;
+typedef struct rr_scene rr_scene;
+typedef struct rr_trace_result rr_trace_result;
+typedef struct rr_images rr_images;
+
+/* Reference-layout tree node (TreeNode, accel_tree.hpp:15-22): post-order,
+ * root last, leaves hold one face. */
+typedef struct {
+  double lo[3], hi[3];
+  int32_t left, right, face_index, pad;
+} rr_tree_node;
+
+/* SourceConfig (emission.hpp:14-20). */
+typedef struct {
+  double position[3];
+  int64_t ray_count;
+} rr_source;
+
+/* Receiver (tracer_types.hpp:21-24). */
+typedef struct {
+  double center[3];
+  double radius;
+} rr_receiver;
+
+/* TraceConfig (tracer.hpp:13-20) plus the ray-subset selector used for
+ * multi-GPU sharding: rays k = first + i*stride (i < count) of the N-ray
+ * lattice; stride <= 0 selects all N.  block > 0 selects block-cyclic
+ * sharding instead: blocks of `block` consecutive rays, block b owned by
+ * rank b % world; `first` is then the rank and `stride` the world size. */
+typedef struct {
+  int32_t max_iterations;  /* reference default 1000 */
+  double speed_of_sound;   /* reference default 343 */
+  double max_range;        /* <= 0: (r/2) sqrt(N) of receiver 0 */
+  int64_t first, stride, count, block;
+  int32_t flags;           /* RR_TRACE_* */
+  /* Optional host array (count x 3) of initial directions for the selected
+   * rays, the Ray span of step() (tracer.hpp:43); NULL = the Fibonacci
+   * lattice evaluated on the device (emission.cpp:17-29, correctly rounded
+   * sin/cos). */
+  const double* directions;
+} rr_trace_config;
+
+#define RR_TRACE_NO_SMEM_CACHE 1 /* traverse without the shared-memory top-level cache */
+#define RR_TRACE_KEEP_UNSORTED 2 /* skip the capture sort (timing only) */
+
+/* Statistics of a trace (TraceResult, tracer.hpp:22-29). */
+typedef struct {
+  int32_t iterations;
+  int32_t truncated;
+  int64_t escaped;
+  int64_t out_of_range;
+  double max_range;
+  int64_t n_captures;
+  int64_t total_history; /* sum of capture face-path lengths */
+  int64_t ray_bounces;   /* nearest-hit queries executed on live rays */
+  int64_t n_rays;        /* rays traced by this call */
+} rr_trace_stats;
+
+/* AirModel (air_absorption.hpp:10-23). */
+typedef struct {
+  int32_t enabled;
+  double temperature_c, relative_humidity, pressure_kpa;
+} rr_air;
+
+/* ClusterOptions (image_sources.hpp:25-31). */
+typedef struct {
+  double tol_scale;       /* reference default 1e-6 */
+  int32_t merge_coplanar; /* ClusterOptions default 0; RunConfig default 1 */
+} rr_cluster_options;
+
+const char* rr_last_error(void);
+const char* rr_version(void);
+
+/* ---------------------------------------------------------------- context */
+rr_status rr_ctx_create(int device, rr_ctx** out);
+rr_status rr_ctx_destroy(rr_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for event timing by callers. */
+void* rr_ctx_stream(rr_ctx* ctx);
+/* Number of this library's kernels launched on the context so far. */
+int64_t rr_ctx_launches(rr_ctx* ctx);
+
+/* ---------------------------------------------------------------- scene
+ * TriangleMesh (geometry.hpp:60-77) + build_tree (accel_tree.hpp:38).
+ * verts: nv*3 f64; tris: nf*4 i32 (a, b, c, material); alpha: nmat*8 f64.
+ * Uploads the mesh, validates it on the device (TriangleMesh::validate,
+ * geometry.cpp:47-75) when validate != 0, and builds the median-split tree on
+ * the device.  nf == 0 fails like build_tree (accel_tree.cpp:71-73). */
+rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv,
+                          const int32_t* tris, int64_t nf, const double* alpha,
+                          int32_t nmat, int32_t validate, rr_scene** out);
+rr_status rr_scene_destroy(rr_scene* scene);
+/* AccelTree::node_count / depth / root (accel_tree.hpp:26-34). */
+rr_status rr_scene_tree_info(rr_scene* scene, int64_t* n_nodes, int32_t* root,
+                             int32_t* depth);
+/* Download the reference-layout tree: 2*nf-1 nodes. */
+rr_status rr_scene_tree(rr_scene* scene, rr_tree_node* nodes);
+/* Face normals (TriangleMesh::face_normal, geometry.cpp:9-14), nf*3 f64. */
+rr_status rr_scene_normals(rr_scene* scene, double* normals);
+/* Seconds spent in the device tree build of this scene (CUDA events). */
+double rr_scene_build_ms(rr_scene* scene);
+
+/* ---------------------------------------------------------------- queries
+ * nearest_hit (accel_tree.hpp:50-51) for n rays; brute != 0 selects
+ * nearest_hit_brute (accel_tree.hpp:54-55).  face[i] = -1 for no hit. */
+rr_status rr_nearest_hit_batch(rr_scene* scene, const double* origins,
+                               const double* dirs, int64_t n, int32_t brute,
+                               int32_t* face, double* delta, double* point);
+
+/* ---------------------------------------------------------------- trace
+ * trace (tracer.hpp:50-52) with n_recv receivers traced on the same
+ * trajectories (a receiver is transparent, tracer.cpp:27-29).  Captures stay
+ * on the device until fetched. */
+rr_status rr_trace(rr_scene* scene, const rr_source* source,
+                   const rr_receiver* receivers, int32_t n_recv,
+                   const rr_trace_config* config, rr_trace_result** out);
+rr_status rr_trace_stats_get(rr_trace_result* res, rr_trace_stats* stats);
+/* Captures sorted by (receiver, ray, path) (tracer.cpp:143-147).  Arrays:
+ * recv/ray n, point/dir n*3, path n, mult n*8, hist_off n+1, hist
+ * total_history.  Any pointer may be NULL to skip that field. */
+rr_status rr_trace_captures(rr_trace_result* res, int32_t* recv, int32_t* ray,
+                            double* point, double* dir, double* path,
+                            double* mult, int64_t* hist_off, int32_t* hist);
+/* Device time of the trace kernel itself (ms, CUDA events). */
+double rr_trace_kernel_ms(rr_trace_result* res);
+rr_status rr_trace_destroy(rr_trace_result* res);
+
+/* ---------------------------------------------------------------- images
+ * build_image_sources (image_sources.hpp:58-61) on the device for receiver
+ * `recv` of a trace.  total_rays = N of the lattice (energy n/N,
+ * image_sources.cpp:138). */
+rr_status rr_build_image_sources(rr_trace_result* res, int32_t recv,
+                                 int64_t total_rays, const rr_air* air,
+                                 const rr_cluster_options* opt,
+                                 rr_images** out);
+rr_status rr_images_info(rr_images* im, int64_t* n, int64_t* total_path);
+/* Sorted by (order, distance, face path) (image_sources.cpp:163-168). */
+rr_status rr_images_get(rr_images* im, double* pos, double* dist,
+                        double* energy, double* mult, int32_t* ray_count,
+                        int32_t* order, int32_t* has_proj, double* proj,
+                        int64_t* path_off, int32_t* path);
+rr_status rr_images_destroy(rr_images* im);
+
+/* air_beta_bands (air_absorption.cpp:59-65), 8 values. */
+rr_status rr_air_beta_bands(const rr_air* air, double* beta);
+
+/* ---------------------------------------------------------------- IR
+ * build_pulse_trains + synthesize (rir.hpp:33-45), per band: events at
+ * sample lround(d/c*fs) with amplitude sqrt(E_b), binned into 8 histograms of
+ * `length` samples, then convolved with the 8 band filters of `taps` taps
+ * (design_band_filter, rir.cpp:32-58; reference: 1023).  Output: per-band
+ * responses band_ir (8*length, may be NULL) and their sum broadband (length,
+ * may be NULL).  Host buffers.  images from n arrays (dist n, energy n*8). */
+rr_status rr_synthesize(rr_ctx* ctx, int64_t n, const double* dist,
+                        const double* energy, double c, double fs,
+                        int32_t taps, int64_t length, double* band_ir,
+                        double* broadband);
+/* Same, from device-resident arrays; outputs stay in caller-provided device
+ * buffers (for multi-GPU reduction).  hist (8*length f64) receives the
+ * binned pulse trains; band_ir may be NULL to stop after binning. */
+rr_status rr_ir_bin_device(rr_ctx* ctx, int64_t n, const double* d_dist,
+                           const double* d_energy, double c, double fs,
+                           int64_t length, double* d_hist);
+rr_status rr_ir_filter_device(rr_ctx* ctx, const double* d_hist, double fs,
+                              int32_t taps, int64_t length, double* d_band_ir,
+                              double* d_broadband);
+/* Length of the reference's response (rir.cpp:78-80): llround(t_last*fs) +
+ * (taps-1)/2 + 1, or 0 without events. */
+rr_status rr_ir_reference_length(int64_t n, const double* dist, double c,
+                                 double fs, int32_t taps, int64_t* length);
+/* design_band_filter restated with a tap count. */
+rr_status rr_band_filter(int32_t band, double fs, int32_t taps, double* out);
+/* Image arrays of a device image set (for rr_ir_bin_device). */
+rr_status rr_images_device(rr_images* im, const double** d_dist,
+                           const double** d_energy, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROOMRAY_B200_H */

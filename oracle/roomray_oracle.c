@@ -674,7 +674,8 @@ ro_trace* ro_trace_run(const ro_scene* s, const double* src, int64_t ray_count,
     stride = 1;
     count = ray_count;
   }
-  if (first + (count - 1) * stride >= ray_count) count = (ray_count - first + stride - 1) / stride;
+  if (count <= 0 || first + (count - 1) * stride >= ray_count)
+    count = (ray_count - first + stride - 1) / stride;
   /* resolved_max_range tracer.cpp:10-15 (first receiver's radius) */
   double mr = max_range > 0.0 ? max_range : 0.5 * recv_radii[0] * sqrt((double)ray_count);
   if (threads < 1) threads = 1;

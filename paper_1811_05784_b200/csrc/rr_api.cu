@@ -1,0 +1,506 @@
+// C ABI entry points (include/roomray_b200.h): argument checks, uploads,
+// error mapping.  All compute runs in the kernels of rr_build.cu,
+// rr_trace.cu, rr_images.cu and rr_ir.cu.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "rr_trace.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+rr_status guarded(F&& f) {
+  try {
+    f();
+    return RR_OK;
+  } catch (const rr::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return RR_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RR_RUNTIME;
+  }
+}
+
+// TriangleMesh::validate (geometry.cpp:47-75): the reference throws at the
+// first face (in index order) that fails vertex range, material range or
+// area, then checks materials.  key = face*4 + kind.
+__global__ void validate_faces_kernel(const double* __restrict__ v, int64_t nv, const int32_t* __restrict__ t,
+                                      int64_t nf, int32_t nmat, unsigned long long* __restrict__ first) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int32_t a = t[4 * f], b = t[4 * f + 1], c = t[4 * f + 2], m = t[4 * f + 3];
+  unsigned long long key = ~0ull;
+  if (a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv) {
+    key = 4ull * f + 0;
+  } else if (m < 0 || m >= nmat) {
+    key = 4ull * f + 1;
+  } else {
+    using namespace rr;
+    const D3 va = d3(v[3 * a], v[3 * a + 1], v[3 * a + 2]);
+    const D3 e1 = d3(v[3 * b], v[3 * b + 1], v[3 * b + 2]) - va;
+    const D3 e2 = d3(v[3 * c], v[3 * c + 1], v[3 * c + 2]) - va;
+    const D3 n = cross(e1, e2);
+    const double area = 0.5 * sqrt(dot(n, n));  // face_area geometry.cpp:22-26
+    if (area <= 1e-12) key = 4ull * f + 2;
+  }
+  if (key != ~0ull) atomicMin(first, key);
+}
+
+// Moller-Trumbore operands and face normals (geometry.cpp:9-14, 80-82).
+__global__ void face_data_kernel(const double* __restrict__ v, const int32_t* __restrict__ t, int64_t nf,
+                                 rr::FaceTri* __restrict__ tri, double* __restrict__ normal,
+                                 int32_t* __restrict__ mat) {
+  using namespace rr;
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int32_t a = t[4 * f], b = t[4 * f + 1], c = t[4 * f + 2];
+  const D3 va = d3(v[3 * a], v[3 * a + 1], v[3 * a + 2]);
+  const D3 e1 = d3(v[3 * b], v[3 * b + 1], v[3 * b + 2]) - va;
+  const D3 e2 = d3(v[3 * c], v[3 * c + 1], v[3 * c + 2]) - va;
+  FaceTri ft;
+  ft.ax = va.x; ft.ay = va.y; ft.az = va.z;
+  ft.e1x = e1.x; ft.e1y = e1.y; ft.e1z = e1.z;
+  ft.e2x = e2.x; ft.e2y = e2.y; ft.e2z = e2.z;
+  ft.pad = 0.0;
+  tri[f] = ft;
+  D3 n = cross(e1, e2);
+  const double z = dot(n, n);
+  if (z > 0.0) {
+    const double s = sqrt(z);
+    n = d3(n.x / s, n.y / s, n.z / s);
+  }
+  normal[3 * f] = n.x;
+  normal[3 * f + 1] = n.y;
+  normal[3 * f + 2] = n.z;
+  mat[f] = t[4 * f + 3];
+}
+
+void check_ptr(const void* p, const char* what) {
+  if (!p) rr::invalid(std::string(what) + " must not be null");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rr_last_error(void) { return g_err.c_str(); }
+const char* rr_version(void) { return "roomray_b200 0.1 (sm_100a)"; }
+
+rr_status rr_ctx_create(int device, rr_ctx** out) {
+  return guarded([&] {
+    check_ptr(out, "out");
+    int n = 0;
+    RR_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) rr::invalid("device index out of range");
+    RR_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<rr_ctx>();
+    c->device = device;
+    RR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    RR_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    cudaDeviceProp prop;
+    RR_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) rr::invalid("roomray_b200 needs an sm_100a (Blackwell) device");
+    *out = c.release();
+  });
+}
+
+rr_status rr_ctx_destroy(rr_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* rr_ctx_stream(rr_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->stream) : nullptr; }
+int64_t rr_ctx_launches(rr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv, const int32_t* tris, int64_t nf,
+                          const double* alpha, int32_t nmat, int32_t validate, rr_scene** out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(out, "out");
+    if (nf <= 0) rr::invalid("cannot build a tree over an empty mesh");  // accel_tree.cpp:71-73
+    if (nf >= (int64_t(1) << 30)) rr::invalid("face count must be < 2^30");
+    check_ptr(verts, "verts");
+    check_ptr(tris, "tris");
+    if (nmat > 0) check_ptr(alpha, "alpha");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    auto s = std::make_unique<rr_scene>();
+    s->ctx = ctx;
+    s->nv = nv;
+    s->nf = nf;
+    s->nmat = nmat;
+    s->verts.alloc(3 * std::max<int64_t>(nv, 1), st);
+    s->tris.alloc(4 * nf, st);
+    if (nv > 0) RR_CUDA(cudaMemcpyAsync(s->verts.p, verts, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice, st));
+    RR_CUDA(cudaMemcpyAsync(s->tris.p, tris, sizeof(int32_t) * 4 * nf, cudaMemcpyHostToDevice, st));
+    const unsigned g = static_cast<unsigned>((nf + 255) / 256);
+    if (validate) {
+      rr::DevBuf<unsigned long long> first;
+      first.alloc(1, st);
+      RR_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), st));
+      validate_faces_kernel<<<g, 256, 0, st>>>(s->verts.p, nv, s->tris.p, nf, nmat, first.p);
+      RR_LAUNCH_CHECK();
+      ctx->launches++;
+      unsigned long long key = 0;
+      RR_CUDA(cudaMemcpyAsync(&key, first.p, sizeof key, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      if (key != ~0ull) {
+        const long long f = static_cast<long long>(key / 4);
+        const int kind = static_cast<int>(key % 4);
+        if (kind == 0) rr::invalid("face " + std::to_string(f) + " references a vertex out of range");
+        if (kind == 1)
+          rr::invalid("face " + std::to_string(f) + " references material " + std::to_string(tris[4 * f + 3]) +
+                      " out of range");
+        rr::invalid("face " + std::to_string(f) + " is degenerate (area <= 1e-12 m^2)");
+      }
+      for (int32_t m = 0; m < nmat; ++m)
+        for (int b = 0; b < rr::kBands; ++b) {
+          const double a = alpha[rr::kBands * m + b];
+          if (a < 0.0 || a > 1.0)
+            rr::invalid("material 'm" + std::to_string(m) + "' has absorption outside [0,1]");
+        }
+    }
+    // 1 - alpha per band (tracer.cpp:57-58), 8*nmat scalars
+    std::vector<double> oma(static_cast<size_t>(rr::kBands) * std::max(nmat, 1), 1.0);
+    for (int64_t i = 0; i < static_cast<int64_t>(rr::kBands) * nmat; ++i) oma[i] = 1.0 - alpha[i];
+    s->oma.alloc(oma.size(), st);
+    RR_CUDA(cudaMemcpyAsync(s->oma.p, oma.data(), sizeof(double) * oma.size(), cudaMemcpyHostToDevice, st));
+    s->tri.alloc(nf, st);
+    s->normal.alloc(3 * nf, st);
+    s->mat.alloc(nf, st);
+    face_data_kernel<<<g, 256, 0, st>>>(s->verts.p, s->tris.p, nf, s->tri.p, s->normal.p, s->mat.p);
+    RR_LAUNCH_CHECK();
+    ctx->launches++;
+    rr::build_scene_tree(s.get());
+    RR_CUDA(cudaStreamSynchronize(st));
+    *out = s.release();
+  });
+}
+
+rr_status rr_scene_destroy(rr_scene* scene) {
+  return guarded([&] {
+    if (!scene) return;
+    cudaSetDevice(scene->ctx->device);
+    cudaStream_t st = scene->ctx->stream;
+    delete scene;
+    cudaStreamSynchronize(st);
+  });
+}
+
+rr_status rr_scene_tree_info(rr_scene* s, int64_t* n_nodes, int32_t* root, int32_t* depth) {
+  return guarded([&] {
+    check_ptr(s, "scene");
+    if (n_nodes) *n_nodes = 2 * s->nf - 1;
+    if (root) *root = s->root;
+    if (depth) *depth = s->depth;
+  });
+}
+
+rr_status rr_scene_tree(rr_scene* s, rr_tree_node* nodes) {
+  return guarded([&] {
+    check_ptr(s, "scene");
+    check_ptr(nodes, "nodes");
+    RR_CUDA(cudaSetDevice(s->ctx->device));
+    RR_CUDA(cudaMemcpyAsync(nodes, s->ref.p, s->ref.bytes(), cudaMemcpyDeviceToHost, s->ctx->stream));
+    RR_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+rr_status rr_scene_normals(rr_scene* s, double* normals) {
+  return guarded([&] {
+    check_ptr(s, "scene");
+    check_ptr(normals, "normals");
+    RR_CUDA(cudaSetDevice(s->ctx->device));
+    RR_CUDA(cudaMemcpyAsync(normals, s->normal.p, s->normal.bytes(), cudaMemcpyDeviceToHost, s->ctx->stream));
+    RR_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  });
+}
+
+double rr_scene_build_ms(rr_scene* s) { return s ? s->build_ms : -1.0; }
+
+rr_status rr_nearest_hit_batch(rr_scene* s, const double* o, const double* d, int64_t n, int32_t brute,
+                               int32_t* face, double* delta, double* point) {
+  return guarded([&] {
+    check_ptr(s, "scene");
+    if (n < 0) rr::invalid("n must be >= 0");
+    if (n == 0) return;
+    check_ptr(o, "origins");
+    check_ptr(d, "dirs");
+    check_ptr(face, "face");
+    check_ptr(delta, "delta");
+    check_ptr(point, "point");
+    RR_CUDA(cudaSetDevice(s->ctx->device));
+    cudaStream_t st = s->ctx->stream;
+    rr::DevBuf<double> dob, ddb, ddel, dpt;
+    rr::DevBuf<int32_t> dface;
+    dob.alloc(3 * n, st);
+    ddb.alloc(3 * n, st);
+    ddel.alloc(n, st);
+    dpt.alloc(3 * n, st);
+    dface.alloc(n, st);
+    RR_CUDA(cudaMemcpyAsync(dob.p, o, dob.bytes(), cudaMemcpyHostToDevice, st));
+    RR_CUDA(cudaMemcpyAsync(ddb.p, d, ddb.bytes(), cudaMemcpyHostToDevice, st));
+    rr::nearest_hit_batch(s, dob.p, ddb.p, n, brute, dface.p, ddel.p, dpt.p);
+    RR_CUDA(cudaMemcpyAsync(face, dface.p, dface.bytes(), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaMemcpyAsync(delta, ddel.p, ddel.bytes(), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaMemcpyAsync(point, dpt.p, dpt.bytes(), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+rr_status rr_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, int32_t n_recv,
+                   const rr_trace_config* cfg, rr_trace_result** out) {
+  return guarded([&] {
+    check_ptr(s, "scene");
+    check_ptr(src, "source");
+    check_ptr(recv, "receivers");
+    check_ptr(cfg, "config");
+    check_ptr(out, "out");
+    RR_CUDA(cudaSetDevice(s->ctx->device));
+    *out = rr::run_trace(s, src, recv, n_recv, cfg, nullptr);
+  });
+}
+
+rr_status rr_trace_stats_get(rr_trace_result* r, rr_trace_stats* stats) {
+  return guarded([&] {
+    check_ptr(r, "result");
+    check_ptr(stats, "stats");
+    *stats = r->stats;
+  });
+}
+
+rr_status rr_trace_captures(rr_trace_result* r, int32_t* recv, int32_t* ray, double* point, double* dir,
+                            double* path, double* mult, int64_t* hist_off, int32_t* hist) {
+  return guarded([&] {
+    check_ptr(r, "result");
+    RR_CUDA(cudaSetDevice(r->scene->ctx->device));
+    cudaStream_t st = r->scene->ctx->stream;
+    const int64_t n = r->stats.n_captures;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    };
+    if (n > 0) {
+      cp(recv, r->c_recv.p, sizeof(int32_t) * n);
+      cp(ray, r->c_ray.p, sizeof(int32_t) * n);
+      cp(point, r->c_point.p, sizeof(double) * 3 * n);
+      cp(dir, r->c_dir.p, sizeof(double) * 3 * n);
+      cp(path, r->c_path.p, sizeof(double) * n);
+      cp(mult, r->c_mult.p, sizeof(double) * rr::kBands * n);
+      cp(hist, r->c_hist.p, sizeof(int32_t) * r->stats.total_history);
+    }
+    cp(hist_off, r->c_off.p, sizeof(int64_t) * (n + 1));
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+double rr_trace_kernel_ms(rr_trace_result* r) { return r ? r->kernel_ms : -1.0; }
+
+rr_status rr_trace_destroy(rr_trace_result* r) {
+  return guarded([&] {
+    if (!r) return;
+    cudaSetDevice(r->scene->ctx->device);
+    cudaStream_t st = r->scene->ctx->stream;
+    delete r;
+    cudaStreamSynchronize(st);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- IR
+namespace rr {
+void ir_bin(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy, double c, double fs, int64_t lh,
+            double* d_hist);
+void ir_filter(rr_ctx* ctx, const double* d_hist, int64_t lh, double fs, int taps, int64_t L, double* d_band_ir,
+               double* d_broadband);
+void band_filter_host(int band, double fs, int taps, double* out, rr_ctx* ctx);
+void air_beta_bands(const rr_air& a, double* beta);
+}  // namespace rr
+
+namespace {
+__global__ void min_dist_kernel(const double* __restrict__ d, int64_t n, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!(d[i] >= 0.0)) *bad = 1;
+}
+}  // namespace
+
+extern "C" {
+
+rr_status rr_band_filter(int32_t band, double fs, int32_t taps, double* out) {
+  return guarded([&] {
+    check_ptr(out, "out");
+    static thread_local rr_ctx* ctx = nullptr;
+    if (!ctx) {
+      if (rr_ctx_create(0, &ctx) != RR_OK) throw rr::Error(RR_CUDA, g_err);
+    }
+    rr::band_filter_host(band, fs, taps, out, ctx);
+  });
+}
+
+rr_status rr_ir_bin_device(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy, double c, double fs,
+                           int64_t length, double* d_hist) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(d_hist, "hist");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");  // rir.cpp:11-13
+    if (length <= 0) rr::invalid("length must be > 0");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    rr::ir_bin(ctx, n, d_dist, d_energy, c, fs, length, d_hist);
+  });
+}
+
+rr_status rr_ir_filter_device(rr_ctx* ctx, const double* d_hist, double fs, int32_t taps, int64_t length,
+                              double* d_band_ir, double* d_broadband) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(d_hist, "hist");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    // d_hist holds length + taps samples per band
+    rr::ir_filter(ctx, d_hist, length + taps, fs, taps, length, d_band_ir, d_broadband);
+  });
+}
+
+rr_status rr_synthesize(rr_ctx* ctx, int64_t n, const double* dist, const double* energy, double c, double fs,
+                        int32_t taps, int64_t length, double* band_ir, double* broadband) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");  // rir.cpp:11-13
+    if (n < 0) rr::invalid("n must be >= 0");
+    if (n > 0) {
+      check_ptr(dist, "dist");
+      check_ptr(energy, "energy");
+    }
+    if (taps < 3) rr::invalid("taps must be >= 3");
+    if (fs < 2.0 * 8000.0 * std::sqrt(2.0)) rr::invalid("sample rate too low for the top band edge");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    rr::DevBuf<double> dd, de;
+    dd.alloc(std::max<int64_t>(n, 1), st);
+    de.alloc(rr::kBands * std::max<int64_t>(n, 1), st);
+    if (n > 0) {
+      RR_CUDA(cudaMemcpyAsync(dd.p, dist, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      RR_CUDA(cudaMemcpyAsync(de.p, energy, sizeof(double) * rr::kBands * n, cudaMemcpyHostToDevice, st));
+      rr::DevBuf<int> bad;
+      bad.alloc(1, st);
+      RR_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+      min_dist_kernel<<<148, 256, 0, st>>>(dd.p, n, bad.p);
+      int hb = 0;
+      RR_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof hb, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      ctx->launches++;
+      if (hb) rr::invalid("pulse events cannot precede t = 0");  // rir.cpp:69-71
+    }
+    if (length <= 0) rr::invalid("length must be > 0 (see rr_ir_reference_length)");
+    const int64_t lh = length + taps;
+    rr::DevBuf<double> hist, bands, bb;
+    hist.alloc(rr::kBands * lh, st);
+    bands.alloc(rr::kBands * length, st);
+    bb.alloc(length, st);
+    rr::ir_bin(ctx, n, dd.p, de.p, c, fs, lh, hist.p);
+    rr::ir_filter(ctx, hist.p, lh, fs, taps, length, bands.p, bb.p);
+    if (band_ir)
+      RR_CUDA(cudaMemcpyAsync(band_ir, bands.p, bands.bytes(), cudaMemcpyDeviceToHost, st));
+    if (broadband) RR_CUDA(cudaMemcpyAsync(broadband, bb.p, bb.bytes(), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// Response length of the reference's synthesize (rir.cpp:78-80):
+// llround(t_last*fs) + (taps-1)/2 + 1, 0 for no events.
+rr_status rr_ir_reference_length(int64_t n, const double* dist, double c, double fs, int32_t taps,
+                                 int64_t* length) {
+  return guarded([&] {
+    check_ptr(length, "length");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");
+    double last = 0.0;
+    for (int64_t i = 0; i < n; ++i) last = std::max(last, dist[i] / c);
+    *length = n > 0 ? static_cast<int64_t>(std::llround(last * fs)) + (taps - 1) / 2 + 1 : 0;
+  });
+}
+
+rr_status rr_air_beta_bands(const rr_air* air, double* beta) {
+  return guarded([&] {
+    check_ptr(air, "air");
+    check_ptr(beta, "beta");
+    rr::air_beta_bands(*air, beta);
+  });
+}
+
+// ---------------------------------------------------------------- images (K5, rr_images.cu)
+rr_status rr_build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_rays, const rr_air* air,
+                                 const rr_cluster_options* opt, rr_images** out) {
+  return guarded([&] {
+    check_ptr(tr, "trace result");
+    check_ptr(air, "air");
+    check_ptr(out, "out");
+    rr_cluster_options o{1e-6, 0};
+    if (opt) o = *opt;
+    RR_CUDA(cudaSetDevice(tr->scene->ctx->device));
+    *out = rr::build_image_sources(tr, recv, total_rays, *air, o);
+  });
+}
+
+rr_status rr_images_info(rr_images* im, int64_t* n, int64_t* total_path) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    if (n) *n = im->n;
+    if (total_path) *total_path = im->total_path;
+  });
+}
+
+rr_status rr_images_get(rr_images* im, double* pos, double* dist, double* energy, double* mult, int32_t* ray_count,
+                        int32_t* order, int32_t* has_proj, double* proj, int64_t* path_off, int32_t* path) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    RR_CUDA(cudaSetDevice(im->scene->ctx->device));
+    cudaStream_t st = im->scene->ctx->stream;
+    const int64_t n = im->n;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    };
+    cp(pos, im->pos.p, sizeof(double) * 3 * n);
+    cp(dist, im->dist.p, sizeof(double) * n);
+    cp(energy, im->energy.p, sizeof(double) * rr::kBands * n);
+    cp(mult, im->mult.p, sizeof(double) * rr::kBands * n);
+    cp(ray_count, im->ray_count.p, sizeof(int32_t) * n);
+    cp(order, im->order.p, sizeof(int32_t) * n);
+    cp(has_proj, im->has_proj.p, sizeof(int32_t) * n);
+    cp(proj, im->proj.p, sizeof(double) * 3 * n);
+    cp(path_off, im->path_off.p, sizeof(int64_t) * (n + 1));
+    cp(path, im->path.p, sizeof(int32_t) * im->total_path);
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+rr_status rr_images_destroy(rr_images* im) {
+  return guarded([&] {
+    if (!im) return;
+    cudaSetDevice(im->scene->ctx->device);
+    cudaStream_t st = im->scene->ctx->stream;
+    delete im;
+    cudaStreamSynchronize(st);
+  });
+}
+
+rr_status rr_images_device(rr_images* im, const double** d_dist, const double** d_energy, int64_t* n) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    if (d_dist) *d_dist = im->dist.p;
+    if (d_energy) *d_energy = im->energy.p;
+    if (n) *n = im->n;
+  });
+}
+
+}  // extern "C"

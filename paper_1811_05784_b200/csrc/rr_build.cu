@@ -1,0 +1,478 @@
+// K1 — device build of the reference median-split tree.
+//
+// Replaces build_tree / Builder::build_range (accel_tree.cpp:19-87).  The
+// reference splits each face range at mid = begin + n/2 after nth_element on
+// the total order (centroid[axis], face index), axis = first argmax of the
+// range box extent (accel_tree.cpp:30-41).  Because that order is total, the
+// set of faces sent left is unique, so the tree is a function of the input
+// alone and is rebuilt here level-synchronously:
+//   * three face lists presorted by (centroid[k], face) (CUB radix sort,
+//     stable => ties by face index, accel_tree.cpp:38-39);
+//   * per level: segmented box reduction (warp-segmented + u64 atomics on
+//     order-preserving keys, exact min/max), axis choice, split flags from the
+//     chosen axis' list (rank < n/2), and a stable segmented partition of all
+//     three lists (one scan) so each stays sorted inside its child segments.
+// Node numbering follows the reference post-order (left subtree, right
+// subtree, node; root last, accel_tree.cpp:43-46): a range [b, b+n) whose
+// subtree starts at s has its node at s + 2n - 2 and children starting at s
+// and s + 2*(n/2) - 1.  Segment sizes depend on nf only, so the host knows
+// every level's segment count without a device round trip.
+//
+// The same pass emits the traversal layout used by the tracer: TNode pairs of
+// conservative fp32 child boxes (outward-rounded and expanded by eps), with
+// the top D levels in BFS order at [0, K) (cached in shared memory by the
+// tracer) and deeper subtrees in preorder at K + begin + (left edges below
+// level D).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+
+#include "rr_internal.cuh"
+
+namespace rr {
+namespace {
+
+constexpr int kMaxCachedNodes = 511;  // 32 KB of TNodes in shared memory
+
+__device__ __forceinline__ uint64_t ord_key(double x) {
+  if (x == 0.0) x = 0.0;  // -0 == +0 in the reference comparisons
+  uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(uint64_t u) {
+  u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+
+struct Seg {
+  int64_t b, n, s;   // range [b, b+n), post-order base of the subtree
+  int32_t parent;    // traversal index of the parent node, -1 for the root
+  int32_t side;      // 0 left child, 1 right child
+  int32_t lam;       // left edges on the path below level D
+  int32_t pad;
+};
+
+// Centroid (geometry.cpp:16-19), face bounds (geometry.cpp:28-35), sort keys.
+__global__ void face_prep_kernel(const double* __restrict__ v,
+                                 const int32_t* __restrict__ t, int64_t nf,
+                                 double* __restrict__ fb,  // nf*6 lo,hi
+                                 uint64_t* __restrict__ keys,  // 3*nf
+                                 int32_t* __restrict__ ids) {  // 3*nf
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int32_t a = t[4 * f], b = t[4 * f + 1], c = t[4 * f + 2];
+  for (int k = 0; k < 3; ++k) {
+    const double va = v[3 * a + k], vb = v[3 * b + k], vc = v[3 * c + k];
+    const double cen = ((va + vb) + vc) / 3.0;
+    double lo = va, hi = va;  // Aabb::extend: std::min/std::max
+    lo = (vb < lo) ? vb : lo;
+    hi = (hi < vb) ? vb : hi;
+    lo = (vc < lo) ? vc : lo;
+    hi = (hi < vc) ? vc : hi;
+    fb[6 * f + k] = lo;
+    fb[6 * f + 3 + k] = hi;
+    keys[k * nf + f] = ord_key(cen);
+    ids[k * nf + f] = static_cast<int32_t>(f);
+  }
+}
+
+// Segmented min/max of face bounds over each active segment.
+__global__ void seg_box_kernel(const int32_t* __restrict__ pos_seg,
+                               const int32_t* __restrict__ perm0,
+                               const double* __restrict__ fb, int64_t nf,
+                               unsigned long long* __restrict__ bmin,
+                               unsigned long long* __restrict__ bmax) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int32_t seg = -1;
+  uint64_t mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+  if (i < nf) {
+    seg = pos_seg[i];
+    if (seg >= 0) {
+      const int32_t f = perm0[i];
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = ord_key(fb[6 * f + k]);
+        mx[k] = ord_key(fb[6 * f + 3 + k]);
+      }
+    }
+  }
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t so = __shfl_down_sync(0xffffffffu, seg, off);
+    const bool ok = (lane + off < 32) && so == seg;
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t a = __shfl_down_sync(0xffffffffu, mn[k], off);
+      const uint64_t b = __shfl_down_sync(0xffffffffu, mx[k], off);
+      if (ok) {
+        mn[k] = a < mn[k] ? a : mn[k];
+        mx[k] = b > mx[k] ? b : mx[k];
+      }
+    }
+  }
+  const int32_t sp = __shfl_up_sync(0xffffffffu, seg, 1);
+  const bool head = seg >= 0 && (lane == 0 || sp != seg);
+  if (head) {
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(bmin + 3 * seg + k, (unsigned long long)mn[k]);
+      atomicMax(bmax + 3 * seg + k, (unsigned long long)mx[k]);
+    }
+  }
+}
+
+__global__ void split_flag_kernel(const Seg* __restrict__ segs, int64_t S,
+                                  int32_t* __restrict__ flag) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < S) flag[j] = segs[j].n >= 2 ? 1 : 0;
+}
+
+__device__ __forceinline__ float lo_f(double x, float eps) {
+  return __fsub_rd(__double2float_rd(x), eps);
+}
+__device__ __forceinline__ float hi_f(double x, float eps) {
+  return __fadd_ru(__double2float_ru(x), eps);
+}
+
+// Node emission, axis choice, child segments.
+__global__ void seg_node_kernel(const Seg* __restrict__ segs, int64_t S,
+                                const int32_t* __restrict__ rank,
+                                const unsigned long long* __restrict__ bmin,
+                                const unsigned long long* __restrict__ bmax,
+                                const int32_t* __restrict__ perm0, int level,
+                                int D, int32_t level_base, int32_t K,
+                                RefNode* __restrict__ ref, TNode* __restrict__ tn,
+                                TravHeader* __restrict__ hdr,
+                                int32_t* __restrict__ seg_axis,
+                                Seg* __restrict__ next) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const Seg sg = segs[j];
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = ord_val(bmin[3 * j + k]);
+    hi[k] = ord_val(bmax[3 * j + k]);
+  }
+  float eps;
+  if (level == 0) {
+    double scale = 1e-3;
+    for (int k = 0; k < 3; ++k) scale = fmax(scale, fmax(fabs(lo[k]), fabs(hi[k])));
+    eps = __double2float_ru(scale * 0x1p-20);
+    hdr->eps = eps;
+    for (int k = 0; k < 3; ++k) {
+      hdr->lo[k] = lo_f(lo[k], eps);
+      hdr->hi[k] = hi_f(hi[k], eps);
+    }
+  } else {
+    eps = hdr->eps;
+  }
+  const int64_t node = sg.s + 2 * sg.n - 2;
+  RefNode r;
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = lo[k];
+    r.hi[k] = hi[k];
+  }
+  r.pad = 0;
+  int32_t my_ref;
+  if (sg.n == 1) {
+    r.face = perm0[sg.b];
+    r.left = r.right = -1;
+    my_ref = ~r.face;
+    seg_axis[j] = -1;
+  } else {
+    const int64_t nl = sg.n / 2, nr = sg.n - nl;
+    r.face = -1;
+    r.left = static_cast<int32_t>(sg.s + 2 * nl - 2);
+    r.right = static_cast<int32_t>((sg.s + 2 * nl - 1) + 2 * nr - 2);
+    // axis = first argmax of the box extent (accel_tree.cpp:30-32)
+    const double ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+    int axis = 0;
+    double best = ex;
+    if (ey > best) { axis = 1; best = ey; }
+    if (ez > best) { axis = 2; }
+    seg_axis[j] = axis;
+    my_ref = level < D ? level_base + rank[j]
+                       : K + static_cast<int32_t>(sg.b) + sg.lam;
+    const int32_t lam_l = (level + 1 < D) ? 0 : (level + 1 == D ? 0 : sg.lam + 1);
+    const int32_t lam_r = (level + 1 < D) ? 0 : (level + 1 == D ? 0 : sg.lam);
+    Seg L{sg.b, nl, sg.s, my_ref, 0, lam_l, 0};
+    Seg R{sg.b + nl, nr, sg.s + 2 * nl - 1, my_ref, 1, lam_r, 0};
+    next[2 * rank[j]] = L;
+    next[2 * rank[j] + 1] = R;
+  }
+  ref[node] = r;
+  if (sg.parent < 0) {
+    hdr->root_ref = my_ref;
+  } else {
+    TNode* p = tn + sg.parent;
+    const float lx = lo_f(lo[0], eps), ly = lo_f(lo[1], eps), lz = lo_f(lo[2], eps);
+    const float hx = hi_f(hi[0], eps), hy = hi_f(hi[1], eps), hz = hi_f(hi[2], eps);
+    if (sg.side == 0) {
+      p->a = make_float4(lx, hx, ly, hy);
+      reinterpret_cast<float2*>(&p->b)[0] = make_float2(lz, hz);
+      p->d.x = my_ref;
+    } else {
+      reinterpret_cast<float2*>(&p->b)[1] = make_float2(lx, hx);
+      p->c = make_float4(ly, hy, lz, hz);
+      p->d.y = my_ref;
+    }
+  }
+}
+
+// flag[face] = goes left, from the chosen axis' sorted list.
+__global__ void face_flag_kernel(const int32_t* __restrict__ pos_seg,
+                                 const Seg* __restrict__ segs,
+                                 const int32_t* __restrict__ seg_axis,
+                                 const int32_t* __restrict__ perm, int64_t nf,
+                                 uint8_t* __restrict__ flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  const int32_t sj = pos_seg[i];
+  if (sj < 0) return;
+  const int32_t axis = seg_axis[sj];
+  if (axis < 0) return;
+  const Seg sg = segs[sj];
+  flag[perm[axis * nf + i]] = (i - sg.b) < sg.n / 2 ? 1 : 0;
+}
+
+__global__ void gather_flag_kernel(const int32_t* __restrict__ perm,
+                                   const uint8_t* __restrict__ flag,
+                                   int64_t total, int32_t* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < total) out[i] = flag[perm[i]];
+}
+
+// Stable segmented partition of the three lists.
+__global__ void scatter_kernel(const int32_t* __restrict__ pos_seg,
+                               const Seg* __restrict__ segs,
+                               const int32_t* __restrict__ seg_axis,
+                               const int32_t* __restrict__ rank,
+                               const int32_t* __restrict__ perm,
+                               const int32_t* __restrict__ fl,
+                               const int32_t* __restrict__ scan, int64_t nf,
+                               int32_t* __restrict__ perm_out,
+                               int32_t* __restrict__ pos_seg_out) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= 3 * nf) return;
+  const int k = static_cast<int>(g / nf);
+  const int64_t i = g - k * nf;
+  const int32_t sj = pos_seg[i];
+  if (sj < 0 || seg_axis[sj] < 0) {
+    perm_out[g] = perm[g];
+    if (k == 0) pos_seg_out[i] = -1;
+    return;
+  }
+  const Seg sg = segs[sj];
+  const int64_t nl = sg.n / 2;
+  const int64_t cnt_l = scan[g] - scan[k * nf + sg.b];
+  const bool left = fl[g] != 0;
+  const int64_t np = left ? sg.b + cnt_l : sg.b + nl + (i - sg.b - cnt_l);
+  perm_out[k * nf + np] = perm[g];
+  if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
+}
+
+__global__ void vert_bounds_kernel(const double* __restrict__ v, int64_t nv,
+                                   unsigned long long* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  uint64_t mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+  for (; i < nv; i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t u = ord_key(v[3 * i + k]);
+      mn[k] = u < mn[k] ? u : mn[k];
+      mx[k] = u > mx[k] ? u : mx[k];
+    }
+  for (int off = 16; off > 0; off >>= 1)
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t a = __shfl_xor_sync(0xffffffffu, mn[k], off);
+      const uint64_t b = __shfl_xor_sync(0xffffffffu, mx[k], off);
+      mn[k] = a < mn[k] ? a : mn[k];
+      mx[k] = b > mx[k] ? b : mx[k];
+    }
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(out + k, (unsigned long long)mn[k]);
+      atomicMax(out + 3 + k, (unsigned long long)mx[k]);
+    }
+}
+
+__global__ void unmap_bounds_kernel(const unsigned long long* in, double* out) {
+  if (threadIdx.x < 6) out[threadIdx.x] = ord_val(in[threadIdx.x]);
+}
+
+inline unsigned grid_for(int64_t n, int block = 256) {
+  return static_cast<unsigned>((n + block - 1) / block);
+}
+
+}  // namespace
+
+void build_scene_tree(rr_scene* s) {
+  cudaStream_t st = s->ctx->stream;
+  const int64_t nf = s->nf;
+  cudaEvent_t e0, e1;
+  RR_CUDA(cudaEventCreate(&e0));
+  RR_CUDA(cudaEventCreate(&e1));
+  RR_CUDA(cudaEventRecord(e0, st));
+
+  // ---- host plan: per-level segment size multisets (depend on nf only)
+  std::vector<std::map<int64_t, int64_t>> levels;
+  levels.push_back({{nf, 1}});
+  for (;;) {
+    std::map<int64_t, int64_t> nx;
+    for (auto [sz, cnt] : levels.back())
+      if (sz >= 2) {
+        nx[sz / 2] += cnt;
+        nx[sz - sz / 2] += cnt;
+      }
+    if (nx.empty()) break;
+    levels.push_back(nx);
+  }
+  const int n_levels = static_cast<int>(levels.size());
+  std::vector<int64_t> seg_count(n_levels), split_count(n_levels);
+  for (int L = 0; L < n_levels; ++L) {
+    int64_t c = 0, sp = 0;
+    for (auto [sz, cnt] : levels[L]) {
+      c += cnt;
+      if (sz >= 2) sp += cnt;
+    }
+    seg_count[L] = c;
+    split_count[L] = sp;
+  }
+  int D = 0;
+  int64_t K = 0;
+  while (D < n_levels && K + split_count[D] <= kMaxCachedNodes) {
+    K += split_count[D];
+    ++D;
+  }
+  std::vector<int32_t> level_base(n_levels, 0);
+  for (int L = 1; L < n_levels; ++L)
+    level_base[L] = level_base[L - 1] + static_cast<int32_t>(split_count[L - 1]);
+  int64_t max_seg = 1;
+  for (auto c : seg_count) max_seg = std::max(max_seg, c);
+
+  s->depth = n_levels - 1;
+  s->K = static_cast<int32_t>(K);
+  s->root = static_cast<int32_t>(2 * nf - 2);
+
+  // ---- buffers
+  DevBuf<double> fb;
+  fb.alloc(6 * nf, st);
+  DevBuf<uint64_t> keys, keys_out;
+  keys.alloc(3 * nf, st);
+  keys_out.alloc(3 * nf, st);
+  DevBuf<int32_t> ids, permA, permB, fl, scan, pos_a, pos_b;
+  ids.alloc(3 * nf, st);
+  permA.alloc(3 * nf, st);
+  permB.alloc(3 * nf, st);
+  fl.alloc(3 * nf, st);
+  scan.alloc(3 * nf, st);
+  pos_a.alloc(nf, st);
+  pos_b.alloc(nf, st);
+  DevBuf<uint8_t> flag;
+  flag.alloc(nf, st);
+  DevBuf<Seg> segA, segB;
+  segA.alloc(max_seg, st);
+  segB.alloc(max_seg, st);
+  DevBuf<int32_t> sflag, srank, saxis;
+  sflag.alloc(max_seg, st);
+  srank.alloc(max_seg, st);
+  saxis.alloc(max_seg, st);
+  DevBuf<unsigned long long> bmin, bmax;
+  bmin.alloc(3 * max_seg, st);
+  bmax.alloc(3 * max_seg, st);
+
+  s->ref.alloc(2 * nf - 1, st);
+  s->tnodes.alloc(K + nf, st);
+  RR_CUDA(cudaMemsetAsync(s->tnodes.p, 0, s->tnodes.bytes(), st));
+  s->dhdr.alloc(1, st);
+  RR_CUDA(cudaMemsetAsync(s->dhdr.p, 0, sizeof(TravHeader), st));
+
+  face_prep_kernel<<<grid_for(nf), 256, 0, st>>>(s->verts.p, s->tris.p, nf, fb.p, keys.p, ids.p);
+  RR_LAUNCH_CHECK();
+  s->ctx->launches++;
+
+  // ---- CUB scratch
+  size_t tmp_sort = 0, tmp_scan = 0, tmp_scan2 = 0;
+  RR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys.p, keys_out.p, ids.p, permA.p,
+                                          static_cast<int>(nf), 0, 64, st));
+  RR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, fl.p, scan.p, static_cast<int>(3 * nf), st));
+  RR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan2, sflag.p, srank.p, static_cast<int>(max_seg), st));
+  DevBuf<uint8_t> tmp;
+  tmp.alloc(std::max(tmp_sort, std::max(tmp_scan, tmp_scan2)) + 16, st);
+  for (int k = 0; k < 3; ++k) {
+    size_t t = tmp.n;
+    RR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, t, keys.p + k * nf, keys_out.p + k * nf, ids.p + k * nf,
+                                            permA.p + k * nf, static_cast<int>(nf), 0, 64, st));
+    s->ctx->launches += 4;
+  }
+
+  // ---- level loop
+  RR_CUDA(cudaMemsetAsync(pos_a.p, 0, sizeof(int32_t) * nf, st));
+  const Seg root{0, nf, 0, -1, 0, 0, 0};
+  RR_CUDA(cudaMemcpyAsync(segA.p, &root, sizeof(Seg), cudaMemcpyHostToDevice, st));
+  int32_t* perm = permA.p;
+  int32_t* perm_o = permB.p;
+  int32_t* pos = pos_a.p;
+  int32_t* pos_o = pos_b.p;
+  Seg* segs = segA.p;
+  Seg* nsegs = segB.p;
+  for (int L = 0; L < n_levels; ++L) {
+    const int64_t S = seg_count[L];
+    RR_CUDA(cudaMemsetAsync(bmin.p, 0xff, sizeof(unsigned long long) * 3 * S, st));
+    RR_CUDA(cudaMemsetAsync(bmax.p, 0x00, sizeof(unsigned long long) * 3 * S, st));
+    seg_box_kernel<<<grid_for(nf), 256, 0, st>>>(pos, perm, fb.p, nf, bmin.p, bmax.p);
+    RR_LAUNCH_CHECK();
+    split_flag_kernel<<<grid_for(S), 256, 0, st>>>(segs, S, sflag.p);
+    RR_LAUNCH_CHECK();
+    size_t t = tmp.n;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, sflag.p, srank.p, static_cast<int>(S), st));
+    seg_node_kernel<<<grid_for(S), 256, 0, st>>>(segs, S, srank.p, bmin.p, bmax.p, perm, L, D,
+                                                 level_base[L], static_cast<int32_t>(K), s->ref.p,
+                                                 s->tnodes.p, s->dhdr.p, saxis.p, nsegs);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 4;
+    if (split_count[L] == 0) break;
+    face_flag_kernel<<<grid_for(nf), 256, 0, st>>>(pos, segs, saxis.p, perm, nf, flag.p);
+    RR_LAUNCH_CHECK();
+    gather_flag_kernel<<<grid_for(3 * nf), 256, 0, st>>>(perm, flag.p, 3 * nf, fl.p);
+    RR_LAUNCH_CHECK();
+    t = tmp.n;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, fl.p, scan.p, static_cast<int>(3 * nf), st));
+    scatter_kernel<<<grid_for(3 * nf), 256, 0, st>>>(pos, segs, saxis.p, srank.p, perm, fl.p, scan.p, nf,
+                                                     perm_o, pos_o);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 4;
+    std::swap(perm, perm_o);
+    std::swap(pos, pos_o);
+    std::swap(segs, nsegs);
+  }
+
+  // ---- TriangleMesh::bounds over all vertices (image-source tolerance)
+  DevBuf<unsigned long long> vb;
+  vb.alloc(6, st);
+  RR_CUDA(cudaMemsetAsync(vb.p, 0xff, sizeof(unsigned long long) * 3, st));
+  RR_CUDA(cudaMemsetAsync(vb.p + 3, 0x00, sizeof(unsigned long long) * 3, st));
+  const int64_t nv = std::max<int64_t>(s->nv, 1);
+  vert_bounds_kernel<<<std::min<unsigned>(grid_for(nv), 1184u), 256, 0, st>>>(s->verts.p, s->nv, vb.p);
+  RR_LAUNCH_CHECK();
+  DevBuf<double> vbd;
+  vbd.alloc(6, st);
+  unmap_bounds_kernel<<<1, 32, 0, st>>>(vb.p, vbd.p);
+  RR_LAUNCH_CHECK();
+  s->ctx->launches += 2;
+  double hb[6];
+  RR_CUDA(cudaMemcpyAsync(hb, vbd.p, sizeof hb, cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaMemcpyAsync(&s->hdr, s->dhdr.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaEventRecord(e1, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < 3; ++k) {
+    s->lo[k] = hb[k];
+    s->hi[k] = hb[3 + k];
+  }
+  s->hdr.K = static_cast<int32_t>(K);
+  s->hdr.depth = s->depth;
+  RR_CUDA(cudaMemcpyAsync(s->dhdr.p, &s->hdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
+  RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+}  // namespace rr

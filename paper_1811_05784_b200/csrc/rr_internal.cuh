@@ -1,0 +1,136 @@
+// Internal declarations of the roomray_b200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "roomray_b200.h"
+
+namespace rr {
+
+constexpr int kBands = RR_NUM_BANDS;
+
+struct Error : std::runtime_error {
+  rr_status code;
+  Error(rr_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void invalid(const std::string& m) {
+  throw Error(RR_INVALID_ARGUMENT, m);
+}
+
+#define RR_CUDA(x)                                                        \
+  do {                                                                    \
+    cudaError_t rr_e_ = (x);                                              \
+    if (rr_e_ != cudaSuccess)                                             \
+      throw ::rr::Error(RR_CUDA, std::string(#x) + ": " +                 \
+                                     cudaGetErrorString(rr_e_));          \
+  } while (0)
+
+#define RR_LAUNCH_CHECK() RR_CUDA(cudaGetLastError())
+
+// Device buffer, stream-ordered allocation on the owning context's stream.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) RR_CUDA(cudaMallocAsync(&p, sizeof(T) * count, stream));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return sizeof(T) * n; }
+};
+
+// Reference-layout node (TreeNode accel_tree.hpp:15-22), same bytes as
+// rr_tree_node.
+struct RefNode {
+  double lo[3], hi[3];
+  int32_t left, right, face, pad;
+};
+static_assert(sizeof(RefNode) == sizeof(rr_tree_node), "layout");
+
+// Traversal node: the two children's conservative fp32 boxes + refs, 64 B
+// (one 128-B line holds two nodes).  ref >= 0: internal node index;
+// ref < 0: leaf, face = ~ref.
+//   a = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)  b = (L.lo.z, L.hi.z, R.lo.x, R.hi.x)
+//   c = (R.lo.y, R.hi.y, R.lo.z, R.hi.z)  d = (L.ref, R.ref, -, -)
+struct __align__(16) TNode {
+  float4 a, b, c;
+  int4 d;
+};
+
+struct TravHeader {
+  float lo[3], hi[3];  // conservative root box
+  int32_t root_ref;    // internal index 0, or ~face for a one-face mesh
+  int32_t K;           // nodes [0, K) are the BFS-ordered top levels
+  float eps;           // absolute box expansion (metres)
+  int32_t depth;
+};
+
+// Per-face fp64 data for Moller-Trumbore: a, b-a, c-a (geometry.cpp:80-82),
+// padded to 80 B for 16-B vector loads.
+struct __align__(16) FaceTri {
+  double ax, ay, az, e1x, e1y, e1z, e2x, e2y, e2z, pad;
+};
+
+}  // namespace rr
+
+struct rr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int sm_count = 0;
+};
+
+struct rr_scene {
+  rr_ctx* ctx = nullptr;
+  int64_t nv = 0, nf = 0;
+  int32_t nmat = 0;
+  rr::DevBuf<double> verts;       // nv*3
+  rr::DevBuf<int32_t> tris;       // nf*4
+  rr::DevBuf<double> oma;         // nmat*8 : 1 - alpha
+  rr::DevBuf<rr::FaceTri> tri;    // nf
+  rr::DevBuf<double> normal;      // nf*3
+  rr::DevBuf<int32_t> mat;        // nf
+  rr::DevBuf<rr::RefNode> ref;    // 2nf-1 (reference layout)
+  rr::DevBuf<rr::TNode> tnodes;   // K + nf
+  rr::DevBuf<rr::TravHeader> dhdr;
+  rr::TravHeader hdr{};
+  int32_t root = -1, depth = 0, K = 0;
+  double lo[3]{}, hi[3]{};        // TriangleMesh::bounds (geometry.cpp:41-45)
+  float build_ms = 0.f;
+};
+
+namespace rr {
+// rr_build.cu
+void build_scene_tree(rr_scene* s);
+// rr_trace.cu
+void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
+                       int64_t n, int brute, int32_t* d_face, double* d_delta,
+                       double* d_point);
+}  // namespace rr

@@ -1,0 +1,470 @@
+// K2+K3+K4 — persistent specular tracer.
+//
+// Replaces trace/step/step_ray (tracer.cpp:19-149), emit/fibonacci_directions
+// (emission.cpp:17-43) and nearest_hit/nearest_hit_brute
+// (accel_tree.cpp:125-191).
+//
+// One persistent kernel per trace: each lane owns one ray from emission to
+// death and pulls a new ray index from a global counter (warp-aggregated
+// atomic) when its ray dies, so no ray state goes back to HBM between
+// bounces.  Per bounce: closest hit (fp32 conservative box traversal over the
+// 64-B TNode pairs, top levels from shared memory, short per-lane stack;
+// fp64 Moller-Trumbore at leaves), receiver-sphere tests, capture append
+// (warp-aggregated atomic into a compact buffer), reflection, path update and
+// one 4-B face-history write.  Band multipliers are not carried per ray: they
+// are the ordered product of (1 - alpha) over the face history and are
+// rebuilt per capture afterwards (bit-identical to the running product of
+// tracer.cpp:57-58).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "rr_sincos.cuh"
+#include "rr_trace.cuh"
+
+namespace rr {
+
+__device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
+  if (p.block > 0) {
+    // block-cyclic: rank = first, world = stride
+    const int64_t blk = i / p.block, off = i - blk * p.block;
+    return (blk * p.stride + p.first) * p.block + off;
+  }
+  return p.first + i * p.stride;
+}
+
+// fibonacci_directions, emission.cpp:17-29
+__device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
+  const double z = 1.0 - (2.0 * static_cast<double>(k) + 1.0) / static_cast<double>(n);
+  const double t = 1.0 - z * z;
+  const double rho = sqrt(0.0 < t ? t : 0.0);
+  const double phi = az_step * static_cast<double>(k);
+  double s, c;
+  sincos_cr(phi, &s, &c);
+  return d3(rho * c, rho * s, z);
+}
+
+__global__ void __launch_bounds__(128) trace_kernel(const TraceParams p) {
+  extern __shared__ TNode smem_nodes[];
+  const int32_t K = p.use_smem ? p.hdr.K : 0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) smem_nodes[i] = p.nodes[i];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int64_t ray = -1;
+  bool exhausted = false;
+  D3 o{}, d{};
+  double path = 0.0;
+  int32_t steps = 0, bounces = 0;
+  unsigned long long st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
+  int32_t st_max = 0;
+
+  for (;;) {
+    const bool need = ray < 0 && !exhausted;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(p.ray_counter, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int64_t i = static_cast<int64_t>(base) + __popc(m & lt_mask);
+        if (i < p.count) {
+          ray = i;
+          o = d3(p.src[0], p.src[1], p.src[2]);
+          if (p.dirs) {
+            d = d3(p.dirs[3 * i], p.dirs[3 * i + 1], p.dirs[3 * i + 2]);
+          } else {
+            d = fib_dir(global_ray(p, i), p.N, p.az_step);
+          }
+          path = 0.0;
+          steps = 0;
+          bounces = 0;
+          if (p.max_iter <= 0) {  // trace() with a zero cap: nothing runs
+            st_alive++;
+            ray = -1;
+          }
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, ray < 0)) {
+      if (__all_sync(0xffffffffu, exhausted)) break;
+      continue;
+    }
+    if (ray < 0) continue;
+
+    // ---- one step_ray (tracer.cpp:19-62)
+    ++steps;
+    const HitResult wall = closest_hit(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d);
+    const bool has_wall = wall.face >= 0;
+    for (int r = 0; r < p.n_recv; ++r) {
+      const double sd = sphere_delta(o, d, d3(p.rc[r][0], p.rc[r][1], p.rc[r][2]), p.rr[r]);
+      bool cap = sd > 0.0 && (!has_wall || sd < wall.delta);
+      double L = 0.0;
+      if (cap) {
+        L = path + sd;
+        cap = L <= p.max_range;
+      }
+      const unsigned act = __activemask();
+      const unsigned cm = __ballot_sync(act, cap);
+      if (cm) {
+        const int leader = __ffs(cm) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(p.cap_count, (unsigned long long)__popc(cm));
+        base = __shfl_sync(act, base, leader);
+        if (cap) {
+          const unsigned long long slot = base + __popc(cm & lt_mask);
+          if (slot < static_cast<unsigned long long>(p.cap_capacity)) {
+            Capture c;
+            const D3 pt = o + sd * d;
+            c.p[0] = pt.x; c.p[1] = pt.y; c.p[2] = pt.z;
+            c.d[0] = d.x; c.d[1] = d.y; c.d[2] = d.z;
+            c.path = L;
+            c.ray = static_cast<int32_t>(ray);
+            c.meta = (bounces << 8) | r;
+            p.caps[slot] = c;
+          }
+        }
+      }
+    }
+    bool dead = false;
+    if (!has_wall) {
+      dead = true;
+      st_esc++;
+    } else {
+      const double* nn = p.normal + 3 * static_cast<int64_t>(wall.face);
+      D3 n = d3(__ldg(nn), __ldg(nn + 1), __ldg(nn + 2));
+      if (dot(n, d) > 0.0) n = d3(-n.x, -n.y, -n.z);
+      const D3 pt = o + wall.delta * d;
+      const double s2 = 2.0 * dot(d, n);
+      d = d - s2 * n;  // reflect, tracer.hpp:33-37
+      o = pt;
+      path += wall.delta;
+      p.hist[ray * p.H + bounces] = wall.face;
+      ++bounces;
+      if (path > p.max_range) {
+        dead = true;
+        st_oor++;
+      }
+    }
+    if (!dead && steps >= p.max_iter) {
+      dead = true;
+      st_alive++;
+    }
+    if (dead) {
+      st_bounce += steps;
+      st_max = max(st_max, steps);
+      ray = -1;
+    }
+  }
+  // ---- statistics
+  for (int off = 16; off > 0; off >>= 1) {
+    st_bounce += __shfl_xor_sync(0xffffffffu, st_bounce, off);
+    st_esc += __shfl_xor_sync(0xffffffffu, st_esc, off);
+    st_oor += __shfl_xor_sync(0xffffffffu, st_oor, off);
+    st_alive += __shfl_xor_sync(0xffffffffu, st_alive, off);
+    st_max = max(st_max, __shfl_xor_sync(0xffffffffu, st_max, off));
+  }
+  if (lane == 0) {
+    atomicAdd(p.stats + 0, st_bounce);
+    atomicAdd(p.stats + 1, st_esc);
+    atomicAdd(p.stats + 2, st_oor);
+    atomicAdd(p.stats + 3, st_alive);
+    atomicMax(p.stats + 4, (unsigned long long)st_max);
+  }
+}
+
+// ---------------------------------------------------------------- captures
+__global__ void capture_keys_kernel(const Capture* __restrict__ caps, int64_t n, TraceParams p,
+                                    unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Capture c = caps[i];
+  const uint64_t k = static_cast<uint64_t>(global_ray(p, c.ray));
+  const uint64_t order = static_cast<uint32_t>(c.meta) >> 8;
+  const uint64_t recv = c.meta & 0xff;
+  keys[i] = (recv << 56) | (k << 20) | order;
+  idx[i] = static_cast<int32_t>(i);
+}
+
+__global__ void capture_len_kernel(const Capture* __restrict__ caps, const int32_t* __restrict__ idx, int64_t n,
+                                   int64_t* __restrict__ len) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) len[i] = static_cast<uint32_t>(caps[idx[i]].meta) >> 8;
+  if (i == n) len[i] = 0;
+}
+
+// Sorted SoA captures + face paths + band multipliers (the ordered product
+// of (1 - alpha), tracer.cpp:57-58).
+__global__ void capture_out_kernel(const Capture* __restrict__ caps, const int32_t* __restrict__ idx, int64_t n,
+                                   TraceParams p, const int32_t* __restrict__ mat, const double* __restrict__ oma,
+                                   const int64_t* __restrict__ off, int32_t* __restrict__ o_recv,
+                                   int32_t* __restrict__ o_ray, double* __restrict__ o_point,
+                                   double* __restrict__ o_dir, double* __restrict__ o_path,
+                                   double* __restrict__ o_mult, int32_t* __restrict__ o_hist) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Capture c = caps[idx[i]];
+  const int32_t order = static_cast<uint32_t>(c.meta) >> 8;
+  o_recv[i] = c.meta & 0xff;
+  o_ray[i] = static_cast<int32_t>(global_ray(p, c.ray));
+  for (int k = 0; k < 3; ++k) {
+    o_point[3 * i + k] = c.p[k];
+    o_dir[3 * i + k] = c.d[k];
+  }
+  o_path[i] = c.path;
+  double m[kBands];
+  for (int b = 0; b < kBands; ++b) m[b] = 1.0;
+  const int32_t* h = p.hist + static_cast<int64_t>(c.ray) * p.H;
+  const int64_t base = off[i];
+  for (int j = 0; j < order; ++j) {
+    const int32_t f = h[j];
+    o_hist[base + j] = f;
+    const double* a = oma + kBands * mat[f];
+    for (int b = 0; b < kBands; ++b) m[b] *= a[b];
+  }
+  for (int b = 0; b < kBands; ++b) o_mult[kBands * i + b] = m[b];
+}
+
+// ---------------------------------------------------------------- queries
+__global__ void nearest_hit_kernel(TravHeader h, const TNode* __restrict__ nodes, const FaceTri* __restrict__ tri,
+                                   const double* __restrict__ o, const double* __restrict__ d, int64_t n,
+                                   int32_t* __restrict__ face, double* __restrict__ delta,
+                                   double* __restrict__ point) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const D3 oo = d3(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+  const D3 dd = d3(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+  const HitResult r = closest_hit(h, nodes, nullptr, 0, tri, oo, dd);
+  face[i] = r.face;
+  delta[i] = r.face >= 0 ? r.delta : 0.0;
+  const D3 pt = r.face >= 0 ? oo + r.delta * dd : d3(0, 0, 0);
+  point[3 * i] = pt.x;
+  point[3 * i + 1] = pt.y;
+  point[3 * i + 2] = pt.z;
+}
+
+// nearest_hit_brute accel_tree.cpp:183-191 (strict <: lowest face on ties)
+__global__ void brute_hit_kernel(const FaceTri* __restrict__ tri, int64_t nf, const double* __restrict__ o,
+                                 const double* __restrict__ d, int64_t n, int32_t* __restrict__ face,
+                                 double* __restrict__ delta, double* __restrict__ point) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const D3 oo = d3(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+  const D3 dd = d3(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+  int32_t bf = -1;
+  double bd = 0.0;
+  for (int64_t f = 0; f < nf; ++f) {
+    const double t = mt_delta(tri, static_cast<int32_t>(f), oo, dd);
+    if (t > 0.0 && (bf < 0 || t < bd)) {
+      bd = t;
+      bf = static_cast<int32_t>(f);
+    }
+  }
+  face[i] = bf;
+  delta[i] = bf >= 0 ? bd : 0.0;
+  const D3 pt = bf >= 0 ? oo + bd * dd : d3(0, 0, 0);
+  point[3 * i] = pt.x;
+  point[3 * i + 1] = pt.y;
+  point[3 * i + 2] = pt.z;
+}
+
+void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d, int64_t n, int brute, int32_t* d_face,
+                       double* d_delta, double* d_point) {
+  if (n <= 0) return;
+  const unsigned g = static_cast<unsigned>((n + 127) / 128);
+  if (brute)
+    brute_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->tri.p, s->nf, d_o, d_d, n, d_face, d_delta, d_point);
+  else
+    nearest_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->hdr, s->tnodes.p, s->tri.p, d_o, d_d, n, d_face,
+                                                       d_delta, d_point);
+  RR_LAUNCH_CHECK();
+  s->ctx->launches++;
+}
+
+}  // namespace rr
+
+namespace rr {
+
+rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, int32_t n_recv,
+                           const rr_trace_config* cfg, const double* d_dirs) {
+  if (n_recv < 1 || n_recv > kMaxRecv) invalid("n_recv must be in [1, 8]");
+  for (int r = 0; r < n_recv; ++r)
+    if (!(recv[r].radius > 0.0)) invalid("receiver radius must be > 0");  // tracer.cpp:111-113
+  if (src->ray_count < 1) invalid("source ray_count must be >= 1");       // emission.cpp:9-11
+  if (cfg->max_iterations > (1 << 20) - 1) invalid("max_iterations must be < 2^20");
+  if (src->ray_count >= (int64_t(1) << 36)) invalid("ray_count must be < 2^36");
+  cudaStream_t st = s->ctx->stream;
+  auto res = std::make_unique<rr_trace_result>();
+  res->scene = s;
+  TraceParams& p = res->params;
+  p.nodes = s->tnodes.p;
+  p.tri = s->tri.p;
+  p.normal = s->normal.p;
+  p.hdr = s->hdr;
+  p.use_smem = (cfg->flags & RR_TRACE_NO_SMEM_CACHE) ? 0 : 1;
+  for (int k = 0; k < 3; ++k) p.src[k] = src->position[k];
+  p.N = src->ray_count;
+  // ray subset
+  int64_t count;
+  if (cfg->block > 0) {
+    const int64_t world = std::max<int64_t>(cfg->stride, 1), rank = cfg->first;
+    if (rank < 0 || rank >= world) invalid("block-cyclic rank out of range");
+    const int64_t nblk = (p.N + cfg->block - 1) / cfg->block;
+    const int64_t my_full = nblk / world + (rank < nblk % world ? 1 : 0);
+    count = my_full * cfg->block;
+    // trim the last (partial) global block if this rank owns it
+    const int64_t last_blk = nblk - 1;
+    if (last_blk % world == rank) count -= nblk * cfg->block - p.N;
+    p.first = rank;
+    p.stride = world;
+    p.block = cfg->block;
+  } else if (cfg->stride <= 0) {
+    count = p.N;
+    p.first = 0;
+    p.stride = 1;
+    p.block = 0;
+  } else {
+    if (cfg->first < 0 || cfg->first >= p.N) invalid("subset first out of range");
+    count = (p.N - cfg->first + cfg->stride - 1) / cfg->stride;
+    if (cfg->count > 0) count = std::min(count, cfg->count);
+    p.first = cfg->first;
+    p.stride = cfg->stride;
+    p.block = 0;
+  }
+  p.count = count;
+  const double golden = (1.0 + std::sqrt(5.0)) / 2.0;
+  p.az_step = 2.0 * M_PI * (1.0 - 1.0 / golden);
+  p.dirs = d_dirs;
+  DevBuf<double> host_dirs;
+  if (!d_dirs && cfg->directions) {
+    host_dirs.alloc(3 * std::max<int64_t>(count, 1), st);
+    RR_CUDA(cudaMemcpyAsync(host_dirs.p, cfg->directions, sizeof(double) * 3 * count, cudaMemcpyHostToDevice, st));
+    p.dirs = host_dirs.p;
+  }
+  p.n_recv = n_recv;
+  for (int r = 0; r < n_recv; ++r) {
+    for (int k = 0; k < 3; ++k) p.rc[r][k] = recv[r].center[k];
+    p.rr[r] = recv[r].radius;
+    res->recv_center.insert(res->recv_center.end(), recv[r].center, recv[r].center + 3);
+    res->recv_radius.push_back(recv[r].radius);
+  }
+  p.max_iter = cfg->max_iterations;
+  // resolved_max_range (tracer.cpp:10-15), first receiver
+  p.max_range = cfg->max_range > 0.0 ? cfg->max_range
+                                     : 0.5 * recv[0].radius * std::sqrt(static_cast<double>(p.N));
+  p.H = std::max(cfg->max_iterations, 1);
+  res->hist.alloc(static_cast<size_t>(std::max<int64_t>(count, 1)) * p.H, st);
+  p.hist = res->hist.p;
+
+  DevBuf<unsigned long long> counters;
+  counters.alloc(8, st);
+  p.cap_count = counters.p;
+  p.ray_counter = counters.p + 1;
+  p.stats = counters.p + 2;
+
+  int64_t capacity = std::max<int64_t>(1 << 16, count / 2 * n_recv);
+  DevBuf<Capture> caps;
+  const size_t smem = p.use_smem ? sizeof(TNode) * static_cast<size_t>(p.hdr.K) : 0;
+  RR_CUDA(cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  int blocks_per_sm = 0;
+  RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_kernel, 128, smem));
+  blocks_per_sm = std::max(blocks_per_sm, 1);
+  const int64_t want = (count + 127) / 128;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)s->ctx->sm_count * blocks_per_sm)));
+  cudaEvent_t e0, e1;
+  RR_CUDA(cudaEventCreate(&e0));
+  RR_CUDA(cudaEventCreate(&e1));
+  unsigned long long hc[8];
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    caps.alloc(capacity, st);
+    p.caps = caps.p;
+    p.cap_capacity = capacity;
+    RR_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * 8, st));
+    RR_CUDA(cudaEventRecord(e0, st));
+    trace_kernel<<<grid, 128, smem, st>>>(p);
+    RR_LAUNCH_CHECK();
+    RR_CUDA(cudaEventRecord(e1, st));
+    s->ctx->launches++;
+    RR_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof hc, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    if (static_cast<int64_t>(hc[0]) <= capacity) break;
+    capacity = static_cast<int64_t>(hc[0]);  // exact re-run with the measured size
+  }
+  RR_CUDA(cudaEventElapsedTime(&res->kernel_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const int64_t nc = static_cast<int64_t>(hc[0]);
+  rr_trace_stats& S = res->stats;
+  S.ray_bounces = static_cast<int64_t>(hc[2]);
+  S.escaped = static_cast<int64_t>(hc[3]);
+  S.out_of_range = static_cast<int64_t>(hc[4]);
+  S.truncated = hc[5] > 0 ? 1 : 0;
+  S.iterations = cfg->max_iterations > 0 ? static_cast<int32_t>(hc[6]) : 0;
+  S.max_range = p.max_range;
+  S.n_captures = nc;
+  S.n_rays = count;
+
+  // ---- sort captures by (receiver, ray, order) and materialise
+  const bool sort = !(cfg->flags & RR_TRACE_KEEP_UNSORTED);
+  DevBuf<unsigned long long> keys, keys_o;
+  DevBuf<int32_t> idx, idx_o;
+  keys.alloc(std::max<int64_t>(nc, 1), st);
+  keys_o.alloc(std::max<int64_t>(nc, 1), st);
+  idx.alloc(std::max<int64_t>(nc, 1), st);
+  idx_o.alloc(std::max<int64_t>(nc, 1), st);
+  res->c_off.alloc(nc + 1, st);
+  if (nc > 0) {
+    const unsigned g = static_cast<unsigned>((nc + 255) / 256);
+    capture_keys_kernel<<<g, 256, 0, st>>>(caps.p, nc, p, keys.p, idx.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches++;
+    int32_t* order_idx = idx.p;
+    if (sort) {
+      size_t tb = 0;
+      RR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_o.p, idx.p, idx_o.p, static_cast<int>(nc),
+                                              0, 64, st));
+      DevBuf<uint8_t> tmp;
+      tmp.alloc(tb, st);
+      RR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_o.p, idx.p, idx_o.p, static_cast<int>(nc), 0,
+                                              64, st));
+      s->ctx->launches += 4;
+      order_idx = idx_o.p;
+    }
+    DevBuf<int64_t> len;
+    len.alloc(nc + 1, st);
+    capture_len_kernel<<<static_cast<unsigned>((nc + 256) / 256), 256, 0, st>>>(caps.p, order_idx, nc, len.p);
+    RR_LAUNCH_CHECK();
+    size_t tb = 0;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, res->c_off.p, static_cast<int>(nc + 1), st));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb, st);
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, len.p, res->c_off.p, static_cast<int>(nc + 1), st));
+    int64_t total = 0;
+    RR_CUDA(cudaMemcpyAsync(&total, res->c_off.p + nc, sizeof total, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    S.total_history = total;
+    res->c_recv.alloc(nc, st);
+    res->c_ray.alloc(nc, st);
+    res->c_point.alloc(3 * nc, st);
+    res->c_dir.alloc(3 * nc, st);
+    res->c_path.alloc(nc, st);
+    res->c_mult.alloc(kBands * nc, st);
+    res->c_hist.alloc(std::max<int64_t>(total, 1), st);
+    capture_out_kernel<<<g, 256, 0, st>>>(caps.p, order_idx, nc, p, s->mat.p, s->oma.p, res->c_off.p,
+                                           res->c_recv.p, res->c_ray.p, res->c_point.p, res->c_dir.p,
+                                           res->c_path.p, res->c_mult.p, res->c_hist.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 4;
+  } else {
+    RR_CUDA(cudaMemsetAsync(res->c_off.p, 0, sizeof(int64_t), st));
+  }
+  RR_CUDA(cudaStreamSynchronize(st));
+  return res.release();
+}
+
+}  // namespace rr

@@ -1,0 +1,78 @@
+// Trace-result layout shared by rr_trace.cu, rr_images.cu and rr_api.cu.
+#pragma once
+
+#include "rr_geom.cuh"
+
+namespace rr {
+
+constexpr int kMaxRecv = 8;
+
+struct Capture {
+  double p[3];
+  double d[3];
+  double path;
+  int32_t ray;   // local ray index (row of the history table)
+  int32_t meta;  // order << 8 | receiver
+};
+static_assert(sizeof(Capture) == 64, "capture record");
+
+struct TraceParams {
+  const TNode* nodes;
+  const FaceTri* tri;
+  const double* normal;
+  TravHeader hdr;
+  int32_t use_smem;
+  // lattice: local ray i -> global index via (first, stride, block)
+  double src[3];
+  int64_t N;
+  int64_t count;
+  int64_t first, stride, block;
+  double az_step;  // 2*pi*(1 - 1/golden) evaluated on the host
+  const double* dirs;  // optional explicit directions (count*3), else lattice
+  int32_t n_recv;
+  double rc[kMaxRecv][3];
+  double rr[kMaxRecv];
+  int32_t max_iter;
+  double max_range;
+  int32_t* hist;  // count * H
+  int64_t H;
+  Capture* caps;
+  unsigned long long* cap_count;
+  int64_t cap_capacity;
+  unsigned long long* ray_counter;
+  unsigned long long* stats;  // 0 bounces, 1 escaped, 2 out_of_range, 3 alive, 4 max steps
+};
+
+}  // namespace rr
+
+struct rr_trace_result {
+  rr_scene* scene = nullptr;
+  rr_trace_stats stats{};
+  float kernel_ms = 0.f;
+  rr::TraceParams params{};
+  rr::DevBuf<int32_t> hist;
+  rr::DevBuf<int32_t> c_recv, c_ray, c_hist;
+  rr::DevBuf<double> c_point, c_dir, c_path, c_mult;
+  rr::DevBuf<int64_t> c_off;
+  std::vector<double> recv_center, recv_radius;
+};
+
+
+namespace rr {
+rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, int32_t n_recv,
+                           const rr_trace_config* cfg, const double* d_dirs);
+}  // namespace rr
+
+// Device image-source set (rr_images.cu), sorted by (order, distance, path).
+struct rr_images {
+  rr_scene* scene = nullptr;
+  int64_t n = 0, total_path = 0;
+  rr::DevBuf<double> pos, dist, energy, mult, proj;
+  rr::DevBuf<int32_t> ray_count, order, has_proj, path;
+  rr::DevBuf<int64_t> path_off;
+};
+
+namespace rr {
+rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_rays, const rr_air& air,
+                               const rr_cluster_options& opt);
+}  // namespace rr

@@ -1,0 +1,441 @@
+"""Host API mirroring the reference's C++ interface for the hot path.
+
+Same names, argument meaning and error behaviour as namespace ``roomray``
+(/root/reference/proj/include/roomray): ``build_tree`` (accel_tree.hpp:38),
+``nearest_hit`` / ``nearest_hit_brute`` (accel_tree.hpp:50-55), ``trace``
+(tracer.hpp:50-52), ``build_image_sources`` (image_sources.hpp:58-61),
+``air_beta_bands`` (air_absorption.hpp:30), ``build_pulse_trains`` +
+``synthesize`` (rir.hpp:33-45), ``design_band_filter`` (rir.hpp:38).
+``std::invalid_argument`` surfaces as ``ValueError``.  Everything runs through
+the C ABI of libroomray_b200.so on the GPU; there is no CPU path.
+Vectorised: queries take (n, 3) arrays where the reference takes one ray.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr
+
+NUM_BANDS = 8
+BAND_CENTERS_HZ = (62.5, 125.0, 250.0, 500.0, 1000.0, 2000.0, 4000.0, 8000.0)
+BAND_FILTER_TAPS = 1023
+SELF_HIT_EPSILON = 1e-6
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape is not None else a
+
+
+class Context:
+    """One CUDA device + stream (rr_ctx)."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.rr_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    @property
+    def stream(self) -> int:
+        return self.lib.rr_ctx_stream(self.h) or 0
+
+    @property
+    def launches(self) -> int:
+        return self.lib.rr_ctx_launches(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.rr_ctx_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class TriangleMesh:
+    """TriangleMesh (geometry.hpp:60-77) as arrays: vertices (nv,3) f64,
+    faces (nf,4) i32 [a, b, c, material_id], absorption (nmat,8) f64."""
+
+    vertices: np.ndarray
+    faces: np.ndarray
+    absorption: np.ndarray
+
+    def __post_init__(self):
+        self.vertices = _f64(self.vertices).reshape(-1, 3)
+        self.faces = np.ascontiguousarray(self.faces, dtype=np.int32).reshape(-1, 4)
+        self.absorption = _f64(self.absorption).reshape(-1, NUM_BANDS)
+
+    def face_count(self) -> int:
+        return len(self.faces)
+
+    def bounds(self):
+        return self.vertices.min(axis=0), self.vertices.max(axis=0)
+
+
+class AccelTree:
+    """Device scene + median-split tree (rr_scene)."""
+
+    def __init__(self, mesh: TriangleMesh, ctx: Context | None = None, validate: bool = True):
+        self.ctx = ctx or Context.default()
+        self.lib = self.ctx.lib
+        self.mesh = mesh
+        h = C.c_void_p()
+        check(self.lib.rr_scene_create(self.ctx.h, mesh.vertices.reshape(-1), len(mesh.vertices),
+                                       mesh.faces.reshape(-1), len(mesh.faces), mesh.absorption.reshape(-1),
+                                       len(mesh.absorption), int(validate), C.byref(h)))
+        self.h = h
+        n, root, depth = C.c_int64(), C.c_int32(), C.c_int32()
+        check(self.lib.rr_scene_tree_info(self.h, C.byref(n), C.byref(root), C.byref(depth)))
+        self._n, self.root, self._depth = n.value, root.value, depth.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.rr_scene_destroy(self.h)
+            self.h = None
+
+    def node_count(self) -> int:
+        return self._n
+
+    def depth(self) -> int:
+        return self._depth
+
+    def nodes(self) -> dict:
+        """Reference-layout nodes (TreeNode accel_tree.hpp:15-22)."""
+        arr = (_lib.TreeNode * self._n)()
+        check(self.lib.rr_scene_tree(self.h, C.cast(arr, C.c_void_p)))
+        raw = np.frombuffer(arr, dtype=np.dtype([("lo", "f8", 3), ("hi", "f8", 3), ("left", "i4"),
+                                                 ("right", "i4"), ("face", "i4"), ("pad", "i4")]))
+        return {k: np.array(raw[k]) for k in ("lo", "hi", "left", "right", "face")}
+
+    def leaf_count(self) -> int:
+        return int((self.nodes()["face"] >= 0).sum())
+
+    def normals(self) -> np.ndarray:
+        out = np.empty((len(self.mesh.faces), 3))
+        check(self.lib.rr_scene_normals(self.h, out.reshape(-1)))
+        return out
+
+    @property
+    def build_ms(self) -> float:
+        return self.lib.rr_scene_build_ms(self.h)
+
+
+def build_tree(mesh: TriangleMesh, ctx: Context | None = None, validate: bool = True) -> AccelTree:
+    """build_tree (accel_tree.hpp:38): device median-split build."""
+    return AccelTree(mesh, ctx, validate)
+
+
+def _hits(tree: AccelTree, origins, dirs, brute: bool):
+    o = _f64(origins).reshape(-1, 3)
+    d = _f64(dirs).reshape(-1, 3)
+    if o.shape != d.shape:
+        raise ValueError("origins and dirs must have the same shape")
+    n = len(o)
+    face = np.empty(n, np.int32)
+    delta = np.empty(n)
+    point = np.empty((n, 3))
+    check(tree.lib.rr_nearest_hit_batch(tree.h, o.reshape(-1), d.reshape(-1), n, int(brute), face, delta,
+                                        point.reshape(-1)))
+    return face, delta, point
+
+
+def nearest_hit(tree: AccelTree, origins, dirs):
+    """nearest_hit (accel_tree.hpp:50-51) for n rays -> (face, delta, point);
+    face = -1 where the reference returns std::nullopt."""
+    return _hits(tree, origins, dirs, False)
+
+
+def nearest_hit_brute(tree: AccelTree, origins, dirs):
+    """nearest_hit_brute (accel_tree.hpp:54-55)."""
+    return _hits(tree, origins, dirs, True)
+
+
+@dataclass
+class SourceConfig:
+    position: tuple = (0.0, 0.0, 0.0)
+    ray_count: int = 1
+
+
+@dataclass
+class Receiver:
+    center: tuple = (0.0, 0.0, 0.0)
+    radius: float = 0.1
+
+
+@dataclass
+class TraceConfig:
+    """TraceConfig (tracer.hpp:13-20).  thread_count is accepted for API
+    compatibility and ignored (the GPU grid replaces it)."""
+
+    max_iterations: int = 1000
+    speed_of_sound: float = 343.0
+    max_range: float = 0.0
+    thread_count: int = 1
+
+
+@dataclass
+class Captures:
+    """Capture records (tracer_types.hpp:27-34) as sorted arrays."""
+
+    recv: np.ndarray
+    ray: np.ndarray
+    point: np.ndarray
+    dir: np.ndarray
+    path: np.ndarray
+    mult: np.ndarray
+    hist_off: np.ndarray
+    hist: np.ndarray
+
+    def __len__(self):
+        return len(self.ray)
+
+    def history(self, i):
+        return self.hist[self.hist_off[i]:self.hist_off[i + 1]]
+
+    def select(self, mask) -> "Captures":
+        idx = np.nonzero(mask)[0]
+        lens = self.hist_off[idx + 1] - self.hist_off[idx]
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        hist = np.concatenate([self.history(i) for i in idx]) if len(idx) else np.zeros(0, np.int32)
+        return Captures(self.recv[idx], self.ray[idx], self.point[idx], self.dir[idx], self.path[idx],
+                        self.mult[idx], off, hist.astype(np.int32))
+
+
+@dataclass
+class TraceResult:
+    """TraceResult (tracer.hpp:22-29) + ray_bounces and kernel time."""
+
+    captures: Captures
+    iterations: int
+    truncated: bool
+    escaped: int
+    out_of_range: int
+    max_range: float
+    ray_bounces: int
+    n_rays: int
+    kernel_ms: float
+
+
+class DeviceTrace:
+    """A trace whose captures are still on the device (rr_trace_result)."""
+
+    def __init__(self, tree: AccelTree, h):
+        self.tree, self.h, self.lib = tree, h, tree.lib
+        st = _lib.TraceStats()
+        check(self.lib.rr_trace_stats_get(self.h, C.byref(st)))
+        self.stats = st
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.rr_trace_destroy(self.h)
+            self.h = None
+
+    @property
+    def kernel_ms(self) -> float:
+        return self.lib.rr_trace_kernel_ms(self.h)
+
+    def captures(self) -> Captures:
+        n = self.stats.n_captures
+        th = self.stats.total_history
+        c = Captures(np.empty(n, np.int32), np.empty(n, np.int32), np.empty((n, 3)), np.empty((n, 3)),
+                     np.empty(n), np.empty((n, NUM_BANDS)), np.empty(n + 1, np.int64),
+                     np.empty(max(th, 1), np.int32))
+        check(self.lib.rr_trace_captures(self.h, ptr(c.recv), ptr(c.ray), ptr(c.point), ptr(c.dir), ptr(c.path),
+                                         ptr(c.mult), ptr(c.hist_off), ptr(c.hist)))
+        c.hist = c.hist[:th]
+        return c
+
+    def result(self) -> TraceResult:
+        s = self.stats
+        return TraceResult(self.captures(), s.iterations, bool(s.truncated), s.escaped, s.out_of_range,
+                           s.max_range, s.ray_bounces, s.n_rays, self.kernel_ms)
+
+
+def trace_device(tree: AccelTree, source: SourceConfig, receivers, config: TraceConfig = TraceConfig(), *,
+                 first: int = 0, stride: int = 0, count: int = 0, block: int = 0, flags: int = 0,
+                 directions: np.ndarray | None = None) -> DeviceTrace:
+    recs = receivers if isinstance(receivers, (list, tuple)) else [receivers]
+    src = _lib.Source((C.c_double * 3)(*map(float, source.position)), int(source.ray_count))
+    rarr = (_lib.Receiver * len(recs))(*[_lib.Receiver((C.c_double * 3)(*map(float, r.center)), float(r.radius))
+                                         for r in recs])
+    dirs = None if directions is None else _f64(directions).reshape(-1, 3)
+    cfg = _lib.TraceConfig(int(config.max_iterations), float(config.speed_of_sound), float(config.max_range),
+                           int(first), int(stride), int(count), int(block), int(flags), ptr(dirs))
+    h = C.c_void_p()
+    check(tree.lib.rr_trace(tree.h, C.byref(src), rarr, len(recs), C.byref(cfg), C.byref(h)))
+    return DeviceTrace(tree, h)
+
+
+def trace(tree: AccelTree, source: SourceConfig, receivers, config: TraceConfig = TraceConfig(),
+          **subset) -> TraceResult:
+    """trace (tracer.hpp:50-52).  ``receivers`` may be one Receiver or a list
+    (each capture records its receiver index).  ``subset`` keywords
+    (first/stride/count or block-cyclic first=rank, stride=world, block=B)
+    select part of the N-ray lattice; ``directions`` (count x 3) replaces the
+    device-evaluated lattice with caller rays (the Ray span of step(),
+    tracer.hpp:43)."""
+    return trace_device(tree, source, receivers, config, **subset).result()
+
+
+@dataclass
+class AirModel:
+    """AirModel (air_absorption.hpp:10-23)."""
+
+    temperature_c: float = 20.0
+    relative_humidity: float = 50.0
+    pressure_kpa: float = 101.325
+    enabled: bool = True
+
+    @staticmethod
+    def off() -> "AirModel":
+        return AirModel(enabled=False)
+
+    def c(self):
+        return _lib.Air(int(self.enabled), self.temperature_c, self.relative_humidity, self.pressure_kpa)
+
+
+def air_beta_bands(air: AirModel) -> np.ndarray:
+    lib = _lib.load()
+    out = np.empty(NUM_BANDS)
+    a = air.c()
+    check(lib.rr_air_beta_bands(C.byref(a), out))
+    return out
+
+
+def design_band_filter(band: int, sample_rate: float, taps: int = BAND_FILTER_TAPS) -> np.ndarray:
+    """design_band_filter (rir.cpp:32-58), tap count parameterised."""
+    lib = _lib.load()
+    out = np.empty(taps)
+    check(lib.rr_band_filter(band, sample_rate, taps, out))
+    return out
+
+
+def reference_length(distance, speed_of_sound: float, sample_rate: float, taps: int = BAND_FILTER_TAPS) -> int:
+    lib = _lib.load()
+    d = _f64(distance).reshape(-1)
+    out = C.c_int64()
+    check(lib.rr_ir_reference_length(len(d), d, speed_of_sound, sample_rate, taps, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class RoomImpulseResponse:
+    """RoomImpulseResponse (rir.hpp:26-30) + the per-band responses."""
+
+    sample_rate: float
+    samples: np.ndarray
+    band_ir: np.ndarray
+
+
+def synthesize(distance, band_energy, speed_of_sound: float, sample_rate: float, taps: int = BAND_FILTER_TAPS,
+               length: int | None = None, ctx: Context | None = None) -> RoomImpulseResponse:
+    """build_pulse_trains + synthesize (rir.hpp:33-45) from image distances
+    and band energies.  ``length`` None = the reference's length
+    (rir.cpp:78-80)."""
+    ctx = ctx or Context.default()
+    d = _f64(distance).reshape(-1)
+    e = _f64(band_energy).reshape(-1, NUM_BANDS)
+    if len(d) != len(e):
+        raise ValueError("distance and band_energy disagree in length")
+    if length is None:
+        length = reference_length(d, speed_of_sound, sample_rate, taps)
+        if length == 0:
+            return RoomImpulseResponse(sample_rate, np.zeros(0), np.zeros((NUM_BANDS, 0)))
+    band = np.empty((NUM_BANDS, length))
+    bb = np.empty(length)
+    check(ctx.lib.rr_synthesize(ctx.h, len(d), d, e.reshape(-1), speed_of_sound, sample_rate, taps, length,
+                                ptr(band), ptr(bb)))
+    return RoomImpulseResponse(sample_rate, bb, band)
+
+
+@dataclass
+class ClusterOptions:
+    """ClusterOptions (image_sources.hpp:25-31)."""
+
+    tol_scale: float = 1e-6
+    merge_coplanar: bool = False
+
+
+@dataclass
+class ImageSources:
+    """ImageSource list (image_sources.hpp:14-23) as arrays, sorted by
+    (order, distance, face path)."""
+
+    position: np.ndarray
+    distance: np.ndarray
+    band_energy: np.ndarray
+    band_multiplier: np.ndarray
+    ray_count: np.ndarray
+    order: np.ndarray
+    has_projection: np.ndarray
+    projection: np.ndarray
+    path_off: np.ndarray
+    path: np.ndarray
+
+    def __len__(self):
+        return len(self.distance)
+
+    def face_path(self, i):
+        return self.path[self.path_off[i]:self.path_off[i + 1]]
+
+
+class DeviceImages:
+    """Image sources resident on the device (rr_images)."""
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+        n, tp = C.c_int64(), C.c_int64()
+        check(lib.rr_images_info(h, C.byref(n), C.byref(tp)))
+        self.n, self.total_path = n.value, tp.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.rr_images_destroy(self.h)
+            self.h = None
+
+    def fetch(self) -> ImageSources:
+        n = self.n
+        im = ImageSources(np.empty((n, 3)), np.empty(n), np.empty((n, NUM_BANDS)), np.empty((n, NUM_BANDS)),
+                          np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32), np.empty((n, 3)),
+                          np.empty(n + 1, np.int64), np.empty(max(self.total_path, 1), np.int32))
+        check(self.lib.rr_images_get(self.h, ptr(im.position), ptr(im.distance), ptr(im.band_energy),
+                                     ptr(im.band_multiplier), ptr(im.ray_count), ptr(im.order),
+                                     ptr(im.has_projection), ptr(im.projection), ptr(im.path_off), ptr(im.path)))
+        im.path = im.path[:self.total_path]
+        return im
+
+    def device_arrays(self):
+        """(dist device ptr, energy device ptr, n) for rr_ir_bin_device."""
+        d, e, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(self.lib.rr_images_device(self.h, C.byref(d), C.byref(e), C.byref(n)))
+        return d.value, e.value, n.value
+
+
+def build_image_sources_device(trace_res: DeviceTrace, total_rays: int, air: AirModel = AirModel(),
+                               options: ClusterOptions = ClusterOptions(), receiver: int = 0) -> DeviceImages:
+    a = air.c()
+    o = _lib.ClusterOptions(float(options.tol_scale), int(options.merge_coplanar))
+    h = C.c_void_p()
+    check(trace_res.lib.rr_build_image_sources(trace_res.h, int(receiver), int(total_rays), C.byref(a), C.byref(o),
+                                               C.byref(h)))
+    return DeviceImages(trace_res.lib, h)
+
+
+def build_image_sources(trace_res: DeviceTrace, total_rays: int, air: AirModel = AirModel(),
+                        options: ClusterOptions = ClusterOptions(), receiver: int = 0) -> ImageSources:
+    """build_image_sources (image_sources.hpp:58-61) for one receiver of a
+    device trace (captures never leave the GPU)."""
+    return build_image_sources_device(trace_res, total_rays, air, options, receiver).fetch()
