@@ -1,0 +1,382 @@
+"""Benchmark: rays*bounces/s of the specular trace on B200 (BASELINE.json
+metric), with the HBM-roofline fraction and the reference CPU path beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                  [--impl ours|reference]
+
+Workload (config.workload): BASELINE.json configs[1] (C2) — gridded 8x6x3 m
+shoebox, 100 000 triangles, seeded per-wall 8-band absorption, 10^6
+Fibonacci rays, 50 reflections, receiver r = 0.5 m; 2 s IR at 48 kHz.
+Synthetic, seeded (the reference ships no such mesh).
+
+One step = one trace of the whole lattice (device emission, persistent
+traversal kernel, capture compaction + sort) on the device-resident scene:
+`value` counts the nearest-hit queries executed (ray*bounces) per second.
+`e2e` is the same metric through the C ABI from pinned host arrays: scene
+upload + validation + device tree build + trace + image sources (coplanar
+merge on, RunConfig default) + 8-band IR synthesis + download of the images
+and IRs, every step.  Multi-GPU (torchrun): weak scaling, each rank traces a
+block-cyclic shard of an N*10^6 lattice, time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rays*bounces/sec (and % of HBM roofline)"
+UNIT = "ray*bounces/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+BRB_FILE = os.path.join(ROOT, "profiles", "brb_frozen.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def brb_model(config):
+    with open(BRB_FILE) as f:
+        return json.load(f)[config]
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_scene(name):
+    from paper_1811_05784_b200 import scenes
+    return scenes.CONFIGS[name]()
+
+
+def cpu_reference_sample(scene, seconds, threads):
+    """The reference's own trace loop (oracle/_ref: unmodified tracer.cpp,
+    step() with thread_count = threads) on a strided subset of the lattice,
+    sized to ~`seconds` of work.  Returns (rate, sample description, kind)."""
+    import oracle
+    if oracle.ref_available():
+        lib = oracle.Ref()
+        sc = lib.scene(oracle.Mesh(scene.vertices, scene.faces, scene.absorption))
+        kind = "reference"
+
+        def run(stride):
+            t = time.perf_counter()
+            _, st = sc.trace(scene.source, scene.ray_count, scene.receivers[0][0], scene.receivers[0][1],
+                             scene.max_iterations, scene.max_range, threads, 0, stride, 0)
+            return st.ray_bounces, time.perf_counter() - t
+    else:
+        lib = oracle.Port()
+        sc = lib.scene(oracle.Mesh(scene.vertices, scene.faces, scene.absorption))
+        kind = "port"
+
+        def run(stride):
+            t = time.perf_counter()
+            _, st = sc.trace(scene.source, scene.ray_count, [scene.receivers[0][0]], [scene.receivers[0][1]],
+                             scene.max_iterations, scene.max_range, threads, 0, stride, 0)
+            return st.ray_bounces, time.perf_counter() - t
+    probe = max(1, scene.ray_count // 2000)
+    rb, dt = run(probe)
+    rate = rb / max(dt, 1e-9)
+    per_ray = rb / ((scene.ray_count + probe - 1) // probe)
+    want_rays = max(threads * 64, int(rate * seconds / max(per_ray, 1)))
+    stride = max(1, scene.ray_count // max(want_rays, 1))
+    rb, dt = run(stride)
+    rays = (scene.ray_count + stride - 1) // stride
+    return rb / dt, f"{rays} of {scene.ray_count} lattice rays (k = 0 mod {stride}), {rb} ray*bounces, {dt:.2f} s", \
+        kind, rb, dt
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_05784_b200 import Context, Receiver, SourceConfig, TraceConfig, TriangleMesh
+    from paper_1811_05784_b200 import roomray as rr
+    from paper_1811_05784_b200 import _lib
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    scene = load_scene(args.config)
+    ctx = Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    mesh = TriangleMesh(scene.vertices, scene.faces, scene.absorption)
+    tree = rr.AccelTree(mesh, ctx)
+    n_total = scene.ray_count * world  # weak scaling: 10^6 rays per GPU
+    src = SourceConfig(scene.source, n_total)
+    recv = Receiver(*scene.receivers[0])
+    cfg = TraceConfig(max_iterations=scene.max_iterations, max_range=scene.max_range)
+    shard = dict(first=rank, stride=world, block=4096) if world > 1 else {}
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_trace():
+        return rr.trace_device(tree, src, recv, cfg, **shard)
+
+    for _ in range(args.warmup):
+        one_trace()
+    # ---- timed: device-resident trace
+    step_ms, kern_ms, bounces, launches = [], [], 0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush (512 MB > 126 MB L2) between steps
+            barrier()
+            l0 = ctx.launches
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record()
+            dt = one_trace()
+            with torch.cuda.stream(stream):
+                e1.record()
+            barrier()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(dt.kernel_ms)
+            bounces += dt.stats.ray_bounces
+            launches += ctx.launches - l0
+            del dt
+    my_ms = sum(step_ms)
+    t = torch.tensor([my_ms, float(bounces)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_ms, total_bounces = tmax[0].item(), tsum[1].item()
+    else:
+        total_ms, total_bounces = my_ms, float(bounces)
+    value = total_bounces / (total_ms / 1e3)
+
+    # ---- e2e through the C ABI from pinned host buffers
+    pv = torch.from_numpy(scene.vertices.reshape(-1)).pin_memory()
+    pt = torch.from_numpy(scene.faces.reshape(-1)).pin_memory()
+    pa = torch.from_numpy(scene.absorption.reshape(-1)).pin_memory()
+    L = int(round(scene.ir_seconds * scene.sample_rate))
+    taps = 1023
+    h2d = pv.numel() * 8 + pt.numel() * 4 + pa.numel() * 8
+    e2e_ms, d2h, breakdown = [], 0, {}
+    lib = _lib.load()
+    import ctypes as C
+
+    for it in range(args.warmup + args.steps):
+        barrier()
+        w0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record()
+        h = C.c_void_p()
+        _lib.check(lib.rr_scene_create(ctx.h, C.c_void_p(pv.data_ptr()), len(scene.vertices),
+                                       C.c_void_p(pt.data_ptr()), len(scene.faces), C.c_void_p(pa.data_ptr()),
+                                       len(scene.absorption), 1, C.byref(h)))
+        sc = rr.AccelTree.__new__(rr.AccelTree)
+        sc.ctx, sc.lib, sc.mesh, sc.h = ctx, lib, mesh, h
+        marks = []
+
+        def mark(name):
+            ev = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                ev.record()
+            marks.append((name, ev))
+
+        mark("scene")
+        dt = rr.trace_device(sc, src, recv, cfg, **shard)
+        mark("trace")
+        images = rr.build_image_sources_device(dt, n_total, rr.AirModel(), rr.ClusterOptions(1e-6, True))
+        mark("images")
+        d_dist, d_en, n_img = images.device_arrays()
+        hist = torch.empty(8 * (L + taps), dtype=torch.float64, device="cuda")
+        band = torch.empty(8 * L, dtype=torch.float64, device="cuda")
+        bb = torch.empty(L, dtype=torch.float64, device="cuda")
+        _lib.check(lib.rr_ir_bin_device(ctx.h, n_img, C.c_void_p(d_dist), C.c_void_p(d_en), scene.speed_of_sound,
+                                        scene.sample_rate, L + taps, C.c_void_p(hist.data_ptr())))
+        if world > 1:
+            torch.cuda.synchronize()
+            dist.all_reduce(hist)  # NCCL sum of the 8-band pulse histograms
+        _lib.check(lib.rr_ir_filter_device(ctx.h, C.c_void_p(hist.data_ptr()), scene.sample_rate, taps, L,
+                                           C.c_void_p(band.data_ptr()), C.c_void_p(bb.data_ptr())))
+        mark("ir")
+        host_ir = torch.empty(8 * L, dtype=torch.float64, pin_memory=True)
+        with torch.cuda.stream(stream):
+            host_ir.copy_(band, non_blocking=True)
+        img = images.fetch()
+        with torch.cuda.stream(stream):
+            e1.record()
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        if it >= args.warmup:
+            e2e_ms.append(max(e0.elapsed_time(e1), (w1 - w0) * 1e3))
+            prev = e0
+            for name, ev in marks + [("fetch", e1)]:
+                breakdown[name] = breakdown.get(name, 0.0) + prev.elapsed_time(ev) / args.steps
+                prev = ev
+            d2h = host_ir.numel() * 8 + sum(a.nbytes for a in (img.position, img.distance, img.band_energy,
+                                                                 img.band_multiplier, img.ray_count, img.order,
+                                                                 img.has_projection, img.projection, img.path_off,
+                                                                 img.path))
+        del images, dt
+        lib.rr_scene_destroy(h)
+        sc.h = None
+    e2e_local = sum(e2e_ms)
+    t = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = total_bounces / (t.item() / 1e3)
+
+    # ---- roofline of the dominant kernel (trace_kernel)
+    model = brb_model(args.config)
+    peak, peak_kind = hbm_peak()
+    kern_s = sum(kern_ms) / 1e3
+    achieved = model["B_rb"] * bounces / kern_s / 1e9
+    traffic = model.get("ncu_dram_bytes_per_launch")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+            "bytes_per_ray_bounce": round(model["B_rb"], 1), "kernel_ms_per_step": round(1e3 * kern_s / args.steps, 3),
+            "kernel_share_of_step": round(sum(kern_ms) / my_ms, 3)}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rate, sample, kind, _, _ = cpu_reference_sample(scene, args.cpu_seconds, threads)
+            cpu = {"value": round(rate, 1), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 conservative box filter)",
+            "data": "synthetic (seeded splitmix64 scene; no dataset)",
+            "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {n_total} rays, "
+                                   f"{scene.max_iterations} refl, 1 receiver",
+                       "rays_per_gpu": scene.ray_count, "parallelism": f"rays block-cyclic x{world}",
+                       "l2": "flushed between timed steps (512 MB write)"},
+            "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": round(t.item() / args.steps, 3),
+                    "stage_ms": {k: round(v, 3) for k, v in breakdown.items()}},
+            "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "ray_bounces_per_step": int(total_bounces / args.steps),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    scene = load_scene(args.config)
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, args.cpu_seconds / 3)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, sample, kind, rb, dt = cpu_reference_sample(scene, per_step, threads)
+        if i >= args.warmup:
+            rates.append((rb, dt, sample, kind))
+    rb = sum(r[0] for r in rates)
+    dt = sum(r[1] for r in rates)
+    value = rb / dt
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+           "data": "synthetic (seeded splitmix64 scene; no dataset)",
+           "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {scene.ray_count} rays, "
+                                  f"{scene.max_iterations} refl, 1 receiver", "parallelism": f"{threads} CPU threads"},
+           "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": rates[0][3],
+                            "sample": rates[0][2] + " per step"},
+           "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -200,6 +200,7 @@ void* rref_trace(void* h, const double* src, int32_t ray_count,
       const auto all = emit(source);
       std::vector<Ray> rays;
       std::vector<int> global;
+      if (count <= 0) count = (ray_count - first + stride - 1) / stride;
       for (int64_t i = 0; i < count; ++i) {
         const int64_t k = first + i * stride;
         if (k >= ray_count) break;

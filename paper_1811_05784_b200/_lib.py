@@ -68,7 +68,7 @@ SIGNATURES = [
     ("rr_ctx_destroy", C.c_int, [_vp]),
     ("rr_ctx_stream", _vp, [_vp]),
     ("rr_ctx_launches", _i64, [_vp]),
-    ("rr_scene_create", C.c_int, [_vp, _f64p, _i64, _i32p, _i64, _f64p, _i32, _i32, C.POINTER(_vp)]),
+    ("rr_scene_create", C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i32, _i32, C.POINTER(_vp)]),
     ("rr_scene_destroy", C.c_int, [_vp]),
     ("rr_scene_tree_info", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)]),
     ("rr_scene_tree", C.c_int, [_vp, _vp]),

@@ -103,6 +103,12 @@ rr_status rr_ctx_create(int device, rr_ctx** out) {
     auto c = std::make_unique<rr_ctx>();
     c->device = device;
     RR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // keep freed stream-ordered allocations cached in the pool, so the
+    // per-call buffers of rr_trace & co. cost no driver round trips
+    cudaMemPool_t pool;
+    RR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    RR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     RR_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     cudaDeviceProp prop;
     RR_CUDA(cudaGetDeviceProperties(&prop, device));

@@ -325,22 +325,22 @@ __global__ void anchor_step_kernel(const int32_t* __restrict__ n_pred, const int
                                    int32_t* __restrict__ changed) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n || owner[i] != kUndet) return;
-  int32_t best = 0x7fffffff;
-  bool all = true;
+  // preds ascending: the first anchor among them owns i; an undecided pred
+  // before it means "wait"; none => i is an anchor
   for (int32_t k = 0; k < n_pred[i]; ++k) {
     const int32_t j = pred[pred_off[i] + k];
     const int32_t o = owner[j];
     if (o == kUndet) {
-      all = false;
-    } else if (o == kAnchor) {
-      best = j < best ? j : best;
+      *changed = 1;
+      return;
+    }
+    if (o == kAnchor) {
+      owner[i] = j;
+      *changed = 1;
+      return;
     }
   }
-  if (!all) {
-    *changed = 1;
-    return;
-  }
-  owner[i] = best == 0x7fffffff ? kAnchor : best;
+  owner[i] = kAnchor;
   *changed = 1;
 }
 
@@ -527,6 +527,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     RR_CUDA(cudaStreamSynchronize(st));
     return im.release();
   }
+  StageTimer tm(st);
   PathView pv{tr->c_off.p, tr->c_hist.p};
   DevBuf<double> retro;
   DevBuf<int32_t> idx, head, gid;
@@ -539,6 +540,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceMergeSort::StableSortKeys(t, b, idx.p, n, PathLess{pv}, st);
   }, st);
+  tm.mark("path sort");
   head_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, pv, head.p);
   RR_LAUNCH_CHECK();
   cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, head.p, gid.p, n, st); }, st);
@@ -581,6 +583,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
                                               tr->c_off.p, T);
   RR_LAUNCH_CHECK();
   ctx->launches += 8;
+  tm.mark("groups");
 
   // multiplier source per image: the representative capture (beam.front())
   DevBuf<double> mpos;
@@ -630,6 +633,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
                                                 n_succ.p, pred_off.p, succ_off.p, pred.p, succ.p);
     RR_LAUNCH_CHECK();
     sort_small_lists_kernel<<<grid(ni), 256, 0, st>>>(n_succ.p, succ_off.p, ni, succ.p);
+    sort_small_lists_kernel<<<grid(ni), 256, 0, st>>>(n_pred.p, pred_off.p, ni, pred.p);
     RR_LAUNCH_CHECK();
     anchor_init_kernel<<<grid(ni), 256, 0, st>>>(n_pred.p, ni, owner.p);
     RR_LAUNCH_CHECK();
@@ -667,6 +671,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     ni = na;
     mult_src = mrep.p + na;
   }
+  tm.mark("coplanar merge");
   EnergyParams ep;
   ep.hdr = s->hdr;
   ep.nodes = s->tnodes.p;
@@ -684,6 +689,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   energy_kernel<<<grid(ni, 128), 128, 0, st>>>(M, mult_src, ni, tr->c_mult.p, ep, dist.p, energy.p, mult.p, has_proj.p,
                                           proj.p);
   RR_LAUNCH_CHECK();
+  tm.mark("energy+project");
   DevBuf<int32_t> perm;
   perm.alloc(ni, st);
   {
@@ -695,6 +701,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceMergeSort::SortKeys(t, b, perm.p, ni, FinalLess{M.order, dist.p, M.rep, pv}, st);
   }, st);
+  tm.mark("final sort");
   DevBuf<int64_t> len;
   len.alloc(ni + 1, st);
   im->path_off.alloc(ni + 1, st);
@@ -724,6 +731,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
                                                        im->path_off.p});
   RR_LAUNCH_CHECK();
   ctx->launches += 6;
+  tm.mark("gather");
   RR_CUDA(cudaStreamSynchronize(st));
   return im.release();
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -66,6 +68,31 @@ struct DevBuf {
   size_t bytes() const { return sizeof(T) * n; }
 };
 
+// Stage timing for development (RR_TIMING=1 prints CUDA-event intervals).
+struct StageTimer {
+  cudaStream_t s;
+  bool on;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  explicit StageTimer(cudaStream_t st) : s(st), on(std::getenv("RR_TIMING") != nullptr) { mark("start"); }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  ~StageTimer() {
+    if (!on) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      std::fprintf(stderr, "[rr timing] %-24s %9.3f ms\n", ev[i].first, ms);
+    }
+    for (auto& p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 // Reference-layout node (TreeNode accel_tree.hpp:15-22), same bytes as
 // rr_tree_node.
 struct RefNode {
@@ -124,6 +151,7 @@ struct rr_scene {
   int32_t root = -1, depth = 0, K = 0;
   double lo[3]{}, hi[3]{};        // TriangleMesh::bounds (geometry.cpp:41-45)
   float build_ms = 0.f;
+  double caps_per_ray = 0.0;      // capture rate of the last trace (buffer sizing)
 };
 
 namespace rr {

@@ -367,13 +367,19 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   p.ray_counter = counters.p + 1;
   p.stats = counters.p + 2;
 
-  int64_t capacity = std::max<int64_t>(1 << 16, count / 2 * n_recv);
+  // capture buffer: 2 per ray and receiver, or 1.25x the rate of the last
+  // trace of this scene; an overflow re-runs the kernel with the exact size
+  const double per_ray = std::max(2.0, 1.25 * s->caps_per_ray);
+  int64_t capacity = std::max<int64_t>(1 << 16, static_cast<int64_t>(per_ray * count * n_recv));
   DevBuf<Capture> caps;
   const size_t smem = p.use_smem ? sizeof(TNode) * static_cast<size_t>(p.hdr.K) : 0;
-  RR_CUDA(cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  int blocks_per_sm = 0;
-  RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_kernel, 128, smem));
-  blocks_per_sm = std::max(blocks_per_sm, 1);
+  static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
+  if (occ_cache_smem != static_cast<int>(smem)) {
+    RR_CUDA(cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache_blocks, trace_kernel, 128, smem));
+    occ_cache_smem = static_cast<int>(smem);
+  }
+  const int blocks_per_sm = std::max(occ_cache_blocks, 1);
   const int64_t want = (count + 127) / 128;
   const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)s->ctx->sm_count * blocks_per_sm)));
   cudaEvent_t e0, e1;
@@ -408,6 +414,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   S.max_range = p.max_range;
   S.n_captures = nc;
   S.n_rays = count;
+  s->caps_per_ray = static_cast<double>(nc) / static_cast<double>(std::max<int64_t>(count, 1) * n_recv);
 
   // ---- sort captures by (receiver, ray, order) and materialise
   const bool sort = !(cfg->flags & RR_TRACE_KEEP_UNSORTED);

@@ -12,6 +12,7 @@ Vectorised: queries take (n, 3) arrays where the reference takes one ray.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import math
 from dataclasses import dataclass, field
@@ -20,6 +21,11 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, ptr
+
+# Device handles are not released during interpreter shutdown (the CUDA
+# runtime may already be torn down); the process exit reclaims them.
+_SHUTDOWN = []
+atexit.register(lambda: _SHUTDOWN.append(True))
 
 NUM_BANDS = 8
 BAND_CENTERS_HZ = (62.5, 125.0, 250.0, 500.0, 1000.0, 2000.0, 4000.0, 8000.0)
@@ -93,16 +99,16 @@ class AccelTree:
         self.lib = self.ctx.lib
         self.mesh = mesh
         h = C.c_void_p()
-        check(self.lib.rr_scene_create(self.ctx.h, mesh.vertices.reshape(-1), len(mesh.vertices),
-                                       mesh.faces.reshape(-1), len(mesh.faces), mesh.absorption.reshape(-1),
-                                       len(mesh.absorption), int(validate), C.byref(h)))
+        check(self.lib.rr_scene_create(self.ctx.h, ptr(mesh.vertices), len(mesh.vertices), ptr(mesh.faces),
+                                       len(mesh.faces), ptr(mesh.absorption), len(mesh.absorption), int(validate),
+                                       C.byref(h)))
         self.h = h
         n, root, depth = C.c_int64(), C.c_int32(), C.c_int32()
         check(self.lib.rr_scene_tree_info(self.h, C.byref(n), C.byref(root), C.byref(depth)))
         self._n, self.root, self._depth = n.value, root.value, depth.value
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and not _SHUTDOWN:
             self.lib.rr_scene_destroy(self.h)
             self.h = None
 
@@ -239,7 +245,7 @@ class DeviceTrace:
         self.stats = st
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and not _SHUTDOWN:
             self.lib.rr_trace_destroy(self.h)
             self.h = None
 
@@ -402,7 +408,7 @@ class DeviceImages:
         self.n, self.total_path = n.value, tp.value
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and not _SHUTDOWN:
             self.lib.rr_images_destroy(self.h)
             self.h = None
 
