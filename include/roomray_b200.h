@@ -72,6 +72,8 @@ typedef struct {
 
 #define RR_TRACE_NO_SMEM_CACHE 1 /* traverse without the shared-memory top-level cache */
 #define RR_TRACE_KEEP_UNSORTED 2 /* skip the capture sort (timing only) */
+#define RR_TRACE_F32_LEAVES 4    /* diagnostic: fp32 leaf classification + fp64 resolution */
+#define RR_TRACE_WIDE 8          /* diagnostic: traverse the 4-wide collapse */
 
 /* Statistics of a trace (TraceResult, tracer.hpp:22-29). */
 typedef struct {
@@ -130,8 +132,9 @@ rr_status rr_scene_normals(rr_scene* scene, double* normals);
 double rr_scene_build_ms(rr_scene* scene);
 
 /* ---------------------------------------------------------------- queries
- * nearest_hit (accel_tree.hpp:50-51) for n rays; brute != 0 selects
- * nearest_hit_brute (accel_tree.hpp:54-55).  face[i] = -1 for no hit. */
+ * nearest_hit (accel_tree.hpp:50-51) for n rays; brute == 1 selects
+ * nearest_hit_brute (accel_tree.hpp:54-55); 2 / 3 select the diagnostic
+ * fp32-leaf / 4-wide traversals.  face[i] = -1 for no hit. */
 rr_status rr_nearest_hit_batch(rr_scene* scene, const double* origins,
                                const double* dirs, int64_t n, int32_t brute,
                                int32_t* face, double* delta, double* point);

@@ -17,6 +17,8 @@ LIB_PATH = os.path.join(HERE, "libroomray_b200.so")
 RR_OK, RR_INVALID_ARGUMENT, RR_RUNTIME, RR_CUDA, RR_NCCL = range(5)
 RR_TRACE_NO_SMEM_CACHE = 1
 RR_TRACE_KEEP_UNSORTED = 2
+RR_TRACE_F32_LEAVES = 4
+RR_TRACE_WIDE = 8
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")

@@ -55,7 +55,8 @@ __global__ void validate_faces_kernel(const double* __restrict__ v, int64_t nv, 
 
 // Moller-Trumbore operands and face normals (geometry.cpp:9-14, 80-82).
 __global__ void face_data_kernel(const double* __restrict__ v, const int32_t* __restrict__ t, int64_t nf,
-                                 rr::FaceTri* __restrict__ tri, double* __restrict__ normal,
+                                 rr::FaceTri* __restrict__ tri, float4* __restrict__ tri32,
+                                 double* __restrict__ normal,
                                  int32_t* __restrict__ mat) {
   using namespace rr;
   int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -70,6 +71,10 @@ __global__ void face_data_kernel(const double* __restrict__ v, const int32_t* __
   ft.e2x = e2.x; ft.e2y = e2.y; ft.e2z = e2.z;
   ft.pad = 0.0;
   tri[f] = ft;
+  tri32[3 * f] = make_float4(__double2float_rn(va.x), __double2float_rn(va.y), __double2float_rn(va.z),
+                             __int_as_float(static_cast<int>(f)));
+  tri32[3 * f + 1] = make_float4(__double2float_rn(e1.x), __double2float_rn(e1.y), __double2float_rn(e1.z), 0.f);
+  tri32[3 * f + 2] = make_float4(__double2float_rn(e2.x), __double2float_rn(e2.y), __double2float_rn(e2.z), 0.f);
   D3 n = cross(e1, e2);
   const double z = dot(n, n);
   if (z > 0.0) {
@@ -184,9 +189,10 @@ rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv, const in
     s->oma.alloc(oma.size(), st);
     RR_CUDA(cudaMemcpyAsync(s->oma.p, oma.data(), sizeof(double) * oma.size(), cudaMemcpyHostToDevice, st));
     s->tri.alloc(nf, st);
+    s->tri32.alloc(3 * nf, st);
     s->normal.alloc(3 * nf, st);
     s->mat.alloc(nf, st);
-    face_data_kernel<<<g, 256, 0, st>>>(s->verts.p, s->tris.p, nf, s->tri.p, s->normal.p, s->mat.p);
+    face_data_kernel<<<g, 256, 0, st>>>(s->verts.p, s->tris.p, nf, s->tri.p, s->tri32.p, s->normal.p, s->mat.p);
     RR_LAUNCH_CHECK();
     ctx->launches++;
     rr::build_scene_tree(s.get());

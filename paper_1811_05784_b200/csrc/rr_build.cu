@@ -34,7 +34,8 @@
 namespace rr {
 namespace {
 
-constexpr int kMaxCachedNodes = 511;  // 32 KB of TNodes in shared memory
+constexpr int kMaxCachedNodes = 511;   // 32 KB of TNodes in shared memory
+constexpr int kMaxCachedQNodes = 384;  // 48 KB of QNodes in shared memory
 
 __device__ __forceinline__ uint64_t ord_key(double x) {
   if (x == 0.0) x = 0.0;  // -0 == +0 in the reference comparisons
@@ -143,7 +144,9 @@ __global__ void seg_node_kernel(const Seg* __restrict__ segs, int64_t S,
                                 RefNode* __restrict__ ref, TNode* __restrict__ tn,
                                 TravHeader* __restrict__ hdr,
                                 int32_t* __restrict__ seg_axis,
-                                Seg* __restrict__ next) {
+                                Seg* __restrict__ next,
+                                int32_t* __restrict__ node_level,
+                                int32_t* __restrict__ node_tidx) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= S) return;
   const Seg sg = segs[j];
@@ -200,6 +203,8 @@ __global__ void seg_node_kernel(const Seg* __restrict__ segs, int64_t S,
     next[2 * rank[j] + 1] = R;
   }
   ref[node] = r;
+  node_level[node] = level;
+  node_tidx[node] = my_ref;
   if (sg.parent < 0) {
     hdr->root_ref = my_ref;
   } else {
@@ -268,6 +273,64 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg,
   const int64_t np = left ? sg.b + cnt_l : sg.b + nl + (i - sg.b - cnt_l);
   perm_out[k * nf + np] = perm[g];
   if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
+}
+
+// ---- 4-wide collapse: the even-depth internal nodes of the reference tree
+// become QNodes, indexed in the order of their BVH2 traversal index (BFS top
+// levels first, then preorder) so the cached prefix is the top of the tree.
+__global__ void q_flag_kernel(const RefNode* __restrict__ ref, const int32_t* __restrict__ level,
+                              const int32_t* __restrict__ tidx, int64_t n_nodes, int32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  if (ref[i].face < 0 && (level[i] & 1) == 0) flag[tidx[i]] = 1;
+}
+
+__device__ __forceinline__ void q_child(const RefNode* __restrict__ ref, const int32_t* __restrict__ tidx,
+                                        const int32_t* __restrict__ qidx, int32_t c, float eps, QNode& q,
+                                        int slot) {
+  const RefNode& n = ref[c];
+  reinterpret_cast<float*>(&q.lx)[slot] = lo_f(n.lo[0], eps);
+  reinterpret_cast<float*>(&q.hx)[slot] = hi_f(n.hi[0], eps);
+  reinterpret_cast<float*>(&q.ly)[slot] = lo_f(n.lo[1], eps);
+  reinterpret_cast<float*>(&q.hy)[slot] = hi_f(n.hi[1], eps);
+  reinterpret_cast<float*>(&q.lz)[slot] = lo_f(n.lo[2], eps);
+  reinterpret_cast<float*>(&q.hz)[slot] = hi_f(n.hi[2], eps);
+  reinterpret_cast<int32_t*>(&q.child)[slot] = n.face >= 0 ? ~n.face : qidx[tidx[c]];
+}
+
+__global__ void q_build_kernel(const RefNode* __restrict__ ref, const int32_t* __restrict__ level,
+                               const int32_t* __restrict__ tidx, const int32_t* __restrict__ qidx,
+                               int64_t n_nodes, const TravHeader* __restrict__ hdr, QNode* __restrict__ q) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  const RefNode n = ref[i];
+  if (n.face >= 0 || (level[i] & 1)) return;
+  const float eps = hdr->eps;
+  QNode out;
+  for (int s = 0; s < 4; ++s) {
+    // empty slot: a point box far outside every scene, never a usable hit
+    reinterpret_cast<float*>(&out.lx)[s] = 1e30f;
+    reinterpret_cast<float*>(&out.hx)[s] = 1e30f;
+    reinterpret_cast<float*>(&out.ly)[s] = 1e30f;
+    reinterpret_cast<float*>(&out.hy)[s] = 1e30f;
+    reinterpret_cast<float*>(&out.lz)[s] = 1e30f;
+    reinterpret_cast<float*>(&out.hz)[s] = 1e30f;
+    reinterpret_cast<int32_t*>(&out.child)[s] = kEmpty;
+  }
+  out.pad = make_int4(0, 0, 0, 0);
+  int slot = 0;
+  const int32_t kids[2] = {n.left, n.right};
+  for (int k = 0; k < 2; ++k) {
+    const RefNode& c = ref[kids[k]];
+    if (c.face >= 0) {
+      q_child(ref, tidx, qidx, kids[k], eps, out, slot++);
+    } else {
+      q_child(ref, tidx, qidx, c.left, eps, out, slot++);
+      q_child(ref, tidx, qidx, c.right, eps, out, slot++);
+    }
+  }
+  out.pad.x = slot;
+  q[qidx[tidx[i]]] = out;
 }
 
 __global__ void vert_bounds_kernel(const double* __restrict__ v, int64_t nv,
@@ -375,6 +438,9 @@ void build_scene_tree(rr_scene* s) {
   sflag.alloc(max_seg, st);
   srank.alloc(max_seg, st);
   saxis.alloc(max_seg, st);
+  DevBuf<int32_t> nlevel, ntidx;
+  nlevel.alloc(2 * nf - 1, st);
+  ntidx.alloc(2 * nf - 1, st);
   DevBuf<unsigned long long> bmin, bmax;
   bmin.alloc(3 * max_seg, st);
   bmax.alloc(3 * max_seg, st);
@@ -426,7 +492,7 @@ void build_scene_tree(rr_scene* s) {
     RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, sflag.p, srank.p, static_cast<int>(S), st));
     seg_node_kernel<<<grid_for(S), 256, 0, st>>>(segs, S, srank.p, bmin.p, bmax.p, perm, L, D,
                                                  level_base[L], static_cast<int32_t>(K), s->ref.p,
-                                                 s->tnodes.p, s->dhdr.p, saxis.p, nsegs);
+                                                 s->tnodes.p, s->dhdr.p, saxis.p, nsegs, nlevel.p, ntidx.p);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 4;
     if (split_count[L] == 0) break;
@@ -443,6 +509,35 @@ void build_scene_tree(rr_scene* s) {
     std::swap(perm, perm_o);
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
+  }
+
+  // ---- 4-wide collapse
+  int32_t k4 = 0;
+  {
+    const int64_t n_nodes = 2 * nf - 1, span = K + nf;
+    DevBuf<int32_t> qflag, qidx;
+    qflag.alloc(span + 1, st);
+    qidx.alloc(span + 1, st);
+    RR_CUDA(cudaMemsetAsync(qflag.p, 0, sizeof(int32_t) * (span + 1), st));
+    q_flag_kernel<<<grid_for(n_nodes), 256, 0, st>>>(s->ref.p, nlevel.p, ntidx.p, n_nodes, qflag.p);
+    RR_LAUNCH_CHECK();
+    size_t t = tmp.n;
+    size_t need = 0;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, qflag.p, qidx.p, static_cast<int>(span + 1), st));
+    if (need > t) tmp.alloc(need, st);
+    t = tmp.n;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, t, qflag.p, qidx.p, static_cast<int>(span + 1), st));
+    int32_t counts[2] = {0, 0};
+    RR_CUDA(cudaMemcpyAsync(&counts[0], qidx.p + span, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaMemcpyAsync(&counts[1], qidx.p + K, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    s->n_qnodes = counts[0];
+    s->qnodes.alloc(std::max<int64_t>(counts[0], 1), st);
+    q_build_kernel<<<grid_for(n_nodes), 256, 0, st>>>(s->ref.p, nlevel.p, ntidx.p, qidx.p, n_nodes, s->dhdr.p,
+                                                      s->qnodes.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 3;
+    k4 = std::min<int32_t>(counts[1], kMaxCachedQNodes);
   }
 
   // ---- TriangleMesh::bounds over all vertices (image-source tolerance)
@@ -468,6 +563,8 @@ void build_scene_tree(rr_scene* s) {
     s->hi[k] = hb[3 + k];
   }
   s->hdr.K = static_cast<int32_t>(K);
+  s->hdr.K4 = k4;
+  s->hdr.root4 = nf == 1 ? s->hdr.root_ref : 0;
   s->hdr.depth = s->depth;
   RR_CUDA(cudaMemcpyAsync(s->dhdr.p, &s->hdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
   RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));

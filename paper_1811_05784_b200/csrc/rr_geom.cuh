@@ -32,7 +32,8 @@ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
 
 constexpr int32_t kPop = 0x7fffffff;
 constexpr int32_t kDone = 0x7ffffffe;
-constexpr int kStack = 32;
+constexpr int kStack = 32;   // BVH2: one push per level, depth <= 30
+constexpr int kStack4 = 48;  // 4-wide: <= 3 pushes per level, depth <= 15
 
 // Moller-Trumbore, geometry.cpp:77-106 (double-sided, det == 0 rejected,
 // delta > kSelfHitEpsilon = 1e-6).  Returns delta or -1.
@@ -216,6 +217,267 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
     }
   }
   if (n_visit) *n_visit = visits;
+  return best;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 triangle classification.  The fp64 Moller-Trumbore decides every hit;
+// this filter only sorts leaves into
+//   0: the fp64 test certainly rejects it,
+//   1: uncertain (kept as a candidate for the fp64 test),
+//   2: the fp64 test certainly accepts it, with delta in [tlo, tup]
+//      (shifted frame), so tup may tighten the pruning bound.
+// u = (O-A).(D x E2), v = D.((O-A) x E1), t = E2.((O-A) x E1), det =
+// E1.(D x E2) are computed in fp32 from fp32-rounded inputs; each carries an
+// absolute error below K * (product of the L1 norms of its three factors),
+// K = 2^-19 (>= 32 units of fp32 roundoff), with |O-A| widened by the scene
+// scale S to cover the rounding of O and A.  Outside the margins the signs
+// of the exact quantities, hence the fp64 decisions, are known.
+__device__ __forceinline__ int mt32(const float4* __restrict__ tri32, int32_t f, const RayF& r, float dx, float dy,
+                                    float dz, float S, float* tlo, float* tup) {
+  const float4 A = __ldg(tri32 + 3 * f), E1 = __ldg(tri32 + 3 * f + 1), E2 = __ldg(tri32 + 3 * f + 2);
+  const float px = dy * E2.z - dz * E2.y, py = dz * E2.x - dx * E2.z, pz = dx * E2.y - dy * E2.x;
+  float det = E1.x * px + E1.y * py + E1.z * pz;
+  const float tx = r.ox - A.x, ty = r.oy - A.y, tz = r.oz - A.z;
+  float u = tx * px + ty * py + tz * pz;
+  const float qx = ty * E1.z - tz * E1.y, qy = tz * E1.x - tx * E1.z, qz = tx * E1.y - ty * E1.x;
+  float v = dx * qx + dy * qy + dz * qz;
+  float t = E2.x * qx + E2.y * qy + E2.z * qz;
+  const float K = 0x1p-19f;
+  const float nd = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  const float n1 = fabsf(E1.x) + fabsf(E1.y) + fabsf(E1.z);
+  const float n2 = fabsf(E2.x) + fabsf(E2.y) + fabsf(E2.z);
+  const float nt = fabsf(tx) + fabsf(ty) + fabsf(tz) + S;
+  const float m_det = K * n1 * nd * n2, m_u = K * nt * nd * n2, m_v = K * nd * nt * n1, m_t = K * n2 * nt * n1;
+  if (det < 0.0f) {
+    det = -det;
+    u = -u;
+    v = -v;
+    t = -t;
+  }
+  if (u < -m_u || v < -m_v || u + v > det + (m_u + m_v + m_det)) return 0;
+  if (det <= m_det) {  // near-parallel: undecidable here
+    *tlo = 0.0f;
+    *tup = __int_as_float(0x7f800000);
+    return 1;
+  }
+  const float lo = (t - m_t) / (det + m_det) * (1.0f - 0x1p-20f);
+  const float hi = (t + m_t) / (det - m_det) * (1.0f + 0x1p-20f);
+  const float sh = static_cast<float>(r.shift);
+  if (hi + sh < 0.5e-6f) return 0;  // delta <= kSelfHitEpsilon for sure
+  *tlo = lo;
+  *tup = hi;
+  const bool robust = u >= m_u && v >= m_v && u + v <= det - (m_u + m_v + m_det) && lo + sh > 2e-6f;
+  return robust ? 2 : 1;
+}
+
+constexpr int kCand = 16;
+
+// fp64-leaf traversal kept out of line: the rare fallback of closest_hit_f.
+static __device__ __noinline__ HitResult closest_hit_slow(const TravHeader& h, const TNode* __restrict__ nodes,
+                                                   const FaceTri* __restrict__ tri, D3 o, D3 d) {
+  return closest_hit(h, nodes, nullptr, 0, tri, o, d);
+}
+
+// Closest hit with an fp32 traversal (boxes + mt32) and fp64 resolution:
+// leaves of class 1/2 become candidates, robust hits tighten the pruning
+// bound, and the fp64 Moller-Trumbore picks the lexicographic (delta, face)
+// minimum among the candidates that can still win.  Same result as
+// closest_hit: a leaf holding the fp64-closest face is never pruned (its
+// entry <= that delta <= the bound) and never classed 0.
+__device__ __forceinline__ HitResult closest_hit_f(const TravHeader& h, const TNode* __restrict__ nodes,
+                                                   const float4* __restrict__ tri32, const FaceTri* __restrict__ tri,
+                                                   D3 o, D3 d) {
+  HitResult best{0.0, -1};
+  RayF r;
+  if (!make_rayf(h, o, d, r)) return best;
+  const float dx = __double2float_rn(d.x), dy = __double2float_rn(d.y), dz = __double2float_rn(d.z);
+  const float S = h.eps * 0x1p20f;
+  float tbest = FLT_MAX;
+  int32_t cand[kCand];
+  float cand_lo[kCand];
+  int nc = 0;
+  int32_t node;
+  if (h.root_ref < 0) {
+    node = h.root_ref;
+  } else {
+    const float t = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest);
+    node = (t == __int_as_float(0x7f800000)) ? kDone : h.root_ref;
+  }
+  int32_t st_n[kStack];
+  float st_t[kStack];
+  int sp = 0;
+  bool overflow = false;
+  auto flush = [&](int32_t f) {  // fp64 decision for one candidate
+    const double t = mt_delta(tri, f, o, d);
+    if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+      best.delta = t;
+      best.face = f;
+      tbest = fminf(tbest, prune_bound(t, r.shift));
+    }
+  };
+  while (node != kDone) {
+    if (node >= 0 && node != kPop) {
+      const float4* p = reinterpret_cast<const float4*>(nodes + node);
+      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      const int4 dd = __ldg(reinterpret_cast<const int4*>(p + 3));
+      const float tl = box_enter(r, a.x, a.y, a.z, a.w, b.x, b.y, tbest);
+      const float tr = box_enter(r, b.z, b.w, c.x, c.y, c.z, c.w, tbest);
+      const bool hl = tl != __int_as_float(0x7f800000), hr = tr != __int_as_float(0x7f800000);
+      if (hl && hr) {
+        const bool lf = tl <= tr;
+        st_n[sp] = lf ? dd.y : dd.x;
+        st_t[sp] = lf ? tr : tl;
+        ++sp;
+        node = lf ? dd.x : dd.y;
+      } else if (hl) {
+        node = dd.x;
+      } else if (hr) {
+        node = dd.y;
+      } else {
+        node = kPop;
+      }
+    } else if (node < 0) {
+      const int32_t f = ~node;
+      float lo, hi;
+      const int cls = mt32(tri32, f, r, dx, dy, dz, S, &lo, &hi);
+      if (cls == 2) tbest = fminf(tbest, hi);
+      if (cls != 0 && lo <= tbest) {
+        if (nc == kCand) {  // pathological: redo this ray with fp64 leaf tests
+          overflow = true;
+          break;
+        }
+        cand[nc] = f;
+        cand_lo[nc] = lo;
+        ++nc;
+      }
+      node = kPop;
+    }
+    if (node == kPop) {
+      node = kDone;
+      while (sp > 0) {
+        --sp;
+        if (st_t[sp] <= tbest) {
+          node = st_n[sp];
+          break;
+        }
+      }
+    }
+  }
+  if (overflow) return closest_hit_slow(h, nodes, tri, o, d);
+  for (int k = 0; k < nc; ++k)
+    if (cand_lo[k] <= tbest) flush(cand[k]);
+  return best;
+}
+
+__device__ __forceinline__ QNode load_qnode(const QNode* __restrict__ g, const QNode* s, int32_t n, int32_t K4) {
+  if (n < K4) return s[n];
+  const float4* p = reinterpret_cast<const float4*>(g + n);
+  QNode q;
+  q.lx = __ldg(p);
+  q.hx = __ldg(p + 1);
+  q.ly = __ldg(p + 2);
+  q.hy = __ldg(p + 3);
+  q.lz = __ldg(p + 4);
+  q.hz = __ldg(p + 5);
+  q.child = __ldg(reinterpret_cast<const int4*>(p + 6));
+  return q;
+}
+
+// Closest hit over the 4-wide collapse of the reference tree.  Same result
+// contract as closest_hit: lexicographic min of (delta, face) over the faces
+// the fp64 test accepts, visiting a superset of the reference's leaves.
+// Leaf children are tested as soon as their box is entered (shrinking the
+// pruning bound early); internal children are visited nearest first.
+__device__ __forceinline__ HitResult closest_hit4(const TravHeader& h, const QNode* __restrict__ nodes,
+                                                  const QNode* smem, int32_t K4, const FaceTri* __restrict__ tri,
+                                                  D3 o, D3 d) {
+  HitResult best{0.0, -1};
+  RayF r;
+  if (!make_rayf(h, o, d, r)) return best;
+  float tbest = FLT_MAX;
+  const float kInf = __int_as_float(0x7f800000);
+  int32_t node;
+  if (h.root4 < 0) {
+    node = h.root4;
+  } else {
+    const float t = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest);
+    node = (t == kInf) ? kDone : h.root4;
+  }
+  int32_t st_n[kStack4];
+  float st_t[kStack4];
+  int sp = 0;
+  while (node != kDone) {
+    if (node >= 0 && node != kPop) {
+      const QNode q = load_qnode(nodes, smem, node, K4);
+      const float lx[4] = {q.lx.x, q.lx.y, q.lx.z, q.lx.w}, hx[4] = {q.hx.x, q.hx.y, q.hx.z, q.hx.w};
+      const float ly[4] = {q.ly.x, q.ly.y, q.ly.z, q.ly.w}, hy[4] = {q.hy.x, q.hy.y, q.hy.z, q.hy.w};
+      const float lz[4] = {q.lz.x, q.lz.y, q.lz.z, q.lz.w}, hz[4] = {q.hz.x, q.hz.y, q.hz.z, q.hz.w};
+      const int32_t ch[4] = {q.child.x, q.child.y, q.child.z, q.child.w};
+      float t[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) t[s] = box_enter(r, lx[s], hx[s], ly[s], hy[s], lz[s], hz[s], tbest);
+      // leaves first (their hits tighten tbest)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (t[s] != kInf && ch[s] < 0 && ch[s] != kEmpty) {
+          const int32_t f = ~ch[s];
+          const double dt = mt_delta(tri, f, o, d);
+          if (dt > 0.0 && (best.face < 0 || dt < best.delta || (dt == best.delta && f < best.face))) {
+            best.delta = dt;
+            best.face = f;
+            tbest = prune_bound(dt, r.shift);
+          }
+        }
+      }
+      // internal children, nearest first
+      int32_t cn[4];
+      float ct[4];
+      int m = 0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (t[s] <= tbest && ch[s] >= 0) {
+          // insertion into the sorted (ascending t) list
+          int k = m++;
+          while (k > 0 && ct[k - 1] > t[s]) {
+            ct[k] = ct[k - 1];
+            cn[k] = cn[k - 1];
+            --k;
+          }
+          ct[k] = t[s];
+          cn[k] = ch[s];
+        }
+      }
+      if (m == 0) {
+        node = kPop;
+      } else {
+        for (int k = m - 1; k >= 1; --k) {
+          st_n[sp] = cn[k];
+          st_t[sp] = ct[k];
+          ++sp;
+        }
+        node = cn[0];
+      }
+    } else if (node < 0) {  // one-face mesh
+      const int32_t f = ~node;
+      const double dt = mt_delta(tri, f, o, d);
+      if (dt > 0.0) {
+        best.delta = dt;
+        best.face = f;
+      }
+      node = kPop;
+    }
+    if (node == kPop) {
+      node = kDone;
+      while (sp > 0) {
+        --sp;
+        if (st_t[sp] <= tbest) {
+          node = st_n[sp];
+          break;
+        }
+      }
+    }
+  }
   return best;
 }
 

@@ -111,12 +111,25 @@ struct __align__(16) TNode {
   int4 d;
 };
 
+// 4-wide traversal node collapsed from the reference tree (the even-depth
+// internal nodes; children = the grandchildren, or a child leaf): one 128-B
+// line, eight independent 16-B loads.  Components are SoA over the 4 slots.
+// child >= 0: QNode index; child < 0: leaf, face = ~child; kEmpty: unused.
+struct __align__(16) QNode {
+  float4 lx, hx, ly, hy, lz, hz;
+  int4 child;
+  int4 pad;
+};
+constexpr int32_t kEmpty = static_cast<int32_t>(0x80000000);
+
 struct TravHeader {
   float lo[3], hi[3];  // conservative root box
   int32_t root_ref;    // internal index 0, or ~face for a one-face mesh
   int32_t K;           // nodes [0, K) are the BFS-ordered top levels
   float eps;           // absolute box expansion (metres)
   int32_t depth;
+  int32_t root4;       // QNode root (0) or ~face for a one-face mesh
+  int32_t K4;          // QNodes [0, K4) are cached in shared memory
 };
 
 // Per-face fp64 data for Moller-Trumbore: a, b-a, c-a (geometry.cpp:80-82),
@@ -142,10 +155,13 @@ struct rr_scene {
   rr::DevBuf<int32_t> tris;       // nf*4
   rr::DevBuf<double> oma;         // nmat*8 : 1 - alpha
   rr::DevBuf<rr::FaceTri> tri;    // nf
+  rr::DevBuf<float4> tri32;       // nf*3: fp32 a (w = face bits), b-a, c-a (48 B leaf record)
   rr::DevBuf<double> normal;      // nf*3
   rr::DevBuf<int32_t> mat;        // nf
   rr::DevBuf<rr::RefNode> ref;    // 2nf-1 (reference layout)
   rr::DevBuf<rr::TNode> tnodes;   // K + nf
+  rr::DevBuf<rr::QNode> qnodes;   // 4-wide nodes
+  int64_t n_qnodes = 0;
   rr::DevBuf<rr::TravHeader> dhdr;
   rr::TravHeader hdr{};
   int32_t root = -1, depth = 0, K = 0;

@@ -45,10 +45,20 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
   return d3(rho * c, rho * s, z);
 }
 
-__global__ void __launch_bounds__(128) trace_kernel(const TraceParams p) {
+// V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
+// V = 1: binary nodes, fp64 test at every leaf (default)
+// V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
+template <int V, int MINB>
+__global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
+  constexpr bool WIDE = V == 2;
   extern __shared__ TNode smem_nodes[];
-  const int32_t K = p.use_smem ? p.hdr.K : 0;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) smem_nodes[i] = p.nodes[i];
+  QNode* smem_q = reinterpret_cast<QNode*>(smem_nodes);
+  const int32_t K = (p.use_smem && V != 0) ? (WIDE ? p.hdr.K4 : p.hdr.K) : 0;
+  if (WIDE) {
+    for (int i = threadIdx.x; i < K; i += blockDim.x) smem_q[i] = p.qnodes[i];
+  } else {
+    for (int i = threadIdx.x; i < K; i += blockDim.x) smem_nodes[i] = p.nodes[i];
+  }
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -99,7 +109,14 @@ __global__ void __launch_bounds__(128) trace_kernel(const TraceParams p) {
 
     // ---- one step_ray (tracer.cpp:19-62)
     ++steps;
-    const HitResult wall = closest_hit(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d);
+    HitResult wall;
+    if (V == 0) {
+      wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
+    } else if (V == 1) {
+      wall = closest_hit(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d);
+    } else {
+      wall = closest_hit4(p.hdr, p.qnodes, smem_q, K, p.tri, o, d);
+    }
     const bool has_wall = wall.face >= 0;
     for (int r = 0; r < p.n_recv; ++r) {
       const double sd = sphere_delta(o, d, d3(p.rc[r][0], p.rc[r][1], p.rc[r][2]), p.rr[r]);
@@ -231,7 +248,8 @@ __global__ void capture_out_kernel(const Capture* __restrict__ caps, const int32
 }
 
 // ---------------------------------------------------------------- queries
-__global__ void nearest_hit_kernel(TravHeader h, const TNode* __restrict__ nodes, const FaceTri* __restrict__ tri,
+__global__ void nearest_hit_kernel(TravHeader h, const TNode* __restrict__ nodes, const QNode* __restrict__ qnodes,
+                                   const float4* __restrict__ tri32, const FaceTri* __restrict__ tri,
                                    const double* __restrict__ o, const double* __restrict__ d, int64_t n,
                                    int32_t* __restrict__ face, double* __restrict__ delta,
                                    double* __restrict__ point) {
@@ -239,7 +257,8 @@ __global__ void nearest_hit_kernel(TravHeader h, const TNode* __restrict__ nodes
   if (i >= n) return;
   const D3 oo = d3(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
   const D3 dd = d3(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
-  const HitResult r = closest_hit(h, nodes, nullptr, 0, tri, oo, dd);
+  const HitResult r = tri32 ? closest_hit_f(h, nodes, tri32, tri, oo, dd) : qnodes ? closest_hit4(h, qnodes, nullptr, 0, tri, oo, dd)
+                             : closest_hit(h, nodes, nullptr, 0, tri, oo, dd);
   face[i] = r.face;
   delta[i] = r.face >= 0 ? r.delta : 0.0;
   const D3 pt = r.face >= 0 ? oo + r.delta * dd : d3(0, 0, 0);
@@ -277,11 +296,12 @@ void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d, int64_
                        double* d_delta, double* d_point) {
   if (n <= 0) return;
   const unsigned g = static_cast<unsigned>((n + 127) / 128);
-  if (brute)
+  if (brute == 1)
     brute_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->tri.p, s->nf, d_o, d_d, n, d_face, d_delta, d_point);
   else
-    nearest_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->hdr, s->tnodes.p, s->tri.p, d_o, d_d, n, d_face,
-                                                       d_delta, d_point);
+    nearest_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->hdr, s->tnodes.p, brute == 3 ? s->qnodes.p : nullptr,
+                                                       brute == 2 ? s->tri32.p : nullptr, s->tri.p, d_o, d_d, n,
+                                                       d_face, d_delta, d_point);
   RR_LAUNCH_CHECK();
   s->ctx->launches++;
 }
@@ -303,10 +323,17 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   res->scene = s;
   TraceParams& p = res->params;
   p.nodes = s->tnodes.p;
+  p.qnodes = s->qnodes.p;
+  // default: binary nodes, fp64 test at every leaf (fastest measured); diagnostics: fp32 leaf classification, 4-wide nodes
+  const int variant = (cfg->flags & RR_TRACE_F32_LEAVES) ? 1 : (cfg->flags & RR_TRACE_WIDE) ? 2 : 0;
+  p.wide = variant == 2 ? 1 : 0;
+  p.tri32 = s->tri32.p;
   p.tri = s->tri.p;
   p.normal = s->normal.p;
   p.hdr = s->hdr;
-  p.use_smem = (cfg->flags & RR_TRACE_NO_SMEM_CACHE) ? 0 : 1;
+  // shared-memory top-level cache: measured slower for the default kernel
+  // (profiles/r1_ab_variants.md), kept for the diagnostic ones
+  p.use_smem = (variant == 0 || (cfg->flags & RR_TRACE_NO_SMEM_CACHE)) ? 0 : 1;
   for (int k = 0; k < 3; ++k) p.src[k] = src->position[k];
   p.N = src->ray_count;
   // ray subset
@@ -372,12 +399,24 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   const double per_ray = std::max(2.0, 1.25 * s->caps_per_ray);
   int64_t capacity = std::max<int64_t>(1 << 16, static_cast<int64_t>(per_ray * count * n_recv));
   DevBuf<Capture> caps;
-  const size_t smem = p.use_smem ? sizeof(TNode) * static_cast<size_t>(p.hdr.K) : 0;
+  const size_t smem = (!p.use_smem || variant == 0) ? 0
+                      : p.wide ? sizeof(QNode) * static_cast<size_t>(p.hdr.K4)
+                               : sizeof(TNode) * static_cast<size_t>(p.hdr.K);
+  // blocks per SM for the register budget (dev override RR_MINB)
+  static const int minb = [] {
+    const char* e = std::getenv("RR_MINB");
+    return e ? std::atoi(e) : 8;
+  }();
+  auto fast = minb >= 10 ? trace_kernel<1, 10> : minb >= 8 ? trace_kernel<1, 8>
+            : minb >= 6 ? trace_kernel<1, 6> : trace_kernel<1, 1>;
+  auto kernel = variant == 0 ? fast : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
-  if (occ_cache_smem != static_cast<int>(smem)) {
-    RR_CUDA(cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache_blocks, trace_kernel, 128, smem));
+  static thread_local const void* occ_cache_fn = nullptr;
+  if (occ_cache_smem != static_cast<int>(smem) || occ_cache_fn != reinterpret_cast<const void*>(kernel)) {
+    RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache_blocks, kernel, 128, smem));
     occ_cache_smem = static_cast<int>(smem);
+    occ_cache_fn = reinterpret_cast<const void*>(kernel);
   }
   const int blocks_per_sm = std::max(occ_cache_blocks, 1);
   const int64_t want = (count + 127) / 128;
@@ -392,7 +431,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     p.cap_capacity = capacity;
     RR_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * 8, st));
     RR_CUDA(cudaEventRecord(e0, st));
-    trace_kernel<<<grid, 128, smem, st>>>(p);
+    kernel<<<grid, 128, smem, st>>>(p);
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaEventRecord(e1, st));
     s->ctx->launches++;

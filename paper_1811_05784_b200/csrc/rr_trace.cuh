@@ -18,7 +18,10 @@ static_assert(sizeof(Capture) == 64, "capture record");
 
 struct TraceParams {
   const TNode* nodes;
+  const QNode* qnodes;
+  int32_t wide;  // 1: traverse the 4-wide QNodes, 0: the binary TNodes
   const FaceTri* tri;
+  const float4* tri32;
   const double* normal;
   TravHeader hdr;
   int32_t use_smem;
