@@ -333,6 +333,61 @@ __global__ void q_build_kernel(const RefNode* __restrict__ ref, const int32_t* _
   q[qidx[tidx[i]]] = out;
 }
 
+// ---- axis-aligned plane ids (coplanar-subtree culling, rr_geom.cuh).
+// A face is flat on axis k when its three vertices share coordinate k
+// exactly (a valid face has at most one such axis); a node is flat when its
+// box has zero extent on k, i.e. all its faces lie on one plane x_k = c.
+__device__ __forceinline__ int flat_axis(const double* lo, const double* hi) {
+  for (int k = 0; k < 3; ++k)
+    if (lo[k] == hi[k]) return k;
+  return -1;
+}
+
+__global__ void plane_key_kernel(const double* __restrict__ fb, int64_t nf, int axis,
+                                 unsigned long long* __restrict__ keys) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int k = flat_axis(fb + 6 * f, fb + 6 * f + 3);
+  keys[f] = k == axis ? ord_key(fb[6 * f + k]) : ~0ull;
+}
+
+__device__ __forceinline__ int32_t plane_lookup(const unsigned long long* __restrict__ table,
+                                                const int64_t* __restrict__ off, int k, double c) {
+  const unsigned long long key = ord_key(c);
+  int64_t lo = off[k], hi = off[k + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (table[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  if (lo < off[k + 1] && table[lo] == key) return static_cast<int32_t>((k << 29) | (lo - off[k]));
+  return -1;
+}
+
+__global__ void face_plane_kernel(const double* __restrict__ fb, int64_t nf,
+                                  const unsigned long long* __restrict__ table, const int64_t* __restrict__ off,
+                                  int32_t* __restrict__ face_plane) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int k = flat_axis(fb + 6 * f, fb + 6 * f + 3);
+  face_plane[f] = k < 0 ? -1 : plane_lookup(table, off, k, fb[6 * f + k]);
+}
+
+__global__ void node_plane_kernel(const RefNode* __restrict__ ref, const int32_t* __restrict__ tidx,
+                                  int64_t n_nodes, const unsigned long long* __restrict__ table,
+                                  const int64_t* __restrict__ off, TNode* __restrict__ tn) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes || ref[i].face >= 0) return;
+  int32_t pl[2];
+  const int32_t kids[2] = {ref[i].left, ref[i].right};
+  for (int s = 0; s < 2; ++s) {
+    const RefNode& c = ref[kids[s]];
+    const int k = flat_axis(c.lo, c.hi);
+    pl[s] = k < 0 ? -1 : plane_lookup(table, off, k, c.lo[k]);
+  }
+  tn[tidx[i]].d.z = pl[0];
+  tn[tidx[i]].d.w = pl[1];
+}
+
 __global__ void vert_bounds_kernel(const double* __restrict__ v, int64_t nv,
                                    unsigned long long* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -509,6 +564,53 @@ void build_scene_tree(rr_scene* s) {
     std::swap(perm, perm_o);
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
+  }
+
+  // ---- axis-aligned plane tables: per axis, the sorted unique plane
+  // coordinates of the flat faces; ids for faces and for tree children
+  {
+    DevBuf<unsigned long long> pkeys, psorted, table;
+    DevBuf<int64_t> doff;
+    DevBuf<int> dnum;
+    pkeys.alloc(nf, st);
+    psorted.alloc(nf, st);
+    table.alloc(3 * nf, st);
+    doff.alloc(4, st);
+    dnum.alloc(1, st);
+    int64_t hoff[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 3; ++k) {
+      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
+      RR_LAUNCH_CHECK();
+      size_t need = 0;
+      RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+      size_t need2 = 0;
+      RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf),
+                                        st));
+      if (std::max(need, need2) > tmp.n) tmp.alloc(std::max(need, need2), st);
+      size_t t = tmp.n;
+      RR_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+      t = tmp.n;
+      RR_CUDA(cub::DeviceSelect::Unique(tmp.p, t, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf), st));
+      int num = 0;
+      unsigned long long last = 0;
+      RR_CUDA(cudaMemcpyAsync(&num, dnum.p, sizeof num, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      if (num > 0)
+        RR_CUDA(cudaMemcpyAsync(&last, table.p + hoff[k] + num - 1, sizeof last, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      if (num > 0 && last == ~0ull) --num;  // the "not flat on k" sentinel
+      hoff[k + 1] = hoff[k] + num;
+      s->ctx->launches += 6;
+    }
+    RR_CUDA(cudaMemcpyAsync(doff.p, hoff, sizeof hoff, cudaMemcpyHostToDevice, st));
+    s->face_plane.alloc(nf, st);
+    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
+    RR_LAUNCH_CHECK();
+    node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, table.p, doff.p,
+                                                           s->tnodes.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 2;
+    RR_CUDA(cudaStreamSynchronize(st));  // hoff is a stack array
   }
 
   // ---- 4-wide collapse

@@ -157,9 +157,14 @@ struct HitResult {
   int32_t face;
 };
 
+// rplane: plane id of the face the ray leaves (or -2).  Children whose whole
+// subtree lies on that axis-aligned plane are skipped: a ray leaving the
+// plane with |d_axis| > 1e-6 meets it only at delta ~ 1e-14 / |d_axis|, which
+// the reference's fp64 test rejects (delta <= kSelfHitEpsilon), so the
+// closest hit is unchanged.
 __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNode* __restrict__ nodes,
                                                  const TNode* smem, int32_t K, const FaceTri* __restrict__ tri,
-                                                 D3 o, D3 d, int32_t* n_visit = nullptr) {
+                                                 D3 o, D3 d, int32_t* n_visit = nullptr, int32_t rplane = -2) {
   HitResult best{0.0, -1};
   RayF r;
   if (!make_rayf(h, o, d, r)) return best;
@@ -179,8 +184,10 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
     if (node >= 0 && node != kPop) {
       ++visits;
       const TNode nd = load_node(nodes, smem, node, K);
-      const float tl = box_enter(r, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y, tbest);
-      const float tr = box_enter(r, nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w, tbest);
+      float tl = box_enter(r, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y, tbest);
+      float tr = box_enter(r, nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w, tbest);
+      if (nd.d.z == rplane) tl = __int_as_float(0x7f800000);
+      if (nd.d.w == rplane) tr = __int_as_float(0x7f800000);
       const bool hl = tl != __int_as_float(0x7f800000), hr = tr != __int_as_float(0x7f800000);
       if (hl && hr) {
         const bool lf = tl <= tr;

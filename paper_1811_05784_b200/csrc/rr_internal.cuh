@@ -158,6 +158,7 @@ struct rr_scene {
   rr::DevBuf<float4> tri32;       // nf*3: fp32 a (w = face bits), b-a, c-a (48 B leaf record)
   rr::DevBuf<double> normal;      // nf*3
   rr::DevBuf<int32_t> mat;        // nf
+  rr::DevBuf<int32_t> face_plane; // nf: axis-aligned plane id (axis << 29 | index) or -1
   rr::DevBuf<rr::RefNode> ref;    // 2nf-1 (reference layout)
   rr::DevBuf<rr::TNode> tnodes;   // K + nf
   rr::DevBuf<rr::QNode> qnodes;   // 4-wide nodes

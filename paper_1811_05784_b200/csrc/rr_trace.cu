@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   bool exhausted = false;
   D3 o{}, d{};
   double path = 0.0;
-  int32_t steps = 0, bounces = 0;
+  int32_t steps = 0, bounces = 0, rplane = -2;
   unsigned long long st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
   int32_t st_max = 0;
 
@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
           path = 0.0;
           steps = 0;
           bounces = 0;
+          rplane = -2;
           if (p.max_iter <= 0) {  // trace() with a zero cap: nothing runs
             st_alive++;
             ray = -1;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 1) {
-      wall = closest_hit(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d);
+      wall = closest_hit(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
       wall = closest_hit4(p.hdr, p.qnodes, smem_q, K, p.tri, o, d);
     }
@@ -160,6 +161,15 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
       const double s2 = 2.0 * dot(d, n);
       d = d - s2 * n;  // reflect, tracer.hpp:33-37
       o = pt;
+      // the next segment leaves this face's plane: cull coplanar subtrees
+      const int32_t pid = __ldg(p.face_plane + wall.face);
+      if (pid >= 0) {
+        const int k = pid >> 29;
+        const double dk = k == 0 ? d.x : (k == 1 ? d.y : d.z);
+        rplane = fabs(dk) > 1e-6 ? pid : -2;
+      } else {
+        rplane = -2;
+      }
       path += wall.delta;
       p.hist[ray * p.H + bounces] = wall.face;
       ++bounces;
@@ -328,6 +338,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   const int variant = (cfg->flags & RR_TRACE_F32_LEAVES) ? 1 : (cfg->flags & RR_TRACE_WIDE) ? 2 : 0;
   p.wide = variant == 2 ? 1 : 0;
   p.tri32 = s->tri32.p;
+  p.face_plane = s->face_plane.p;
   p.tri = s->tri.p;
   p.normal = s->normal.p;
   p.hdr = s->hdr;

@@ -22,6 +22,7 @@ struct TraceParams {
   int32_t wide;  // 1: traverse the 4-wide QNodes, 0: the binary TNodes
   const FaceTri* tri;
   const float4* tri32;
+  const int32_t* face_plane;
   const double* normal;
   TravHeader hdr;
   int32_t use_smem;
