@@ -147,12 +147,26 @@ rr_status rr_trace(rr_scene* scene, const rr_source* source,
                    const rr_receiver* receivers, int32_t n_recv,
                    const rr_trace_config* config, rr_trace_result** out);
 rr_status rr_trace_stats_get(rr_trace_result* res, rr_trace_stats* stats);
-/* Captures sorted by (receiver, ray, path) (tracer.cpp:143-147).  Arrays:
+/* Captures sorted by (receiver, ray, path) (tracer.cpp:143-147).  Host or
+ * device destination pointers (UVA).  Arrays:
  * recv/ray n, point/dir n*3, path n, mult n*8, hist_off n+1, hist
  * total_history.  Any pointer may be NULL to skip that field. */
 rr_status rr_trace_captures(rr_trace_result* res, int32_t* recv, int32_t* ray,
                             double* point, double* dir, double* path,
                             double* mult, int64_t* hist_off, int32_t* hist);
+/* Import caller-held capture records (host or device pointers, UVA) as a
+ * trace result, e.g. the captures an owner rank received in the multi-GPU
+ * exchange, or the std::vector<Capture> argument of build_image_sources
+ * (image_sources.hpp:58-61).  Records are re-sorted into the reference order
+ * (receiver, ray, path) (tracer.cpp:143-147).  recv may be NULL (all 0);
+ * mult may be NULL (rebuilt from the face history as the ordered product of
+ * 1 - alpha, tracer.cpp:57-58).  hist_off has n+1 entries starting at 0. */
+rr_status rr_captures_import(rr_scene* scene, int64_t n, const int32_t* recv,
+                             const int32_t* ray, const double* point,
+                             const double* dir, const double* path,
+                             const double* mult, const int64_t* hist_off,
+                             const int32_t* hist, const rr_receiver* receivers,
+                             int32_t n_recv, rr_trace_result** out);
 /* Device time of the trace kernel itself (ms, CUDA events). */
 double rr_trace_kernel_ms(rr_trace_result* res);
 rr_status rr_trace_destroy(rr_trace_result* res);
@@ -196,6 +210,13 @@ rr_status rr_ir_bin_device(rr_ctx* ctx, int64_t n, const double* d_dist,
 rr_status rr_ir_filter_device(rr_ctx* ctx, const double* d_hist, double fs,
                               int32_t taps, int64_t length, double* d_band_ir,
                               double* d_broadband);
+/* synthesize (rir.hpp:45) from explicit pulse trains (PulseTrains,
+ * rir.hpp:12-23): band b owns events [band_off[b], band_off[b+1]) of
+ * time (s) and amplitude; band_off has 9 entries.  Host buffers. */
+rr_status rr_synthesize_trains(rr_ctx* ctx, const int64_t* band_off,
+                               const double* time, const double* amplitude,
+                               double fs, int32_t taps, int64_t length,
+                               double* band_ir, double* broadband);
 /* Length of the reference's response (rir.cpp:78-80): llround(t_last*fs) +
  * (taps-1)/2 + 1, or 0 without events. */
 rr_status rr_ir_reference_length(int64_t n, const double* dist, double c,

@@ -1,0 +1,530 @@
+// roomray_b200.hpp — header-only C++ facade over the C ABI (roomray_b200.h).
+//
+// Re-exposes the reference's C++ API for the ray-propagation path
+// (namespace roomray, /root/reference/proj/include/roomray) with the same
+// names, argument meaning and exceptions, on Eigen-free value types, so a
+// caller such as run_trace_pipeline (pipeline.cpp:154-175) can switch by
+// changing the namespace.  All compute runs on the GPU through
+// libroomray_b200.so; there is no CPU path.  Link: -lroomray_b200.
+//
+// Differences from the reference, all outside the hot path:
+//  * Vec3 is {x, y, z} with operator[]; BandArray is std::array<double, 8>.
+//  * AccelTree holds the device scene; its reference-layout node table is
+//    downloaded on first use through nodes() (a method, not a field).
+//  * Hit carries delta, point and face_index (lambda / mu are not reported).
+//  * RoomImpulseResponse additionally holds the 8 per-band responses.
+//  * step() (tracer.hpp:43-45, used by the reference's bench) is not
+//    provided: the persistent kernel traces each ray to completion.
+#ifndef ROOMRAY_B200_HPP
+#define ROOMRAY_B200_HPP
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "roomray_b200.h"
+
+namespace roomray_b200 {
+
+inline constexpr int kNumBands = RR_NUM_BANDS;                       // types.hpp:15
+inline constexpr std::array<double, kNumBands> kBandCentersHz = {   // types.hpp:20-21
+    62.5, 125.0, 250.0, 500.0, 1000.0, 2000.0, 4000.0, 8000.0};
+inline constexpr double kSelfHitEpsilon = 1e-6;                       // types.hpp:31
+inline constexpr int kBandFilterTaps = 1023;                          // rir.hpp:40
+inline constexpr int kBandFilterDelay = (kBandFilterTaps - 1) / 2;    // rir.hpp:41
+
+struct Vec3 {
+  double x = 0.0, y = 0.0, z = 0.0;
+  double operator[](int i) const { return i == 0 ? x : (i == 1 ? y : z); }
+  double& operator[](int i) { return i == 0 ? x : (i == 1 ? y : z); }
+  bool operator==(const Vec3& o) const { return x == o.x && y == o.y && z == o.z; }
+};
+using BandArray = std::array<double, kNumBands>;
+
+inline BandArray band_ones() {
+  BandArray a;
+  a.fill(1.0);
+  return a;
+}
+
+// ------------------------------------------------------------------ errors
+namespace detail {
+inline void check(rr_status s) {
+  if (s == RR_OK) return;
+  const std::string msg = rr_last_error();
+  if (s == RR_INVALID_ARGUMENT) throw std::invalid_argument(msg);  // as the reference
+  throw std::runtime_error("roomray_b200: " + msg);
+}
+}  // namespace detail
+
+// ------------------------------------------------------------------ device
+/// One GPU and its stream (rr_ctx).  A process-wide instance per device is
+/// created on first use; a context is not thread-safe.
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    rr_ctx* c = nullptr;
+    detail::check(rr_ctx_create(device, &c));
+    ctx_.reset(c, [](rr_ctx* p) { rr_ctx_destroy(p); });
+  }
+  static Device& get(int device = 0) {
+    static std::vector<std::unique_ptr<Device>> devs;
+    if (device < 0) throw std::invalid_argument("device index must be >= 0");
+    if (static_cast<int>(devs.size()) <= device) devs.resize(device + 1);
+    if (!devs[device]) devs[device] = std::make_unique<Device>(device);
+    return *devs[device];
+  }
+  rr_ctx* handle() const { return ctx_.get(); }
+  int64_t launches() const { return rr_ctx_launches(ctx_.get()); }
+
+ private:
+  std::shared_ptr<rr_ctx> ctx_;
+};
+
+// ------------------------------------------------------------------ geometry (geometry.hpp)
+struct Material {
+  std::string name;
+  BandArray absorption{};
+};
+
+struct Triangle {
+  int a = 0, b = 0, c = 0;
+  int material_id = 0;
+};
+
+struct Aabb {
+  Vec3 min, max;
+  double diagonal() const {
+    const double dx = max.x - min.x, dy = max.y - min.y, dz = max.z - min.z;
+    return std::sqrt((dx * dx + dy * dy) + dz * dz);
+  }
+};
+
+struct Hit {
+  double delta = 0.0;
+  Vec3 point;
+  int face_index = -1;
+};
+
+struct TriangleMesh {
+  std::vector<Vec3> vertices;
+  std::vector<Triangle> faces;
+  std::vector<Material> materials;
+  std::size_t face_count() const { return faces.size(); }
+};
+
+// ------------------------------------------------------------------ tree (accel_tree.hpp)
+struct TreeNode {
+  Aabb box;
+  std::int32_t left = -1;
+  std::int32_t right = -1;
+  std::int32_t face_index = -1;
+  bool is_leaf() const { return face_index >= 0; }
+};
+
+/// Device scene + median-split tree, built on the GPU by build_tree.
+class AccelTree {
+ public:
+  std::int32_t root = -1;
+  std::size_t node_count() const { return static_cast<std::size_t>(n_nodes_); }
+  int depth() const { return depth_; }
+  std::size_t leaf_count() const {
+    std::size_t n = 0;
+    for (const TreeNode& t : nodes()) n += t.is_leaf() ? 1 : 0;
+    return n;
+  }
+  /// Reference-layout nodes (post-order, root last), downloaded once.
+  const std::vector<TreeNode>& nodes() const {
+    if (nodes_.empty() && n_nodes_ > 0) {
+      std::vector<rr_tree_node> raw(static_cast<std::size_t>(n_nodes_));
+      detail::check(rr_scene_tree(scene_.get(), raw.data()));
+      nodes_.resize(raw.size());
+      for (std::size_t i = 0; i < raw.size(); ++i) {
+        TreeNode& t = nodes_[i];
+        t.box.min = {raw[i].lo[0], raw[i].lo[1], raw[i].lo[2]};
+        t.box.max = {raw[i].hi[0], raw[i].hi[1], raw[i].hi[2]};
+        t.left = raw[i].left;
+        t.right = raw[i].right;
+        t.face_index = raw[i].face_index;
+      }
+    }
+    return nodes_;
+  }
+  rr_scene* handle() const { return scene_.get(); }
+  const Aabb& bounds() const { return bounds_; }
+  double build_ms() const { return rr_scene_build_ms(scene_.get()); }
+
+ private:
+  friend AccelTree build_tree(const TriangleMesh&, int);
+  std::shared_ptr<rr_scene> scene_;
+  int64_t n_nodes_ = 0;
+  int depth_ = 0;
+  Aabb bounds_;
+  mutable std::vector<TreeNode> nodes_;
+};
+
+/// build_tree (accel_tree.hpp:38): uploads the mesh, validates it and builds
+/// the reference's median-split tree on the device.  Empty mesh, bad indices
+/// or degenerate faces throw std::invalid_argument.
+inline AccelTree build_tree(const TriangleMesh& mesh, int device = 0) {
+  Device& dev = Device::get(device);
+  std::vector<double> v(3 * mesh.vertices.size());
+  Aabb box;
+  box.min = {HUGE_VAL, HUGE_VAL, HUGE_VAL};
+  box.max = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+  for (std::size_t i = 0; i < mesh.vertices.size(); ++i) {
+    for (int k = 0; k < 3; ++k) {
+      v[3 * i + k] = mesh.vertices[i][k];
+      box.min[k] = std::min(box.min[k], mesh.vertices[i][k]);
+      box.max[k] = std::max(box.max[k], mesh.vertices[i][k]);
+    }
+  }
+  std::vector<int32_t> f(4 * mesh.faces.size());
+  for (std::size_t i = 0; i < mesh.faces.size(); ++i) {
+    f[4 * i] = mesh.faces[i].a;
+    f[4 * i + 1] = mesh.faces[i].b;
+    f[4 * i + 2] = mesh.faces[i].c;
+    f[4 * i + 3] = mesh.faces[i].material_id;
+  }
+  std::vector<double> alpha(kNumBands * std::max<std::size_t>(mesh.materials.size(), 1), 0.0);
+  for (std::size_t m = 0; m < mesh.materials.size(); ++m)
+    for (int b = 0; b < kNumBands; ++b) alpha[kNumBands * m + b] = mesh.materials[m].absorption[b];
+  rr_scene* s = nullptr;
+  detail::check(rr_scene_create(dev.handle(), v.data(), static_cast<int64_t>(mesh.vertices.size()), f.data(),
+                                static_cast<int64_t>(mesh.faces.size()), alpha.data(),
+                                static_cast<int32_t>(std::max<std::size_t>(mesh.materials.size(), 1)), 1, &s));
+  AccelTree t;
+  t.scene_.reset(s, [](rr_scene* p) { rr_scene_destroy(p); });
+  int32_t root = -1, depth = 0;
+  detail::check(rr_scene_tree_info(s, &t.n_nodes_, &root, &depth));
+  t.root = root;
+  t.depth_ = depth;
+  t.bounds_ = box;
+  return t;
+}
+
+/// Batched nearest_hit: one optional Hit per (origin, dir) pair.
+inline std::vector<std::optional<Hit>> nearest_hit_batch(const AccelTree& tree, const std::vector<Vec3>& origins,
+                                                         const std::vector<Vec3>& dirs, bool brute = false) {
+  if (origins.size() != dirs.size()) throw std::invalid_argument("origins and dirs differ in length");
+  const std::size_t n = origins.size();
+  std::vector<double> o(3 * n), d(3 * n), delta(n), point(3 * n);
+  std::vector<int32_t> face(n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      o[3 * i + k] = origins[i][k];
+      d[3 * i + k] = dirs[i][k];
+    }
+  detail::check(rr_nearest_hit_batch(tree.handle(), o.data(), d.data(), static_cast<int64_t>(n), brute ? 1 : 0,
+                                     face.data(), delta.data(), point.data()));
+  std::vector<std::optional<Hit>> out(n);
+  for (std::size_t i = 0; i < n; ++i)
+    if (face[i] >= 0) out[i] = Hit{delta[i], {point[3 * i], point[3 * i + 1], point[3 * i + 2]}, face[i]};
+  return out;
+}
+
+/// nearest_hit (accel_tree.hpp:50-51).  `mesh` must be the mesh the tree
+/// was built from (the tree holds its device copy).
+inline std::optional<Hit> nearest_hit(const AccelTree& tree, const TriangleMesh& /*mesh*/, const Vec3& origin,
+                                      const Vec3& dir) {
+  return nearest_hit_batch(tree, {origin}, {dir}, false)[0];
+}
+
+/// nearest_hit_brute (accel_tree.hpp:54-55) over the tree's device mesh.
+inline std::optional<Hit> nearest_hit_brute(const AccelTree& tree, const Vec3& origin, const Vec3& dir) {
+  return nearest_hit_batch(tree, {origin}, {dir}, true)[0];
+}
+
+/// nearest_hit_brute with the reference signature: uploads `mesh` first.
+inline std::optional<Hit> nearest_hit_brute(const TriangleMesh& mesh, const Vec3& origin, const Vec3& dir) {
+  return nearest_hit_brute(build_tree(mesh), origin, dir);
+}
+
+// ------------------------------------------------------------------ tracer (tracer.hpp, tracer_types.hpp, emission.hpp)
+struct SourceConfig {
+  Vec3 position;
+  int ray_count = 1;
+  BandArray initial_energy = band_ones();  // ignored by emit, as in the reference
+};
+
+struct Receiver {
+  Vec3 center;
+  double radius = 0.1;
+};
+
+struct TraceConfig {
+  int max_iterations = 1000;
+  double speed_of_sound = 343.0;
+  double max_range = 0.0;  // <= 0: (r/2)*sqrt(N)
+  int thread_count = 1;    // accepted for compatibility; the GPU grid replaces it
+  double resolved_max_range(const Receiver& receiver, int ray_count) const {
+    if (max_range > 0.0) return max_range;  // tracer.cpp:10-15
+    return 0.5 * receiver.radius * std::sqrt(static_cast<double>(ray_count));
+  }
+};
+
+struct Capture {
+  int ray_index = -1;
+  Vec3 point;
+  Vec3 incoming_dir{0.0, 0.0, 1.0};
+  double path_length = 0.0;
+  BandArray band_multiplier = band_ones();
+  std::vector<int> face_history;
+};
+
+struct TraceResult {
+  std::vector<Capture> captures;  // sorted by (ray index, path length)
+  int iterations = 0;
+  bool truncated = false;
+  std::size_t escaped = 0;
+  std::size_t out_of_range = 0;
+  double max_range = 0.0;
+  int64_t ray_bounces = 0;  // nearest-hit queries executed (extension)
+  double kernel_ms = 0.0;   // device time of the trace kernel (extension)
+};
+
+/// Specular mirror bounce u - 2(u.n)n (tracer.hpp:33-37).
+inline Vec3 reflect(const Vec3& u, const Vec3& n) {
+  const double s = 2.0 * ((u.x * n.x + u.y * n.y) + u.z * n.z);
+  return {u.x - s * n.x, u.y - s * n.y, u.z - s * n.z};
+}
+
+namespace detail {
+struct TraceHandle {
+  rr_trace_result* h = nullptr;
+  explicit TraceHandle(rr_trace_result* p) : h(p) {}
+  ~TraceHandle() {
+    if (h) rr_trace_destroy(h);
+  }
+  TraceHandle(const TraceHandle&) = delete;
+  TraceHandle& operator=(const TraceHandle&) = delete;
+};
+}  // namespace detail
+
+/// trace (tracer.hpp:50-52): the whole Fibonacci lattice on the GPU.
+inline TraceResult trace(const TriangleMesh& /*mesh*/, const AccelTree& tree, const SourceConfig& source,
+                         const Receiver& receiver, const TraceConfig& config) {
+  rr_source src{{source.position.x, source.position.y, source.position.z}, source.ray_count};
+  rr_receiver rc{{receiver.center.x, receiver.center.y, receiver.center.z}, receiver.radius};
+  rr_trace_config cfg{};
+  cfg.max_iterations = config.max_iterations;
+  cfg.speed_of_sound = config.speed_of_sound;
+  cfg.max_range = config.max_range;
+  rr_trace_result* h = nullptr;
+  detail::check(rr_trace(tree.handle(), &src, &rc, 1, &cfg, &h));
+  detail::TraceHandle guard(h);
+  rr_trace_stats st{};
+  detail::check(rr_trace_stats_get(h, &st));
+  const std::size_t n = static_cast<std::size_t>(st.n_captures);
+  std::vector<int32_t> ray(n), hist(std::max<int64_t>(st.total_history, 1));
+  std::vector<double> point(3 * n), dir(3 * n), path(n), mult(kNumBands * n);
+  std::vector<int64_t> off(n + 1);
+  detail::check(rr_trace_captures(h, nullptr, ray.data(), point.data(), dir.data(), path.data(), mult.data(),
+                                  off.data(), hist.data()));
+  TraceResult r;
+  r.iterations = st.iterations;
+  r.truncated = st.truncated != 0;
+  r.escaped = static_cast<std::size_t>(st.escaped);
+  r.out_of_range = static_cast<std::size_t>(st.out_of_range);
+  r.max_range = st.max_range;
+  r.ray_bounces = st.ray_bounces;
+  r.kernel_ms = rr_trace_kernel_ms(h);
+  r.captures.resize(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    Capture& c = r.captures[i];
+    c.ray_index = ray[i];
+    c.point = {point[3 * i], point[3 * i + 1], point[3 * i + 2]};
+    c.incoming_dir = {dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]};
+    c.path_length = path[i];
+    for (int b = 0; b < kNumBands; ++b) c.band_multiplier[b] = mult[kNumBands * i + b];
+    c.face_history.assign(hist.begin() + off[i], hist.begin() + off[i + 1]);
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------ air (air_absorption.hpp)
+struct AirModel {
+  double temperature_c = 20.0;
+  double relative_humidity = 50.0;
+  double pressure_kpa = 101.325;
+  bool enabled = true;
+};
+
+/// air_beta_bands (air_absorption.hpp:35): energy attenuation per metre.
+inline BandArray air_beta_bands(const AirModel& air) {
+  rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
+  BandArray out{};
+  detail::check(rr_air_beta_bands(&a, out.data()));
+  return out;
+}
+
+// ------------------------------------------------------------------ image sources (image_sources.hpp)
+struct ImageSource {
+  Vec3 position;
+  double distance = 0.0;
+  BandArray band_energy{};
+  BandArray band_multiplier = band_ones();
+  int ray_count = 0;
+  int order = 0;
+  std::vector<int> face_path;
+  std::optional<Vec3> projection;
+};
+
+struct ClusterOptions {
+  double tol_scale = 1e-6;
+  bool merge_coplanar = false;
+};
+
+/// retro_propagate (image_sources.hpp:34): point - path * dir.
+inline Vec3 retro_propagate(const Capture& c) {
+  return {c.point.x - c.path_length * c.incoming_dir.x, c.point.y - c.path_length * c.incoming_dir.y,
+          c.point.z - c.path_length * c.incoming_dir.z};
+}
+
+/// build_image_sources (image_sources.hpp:58-61): cluster + attach_energy +
+/// project on the GPU, sorted by (order, distance, face path).
+inline std::vector<ImageSource> build_image_sources(const std::vector<Capture>& captures, int total_rays,
+                                                    const AirModel& air, const Vec3& receiver_center,
+                                                    const TriangleMesh& /*mesh*/, const AccelTree& tree,
+                                                    const ClusterOptions& options = {}) {
+  const std::size_t n = captures.size();
+  std::vector<int32_t> ray(n), hist;
+  std::vector<double> point(3 * n), dir(3 * n), path(n), mult(kNumBands * n);
+  std::vector<int64_t> off(n + 1, 0);
+  for (std::size_t i = 0; i < n; ++i) {
+    const Capture& c = captures[i];
+    ray[i] = c.ray_index;
+    for (int k = 0; k < 3; ++k) {
+      point[3 * i + k] = c.point[k];
+      dir[3 * i + k] = c.incoming_dir[k];
+    }
+    path[i] = c.path_length;
+    for (int b = 0; b < kNumBands; ++b) mult[kNumBands * i + b] = c.band_multiplier[b];
+    hist.insert(hist.end(), c.face_history.begin(), c.face_history.end());
+    off[i + 1] = static_cast<int64_t>(hist.size());
+  }
+  if (hist.empty()) hist.push_back(0);
+  rr_receiver rc{{receiver_center.x, receiver_center.y, receiver_center.z}, 1.0};
+  rr_trace_result* h = nullptr;
+  detail::check(rr_captures_import(tree.handle(), static_cast<int64_t>(n), nullptr, ray.data(), point.data(),
+                                   dir.data(), path.data(), mult.data(), off.data(), hist.data(), &rc, 1, &h));
+  detail::TraceHandle guard(h);
+  rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
+  rr_cluster_options o{options.tol_scale, options.merge_coplanar ? 1 : 0};
+  rr_images* im = nullptr;
+  detail::check(rr_build_image_sources(h, 0, total_rays, &a, &o, &im));
+  std::unique_ptr<rr_images, void (*)(rr_images*)> img(im, [](rr_images* p) { rr_images_destroy(p); });
+  int64_t ni = 0, tp = 0;
+  detail::check(rr_images_info(im, &ni, &tp));
+  const std::size_t m = static_cast<std::size_t>(ni);
+  std::vector<double> pos(3 * m), dist(m), en(kNumBands * m), mu(kNumBands * m), proj(3 * m);
+  std::vector<int32_t> cnt(m), order(m), hp(m), pth(std::max<int64_t>(tp, 1));
+  std::vector<int64_t> poff(m + 1);
+  detail::check(rr_images_get(im, pos.data(), dist.data(), en.data(), mu.data(), cnt.data(), order.data(), hp.data(),
+                              proj.data(), poff.data(), pth.data()));
+  std::vector<ImageSource> out(m);
+  for (std::size_t i = 0; i < m; ++i) {
+    ImageSource& s = out[i];
+    s.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    s.distance = dist[i];
+    for (int b = 0; b < kNumBands; ++b) {
+      s.band_energy[b] = en[kNumBands * i + b];
+      s.band_multiplier[b] = mu[kNumBands * i + b];
+    }
+    s.ray_count = cnt[i];
+    s.order = order[i];
+    s.face_path.assign(pth.begin() + poff[i], pth.begin() + poff[i + 1]);
+    if (hp[i]) s.projection = Vec3{proj[3 * i], proj[3 * i + 1], proj[3 * i + 2]};
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ RIR (rir.hpp)
+struct PulseEvent {
+  double time_s = 0.0;
+  double amplitude = 0.0;
+};
+
+struct BandPulseTrain {
+  int band = 0;
+  std::vector<PulseEvent> events;
+};
+
+using PulseTrains = std::array<BandPulseTrain, kNumBands>;
+
+struct RoomImpulseResponse {
+  double sample_rate = 44100.0;
+  std::vector<double> samples;                           // broadband
+  PulseTrains band_trains;
+  std::array<std::vector<double>, kNumBands> band_samples;  // per-band responses (extension)
+};
+
+/// build_pulse_trains (rir.cpp:9-30): one event per image per band at
+/// t = d / c with amplitude sqrt(E), each train sorted by (time, amplitude).
+inline PulseTrains build_pulse_trains(const std::vector<ImageSource>& images, double speed_of_sound) {
+  if (speed_of_sound <= 0.0) throw std::invalid_argument("speed of sound must be > 0");
+  PulseTrains trains;
+  for (int b = 0; b < kNumBands; ++b) {
+    trains[b].band = b;
+    trains[b].events.reserve(images.size());
+  }
+  for (const ImageSource& im : images) {
+    const double t = im.distance / speed_of_sound;
+    for (int b = 0; b < kNumBands; ++b) trains[b].events.push_back({t, std::sqrt(im.band_energy[b])});
+  }
+  for (auto& tr : trains)
+    std::sort(tr.events.begin(), tr.events.end(), [](const PulseEvent& a, const PulseEvent& b) {
+      if (a.time_s != b.time_s) return a.time_s < b.time_s;
+      return a.amplitude < b.amplitude;
+    });
+  return trains;
+}
+
+/// design_band_filter (rir.cpp:32-58), `taps` taps (reference: 1023).
+inline std::vector<double> design_band_filter(int band, double sample_rate, int taps = kBandFilterTaps) {
+  std::vector<double> k(static_cast<std::size_t>(std::max(taps, 0)));
+  detail::check(rr_band_filter(band, sample_rate, taps, k.data()));
+  return k;
+}
+
+/// synthesize (rir.cpp:60-96) on the GPU: pulse histograms at
+/// lround(t*fs), 8 FIR band filters, broadband sum; length
+/// llround(t_last*fs) + delay + 1 as in the reference.
+inline RoomImpulseResponse synthesize(const PulseTrains& trains, double sample_rate, int taps = kBandFilterTaps) {
+  RoomImpulseResponse rir;
+  rir.sample_rate = sample_rate;
+  rir.band_trains = trains;
+  std::vector<int64_t> off(kNumBands + 1, 0);
+  std::vector<double> t, a;
+  double last = 0.0;
+  bool any = false;
+  for (int b = 0; b < kNumBands; ++b) {
+    for (const PulseEvent& e : trains[b].events) {
+      if (e.time_s < 0.0) throw std::invalid_argument("pulse events cannot precede t = 0");
+      t.push_back(e.time_s);
+      a.push_back(e.amplitude);
+      last = std::max(last, e.time_s);
+      any = true;
+    }
+    off[b + 1] = static_cast<int64_t>(t.size());
+  }
+  if (!any) return rir;
+  const int64_t length = static_cast<int64_t>(std::llround(last * sample_rate)) + (taps - 1) / 2 + 1;
+  std::vector<double> band(static_cast<std::size_t>(kNumBands * length));
+  rir.samples.assign(static_cast<std::size_t>(length), 0.0);
+  detail::check(rr_synthesize_trains(Device::get(0).handle(), off.data(), t.data(), a.data(), sample_rate, taps,
+                                     length, band.data(), rir.samples.data()));
+  for (int b = 0; b < kNumBands; ++b)
+    rir.band_samples[b].assign(band.begin() + b * length, band.begin() + (b + 1) * length);
+  return rir;
+}
+
+}  // namespace roomray_b200
+
+#endif  // ROOMRAY_B200_HPP

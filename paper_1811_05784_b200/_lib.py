@@ -81,6 +81,8 @@ SIGNATURES = [
                            C.POINTER(_vp)]),
     ("rr_trace_stats_get", C.c_int, [_vp, C.POINTER(TraceStats)]),
     ("rr_trace_captures", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("rr_captures_import", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(Receiver), _i32,
+                                     C.POINTER(_vp)]),
     ("rr_trace_kernel_ms", _d, [_vp]),
     ("rr_trace_destroy", C.c_int, [_vp]),
     ("rr_build_image_sources", C.c_int, [_vp, _i32, _i64, C.POINTER(Air), C.POINTER(ClusterOptions),
@@ -93,6 +95,7 @@ SIGNATURES = [
     ("rr_synthesize", C.c_int, [_vp, _i64, _f64p, _f64p, _d, _d, _i32, _i64, _vp, _vp]),
     ("rr_ir_bin_device", C.c_int, [_vp, _i64, _vp, _vp, _d, _d, _i64, _vp]),
     ("rr_ir_filter_device", C.c_int, [_vp, _vp, _d, _i32, _i64, _vp, _vp]),
+    ("rr_synthesize_trains", C.c_int, [_vp, _i64p, _vp, _vp, _d, _i32, _i64, _vp, _vp]),
     ("rr_ir_reference_length", C.c_int, [_i64, _f64p, _d, _d, _i32, C.POINTER(_i64)]),
     ("rr_band_filter", C.c_int, [_i32, _d, _i32, _f64p]),
 ]

@@ -122,13 +122,29 @@ rr_status rr_ctx_create(int device, rr_ctx** out) {
   });
 }
 
+namespace {
+void ctx_release(rr_ctx* ctx) {
+  if (--ctx->refs > 0) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void scene_release(rr_scene* scene) {
+  if (--scene->refs > 0) return;
+  rr_ctx* ctx = scene->ctx;
+  cudaSetDevice(ctx->device);
+  delete scene;
+  cudaStreamSynchronize(ctx->stream);
+  ctx_release(ctx);
+}
+}  // namespace
+
 rr_status rr_ctx_destroy(rr_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    ctx_release(ctx);
   });
 }
 
@@ -197,6 +213,7 @@ rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv, const in
     ctx->launches++;
     rr::build_scene_tree(s.get());
     RR_CUDA(cudaStreamSynchronize(st));
+    ctx->refs++;  // the scene holds its context
     *out = s.release();
   });
 }
@@ -204,10 +221,7 @@ rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv, const in
 rr_status rr_scene_destroy(rr_scene* scene) {
   return guarded([&] {
     if (!scene) return;
-    cudaSetDevice(scene->ctx->device);
-    cudaStream_t st = scene->ctx->stream;
-    delete scene;
-    cudaStreamSynchronize(st);
+    scene_release(scene);
   });
 }
 
@@ -282,6 +296,7 @@ rr_status rr_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, i
     check_ptr(out, "out");
     RR_CUDA(cudaSetDevice(s->ctx->device));
     *out = rr::run_trace(s, src, recv, n_recv, cfg, nullptr);
+    (*out)->scene->refs++;
   });
 }
 
@@ -301,7 +316,7 @@ rr_status rr_trace_captures(rr_trace_result* r, int32_t* recv, int32_t* ray, dou
     cudaStream_t st = r->scene->ctx->stream;
     const int64_t n = r->stats.n_captures;
     auto cp = [&](void* dst, const void* src, size_t bytes) {
-      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
     };
     if (n > 0) {
       cp(recv, r->c_recv.p, sizeof(int32_t) * n);
@@ -319,13 +334,35 @@ rr_status rr_trace_captures(rr_trace_result* r, int32_t* recv, int32_t* ray, dou
 
 double rr_trace_kernel_ms(rr_trace_result* r) { return r ? r->kernel_ms : -1.0; }
 
+rr_status rr_captures_import(rr_scene* scene, int64_t n, const int32_t* recv, const int32_t* ray, const double* point,
+                             const double* dir, const double* path, const double* mult, const int64_t* hist_off,
+                             const int32_t* hist, const rr_receiver* receivers, int32_t n_recv,
+                             rr_trace_result** out) {
+  return guarded([&] {
+    check_ptr(scene, "scene");
+    check_ptr(receivers, "receivers");
+    check_ptr(out, "out");
+    if (n > 0) {
+      check_ptr(ray, "ray");
+      check_ptr(point, "point");
+      check_ptr(dir, "dir");
+      check_ptr(path, "path");
+      check_ptr(hist_off, "hist_off");
+    }
+    RR_CUDA(cudaSetDevice(scene->ctx->device));
+    *out = rr::import_captures(scene, n, recv, ray, point, dir, path, mult, hist_off, hist, receivers, n_recv);
+    (*out)->scene->refs++;
+  });
+}
+
 rr_status rr_trace_destroy(rr_trace_result* r) {
   return guarded([&] {
     if (!r) return;
-    cudaSetDevice(r->scene->ctx->device);
-    cudaStream_t st = r->scene->ctx->stream;
+    rr_scene* sc = r->scene;
+    cudaSetDevice(sc->ctx->device);
     delete r;
-    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(sc->ctx->stream);
+    scene_release(sc);
   });
 }
 
@@ -338,6 +375,8 @@ void ir_bin(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy
 void ir_filter(rr_ctx* ctx, const double* d_hist, int64_t lh, double fs, int taps, int64_t L, double* d_band_ir,
                double* d_broadband);
 void band_filter_host(int band, double fs, int taps, double* out, rr_ctx* ctx);
+void ir_bin_events(rr_ctx* ctx, const int64_t* d_off, int64_t n, const double* d_time, const double* d_amp, double fs,
+                   int64_t lh, double* d_hist);
 void air_beta_bands(const rr_air& a, double* beta);
 }  // namespace rr
 
@@ -429,6 +468,48 @@ rr_status rr_synthesize(rr_ctx* ctx, int64_t n, const double* dist, const double
   });
 }
 
+rr_status rr_synthesize_trains(rr_ctx* ctx, const int64_t* band_off, const double* time, const double* amplitude,
+                               double fs, int32_t taps, int64_t length, double* band_ir, double* broadband) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(band_off, "band_off");
+    if (band_off[0] != 0) rr::invalid("band_off[0] must be 0");
+    for (int b = 0; b < rr::kBands; ++b)
+      if (band_off[b + 1] < band_off[b]) rr::invalid("band_off must be non-decreasing");
+    const int64_t n = band_off[rr::kBands];
+    if (n > 0) {
+      check_ptr(time, "time");
+      check_ptr(amplitude, "amplitude");
+      for (int64_t i = 0; i < n; ++i)
+        if (!(time[i] >= 0.0)) rr::invalid("pulse events cannot precede t = 0");  // rir.cpp:69-71
+    }
+    if (taps < 3) rr::invalid("taps must be >= 3");
+    if (fs < 2.0 * 8000.0 * std::sqrt(2.0)) rr::invalid("sample rate too low for the top band edge");
+    if (length <= 0) rr::invalid("length must be > 0");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t lh = length + taps;
+    rr::DevBuf<int64_t> doff;
+    rr::DevBuf<double> dt, da, hist, bands, bb;
+    doff.alloc(rr::kBands + 1, st);
+    dt.alloc(std::max<int64_t>(n, 1), st);
+    da.alloc(std::max<int64_t>(n, 1), st);
+    RR_CUDA(cudaMemcpyAsync(doff.p, band_off, sizeof(int64_t) * (rr::kBands + 1), cudaMemcpyHostToDevice, st));
+    if (n > 0) {
+      RR_CUDA(cudaMemcpyAsync(dt.p, time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      RR_CUDA(cudaMemcpyAsync(da.p, amplitude, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    }
+    hist.alloc(rr::kBands * lh, st);
+    bands.alloc(rr::kBands * length, st);
+    bb.alloc(length, st);
+    rr::ir_bin_events(ctx, doff.p, n, dt.p, da.p, fs, lh, hist.p);
+    rr::ir_filter(ctx, hist.p, lh, fs, taps, length, bands.p, bb.p);
+    if (band_ir) RR_CUDA(cudaMemcpyAsync(band_ir, bands.p, bands.bytes(), cudaMemcpyDeviceToHost, st));
+    if (broadband) RR_CUDA(cudaMemcpyAsync(broadband, bb.p, bb.bytes(), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 // Response length of the reference's synthesize (rir.cpp:78-80):
 // llround(t_last*fs) + (taps-1)/2 + 1, 0 for no events.
 rr_status rr_ir_reference_length(int64_t n, const double* dist, double c, double fs, int32_t taps,
@@ -461,6 +542,7 @@ rr_status rr_build_image_sources(rr_trace_result* tr, int32_t recv, int64_t tota
     if (opt) o = *opt;
     RR_CUDA(cudaSetDevice(tr->scene->ctx->device));
     *out = rr::build_image_sources(tr, recv, total_rays, *air, o);
+    (*out)->scene->refs++;
   });
 }
 
@@ -480,7 +562,7 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist, double* energy
     cudaStream_t st = im->scene->ctx->stream;
     const int64_t n = im->n;
     auto cp = [&](void* dst, const void* src, size_t bytes) {
-      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
     };
     cp(pos, im->pos.p, sizeof(double) * 3 * n);
     cp(dist, im->dist.p, sizeof(double) * n);
@@ -499,10 +581,11 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist, double* energy
 rr_status rr_images_destroy(rr_images* im) {
   return guarded([&] {
     if (!im) return;
-    cudaSetDevice(im->scene->ctx->device);
-    cudaStream_t st = im->scene->ctx->stream;
+    rr_scene* sc = im->scene;
+    cudaSetDevice(sc->ctx->device);
     delete im;
-    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(sc->ctx->stream);
+    scene_release(sc);
   });
 }
 

@@ -140,7 +140,11 @@ struct __align__(16) FaceTri {
 
 }  // namespace rr
 
+// Handles are reference counted: a scene holds its context, a trace result
+// or image set holds its scene, so destroying handles in any order (e.g. a
+// garbage collector's) never frees memory still reachable from a live one.
 struct rr_ctx {
+  int refs = 1;
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
@@ -148,6 +152,7 @@ struct rr_ctx {
 };
 
 struct rr_scene {
+  int refs = 1;
   rr_ctx* ctx = nullptr;
   int64_t nv = 0, nf = 0;
   int32_t nmat = 0;

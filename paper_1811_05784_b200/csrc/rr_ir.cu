@@ -61,6 +61,41 @@ __global__ void unfix_kernel(const unsigned long long* __restrict__ acc, int64_t
   out[i] = static_cast<double>(acc[i]) / scale;
 }
 
+// Pulse trains given as events (build_pulse_trains output, rir.hpp:12-23):
+// band b owns events [off[b], off[b+1]) with times t and amplitudes a.
+__global__ void max_abs_kernel(const double* __restrict__ a, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(a[i]));
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void bin_events_kernel(const int64_t* __restrict__ off, const double* __restrict__ time,
+                                  const double* __restrict__ amp, int64_t n, double fs, int64_t lh,
+                                  const unsigned long long* __restrict__ max_bits,
+                                  unsigned long long* __restrict__ pos, unsigned long long* __restrict__ neg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int b = 0;
+  while (b < kBands - 1 && i >= off[b + 1]) ++b;
+  const double scale = fixed_scale(*max_bits, n);
+  const long long center = llround(time[i] * fs);  // rir.cpp:86
+  if (center < 0 || center >= lh) return;
+  const double a = amp[i];
+  const unsigned long long q = static_cast<unsigned long long>(llrint(fabs(a) * scale));
+  if (q) atomicAdd((a < 0.0 ? neg : pos) + b * lh + center, q);
+}
+
+__global__ void unfix2_kernel(const unsigned long long* __restrict__ pos, const unsigned long long* __restrict__ neg,
+                              int64_t total, int64_t n, const unsigned long long* __restrict__ max_bits,
+                              double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const double scale = fixed_scale(*max_bits, n);
+  out[i] = static_cast<double>(pos[i]) / scale - static_cast<double>(neg[i]) / scale;
+}
+
 // design_band_filter rir.cpp:32-58 with `taps` taps, delay (taps-1)/2.
 __global__ void design_kernel(double fs, int taps, double* __restrict__ k) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,6 +194,32 @@ void ir_bin(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy
   unfix_kernel<<<static_cast<unsigned>((kBands * lh + 255) / 256), 256, 0, st>>>(acc.p, kBands * lh,
                                                                                   std::max<int64_t>(n, 1), mx.p,
                                                                                   d_hist);
+  RR_LAUNCH_CHECK();
+  ctx->launches++;
+}
+
+// Histogram of explicit pulse trains (times in seconds, signed amplitudes).
+void ir_bin_events(rr_ctx* ctx, const int64_t* d_off, int64_t n, const double* d_time, const double* d_amp, double fs,
+                   int64_t lh, double* d_hist) {
+  cudaStream_t st = ctx->stream;
+  DevBuf<unsigned long long> pos, neg, mx;
+  pos.alloc(kBands * lh, st);
+  neg.alloc(kBands * lh, st);
+  mx.alloc(1, st);
+  RR_CUDA(cudaMemsetAsync(pos.p, 0, pos.bytes(), st));
+  RR_CUDA(cudaMemsetAsync(neg.p, 0, neg.bytes(), st));
+  RR_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
+  if (n > 0) {
+    max_abs_kernel<<<592, 256, 0, st>>>(d_amp, n, mx.p);
+    RR_LAUNCH_CHECK();
+    bin_events_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(d_off, d_time, d_amp, n, fs, lh, mx.p,
+                                                                              pos.p, neg.p);
+    RR_LAUNCH_CHECK();
+    ctx->launches += 2;
+  }
+  unfix2_kernel<<<static_cast<unsigned>((kBands * lh + 255) / 256), 256, 0, st>>>(pos.p, neg.p, kBands * lh,
+                                                                                   std::max<int64_t>(n, 1), mx.p,
+                                                                                   d_hist);
   RR_LAUNCH_CHECK();
   ctx->launches++;
 }

@@ -65,6 +65,10 @@ struct rr_trace_result {
 namespace rr {
 rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, int32_t n_recv,
                            const rr_trace_config* cfg, const double* d_dirs);
+// rr_import.cu
+rr_trace_result* import_captures(rr_scene* s, int64_t n, const int32_t* recv, const int32_t* ray, const double* point,
+                                 const double* dir, const double* path, const double* mult, const int64_t* hist_off,
+                                 const int32_t* hist, const rr_receiver* receivers, int32_t n_recv);
 }  // namespace rr
 
 // Device image-source set (rr_images.cu), sorted by (order, distance, path).
