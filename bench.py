@@ -56,48 +56,58 @@ def brb_model(config):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled every 10 ms through NVML while
+    the timed region runs (nvidia-smi's 200 ms loop would miss a short
+    region)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
-        self.proc = None
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.sm.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                bits = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    if bits & getattr(N, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.01)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 # ---------------------------------------------------------------- helpers
@@ -158,6 +168,7 @@ def run_ours(args):
     from paper_1811_05784_b200 import Context, Receiver, SourceConfig, TraceConfig, TriangleMesh
     from paper_1811_05784_b200 import roomray as rr
     from paper_1811_05784_b200 import _lib
+    from paper_1811_05784_b200.shard import run_sharded
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -170,7 +181,7 @@ def run_ours(args):
     tree = rr.AccelTree(mesh, ctx)
     n_total = scene.ray_count * world  # weak scaling: 10^6 rays per GPU
     src = SourceConfig(scene.source, n_total)
-    recv = Receiver(*scene.receivers[0])
+    recv = [Receiver(*r) for r in scene.receivers]
     cfg = TraceConfig(max_iterations=scene.max_iterations, max_range=scene.max_range)
     shard = dict(first=rank, stride=world, block=4096) if world > 1 else {}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -225,6 +236,16 @@ def run_ours(args):
     taps = 1023
     h2d = pv.numel() * 8 + pt.numel() * 4 + pa.numel() * 8
     e2e_ms, d2h, breakdown = [], 0, {}
+    pool = {}
+
+    def pinned(key, t):
+        """Device tensor -> reused pinned host buffer (async copy)."""
+        buf = pool.get(key)
+        if buf is None or buf.numel() < t.numel() or buf.dtype != t.dtype:
+            buf = pool[key] = torch.empty(max(t.numel(), 1), dtype=t.dtype, pin_memory=True)
+        out = buf[: t.numel()].view(t.shape)
+        out.copy_(t, non_blocking=True)
+        return out
     lib = _lib.load()
     import ctypes as C
 
@@ -249,26 +270,16 @@ def run_ours(args):
             marks.append((name, ev))
 
         mark("scene")
-        dt = rr.trace_device(sc, src, recv, cfg, **shard)
-        mark("trace")
-        images = rr.build_image_sources_device(dt, n_total, rr.AirModel(), rr.ClusterOptions(1e-6, True))
-        mark("images")
-        d_dist, d_en, n_img = images.device_arrays()
-        hist = torch.empty(8 * (L + taps), dtype=torch.float64, device="cuda")
-        band = torch.empty(8 * L, dtype=torch.float64, device="cuda")
-        bb = torch.empty(L, dtype=torch.float64, device="cuda")
-        _lib.check(lib.rr_ir_bin_device(ctx.h, n_img, C.c_void_p(d_dist), C.c_void_p(d_en), scene.speed_of_sound,
-                                        scene.sample_rate, L + taps, C.c_void_p(hist.data_ptr())))
-        if world > 1:
-            torch.cuda.synchronize()
-            dist.all_reduce(hist)  # NCCL sum of the 8-band pulse histograms
-        _lib.check(lib.rr_ir_filter_device(ctx.h, C.c_void_p(hist.data_ptr()), scene.sample_rate, taps, L,
-                                           C.c_void_p(band.data_ptr()), C.c_void_p(bb.data_ptr())))
-        mark("ir")
-        host_ir = torch.empty(8 * L, dtype=torch.float64, pin_memory=True)
-        with torch.cuda.stream(stream):
-            host_ir.copy_(band, non_blocking=True)
-        img = images.fetch()
+        res = run_sharded(sc, src, recv, cfg, air=rr.AirModel(), options=rr.ClusterOptions(1e-6, True),
+                          sample_rate=scene.sample_rate, length=L, taps=taps, mark=mark)
+        # results to pinned host memory: the 8 band IRs (every rank) and the
+        # merged image list (rank 0)
+        fetched = []
+        for r, band in enumerate(res.band_ir):
+            fetched.append(pinned(("ir", r), band.reshape(-1)))
+            if res.images[r] is not None:
+                for f in res.images[r].__dataclass_fields__:
+                    fetched.append(pinned((f, r), getattr(res.images[r], f)))
         with torch.cuda.stream(stream):
             e1.record()
         torch.cuda.synchronize()
@@ -279,11 +290,8 @@ def run_ours(args):
             for name, ev in marks + [("fetch", e1)]:
                 breakdown[name] = breakdown.get(name, 0.0) + prev.elapsed_time(ev) / args.steps
                 prev = ev
-            d2h = host_ir.numel() * 8 + sum(a.nbytes for a in (img.position, img.distance, img.band_energy,
-                                                                 img.band_multiplier, img.ray_count, img.order,
-                                                                 img.has_projection, img.projection, img.path_off,
-                                                                 img.path))
-        del images, dt
+            d2h = sum(t.numel() * t.element_size() for t in fetched)
+        del res
         lib.rr_scene_destroy(h)
         sc.h = None
     e2e_local = sum(e2e_ms)
@@ -316,7 +324,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 conservative box filter)",
             "data": "synthetic (seeded splitmix64 scene; no dataset)",
             "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {n_total} rays, "
-                                   f"{scene.max_iterations} refl, 1 receiver",
+                                   f"{scene.max_iterations} refl, {len(scene.receivers)} receiver(s)",
                        "rays_per_gpu": scene.ray_count, "parallelism": f"rays block-cyclic x{world}",
                        "l2": "flushed between timed steps (512 MB write)"},
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -354,7 +362,7 @@ def run_reference(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
            "data": "synthetic (seeded splitmix64 scene; no dataset)",
            "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {scene.ray_count} rays, "
-                                  f"{scene.max_iterations} refl, 1 receiver", "parallelism": f"{threads} CPU threads"},
+                                  f"{scene.max_iterations} refl, {len(scene.receivers)} receiver(s)", "parallelism": f"{threads} CPU threads"},
            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": rates[0][3],
                             "sample": rates[0][2] + " per step"},
            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -365,7 +373,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")

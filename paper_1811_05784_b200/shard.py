@@ -320,49 +320,76 @@ def images_to_tensors(dimages) -> ImageSet:
 
 @dataclass
 class ShardedResult:
-    images: ImageSet | None      # rank 0 only
-    band_ir: torch.Tensor        # (8, L) on every rank
-    broadband: torch.Tensor      # (L,)
+    """Per receiver r: images[r] (merged list, rank 0 only; None elsewhere),
+    band_ir[r] (8, L) and broadband[r] (L,) on every rank."""
+
+    images: list
+    band_ir: list
+    broadband: list
     ray_bounces: int             # this rank's
-    local_images: int
+    local_images: int            # image sources built on this rank (all receivers)
 
 
-def run_sharded(tree, source, receiver, config, *, air, options, sample_rate: float, length: int, taps: int = 1023,
-                block: int = 4096, group=None) -> ShardedResult:
-    """trace → exchange → image sources → IR for one receiver, ranks of
-    `group` each tracing a block-cyclic shard of the N-ray lattice.  With a
-    single rank it is the plain single-GPU pipeline."""
+def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: float, length: int, taps: int = 1023,
+                block: int = 4096, group=None, mark=None) -> ShardedResult:
+    """trace -> exchange -> image sources -> IR for every receiver, the ranks
+    of `group` each tracing a block-cyclic shard of the N-ray lattice (one
+    trace serves all receivers: a receiver never alters a ray,
+    tracer.cpp:27-29).  With a single rank it is the plain single-GPU
+    pipeline."""
     import ctypes as C
 
     from . import _lib
     from .roomray import build_image_sources_device, trace_device
 
+    recs = list(receivers) if isinstance(receivers, (list, tuple)) else [receivers]
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     shard = dict(first=rank, stride=world, block=block) if world > 1 else {}
-    dt = trace_device(tree, source, receiver, config, **shard)
-    if world > 1:
-        caps = device_captures(dt, 0)
-        owner = order_owners(caps, config.max_iterations, group)
-        mine = exchange_captures(caps, owner, group)
-        dt_local = import_captures(tree, mine, receiver)
-    else:
-        dt_local = dt
-    dimg = build_image_sources_device(dt_local, source.ray_count, air, options)
+    mark = mark or (lambda name: None)
+    dt = trace_device(tree, source, recs, config, **shard)
+    mark("trace")
     lib = tree.lib
     dev = torch.device("cuda", tree.ctx.device)
-    d_dist, d_en, n_img = dimg.device_arrays()
-    hist = torch.empty(NUM_BANDS * (length + taps), dtype=torch.float64, device=dev)
-    _lib.check(lib.rr_ir_bin_device(tree.ctx.h, n_img, C.c_void_p(d_dist), C.c_void_p(d_en),
-                                    config.speed_of_sound, sample_rate, length + taps, C.c_void_p(hist.data_ptr())))
-    torch.cuda.synchronize(dev)
-    reduce_histogram(hist, group)
-    torch.cuda.synchronize(dev)
-    band = torch.empty(NUM_BANDS * length, dtype=torch.float64, device=dev)
-    bb = torch.empty(length, dtype=torch.float64, device=dev)
-    _lib.check(lib.rr_ir_filter_device(tree.ctx.h, C.c_void_p(hist.data_ptr()), sample_rate, taps, length,
-                                       C.c_void_p(band.data_ptr()), C.c_void_p(bb.data_ptr())))
-    local = images_to_tensors(dimg)
-    images = gather_images(local, group) if world > 1 else local
-    torch.cuda.synchronize(dev)
-    return ShardedResult(images, band.view(NUM_BANDS, length), bb, int(dt.stats.ray_bounces), len(local))
+    out = ShardedResult([], [], [], int(dt.stats.ray_bounces), 0)
+    caps_all = device_captures(dt) if world > 1 else None
+    recv_ids = None
+    if world > 1:
+        n = int(dt.stats.n_captures)
+        recv_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        _lib.check(lib.rr_trace_captures(dt.h, C.c_void_p(recv_ids.data_ptr()), None, None, None, None, None, None,
+                                         None))
+        recv_ids = recv_ids[:n]
+    for r in range(len(recs)):
+        if world > 1:
+            caps = select(caps_all, recv_ids == r)
+            owner = order_owners(caps, config.max_iterations, group)
+            mine = exchange_captures(caps, owner, group)
+            dt_local, ridx = import_captures(tree, mine, recs, r), r
+            mark("exchange")
+        else:
+            dt_local, ridx = dt, r
+        dimg = build_image_sources_device(dt_local, source.ray_count, air, options, receiver=ridx)
+        mark("images")
+        d_dist, d_en, n_img = dimg.device_arrays()
+        hist = torch.empty(NUM_BANDS * (length + taps), dtype=torch.float64, device=dev)
+        _lib.check(lib.rr_ir_bin_device(tree.ctx.h, n_img, C.c_void_p(d_dist), C.c_void_p(d_en),
+                                        config.speed_of_sound, sample_rate, length + taps,
+                                        C.c_void_p(hist.data_ptr())))
+        torch.cuda.synchronize(dev)
+        reduce_histogram(hist, group)
+        torch.cuda.synchronize(dev)
+        band = torch.empty(NUM_BANDS * length, dtype=torch.float64, device=dev)
+        bb = torch.empty(length, dtype=torch.float64, device=dev)
+        _lib.check(lib.rr_ir_filter_device(tree.ctx.h, C.c_void_p(hist.data_ptr()), sample_rate, taps, length,
+                                           C.c_void_p(band.data_ptr()), C.c_void_p(bb.data_ptr())))
+        torch.cuda.synchronize(dev)
+        mark("ir")
+        local = images_to_tensors(dimg)
+        out.local_images += len(local)
+        out.images.append(gather_images(local, group) if world > 1 else local)
+        out.band_ir.append(band.view(NUM_BANDS, length))
+        out.broadband.append(bb)
+        torch.cuda.synchronize(dev)
+        mark("gather")
+    return out
