@@ -159,7 +159,7 @@ __global__ void seg_node_kernel(const Seg* __restrict__ segs, int64_t S,
   if (level == 0) {
     double scale = 1e-3;
     for (int k = 0; k < 3; ++k) scale = fmax(scale, fmax(fabs(lo[k]), fabs(hi[k])));
-    eps = __double2float_ru(scale * 0x1p-20);
+    eps = __double2float_ru(scale * 0x1p-19);  // see rr_geom.cuh box_enter
     hdr->eps = eps;
     for (int k = 0; k < 3; ++k) {
       hdr->lo[k] = lo_f(lo[k], eps);

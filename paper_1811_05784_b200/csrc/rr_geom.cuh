@@ -4,7 +4,7 @@
 // compiled with -fmad=false so no FMA is contracted into them (the oracle is
 // compiled for baseline x86-64 with -ffp-contract=off).  The fp32 box test is
 // a conservative filter only: node boxes are rounded outward and expanded by
-// eps = scale * 2^-20, which dominates the fp32 origin/slab rounding error,
+// eps = scale * 2^-19, which dominates the fp32 origin/slab rounding error,
 // so every box the fp64 reference could enter is entered here too, and the
 // closest hit is decided by the fp64 triangle test alone.
 #pragma once
@@ -76,6 +76,7 @@ __device__ __forceinline__ double sphere_delta(D3 o, D3 d, D3 c, double r) {
 // Per-segment fp32 ray for the box filter.
 struct RayF {
   float ox, oy, oz, ix, iy, iz;
+  float nx, ny, nz;  // -(o * inv) for the fused slab test
   double shift;  // the fp32 origin sits at o + shift*d (shift > 0 only for far origins)
 };
 
@@ -89,7 +90,7 @@ __device__ __forceinline__ float inv_dir(double dk) {
 // Origins farther than 4*scale from 0 are moved (in fp64) to the root box
 // entry so that fp32 rounding of the origin stays below eps.
 __device__ __forceinline__ bool make_rayf(const TravHeader& h, D3 o, D3 d, RayF& r) {
-  const double scale = static_cast<double>(h.eps) * 0x1p20;
+  const double scale = static_cast<double>(h.eps) * 0x1p19;
   double shift = 0.0;
   if (fabs(o.x) > 4.0 * scale || fabs(o.y) > 4.0 * scale || fabs(o.z) > 4.0 * scale) {
     double tn = 0.0, tf = 1e300;
@@ -116,6 +117,9 @@ __device__ __forceinline__ bool make_rayf(const TravHeader& h, D3 o, D3 d, RayF&
   r.ix = inv_dir(d.x);
   r.iy = inv_dir(d.y);
   r.iz = inv_dir(d.z);
+  r.nx = -(r.ox * r.ix);
+  r.ny = -(r.oy * r.iy);
+  r.nz = -(r.oz * r.iz);
   r.shift = shift;
   return true;
 }
@@ -129,9 +133,13 @@ __device__ __forceinline__ float prune_bound(double delta, double shift) {
 // beyond tmax.
 __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, float ly, float hy, float lz, float hz,
                                            float tmax) {
-  const float x0 = (lx - r.ox) * r.ix, x1 = (hx - r.ox) * r.ix;
-  const float y0 = (ly - r.oy) * r.iy, y1 = (hy - r.oy) * r.iy;
-  const float z0 = (lz - r.oz) * r.iz, z1 = (hz - r.oz) * r.iz;
+  // fused slab distances l*inv - o*inv: besides the rounding of o and inv
+  // (each below scale * 2^-22 in space units), the rounded product o*inv
+  // adds at most |o| * 2^-24 <= scale * 2^-22 (|o| <= 4 scale, make_rayf);
+  // together below the eps = scale * 2^-19 expansion of every box.
+  const float x0 = __fmaf_rn(lx, r.ix, r.nx), x1 = __fmaf_rn(hx, r.ix, r.nx);
+  const float y0 = __fmaf_rn(ly, r.iy, r.ny), y1 = __fmaf_rn(hy, r.iy, r.ny);
+  const float z0 = __fmaf_rn(lz, r.iz, r.nz), z1 = __fmaf_rn(hz, r.iz, r.nz);
   const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.0f));
   const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));
   return tn <= tf ? tn : __int_as_float(0x7f800000);
@@ -162,6 +170,11 @@ struct HitResult {
 // plane with |d_axis| > 1e-6 meets it only at delta ~ 1e-14 / |d_axis|, which
 // the reference's fp64 test rejects (delta <= kSelfHitEpsilon), so the
 // closest hit is unchanged.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <bool PF = false>
 __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNode* __restrict__ nodes,
                                                  const TNode* smem, int32_t K, const FaceTri* __restrict__ tri,
                                                  D3 o, D3 d, int32_t* n_visit = nullptr, int32_t rplane = -2) {
@@ -184,6 +197,10 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
     if (node >= 0 && node != kPop) {
       ++visits;
       const TNode nd = load_node(nodes, smem, node, K);
+      if (PF) {  // start fetching both children while the boxes are tested
+        prefetch_l1(nd.d.x >= 0 ? static_cast<const void*>(nodes + nd.d.x) : static_cast<const void*>(tri + ~nd.d.x));
+        prefetch_l1(nd.d.y >= 0 ? static_cast<const void*>(nodes + nd.d.y) : static_cast<const void*>(tri + ~nd.d.y));
+      }
       float tl = box_enter(r, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y, tbest);
       float tr = box_enter(r, nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w, tbest);
       if (nd.d.z == rplane) tl = __int_as_float(0x7f800000);
@@ -299,7 +316,7 @@ __device__ __forceinline__ HitResult closest_hit_f(const TravHeader& h, const TN
   RayF r;
   if (!make_rayf(h, o, d, r)) return best;
   const float dx = __double2float_rn(d.x), dy = __double2float_rn(d.y), dz = __double2float_rn(d.z);
-  const float S = h.eps * 0x1p20f;
+  const float S = h.eps * 0x1p19f;
   float tbest = FLT_MAX;
   int32_t cand[kCand];
   float cand_lo[kCand];

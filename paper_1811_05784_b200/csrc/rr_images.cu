@@ -150,18 +150,29 @@ __device__ void heap_sort(int32_t* a, int64_t n, const double* retro, int64_t c0
 }
 
 // Pass A: spread test; split groups get sorted and their beams counted.
+// rs: retro points gathered into path-sorted order (contiguous per group, so
+// the sequential fp64 sums below stream instead of chasing indices).
+__global__ void gather_retro_kernel(const int32_t* __restrict__ idx, int64_t n, const double* __restrict__ retro,
+                                    int64_t c0, double* __restrict__ rs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = idx[i] - c0;
+  for (int k = 0; k < 3; ++k) rs[3 * i + k] = retro[3 * j + k];
+}
+
 __global__ void group_count_kernel(int32_t* __restrict__ idx, const int64_t* __restrict__ gstart, int64_t ng,
-                                   int64_t n, const double* __restrict__ retro, int64_t c0, double tol,
-                                   int32_t* __restrict__ n_img, int32_t* __restrict__ is_split) {
+                                   int64_t n, const double* __restrict__ retro, const double* __restrict__ rs,
+                                   int64_t c0, double tol, int32_t* __restrict__ n_img,
+                                   int32_t* __restrict__ is_split) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n, m = e - s;
   D3 mean = d3(0, 0, 0);
-  for (int64_t i = s; i < e; ++i) mean = mean + ld3(retro, idx[i] - c0);
+  for (int64_t i = s; i < e; ++i) mean = mean + ld3(rs, i);  // capture order, as the reference
   mean = d3(mean.x / static_cast<double>(m), mean.y / static_cast<double>(m), mean.z / static_cast<double>(m));
   double spread = 0.0;
   for (int64_t i = s; i < e; ++i) {
-    const double dd = norm3(ld3(retro, idx[i] - c0) - mean);
+    const double dd = norm3(ld3(rs, i) - mean);
     spread = (spread < dd) ? dd : spread;
   }
   if (spread <= tol) {
@@ -206,15 +217,24 @@ __device__ void emit_image(const int32_t* idx, int64_t b0, int64_t b1, const dou
 }
 
 __global__ void group_emit_kernel(const int32_t* __restrict__ idx, const int64_t* __restrict__ gstart, int64_t ng,
-                                  int64_t n, const double* __restrict__ retro, int64_t c0, double tol,
-                                  const int32_t* __restrict__ is_split, const int32_t* __restrict__ img_off,
-                                  const int64_t* __restrict__ off, ImgTmp t) {
+                                  int64_t n, const double* __restrict__ retro, const double* __restrict__ rs,
+                                  int64_t c0, double tol, const int32_t* __restrict__ is_split,
+                                  const int32_t* __restrict__ img_off, const int64_t* __restrict__ off, ImgTmp t) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n;
   int64_t slot = img_off[g];
-  if (!is_split[g]) {
-    emit_image(idx, s, e, retro, c0, off, t, slot);
+  if (!is_split[g]) {  // make_image over the whole group, contiguous retro points
+    D3 sum = d3(0, 0, 0);
+    for (int64_t i = s; i < e; ++i) sum = sum + ld3(rs, i);
+    const double m = static_cast<double>(e - s);
+    t.pos[3 * slot] = sum.x / m;
+    t.pos[3 * slot + 1] = sum.y / m;
+    t.pos[3 * slot + 2] = sum.z / m;
+    t.count[slot] = static_cast<int32_t>(e - s);
+    const int32_t rep = idx[s];
+    t.rep[slot] = rep;
+    t.order[slot] = static_cast<int32_t>(off[rep + 1] - off[rep]);
     return;
   }
   int64_t b0 = s;
@@ -241,7 +261,36 @@ __device__ __forceinline__ unsigned long long cell_key(int32_t order, const long
     h *= 0xBF58476D1CE4E5B9ull;
     h ^= h >> 31;
   }
-  return h;
+  return h == ~0ull ? ~1ull : h;  // ~0 marks an empty hash slot
+}
+
+// Open-addressing table: sorted cell key -> first index of its run.
+__device__ __forceinline__ unsigned long long ht_slot(unsigned long long key, unsigned long long mask) {
+  return (key ^ (key >> 29)) & mask;
+}
+
+__global__ void ht_insert_kernel(const unsigned long long* __restrict__ skeys, int64_t n,
+                                 unsigned long long* tkey, int32_t* __restrict__ tstart, unsigned long long mask) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || (i > 0 && skeys[i] == skeys[i - 1])) return;
+  const unsigned long long key = skeys[i];
+  for (unsigned long long h = ht_slot(key, mask);; h = (h + 1) & mask) {
+    const unsigned long long prev = atomicCAS(tkey + h, ~0ull, key);
+    if (prev == ~0ull || prev == key) {
+      tstart[h] = static_cast<int32_t>(i);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ int32_t ht_find(const unsigned long long* __restrict__ tkey,
+                                           const int32_t* __restrict__ tstart, unsigned long long mask,
+                                           unsigned long long key) {
+  for (unsigned long long h = ht_slot(key, mask);; h = (h + 1) & mask) {
+    const unsigned long long k = tkey[h];
+    if (k == key) return tstart[h];
+    if (k == ~0ull) return -1;
+  }
 }
 
 __global__ void cell_key_kernel(ImgTmp t, int64_t n, double cs, unsigned long long* __restrict__ keys,
@@ -254,100 +303,120 @@ __global__ void cell_key_kernel(ImgTmp t, int64_t n, double cs, unsigned long lo
   ids[i] = static_cast<int32_t>(i);
 }
 
-// cond(i, j) of image_sources.cpp:111-116 (i the anchor candidate)
-__device__ __forceinline__ bool merge_cond(ImgTmp t, const double* mult, int64_t i, int64_t j, double tol) {
-  if (t.order[i] != t.order[j]) return false;
-  if (norm3(ld3(t.pos, j) - ld3(t.pos, i)) > tol) return false;
-  const double* mi = mult + kBands * static_cast<int64_t>(t.rep[i]);
-  const double* mj = mult + kBands * static_cast<int64_t>(t.rep[j]);
-  for (int b = 0; b < kBands; ++b)
-    if (fabs(mj[b] - mi[b]) > 1e-12) return false;
-  return true;
-}
-
-// For each image: candidate neighbours (pred j < i, succ j > i) with cond.
-// mode 0: count; mode 1: fill.
-__global__ void neighbour_kernel(ImgTmp t, const double* __restrict__ mult, int64_t n, double cs, double tol,
-                                 const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ sids,
-                                 int mode, int32_t* __restrict__ n_pred, int32_t* __restrict__ n_succ,
-                                 const int64_t* __restrict__ pred_off, const int64_t* __restrict__ succ_off,
-                                 int32_t* __restrict__ pred, int32_t* __restrict__ succ) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  long long c[3];
-  cell_of(t.pos, i, cs, c);
-  int32_t np = 0, ns = 0;
-  for (int dx = -1; dx <= 1; ++dx)
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dz = -1; dz <= 1; ++dz) {
-        long long cc[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
-        const unsigned long long key = cell_key(t.order[i], cc);
-        int64_t lo = 0, hi = n;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) / 2;
-          if (skeys[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        for (int64_t p = lo; p < n && skeys[p] == key; ++p) {
-          const int32_t j = sids[p];
-          if (j == i) continue;
-          long long cj[3];
-          cell_of(t.pos, j, cs, cj);
-          if (cj[0] != cc[0] || cj[1] != cc[1] || cj[2] != cc[2]) continue;  // hash collision
-          if (j < i) {
-            if (!merge_cond(t, mult, j, i, tol)) continue;
-            if (mode) pred[pred_off[i] + np] = j;
-            ++np;
-          } else {
-            if (!merge_cond(t, mult, i, j, tol)) continue;
-            if (mode) succ[succ_off[i] + ns] = j;
-            ++ns;
-          }
-        }
-      }
-  if (!mode) {
-    n_pred[i] = np;
-    n_succ[i] = ns;
-  }
-}
-
 constexpr int32_t kUndet = -2;
 constexpr int32_t kAnchor = -1;
 
-__global__ void anchor_init_kernel(const int32_t* __restrict__ n_pred, int64_t n, int32_t* __restrict__ owner) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) owner[i] = n_pred[i] == 0 ? kAnchor : kUndet;
+// Candidates in cell-sorted order, contiguous so the threads of one cell
+// stream the same records: position, multipliers (of the image's beam) and
+// order.
+struct Cand {
+  const double* pos;   // 3 per entry
+  const double* mult;  // 8 per entry
+  const int32_t* order;
+  const int32_t* id;   // image index
+};
+
+__global__ void cand_gather_kernel(ImgTmp t, const double* __restrict__ mult, const int32_t* __restrict__ sids,
+                                   int64_t n, double* __restrict__ cpos, double* __restrict__ cmult,
+                                   int32_t* __restrict__ corder) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int32_t j = sids[q];
+  for (int k = 0; k < 3; ++k) cpos[3 * q + k] = t.pos[3 * j + k];
+  const double* m = mult + kBands * static_cast<int64_t>(t.rep[j]);
+  for (int b = 0; b < kBands; ++b) cmult[kBands * q + b] = m[b];
+  corder[q] = t.order[j];
 }
 
-// i is claimed by the smallest anchor among its preds; an anchor when none
-// of its preds is one.  Decided once every pred is decided.
-__global__ void anchor_step_kernel(const int32_t* __restrict__ n_pred, const int64_t* __restrict__ pred_off,
-                                   const int32_t* __restrict__ pred, int64_t n, int32_t* __restrict__ owner,
-                                   int32_t* __restrict__ changed) {
+__global__ void owner_init_kernel(int32_t* __restrict__ owner, int64_t n) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || owner[i] != kUndet) return;
-  // preds ascending: the first anchor among them owns i; an undecided pred
-  // before it means "wait"; none => i is an anchor
-  for (int32_t k = 0; k < n_pred[i]; ++k) {
-    const int32_t j = pred[pred_off[i] + k];
-    const int32_t o = owner[j];
-    if (o == kUndet) {
-      *changed = 1;
-      return;
-    }
-    if (o == kAnchor) {
-      owner[i] = j;
-      *changed = 1;
-      return;
-    }
+  if (i < n) owner[i] = kUndet;
+}
+
+// One round of the greedy of image_sources.cpp:103-128 without edge lists.
+// Image i is claimed by the smallest-index anchor among its preds
+// (j < i with cond(j, i): same order, |pos_i - pos_j| <= tol, multipliers
+// within 1e-12); it is an anchor when no pred is.  i is decided once every
+// pred below that anchor is decided.  Decisions only move from undecided to
+// final, so reading a neighbour's value while it is being written is safe.
+// Candidate cells: per axis those met by [p - tol, p + tol] (cell size
+// 2 tol, widened by 1 % against rounding of the cell index).
+__global__ void resolve_round_kernel(ImgTmp t, const double* __restrict__ mult, int64_t n, double cs, double tol,
+                                     const unsigned long long* __restrict__ skeys, Cand cand,
+                                     const unsigned long long* __restrict__ tkey, const int32_t* __restrict__ tstart,
+                                     unsigned long long mask, int32_t* owner, int32_t* __restrict__ progress) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  volatile int32_t* vo = owner;
+  if (vo[i] != kUndet) return;
+  const int32_t oi = t.order[i];
+  const D3 pi = ld3(t.pos, i);
+  const double* mi = mult + kBands * static_cast<int64_t>(t.rep[i]);
+  double m8[kBands];
+  for (int b = 0; b < kBands; ++b) m8[b] = mi[b];
+  long long lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    const double x = t.pos[3 * i + k];
+    lo[k] = static_cast<long long>(floor((x - 1.01 * tol) / cs));
+    hi[k] = static_cast<long long>(floor((x + 1.01 * tol) / cs));
   }
-  owner[i] = kAnchor;
-  *changed = 1;
+  int32_t best_anchor = INT32_MAX, min_undet = INT32_MAX;
+  for (long long cx = lo[0]; cx <= hi[0]; ++cx)
+    for (long long cy = lo[1]; cy <= hi[1]; ++cy)
+      for (long long cz = lo[2]; cz <= hi[2]; ++cz) {
+        long long cc[3] = {cx, cy, cz};
+        const unsigned long long key = cell_key(oi, cc);
+        const int32_t start = ht_find(tkey, tstart, mask, key);
+        if (start < 0) continue;
+        for (int64_t q = start; q < n && skeys[q] == key; ++q) {
+          const int32_t j = cand.id[q];
+          if (j >= i || j >= best_anchor) break;  // ids ascend inside a run: no later entry can win
+          if (cand.order[q] != oi) continue;
+          const D3 pj = ld3(cand.pos, q);
+          if (static_cast<long long>(floor(pj.x / cs)) != cx || static_cast<long long>(floor(pj.y / cs)) != cy ||
+              static_cast<long long>(floor(pj.z / cs)) != cz)
+            continue;  // hash collision
+          // cond(j, i), j the anchor candidate (image_sources.cpp:111-116)
+          if (norm3(pi - pj) > tol) continue;
+          const double* mj = cand.mult + kBands * q;
+          bool same = true;
+          for (int b = 0; b < kBands; ++b) same = same && !(fabs(m8[b] - mj[b]) > 1e-12);
+          if (!same) continue;
+          const int32_t o = vo[j];
+          if (o == kAnchor) best_anchor = j;
+          else if (o == kUndet) min_undet = min(min_undet, j);
+        }
+      }
+  if (min_undet < best_anchor) {
+    progress[1] = 1;  // still waiting on a smaller undecided pred
+    return;
+  }
+  vo[i] = best_anchor == INT32_MAX ? kAnchor : best_anchor;
+  progress[0] = 1;
 }
 
-// merged image per anchor: image_sources.cpp:103-128
+// claims sorted by (owner, index): key owner << 32 | index, anchors ~0
+__global__ void claim_key_kernel(const int32_t* __restrict__ owner, int64_t n, unsigned long long* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t o = owner[i];
+  keys[i] = o >= 0 ? (static_cast<unsigned long long>(static_cast<uint32_t>(o)) << 32) | static_cast<uint32_t>(i)
+                   : ~0ull;
+}
+
+__global__ void claim_start_kernel(const unsigned long long* __restrict__ skeys, int64_t n,
+                                   int32_t* __restrict__ claim_start) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n || skeys[q] == ~0ull) return;
+  const uint32_t a = static_cast<uint32_t>(skeys[q] >> 32);
+  if (q == 0 || static_cast<uint32_t>(skeys[q - 1] >> 32) != a) claim_start[a] = static_cast<int32_t>(q);
+}
+
+// merged image per anchor: weighted mean over the anchor and its claims in
+// index order, lexicographically smallest path (image_sources.cpp:103-128)
 __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict__ owner,
-                                  const int32_t* __restrict__ n_succ, const int64_t* __restrict__ succ_off,
-                                  const int32_t* __restrict__ succ, const int32_t* __restrict__ anchor_rank,
+                                  const unsigned long long* __restrict__ claims,
+                                  const int32_t* __restrict__ claim_start, const int32_t* __restrict__ anchor_rank,
                                   PathView pv, ImgTmp out, int64_t n_out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n || owner[i] != kAnchor) return;
@@ -355,14 +424,17 @@ __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict
   D3 w = d3(t.pos[3 * i] * static_cast<double>(cnt), t.pos[3 * i + 1] * static_cast<double>(cnt),
             t.pos[3 * i + 2] * static_cast<double>(cnt));
   int32_t rep = t.rep[i];
-  // claims in increasing index order (the succ list is sorted below)
-  for (int32_t k = 0; k < n_succ[i]; ++k) {
-    const int32_t j = succ[succ_off[i] + k];
-    if (owner[j] != i) continue;
-    const double cj = static_cast<double>(t.count[j]);
-    w = w + d3(t.pos[3 * j] * cj, t.pos[3 * j + 1] * cj, t.pos[3 * j + 2] * cj);
-    cnt += t.count[j];
-    if (pv.cmp(t.rep[j], rep) < 0) rep = t.rep[j];
+  const int32_t q0 = claim_start[i];
+  if (q0 >= 0) {
+    for (int64_t q = q0; q < n && claims[q] != ~0ull &&
+                         static_cast<uint32_t>(claims[q] >> 32) == static_cast<uint32_t>(i);
+         ++q) {
+      const int32_t j = static_cast<int32_t>(claims[q] & 0xffffffffu);
+      const double cj = static_cast<double>(t.count[j]);
+      w = w + d3(t.pos[3 * j] * cj, t.pos[3 * j + 1] * cj, t.pos[3 * j + 2] * cj);
+      cnt += t.count[j];
+      if (pv.cmp(t.rep[j], rep) < 0) rep = t.rep[j];
+    }
   }
   const int64_t s = anchor_rank[i];
   const double m = static_cast<double>(cnt);
@@ -371,25 +443,8 @@ __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict
   out.pos[3 * s + 2] = w.z / m;
   out.count[s] = cnt;
   out.order[s] = t.order[i];
-  out.rep[s] = rep;       // path source (lexicographic minimum)
+  out.rep[s] = rep;               // path source (lexicographic minimum)
   out.rep[n_out + s] = t.rep[i];  // multiplier source (the anchor's, :113)
-}
-
-__global__ void sort_small_lists_kernel(const int32_t* __restrict__ cnt, const int64_t* __restrict__ off, int64_t n,
-                                        int32_t* __restrict__ list) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int32_t* a = list + off[i];
-  const int32_t m = cnt[i];
-  for (int32_t x = 1; x < m; ++x) {  // insertion sort (lists are tiny)
-    const int32_t v = a[x];
-    int32_t y = x - 1;
-    while (y >= 0 && a[y] > v) {
-      a[y + 1] = a[y];
-      --y;
-    }
-    a[y + 1] = v;
-  }
 }
 
 __global__ void flag_anchor_kernel(const int32_t* __restrict__ owner, int64_t n, int32_t* __restrict__ f) {
@@ -563,7 +618,11 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   n_img.alloc(ng + 1, st);
   is_split.alloc(ng, st);
   img_off.alloc(ng + 1, st);
-  group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, c0, tol, n_img.p, is_split.p);
+  DevBuf<double> rs;
+  rs.alloc(3 * n, st);
+  gather_retro_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, retro.p, c0, rs.p);
+  group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, n_img.p,
+                                                    is_split.p);
   RR_LAUNCH_CHECK();
   RR_CUDA(cudaMemsetAsync(n_img.p + ng, 0, sizeof(int32_t), st));
   cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, n_img.p, img_off.p, ng + 1, st); },
@@ -579,8 +638,8 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   torder.alloc(ni, st);
   trep.alloc(2 * ni, st);
   ImgTmp T{tpos.p, tcount.p, torder.p, trep.p};
-  group_emit_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, c0, tol, is_split.p, img_off.p,
-                                              tr->c_off.p, T);
+  group_emit_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, is_split.p,
+                                                   img_off.p, tr->c_off.p, T);
   RR_LAUNCH_CHECK();
   ctx->launches += 8;
   tm.mark("groups");
@@ -603,51 +662,54 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     cub_call([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, keys.p, skeys.p, ids.p, sids.p, ni, 0, 64, st);
     }, st);
-    DevBuf<int32_t> n_pred, n_succ;
-    DevBuf<int64_t> pred_off, succ_off;
-    n_pred.alloc(ni + 1, st);
-    n_succ.alloc(ni + 1, st);
-    pred_off.alloc(ni + 1, st);
-    succ_off.alloc(ni + 1, st);
-    RR_CUDA(cudaMemsetAsync(n_pred.p + ni, 0, sizeof(int32_t), st));
-    RR_CUDA(cudaMemsetAsync(n_succ.p + ni, 0, sizeof(int32_t), st));
-    neighbour_kernel<<<grid(ni, 128), 128, 0, st>>>(T, tr->c_mult.p, ni, cs, tol, skeys.p, sids.p, 0, n_pred.p,
-                                                n_succ.p, nullptr, nullptr, nullptr, nullptr);
-    RR_LAUNCH_CHECK();
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, n_pred.p, pred_off.p, ni + 1, st);
-    }, st);
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, n_succ.p, succ_off.p, ni + 1, st);
-    }, st);
-    int64_t tp = 0, ts = 0;
-    RR_CUDA(cudaMemcpyAsync(&tp, pred_off.p + ni, sizeof tp, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaMemcpyAsync(&ts, succ_off.p + ni, sizeof ts, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaStreamSynchronize(st));
-    DevBuf<int32_t> pred, succ, owner, changed;
-    pred.alloc(std::max<int64_t>(tp, 1), st);
-    succ.alloc(std::max<int64_t>(ts, 1), st);
+    unsigned long long tsize = 1024;
+    while (tsize < 2ull * static_cast<unsigned long long>(ni)) tsize <<= 1;
+    DevBuf<unsigned long long> tkey;
+    DevBuf<int32_t> tstart;
+    tkey.alloc(tsize, st);
+    tstart.alloc(tsize, st);
+    RR_CUDA(cudaMemsetAsync(tkey.p, 0xff, tkey.bytes(), st));
+    ht_insert_kernel<<<grid(ni), 256, 0, st>>>(skeys.p, ni, tkey.p, tstart.p, tsize - 1);
+    DevBuf<double> cpos, cmult;
+    DevBuf<int32_t> corder, owner, progress;
+    cpos.alloc(3 * ni, st);
+    cmult.alloc(kBands * ni, st);
+    corder.alloc(ni, st);
     owner.alloc(ni, st);
-    changed.alloc(1, st);
-    neighbour_kernel<<<grid(ni, 128), 128, 0, st>>>(T, tr->c_mult.p, ni, cs, tol, skeys.p, sids.p, 1, n_pred.p,
-                                                n_succ.p, pred_off.p, succ_off.p, pred.p, succ.p);
+    progress.alloc(2, st);
+    cand_gather_kernel<<<grid(ni), 256, 0, st>>>(T, tr->c_mult.p, sids.p, ni, cpos.p, cmult.p, corder.p);
+    owner_init_kernel<<<grid(ni), 256, 0, st>>>(owner.p, ni);
     RR_LAUNCH_CHECK();
-    sort_small_lists_kernel<<<grid(ni), 256, 0, st>>>(n_succ.p, succ_off.p, ni, succ.p);
-    sort_small_lists_kernel<<<grid(ni), 256, 0, st>>>(n_pred.p, pred_off.p, ni, pred.p);
-    RR_LAUNCH_CHECK();
-    anchor_init_kernel<<<grid(ni), 256, 0, st>>>(n_pred.p, ni, owner.p);
-    RR_LAUNCH_CHECK();
-    ctx->launches += 8;
-    for (int it = 0; it < 100000; ++it) {
-      int32_t h = 0;
-      RR_CUDA(cudaMemsetAsync(changed.p, 0, sizeof(int32_t), st));
-      anchor_step_kernel<<<grid(ni), 256, 0, st>>>(n_pred.p, pred_off.p, pred.p, ni, owner.p, changed.p);
+    ctx->launches += 7;
+    tm.mark("merge: cells");
+    const Cand cand{cpos.p, cmult.p, corder.p, sids.p};
+    for (int round = 0;; ++round) {
+      int32_t h[2] = {0, 0};
+      RR_CUDA(cudaMemsetAsync(progress.p, 0, 2 * sizeof(int32_t), st));
+      resolve_round_kernel<<<grid(ni, 128), 128, 0, st>>>(T, tr->c_mult.p, ni, cs, tol, skeys.p, cand, tkey.p,
+                                                          tstart.p, tsize - 1, owner.p, progress.p);
       RR_LAUNCH_CHECK();
       ctx->launches++;
-      RR_CUDA(cudaMemcpyAsync(&h, changed.p, sizeof h, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaMemcpyAsync(h, progress.p, sizeof h, cudaMemcpyDeviceToHost, st));
       RR_CUDA(cudaStreamSynchronize(st));
-      if (!h) break;
+      if (!h[1]) break;  // nobody left waiting
+      if (!h[0]) throw Error(RR_RUNTIME, "coplanar merge made no progress");  // impossible: preds are smaller
     }
+    tm.mark("merge: resolve");
+    DevBuf<unsigned long long> ckeys, cskeys;
+    DevBuf<int32_t> claim_start;
+    ckeys.alloc(ni, st);
+    cskeys.alloc(ni, st);
+    claim_start.alloc(ni, st);
+    claim_key_kernel<<<grid(ni), 256, 0, st>>>(owner.p, ni, ckeys.p);
+    RR_LAUNCH_CHECK();
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, ckeys.p, cskeys.p, ni, 0, 64, st);
+    }, st);
+    RR_CUDA(cudaMemsetAsync(claim_start.p, 0xff, claim_start.bytes(), st));
+    claim_start_kernel<<<grid(ni), 256, 0, st>>>(cskeys.p, ni, claim_start.p);
+    RR_LAUNCH_CHECK();
+    tm.mark("merge: claims");
     DevBuf<int32_t> aflag, arank;
     aflag.alloc(ni + 1, st);
     arank.alloc(ni + 1, st);
@@ -665,7 +727,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     mrep.alloc(2 * static_cast<int64_t>(na), st);
     M = ImgTmp{mpos.p, mcount.p, morder.p, mrep.p};
     // path reps at [0, na), multiplier reps at [na, 2na)
-    merge_emit_kernel<<<grid(ni), 256, 0, st>>>(T, ni, owner.p, n_succ.p, succ_off.p, succ.p, arank.p, pv, M, na);
+    merge_emit_kernel<<<grid(ni), 256, 0, st>>>(T, ni, owner.p, cskeys.p, claim_start.p, arank.p, pv, M, na);
     RR_LAUNCH_CHECK();
     ctx->launches += 3;
     ni = na;
