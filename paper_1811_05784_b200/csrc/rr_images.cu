@@ -99,6 +99,56 @@ __global__ void retro_kernel(const double* __restrict__ point, const double* __r
   idx[i] = static_cast<int32_t>(c);
 }
 
+// Path sort, stage 1: radix key of the first three faces (21 bits each,
+// face + 1, 0 past the end: a proper prefix sorts first, as in
+// std::lexicographical_compare).
+__global__ void prefix_key_kernel(const int32_t* __restrict__ idx, int64_t n, PathView pv,
+                                  unsigned long long* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t c = idx[i], a0 = pv.off[c], len = pv.off[c + 1] - a0;
+  unsigned long long k = 0;
+  for (int j = 0; j < 3; ++j) {
+    const unsigned long long f = j < len ? static_cast<unsigned long long>(pv.hist[a0 + j]) + 1ull : 0ull;
+    k = (k << 21) | f;
+  }
+  keys[i] = k;
+}
+
+// Stage 2: one thread per run of equal prefix keys finishes the order with a
+// stable insertion sort on the full comparator (runs are beams of identical
+// paths or a handful of paths that share three faces).
+// A run needs sorting only if two neighbours in it differ (all-identical
+// beams are already in capture order): flag its first element in parallel.
+__global__ void prefix_run_flag_kernel(const unsigned long long* __restrict__ keys, int64_t n, PathView pv,
+                                       const int32_t* __restrict__ idx, int32_t* __restrict__ dirty) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  if (q == 0 || keys[q] != keys[q - 1]) return;  // dirty[] is zeroed beforehand
+  if (pv.cmp(idx[q - 1], idx[q]) == 0) return;
+  int64_t s = q - 1;
+  while (s > 0 && keys[s - 1] == keys[q]) --s;
+  atomicOr(dirty + s, 1);
+}
+
+__global__ void prefix_run_sort_kernel(const unsigned long long* __restrict__ keys, int64_t n, PathView pv,
+                                       const int32_t* dirty, int32_t* __restrict__ idx) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n || (s > 0 && keys[s] == keys[s - 1]) || !dirty[s]) return;
+  int64_t e = s + 1;
+  while (e < n && keys[e] == keys[s]) ++e;
+  if (e - s < 2) return;
+  for (int64_t x = s + 1; x < e; ++x) {
+    const int32_t v = idx[x];
+    int64_t y = x - 1;
+    while (y >= s && pv.cmp(idx[y], v) > 0) {
+      idx[y + 1] = idx[y];
+      --y;
+    }
+    idx[y + 1] = v;
+  }
+}
+
 __global__ void head_kernel(const int32_t* __restrict__ idx, int64_t n, PathView pv, int32_t* __restrict__ head) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -592,9 +642,32 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   gid.alloc(n, st);
   retro_kernel<<<grid(n), 256, 0, st>>>(tr->c_point.p, tr->c_dir.p, tr->c_path.p, c0, n, retro.p, idx.p);
   RR_LAUNCH_CHECK();
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceMergeSort::StableSortKeys(t, b, idx.p, n, PathLess{pv}, st);
-  }, st);
+  if (s->nf < (1 << 21) - 1) {
+    // radix sort on the 3-face prefix (stable: ties keep capture order), then
+    // per-run stable insertion sorts on the full path
+    DevBuf<unsigned long long> pk, pk_s;
+    DevBuf<int32_t> idx_s;
+    pk.alloc(n, st);
+    pk_s.alloc(n, st);
+    idx_s.alloc(n, st);
+    prefix_key_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, pv, pk.p);
+    RR_LAUNCH_CHECK();
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, pk.p, pk_s.p, idx.p, idx_s.p, n, 0, 63, st);
+    }, st);
+    DevBuf<int32_t> dirty;
+    dirty.alloc(n, st);
+    RR_CUDA(cudaMemsetAsync(dirty.p, 0, dirty.bytes(), st));
+    prefix_run_flag_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, idx_s.p, dirty.p);
+    prefix_run_sort_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, dirty.p, idx_s.p);
+    RR_LAUNCH_CHECK();
+    idx = std::move(idx_s);
+    ctx->launches += 6;
+  } else {
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceMergeSort::StableSortKeys(t, b, idx.p, n, PathLess{pv}, st);
+    }, st);
+  }
   tm.mark("path sort");
   head_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, pv, head.p);
   RR_LAUNCH_CHECK();

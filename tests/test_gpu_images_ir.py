@@ -130,3 +130,27 @@ def test_band_filter_matches_reference(ctx, port):
     for b in range(8):
         np.testing.assert_allclose(rr.design_band_filter(b, 44100.0), port.band_filter(b, 44100.0), rtol=1e-12,
                                    atol=1e-15)
+
+
+@pytest.mark.parametrize("merge", [False, True])
+def test_image_sources_config2_subset(ctx, port, merge):
+    """Gridded 100 000-triangle room: thousands of coplanar beams per wall
+    (large merge clusters, long shared path prefixes), 20 000 rays of the
+    10^6 lattice, 50 reflections, against the oracle bit for bit."""
+    s = scenes.config2()
+    n, stride = s.ray_count, 50
+    tree = AccelTree(TriangleMesh(s.vertices, s.faces, s.absorption), ctx)
+    cnt = n // stride
+    dirs = port.fibonacci(n, 0, stride, cnt)
+    rc, rad = s.receivers[0]
+    dt = rr.trace_device(tree, SourceConfig(s.source, n), Receiver(rc, rad),
+                         TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range), directions=dirs,
+                         first=0, stride=stride)
+    gi = rr.build_image_sources(dt, n, rr.AirModel(), rr.ClusterOptions(1e-6, merge))
+    ps = port.scene(oracle.Mesh(s.vertices, s.faces, s.absorption))
+    oc, _ = ps.trace(s.source, n, [rc], [rad], s.max_iterations, s.max_range, 8, 0, stride, 0)
+    oi = ps.image_sources(oc, n, AIR, rc, 1e-6, merge)
+    assert len(oc) > 5000
+    _compare_images(gi, oi)
+    if merge:
+        assert len(gi) < len(oc)  # coplanar beams did merge
