@@ -80,8 +80,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
       if (lane == leader) base = atomicAdd(p.ray_counter, (unsigned long long)__popc(m));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (need) {
-        const int64_t i = static_cast<int64_t>(base) + __popc(m & lt_mask);
-        if (i < p.count) {
+        const int64_t c = static_cast<int64_t>(base) + __popc(m & lt_mask);
+        if (c < p.count) {
+          const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + c)) : c;
           ray = i;
           o = d3(p.src[0], p.src[1], p.src[2]);
           if (p.dirs) {
@@ -306,8 +307,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_df(const TraceParams p
       if (lane == leader) base = atomicAdd(p.ray_counter, (unsigned long long)__popc(m));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (need) {
-        const int64_t i = static_cast<int64_t>(base) + __popc(m & lt_mask);
-        if (i < p.count) {
+        const int64_t c = static_cast<int64_t>(base) + __popc(m & lt_mask);
+        if (c < p.count) {
+          const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + c)) : c;
           ray = i;
           LaneRay x;
           x.o = d3(p.src[0], p.src[1], p.src[2]);
@@ -482,6 +484,51 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_df(const TraceParams p
     atomicAdd(p.stats + 3, st_alive);
     atomicMax(p.stats + 4, (unsigned long long)st_max);
   }
+}
+
+// ---------------------------------------------------------------- ray order
+// Warps take rays in a spatially coherent order: neighbours of a Fibonacci
+// point are far apart in index (azimuth step = golden angle), so the lattice
+// order puts 32 unrelated directions in a warp.  Sorting the rays by the
+// Morton code of an approximate direction groups nearby directions; mirror
+// reflection keeps such beams together for many bounces, so warps traverse
+// similar nodes.  Only the processing order changes (captures are sorted by
+// ray index afterwards), never a result.
+__device__ __forceinline__ uint32_t part1by2(uint32_t x) {
+  x &= 0x3ff;
+  x = (x | (x << 16)) & 0x030000ff;
+  x = (x | (x << 8)) & 0x0300f00f;
+  x = (x | (x << 4)) & 0x030c30c3;
+  x = (x | (x << 2)) & 0x09249249;
+  return x;
+}
+
+__global__ void ray_order_key_kernel(const TraceParams p, uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= p.count) return;
+  float x, y, z;
+  if (p.dirs) {
+    x = static_cast<float>(p.dirs[3 * c]);
+    y = static_cast<float>(p.dirs[3 * c + 1]);
+    z = static_cast<float>(p.dirs[3 * c + 2]);
+  } else {
+    const int64_t k = global_ray(p, c);
+    const double zz = 1.0 - (2.0 * static_cast<double>(k) + 1.0) / static_cast<double>(p.N);
+    const double rho = sqrt(fmax(0.0, 1.0 - zz * zz));
+    // azimuth modulo 2 pi from the fractional part of k * (1 - 1/golden)
+    const double f = static_cast<double>(k) * 0.38196601125010515;
+    const float phi = static_cast<float>(6.283185307179586 * (f - floor(f)));
+    float s, co;
+    sincosf(phi, &s, &co);
+    x = static_cast<float>(rho) * co;
+    y = static_cast<float>(rho) * s;
+    z = static_cast<float>(zz);
+  }
+  const uint32_t qx = static_cast<uint32_t>(fminf(fmaxf((x + 1.0f) * 512.0f, 0.0f), 1023.0f));
+  const uint32_t qy = static_cast<uint32_t>(fminf(fmaxf((y + 1.0f) * 512.0f, 0.0f), 1023.0f));
+  const uint32_t qz = static_cast<uint32_t>(fminf(fmaxf((z + 1.0f) * 512.0f, 0.0f), 1023.0f));
+  keys[c] = (part1by2(qx) << 2) | (part1by2(qy) << 1) | part1by2(qz);
+  vals[c] = static_cast<int32_t>(c);
 }
 
 // ---------------------------------------------------------------- captures
@@ -723,6 +770,32 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   const int blocks_per_sm = std::max(occ_cache_blocks, 1);
   const int64_t want = (count + 127) / 128;
   const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)s->ctx->sm_count * blocks_per_sm)));
+  // spatially coherent work order (RR_ORDER=0 keeps the lattice order)
+  static const int order_env = [] {
+    const char* e = std::getenv("RR_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
+  DevBuf<int32_t> order;
+  p.order = nullptr;
+  if (order_env && count > 1 && count < (int64_t(1) << 31)) {
+    DevBuf<uint32_t> ok, ok_s;
+    DevBuf<int32_t> ov;
+    ok.alloc(count, st);
+    ok_s.alloc(count, st);
+    ov.alloc(count, st);
+    order.alloc(count, st);
+    ray_order_key_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(p, ok.p, ov.p);
+    RR_LAUNCH_CHECK();
+    size_t tb = 0;
+    RR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ok.p, ok_s.p, ov.p, order.p, static_cast<int>(count), 0, 30,
+                                            st));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb, st);
+    RR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ok.p, ok_s.p, ov.p, order.p, static_cast<int>(count), 0, 30,
+                                            st));
+    s->ctx->launches += 5;
+    p.order = order.p;
+  }
   cudaEvent_t e0, e1;
   RR_CUDA(cudaEventCreate(&e0));
   RR_CUDA(cudaEventCreate(&e1));

@@ -33,6 +33,7 @@ struct TraceParams {
   int64_t first, stride, block;
   double az_step;  // 2*pi*(1 - 1/golden) evaluated on the host
   const double* dirs;  // optional explicit directions (count*3), else lattice
+  const int32_t* order;  // optional work order: the c-th ray taken is order[c] (spatially coherent warps)
   int32_t n_recv;
   double rc[kMaxRecv][3];
   double rr[kMaxRecv];
