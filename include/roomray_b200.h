@@ -187,6 +187,11 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist,
                         int64_t* path_off, int32_t* path);
 rr_status rr_images_destroy(rr_images* im);
 
+/* Measurement helper (no reference counterpart): sustained L2 read
+ * bandwidth (GB/s) streaming an L2-resident buffer of `bytes`, `iters`
+ * passes in one launch; the L2 roofline denominator of bench.py. */
+rr_status rr_l2_read_gbs(rr_ctx* ctx, int64_t bytes, int32_t iters, double* gbs);
+
 /* air_beta_bands (air_absorption.cpp:59-65), 8 values. */
 rr_status rr_air_beta_bands(const rr_air* air, double* beta);
 

@@ -98,6 +98,7 @@ SIGNATURES = [
     ("rr_synthesize_trains", C.c_int, [_vp, _i64p, _vp, _vp, _d, _i32, _i64, _vp, _vp]),
     ("rr_ir_reference_length", C.c_int, [_i64, _f64p, _d, _d, _i32, C.POINTER(_i64)]),
     ("rr_band_filter", C.c_int, [_i32, _d, _i32, _f64p]),
+    ("rr_l2_read_gbs", C.c_int, [_vp, _i64, _i32, C.POINTER(_d)]),
 ]
 
 _LIB = None

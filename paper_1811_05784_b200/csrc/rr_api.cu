@@ -523,6 +523,51 @@ rr_status rr_ir_reference_length(int64_t n, const double* dist, double c, double
   });
 }
 
+// L2 read-bandwidth probe for the roofline report: every block streams the
+// whole (L2-resident) buffer `iters` times with 16-B loads, grid = 4 x SMs.
+namespace {
+__global__ void l2_read_kernel(const float4* __restrict__ buf, int64_t n4, int iters, float* __restrict__ sink) {
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 v = __ldcg(buf + i);  // L2 only (bypasses L1)
+      acc += v.x + v.y + v.z + v.w;
+    }
+  if (acc == 1234.5f) *sink = acc;  // keep the loads
+}
+}  // namespace
+
+rr_status rr_l2_read_gbs(rr_ctx* ctx, int64_t bytes, int32_t iters, double* gbs) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(gbs, "gbs");
+    if (bytes < (1 << 20) || iters < 1) rr::invalid("bytes >= 1 MiB and iters >= 1 required");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t n4 = bytes / 16;
+    rr::DevBuf<float4> buf;
+    rr::DevBuf<float> sink;
+    buf.alloc(n4, st);
+    sink.alloc(1, st);
+    RR_CUDA(cudaMemsetAsync(buf.p, 0, buf.bytes(), st));
+    const unsigned grid = static_cast<unsigned>(4 * ctx->sm_count);
+    l2_read_kernel<<<grid, 512, 0, st>>>(buf.p, n4, 1, sink.p);  // warm: pull into L2
+    cudaEvent_t e0, e1;
+    RR_CUDA(cudaEventCreate(&e0));
+    RR_CUDA(cudaEventCreate(&e1));
+    RR_CUDA(cudaEventRecord(e0, st));
+    l2_read_kernel<<<grid, 512, 0, st>>>(buf.p, n4, iters, sink.p);
+    RR_CUDA(cudaEventRecord(e1, st));
+    RR_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    RR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ctx->launches += 2;
+    *gbs = static_cast<double>(n4) * 16.0 * iters / (ms * 1e-3) / 1e9;
+  });
+}
+
 rr_status rr_air_beta_bands(const rr_air* air, double* beta) {
   return guarded([&] {
     check_ptr(air, "air");
