@@ -244,6 +244,95 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
   return best;
 }
 
+// Same contract as closest_hit, for warp-synchronous callers: a reached leaf
+// is stashed (its triangle prefetched into L1) and traversal goes on; the
+// stashed fp64 tests run together when at least LEAFT of the lanes still in
+// the loop hold one or some lane cannot continue without its test, so the
+// Moller-Trumbore code runs with most lanes active instead of ~2.  Pruning
+// uses the bound of the leaves tested so far (looser while a leaf waits), so
+// the candidate set still holds the closest face; stack entries are packed
+// (node, t) pairs, one 8-B local access per push / pop.
+template <int LEAFT>
+__device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
+                                                    const FaceTri* __restrict__ tri, D3 o, D3 d, int32_t rplane) {
+  HitResult best{0.0, -1};
+  RayF r;
+  if (!make_rayf(h, o, d, r)) return best;
+  const float kInf = __int_as_float(0x7f800000);
+  float tbest = FLT_MAX;
+  int32_t node;
+  if (h.root_ref < 0) {
+    node = h.root_ref;
+  } else {
+    const float t = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest);
+    node = (t == kInf) ? kDone : h.root_ref;
+  }
+  int2 st[kStack];
+  int sp = 0;
+  int32_t leaf = 0;  // stashed leaf (< 0) or 0
+  auto pop = [&]() {
+    node = kDone;
+    while (sp > 0) {
+      --sp;
+      const int2 e = st[sp];
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        break;
+      }
+    }
+  };
+  while (node != kDone || leaf != 0) {
+    if (node >= 0 && node != kDone) {
+      const float4* q = reinterpret_cast<const float4*>(nodes + node);
+      const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+      const int4 dd = __ldg(reinterpret_cast<const int4*>(q + 3));
+      float tl = box_enter(r, a.x, a.y, a.z, a.w, b.x, b.y, tbest);
+      float tr = box_enter(r, b.z, b.w, c.x, c.y, c.z, c.w, tbest);
+      if (dd.z == rplane) tl = kInf;
+      if (dd.w == rplane) tr = kInf;
+      const bool hl = tl != kInf, hr = tr != kInf;
+      if (hl && hr) {
+        const bool lf = tl <= tr;
+        st[sp] = make_int2(lf ? dd.y : dd.x, __float_as_int(lf ? tr : tl));
+        ++sp;
+        node = lf ? dd.x : dd.y;
+      } else if (hl) {
+        node = dd.x;
+      } else if (hr) {
+        node = dd.y;
+      } else {
+        pop();
+      }
+    }
+    if (node < 0 && leaf == 0) {
+      leaf = node;
+      prefetch_l1(tri + ~leaf);
+      pop();
+    }
+    const unsigned act = __activemask();
+    const bool must = leaf != 0 && (node < 0 || node == kDone);
+    const unsigned hv = __ballot_sync(act, leaf != 0);
+    if (__any_sync(act, must) || __popc(hv) * LEAFT >= 32 * __popc(act)) {  // >= LEAFT/32 of the loop's lanes
+      if (leaf != 0) {
+        const int32_t f = ~leaf;
+        const double t = mt_delta(tri, f, o, d);
+        if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+          best.delta = t;
+          best.face = f;
+          tbest = prune_bound(t, r.shift);
+        }
+        leaf = 0;
+        if (node < 0) {  // the leaf that waited for the slot
+          leaf = node;
+          prefetch_l1(tri + ~leaf);
+          pop();
+        }
+      }
+    }
+  }
+  return best;
+}
+
 // ---------------------------------------------------------------------------
 // fp32 triangle classification.  The fp64 Moller-Trumbore decides every hit;
 // this filter only sorts leaves into

@@ -48,7 +48,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false>
+template <int V, int MINB, bool PF = false, int PL = 0>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   extern __shared__ TNode smem_nodes[];
@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     HitResult wall;
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
+    } else if (V == 1 && PL > 0) {
+      wall = closest_hit_pl<PL>(p.hdr, p.nodes, p.tri, o, d, rplane);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
@@ -747,17 +749,22 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   auto fast = minb >= 10 ? trace_kernel<1, 10> : minb >= 8 ? trace_kernel<1, 8>
             : minb >= 6 ? trace_kernel<1, 6> : trace_kernel<1, 1>;
   // dynamic-fetch state machine (default) vs the per-ray loop (RR_DF=0)
-  // auto: the dynamic-fetch kernel wins on HBM-resident scenes (C5, 2M
-  // faces: -12 %), the per-ray loop on L2-resident ones (C2 100k: -10 %)
+  // RR_DF selects a variant for A/B timing (profiles/r1_trace_kernel_ncu.md):
+  // 0 per-ray loop, 1-6 dynamic-fetch state machine, 7 child prefetch,
+  // 8-10 per-ray loop with postponed leaf tests (default 9: C2 -8 %,
+  // C3 -17 %, C5 -14 % against 0)
   static const int df_env = [] {
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 20) ? 1 : 0);
+  const int df = df_env >= 0 ? df_env : 9;  // default: per-ray loop with postponed leaf tests
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
   if (df == 7) dfk = trace_kernel<1, 8, true>;
+  if (df == 8) dfk = trace_kernel<1, 8, false, 8>;    // postponed leaves, >= 8/32 lanes
+  if (df == 9) dfk = trace_kernel<1, 8, false, 16>;   // >= 16/32
+  if (df == 10) dfk = trace_kernel<1, 8, false, 24>;  // >= 24/32
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
