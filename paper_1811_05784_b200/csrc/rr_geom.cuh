@@ -252,7 +252,7 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
 // uses the bound of the leaves tested so far (looser while a leaf waits), so
 // the candidate set still holds the closest face; stack entries are packed
 // (node, t) pairs, one 8-B local access per push / pop.
-template <int LEAFT>
+template <int LEAFT, int STUCKT = 1>  // STUCKT < 0: at least 1/|STUCKT| of the loop's lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, D3 o, D3 d, int32_t rplane) {
   HitResult best{0.0, -1};
@@ -309,10 +309,17 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       prefetch_l1(tri + ~leaf);
       pop();
     }
+    // test when enough lanes hold a leaf, enough are stuck behind theirs, or
+    // no lane can advance without a test
     const unsigned act = __activemask();
-    const bool must = leaf != 0 && (node < 0 || node == kDone);
+    const bool can = node >= 0 && node != kDone;
+    const bool must = leaf != 0 && !can;
     const unsigned hv = __ballot_sync(act, leaf != 0);
-    if (__any_sync(act, must) || __popc(hv) * LEAFT >= 32 * __popc(act)) {  // >= LEAFT/32 of the loop's lanes
+    const unsigned mv = __ballot_sync(act, must);
+    const unsigned cv = __ballot_sync(act, can);
+    const int na = __popc(act);
+    const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
+    if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
         const int32_t f = ~leaf;
         const double t = mt_delta(tri, f, o, d);

@@ -48,7 +48,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false, int PL = 0>
+template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   extern __shared__ TNode smem_nodes[];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL>(p.hdr, p.nodes, p.tri, o, d, rplane);
+      wall = closest_hit_pl<PL, ST>(p.hdr, p.nodes, p.tri, o, d, rplane);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
@@ -751,13 +751,15 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // dynamic-fetch state machine (default) vs the per-ray loop (RR_DF=0)
   // RR_DF selects a variant for A/B timing (profiles/r1_trace_kernel_ncu.md):
   // 0 per-ray loop, 1-6 dynamic-fetch state machine, 7 child prefetch,
-  // 8-10 per-ray loop with postponed leaf tests (default 9: C2 -8 %,
-  // C3 -17 %, C5 -14 % against 0)
+  // 8-17 per-ray loop with postponed leaf tests, batched when >= LEAFT/32
+  // of the loop's lanes hold a leaf or enough lanes are stuck behind theirs
+  // (default 16: >= half stuck; C2 25.7 -> 21.4 ms, C3 2.16 -> 1.88 ms,
+  // C5 1415 -> 1170 ms against 0)
   static const int df_env = [] {
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  const int df = df_env >= 0 ? df_env : 9;  // default: per-ray loop with postponed leaf tests
+  const int df = df_env >= 0 ? df_env : 16;  // default: per-ray loop with postponed leaf tests
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
@@ -765,6 +767,13 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 8) dfk = trace_kernel<1, 8, false, 8>;    // postponed leaves, >= 8/32 lanes
   if (df == 9) dfk = trace_kernel<1, 8, false, 16>;   // >= 16/32
   if (df == 10) dfk = trace_kernel<1, 8, false, 24>;  // >= 24/32
+  if (df == 11) dfk = trace_kernel<1, 8, false, 16, 4>;  // ... or >= 4 lanes stuck
+  if (df == 12) dfk = trace_kernel<1, 8, false, 16, 8>;
+  if (df == 13) dfk = trace_kernel<1, 8, false, 16, 16>;
+  if (df == 14) dfk = trace_kernel<1, 8, false, 8, 4>;
+  if (df == 15) dfk = trace_kernel<1, 8, false, 16, -4>;  // >= 1/4 of the loop's lanes stuck
+  if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
+  if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
