@@ -252,12 +252,19 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
 // uses the bound of the leaves tested so far (looser while a leaf waits), so
 // the candidate set still holds the closest face; stack entries are packed
 // (node, t) pairs, one 8-B local access per push / pop.
-template <int LEAFT, int STUCKT = 1>  // STUCKT < 0: at least 1/|STUCKT| of the loop's lanes
+struct RegRay {  // ray held in registers
+  D3 o, d;
+  __device__ __forceinline__ D3 org() const { return o; }
+  __device__ __forceinline__ D3 dir() const { return d; }
+};
+
+template <int LEAFT, int STUCKT = 1, typename RAY = RegRay>  // STUCKT < 0: at least 1/|STUCKT| of the loop's lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
-                                                    const FaceTri* __restrict__ tri, D3 o, D3 d, int32_t rplane) {
+                                                    const FaceTri* __restrict__ tri, const RAY& ray,
+                                                    int32_t rplane) {
   HitResult best{0.0, -1};
   RayF r;
-  if (!make_rayf(h, o, d, r)) return best;
+  if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
   const float kInf = __int_as_float(0x7f800000);
   float tbest = FLT_MAX;
   int32_t node;
@@ -322,7 +329,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
         const int32_t f = ~leaf;
-        const double t = mt_delta(tri, f, o, d);
+        const double t = mt_delta(tri, f, ray.org(), ray.dir());
         if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
           best.delta = t;
           best.face = f;

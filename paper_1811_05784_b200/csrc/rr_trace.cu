@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST>(p.hdr, p.nodes, p.tri, o, d, rplane);
+      wall = closest_hit_pl<PL, ST>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
