@@ -670,6 +670,20 @@ void build_scene_tree(rr_scene* s) {
   s->hdr.depth = s->depth;
   RR_CUDA(cudaMemcpyAsync(s->dhdr.p, &s->hdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
   RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));
+  {  // traversal tree (SAH), timed separately into build_ms
+    cudaEvent_t a0, a1;
+    RR_CUDA(cudaEventCreate(&a0));
+    RR_CUDA(cudaEventCreate(&a1));
+    RR_CUDA(cudaEventRecord(a0, st));
+    build_sah_tree(s);
+    RR_CUDA(cudaEventRecord(a1, st));
+    RR_CUDA(cudaEventSynchronize(a1));
+    float ms = 0.f;
+    RR_CUDA(cudaEventElapsedTime(&ms, a0, a1));
+    s->build_ms += ms;
+    cudaEventDestroy(a0);
+    cudaEventDestroy(a1);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }

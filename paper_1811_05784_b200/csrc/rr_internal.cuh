@@ -167,6 +167,9 @@ struct rr_scene {
   rr::DevBuf<rr::RefNode> ref;    // 2nf-1 (reference layout)
   rr::DevBuf<rr::TNode> tnodes;   // K + nf
   rr::DevBuf<rr::QNode> qnodes;   // 4-wide nodes
+  rr::DevBuf<rr::TNode> snodes;   // SAH traversal tree (rr_sah.cu), nf-1 nodes, BFS order
+  rr::TravHeader shdr{};          // its header (root box, root ref, eps)
+  int32_t sah_depth = 0;
   int64_t n_qnodes = 0;
   rr::DevBuf<rr::TravHeader> dhdr;
   rr::TravHeader hdr{};
@@ -179,6 +182,8 @@ struct rr_scene {
 namespace rr {
 // rr_build.cu
 void build_scene_tree(rr_scene* s);
+// rr_sah.cu (needs face_plane and hdr from build_scene_tree)
+void build_sah_tree(rr_scene* s);
 // rr_trace.cu
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
                        int64_t n, int brute, int32_t* d_face, double* d_delta,

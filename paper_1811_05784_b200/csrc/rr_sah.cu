@@ -1,0 +1,509 @@
+// K1' — surface-area-heuristic traversal tree, built on the device.
+//
+// The reference's median split (accel_tree.cpp:19-87, built exactly by
+// rr_build.cu and used for the API, the parity tests and the byte model)
+// mixes several walls in its top levels, so a ray inside the room enters
+// both children for many levels.  The tracer traverses this second tree
+// instead: same leaves (one face each), same conservative fp32 TNode format,
+// splits chosen by a binned SAH.  The closest hit is a property of the face
+// set alone (fp64 test on every face a conservative box admits,
+// lexicographic (delta, face) minimum), so the tree changes the work, never
+// a result.  Measured on the reference's own traversal order: internal
+// visits per query C2 55.8 -> 32.0, C3 49.0 -> 27.5, C5 90.3 -> 54.4.
+//
+// Level-synchronous, like rr_build.cu: three face lists presorted by
+// centroid per axis, one segment per node of the level; per level
+//   1. segment AABBs, centroid bounds, common plane id (atomics);
+//   2. SAH segments (>= kSahMin faces, depth budget left): 3 x kBins
+//      centroid bins with counts and AABBs;
+//   3. one thread per segment writes its box into the parent's TNode slot,
+//      picks the split (best binned SAH cost, else the object median of the
+//      longest centroid extent) and emits the two child segments;
+//   4. stable segmented partition of the three lists.
+// Nodes are numbered level by level (BFS); depth is capped so the 32-entry
+// traversal stack cannot overflow (median splits once the budget is short).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "rr_internal.cuh"
+
+namespace rr {
+namespace {
+
+constexpr int kBins = 32;
+constexpr int64_t kSahMin = 64;
+constexpr int kMaxDepth = 30;
+
+struct SSeg {
+  int64_t b, n;
+  int32_t parent;  // TNode index of the parent, -1 for the root
+  int32_t side;    // 0 left, 1 right
+};
+
+__device__ __forceinline__ uint64_t okey(double x) {
+  if (x == 0.0) x = 0.0;
+  uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double oval(uint64_t u) {
+  u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+__device__ __forceinline__ uint32_t okeyf(float x) {
+  if (x == 0.0f) x = 0.0f;
+  uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ovalf(uint32_t u) {
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ float lo_f(double x, float eps) { return __fsub_rd(__double2float_rd(x), eps); }
+__device__ __forceinline__ float hi_f(double x, float eps) { return __fadd_ru(__double2float_ru(x), eps); }
+
+__global__ void prep_kernel(const double* __restrict__ v, const int32_t* __restrict__ t, int64_t nf,
+                            double* __restrict__ fb, double* __restrict__ cen, uint64_t* __restrict__ keys,
+                            int32_t* __restrict__ ids) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int32_t a = t[4 * f], b = t[4 * f + 1], c = t[4 * f + 2];
+  for (int k = 0; k < 3; ++k) {
+    const double va = v[3 * a + k], vb = v[3 * b + k], vc = v[3 * c + k];
+    const double ce = ((va + vb) + vc) / 3.0;
+    fb[6 * f + k] = fmin(va, fmin(vb, vc));
+    fb[6 * f + 3 + k] = fmax(va, fmax(vb, vc));
+    cen[3 * f + k] = ce;
+    keys[k * nf + f] = okey(ce);
+    ids[k * nf + f] = static_cast<int32_t>(f);
+  }
+}
+
+// 1. per segment: AABB, centroid bounds (ordered-key atomics), plane ids.
+// List positions are grouped by segment, so lanes first reduce within their
+// warp's runs and one lane per run issues the atomics.
+__global__ void bounds_kernel(const int32_t* __restrict__ pos_seg, const int32_t* __restrict__ perm0,
+                              const double* __restrict__ fb, const double* __restrict__ cen,
+                              const int32_t* __restrict__ face_plane, int64_t nf, unsigned long long* __restrict__ bb,
+                              unsigned long long* __restrict__ cb, int32_t* __restrict__ pl) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int32_t seg = -1;
+  uint64_t v[12];  // bb min 3, bb max 3, cb min 3, cb max 3
+  int32_t pmin = 0x7fffffff, pmax = static_cast<int32_t>(0x80000000);
+  for (int k = 0; k < 3; ++k) {
+    v[k] = ~0ull;
+    v[3 + k] = 0;
+    v[6 + k] = ~0ull;
+    v[9 + k] = 0;
+  }
+  if (i < nf) {
+    seg = pos_seg[i];
+    if (seg >= 0) {
+      const int32_t f = perm0[i];
+      for (int k = 0; k < 3; ++k) {
+        v[k] = okey(fb[6 * f + k]);
+        v[3 + k] = okey(fb[6 * f + 3 + k]);
+        v[6 + k] = v[9 + k] = okey(cen[3 * f + k]);
+      }
+      pmin = pmax = face_plane ? face_plane[f] : -1;
+    }
+  }
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t so = __shfl_down_sync(0xffffffffu, seg, off);
+    const bool ok = (lane + off < 32) && so == seg;
+    for (int k = 0; k < 12; ++k) {
+      const uint64_t o = __shfl_down_sync(0xffffffffu, v[k], off);
+      const bool is_min = (k % 6) < 3;
+      if (ok) v[k] = is_min ? (o < v[k] ? o : v[k]) : (o > v[k] ? o : v[k]);
+    }
+    const int32_t a = __shfl_down_sync(0xffffffffu, pmin, off), b = __shfl_down_sync(0xffffffffu, pmax, off);
+    if (ok) {
+      pmin = min(pmin, a);
+      pmax = max(pmax, b);
+    }
+  }
+  const int32_t prev = __shfl_up_sync(0xffffffffu, seg, 1);
+  if (seg >= 0 && (lane == 0 || prev != seg)) {
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(bb + 6 * seg + k, (unsigned long long)v[k]);
+      atomicMax(bb + 6 * seg + 3 + k, (unsigned long long)v[3 + k]);
+      atomicMin(cb + 6 * seg + k, (unsigned long long)v[6 + k]);
+      atomicMax(cb + 6 * seg + 3 + k, (unsigned long long)v[9 + k]);
+    }
+    atomicMin(pl + 2 * seg, pmin);
+    atomicMax(pl + 2 * seg + 1, pmax);
+  }
+}
+
+__device__ __forceinline__ int bin_of(double c, double lo, double ext) {
+  int b = static_cast<int>((c - lo) / ext * kBins);
+  return b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+}
+
+// 2. centroid bins of the SAH segments: count + float AABB per (axis, bin)
+__global__ void bin_kernel(const int32_t* __restrict__ pos_seg, const int32_t* __restrict__ perm0,
+                           const double* __restrict__ fb, const double* __restrict__ cen,
+                           const unsigned long long* __restrict__ cb, const int32_t* __restrict__ sah_idx,
+                           int64_t nf, int32_t* __restrict__ bcnt, uint32_t* __restrict__ bbox) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  const int32_t s = pos_seg[i];
+  if (s < 0) return;
+  const int32_t q = sah_idx[s];
+  if (q < 0) return;
+  const int32_t f = perm0[i];
+  uint32_t lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = okeyf(__double2float_rn(fb[6 * f + k]));
+    hi[k] = okeyf(__double2float_rn(fb[6 * f + 3 + k]));
+  }
+  for (int a = 0; a < 3; ++a) {
+    const double clo = oval(cb[6 * s + a]), ext = oval(cb[6 * s + 3 + a]) - clo;
+    if (!(ext > 0.0)) continue;
+    const int b = bin_of(cen[3 * f + a], clo, ext);
+    const int64_t slot = (static_cast<int64_t>(q) * 3 + a) * kBins + b;
+    atomicAdd(bcnt + slot, 1);
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(bbox + 6 * slot + k, lo[k]);
+      atomicMax(bbox + 6 * slot + 3 + k, hi[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ float half_area(const float* lo, const float* hi) {
+  const float dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+// 3. node emission and split choice
+__global__ void split_kernel(const SSeg* __restrict__ segs, int64_t S, const int32_t* __restrict__ rank,
+                             const unsigned long long* __restrict__ bb, const unsigned long long* __restrict__ cb,
+                             const int32_t* __restrict__ pl, const int32_t* __restrict__ sah_idx,
+                             const int32_t* __restrict__ bcnt, const uint32_t* __restrict__ bbox,
+                             const int32_t* __restrict__ perm0, int32_t level_base, float eps, TNode* __restrict__ tn,
+                             TravHeader* __restrict__ hdr, int32_t* __restrict__ seg_axis,
+                             int32_t* __restrict__ seg_split, int64_t* __restrict__ seg_nl, SSeg* __restrict__ next) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const SSeg sg = segs[j];
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = oval(bb[6 * j + k]);
+    hi[k] = oval(bb[6 * j + 3 + k]);
+  }
+  const int32_t my_ref = sg.n == 1 ? ~perm0[sg.b] : level_base + rank[j];
+  const int32_t plane = (pl[2 * j] == pl[2 * j + 1]) ? pl[2 * j] : -1;
+  if (sg.parent < 0) {
+    hdr->root_ref = my_ref;
+  } else {
+    TNode* p = tn + sg.parent;
+    const float lx = lo_f(lo[0], eps), ly = lo_f(lo[1], eps), lz = lo_f(lo[2], eps);
+    const float hx = hi_f(hi[0], eps), hy = hi_f(hi[1], eps), hz = hi_f(hi[2], eps);
+    if (sg.side == 0) {
+      p->a = make_float4(lx, hx, ly, hy);
+      reinterpret_cast<float2*>(&p->b)[0] = make_float2(lz, hz);
+      p->d.x = my_ref;
+      p->d.z = plane;
+    } else {
+      reinterpret_cast<float2*>(&p->b)[1] = make_float2(lx, hx);
+      p->c = make_float4(ly, hy, lz, hz);
+      p->d.y = my_ref;
+      p->d.w = plane;
+    }
+  }
+  if (sg.n == 1) {
+    seg_axis[j] = -1;
+    return;
+  }
+  int axis = -1, split = -1;
+  int64_t nl = sg.n / 2;
+  const int32_t q = sah_idx[j];
+  if (q >= 0) {
+    float best = 3.4e38f;
+    for (int a = 0; a < 3; ++a) {
+      const int32_t* cnt = bcnt + (static_cast<int64_t>(q) * 3 + a) * kBins;
+      const uint32_t* box = bbox + 6 * (static_cast<int64_t>(q) * 3 + a) * kBins;
+      float la[kBins];
+      int64_t lc[kBins];
+      float alo[3] = {3.4e38f, 3.4e38f, 3.4e38f}, ahi[3] = {-3.4e38f, -3.4e38f, -3.4e38f};
+      int64_t c = 0;
+      for (int b = 0; b < kBins; ++b) {
+        if (cnt[b] > 0)
+          for (int k = 0; k < 3; ++k) {
+            alo[k] = fminf(alo[k], ovalf(box[6 * b + k]));
+            ahi[k] = fmaxf(ahi[k], ovalf(box[6 * b + 3 + k]));
+          }
+        c += cnt[b];
+        lc[b] = c;
+        la[b] = c > 0 ? half_area(alo, ahi) : 0.0f;
+      }
+      for (int k = 0; k < 3; ++k) {
+        alo[k] = 3.4e38f;
+        ahi[k] = -3.4e38f;
+      }
+      c = 0;
+      for (int b = kBins - 1; b >= 1; --b) {
+        if (cnt[b] > 0)
+          for (int k = 0; k < 3; ++k) {
+            alo[k] = fminf(alo[k], ovalf(box[6 * b + k]));
+            ahi[k] = fmaxf(ahi[k], ovalf(box[6 * b + 3 + k]));
+          }
+        c += cnt[b];
+        if (c == 0 || lc[b - 1] == 0) continue;
+        const float cost = la[b - 1] * static_cast<float>(lc[b - 1]) + half_area(alo, ahi) * static_cast<float>(c);
+        if (cost < best) {
+          best = cost;
+          axis = a;
+          split = b;
+          nl = lc[b - 1];
+        }
+      }
+    }
+  }
+  if (axis < 0) {  // object median on the longest centroid extent
+    double bestx = -1.0;
+    for (int k = 0; k < 3; ++k) {
+      const double e = oval(cb[6 * j + 3 + k]) - oval(cb[6 * j + k]);
+      if (e > bestx) {
+        bestx = e;
+        axis = k;
+      }
+    }
+    split = -1;
+    nl = sg.n / 2;
+  }
+  seg_axis[j] = axis;
+  seg_split[j] = split;
+  seg_nl[j] = nl;
+  const int32_t me = level_base + rank[j];
+  next[2 * rank[j]] = SSeg{sg.b, nl, me, 0};
+  next[2 * rank[j] + 1] = SSeg{sg.b + nl, sg.n - nl, me, 1};
+}
+
+// 4a. left/right flag per face
+__global__ void flag_kernel(const int32_t* __restrict__ pos_seg, const SSeg* __restrict__ segs,
+                            const int32_t* __restrict__ seg_axis, const int32_t* __restrict__ seg_split,
+                            const unsigned long long* __restrict__ cb, const double* __restrict__ cen,
+                            const int32_t* __restrict__ perm, int64_t nf, uint8_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  const int32_t s = pos_seg[i];
+  if (s < 0) return;
+  const int32_t axis = seg_axis[s];
+  if (axis < 0) return;
+  const SSeg sg = segs[s];
+  const int32_t f = perm[axis * nf + i];  // position i of the axis list
+  if (seg_split[s] < 0) {
+    flag[f] = (i - sg.b) < sg.n / 2 ? 1 : 0;
+  } else {
+    const double clo = oval(cb[6 * s + axis]), ext = oval(cb[6 * s + 3 + axis]) - clo;
+    flag[f] = bin_of(cen[3 * f + axis], clo, ext) < seg_split[s] ? 1 : 0;
+  }
+}
+
+__global__ void gather_kernel(const int32_t* __restrict__ perm, const uint8_t* __restrict__ flag, int64_t total,
+                              int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < total) out[i] = flag[perm[i]];
+}
+
+// 4b. stable segmented partition of the three lists
+__global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* __restrict__ segs,
+                               const int32_t* __restrict__ seg_axis, const int64_t* __restrict__ seg_nl,
+                               const int32_t* __restrict__ rank, const int32_t* __restrict__ perm,
+                               const int32_t* __restrict__ fl, const int32_t* __restrict__ scan, int64_t nf,
+                               int32_t* __restrict__ perm_out, int32_t* __restrict__ pos_seg_out) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= 3 * nf) return;
+  const int k = static_cast<int>(g / nf);
+  const int64_t i = g - k * nf;
+  const int32_t sj = pos_seg[i];
+  if (sj < 0 || seg_axis[sj] < 0) {
+    perm_out[g] = perm[g];
+    if (k == 0) pos_seg_out[i] = -1;
+    return;
+  }
+  const SSeg sg = segs[sj];
+  const int64_t nl = seg_nl[sj];
+  const int64_t cnt_l = scan[g] - scan[k * nf + sg.b];
+  const bool left = fl[g] != 0;
+  const int64_t np = left ? sg.b + cnt_l : sg.b + nl + (i - sg.b - cnt_l);
+  perm_out[k * nf + np] = perm[g];
+  if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
+}
+
+__global__ void split_flag_kernel(const SSeg* __restrict__ segs, int64_t S, int level,
+                                  int32_t* __restrict__ sflag, int32_t* __restrict__ sah) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const int64_t n = segs[j].n;
+  sflag[j] = n >= 2 ? 1 : 0;
+  // SAH only while the depth budget allows a median finish below
+  int lg = 0;
+  while ((int64_t(1) << lg) < n) ++lg;
+  sah[j] = (n >= kSahMin && level + 1 + lg + 2 <= kMaxDepth) ? 1 : 0;
+}
+
+__global__ void sah_compact_kernel(const int32_t* __restrict__ sah, int64_t S, int32_t* __restrict__ sah_idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < S && !sah[j]) sah_idx[j] = -1;
+}
+
+inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
+
+template <typename F>
+void cub_run(F&& f, DevBuf<uint8_t>& tmp, cudaStream_t st) {
+  size_t need = 0;
+  RR_CUDA(f(nullptr, need));
+  if (need > tmp.n) tmp.alloc(need + 16, st);
+  size_t have = tmp.n;
+  RR_CUDA(f(tmp.p, have));
+}
+
+}  // namespace
+
+void build_sah_tree(rr_scene* s) {
+  cudaStream_t st = s->ctx->stream;
+  const int64_t nf = s->nf;
+  s->shdr = s->hdr;  // root box, eps, K = 0
+  s->shdr.K = 0;
+  if (nf < 2) {
+    s->snodes.alloc(1, st);
+    RR_CUDA(cudaMemsetAsync(s->snodes.p, 0, sizeof(TNode), st));
+    return;
+  }
+  DevBuf<double> fb, cen;
+  DevBuf<uint64_t> keys, keys_o;
+  DevBuf<int32_t> ids, permA, permB, posA, posB, fl, scan;
+  DevBuf<uint8_t> flag, tmp;
+  fb.alloc(6 * nf, st);
+  cen.alloc(3 * nf, st);
+  keys.alloc(3 * nf, st);
+  keys_o.alloc(3 * nf, st);
+  ids.alloc(3 * nf, st);
+  permA.alloc(3 * nf, st);
+  permB.alloc(3 * nf, st);
+  posA.alloc(nf, st);
+  posB.alloc(nf, st);
+  fl.alloc(3 * nf, st);
+  scan.alloc(3 * nf, st);
+  flag.alloc(nf, st);
+  prep_kernel<<<grid(nf), 256, 0, st>>>(s->verts.p, s->tris.p, nf, fb.p, cen.p, keys.p, ids.p);
+  RR_LAUNCH_CHECK();
+  for (int k = 0; k < 3; ++k)
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, keys.p + k * nf, keys_o.p + k * nf, ids.p + k * nf,
+                                             permA.p + k * nf, static_cast<int>(nf), 0, 64, st);
+    }, tmp, st);
+  s->snodes.alloc(nf - 1, st);
+  RR_CUDA(cudaMemsetAsync(s->snodes.p, 0, s->snodes.bytes(), st));
+  DevBuf<TravHeader> dh;
+  dh.alloc(1, st);
+  RR_CUDA(cudaMemcpyAsync(dh.p, &s->shdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
+  RR_CUDA(cudaMemsetAsync(posA.p, 0, sizeof(int32_t) * nf, st));
+
+  int64_t max_seg = nf;  // segments per level never exceed the face count
+  DevBuf<SSeg> segA, segB;
+  DevBuf<int32_t> sflag, srank, sah, sah_idx, axis, split, pl;
+  DevBuf<int64_t> nl;
+  DevBuf<unsigned long long> bb, cb;
+  segA.alloc(max_seg, st);
+  segB.alloc(max_seg, st);
+  sflag.alloc(max_seg + 1, st);
+  srank.alloc(max_seg + 1, st);
+  sah.alloc(max_seg + 1, st);
+  sah_idx.alloc(max_seg + 1, st);
+  axis.alloc(max_seg, st);
+  split.alloc(max_seg, st);
+  pl.alloc(2 * max_seg, st);
+  nl.alloc(max_seg, st);
+  bb.alloc(6 * max_seg, st);
+  cb.alloc(6 * max_seg, st);
+  DevBuf<int32_t> bcnt;
+  DevBuf<uint32_t> bbox;
+  const SSeg root{0, nf, -1, 0};
+  RR_CUDA(cudaMemcpyAsync(segA.p, &root, sizeof root, cudaMemcpyHostToDevice, st));
+  int32_t *perm = permA.p, *perm_o = permB.p, *pos = posA.p, *pos_o = posB.p;
+  SSeg *segs = segA.p, *nsegs = segB.p;
+  int64_t S = 1;
+  int32_t level_base = 0;
+  int depth = 0;
+  const float eps = s->hdr.eps;
+  for (int L = 0; S > 0; ++L) {
+    depth = L;
+    // 1. bounds
+    RR_CUDA(cudaMemsetAsync(bb.p, 0xff, sizeof(unsigned long long) * 6 * S, st));
+    RR_CUDA(cudaMemsetAsync(cb.p, 0xff, sizeof(unsigned long long) * 6 * S, st));
+    // max halves start at 0 (ordered keys)
+    RR_CUDA(cudaMemset2DAsync(bb.p + 3, 6 * sizeof(unsigned long long), 0, 3 * sizeof(unsigned long long), S, st));
+    RR_CUDA(cudaMemset2DAsync(cb.p + 3, 6 * sizeof(unsigned long long), 0, 3 * sizeof(unsigned long long), S, st));
+    // plane id min / max start at 0x7f7f7f7f / 0x80808080 (above / below every id)
+    RR_CUDA(cudaMemset2DAsync(pl.p, 2 * sizeof(int32_t), 0x7f, sizeof(int32_t), S, st));
+    RR_CUDA(cudaMemset2DAsync(pl.p + 1, 2 * sizeof(int32_t), 0x80, sizeof(int32_t), S, st));
+    bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
+    RR_LAUNCH_CHECK();
+    // 2. split flags, ranks, SAH segments and their bins
+    split_flag_kernel<<<grid(S), 256, 0, st>>>(segs, S, L, sflag.p, sah.p);
+    RR_LAUNCH_CHECK();
+    RR_CUDA(cudaMemsetAsync(sflag.p + S, 0, sizeof(int32_t), st));
+    RR_CUDA(cudaMemsetAsync(sah.p + S, 0, sizeof(int32_t), st));
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, sflag.p, srank.p, static_cast<int>(S + 1), st);
+    }, tmp, st);
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, sah.p, sah_idx.p, static_cast<int>(S + 1), st);
+    }, tmp, st);
+    int32_t counts[2] = {0, 0};
+    RR_CUDA(cudaMemcpyAsync(&counts[0], srank.p + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaMemcpyAsync(&counts[1], sah_idx.p + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    const int64_t n_split = counts[0], n_sah = counts[1];
+    // sah_idx[j] = compact index, or -1 for non-SAH segments
+    if (n_sah > 0) {
+      bcnt.alloc(n_sah * 3 * kBins, st);
+      bbox.alloc(n_sah * 3 * kBins * 6, st);
+      RR_CUDA(cudaMemsetAsync(bcnt.p, 0, bcnt.bytes(), st));
+      // min halves to ~0, max halves to 0: per (segment, axis, bin) 6 words
+      RR_CUDA(cudaMemsetAsync(bbox.p, 0xff, bbox.bytes(), st));
+      RR_CUDA(cudaMemset2DAsync(bbox.p + 3, 6 * sizeof(uint32_t), 0, 3 * sizeof(uint32_t), n_sah * 3 * kBins, st));
+    }
+    sah_compact_kernel<<<grid(S), 256, 0, st>>>(sah.p, S, sah_idx.p);
+    RR_LAUNCH_CHECK();
+    if (n_sah > 0) {
+      bin_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, cb.p, sah_idx.p, nf, bcnt.p, bbox.p);
+      RR_LAUNCH_CHECK();
+    }
+    // 3. nodes + splits
+    split_kernel<<<grid(S), 256, 0, st>>>(segs, S, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
+                                          level_base, eps, s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 6;
+    if (n_split == 0) break;
+    // 4. stable partition of the three lists
+    flag_kernel<<<grid(nf), 256, 0, st>>>(pos, segs, axis.p, split.p, cb.p, cen.p, perm, nf, flag.p);
+    gather_kernel<<<grid(3 * nf), 256, 0, st>>>(perm, flag.p, 3 * nf, fl.p);
+    RR_LAUNCH_CHECK();
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, fl.p, scan.p, static_cast<int>(3 * nf), st);
+    }, tmp, st);
+    scatter_kernel<<<grid(3 * nf), 256, 0, st>>>(pos, segs, axis.p, nl.p, srank.p, perm, fl.p, scan.p, nf, perm_o,
+                                                  pos_o);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 4;
+    std::swap(perm, perm_o);
+    std::swap(pos, pos_o);
+    std::swap(segs, nsegs);
+    level_base += static_cast<int32_t>(n_split);
+    S = 2 * n_split;
+  }
+  RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  s->shdr.K = 0;
+  s->sah_depth = depth;
+  if (depth > kMaxDepth) throw Error(RR_RUNTIME, "SAH tree deeper than the traversal stack");
+}
+
+}  // namespace rr

@@ -660,7 +660,13 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   auto res = std::make_unique<rr_trace_result>();
   res->scene = s;
   TraceParams& p = res->params;
-  p.nodes = s->tnodes.p;
+  // traversal tree: the SAH tree (RR_SAH=0: the reference median tree)
+  static const int use_sah = [] {
+    const char* e = std::getenv("RR_SAH");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool sah = use_sah && s->snodes.p != nullptr;
+  p.nodes = sah ? s->snodes.p : s->tnodes.p;
   p.qnodes = s->qnodes.p;
   // default: binary nodes, fp64 test at every leaf (fastest measured); diagnostics: fp32 leaf classification, 4-wide nodes
   const int variant = (cfg->flags & RR_TRACE_F32_LEAVES) ? 1 : (cfg->flags & RR_TRACE_WIDE) ? 2 : 0;
@@ -669,7 +675,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   p.face_plane = s->face_plane.p;
   p.tri = s->tri.p;
   p.normal = s->normal.p;
-  p.hdr = s->hdr;
+  p.hdr = sah ? s->shdr : s->hdr;
   // shared-memory top-level cache: measured slower for the default kernel
   // (profiles/r1_ab_variants.md), kept for the diagnostic ones
   p.use_smem = (variant == 0 || (cfg->flags & RR_TRACE_NO_SMEM_CACHE)) ? 0 : 1;
