@@ -306,11 +306,22 @@ def run_ours(args):
     kern_s = sum(kern_ms) / 1e3
     achieved = model["B_rb"] * bounces / kern_s / 1e9
     traffic = model.get("ncu_dram_bytes_per_launch")
+    # the same byte model on the work this kernel actually does (SAH tree,
+    # conservative boxes, coplanar culling): one instrumented, untimed trace
+    cnt = rr.trace_device(tree, src, recv, cfg, flags=_lib.RR_TRACE_COUNT, **shard).stats
+    b_bar = cnt.ray_bounces / max(cnt.n_rays, 1)
+    v_rb, l_rb = cnt.node_visits / cnt.ray_bounces, cnt.leaf_tests / cnt.ray_bounces
+    b_kernel = 64 * v_rb + 48 * l_rb + 48 + 4 + 128 / b_bar
     # L2 roofline of the same byte model (the C1-C3 scenes live in the 126 MB L2)
     l2 = C.c_double()
     _lib.check(lib.rr_l2_read_gbs(ctx.h, 48 << 20, 40, C.byref(l2)))
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "l2_peak_measured": round(l2.value, 1), "l2_frac": round(achieved / l2.value, 4),
+            "kernel_model": {"node_visits_per_rb": round(v_rb, 2), "leaf_tests_per_rb": round(l_rb, 2),
+                             "bytes_per_rb": round(b_kernel, 1),
+                             "achieved": round(b_kernel * bounces / kern_s / 1e9, 1),
+                             "frac_hbm": round(b_kernel * bounces / kern_s / 1e9 / peak, 4),
+                             "frac_l2": round(b_kernel * bounces / kern_s / 1e9 / l2.value, 4)},
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
             "bytes_per_ray_bounce": round(model["B_rb"], 1), "kernel_ms_per_step": round(1e3 * kern_s / args.steps, 3),
             "kernel_share_of_step": round(sum(kern_ms) / my_ms, 3)}

@@ -74,6 +74,7 @@ typedef struct {
 #define RR_TRACE_KEEP_UNSORTED 2 /* skip the capture sort (timing only) */
 #define RR_TRACE_F32_LEAVES 4    /* diagnostic: fp32 leaf classification + fp64 resolution */
 #define RR_TRACE_WIDE 8          /* diagnostic: traverse the 4-wide collapse */
+#define RR_TRACE_COUNT 16        /* instrumented kernel: count node visits and leaf tests */
 
 /* Statistics of a trace (TraceResult, tracer.hpp:22-29). */
 typedef struct {
@@ -86,6 +87,8 @@ typedef struct {
   int64_t total_history; /* sum of capture face-path lengths */
   int64_t ray_bounces;   /* nearest-hit queries executed on live rays */
   int64_t n_rays;        /* rays traced by this call */
+  int64_t node_visits;   /* internal-node visits (RR_TRACE_COUNT), else -1 */
+  int64_t leaf_tests;    /* fp64 triangle tests (RR_TRACE_COUNT), else -1 */
 } rr_trace_stats;
 
 /* AirModel (air_absorption.hpp:10-23). */

@@ -19,6 +19,7 @@ RR_TRACE_NO_SMEM_CACHE = 1
 RR_TRACE_KEEP_UNSORTED = 2
 RR_TRACE_F32_LEAVES = 4
 RR_TRACE_WIDE = 8
+RR_TRACE_COUNT = 16
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
@@ -51,7 +52,7 @@ class TraceConfig(C.Structure):
 class TraceStats(C.Structure):
     _fields_ = [("iterations", _i32), ("truncated", _i32), ("escaped", _i64), ("out_of_range", _i64),
                 ("max_range", _d), ("n_captures", _i64), ("total_history", _i64), ("ray_bounces", _i64),
-                ("n_rays", _i64)]
+                ("n_rays", _i64), ("node_visits", _i64), ("leaf_tests", _i64)]
 
 
 class Air(C.Structure):

@@ -258,10 +258,11 @@ struct RegRay {  // ray held in registers
   __device__ __forceinline__ D3 dir() const { return d; }
 };
 
-template <int LEAFT, int STUCKT = 1, typename RAY = RegRay>  // STUCKT < 0: at least 1/|STUCKT| of the loop's lanes
+// CNT: count internal-node visits and leaf tests into *cnt (instrumented build)
+template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false>  // STUCKT < 0: >= 1/|STUCKT| of lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
-                                                    int32_t rplane) {
+                                                    int32_t rplane, unsigned long long* cnt = nullptr) {
   HitResult best{0.0, -1};
   RayF r;
   if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
@@ -290,6 +291,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   };
   while (node != kDone || leaf != 0) {
     if (node >= 0 && node != kDone) {
+      if (CNT) ++cnt[0];
       const float4* q = reinterpret_cast<const float4*>(nodes + node);
       const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
       const int4 dd = __ldg(reinterpret_cast<const int4*>(q + 3));
@@ -329,6 +331,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
         const int32_t f = ~leaf;
+        if (CNT) ++cnt[1];
         const double t = mt_delta(tri, f, ray.org(), ray.dir());
         if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
           best.delta = t;

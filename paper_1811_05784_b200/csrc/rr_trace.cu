@@ -48,7 +48,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1>
+template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   extern __shared__ TNode smem_nodes[];
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   double path = 0.0;
   int32_t steps = 0, bounces = 0, rplane = -2;
   unsigned long long st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
+  unsigned long long st_cnt[2] = {0, 0};  // node visits, leaf tests (CNT)
   int32_t st_max = 0;
 
   for (;;) {
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane);
+      wall = closest_hit_pl<PL, ST, RegRay, CNT>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
@@ -205,6 +206,16 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     atomicAdd(p.stats + 2, st_oor);
     atomicAdd(p.stats + 3, st_alive);
     atomicMax(p.stats + 4, (unsigned long long)st_max);
+  }
+  if (CNT) {
+    for (int off = 16; off > 0; off >>= 1) {
+      st_cnt[0] += __shfl_xor_sync(0xffffffffu, st_cnt[0], off);
+      st_cnt[1] += __shfl_xor_sync(0xffffffffu, st_cnt[1], off);
+    }
+    if (lane == 0) {
+      atomicAdd(p.stats + 5, st_cnt[0]);
+      atomicAdd(p.stats + 6, st_cnt[1]);
+    }
   }
 }
 
@@ -734,7 +745,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   p.hist = res->hist.p;
 
   DevBuf<unsigned long long> counters;
-  counters.alloc(8, st);
+  counters.alloc(10, st);
   p.cap_count = counters.p;
   p.ray_counter = counters.p + 1;
   p.stats = counters.p + 2;
@@ -780,6 +791,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 15) dfk = trace_kernel<1, 8, false, 16, -4>;  // >= 1/4 of the loop's lanes stuck
   if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
   if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
+  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true>;
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
@@ -821,12 +833,12 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   cudaEvent_t e0, e1;
   RR_CUDA(cudaEventCreate(&e0));
   RR_CUDA(cudaEventCreate(&e1));
-  unsigned long long hc[8];
+  unsigned long long hc[10];
   for (int attempt = 0; attempt < 2; ++attempt) {
     caps.alloc(capacity, st);
     p.caps = caps.p;
     p.cap_capacity = capacity;
-    RR_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * 8, st));
+    RR_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * 10, st));
     RR_CUDA(cudaEventRecord(e0, st));
     kernel<<<grid, 128, smem, st>>>(p);
     RR_LAUNCH_CHECK();
@@ -850,6 +862,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   S.max_range = p.max_range;
   S.n_captures = nc;
   S.n_rays = count;
+  S.node_visits = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[7]) : -1;
+  S.leaf_tests = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[8]) : -1;
   s->caps_per_ray = static_cast<double>(nc) / static_cast<double>(std::max<int64_t>(count, 1) * n_recv);
 
   // ---- sort captures by (receiver, ray, order) and materialise

@@ -45,7 +45,7 @@ struct TraceParams {
   unsigned long long* cap_count;
   int64_t cap_capacity;
   unsigned long long* ray_counter;
-  unsigned long long* stats;  // 0 bounces, 1 escaped, 2 out_of_range, 3 alive, 4 max steps
+  unsigned long long* stats;  // 0 bounces, 1 escaped, 2 out_of_range, 3 alive, 4 max steps, 5 visits, 6 leaves
 };
 
 }  // namespace rr
