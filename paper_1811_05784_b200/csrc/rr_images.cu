@@ -420,7 +420,9 @@ __global__ void resolve_round_kernel(ImgTmp t, const double* __restrict__ mult, 
         if (start < 0) continue;
         for (int64_t q = start; q < n && skeys[q] == key; ++q) {
           const int32_t j = cand.id[q];
-          if (j >= i || j >= best_anchor) break;  // ids ascend inside a run: no later entry can win
+          // ids ascend inside a run: once past i, the best anchor or the
+          // smallest undecided pred seen, no later entry can change the outcome
+          if (j >= i || j >= best_anchor || j >= min_undet) break;
           if (cand.order[q] != oi) continue;
           const D3 pj = ld3(cand.pos, q);
           if (static_cast<long long>(floor(pj.x / cs)) != cx || static_cast<long long>(floor(pj.y / cs)) != cy ||
@@ -765,7 +767,10 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
       ctx->launches++;
       RR_CUDA(cudaMemcpyAsync(h, progress.p, sizeof h, cudaMemcpyDeviceToHost, st));
       RR_CUDA(cudaStreamSynchronize(st));
-      if (!h[1]) break;  // nobody left waiting
+      if (!h[1]) {  // nobody left waiting
+        if (std::getenv("RR_TIMING")) std::fprintf(stderr, "[rr timing] merge rounds %d\n", round + 1);
+        break;
+      }
       if (!h[0]) throw Error(RR_RUNTIME, "coplanar merge made no progress");  // impossible: preds are smaller
     }
     tm.mark("merge: resolve");
