@@ -225,6 +225,31 @@ rr_status rr_synthesize_trains(rr_ctx* ctx, const int64_t* band_off,
                                const double* time, const double* amplitude,
                                double fs, int32_t taps, int64_t length,
                                double* band_ir, double* broadband);
+/* ---------------------------------------------------------------- metrics
+ * PerceptiveFactors / MetricValue (metrics.hpp:30-48): per band EDT, T30
+ * (least-squares decay fits of the Schroeder curve), SPL, C80, D50, Ts. */
+typedef struct {
+  double value;
+  int32_t reliable;
+} rr_metric;
+
+typedef struct {
+  rr_metric edt_s, t30_s, spl_db, c80_db, d50_pct, ts_ms;
+} rr_factors;
+
+/* factors(const PulseTrains&) (metrics.hpp:56-60) on the device; out[0..7]
+ * per band, out[8] the 500 Hz / 1 kHz average ("mid").  Trains as in
+ * rr_synthesize_trains (host arrays, band_off 9 entries). */
+rr_status rr_band_factors(rr_ctx* ctx, const int64_t* band_off,
+                          const double* time, const double* amplitude,
+                          rr_factors* out);
+/* The same for the trains of an image set (build_pulse_trains: t = d / c,
+ * amplitude sqrt(E_b)); dist / energy host or device arrays (UVA). */
+rr_status rr_factors_from_images(rr_ctx* ctx, int64_t n, const double* dist,
+                                 const double* energy, double c,
+                                 rr_factors* out);
+rr_status rr_images_factors(rr_images* im, double c, rr_factors* out);
+
 /* Length of the reference's response (rir.cpp:78-80): llround(t_last*fs) +
  * (taps-1)/2 + 1, or 0 without events. */
 rr_status rr_ir_reference_length(int64_t n, const double* dist, double c,

@@ -525,6 +525,47 @@ inline RoomImpulseResponse synthesize(const PulseTrains& trains, double sample_r
   return rir;
 }
 
+// ------------------------------------------------------------------ metrics (metrics.hpp)
+struct MetricValue {
+  double value = 0.0;
+  bool reliable = false;
+};
+
+struct PerceptiveFactors {
+  MetricValue edt_s, t30_s, spl_db, c80_db, d50_pct, ts_ms;
+};
+
+struct BandFactors {
+  std::array<PerceptiveFactors, kNumBands> bands;
+  PerceptiveFactors mid;  // 500 Hz / 1 kHz average
+};
+
+namespace detail {
+inline PerceptiveFactors to_factors(const rr_factors& f) {
+  auto m = [](const rr_metric& x) { return MetricValue{x.value, x.reliable != 0}; };
+  return PerceptiveFactors{m(f.edt_s), m(f.t30_s), m(f.spl_db), m(f.c80_db), m(f.d50_pct), m(f.ts_ms)};
+}
+}  // namespace detail
+
+/// factors(const PulseTrains&) (metrics.hpp:56-60) on the GPU.
+inline BandFactors factors(const PulseTrains& trains) {
+  std::vector<int64_t> off(kNumBands + 1, 0);
+  std::vector<double> t, a;
+  for (int b = 0; b < kNumBands; ++b) {
+    for (const PulseEvent& e : trains[b].events) {
+      t.push_back(e.time_s);
+      a.push_back(e.amplitude);
+    }
+    off[b + 1] = static_cast<int64_t>(t.size());
+  }
+  rr_factors out[kNumBands + 1];
+  detail::check(rr_band_factors(Device::get(0).handle(), off.data(), t.data(), a.data(), out));
+  BandFactors bf;
+  for (int b = 0; b < kNumBands; ++b) bf.bands[b] = detail::to_factors(out[b]);
+  bf.mid = detail::to_factors(out[kNumBands]);
+  return bf;
+}
+
 }  // namespace roomray_b200
 
 #endif  // ROOMRAY_B200_HPP

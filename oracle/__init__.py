@@ -353,6 +353,8 @@ class Ref:
         L.rref_air_alpha.restype = C.c_double
         L.rref_air_alpha.argtypes = [_f64p, C.c_double]
         L.rref_band_filter.argtypes = [C.c_int, C.c_double, _f64p]
+        L.rref_factors.restype = C.c_int
+        L.rref_factors.argtypes = [_i64, _f64p, _f64p, C.c_double, _f64p]
         L.rref_synthesize.restype = _i64
         L.rref_synthesize.argtypes = [_i64, _f64p, _f64p, C.c_double, C.c_double, _i32, _vp, _i64]
         L.rref_lattice.restype = _vp
@@ -413,6 +415,16 @@ class Ref:
         if length:
             self.L.rref_synthesize(n, dist, energy, c, fs, band_mask, out.ctypes.data, length)
         return out
+
+    def factors(self, dist, energy, c):
+        """factors(build_pulse_trains(images, c)) (metrics.cpp:168-180):
+        (9, 6, 2) array — bands 0..7 then mid; edt_s, t30_s, spl_db, c80_db,
+        d50_pct, ts_ms; (value, reliable)."""
+        dist = _c(dist, np.float64)
+        out = np.zeros(9 * 6 * 2)
+        if self.L.rref_factors(len(dist), dist, _c(energy, np.float64).reshape(-1), c, out):
+            self._err()
+        return out.reshape(9, 6, 2)
 
     def lattice(self, dims, walls_alpha, src, recv, max_distance, radius, air4):
         n = _i64()

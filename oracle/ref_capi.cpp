@@ -14,6 +14,7 @@
 //   build_image_sources   image_sources.hpp:58-61
 //   build_pulse_trains / synthesize / design_band_filter  rir.hpp:33-45
 //   air_beta_bands        air_absorption.hpp:30
+//   factors               metrics.hpp:56-60
 //   enumerate_images      shoebox.hpp:43
 #include <algorithm>
 #include <cstdint>
@@ -29,6 +30,7 @@
 #include "roomray/emission.hpp"
 #include "roomray/image_sources.hpp"
 #include "roomray/mesh_gen.hpp"
+#include "roomray/metrics.hpp"
 #include "roomray/rir.hpp"
 #include "roomray/shoebox.hpp"
 #include "roomray/tracer.hpp"
@@ -405,6 +407,29 @@ int64_t rref_synthesize(int64_t n, const double* dist, const double* energy,
     }
   });
   return rc == 0 ? len : -1;
+}
+
+// factors(build_pulse_trains(images, c)) (metrics.cpp:168-180, rir.cpp:9-30):
+// out = 9 x 6 x {value, reliable}, bands 0..7 then "mid"; factor order
+// edt_s, t30_s, spl_db, c80_db, d50_pct, ts_ms (metrics.hpp:39-46).
+int rref_factors(int64_t n, const double* dist, const double* energy, double c, double* out) {
+  return guarded([&] {
+    std::vector<ImageSource> images(n);
+    for (int64_t i = 0; i < n; ++i) {
+      images[i].distance = dist[i];
+      for (int b = 0; b < kNumBands; ++b) images[i].band_energy[b] = energy[kNumBands * i + b];
+    }
+    const BandFactors bf = factors(build_pulse_trains(images, c));
+    auto put = [&](int slot, const PerceptiveFactors& f) {
+      const MetricValue* m[6] = {&f.edt_s, &f.t30_s, &f.spl_db, &f.c80_db, &f.d50_pct, &f.ts_ms};
+      for (int k = 0; k < 6; ++k) {
+        out[(slot * 6 + k) * 2] = m[k]->value;
+        out[(slot * 6 + k) * 2 + 1] = m[k]->reliable ? 1.0 : 0.0;
+      }
+    };
+    for (int b = 0; b < kNumBands; ++b) put(b, bf.bands[b]);
+    put(kNumBands, bf.mid);
+  });
 }
 
 // Shoebox lattice oracle (shoebox.cpp:43-116): count, then fetch.

@@ -59,6 +59,15 @@ class Air(C.Structure):
     _fields_ = [("enabled", _i32), ("temperature_c", _d), ("relative_humidity", _d), ("pressure_kpa", _d)]
 
 
+class Metric(C.Structure):
+    _fields_ = [("value", _d), ("reliable", _i32)]
+
+
+class Factors(C.Structure):
+    _fields_ = [("edt_s", Metric), ("t30_s", Metric), ("spl_db", Metric), ("c80_db", Metric), ("d50_pct", Metric),
+                ("ts_ms", Metric)]
+
+
 class ClusterOptions(C.Structure):
     _fields_ = [("tol_scale", _d), ("merge_coplanar", _i32)]
 
@@ -100,6 +109,9 @@ SIGNATURES = [
     ("rr_ir_reference_length", C.c_int, [_i64, _f64p, _d, _d, _i32, C.POINTER(_i64)]),
     ("rr_band_filter", C.c_int, [_i32, _d, _i32, _f64p]),
     ("rr_l2_read_gbs", C.c_int, [_vp, _i64, _i32, C.POINTER(_d)]),
+    ("rr_band_factors", C.c_int, [_vp, _i64p, _vp, _vp, _vp]),
+    ("rr_factors_from_images", C.c_int, [_vp, _i64, _vp, _vp, _d, _vp]),
+    ("rr_images_factors", C.c_int, [_vp, _d, _vp]),
 ]
 
 _LIB = None

@@ -510,6 +510,86 @@ rr_status rr_synthesize_trains(rr_ctx* ctx, const int64_t* band_off, const doubl
   });
 }
 
+}  // extern "C"
+namespace rr {
+void band_factors(rr_ctx* ctx, const double* d_t, const double* d_a, int64_t n, rr_factors* d_out);
+void image_factors(rr_ctx* ctx, const double* d_dist, const double* d_energy, int64_t n, double c, rr_factors* out);
+}  // namespace rr
+extern "C" {
+
+rr_status rr_band_factors(rr_ctx* ctx, const int64_t* band_off, const double* time, const double* amplitude,
+                          rr_factors* out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(band_off, "band_off");
+    check_ptr(out, "out");
+    if (band_off[0] != 0) rr::invalid("band_off[0] must be 0");
+    for (int b = 0; b < rr::kBands; ++b)
+      if (band_off[b + 1] < band_off[b]) rr::invalid("band_off must be non-decreasing");
+    const int64_t n = band_off[rr::kBands];
+    if (n > 0) {
+      check_ptr(time, "time");
+      check_ptr(amplitude, "amplitude");
+    }
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    rr::DevBuf<double> t, a;
+    rr::DevBuf<rr_factors> d_out;
+    t.alloc(std::max<int64_t>(n, 1), st);
+    a.alloc(std::max<int64_t>(n, 1), st);
+    d_out.alloc(rr::kBands, st);
+    if (n > 0) {
+      RR_CUDA(cudaMemcpyAsync(t.p, time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      RR_CUDA(cudaMemcpyAsync(a.p, amplitude, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    }
+    for (int b = 0; b < rr::kBands; ++b)
+      rr::band_factors(ctx, t.p + band_off[b], a.p + band_off[b], band_off[b + 1] - band_off[b], d_out.p + b);
+    RR_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(rr_factors) * rr::kBands, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    auto avg = [](rr_metric x, rr_metric y) {
+      return rr_metric{0.5 * (x.value + y.value), x.reliable && y.reliable};
+    };
+    out[8] = rr_factors{avg(out[3].edt_s, out[4].edt_s), avg(out[3].t30_s, out[4].t30_s),
+                        avg(out[3].spl_db, out[4].spl_db), avg(out[3].c80_db, out[4].c80_db),
+                        avg(out[3].d50_pct, out[4].d50_pct), avg(out[3].ts_ms, out[4].ts_ms)};
+  });
+}
+
+rr_status rr_factors_from_images(rr_ctx* ctx, int64_t n, const double* dist, const double* energy, double c,
+                                 rr_factors* out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(out, "out");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");  // rir.cpp:11-13
+    if (n < 0) rr::invalid("n must be >= 0");
+    if (n > 0) {
+      check_ptr(dist, "dist");
+      check_ptr(energy, "energy");
+    }
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    rr::DevBuf<double> dd, de;
+    dd.alloc(std::max<int64_t>(n, 1), st);
+    de.alloc(rr::kBands * std::max<int64_t>(n, 1), st);
+    if (n > 0) {
+      RR_CUDA(cudaMemcpyAsync(dd.p, dist, sizeof(double) * n, cudaMemcpyDefault, st));
+      RR_CUDA(cudaMemcpyAsync(de.p, energy, sizeof(double) * rr::kBands * n, cudaMemcpyDefault, st));
+    }
+    rr::image_factors(ctx, dd.p, de.p, n, c, out);
+  });
+}
+
+rr_status rr_images_factors(rr_images* im, double c, rr_factors* out) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    check_ptr(out, "out");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");
+    rr_ctx* ctx = im->scene->ctx;
+    RR_CUDA(cudaSetDevice(ctx->device));
+    rr::image_factors(ctx, im->dist.p, im->energy.p, im->n, c, out);
+  });
+}
+
 // Response length of the reference's synthesize (rir.cpp:78-80):
 // llround(t_last*fs) + (taps-1)/2 + 1, 0 for no events.
 rr_status rr_ir_reference_length(int64_t n, const double* dist, double c, double fs, int32_t taps,

@@ -445,3 +445,32 @@ def build_image_sources(trace_res: DeviceTrace, total_rays: int, air: AirModel =
     """build_image_sources (image_sources.hpp:58-61) for one receiver of a
     device trace (captures never leave the GPU)."""
     return build_image_sources_device(trace_res, total_rays, air, options, receiver).fetch()
+
+
+FACTOR_NAMES = ("edt_s", "t30_s", "spl_db", "c80_db", "d50_pct", "ts_ms")
+
+
+def _factors_out(arr) -> dict:
+    """9 rr_factors -> {"bands": [8 x {name: (value, reliable)}], "mid": {...}}."""
+    conv = [{k: (getattr(f, k).value, bool(getattr(f, k).reliable)) for k in FACTOR_NAMES} for f in arr]
+    return {"bands": conv[:NUM_BANDS], "mid": conv[NUM_BANDS]}
+
+
+def factors(distance, band_energy, speed_of_sound: float = 343.0, ctx: Context | None = None) -> dict:
+    """factors(build_pulse_trains(images, c)) (metrics.hpp:56-60, rir.hpp:33)
+    on the device: per band EDT, T30, SPL, C80, D50, Ts and the 500 Hz -
+    1 kHz "mid" average, each as (value, reliable)."""
+    ctx = ctx or Context.default()
+    d = _f64(distance).reshape(-1)
+    e = _f64(band_energy).reshape(-1, NUM_BANDS)
+    out = (_lib.Factors * 9)()
+    check(ctx.lib.rr_factors_from_images(ctx.h, len(d), ptr(d), ptr(e), float(speed_of_sound),
+                                         C.cast(out, C.c_void_p)))
+    return _factors_out(out)
+
+
+def factors_of_images(images: "DeviceImages", speed_of_sound: float = 343.0) -> dict:
+    """factors() of a device image set without leaving the GPU."""
+    out = (_lib.Factors * 9)()
+    check(images.lib.rr_images_factors(images.h, float(speed_of_sound), C.cast(out, C.c_void_p)))
+    return _factors_out(out)

@@ -150,6 +150,17 @@ int main(int argc, char** argv) {
     std::vector<double> bands;
     for (const auto& b : rir.band_samples) bands.insert(bands.end(), b.begin(), b.end());
     write_all(out + "/rir_bands.f64", bands);
+    const rb::BandFactors bf = rb::factors(trains);
+    std::vector<double> fac;
+    auto put = [&](const rb::PerceptiveFactors& f) {
+      for (const rb::MetricValue* m : {&f.edt_s, &f.t30_s, &f.spl_db, &f.c80_db, &f.d50_pct, &f.ts_ms}) {
+        fac.push_back(m->value);
+        fac.push_back(m->reliable ? 1.0 : 0.0);
+      }
+    };
+    for (const auto& f : bf.bands) put(f);
+    put(bf.mid);
+    write_all(out + "/factors.f64", fac);
     try {
       rb::build_pulse_trains(images, 0.0);
       std::cerr << "c = 0 did not throw\n";

@@ -102,5 +102,10 @@ def test_facade_matches_oracle(tmp_path, port, merge):
     assert len(rir) == len(want)
     peak = np.abs(want).max()
     np.testing.assert_allclose(rir, want, rtol=0, atol=1e-6 * peak)
+    fac = np.fromfile(out / "factors.f64").reshape(9, 6, 2)
+    want_f = oracle.Ref().factors(ref.dist, ref.energy, 343.0) if oracle.ref_available() else None
+    if want_f is not None:
+        assert np.array_equal(fac[:, :, 1], want_f[:, :, 1])
+        np.testing.assert_allclose(fac[:, :, 0], want_f[:, :, 0], rtol=1e-6, atol=1e-9)
     bands = np.fromfile(out / "rir_bands.f64").reshape(8, -1)
     np.testing.assert_allclose(bands.sum(0), rir, rtol=0, atol=1e-12 * peak)
