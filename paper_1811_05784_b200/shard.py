@@ -331,7 +331,7 @@ class ShardedResult:
 
 
 def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: float, length: int, taps: int = 1023,
-                block: int = 4096, group=None, mark=None) -> ShardedResult:
+                block: int = 4096, group=None, mark=None, exchange: bool | None = None) -> ShardedResult:
     """trace -> exchange -> image sources -> IR for every receiver, the ranks
     of `group` each tracing a block-cyclic shard of the N-ray lattice (one
     trace serves all receivers: a receiver never alters a ray,
@@ -346,22 +346,24 @@ def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: f
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     shard = dict(first=rank, stride=world, block=block) if world > 1 else {}
+    # exchange=True forces the collective path on one rank (tests)
+    xch = world > 1 if exchange is None else bool(exchange)
     mark = mark or (lambda name: None)
     dt = trace_device(tree, source, recs, config, **shard)
     mark("trace")
     lib = tree.lib
     dev = torch.device("cuda", tree.ctx.device)
     out = ShardedResult([], [], [], int(dt.stats.ray_bounces), 0)
-    caps_all = device_captures(dt) if world > 1 else None
+    caps_all = device_captures(dt) if xch else None
     recv_ids = None
-    if world > 1:
+    if xch:
         n = int(dt.stats.n_captures)
         recv_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         _lib.check(lib.rr_trace_captures(dt.h, C.c_void_p(recv_ids.data_ptr()), None, None, None, None, None, None,
                                          None))
         recv_ids = recv_ids[:n]
     for r in range(len(recs)):
-        if world > 1:
+        if xch:
             caps = select(caps_all, recv_ids == r)
             owner = order_owners(caps, config.max_iterations, group)
             mine = exchange_captures(caps, owner, group)
@@ -387,7 +389,7 @@ def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: f
         mark("ir")
         local = images_to_tensors(dimg)
         out.local_images += len(local)
-        out.images.append(gather_images(local, group) if world > 1 else local)
+        out.images.append(gather_images(local, group) if xch else local)
         out.band_ir.append(band.view(NUM_BANDS, length))
         out.broadband.append(bb)
         torch.cuda.synchronize(dev)

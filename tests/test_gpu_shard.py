@@ -146,3 +146,20 @@ def test_import_rejects_bad_records(ctx):
                          torch.tensor([0, 1], device="cuda"), torch.tensor([10 ** 6], dtype=torch.int32, device="cuda"))
     with pytest.raises(ValueError):
         _import_no_mult(tree, c, rr.Receiver(*s.receivers[0]))
+
+
+def test_nccl_exchange_path_single_rank():
+    """The collective path of run_sharded through NCCL (one rank, forced)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "native", "nccl_single.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "exchange ok" in r.stdout
