@@ -352,6 +352,39 @@ __global__ void sah_compact_kernel(const int32_t* __restrict__ sah, int64_t S, i
   if (j < S && !sah[j]) sah_idx[j] = -1;
 }
 
+// ---- depth-first relayout: nodes of a subtree become contiguous and a
+// left child directly follows its parent (like the reference tree's layout),
+// so a traversal walks through neighbouring cache lines.
+// size[n] = internal nodes in the subtree of n, bottom-up per level
+__global__ void subtree_size_kernel(const TNode* __restrict__ tn, int32_t lo, int32_t hi,
+                                    int32_t* __restrict__ size) {
+  const int32_t n = lo + static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= hi) return;
+  const int4 d = tn[n].d;
+  size[n] = 1 + (d.x >= 0 ? size[d.x] : 0) + (d.y >= 0 ? size[d.y] : 0);
+}
+
+// preorder ids, top-down per level
+__global__ void preorder_kernel(const TNode* __restrict__ tn, int32_t lo, int32_t hi,
+                                const int32_t* __restrict__ size, int32_t* __restrict__ pre) {
+  const int32_t n = lo + static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= hi) return;
+  const int4 d = tn[n].d;
+  const int32_t p = pre[n];
+  if (d.x >= 0) pre[d.x] = p + 1;
+  if (d.y >= 0) pre[d.y] = p + 1 + (d.x >= 0 ? size[d.x] : 0);
+}
+
+__global__ void relayout_kernel(const TNode* __restrict__ tn, int32_t n_nodes, const int32_t* __restrict__ pre,
+                                TNode* __restrict__ out) {
+  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= n_nodes) return;
+  TNode t = tn[n];
+  if (t.d.x >= 0) t.d.x = pre[t.d.x];
+  if (t.d.y >= 0) t.d.y = pre[t.d.y];
+  out[pre[n]] = t;
+}
+
 inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
 
 template <typename F>
@@ -430,6 +463,7 @@ void build_sah_tree(rr_scene* s) {
   SSeg *segs = segA.p, *nsegs = segB.p;
   int64_t S = 1;
   int32_t level_base = 0;
+  std::vector<int32_t> bases{0};  // internal nodes of level L: [bases[L], bases[L+1])
   int depth = 0;
   const float eps = s->hdr.eps;
   for (int L = 0; S > 0; ++L) {
@@ -497,7 +531,34 @@ void build_sah_tree(rr_scene* s) {
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
     level_base += static_cast<int32_t>(n_split);
+    bases.push_back(level_base);
     S = 2 * n_split;
+  }
+  {  // depth-first relayout (RR_SAH_DFS=1); measured neutral (C2 -0.5 %,
+     // C3 +3.6 %, C5 -0.5 %), so the level order is kept by default
+    static const int dfs = [] {
+      const char* e = std::getenv("RR_SAH_DFS");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int32_t n_int = static_cast<int32_t>(nf - 1);
+    if (dfs && n_int > 1) {
+      DevBuf<int32_t> size, pre;
+      DevBuf<TNode> out;
+      size.alloc(n_int, st);
+      pre.alloc(n_int, st);
+      out.alloc(n_int, st);
+      for (int L = static_cast<int>(bases.size()) - 2; L >= 0; --L)
+        subtree_size_kernel<<<grid(bases[L + 1] - bases[L]), 256, 0, st>>>(s->snodes.p, bases[L], bases[L + 1],
+                                                                             size.p);
+      RR_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int32_t), st));  // the root (BFS 0) stays 0
+      for (size_t L = 0; L + 1 < bases.size(); ++L)
+        preorder_kernel<<<grid(bases[L + 1] - bases[L]), 256, 0, st>>>(s->snodes.p, bases[L], bases[L + 1], size.p,
+                                                                       pre.p);
+      relayout_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, pre.p, out.p);
+      RR_LAUNCH_CHECK();
+      s->ctx->launches += 2 * static_cast<int64_t>(bases.size()) + 1;
+      s->snodes = std::move(out);
+    }
   }
   RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
