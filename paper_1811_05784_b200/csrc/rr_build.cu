@@ -430,6 +430,7 @@ void build_scene_tree(rr_scene* s) {
   RR_CUDA(cudaEventCreate(&e1));
   RR_CUDA(cudaEventRecord(e0, st));
 
+  StageTimer tm(st);
   // ---- host plan: per-level segment size multisets (depend on nf only)
   std::vector<std::map<int64_t, int64_t>> levels;
   levels.push_back({{nf, 1}});
@@ -566,6 +567,7 @@ void build_scene_tree(rr_scene* s) {
     std::swap(segs, nsegs);
   }
 
+  tm.mark("build: reference levels");
   // ---- axis-aligned plane tables: per axis, the sorted unique plane
   // coordinates of the flat faces; ids for faces and for tree children
   {
@@ -613,6 +615,7 @@ void build_scene_tree(rr_scene* s) {
     RR_CUDA(cudaStreamSynchronize(st));  // hoff is a stack array
   }
 
+  tm.mark("build: plane tables");
   // ---- 4-wide collapse
   int32_t k4 = 0;
   {
@@ -642,6 +645,7 @@ void build_scene_tree(rr_scene* s) {
     k4 = std::min<int32_t>(counts[1], kMaxCachedQNodes);
   }
 
+  tm.mark("build: 4-wide collapse");
   // ---- TriangleMesh::bounds over all vertices (image-source tolerance)
   DevBuf<unsigned long long> vb;
   vb.alloc(6, st);
@@ -675,7 +679,9 @@ void build_scene_tree(rr_scene* s) {
     RR_CUDA(cudaEventCreate(&a0));
     RR_CUDA(cudaEventCreate(&a1));
     RR_CUDA(cudaEventRecord(a0, st));
+    tm.mark("build: bounds");
     build_sah_tree(s);
+    tm.mark("build: SAH tree");
     RR_CUDA(cudaEventRecord(a1, st));
     RR_CUDA(cudaEventSynchronize(a1));
     float ms = 0.f;
