@@ -259,7 +259,8 @@ struct RegRay {  // ray held in registers
 };
 
 // CNT: count internal-node visits and leaf tests into *cnt (instrumented build)
-template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false>  // STUCKT < 0: >= 1/|STUCKT| of lanes
+// UNR: internal nodes a lane may process per vote round (amortises the votes)
+template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1>  // STUCKT < 0: >= 1/|STUCKT| of lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
                                                     int32_t rplane, unsigned long long* cnt = nullptr) {
@@ -290,7 +291,8 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     }
   };
   while (node != kDone || leaf != 0) {
-    if (node >= 0 && node != kDone) {
+#pragma unroll 1
+    for (int u = 0; u < UNR && node >= 0 && node != kDone && (u == 0 || leaf == 0); ++u) {
       if (CNT) ++cnt[0];
       const float4* q = reinterpret_cast<const float4*>(nodes + node);
       const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -312,11 +314,11 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       } else {
         pop();
       }
-    }
-    if (node < 0 && leaf == 0) {
-      leaf = node;
-      prefetch_l1(tri + ~leaf);
-      pop();
+      if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
+        leaf = node;
+        prefetch_l1(tri + ~leaf);
+        pop();
+      }
     }
     // test when enough lanes hold a leaf, enough are stuck behind theirs, or
     // no lane can advance without a test

@@ -20,8 +20,11 @@
 //      picks the split (best binned SAH cost, else the object median of the
 //      longest centroid extent) and emits the two child segments;
 //   4. stable segmented partition of the three lists.
-// Nodes are numbered level by level (BFS); depth is capped so the 32-entry
-// traversal stack cannot overflow (median splits once the budget is short).
+// Nodes of the large segments are numbered level by level (BFS); segments
+// of <= kSmall faces are finished in one kernel (one thread each, median
+// splits, preorder ids from the top of the array), which removes the last
+// ~4 levels of launches.  Depth is capped so the 32-entry traversal stack
+// cannot overflow (median splits once the budget is short).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -36,6 +39,18 @@ namespace {
 constexpr int kBins = 32;
 constexpr int64_t kSahMin = 64;
 constexpr int kMaxDepth = 30;
+constexpr int kSmall = 16;  // segments this small are built in one go by one thread
+const char* const kLevelNames[64] = {
+    "sah level 0",  "sah level 1",  "sah level 2",  "sah level 3",  "sah level 4",  "sah level 5",  "sah level 6",
+    "sah level 7",  "sah level 8",  "sah level 9",  "sah level 10", "sah level 11", "sah level 12", "sah level 13",
+    "sah level 14", "sah level 15", "sah level 16", "sah level 17", "sah level 18", "sah level 19", "sah level 20",
+    "sah level 21", "sah level 22", "sah level 23", "sah level 24", "sah level 25", "sah level 26", "sah level 27",
+    "sah level 28", "sah level 29", "sah level 30", "sah level 31", "sah level 32", "sah level 33", "sah level 34",
+    "sah level 35", "sah level 36", "sah level 37", "sah level 38", "sah level 39", "sah level 40", "sah level 41",
+    "sah level 42", "sah level 43", "sah level 44", "sah level 45", "sah level 46", "sah level 47", "sah level 48",
+    "sah level 49", "sah level 50", "sah level 51", "sah level 52", "sah level 53", "sah level 54", "sah level 55",
+    "sah level 56", "sah level 57", "sah level 58", "sah level 59", "sah level 60", "sah level 61", "sah level 62",
+    "sah level 63"};
 
 struct SSeg {
   int64_t b, n;
@@ -143,32 +158,72 @@ __device__ __forceinline__ int bin_of(double c, double lo, double ext) {
   return b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
 }
 
-// 2. centroid bins of the SAH segments: count + float AABB per (axis, bin)
-__global__ void bin_kernel(const int32_t* __restrict__ pos_seg, const int32_t* __restrict__ perm0,
-                           const double* __restrict__ fb, const double* __restrict__ cen,
-                           const unsigned long long* __restrict__ cb, const int32_t* __restrict__ sah_idx,
-                           int64_t nf, int32_t* __restrict__ bcnt, uint32_t* __restrict__ bbox) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nf) return;
-  const int32_t s = pos_seg[i];
-  if (s < 0) return;
-  const int32_t q = sah_idx[s];
-  if (q < 0) return;
-  const int32_t f = perm0[i];
-  uint32_t lo[3], hi[3];
-  for (int k = 0; k < 3; ++k) {
-    lo[k] = okeyf(__double2float_rn(fb[6 * f + k]));
-    hi[k] = okeyf(__double2float_rn(fb[6 * f + 3 + k]));
+// 2. centroid bins of the SAH segments: count + float AABB per (axis, bin).
+// Blocks whose 256 positions all lie in one segment (the large top-level
+// segments) accumulate in shared memory and flush once; others go straight
+// to global atomics.
+__global__ void __launch_bounds__(256) bin_kernel(const int32_t* __restrict__ pos_seg, const int32_t* __restrict__ perm0,
+                                                  const double* __restrict__ fb, const double* __restrict__ cen,
+                                                  const unsigned long long* __restrict__ cb,
+                                                  const int32_t* __restrict__ sah_idx, int64_t nf,
+                                                  int32_t* __restrict__ bcnt, uint32_t* __restrict__ bbox) {
+  __shared__ int32_t s_cnt[3 * kBins];
+  __shared__ uint32_t s_box[3 * kBins * 6];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int64_t i = i0 + threadIdx.x;
+  const int64_t last = min(i0 + static_cast<int64_t>(blockDim.x), nf) - 1;
+  const int32_t s0 = pos_seg[i0], s1 = pos_seg[last];
+  const bool shared = s0 >= 0 && s0 == s1 && sah_idx[s0] >= 0;  // block-uniform
+  if (shared) {
+    for (int t = threadIdx.x; t < 3 * kBins; t += blockDim.x) {
+      s_cnt[t] = 0;
+      for (int k = 0; k < 3; ++k) {
+        s_box[6 * t + k] = 0xffffffffu;
+        s_box[6 * t + 3 + k] = 0u;
+      }
+    }
+    __syncthreads();
   }
-  for (int a = 0; a < 3; ++a) {
-    const double clo = oval(cb[6 * s + a]), ext = oval(cb[6 * s + 3 + a]) - clo;
-    if (!(ext > 0.0)) continue;
-    const int b = bin_of(cen[3 * f + a], clo, ext);
-    const int64_t slot = (static_cast<int64_t>(q) * 3 + a) * kBins + b;
-    atomicAdd(bcnt + slot, 1);
+  const int32_t s = i < nf ? pos_seg[i] : -1;
+  const int32_t q = s >= 0 ? sah_idx[s] : -1;
+  if (q >= 0) {
+    const int32_t f = perm0[i];
+    uint32_t lo[3], hi[3];
     for (int k = 0; k < 3; ++k) {
-      atomicMin(bbox + 6 * slot + k, lo[k]);
-      atomicMax(bbox + 6 * slot + 3 + k, hi[k]);
+      lo[k] = okeyf(__double2float_rn(fb[6 * f + k]));
+      hi[k] = okeyf(__double2float_rn(fb[6 * f + 3 + k]));
+    }
+    for (int a = 0; a < 3; ++a) {
+      const double clo = oval(cb[6 * s + a]), ext = oval(cb[6 * s + 3 + a]) - clo;
+      if (!(ext > 0.0)) continue;
+      const int b = bin_of(cen[3 * f + a], clo, ext);
+      if (shared) {
+        const int t = a * kBins + b;
+        atomicAdd(s_cnt + t, 1);
+        for (int k = 0; k < 3; ++k) {
+          atomicMin(s_box + 6 * t + k, lo[k]);
+          atomicMax(s_box + 6 * t + 3 + k, hi[k]);
+        }
+      } else {
+        const int64_t slot = (static_cast<int64_t>(q) * 3 + a) * kBins + b;
+        atomicAdd(bcnt + slot, 1);
+        for (int k = 0; k < 3; ++k) {
+          atomicMin(bbox + 6 * slot + k, lo[k]);
+          atomicMax(bbox + 6 * slot + 3 + k, hi[k]);
+        }
+      }
+    }
+  }
+  if (shared) {
+    __syncthreads();
+    const int64_t base = static_cast<int64_t>(sah_idx[s0]) * 3 * kBins;
+    for (int t = threadIdx.x; t < 3 * kBins; t += blockDim.x) {
+      if (!s_cnt[t]) continue;
+      atomicAdd(bcnt + base + t, s_cnt[t]);
+      for (int k = 0; k < 3; ++k) {
+        atomicMin(bbox + 6 * (base + t) + k, s_box[6 * t + k]);
+        atomicMax(bbox + 6 * (base + t) + 3 + k, s_box[6 * t + 3 + k]);
+      }
     }
   }
 }
@@ -189,6 +244,10 @@ __global__ void split_kernel(const SSeg* __restrict__ segs, int64_t S, const int
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= S) return;
   const SSeg sg = segs[j];
+  if (sg.n >= 2 && sg.n <= kSmall) {  // finish_kernel's
+    seg_axis[j] = -1;
+    return;
+  }
   double lo[3], hi[3];
   for (int k = 0; k < 3; ++k) {
     lo[k] = oval(bb[6 * j + k]);
@@ -283,6 +342,122 @@ __global__ void split_kernel(const SSeg* __restrict__ segs, int64_t S, const int
   next[2 * rank[j] + 1] = SSeg{sg.b + nl, sg.n - nl, me, 1};
 }
 
+// 3b. small segments (2..kSmall faces): one thread builds the whole subtree
+// with object-median splits on the longest centroid extent, numbering its
+// n - 1 internal nodes in preorder inside a block taken from the top of the
+// node array (the level-order nodes grow from the bottom; together exactly
+// nf - 1), and writes the segment's own slot in its parent.
+__device__ void child_slot(TNode* p, int side, const double* lo, const double* hi, float eps, int32_t ref,
+                           int32_t plane) {
+  const float lx = lo_f(lo[0], eps), ly = lo_f(lo[1], eps), lz = lo_f(lo[2], eps);
+  const float hx = hi_f(hi[0], eps), hy = hi_f(hi[1], eps), hz = hi_f(hi[2], eps);
+  if (side == 0) {
+    p->a = make_float4(lx, hx, ly, hy);
+    reinterpret_cast<float2*>(&p->b)[0] = make_float2(lz, hz);
+    p->d.x = ref;
+    p->d.z = plane;
+  } else {
+    reinterpret_cast<float2*>(&p->b)[1] = make_float2(lx, hx);
+    p->c = make_float4(ly, hy, lz, hz);
+    p->d.y = ref;
+    p->d.w = plane;
+  }
+}
+
+__global__ void finish_kernel(const SSeg* __restrict__ segs, int64_t S, const int32_t* __restrict__ perm0,
+                              const double* __restrict__ fb, const double* __restrict__ cen,
+                              const int32_t* __restrict__ face_plane, int64_t nf, float eps, TNode* __restrict__ tn,
+                              TravHeader* __restrict__ hdr, unsigned long long* __restrict__ top) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const SSeg sg = segs[j];
+  const int n = static_cast<int>(sg.n);
+  if (n < 2 || n > kSmall) return;
+  int32_t f[kSmall];
+  for (int i = 0; i < n; ++i) f[i] = perm0[sg.b + i];
+  const int32_t base = static_cast<int32_t>(nf - 1 - static_cast<int64_t>(atomicAdd(top, (unsigned long long)(n - 1))) -
+                                            (n - 1));
+  // range [a, b) of f -> AABB (exact, fp64) and common plane id
+  auto range_box = [&](int a, int b, double* lo, double* hi, int32_t* plane) {
+    int32_t pmin = 0x7fffffff, pmax = static_cast<int32_t>(0x80000000);
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = HUGE_VAL;
+      hi[k] = -HUGE_VAL;
+    }
+    for (int i = a; i < b; ++i) {
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = fmin(lo[k], fb[6 * f[i] + k]);
+        hi[k] = fmax(hi[k], fb[6 * f[i] + 3 + k]);
+      }
+      const int32_t p = face_plane ? face_plane[f[i]] : -1;
+      pmin = min(pmin, p);
+      pmax = max(pmax, p);
+    }
+    *plane = pmin == pmax ? pmin : -1;
+  };
+  {  // the segment itself, in its parent's slot (or as the root)
+    double lo[3], hi[3];
+    int32_t plane;
+    range_box(0, n, lo, hi, &plane);
+    if (sg.parent < 0) hdr->root_ref = base;
+    else child_slot(tn + sg.parent, sg.side, lo, hi, eps, base, plane);
+  }
+  // explicit stack of ranges still to split: (a, b, node index)
+  int sa[kSmall], sb[kSmall], sn[kSmall];
+  int sp = 0;
+  sa[0] = 0;
+  sb[0] = n;
+  sn[0] = base;
+  sp = 1;
+  while (sp > 0) {
+    --sp;
+    const int a = sa[sp], b = sb[sp], me = sn[sp];
+    // longest centroid extent, then insertion sort of f[a, b) on that axis
+    double clo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, chi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+    for (int i = a; i < b; ++i)
+      for (int k = 0; k < 3; ++k) {
+        clo[k] = fmin(clo[k], cen[3 * f[i] + k]);
+        chi[k] = fmax(chi[k], cen[3 * f[i] + k]);
+      }
+    int ax = 0;
+    for (int k = 1; k < 3; ++k)
+      if (chi[k] - clo[k] > chi[ax] - clo[ax]) ax = k;
+    for (int x = a + 1; x < b; ++x) {
+      const int32_t v = f[x];
+      const double cv = cen[3 * v + ax];
+      int y = x - 1;
+      while (y >= a && (cen[3 * f[y] + ax] > cv || (cen[3 * f[y] + ax] == cv && f[y] > v))) {
+        f[y + 1] = f[y];
+        --y;
+      }
+      f[y + 1] = v;
+    }
+    const int m = a + (b - a) / 2;
+    const int rng[2][2] = {{a, m}, {m, b}};
+    // preorder ids: the subtree of `me` (range size s) owns [me, me + s - 1);
+    // left child me + 1, right child me + (m - a)
+    const int32_t ref[2] = {(m - a) >= 2 ? me + 1 : ~f[a], (b - m) >= 2 ? me + (m - a) : ~f[m]};
+    for (int side = 0; side < 2; ++side) {
+      double lo[3], hi[3];
+      int32_t plane;
+      range_box(rng[side][0], rng[side][1], lo, hi, &plane);
+      child_slot(tn + me, side, lo, hi, eps, ref[side], plane);
+    }
+    if (b - m >= 2) {
+      sa[sp] = m;
+      sb[sp] = b;
+      sn[sp] = ref[1];
+      ++sp;
+    }
+    if (m - a >= 2) {
+      sa[sp] = a;
+      sb[sp] = m;
+      sn[sp] = ref[0];
+      ++sp;
+    }
+  }
+}
+
 // 4a. left/right flag per face
 __global__ void flag_kernel(const int32_t* __restrict__ pos_seg, const SSeg* __restrict__ segs,
                             const int32_t* __restrict__ seg_axis, const int32_t* __restrict__ seg_split,
@@ -335,54 +510,53 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* 
   if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
 }
 
-__global__ void split_flag_kernel(const SSeg* __restrict__ segs, int64_t S, int level,
-                                  int32_t* __restrict__ sflag, int32_t* __restrict__ sah) {
+__global__ void seg_init_kernel(int64_t S, unsigned long long* __restrict__ bb, unsigned long long* __restrict__ cb,
+                                int32_t* __restrict__ pl) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= S) return;
+  for (int k = 0; k < 3; ++k) {  // ordered keys: min from ~0, max from 0
+    bb[6 * j + k] = ~0ull;
+    bb[6 * j + 3 + k] = 0ull;
+    cb[6 * j + k] = ~0ull;
+    cb[6 * j + 3 + k] = 0ull;
+  }
+  pl[2 * j] = 0x7fffffff;
+  pl[2 * j + 1] = static_cast<int32_t>(0x80000000);
+}
+
+// packed flags: split (>= kSmall + 1 faces) << 32 | SAH-eligible
+__global__ void split_flag_kernel(const SSeg* __restrict__ segs, int64_t S, int level,
+                                  unsigned long long* __restrict__ flags) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j > S) return;
+  if (j == S) {
+    flags[j] = 0;
+    return;
+  }
   const int64_t n = segs[j].n;
-  sflag[j] = n >= 2 ? 1 : 0;
+  const unsigned long long split = n > kSmall ? 1ull : 0ull;  // 2..kSmall: finish_kernel
   // SAH only while the depth budget allows a median finish below
   int lg = 0;
   while ((int64_t(1) << lg) < n) ++lg;
-  sah[j] = (n >= kSahMin && level + 1 + lg + 2 <= kMaxDepth) ? 1 : 0;
+  const unsigned long long sah = (n >= kSahMin && level + 1 + lg + 2 <= kMaxDepth) ? 1ull : 0ull;
+  flags[j] = (split << 32) | sah;
 }
 
-__global__ void sah_compact_kernel(const int32_t* __restrict__ sah, int64_t S, int32_t* __restrict__ sah_idx) {
+__global__ void rank_kernel(const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ ranks,
+                            int64_t S, int32_t* __restrict__ srank, int32_t* __restrict__ sah_idx, int64_t n_bins,
+                            int32_t* __restrict__ bcnt, uint32_t* __restrict__ bbox) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < S && !sah[j]) sah_idx[j] = -1;
-}
-
-// ---- depth-first relayout: nodes of a subtree become contiguous and a
-// left child directly follows its parent (like the reference tree's layout),
-// so a traversal walks through neighbouring cache lines.
-// size[n] = internal nodes in the subtree of n, bottom-up per level
-__global__ void subtree_size_kernel(const TNode* __restrict__ tn, int32_t lo, int32_t hi,
-                                    int32_t* __restrict__ size) {
-  const int32_t n = lo + static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
-  if (n >= hi) return;
-  const int4 d = tn[n].d;
-  size[n] = 1 + (d.x >= 0 ? size[d.x] : 0) + (d.y >= 0 ? size[d.y] : 0);
-}
-
-// preorder ids, top-down per level
-__global__ void preorder_kernel(const TNode* __restrict__ tn, int32_t lo, int32_t hi,
-                                const int32_t* __restrict__ size, int32_t* __restrict__ pre) {
-  const int32_t n = lo + static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
-  if (n >= hi) return;
-  const int4 d = tn[n].d;
-  const int32_t p = pre[n];
-  if (d.x >= 0) pre[d.x] = p + 1;
-  if (d.y >= 0) pre[d.y] = p + 1 + (d.x >= 0 ? size[d.x] : 0);
-}
-
-__global__ void relayout_kernel(const TNode* __restrict__ tn, int32_t n_nodes, const int32_t* __restrict__ pre,
-                                TNode* __restrict__ out) {
-  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
-  if (n >= n_nodes) return;
-  TNode t = tn[n];
-  if (t.d.x >= 0) t.d.x = pre[t.d.x];
-  if (t.d.y >= 0) t.d.y = pre[t.d.y];
-  out[pre[n]] = t;
+  if (j < S) {
+    srank[j] = static_cast<int32_t>(ranks[j] >> 32);
+    sah_idx[j] = (flags[j] & 0xffffffffull) ? static_cast<int32_t>(ranks[j] & 0xffffffffull) : -1;
+  }
+  if (j < n_bins) {
+    bcnt[j] = 0;
+    for (int k = 0; k < 3; ++k) {
+      bbox[6 * j + k] = 0xffffffffu;
+      bbox[6 * j + 3 + k] = 0u;
+    }
+  }
 }
 
 inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
@@ -440,14 +614,15 @@ void build_sah_tree(rr_scene* s) {
 
   int64_t max_seg = nf;  // segments per level never exceed the face count
   DevBuf<SSeg> segA, segB;
-  DevBuf<int32_t> sflag, srank, sah, sah_idx, axis, split, pl;
+  DevBuf<int32_t> srank, sah_idx, axis, split, pl;
+  DevBuf<unsigned long long> flags, franks;
   DevBuf<int64_t> nl;
   DevBuf<unsigned long long> bb, cb;
   segA.alloc(max_seg, st);
   segB.alloc(max_seg, st);
-  sflag.alloc(max_seg + 1, st);
+  flags.alloc(max_seg + 1, st);
+  franks.alloc(max_seg + 1, st);
   srank.alloc(max_seg + 1, st);
-  sah.alloc(max_seg + 1, st);
   sah_idx.alloc(max_seg + 1, st);
   axis.alloc(max_seg, st);
   split.alloc(max_seg, st);
@@ -463,48 +638,37 @@ void build_sah_tree(rr_scene* s) {
   SSeg *segs = segA.p, *nsegs = segB.p;
   int64_t S = 1;
   int32_t level_base = 0;
-  std::vector<int32_t> bases{0};  // internal nodes of level L: [bases[L], bases[L+1])
+  DevBuf<unsigned long long> top;  // internal nodes handed to finish_kernel (from the top)
+  top.alloc(1, st);
+  RR_CUDA(cudaMemsetAsync(top.p, 0, sizeof(unsigned long long), st));
   int depth = 0;
   const float eps = s->hdr.eps;
+  StageTimer tm(st);
   for (int L = 0; S > 0; ++L) {
     depth = L;
-    // 1. bounds
-    RR_CUDA(cudaMemsetAsync(bb.p, 0xff, sizeof(unsigned long long) * 6 * S, st));
-    RR_CUDA(cudaMemsetAsync(cb.p, 0xff, sizeof(unsigned long long) * 6 * S, st));
-    // max halves start at 0 (ordered keys)
-    RR_CUDA(cudaMemset2DAsync(bb.p + 3, 6 * sizeof(unsigned long long), 0, 3 * sizeof(unsigned long long), S, st));
-    RR_CUDA(cudaMemset2DAsync(cb.p + 3, 6 * sizeof(unsigned long long), 0, 3 * sizeof(unsigned long long), S, st));
-    // plane id min / max start at 0x7f7f7f7f / 0x80808080 (above / below every id)
-    RR_CUDA(cudaMemset2DAsync(pl.p, 2 * sizeof(int32_t), 0x7f, sizeof(int32_t), S, st));
-    RR_CUDA(cudaMemset2DAsync(pl.p + 1, 2 * sizeof(int32_t), 0x80, sizeof(int32_t), S, st));
+    if (tm.on) tm.mark(L < 64 ? kLevelNames[L] : "level");
+    // 1. bounds (one init launch for the per-segment accumulators)
+    seg_init_kernel<<<grid(S), 256, 0, st>>>(S, bb.p, cb.p, pl.p);
     bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
+    // 2. split flags and SAH flags, both ranks from one 64-bit scan
+    //    (split flag in the high word, SAH flag in the low word)
+    split_flag_kernel<<<grid(S + 1), 256, 0, st>>>(segs, S, L, flags.p);
     RR_LAUNCH_CHECK();
-    // 2. split flags, ranks, SAH segments and their bins
-    split_flag_kernel<<<grid(S), 256, 0, st>>>(segs, S, L, sflag.p, sah.p);
-    RR_LAUNCH_CHECK();
-    RR_CUDA(cudaMemsetAsync(sflag.p + S, 0, sizeof(int32_t), st));
-    RR_CUDA(cudaMemsetAsync(sah.p + S, 0, sizeof(int32_t), st));
     cub_run([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, sflag.p, srank.p, static_cast<int>(S + 1), st);
+      return cub::DeviceScan::ExclusiveSum(t, b, flags.p, franks.p, static_cast<int>(S + 1), st);
     }, tmp, st);
-    cub_run([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, sah.p, sah_idx.p, static_cast<int>(S + 1), st);
-    }, tmp, st);
-    int32_t counts[2] = {0, 0};
-    RR_CUDA(cudaMemcpyAsync(&counts[0], srank.p + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaMemcpyAsync(&counts[1], sah_idx.p + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    unsigned long long both = 0;
+    RR_CUDA(cudaMemcpyAsync(&both, franks.p + S, sizeof both, cudaMemcpyDeviceToHost, st));
     RR_CUDA(cudaStreamSynchronize(st));
-    const int64_t n_split = counts[0], n_sah = counts[1];
-    // sah_idx[j] = compact index, or -1 for non-SAH segments
+    const int64_t n_split = static_cast<int64_t>(both >> 32), n_sah = static_cast<int64_t>(both & 0xffffffffull);
+    // srank[j] / sah_idx[j] (compact index, -1 for non-SAH segments), bins reset
     if (n_sah > 0) {
       bcnt.alloc(n_sah * 3 * kBins, st);
       bbox.alloc(n_sah * 3 * kBins * 6, st);
-      RR_CUDA(cudaMemsetAsync(bcnt.p, 0, bcnt.bytes(), st));
-      // min halves to ~0, max halves to 0: per (segment, axis, bin) 6 words
-      RR_CUDA(cudaMemsetAsync(bbox.p, 0xff, bbox.bytes(), st));
-      RR_CUDA(cudaMemset2DAsync(bbox.p + 3, 6 * sizeof(uint32_t), 0, 3 * sizeof(uint32_t), n_sah * 3 * kBins, st));
     }
-    sah_compact_kernel<<<grid(S), 256, 0, st>>>(sah.p, S, sah_idx.p);
+    rank_kernel<<<grid(std::max<int64_t>(S, n_sah * 3 * kBins)), 256, 0, st>>>(flags.p, franks.p, S, srank.p,
+                                                                               sah_idx.p, n_sah * 3 * kBins,
+                                                                               bcnt.p, bbox.p);
     RR_LAUNCH_CHECK();
     if (n_sah > 0) {
       bin_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, cb.p, sah_idx.p, nf, bcnt.p, bbox.p);
@@ -513,6 +677,8 @@ void build_sah_tree(rr_scene* s) {
     // 3. nodes + splits
     split_kernel<<<grid(S), 256, 0, st>>>(segs, S, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
                                           level_base, eps, s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
+    finish_kernel<<<grid(S, 64), 64, 0, st>>>(segs, S, perm, fb.p, cen.p, s->face_plane.p, nf, eps, s->snodes.p,
+                                              dh.p, top.p);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 6;
     if (n_split == 0) break;
@@ -531,34 +697,7 @@ void build_sah_tree(rr_scene* s) {
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
     level_base += static_cast<int32_t>(n_split);
-    bases.push_back(level_base);
     S = 2 * n_split;
-  }
-  {  // depth-first relayout (RR_SAH_DFS=1); measured neutral (C2 -0.5 %,
-     // C3 +3.6 %, C5 -0.5 %), so the level order is kept by default
-    static const int dfs = [] {
-      const char* e = std::getenv("RR_SAH_DFS");
-      return e ? std::atoi(e) : 0;
-    }();
-    const int32_t n_int = static_cast<int32_t>(nf - 1);
-    if (dfs && n_int > 1) {
-      DevBuf<int32_t> size, pre;
-      DevBuf<TNode> out;
-      size.alloc(n_int, st);
-      pre.alloc(n_int, st);
-      out.alloc(n_int, st);
-      for (int L = static_cast<int>(bases.size()) - 2; L >= 0; --L)
-        subtree_size_kernel<<<grid(bases[L + 1] - bases[L]), 256, 0, st>>>(s->snodes.p, bases[L], bases[L + 1],
-                                                                             size.p);
-      RR_CUDA(cudaMemsetAsync(pre.p, 0, sizeof(int32_t), st));  // the root (BFS 0) stays 0
-      for (size_t L = 0; L + 1 < bases.size(); ++L)
-        preorder_kernel<<<grid(bases[L + 1] - bases[L]), 256, 0, st>>>(s->snodes.p, bases[L], bases[L + 1], size.p,
-                                                                       pre.p);
-      relayout_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, pre.p, out.p);
-      RR_LAUNCH_CHECK();
-      s->ctx->launches += 2 * static_cast<int64_t>(bases.size()) + 1;
-      s->snodes = std::move(out);
-    }
   }
   RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));

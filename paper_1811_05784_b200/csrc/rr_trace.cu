@@ -48,7 +48,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false>
+template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   extern __shared__ TNode smem_nodes[];
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST, RegRay, CNT>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt);
+      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
