@@ -595,6 +595,24 @@ __global__ void final_gather_kernel(const int32_t* __restrict__ perm, int64_t n,
 
 inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
 
+// [c0, c1) of receiver r in the (receiver, ray, path)-sorted captures
+__global__ void recv_range_kernel(const int32_t* __restrict__ recv, int64_t n, int32_t r, int64_t* __restrict__ out) {
+  if (threadIdx.x > 1) return;
+  const int32_t key = threadIdx.x == 0 ? r : r + 1;  // lower bounds of r and r + 1
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (recv[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  out[threadIdx.x] = lo;
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<int32_t>(i);
+}
+
 template <typename F>
 void cub_call(F&& f, cudaStream_t st) {
   size_t bytes = 0;
@@ -617,11 +635,17 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   air_beta_bands(air, beta);
   // receiver range of the (receiver, ray, path)-sorted captures
   const int64_t nc_all = tr->stats.n_captures;
-  std::vector<int32_t> hrecv(nc_all);
-  if (nc_all) RR_CUDA(cudaMemcpyAsync(hrecv.data(), tr->c_recv.p, sizeof(int32_t) * nc_all, cudaMemcpyDeviceToHost, st));
-  RR_CUDA(cudaStreamSynchronize(st));
-  const int64_t c0 = std::lower_bound(hrecv.begin(), hrecv.end(), recv) - hrecv.begin();
-  const int64_t c1 = std::upper_bound(hrecv.begin(), hrecv.end(), recv) - hrecv.begin();
+  int64_t range[2] = {0, 0};
+  if (nc_all) {
+    DevBuf<int64_t> dr;
+    dr.alloc(2, st);
+    recv_range_kernel<<<1, 32, 0, st>>>(tr->c_recv.p, nc_all, recv, dr.p);
+    RR_LAUNCH_CHECK();
+    ctx->launches++;
+    RR_CUDA(cudaMemcpyAsync(range, dr.p, sizeof range, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+  }
+  const int64_t c0 = range[0], c1 = range[1];
   const int64_t n = c1 - c0;
   auto im = std::make_unique<rr_images>();
   im->scene = s;
@@ -696,9 +720,11 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   DevBuf<double> rs;
   rs.alloc(3 * n, st);
   gather_retro_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, retro.p, c0, rs.p);
+  tm.mark("groups: heads");
   group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, n_img.p,
                                                     is_split.p);
   RR_LAUNCH_CHECK();
+  tm.mark("groups: count");
   RR_CUDA(cudaMemsetAsync(n_img.p + ng, 0, sizeof(int32_t), st));
   cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, n_img.p, img_off.p, ng + 1, st); },
            st);
@@ -833,10 +859,9 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   DevBuf<int32_t> perm;
   perm.alloc(ni, st);
   {
-    std::vector<int32_t> iota(ni);
-    for (int64_t i = 0; i < ni; ++i) iota[i] = static_cast<int32_t>(i);
-    RR_CUDA(cudaMemcpyAsync(perm.p, iota.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, st));
-    RR_CUDA(cudaStreamSynchronize(st));
+    iota_kernel<<<grid(ni), 256, 0, st>>>(perm.p, ni);
+    RR_LAUNCH_CHECK();
+    ctx->launches++;
   }
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceMergeSort::SortKeys(t, b, perm.p, ni, FinalLess{M.order, dist.p, M.rep, pv}, st);
