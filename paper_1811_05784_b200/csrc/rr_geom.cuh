@@ -352,6 +352,116 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   return best;
 }
 
+// closest_hit_pl over the 4-wide collapse of the SAH tree: one QNode visit
+// replaces two binary levels (half the dependent node fetches); hit slots
+// are ordered by entry distance, the nearest taken next and the others
+// pushed (leaves included, so a popped entry may be a leaf); coplanar slots
+// culled via QNode.pad; same postponed, warp-batched leaf tests.
+template <int LEAFT, int STUCKT, typename RAY>
+__device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const QNode* __restrict__ q4,
+                                                     int32_t root4, const FaceTri* __restrict__ tri,
+                                                     const RAY& ray, int32_t rplane) {
+  HitResult best{0.0, -1};
+  RayF r;
+  if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
+  const float kInf = __int_as_float(0x7f800000);
+  float tbest = FLT_MAX;
+  int32_t node;
+  if (root4 < 0) {
+    node = root4;
+  } else {
+    const float t = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest);
+    node = (t == kInf) ? kDone : root4;
+  }
+  int2 st[kStack4];
+  int sp = 0;
+  int32_t leaf = 0;
+  auto pop = [&]() {
+    node = kDone;
+    while (sp > 0) {
+      --sp;
+      const int2 e = st[sp];
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        break;
+      }
+    }
+  };
+  while (node != kDone || leaf != 0) {
+    if (node >= 0 && node != kDone) {
+      const float4* p = reinterpret_cast<const float4*>(q4 + node);
+      const float4 lx = __ldg(p), hx = __ldg(p + 1), ly = __ldg(p + 2), hy = __ldg(p + 3);
+      const float4 lz = __ldg(p + 4), hz = __ldg(p + 5);
+      const int4 ch = __ldg(reinterpret_cast<const int4*>(p + 6));
+      const int4 pl = __ldg(reinterpret_cast<const int4*>(p + 7));
+      float t0 = box_enter(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tbest);
+      float t1 = box_enter(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tbest);
+      float t2 = box_enter(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tbest);
+      float t3 = box_enter(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tbest);
+      if (pl.x == rplane || ch.x == kEmpty) t0 = kInf;
+      if (pl.y == rplane || ch.y == kEmpty) t1 = kInf;
+      if (pl.z == rplane || ch.z == kEmpty) t2 = kInf;
+      if (pl.w == rplane || ch.w == kEmpty) t3 = kInf;
+      // sort the four (t, ref) pairs ascending (5 compare-exchanges)
+      int32_t c0 = ch.x, c1 = ch.y, c2 = ch.z, c3 = ch.w;
+      auto cx = [](float& ta, int32_t& ca, float& tb, int32_t& cb) {
+        const bool sw = tb < ta;
+        const float tt = sw ? tb : ta;
+        tb = sw ? ta : tb;
+        ta = tt;
+        const int32_t cc = sw ? cb : ca;
+        cb = sw ? ca : cb;
+        ca = cc;
+      };
+      cx(t0, c0, t1, c1);
+      cx(t2, c2, t3, c3);
+      cx(t0, c0, t2, c2);
+      cx(t1, c1, t3, c3);
+      cx(t1, c1, t2, c2);
+      // push the far hits (descending), continue with the nearest
+      if (t3 != kInf) st[sp++] = make_int2(c3, __float_as_int(t3));
+      if (t2 != kInf) st[sp++] = make_int2(c2, __float_as_int(t2));
+      if (t1 != kInf) st[sp++] = make_int2(c1, __float_as_int(t1));
+      if (t0 != kInf) {
+        node = c0;
+      } else {
+        pop();
+      }
+    }
+    if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
+      leaf = node;
+      prefetch_l1(tri + ~leaf);
+      pop();
+    }
+    const unsigned act = __activemask();
+    const bool can = node >= 0 && node != kDone;
+    const bool must = leaf != 0 && !can;
+    const unsigned hv = __ballot_sync(act, leaf != 0);
+    const unsigned mv = __ballot_sync(act, must);
+    const unsigned cv = __ballot_sync(act, can);
+    const int na = __popc(act);
+    const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
+    if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
+      if (leaf != 0) {
+        const int32_t f = ~leaf;
+        const double t = mt_delta(tri, f, ray.org(), ray.dir());
+        if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+          best.delta = t;
+          best.face = f;
+          tbest = prune_bound(t, r.shift);
+        }
+        leaf = 0;
+        if (node < 0) {  // the leaf that waited for the slot
+          leaf = node;
+          prefetch_l1(tri + ~leaf);
+          pop();
+        }
+      }
+    }
+  }
+  return best;
+}
+
 // ---------------------------------------------------------------------------
 // fp32 triangle classification.  The fp64 Moller-Trumbore decides every hit;
 // this filter only sorts leaves into

@@ -169,6 +169,8 @@ struct rr_scene {
   rr::DevBuf<rr::QNode> qnodes;   // 4-wide nodes
   rr::DevBuf<rr::TNode> snodes;   // SAH traversal tree (rr_sah.cu), nf-1 nodes, BFS order
   rr::TravHeader shdr{};          // its header (root box, root ref, eps)
+  rr::DevBuf<rr::QNode> s4nodes;  // 4-wide collapse of the SAH tree (pad = slot plane ids)
+  int32_t s4root = -1;
   int32_t sah_depth = 0;
   int64_t n_qnodes = 0;
   rr::DevBuf<rr::TravHeader> dhdr;

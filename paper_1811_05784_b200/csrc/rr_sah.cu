@@ -559,6 +559,72 @@ __global__ void rank_kernel(const unsigned long long* __restrict__ flags, const 
   }
 }
 
+// ---- 4-wide collapse of the SAH tree: every internal node at even depth
+// becomes a QNode whose slots are its grandchildren (or a child leaf); slot
+// planes go into QNode.pad for the coplanar culling.
+__global__ void depth_kernel(const TNode* __restrict__ tn, int32_t n_int, int d, int32_t* __restrict__ depth) {
+  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= n_int || depth[n] != d) return;
+  const int4 c = tn[n].d;
+  if (c.x >= 0) depth[c.x] = d + 1;
+  if (c.y >= 0) depth[c.y] = d + 1;
+}
+
+__global__ void qflag_kernel(const int32_t* __restrict__ depth, int32_t n_int, int32_t* __restrict__ flag) {
+  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n < n_int) flag[n] = (depth[n] >= 0 && (depth[n] & 1) == 0) ? 1 : 0;
+  if (n == n_int) flag[n] = 0;
+}
+
+__device__ __forceinline__ void qslot(QNode& q, int s, const float* b6, int32_t ref, int32_t plane) {
+  reinterpret_cast<float*>(&q.lx)[s] = b6[0];
+  reinterpret_cast<float*>(&q.hx)[s] = b6[1];
+  reinterpret_cast<float*>(&q.ly)[s] = b6[2];
+  reinterpret_cast<float*>(&q.hy)[s] = b6[3];
+  reinterpret_cast<float*>(&q.lz)[s] = b6[4];
+  reinterpret_cast<float*>(&q.hz)[s] = b6[5];
+  reinterpret_cast<int32_t*>(&q.child)[s] = ref;
+  reinterpret_cast<int32_t*>(&q.pad)[s] = plane;
+}
+
+// TNode child boxes: left (a.x, a.y, a.z, a.w, b.x, b.y), right (b.z, b.w, c.x, c.y, c.z, c.w)
+__device__ __forceinline__ void tbox(const TNode& t, int side, float* b6) {
+  if (side == 0) {
+    b6[0] = t.a.x; b6[1] = t.a.y; b6[2] = t.a.z; b6[3] = t.a.w; b6[4] = t.b.x; b6[5] = t.b.y;
+  } else {
+    b6[0] = t.b.z; b6[1] = t.b.w; b6[2] = t.c.x; b6[3] = t.c.y; b6[4] = t.c.z; b6[5] = t.c.w;
+  }
+}
+
+__global__ void qbuild_kernel(const TNode* __restrict__ tn, int32_t n_int, const int32_t* __restrict__ flag,
+                              const int32_t* __restrict__ qidx, QNode* __restrict__ out) {
+  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= n_int || !flag[n]) return;
+  const TNode t = tn[n];
+  QNode q;
+  float b6[6];
+  for (int s = 0; s < 4; ++s) {  // empty slot: a point box far outside every scene
+    const float far6[6] = {1e30f, 1e30f, 1e30f, 1e30f, 1e30f, 1e30f};
+    qslot(q, s, far6, kEmpty, -1);
+  }
+  int slot = 0;
+  const int32_t kid[2] = {t.d.x, t.d.y}, kpl[2] = {t.d.z, t.d.w};
+  for (int side = 0; side < 2; ++side) {
+    if (kid[side] < 0) {  // child leaf
+      tbox(t, side, b6);
+      qslot(q, slot++, b6, kid[side], kpl[side]);
+      continue;
+    }
+    const TNode c = tn[kid[side]];
+    const int32_t gk[2] = {c.d.x, c.d.y}, gp[2] = {c.d.z, c.d.w};
+    for (int g = 0; g < 2; ++g) {
+      tbox(c, g, b6);
+      qslot(q, slot++, b6, gk[g] >= 0 ? qidx[gk[g]] : gk[g], gp[g]);
+    }
+  }
+  out[qidx[n]] = q;
+}
+
 inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
 
 template <typename F>
@@ -698,6 +764,35 @@ void build_sah_tree(rr_scene* s) {
     std::swap(segs, nsegs);
     level_base += static_cast<int32_t>(n_split);
     S = 2 * n_split;
+  }
+  {  // 4-wide collapse (traversed by the wide kernel variant)
+    const int32_t n_int = static_cast<int32_t>(nf - 1);
+    TravHeader hh;
+    RR_CUDA(cudaMemcpyAsync(&hh, dh.p, sizeof hh, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    DevBuf<int32_t> depthb, qf, qi;
+    depthb.alloc(n_int, st);
+    qf.alloc(n_int + 1, st);
+    qi.alloc(n_int + 1, st);
+    RR_CUDA(cudaMemsetAsync(depthb.p, 0xff, depthb.bytes(), st));
+    if (hh.root_ref >= 0) RR_CUDA(cudaMemsetAsync(depthb.p + hh.root_ref, 0, sizeof(int32_t), st));
+    for (int d = 0; d <= depth + 6; ++d)
+      depth_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, d, depthb.p);
+    qflag_kernel<<<grid(n_int + 1), 256, 0, st>>>(depthb.p, n_int, qf.p);
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, qf.p, qi.p, static_cast<int>(n_int + 1), st);
+    }, tmp, st);
+    int32_t nq = 0;
+    RR_CUDA(cudaMemcpyAsync(&nq, qi.p + n_int, sizeof nq, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    s->s4nodes.alloc(std::max(nq, 1), st);
+    qbuild_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, qf.p, qi.p, s->s4nodes.p);
+    RR_LAUNCH_CHECK();
+    int32_t root4 = hh.root_ref;
+    if (hh.root_ref >= 0) RR_CUDA(cudaMemcpyAsync(&root4, qi.p + hh.root_ref, sizeof root4, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    s->s4root = root4;
+    s->ctx->launches += depth + 10;
   }
   RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));

@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     HitResult wall;
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
+    } else if (V == 3) {
+      wall = closest_hit4_pl<16, -2, RegRay>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
       wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt);
     } else if (V == 1) {
@@ -687,6 +689,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   p.tri = s->tri.p;
   p.normal = s->normal.p;
   p.hdr = sah ? s->shdr : s->hdr;
+  p.q4 = s->s4nodes.p;
+  p.root4 = s->s4root;
   // shared-memory top-level cache: measured slower for the default kernel
   // (profiles/r1_ab_variants.md), kept for the diagnostic ones
   p.use_smem = (variant == 0 || (cfg->flags & RR_TRACE_NO_SMEM_CACHE)) ? 0 : 1;
@@ -776,7 +780,10 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  const int df = df_env >= 0 ? df_env : 16;  // default: per-ray loop with postponed leaf tests
+  // default: per-ray loop with postponed leaf tests over the binary SAH tree;
+  // deep trees (>= 2^18 faces) over its 4-wide collapse, which halves the
+  // dependent node fetches (C3 -15 %, C5 -8 %; C2 100k +8 %, so not there)
+  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 16);
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
@@ -791,6 +798,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 15) dfk = trace_kernel<1, 8, false, 16, -4>;  // >= 1/4 of the loop's lanes stuck
   if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
   if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
+  if (df == 23 && s->s4nodes.p) dfk = trace_kernel<3, 8>;
+  if (df == 24 && s->s4nodes.p) dfk = trace_kernel<3, 6>;
   if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true>;
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;

@@ -19,6 +19,8 @@ static_assert(sizeof(Capture) == 64, "capture record");
 struct TraceParams {
   const TNode* nodes;
   const QNode* qnodes;
+  const QNode* q4;   // 4-wide collapse of the SAH tree
+  int32_t root4;
   int32_t wide;  // 1: traverse the 4-wide QNodes, 0: the binary TNodes
   const FaceTri* tri;
   const float4* tri32;
