@@ -1,0 +1,343 @@
+// roomray_b200_io.hpp — host ingestion for the C++ facade: the OBJ subset and
+// the material table of the reference (obj_loader.hpp), so a reference
+// caller can load the same scene files and hand them to build_tree.
+//
+// Same record rules, errors and report as the reference:
+//   * `v x y z`, `f i j k ...` (1-based; negative indices count from the end;
+//     tokens i, i/j, i/j/k, i//k — only the vertex index is used),
+//     `usemtl name`, `#` comments, other records ignored, CRLF tolerated;
+//   * polygons are fan-triangulated; triangles with area <= 1e-12 m^2 are
+//     dropped with a warning "line N: degenerate face skipped";
+//   * ObjParseError (with the 1-based line) on malformed records, faces
+//     before any usemtl, fewer than 3 corners, out-of-range indices;
+//     UnresolvedMaterialError when a usemtl name is not in the table;
+//   * the material table is a JSON array of {"name": string, "absorption":
+//     [8 reals in [0, 1]]} (own minimal JSON reader, no dependency).
+// Mesh validation beyond the parser (TriangleMesh::validate) happens in
+// build_tree, on the device.
+#ifndef ROOMRAY_B200_IO_HPP
+#define ROOMRAY_B200_IO_HPP
+
+#include <cctype>
+#include <cerrno>
+#include <cmath>
+#include <cstdlib>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "roomray_b200.hpp"
+
+namespace roomray_b200 {
+
+struct LoadReport {
+  std::size_t vertex_count = 0;
+  std::size_t face_count = 0;
+  std::size_t degenerate_skipped = 0;
+  std::vector<std::string> warnings;
+};
+
+class ObjParseError : public std::runtime_error {
+ public:
+  ObjParseError(const std::string& what, int line) : std::runtime_error(what), line_(line) {}
+  int line() const { return line_; }
+
+ private:
+  int line_;
+};
+
+class UnresolvedMaterialError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+
+inline double tri_area(const Vec3& a, const Vec3& b, const Vec3& c) {
+  const double ux = b.x - a.x, uy = b.y - a.y, uz = b.z - a.z;
+  const double vx = c.x - a.x, vy = c.y - a.y, vz = c.z - a.z;
+  const double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
+  return 0.5 * std::sqrt((cx * cx + cy * cy) + cz * cz);
+}
+
+// ------------------------------------------------------------- tiny JSON
+struct Json {
+  enum Kind { Null, Bool, Num, Str, Arr, Obj } kind = Null;
+  bool b = false;
+  double num = 0.0;
+  std::string str;
+  std::vector<Json> arr;
+  std::vector<std::pair<std::string, Json>> obj;
+  const Json* get(const std::string& k) const {
+    for (const auto& kv : obj)
+      if (kv.first == k) return &kv.second;
+    return nullptr;
+  }
+};
+
+class JsonReader {
+ public:
+  explicit JsonReader(const std::string& t) : t_(t) {}
+  Json parse() {
+    Json v = value();
+    ws();
+    if (i_ != t_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  const std::string& t_;
+  std::size_t i_ = 0;
+  [[noreturn]] void fail(const std::string& m) const {
+    throw std::runtime_error("material table JSON: " + m + " at offset " + std::to_string(i_));
+  }
+  void ws() {
+    while (i_ < t_.size() && std::isspace(static_cast<unsigned char>(t_[i_]))) ++i_;
+  }
+  bool lit(const char* w) {
+    std::size_t n = std::char_traits<char>::length(w);
+    if (t_.compare(i_, n, w) == 0) {
+      i_ += n;
+      return true;
+    }
+    return false;
+  }
+  std::string string() {
+    if (t_[i_] != '"') fail("expected a string");
+    ++i_;
+    std::string out;
+    while (i_ < t_.size() && t_[i_] != '"') {
+      char c = t_[i_++];
+      if (c == '\\') {
+        if (i_ >= t_.size()) fail("bad escape");
+        const char e = t_[i_++];
+        switch (e) {
+          case 'n': c = '\n'; break;
+          case 't': c = '\t'; break;
+          case 'r': c = '\r'; break;
+          case 'b': c = '\b'; break;
+          case 'f': c = '\f'; break;
+          case 'u': {  // basic multilingual plane only, encoded as UTF-8
+            if (i_ + 4 > t_.size()) fail("bad \\u escape");
+            const unsigned cp = static_cast<unsigned>(std::stoul(t_.substr(i_, 4), nullptr, 16));
+            i_ += 4;
+            if (cp < 0x80) {
+              out += static_cast<char>(cp);
+            } else if (cp < 0x800) {
+              out += static_cast<char>(0xC0 | (cp >> 6));
+              out += static_cast<char>(0x80 | (cp & 0x3F));
+            } else {
+              out += static_cast<char>(0xE0 | (cp >> 12));
+              out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+              out += static_cast<char>(0x80 | (cp & 0x3F));
+            }
+            continue;
+          }
+          default: c = e;
+        }
+      }
+      out += c;
+    }
+    if (i_ >= t_.size()) fail("unterminated string");
+    ++i_;
+    return out;
+  }
+  Json value() {
+    ws();
+    if (i_ >= t_.size()) fail("unexpected end");
+    Json v;
+    const char c = t_[i_];
+    if (c == '[') {
+      v.kind = Json::Arr;
+      ++i_;
+      ws();
+      if (i_ < t_.size() && t_[i_] == ']') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        v.arr.push_back(value());
+        ws();
+        if (i_ < t_.size() && t_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < t_.size() && t_[i_] == ']') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or ']'");
+      }
+    }
+    if (c == '{') {
+      v.kind = Json::Obj;
+      ++i_;
+      ws();
+      if (i_ < t_.size() && t_[i_] == '}') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        ws();
+        std::string k = string();
+        ws();
+        if (i_ >= t_.size() || t_[i_] != ':') fail("expected ':'");
+        ++i_;
+        v.obj.emplace_back(std::move(k), value());
+        ws();
+        if (i_ < t_.size() && t_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < t_.size() && t_[i_] == '}') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or '}'");
+      }
+    }
+    if (c == '"') {
+      v.kind = Json::Str;
+      v.str = string();
+      return v;
+    }
+    if (lit("true")) {
+      v.kind = Json::Bool;
+      v.b = true;
+      return v;
+    }
+    if (lit("false")) {
+      v.kind = Json::Bool;
+      return v;
+    }
+    if (lit("null")) return v;
+    const char* start = t_.c_str() + i_;
+    char* end = nullptr;
+    v.num = std::strtod(start, &end);
+    if (end == start) fail("unexpected character");
+    i_ += static_cast<std::size_t>(end - start);
+    v.kind = Json::Num;
+    return v;
+  }
+};
+
+inline std::string read_file(const std::string& path, const char* what) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error(std::string("cannot open ") + what + ": " + path);
+  std::ostringstream b;
+  b << f.rdbuf();
+  return b.str();
+}
+
+}  // namespace detail
+
+/// parse_material_table (obj_loader.hpp): name -> Material.
+inline std::map<std::string, Material> parse_material_table(const std::string& json_text) {
+  const detail::Json doc = detail::JsonReader(json_text).parse();
+  if (doc.kind != detail::Json::Arr) throw std::runtime_error("material table must be a JSON array");
+  std::map<std::string, Material> table;
+  for (const detail::Json& e : doc.arr) {
+    const detail::Json* name = e.kind == detail::Json::Obj ? e.get("name") : nullptr;
+    const detail::Json* abs = e.kind == detail::Json::Obj ? e.get("absorption") : nullptr;
+    if (!name || name->kind != detail::Json::Str) throw std::runtime_error("material entry needs a string 'name'");
+    if (!abs) throw std::runtime_error("material '" + name->str + "' needs 'absorption'");
+    Material m;
+    m.name = name->str;
+    if (abs->kind != detail::Json::Arr || abs->arr.size() != static_cast<std::size_t>(kNumBands))
+      throw std::runtime_error("material '" + m.name + "' needs exactly " + std::to_string(kNumBands) +
+                               " absorption values");
+    for (int b = 0; b < kNumBands; ++b) {
+      if (abs->arr[b].kind != detail::Json::Num)
+        throw std::runtime_error("material '" + m.name + "' has a non-numeric absorption value");
+      m.absorption[b] = abs->arr[b].num;
+      if (m.absorption[b] < 0.0 || m.absorption[b] > 1.0)
+        throw std::runtime_error("material '" + m.name + "' has absorption outside [0,1]");
+    }
+    table[m.name] = m;
+  }
+  return table;
+}
+
+inline std::map<std::string, Material> load_material_table(const std::string& path) {
+  return parse_material_table(detail::read_file(path, "material table"));
+}
+
+/// parse_obj (obj_loader.hpp).
+inline TriangleMesh parse_obj(const std::string& text, const std::map<std::string, Material>& material_map,
+                              LoadReport* report = nullptr) {
+  TriangleMesh mesh;
+  LoadReport local;
+  std::map<std::string, int> ids;  // material name -> index in mesh.materials
+  int current = -1;
+  std::istringstream in(text);
+  std::string line;
+  int line_no = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    std::istringstream ls(line);
+    std::string tag;
+    if (!(ls >> tag) || tag[0] == '#') continue;
+    if (tag == "v") {
+      Vec3 v;
+      if (!(ls >> v.x >> v.y >> v.z)) throw ObjParseError("malformed vertex record", line_no);
+      mesh.vertices.push_back(v);
+    } else if (tag == "usemtl") {
+      std::string name;
+      if (!(ls >> name)) throw ObjParseError("usemtl without a material name", line_no);
+      const auto known = ids.find(name);
+      if (known != ids.end()) {
+        current = known->second;
+      } else {
+        const auto entry = material_map.find(name);
+        if (entry == material_map.end())
+          throw UnresolvedMaterialError("material '" + name + "' not found in the material table");
+        current = static_cast<int>(mesh.materials.size());
+        mesh.materials.push_back(entry->second);
+        ids.emplace(name, current);
+      }
+    } else if (tag == "f") {
+      std::vector<int> corners;
+      std::string token;
+      while (ls >> token) {
+        const std::string head = token.substr(0, token.find('/'));
+        const char* s = head.c_str();
+        char* end = nullptr;
+        errno = 0;
+        const long raw = head.empty() ? 0 : std::strtol(s, &end, 10);
+        if (head.empty() || end != s + head.size() || errno == ERANGE)
+          throw ObjParseError("malformed face index '" + token + "'", line_no);
+        long idx = raw < 0 ? raw + static_cast<long>(mesh.vertices.size()) + 1 : raw;  // -1 = last vertex
+        if (idx < 1 || idx > static_cast<long>(mesh.vertices.size()))
+          throw ObjParseError("vertex index " + std::to_string(raw) + " out of range", line_no);
+        corners.push_back(static_cast<int>(idx - 1));
+      }
+      if (corners.size() < 3) throw ObjParseError("face with fewer than 3 vertices", line_no);
+      if (current < 0) throw ObjParseError("face before any usemtl record", line_no);
+      for (std::size_t k = 1; k + 1 < corners.size(); ++k) {  // fan triangulation
+        const Triangle t{corners[0], corners[k], corners[k + 1], current};
+        if (detail::tri_area(mesh.vertices[t.a], mesh.vertices[t.b], mesh.vertices[t.c]) <= 1e-12) {
+          ++local.degenerate_skipped;
+          local.warnings.push_back("line " + std::to_string(line_no) + ": degenerate face skipped");
+          continue;
+        }
+        mesh.faces.push_back(t);
+      }
+    }
+  }
+  local.vertex_count = mesh.vertices.size();
+  local.face_count = mesh.faces.size();
+  if (report) *report = local;
+  return mesh;
+}
+
+inline TriangleMesh load_obj(const std::string& path, const std::map<std::string, Material>& material_map,
+                             LoadReport* report = nullptr) {
+  return parse_obj(detail::read_file(path, "mesh file"), material_map, report);
+}
+
+}  // namespace roomray_b200
+
+#endif  // ROOMRAY_B200_IO_HPP

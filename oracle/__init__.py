@@ -353,6 +353,13 @@ class Ref:
         L.rref_air_alpha.restype = C.c_double
         L.rref_air_alpha.argtypes = [_f64p, C.c_double]
         L.rref_band_filter.argtypes = [C.c_int, C.c_double, _f64p]
+        self.has_obj = hasattr(L, "rref_parse_obj")
+        if self.has_obj:
+            L.rref_parse_obj.restype = C.c_int
+            L.rref_parse_obj.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(_vp), C.POINTER(_i32)]
+            L.rref_obj_info.argtypes = [_vp] + [C.POINTER(_i64)] * 4
+            L.rref_obj_get.argtypes = [_vp, _f64p, _i32p, _f64p]
+            L.rref_obj_free.argtypes = [_vp]
         L.rref_factors.restype = C.c_int
         L.rref_factors.argtypes = [_i64, _f64p, _f64p, C.c_double, _f64p]
         L.rref_synthesize.restype = _i64
@@ -415,6 +422,27 @@ class Ref:
         if length:
             self.L.rref_synthesize(n, dist, energy, c, fs, band_mask, out.ctypes.data, length)
         return out
+
+    def parse_obj(self, obj_text: str, mat_json: str) -> dict:
+        """parse_material_table + parse_obj (obj_loader.cpp:25-152): {"ok": True,
+        vertices, faces, absorption, degenerate} or {"ok": False, "kind":
+        "parse" | "material" | "other", "line", "msg"}."""
+        h, line = _vp(), _i32()
+        rc = self.L.rref_parse_obj(obj_text.encode(), mat_json.encode(), C.byref(h), C.byref(line))
+        if rc:
+            return {"ok": False, "kind": {1: "parse", 2: "material"}.get(rc, "other"), "line": line.value,
+                    "msg": self.L.rref_last_error().decode()}
+        try:
+            nv, nf, nm, dg = (_i64() for _ in range(4))
+            self.L.rref_obj_info(h, C.byref(nv), C.byref(nf), C.byref(nm), C.byref(dg))
+            v = np.zeros(max(nv.value, 1) * 3)
+            f = np.zeros(max(nf.value, 1) * 4, np.int32)
+            a = np.zeros(max(nm.value, 1) * 8)
+            self.L.rref_obj_get(h, v, f, a)
+            return {"ok": True, "vertices": v[: 3 * nv.value].reshape(-1, 3), "faces": f[: 4 * nf.value].reshape(-1, 4),
+                    "absorption": a[: 8 * nm.value].reshape(-1, 8), "degenerate": dg.value}
+        finally:
+            self.L.rref_obj_free(h)
 
     def factors(self, dist, energy, c):
         """factors(build_pulse_trains(images, c)) (metrics.cpp:168-180):

@@ -31,6 +31,9 @@
 #include "roomray/image_sources.hpp"
 #include "roomray/mesh_gen.hpp"
 #include "roomray/metrics.hpp"
+#ifdef RREF_HAVE_OBJ
+#include "roomray/obj_loader.hpp"
+#endif
 #include "roomray/rir.hpp"
 #include "roomray/shoebox.hpp"
 #include "roomray/tracer.hpp"
@@ -431,6 +434,59 @@ int rref_factors(int64_t n, const double* dist, const double* energy, double c, 
     put(kNumBands, bf.mid);
   });
 }
+
+#ifdef RREF_HAVE_OBJ
+// parse_material_table + parse_obj (obj_loader.cpp:25-152).  Returns 0 ok,
+// 1 ObjParseError (*line set), 2 UnresolvedMaterialError, 3 other error;
+// the mesh stays in a handle for rref_obj_get.
+struct RefObj {
+  TriangleMesh mesh;
+  LoadReport report;
+};
+int rref_parse_obj(const char* obj_text, const char* mat_json, void** out, int32_t* line) {
+  *out = nullptr;
+  *line = 0;
+  try {
+    auto r = std::make_unique<RefObj>();
+    const auto table = parse_material_table(mat_json);
+    r->mesh = parse_obj(obj_text, table, &r->report);
+    *out = r.release();
+    return 0;
+  } catch (const ObjParseError& e) {
+    g_err = e.what();
+    *line = e.line();
+    return 1;
+  } catch (const UnresolvedMaterialError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+void rref_obj_info(void* h, int64_t* nv, int64_t* nf, int64_t* nmat, int64_t* degenerate) {
+  auto* r = static_cast<RefObj*>(h);
+  *nv = static_cast<int64_t>(r->mesh.vertices.size());
+  *nf = static_cast<int64_t>(r->mesh.faces.size());
+  *nmat = static_cast<int64_t>(r->mesh.materials.size());
+  *degenerate = static_cast<int64_t>(r->report.degenerate_skipped);
+}
+void rref_obj_get(void* h, double* verts, int32_t* tris, double* alpha) {
+  auto* r = static_cast<RefObj*>(h);
+  for (std::size_t i = 0; i < r->mesh.vertices.size(); ++i)
+    for (int k = 0; k < 3; ++k) verts[3 * i + k] = r->mesh.vertices[i][k];
+  for (std::size_t f = 0; f < r->mesh.faces.size(); ++f) {
+    const Triangle& t = r->mesh.faces[f];
+    tris[4 * f] = t.a;
+    tris[4 * f + 1] = t.b;
+    tris[4 * f + 2] = t.c;
+    tris[4 * f + 3] = t.material_id;
+  }
+  for (std::size_t m = 0; m < r->mesh.materials.size(); ++m)
+    for (int b = 0; b < kNumBands; ++b) alpha[kNumBands * m + b] = r->mesh.materials[m].absorption[b];
+}
+void rref_obj_free(void* h) { delete static_cast<RefObj*>(h); }
+#endif
 
 // Shoebox lattice oracle (shoebox.cpp:43-116): count, then fetch.
 void* rref_lattice(const double* dims, const double* walls_alpha /*6x8*/,
