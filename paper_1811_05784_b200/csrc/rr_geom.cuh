@@ -321,11 +321,12 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       }
     }
     // test when enough lanes hold a leaf, enough are stuck behind theirs, or
-    // no lane can advance without a test
+    // no lane can advance without a test (nothing to decide if none holds one)
     const unsigned act = __activemask();
+    const unsigned hv = __ballot_sync(act, leaf != 0);
+    if (hv == 0) continue;
     const bool can = node >= 0 && node != kDone;
     const bool must = leaf != 0 && !can;
-    const unsigned hv = __ballot_sync(act, leaf != 0);
     const unsigned mv = __ballot_sync(act, must);
     const unsigned cv = __ballot_sync(act, can);
     const int na = __popc(act);
