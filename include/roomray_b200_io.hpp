@@ -15,11 +15,17 @@
 //     [8 reals in [0, 1]]} (own minimal JSON reader, no dependency).
 // Mesh validation beyond the parser (TriangleMesh::validate) happens in
 // build_tree, on the device.
+//
+// RunConfig (run_config.hpp) and run_trace_pipeline (pipeline.hpp:38) run the
+// whole reference pipeline — load, tree, trace, image sources, pulse trains,
+// impulse response, perceptive factors — with every stage on the GPU.
 #ifndef ROOMRAY_B200_IO_HPP
 #define ROOMRAY_B200_IO_HPP
 
 #include <cctype>
 #include <cerrno>
+#include <chrono>
+#include <filesystem>
 #include <cmath>
 #include <cstdlib>
 #include <fstream>
@@ -336,6 +342,173 @@ inline TriangleMesh parse_obj(const std::string& text, const std::map<std::strin
 inline TriangleMesh load_obj(const std::string& path, const std::map<std::string, Material>& material_map,
                              LoadReport* report = nullptr) {
   return parse_obj(detail::read_file(path, "mesh file"), material_map, report);
+}
+
+// ------------------------------------------------------------------ run configuration (run_config.hpp)
+struct RunConfig {
+  std::string mesh_path;
+  std::string material_path;
+  SourceConfig source;
+  Receiver receiver;
+  AirModel air;
+  double speed_of_sound = 343.0;
+  double sample_rate = 44100.0;
+  double max_range = 0.0;  // 0 derives (r/2) * sqrt(N)
+  int max_iterations = 1000;
+  bool merge_coplanar = true;
+  bool deterministic = false;  // the GPU path is deterministic either way
+  int thread_count = 1;        // accepted, the GPU grid replaces it
+  std::string output_dir = "out";
+  bool dump_captures = false;
+  bool dump_tree_stats = false;
+
+  /// run_config.cpp:22-54: required mesh, materials, source{position,
+  /// ray_count}, receiver{center, radius}; optional air{...} and scalars.
+  static RunConfig from_json_text(const std::string& text) {
+    using detail::Json;
+    const Json doc = detail::JsonReader(text).parse();
+    if (doc.kind != Json::Obj) throw std::runtime_error("run config must be a JSON object");
+    auto at = [](const Json& o, const char* k) -> const Json& {
+      const Json* v = o.kind == Json::Obj ? o.get(k) : nullptr;
+      if (!v) throw std::runtime_error(std::string("run config: missing field '") + k + "'");
+      return *v;
+    };
+    auto num = [](const Json& v, const char* k) {
+      if (v.kind != Json::Num) throw std::runtime_error(std::string("run config: '") + k + "' must be a number");
+      return v.num;
+    };
+    auto str = [](const Json& v, const char* k) {
+      if (v.kind != Json::Str) throw std::runtime_error(std::string("run config: '") + k + "' must be a string");
+      return v.str;
+    };
+    auto vec3 = [&](const Json& v, const std::string& field) {
+      if (v.kind != Json::Arr || v.arr.size() != 3) throw std::invalid_argument(field + " must be an array of 3 numbers");
+      return Vec3{num(v.arr[0], field.c_str()), num(v.arr[1], field.c_str()), num(v.arr[2], field.c_str())};
+    };
+    auto opt_num = [&](const Json& o, const char* k, double d) {
+      const Json* v = o.get(k);
+      return v ? num(*v, k) : d;
+    };
+    auto opt_bool = [&](const Json& o, const char* k, bool d) {
+      const Json* v = o.get(k);
+      if (!v) return d;
+      if (v->kind != Json::Bool) throw std::runtime_error(std::string("run config: '") + k + "' must be a boolean");
+      return v->b;
+    };
+    RunConfig c;
+    c.mesh_path = str(at(doc, "mesh"), "mesh");
+    c.material_path = str(at(doc, "materials"), "materials");
+    const Json& src = at(doc, "source");
+    c.source.position = vec3(at(src, "position"), "source.position");
+    c.source.ray_count = static_cast<int>(num(at(src, "ray_count"), "ray_count"));
+    const Json& rec = at(doc, "receiver");
+    c.receiver.center = vec3(at(rec, "center"), "receiver.center");
+    c.receiver.radius = num(at(rec, "radius"), "radius");
+    if (const Json* air = doc.get("air")) {
+      c.air.enabled = opt_bool(*air, "enabled", true);
+      c.air.temperature_c = opt_num(*air, "temperature_c", 20.0);
+      c.air.relative_humidity = opt_num(*air, "relative_humidity", 50.0);
+      c.air.pressure_kpa = opt_num(*air, "pressure_kpa", 101.325);
+    }
+    c.speed_of_sound = opt_num(doc, "speed_of_sound", 343.0);
+    c.sample_rate = opt_num(doc, "sample_rate", 44100.0);
+    c.max_range = opt_num(doc, "max_range", 0.0);
+    c.max_iterations = static_cast<int>(opt_num(doc, "max_iterations", 1000));
+    c.merge_coplanar = opt_bool(doc, "merge_coplanar", true);
+    c.deterministic = opt_bool(doc, "deterministic", false);
+    c.thread_count = static_cast<int>(opt_num(doc, "thread_count", 1));
+    if (const Json* o = doc.get("output_dir")) c.output_dir = str(*o, "output_dir");
+    return c;
+  }
+
+  /// run_config.cpp:56-73: relative paths resolve against the config file.
+  static RunConfig from_json_file(const std::string& path) {
+    RunConfig c = from_json_text(detail::read_file(path, "config"));
+    const auto base = std::filesystem::path(path).parent_path();
+    for (std::string* p : {&c.mesh_path, &c.material_path})
+      if (!p->empty() && std::filesystem::path(*p).is_relative()) *p = (base / *p).string();
+    return c;
+  }
+
+  /// run_config.cpp:75-107: std::invalid_argument naming the field.
+  void validate() const {
+    if (!std::filesystem::exists(mesh_path)) throw std::invalid_argument("mesh: file does not exist: " + mesh_path);
+    if (!std::filesystem::exists(material_path))
+      throw std::invalid_argument("materials: file does not exist: " + material_path);
+    if (source.ray_count < 1) throw std::invalid_argument("source.ray_count: must be >= 1");
+    if (receiver.radius <= 0.0) throw std::invalid_argument("receiver.radius: must be > 0");
+    if (speed_of_sound <= 0.0) throw std::invalid_argument("speed_of_sound: must be > 0");
+    if (sample_rate < 2.0 * kBandCentersHz[kNumBands - 1] * std::sqrt(2.0))
+      throw std::invalid_argument("sample_rate: must be >= twice the top band edge (22628 Hz)");
+    if (max_iterations < 1) throw std::invalid_argument("max_iterations: must be >= 1");
+    if (thread_count < 1) throw std::invalid_argument("thread_count: must be >= 1");
+    if (air.enabled) {  // AirModel::validate (air_absorption.cpp:8-19)
+      if (air.temperature_c < -20.0 || air.temperature_c > 50.0)
+        throw std::invalid_argument("air: air temperature outside [-20, 50] C");
+      if (air.relative_humidity < 10.0 || air.relative_humidity > 100.0)
+        throw std::invalid_argument("air: relative humidity outside [10, 100] %");
+      if (air.pressure_kpa < 80.0 || air.pressure_kpa > 120.0)
+        throw std::invalid_argument("air: pressure outside [80, 120] kPa");
+    }
+  }
+};
+
+// ------------------------------------------------------------------ pipeline (pipeline.hpp)
+struct StageTiming {
+  std::string name;
+  double seconds = 0.0;
+};
+
+struct RunArtifacts {
+  TriangleMesh mesh;
+  AccelTree tree;
+  LoadReport load_report;
+  TraceResult trace;
+  std::vector<ImageSource> images;
+  PulseTrains trains;
+  RoomImpulseResponse rir;
+  BandFactors metrics;
+  std::vector<StageTiming> timings;
+  double total_seconds = 0.0;
+  double tree_build_seconds = 0.0;
+};
+
+/// run_trace_pipeline (pipeline.cpp:144-185) with every stage on the GPU.
+inline RunArtifacts run_trace_pipeline(const RunConfig& config) {
+  config.validate();
+  RunArtifacts a;
+  using clock = std::chrono::steady_clock;
+  const auto start = clock::now();
+  auto last = start;
+  auto mark = [&](const char* name) {
+    const auto now = clock::now();
+    a.timings.push_back({name, std::chrono::duration<double>(now - last).count()});
+    last = now;
+  };
+  a.mesh = load_obj(config.mesh_path, load_material_table(config.material_path), &a.load_report);
+  mark("load");
+  a.tree = build_tree(a.mesh);
+  mark("tree_build");
+  a.tree_build_seconds = a.timings.back().seconds;
+  TraceConfig tc;
+  tc.max_iterations = config.max_iterations;
+  tc.speed_of_sound = config.speed_of_sound;
+  tc.max_range = config.max_range;
+  tc.thread_count = config.deterministic ? 1 : config.thread_count;
+  a.trace = trace(a.mesh, a.tree, config.source, config.receiver, tc);
+  mark("trace");
+  ClusterOptions co;
+  co.merge_coplanar = config.merge_coplanar;
+  a.images = build_image_sources(a.trace.captures, config.source.ray_count, config.air, config.receiver.center,
+                                 a.mesh, a.tree, co);
+  mark("image_sources");
+  a.trains = build_pulse_trains(a.images, config.speed_of_sound);
+  a.rir = synthesize(a.trains, config.sample_rate);
+  mark("rir");
+  a.metrics = factors(a.trains);
+  mark("metrics");
+  a.total_seconds = std::chrono::duration<double>(clock::now() - start).count();
+  return a;
 }
 
 }  // namespace roomray_b200

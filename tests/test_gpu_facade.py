@@ -109,3 +109,99 @@ def test_facade_matches_oracle(tmp_path, port, merge):
         np.testing.assert_allclose(fac[:, :, 0], want_f[:, :, 0], rtol=1e-6, atol=1e-9)
     bands = np.fromfile(out / "rir_bands.f64").reshape(8, -1)
     np.testing.assert_allclose(bands.sum(0), rir, rtol=0, atol=1e-12 * peak)
+
+
+# ---------------------------------------------------------------- pipeline
+PIPE_SRC = os.path.join(ROOT, "tests", "native", "pipeline_run.cpp")
+CONCRETE = [0.36, 0.36, 0.44, 0.31, 0.29, 0.39, 0.25, 0.25]
+PODIUM = [0.4, 0.4, 0.3, 0.2, 0.17, 0.15, 0.1, 0.1]
+BOX_OBJ = """# [5, 4, 3] m rectangular room, one material group per wall
+v 0 0 0
+v 5 0 0
+v 5 4 0
+v 0 4 0
+v 0 0 3
+v 5 0 3
+v 5 4 3
+v 0 4 3
+usemtl concrete_block_coarse
+f 1 5 8 4
+usemtl hollow_wooden_podium
+f 2 3 7 6
+usemtl concrete_block_coarse
+f 1 2 6 5
+usemtl hollow_wooden_podium
+f 4 8 7 3
+usemtl concrete_block_coarse
+f 1 4 3 2
+usemtl hollow_wooden_podium
+f 5 6 7 8
+"""
+
+
+def _pipeline_files(tmp_path, **over):
+    import json
+    mats = [{"name": "concrete_block_coarse", "absorption": CONCRETE},
+            {"name": "hollow_wooden_podium", "absorption": PODIUM}]
+    (tmp_path / "room.obj").write_text(BOX_OBJ)
+    (tmp_path / "materials.json").write_text(json.dumps(mats))
+    run = {"mesh": "room.obj", "materials": "materials.json", "source": {"position": [4, 2, 1.7], "ray_count": 20000},
+           "receiver": {"center": [2, 2, 1.7], "radius": 0.2},
+           "air": {"enabled": True, "temperature_c": 20, "relative_humidity": 50, "pressure_kpa": 101.325},
+           "speed_of_sound": 343.0, "sample_rate": 44100.0, "max_iterations": 1000, "merge_coplanar": True}
+    run.update(over)
+    (tmp_path / "run.json").write_text(json.dumps(run))
+    return tmp_path / "run.json"
+
+
+def _compile_pipeline(out):
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    PIPE_SRC, "-L", os.path.join(ROOT, "paper_1811_05784_b200"), "-lroomray_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_1811_05784_b200"), "-o", out], check=True)
+    return out
+
+
+@pytest.mark.parametrize("over,msg", [({"source": {"position": [4, 2, 1.7], "ray_count": 0}},
+                                       "source.ray_count: must be >= 1"),
+                                      ({"mesh": "missing.obj"}, "mesh: file does not exist"),
+                                      ({"sample_rate": 8000.0}, "sample_rate: must be >= twice"),
+                                      ({"air": {"temperature_c": 90}}, "air: air temperature outside")])
+def test_pipeline_config_errors(tmp_path, over, msg):
+    """RunConfig::validate (run_config.cpp:75-107) fails before any GPU work."""
+    exe = _compile_pipeline(str(tmp_path / "pipeline_run"))
+    out = tmp_path / "out"
+    out.mkdir()
+    r = subprocess.run([exe, str(_pipeline_files(tmp_path, **over)), str(out)], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 3 and msg in r.stdout, (r.returncode, r.stdout, r.stderr)
+
+
+@pytest.mark.gpu
+def test_pipeline_matches_oracle(tmp_path, port, ref):
+    """run_trace_pipeline on the reference's shoebox fixture shape: images,
+    RIR and factors against the reference's own stages."""
+    import oracle
+    exe = _compile_pipeline(str(tmp_path / "pipeline_run"))
+    out = tmp_path / "out"
+    out.mkdir()
+    r = subprocess.run([exe, str(_pipeline_files(tmp_path)), str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "pipeline ok" in r.stdout
+    mesh = ref.parse_obj(BOX_OBJ, open(tmp_path / "materials.json").read())
+    assert mesh["ok"] and len(mesh["faces"]) == 12
+    sc = port.scene(oracle.Mesh(mesh["vertices"], mesh["faces"], mesh["absorption"]))
+    cap, _ = sc.trace((4, 2, 1.7), 20000, [(2, 2, 1.7)], [0.2], 1000, 0.0)
+    want = sc.image_sources(cap, 20000, np.array([1.0, 20.0, 50.0, 101.325]), np.array([2, 2, 1.7]), 1e-6, True)
+    img = np.fromfile(out / "images.f64").reshape(-1, 14)
+    assert len(img) == len(want) > 10
+    np.testing.assert_allclose(img[:, 0:3], want.pos, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(img[:, 4:12], want.energy, rtol=1e-9)
+    assert np.array_equal(img[:, 12], want.ray_count) and np.array_equal(img[:, 13], want.order)
+    rir = np.fromfile(out / "rir.f64")
+    w = ref.synthesize(want.dist, want.energy, 343.0, 44100.0)
+    assert len(rir) == len(w)
+    np.testing.assert_allclose(rir, w, rtol=0, atol=1e-6 * np.abs(w).max())
+    fac = np.fromfile(out / "factors.f64").reshape(9, 6, 2)
+    wf = ref.factors(want.dist, want.energy, 343.0)
+    assert np.array_equal(fac[:, :, 1], wf[:, :, 1])
+    np.testing.assert_allclose(fac[:, :, 0], wf[:, :, 0], rtol=1e-6, atol=1e-9)
