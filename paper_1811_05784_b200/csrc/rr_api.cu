@@ -149,7 +149,7 @@ rr_status rr_ctx_destroy(rr_ctx* ctx) {
 }
 
 void* rr_ctx_stream(rr_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->stream) : nullptr; }
-int64_t rr_ctx_launches(rr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t rr_ctx_launches(rr_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 rr_status rr_scene_create(rr_ctx* ctx, const double* verts, int64_t nv, const int32_t* tris, int64_t nf,
                           const double* alpha, int32_t nmat, int32_t validate, rr_scene** out) {

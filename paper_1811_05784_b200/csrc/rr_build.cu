@@ -27,7 +27,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <exception>
 #include <map>
+#include <thread>
 
 #include "rr_internal.cuh"
 
@@ -511,6 +513,92 @@ void build_scene_tree(rr_scene* s) {
   RR_LAUNCH_CHECK();
   s->ctx->launches++;
 
+  // ---- axis-aligned plane tables: per axis, the sorted unique plane
+  // coordinates of the flat faces; ids for faces and for tree children
+  DevBuf<unsigned long long> table;
+  DevBuf<int64_t> doff;
+  {
+    DevBuf<unsigned long long> pkeys, psorted;
+    DevBuf<int> dnum;
+    DevBuf<uint8_t> ptmp;
+    pkeys.alloc(nf, st);
+    psorted.alloc(nf, st);
+    table.alloc(3 * nf, st);
+    doff.alloc(4, st);
+    dnum.alloc(1, st);
+    int64_t hoff[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 3; ++k) {
+      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
+      RR_LAUNCH_CHECK();
+      size_t need = 0;
+      RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+      size_t need2 = 0;
+      RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf),
+                                        st));
+      if (std::max(need, need2) > ptmp.n) ptmp.alloc(std::max(need, need2), st);
+      size_t t = ptmp.n;
+      RR_CUDA(cub::DeviceRadixSort::SortKeys(ptmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+      t = ptmp.n;
+      RR_CUDA(cub::DeviceSelect::Unique(ptmp.p, t, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf), st));
+      int num = 0;
+      unsigned long long last = 0;
+      RR_CUDA(cudaMemcpyAsync(&num, dnum.p, sizeof num, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      if (num > 0)
+        RR_CUDA(cudaMemcpyAsync(&last, table.p + hoff[k] + num - 1, sizeof last, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      if (num > 0 && last == ~0ull) --num;  // the "not flat on k" sentinel
+      hoff[k + 1] = hoff[k] + num;
+      s->ctx->launches += 6;
+    }
+    RR_CUDA(cudaMemcpyAsync(doff.p, hoff, sizeof hoff, cudaMemcpyHostToDevice, st));
+    s->face_plane.alloc(nf, st);
+    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 1;
+    RR_CUDA(cudaStreamSynchronize(st));  // hoff is a stack array
+  }
+
+  // ---- the SAH traversal tree (rr_sah.cu) needs only the faces and their
+  // plane ids: build it on a second stream from a second host thread while
+  // this thread builds the reference tree
+  cudaStream_t st2 = nullptr;
+  RR_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  cudaEvent_t ready;
+  RR_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  RR_CUDA(cudaEventRecord(ready, st));
+  RR_CUDA(cudaStreamWaitEvent(st2, ready, 0));
+  cudaEventDestroy(ready);
+  std::exception_ptr sah_error;
+  float sah_ms = 0.f;
+  std::thread sah_thread([s, st2, &sah_error, &sah_ms] {
+    try {
+      RR_CUDA(cudaSetDevice(s->ctx->device));
+      cudaEvent_t a0, a1;
+      RR_CUDA(cudaEventCreate(&a0));
+      RR_CUDA(cudaEventCreate(&a1));
+      RR_CUDA(cudaEventRecord(a0, st2));
+      build_sah_tree(s, st2);
+      RR_CUDA(cudaEventRecord(a1, st2));
+      RR_CUDA(cudaEventSynchronize(a1));
+      RR_CUDA(cudaEventElapsedTime(&sah_ms, a0, a1));
+      cudaEventDestroy(a0);
+      cudaEventDestroy(a1);
+    } catch (...) {
+      sah_error = std::current_exception();
+    }
+  });
+  struct Joiner {  // join on every exit path (exceptions included)
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{sah_thread};
+  // large scenes keep the GPU busy with one build at a time (C5: 27 ms
+  // sequential vs 33 ms overlapped); small ones are launch-latency bound and
+  // overlap well (C2: 6.1 -> 4.8 ms)
+  if (nf > (int64_t(1) << 18)) sah_thread.join();
+
   // ---- CUB scratch
   size_t tmp_sort = 0, tmp_scan = 0, tmp_scan2 = 0;
   RR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys.p, keys_out.p, ids.p, permA.p,
@@ -568,54 +656,11 @@ void build_scene_tree(rr_scene* s) {
   }
 
   tm.mark("build: reference levels");
-  // ---- axis-aligned plane tables: per axis, the sorted unique plane
-  // coordinates of the flat faces; ids for faces and for tree children
-  {
-    DevBuf<unsigned long long> pkeys, psorted, table;
-    DevBuf<int64_t> doff;
-    DevBuf<int> dnum;
-    pkeys.alloc(nf, st);
-    psorted.alloc(nf, st);
-    table.alloc(3 * nf, st);
-    doff.alloc(4, st);
-    dnum.alloc(1, st);
-    int64_t hoff[4] = {0, 0, 0, 0};
-    for (int k = 0; k < 3; ++k) {
-      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
-      RR_LAUNCH_CHECK();
-      size_t need = 0;
-      RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-      size_t need2 = 0;
-      RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf),
-                                        st));
-      if (std::max(need, need2) > tmp.n) tmp.alloc(std::max(need, need2), st);
-      size_t t = tmp.n;
-      RR_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-      t = tmp.n;
-      RR_CUDA(cub::DeviceSelect::Unique(tmp.p, t, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf), st));
-      int num = 0;
-      unsigned long long last = 0;
-      RR_CUDA(cudaMemcpyAsync(&num, dnum.p, sizeof num, cudaMemcpyDeviceToHost, st));
-      RR_CUDA(cudaStreamSynchronize(st));
-      if (num > 0)
-        RR_CUDA(cudaMemcpyAsync(&last, table.p + hoff[k] + num - 1, sizeof last, cudaMemcpyDeviceToHost, st));
-      RR_CUDA(cudaStreamSynchronize(st));
-      if (num > 0 && last == ~0ull) --num;  // the "not flat on k" sentinel
-      hoff[k + 1] = hoff[k] + num;
-      s->ctx->launches += 6;
-    }
-    RR_CUDA(cudaMemcpyAsync(doff.p, hoff, sizeof hoff, cudaMemcpyHostToDevice, st));
-    s->face_plane.alloc(nf, st);
-    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
-    RR_LAUNCH_CHECK();
-    node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, table.p, doff.p,
-                                                           s->tnodes.p);
-    RR_LAUNCH_CHECK();
-    s->ctx->launches += 2;
-    RR_CUDA(cudaStreamSynchronize(st));  // hoff is a stack array
-  }
-
   tm.mark("build: plane tables");
+  node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, table.p, doff.p,
+                                                         s->tnodes.p);
+  RR_LAUNCH_CHECK();
+  s->ctx->launches++;
   // ---- 4-wide collapse
   int32_t k4 = 0;
   {
@@ -674,22 +719,15 @@ void build_scene_tree(rr_scene* s) {
   s->hdr.depth = s->depth;
   RR_CUDA(cudaMemcpyAsync(s->dhdr.p, &s->hdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
   RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));
-  {  // traversal tree (SAH), timed separately into build_ms
-    cudaEvent_t a0, a1;
-    RR_CUDA(cudaEventCreate(&a0));
-    RR_CUDA(cudaEventCreate(&a1));
-    RR_CUDA(cudaEventRecord(a0, st));
-    tm.mark("build: bounds");
-    build_sah_tree(s);
-    tm.mark("build: SAH tree");
-    RR_CUDA(cudaEventRecord(a1, st));
-    RR_CUDA(cudaEventSynchronize(a1));
-    float ms = 0.f;
-    RR_CUDA(cudaEventElapsedTime(&ms, a0, a1));
-    s->build_ms += ms;
-    cudaEventDestroy(a0);
-    cudaEventDestroy(a1);
-  }
+  if (sah_thread.joinable()) sah_thread.join();
+  RR_CUDA(cudaStreamSynchronize(st2));
+  // the SAH buffers were allocated on st2: later frees go to the scene's stream
+  s->snodes.s = st;
+  s->s4nodes.s = st;
+  cudaStreamDestroy(st2);
+  if (sah_error) std::rethrow_exception(sah_error);
+  tm.mark("build: SAH tree (joined)");
+  s->build_ms = std::max(s->build_ms, sah_ms);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }

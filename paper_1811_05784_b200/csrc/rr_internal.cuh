@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -147,7 +149,7 @@ struct rr_ctx {
   int refs = 1;
   int device = 0;
   cudaStream_t stream = nullptr;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};  // the scene build counts from two host threads
   int sm_count = 0;
 };
 
@@ -184,8 +186,8 @@ struct rr_scene {
 namespace rr {
 // rr_build.cu
 void build_scene_tree(rr_scene* s);
-// rr_sah.cu (needs face_plane and hdr from build_scene_tree)
-void build_sah_tree(rr_scene* s);
+// rr_sah.cu (needs face_plane; runs on its own stream)
+void build_sah_tree(rr_scene* s, cudaStream_t st);
 // rr_trace.cu
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
                        int64_t n, int brute, int32_t* d_face, double* d_delta,

@@ -233,6 +233,25 @@ __device__ __forceinline__ float half_area(const float* lo, const float* hi) {
   return dx * dy + dy * dz + dz * dx;
 }
 
+// root box and box expansion of the SAH tree, as rr_build.cu's level 0 does
+// for the reference tree (same union of face boxes, hence the same values)
+__global__ void root_hdr_kernel(const unsigned long long* __restrict__ bb, TravHeader* __restrict__ hdr) {
+  if (threadIdx.x) return;
+  double lo[3], hi[3];
+  double scale = 1e-3;
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = oval(bb[k]);
+    hi[k] = oval(bb[3 + k]);
+    scale = fmax(scale, fmax(fabs(lo[k]), fabs(hi[k])));
+  }
+  const float eps = __double2float_ru(scale * 0x1p-19);  // see rr_geom.cuh box_enter
+  hdr->eps = eps;
+  for (int k = 0; k < 3; ++k) {
+    hdr->lo[k] = lo_f(lo[k], eps);
+    hdr->hi[k] = hi_f(hi[k], eps);
+  }
+}
+
 // 3. node emission and split choice
 __global__ void split_kernel(const SSeg* __restrict__ segs, int64_t S, const int32_t* __restrict__ rank,
                              const unsigned long long* __restrict__ bb, const unsigned long long* __restrict__ cb,
@@ -638,16 +657,9 @@ void cub_run(F&& f, DevBuf<uint8_t>& tmp, cudaStream_t st) {
 
 }  // namespace
 
-void build_sah_tree(rr_scene* s) {
-  cudaStream_t st = s->ctx->stream;
+void build_sah_tree(rr_scene* s, cudaStream_t st) {
   const int64_t nf = s->nf;
-  s->shdr = s->hdr;  // root box, eps, K = 0
-  s->shdr.K = 0;
-  if (nf < 2) {
-    s->snodes.alloc(1, st);
-    RR_CUDA(cudaMemsetAsync(s->snodes.p, 0, sizeof(TNode), st));
-    return;
-  }
+  if (nf < 2) return;  // a one-face scene is traversed through the reference tree
   DevBuf<double> fb, cen;
   DevBuf<uint64_t> keys, keys_o;
   DevBuf<int32_t> ids, permA, permB, posA, posB, fl, scan;
@@ -675,7 +687,7 @@ void build_sah_tree(rr_scene* s) {
   RR_CUDA(cudaMemsetAsync(s->snodes.p, 0, s->snodes.bytes(), st));
   DevBuf<TravHeader> dh;
   dh.alloc(1, st);
-  RR_CUDA(cudaMemcpyAsync(dh.p, &s->shdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
+  RR_CUDA(cudaMemsetAsync(dh.p, 0, sizeof(TravHeader), st));
   RR_CUDA(cudaMemsetAsync(posA.p, 0, sizeof(int32_t) * nf, st));
 
   int64_t max_seg = nf;  // segments per level never exceed the face count
@@ -708,7 +720,7 @@ void build_sah_tree(rr_scene* s) {
   top.alloc(1, st);
   RR_CUDA(cudaMemsetAsync(top.p, 0, sizeof(unsigned long long), st));
   int depth = 0;
-  const float eps = s->hdr.eps;
+  float eps = 0.f;  // from the root box, read back with level 0's counts
   StageTimer tm(st);
   for (int L = 0; S > 0; ++L) {
     depth = L;
@@ -716,6 +728,7 @@ void build_sah_tree(rr_scene* s) {
     // 1. bounds (one init launch for the per-segment accumulators)
     seg_init_kernel<<<grid(S), 256, 0, st>>>(S, bb.p, cb.p, pl.p);
     bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
+    if (L == 0) root_hdr_kernel<<<1, 32, 0, st>>>(bb.p, dh.p);
     // 2. split flags and SAH flags, both ranks from one 64-bit scan
     //    (split flag in the high word, SAH flag in the low word)
     split_flag_kernel<<<grid(S + 1), 256, 0, st>>>(segs, S, L, flags.p);
@@ -725,6 +738,7 @@ void build_sah_tree(rr_scene* s) {
     }, tmp, st);
     unsigned long long both = 0;
     RR_CUDA(cudaMemcpyAsync(&both, franks.p + S, sizeof both, cudaMemcpyDeviceToHost, st));
+    if (L == 0) RR_CUDA(cudaMemcpyAsync(&eps, &dh.p->eps, sizeof eps, cudaMemcpyDeviceToHost, st));
     RR_CUDA(cudaStreamSynchronize(st));
     const int64_t n_split = static_cast<int64_t>(both >> 32), n_sah = static_cast<int64_t>(both & 0xffffffffull);
     // srank[j] / sah_idx[j] (compact index, -1 for non-SAH segments), bins reset
@@ -797,6 +811,8 @@ void build_sah_tree(rr_scene* s) {
   RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
   s->shdr.K = 0;
+  s->shdr.K4 = 0;
+  s->shdr.root4 = 0;
   s->sah_depth = depth;
   if (depth > kMaxDepth) throw Error(RR_RUNTIME, "SAH tree deeper than the traversal stack");
 }
