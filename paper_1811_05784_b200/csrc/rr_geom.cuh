@@ -435,9 +435,10 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
       pop();
     }
     const unsigned act = __activemask();
+    const unsigned hv = __ballot_sync(act, leaf != 0);
+    if (hv == 0) continue;  // no lane holds a leaf: nothing to decide
     const bool can = node >= 0 && node != kDone;
     const bool must = leaf != 0 && !can;
-    const unsigned hv = __ballot_sync(act, leaf != 0);
     const unsigned mv = __ballot_sync(act, must);
     const unsigned cv = __ballot_sync(act, can);
     const int na = __popc(act);
