@@ -213,21 +213,28 @@ __global__ void gather_retro_kernel(const int32_t* __restrict__ idx, int64_t n, 
 __global__ void group_count_kernel(int32_t* __restrict__ idx, const int64_t* __restrict__ gstart, int64_t ng,
                                    int64_t n, const double* __restrict__ retro, const double* __restrict__ rs,
                                    int64_t c0, double tol, int32_t* __restrict__ n_img,
-                                   int32_t* __restrict__ is_split) {
+                                   int32_t* __restrict__ is_split, double* __restrict__ gmean) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n, m = e - s;
   D3 mean = d3(0, 0, 0);
   for (int64_t i = s; i < e; ++i) mean = mean + ld3(rs, i);  // capture order, as the reference
   mean = d3(mean.x / static_cast<double>(m), mean.y / static_cast<double>(m), mean.z / static_cast<double>(m));
-  double spread = 0.0;
+  // max of the norms = sqrt of the max squared norm (sqrt is monotone and
+  // correctly rounded): one square root per group, the same bits
+  double spread2 = 0.0;
   for (int64_t i = s; i < e; ++i) {
-    const double dd = norm3(ld3(rs, i) - mean);
-    spread = (spread < dd) ? dd : spread;
+    const D3 v = ld3(rs, i) - mean;
+    const double q = dot(v, v);
+    spread2 = (spread2 < q) ? q : spread2;
   }
+  const double spread = sqrt(spread2);
   if (spread <= tol) {
     n_img[g] = 1;
     is_split[g] = 0;
+    gmean[3 * g] = mean.x;  // make_image's position for the unsplit group
+    gmean[3 * g + 1] = mean.y;
+    gmean[3 * g + 2] = mean.z;
     return;
   }
   is_split[g] = 1;
@@ -269,18 +276,16 @@ __device__ void emit_image(const int32_t* idx, int64_t b0, int64_t b1, const dou
 __global__ void group_emit_kernel(const int32_t* __restrict__ idx, const int64_t* __restrict__ gstart, int64_t ng,
                                   int64_t n, const double* __restrict__ retro, const double* __restrict__ rs,
                                   int64_t c0, double tol, const int32_t* __restrict__ is_split,
-                                  const int32_t* __restrict__ img_off, const int64_t* __restrict__ off, ImgTmp t) {
+                                  const int32_t* __restrict__ img_off, const int64_t* __restrict__ off,
+                                  const double* __restrict__ gmean, ImgTmp t) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n;
   int64_t slot = img_off[g];
-  if (!is_split[g]) {  // make_image over the whole group, contiguous retro points
-    D3 sum = d3(0, 0, 0);
-    for (int64_t i = s; i < e; ++i) sum = sum + ld3(rs, i);
-    const double m = static_cast<double>(e - s);
-    t.pos[3 * slot] = sum.x / m;
-    t.pos[3 * slot + 1] = sum.y / m;
-    t.pos[3 * slot + 2] = sum.z / m;
+  if (!is_split[g]) {  // make_image over the whole group: the mean computed by the count pass
+    t.pos[3 * slot] = gmean[3 * g];
+    t.pos[3 * slot + 1] = gmean[3 * g + 1];
+    t.pos[3 * slot + 2] = gmean[3 * g + 2];
     t.count[slot] = static_cast<int32_t>(e - s);
     const int32_t rep = idx[s];
     t.rep[slot] = rep;
@@ -478,6 +483,9 @@ __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict
   int32_t rep = t.rep[i];
   const int32_t q0 = claim_start[i];
   if (q0 >= 0) {
+    // the reference keeps the lexicographically smallest face path
+    // (image_sources.cpp:121-123); images are indexed in path order and every
+    // claim j > i, so that is always the anchor's own path
     for (int64_t q = q0; q < n && claims[q] != ~0ull &&
                          static_cast<uint32_t>(claims[q] >> 32) == static_cast<uint32_t>(i);
          ++q) {
@@ -485,7 +493,6 @@ __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict
       const double cj = static_cast<double>(t.count[j]);
       w = w + d3(t.pos[3 * j] * cj, t.pos[3 * j + 1] * cj, t.pos[3 * j + 2] * cj);
       cnt += t.count[j];
-      if (pv.cmp(t.rep[j], rep) < 0) rep = t.rep[j];
     }
   }
   const int64_t s = anchor_rank[i];
@@ -721,10 +728,30 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   rs.alloc(3 * n, st);
   gather_retro_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, retro.p, c0, rs.p);
   tm.mark("groups: heads");
+  DevBuf<double> gmean;
+  gmean.alloc(3 * ng, st);
   group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, n_img.p,
-                                                    is_split.p);
+                                                    is_split.p, gmean.p);
   RR_LAUNCH_CHECK();
   tm.mark("groups: count");
+  if (tm.on) {  // group statistics (development)
+    std::vector<int64_t> gs(ng + 1);
+    std::vector<int32_t> sp(ng);
+    RR_CUDA(cudaMemcpyAsync(gs.data(), gstart.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaMemcpyAsync(sp.data(), is_split.p, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    gs[ng] = n;
+    int64_t mx = 0, nsplit = 0, mxs = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+      mx = std::max(mx, gs[g + 1] - gs[g]);
+      if (sp[g]) {
+        ++nsplit;
+        mxs = std::max(mxs, gs[g + 1] - gs[g]);
+      }
+    }
+    std::fprintf(stderr, "[rr timing] groups: %lld, largest %lld, split %lld (largest split %lld)\n", (long long)ng,
+                 (long long)mx, (long long)nsplit, (long long)mxs);
+  }
   RR_CUDA(cudaMemsetAsync(n_img.p + ng, 0, sizeof(int32_t), st));
   cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, n_img.p, img_off.p, ng + 1, st); },
            st);
@@ -740,7 +767,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   trep.alloc(2 * ni, st);
   ImgTmp T{tpos.p, tcount.p, torder.p, trep.p};
   group_emit_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, is_split.p,
-                                                   img_off.p, tr->c_off.p, T);
+                                                   img_off.p, tr->c_off.p, gmean.p, T);
   RR_LAUNCH_CHECK();
   ctx->launches += 8;
   tm.mark("groups");
