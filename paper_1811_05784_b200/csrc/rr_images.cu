@@ -553,18 +553,41 @@ __global__ void energy_kernel(ImgTmp t, const int32_t* __restrict__ mult_src, in
   proj[3 * i + 2] = pt.z;
 }
 
-// final order (order, distance, face path), image_sources.cpp:163-168
-struct FinalLess {
-  const int32_t* order;
-  const double* dist;
-  const int32_t* rep;
-  PathView pv;
-  __device__ bool operator()(int32_t a, int32_t b) const {
-    if (order[a] != order[b]) return order[a] < order[b];
-    if (dist[a] != dist[b]) return dist[a] < dist[b];
-    return pv.cmp(rep[a], rep[b]) < 0;
+// final order (order, distance, face path), image_sources.cpp:163-168: see the final sort
+
+// final sort keys: distance bits (64) or order (32) of image perm[i]
+__global__ void final_key_kernel(const int32_t* __restrict__ perm, int64_t n, const double* __restrict__ dist,
+                                 const int32_t* __restrict__ order, unsigned long long* __restrict__ kd,
+                                 uint32_t* __restrict__ ko) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t s = perm[i];
+  if (kd) kd[i] = static_cast<unsigned long long>(__double_as_longlong(dist[s]));
+  if (ko) ko[i] = static_cast<uint32_t>(order[s]);
+}
+
+// runs of equal (order, distance): insertion sort on the face path
+__global__ void final_ties_kernel(int32_t* __restrict__ perm, int64_t n, const double* __restrict__ dist,
+                                  const int32_t* __restrict__ order, const int32_t* __restrict__ rep, PathView pv) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  auto same = [&](int64_t a, int64_t b) {
+    return order[perm[a]] == order[perm[b]] && dist[perm[a]] == dist[perm[b]];
+  };
+  if (s > 0 && same(s - 1, s)) return;  // not the first of its run
+  if (s + 1 >= n || !same(s, s + 1)) return;  // run of one
+  int64_t e = s + 1;
+  while (e < n && same(s, e)) ++e;
+  for (int64_t x = s + 1; x < e; ++x) {
+    const int32_t v = perm[x];
+    int64_t y = x - 1;
+    while (y >= s && pv.cmp(rep[perm[y]], rep[v]) > 0) {
+      perm[y + 1] = perm[y];
+      --y;
+    }
+    perm[y + 1] = v;
   }
-};
+}
 
 __global__ void final_len_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ order, int64_t n,
                                  int64_t* __restrict__ len) {
@@ -890,9 +913,30 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     RR_LAUNCH_CHECK();
     ctx->launches++;
   }
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceMergeSort::SortKeys(t, b, perm.p, ni, FinalLess{M.order, dist.p, M.rep, pv}, st);
-  }, st);
+  {
+    // (order, distance) by two stable radix passes (distances are >= 0, so
+    // their bits order like the values), then runs of equal (order,
+    // distance) — rare exact ties — finish on the face path
+    DevBuf<unsigned long long> k64, k64s;
+    DevBuf<uint32_t> k32, k32s;
+    DevBuf<int32_t> perm2;
+    k64.alloc(ni, st);
+    k64s.alloc(ni, st);
+    k32.alloc(ni, st);
+    k32s.alloc(ni, st);
+    perm2.alloc(ni, st);
+    final_key_kernel<<<grid(ni), 256, 0, st>>>(perm.p, ni, dist.p, M.order, k64.p, nullptr);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k64.p, k64s.p, perm.p, perm2.p, ni, 0, 64, st);
+    }, st);
+    final_key_kernel<<<grid(ni), 256, 0, st>>>(perm2.p, ni, dist.p, M.order, nullptr, k32.p);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k32.p, k32s.p, perm2.p, perm.p, ni, 0, 32, st);
+    }, st);
+    final_ties_kernel<<<grid(ni), 256, 0, st>>>(perm.p, ni, dist.p, M.order, M.rep, pv);
+    RR_LAUNCH_CHECK();
+    ctx->launches += 11;
+  }
   tm.mark("final sort");
   DevBuf<int64_t> len;
   len.alloc(ni + 1, st);
