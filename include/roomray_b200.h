@@ -170,6 +170,20 @@ rr_status rr_captures_import(rr_scene* scene, int64_t n, const int32_t* recv,
                              const double* mult, const int64_t* hist_off,
                              const int32_t* hist, const rr_receiver* receivers,
                              int32_t n_recv, rr_trace_result** out);
+/* step (tracer.hpp:43-45): one iteration over n caller rays, in place —
+ * the Ray span of the reference (tracer_types.hpp:11-18) as SoA arrays:
+ * origin/dir n*3, mult n*8 (band multipliers), path n, alive n, hist
+ * n*hist_cap face history with n_hist n entries used.  Host or device
+ * arrays (device ones are updated without copies).  brute != 0 selects
+ * nearest_hit_brute (the reference's step(tree = nullptr)).  max_range of
+ * config (<= 0: (r/2) sqrt(n), tracer.cpp:70-71).  The captures of this
+ * iteration, in ray order, come back as a trace result (receiver 0);
+ * rr_trace_kernel_ms gives the step kernel's device time. */
+rr_status rr_step(rr_scene* scene, int64_t n, double* origin, double* dir,
+                  double* mult, double* path, int32_t* alive, int32_t* hist,
+                  int32_t* n_hist, int32_t hist_cap,
+                  const rr_receiver* receiver, const rr_trace_config* config,
+                  int32_t brute, rr_trace_result** out);
 /* Device time of the trace kernel itself (ms, CUDA events). */
 double rr_trace_kernel_ms(rr_trace_result* res);
 rr_status rr_trace_destroy(rr_trace_result* res);

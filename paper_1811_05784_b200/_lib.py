@@ -93,6 +93,8 @@ SIGNATURES = [
     ("rr_trace_captures", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("rr_captures_import", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(Receiver), _i32,
                                      C.POINTER(_vp)]),
+    ("rr_step", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, C.POINTER(Receiver),
+                          C.POINTER(TraceConfig), _i32, C.POINTER(_vp)]),
     ("rr_trace_kernel_ms", _d, [_vp]),
     ("rr_trace_destroy", C.c_int, [_vp]),
     ("rr_build_image_sources", C.c_int, [_vp, _i32, _i64, C.POINTER(Air), C.POINTER(ClusterOptions),

@@ -334,6 +334,31 @@ rr_status rr_trace_captures(rr_trace_result* r, int32_t* recv, int32_t* ray, dou
 
 double rr_trace_kernel_ms(rr_trace_result* r) { return r ? r->kernel_ms : -1.0; }
 
+rr_status rr_step(rr_scene* scene, int64_t n, double* origin, double* dir, double* mult, double* path,
+                  int32_t* alive, int32_t* hist, int32_t* n_hist, int32_t hist_cap, const rr_receiver* receiver,
+                  const rr_trace_config* config, int32_t brute, rr_trace_result** out) {
+  return guarded([&] {
+    check_ptr(scene, "scene");
+    check_ptr(receiver, "receiver");
+    check_ptr(config, "config");
+    check_ptr(out, "out");
+    if (n > 0) {
+      check_ptr(origin, "origin");
+      check_ptr(dir, "dir");
+      check_ptr(mult, "mult");
+      check_ptr(path, "path");
+      check_ptr(alive, "alive");
+      check_ptr(hist, "hist");
+      check_ptr(n_hist, "n_hist");
+    }
+    RR_CUDA(cudaSetDevice(scene->ctx->device));
+    float ms = 0.f;
+    *out = rr::step_rays(scene, n, origin, dir, mult, path, alive, hist, n_hist, hist_cap, receiver, config, brute,
+                         &ms);
+    (*out)->scene->refs++;
+  });
+}
+
 rr_status rr_captures_import(rr_scene* scene, int64_t n, const int32_t* recv, const int32_t* ray, const double* point,
                              const double* dir, const double* path, const double* mult, const int64_t* hist_off,
                              const int32_t* hist, const rr_receiver* receivers, int32_t n_recv,

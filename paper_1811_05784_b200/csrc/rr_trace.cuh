@@ -68,6 +68,10 @@ struct rr_trace_result {
 namespace rr {
 rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver* recv, int32_t n_recv,
                            const rr_trace_config* cfg, const double* d_dirs);
+// rr_step.cu
+rr_trace_result* step_rays(rr_scene* s, int64_t n, double* origin, double* dir, double* mult, double* path,
+                           int32_t* alive, int32_t* hist, int32_t* n_hist, int32_t hist_cap, const rr_receiver* recv,
+                           const rr_trace_config* cfg, int32_t brute, float* kernel_ms);
 // rr_import.cu
 rr_trace_result* import_captures(rr_scene* s, int64_t n, const int32_t* recv, const int32_t* ray, const double* point,
                                  const double* dir, const double* path, const double* mult, const int64_t* hist_off,

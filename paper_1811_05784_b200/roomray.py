@@ -474,3 +474,55 @@ def factors_of_images(images: "DeviceImages", speed_of_sound: float = 343.0) -> 
     out = (_lib.Factors * 9)()
     check(images.lib.rr_images_factors(images.h, float(speed_of_sound), C.cast(out, C.c_void_p)))
     return _factors_out(out)
+
+
+@dataclass
+class Rays:
+    """A span of Ray (tracer_types.hpp:11-18) as SoA arrays for step():
+    origin/dir (n,3), mult (n,8), path (n,), alive (n,) int32, hist
+    (n, hist_cap) int32 face history with n_hist (n,) entries used.  numpy
+    arrays (host) or CUDA tensors (device, updated in place)."""
+
+    origin: object
+    dir: object
+    mult: object
+    path: object
+    alive: object
+    hist: object
+    n_hist: object
+
+    @staticmethod
+    def emit(source: SourceConfig, hist_cap: int, directions=None) -> "Rays":
+        """emit (emission.cpp:31-43): rays at the source with multiplier 1;
+        directions default to the Fibonacci lattice (host, the oracle-free
+        numpy restatement of emission.cpp:17-29)."""
+        n = int(source.ray_count)
+        if directions is None:
+            k = np.arange(n, dtype=np.float64)
+            z = 1.0 - (2.0 * k + 1.0) / n
+            rho = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+            phi = (2.0 * math.pi * (1.0 - 1.0 / ((1.0 + math.sqrt(5.0)) / 2.0))) * k
+            directions = np.stack([rho * np.cos(phi), rho * np.sin(phi), z], 1)
+        return Rays(np.tile(np.asarray(source.position, np.float64), (n, 1)), _f64(directions).reshape(n, 3).copy(),
+                    np.ones((n, NUM_BANDS)), np.zeros(n), np.ones(n, np.int32), np.zeros((n, hist_cap), np.int32),
+                    np.zeros(n, np.int32))
+
+
+def _vptr(a):
+    return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
+
+
+def step(tree: AccelTree, rays: Rays, receiver: Receiver, config: TraceConfig = TraceConfig(),
+         brute: bool = False) -> DeviceTrace:
+    """step (tracer.hpp:43-45): one iteration over `rays` in place; returns
+    this iteration's captures (DeviceTrace.captures(), .kernel_ms)."""
+    n = len(rays.path)
+    hist_cap = rays.hist.shape[1]
+    rec = _lib.Receiver((C.c_double * 3)(*map(float, receiver.center)), float(receiver.radius))
+    cfg = _lib.TraceConfig(int(config.max_iterations), float(config.speed_of_sound), float(config.max_range), 0, 0, 0,
+                           0, 0, None)
+    h = C.c_void_p()
+    check(tree.lib.rr_step(tree.h, n, _vptr(rays.origin), _vptr(rays.dir), _vptr(rays.mult), _vptr(rays.path),
+                           _vptr(rays.alive), _vptr(rays.hist), _vptr(rays.n_hist), int(hist_cap), C.byref(rec),
+                           C.byref(cfg), int(brute), C.byref(h)))
+    return DeviceTrace(tree, h)

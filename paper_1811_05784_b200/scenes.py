@@ -271,6 +271,49 @@ def _shoebox_grid_for(dims, n_tri):
     return grids
 
 
+def subdivided_tetrahedron(log2_faces: int):
+    """The paper's complexity fixture (the reference's
+    make_subdivided_tetrahedron, mesh_gen.cpp:111-153, restated): a regular
+    tetrahedron inscribed in the unit sphere, 4-way flat midpoint subdivision
+    to 4^q faces, plus one longest-edge bisection pass for odd exponents, so
+    exactly 2^log2_faces faces.  Returns (vertices, faces, absorption=0)."""
+    if log2_faces < 2:
+        raise ValueError("need log2_faces >= 2 (a tetrahedron has 4 faces)")
+    s = 1.0 / 3.0 ** 0.5
+    v = [(s, s, s), (s, -s, -s), (-s, s, -s), (-s, -s, s)]
+    f = [(0, 1, 2), (0, 3, 1), (0, 2, 3), (1, 3, 2)]
+    V = np.array(v, np.float64)
+    F = np.array(f, np.int64)
+    for _ in range((log2_faces - 2) // 2):
+        e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+        key = np.sort(e, 1)
+        uniq, inv = np.unique(key[:, 0] * len(V) + key[:, 1], return_inverse=True)
+        a, b = uniq // len(V), uniq % len(V)
+        mid = 0.5 * (V[a] + V[b])
+        m = inv.reshape(3, -1).T + len(V)  # midpoints of edges (ab, bc, ca)
+        V = np.concatenate([V, mid])
+        F = np.concatenate([np.stack([F[:, 0], m[:, 0], m[:, 2]], 1), np.stack([m[:, 0], F[:, 1], m[:, 1]], 1),
+                            np.stack([m[:, 2], m[:, 1], F[:, 2]], 1), m])
+    if log2_faces % 2 == 1:
+        a, b, c = F[:, 0], F[:, 1], F[:, 2]
+        lab = np.linalg.norm(V[a] - V[b], axis=1)
+        lbc = np.linalg.norm(V[b] - V[c], axis=1)
+        lca = np.linalg.norm(V[c] - V[a], axis=1)
+        u, w, x = a.copy(), b.copy(), c.copy()  # split edge (u, w), apex x
+        sel_bc = (lbc >= lab) & (lbc >= lca)
+        sel_ca = ~sel_bc & (lca >= lab) & (lca >= lbc)
+        u[sel_bc], w[sel_bc], x[sel_bc] = b[sel_bc], c[sel_bc], a[sel_bc]
+        u[sel_ca], w[sel_ca], x[sel_ca] = c[sel_ca], a[sel_ca], b[sel_ca]
+        key = np.sort(np.stack([u, w], 1), 1)
+        uniq, inv = np.unique(key[:, 0] * len(V) + key[:, 1], return_inverse=True)
+        mid = 0.5 * (V[uniq // len(V)] + V[uniq % len(V)])
+        mi = inv + len(V)
+        V = np.concatenate([V, mid])
+        F = np.concatenate([np.stack([u, mi, x], 1), np.stack([mi, w, x], 1)])
+    assert len(F) == 1 << log2_faces
+    return V, np.c_[F, np.zeros(len(F), np.int64)].astype(np.int32), np.zeros((1, 8))
+
+
 def config3(seed: int = 20240612) -> Scene:
     """C3: procedural open-air semicircular amphitheatre, exactly 436 000
     triangles: 100 m diameter cavea of 40 tiers (0.4 m rise, 0.8 m tread)
