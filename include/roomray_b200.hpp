@@ -13,8 +13,12 @@
 //    downloaded on first use through nodes() (a method, not a field).
 //  * Hit carries delta, point and face_index (lambda / mu are not reported).
 //  * RoomImpulseResponse additionally holds the 8 per-band responses.
-//  * step() (tracer.hpp:43-45, used by the reference's bench) is not
-//    provided: the persistent kernel traces each ray to completion.
+//  * step() takes std::vector<Ray>& (the reference takes std::span<Ray>);
+//    with tree == nullptr it builds a device scene from the mesh for the
+//    brute-force scan.  trace() does not call it: the persistent kernel
+//    traces each ray to completion.
+//  * nearest_hit_brute takes the AccelTree (its device copy of the mesh)
+//    where the reference takes the TriangleMesh.
 #ifndef ROOMRAY_B200_HPP
 #define ROOMRAY_B200_HPP
 
@@ -346,6 +350,110 @@ inline TraceResult trace(const TriangleMesh& /*mesh*/, const AccelTree& tree, co
     c.face_history.assign(hist.begin() + off[i], hist.begin() + off[i + 1]);
   }
   return r;
+}
+
+/// Ray (tracer_types.hpp:11-18).
+struct Ray {
+  Vec3 origin{};
+  Vec3 dir{0.0, 0.0, 1.0};
+  BandArray band_multiplier = band_ones();  // product of (1 - alpha) so far
+  double path_length = 0.0;
+  std::vector<int> face_history;
+  bool alive = true;
+};
+
+/// fibonacci_directions (emission.hpp, emission.cpp:17-29), on the host with
+/// the C library's sin/cos exactly as the reference evaluates it.
+inline std::vector<Vec3> fibonacci_directions(int n) {
+  if (n < 1) throw std::invalid_argument("fibonacci_directions needs n >= 1");
+  const double golden = (1.0 + std::sqrt(5.0)) / 2.0;
+  const double step_phi = 2.0 * M_PI * (1.0 - 1.0 / golden);
+  std::vector<Vec3> d(static_cast<std::size_t>(n));
+  for (int k = 0; k < n; ++k) {
+    const double z = 1.0 - (2.0 * k + 1.0) / n;
+    const double rho = std::sqrt(std::max(0.0, 1.0 - z * z));
+    const double phi = step_phi * k;
+    d[k] = {rho * std::cos(phi), rho * std::sin(phi), z};
+  }
+  return d;
+}
+
+/// emit (emission.hpp:27, emission.cpp:31-43): one live ray per lattice
+/// direction at the source, multiplier 1, path 0.
+inline std::vector<Ray> emit(const SourceConfig& source) {
+  if (source.ray_count < 1) throw std::invalid_argument("source ray_count must be >= 1");
+  for (double e : source.initial_energy)
+    if (e < 0.0) throw std::invalid_argument("source initial_energy must be >= 0");
+  const auto dirs = fibonacci_directions(source.ray_count);
+  std::vector<Ray> rays(dirs.size());
+  for (std::size_t i = 0; i < dirs.size(); ++i) {
+    rays[i].origin = source.position;
+    rays[i].dir = dirs[i];
+  }
+  return rays;
+}
+
+/// step (tracer.hpp:43-45, tracer.cpp:19-68): advance every live ray by one
+/// wall interaction on the GPU, in place, and return this iteration's
+/// receiver captures in ray order.  A null tree selects the brute-force
+/// nearest-face search (over a device copy of `mesh`).  max_range <= 0
+/// resolves to (r/2)*sqrt(rays.size()) as in the reference's bench.
+inline std::vector<Capture> step(std::vector<Ray>& rays, const TriangleMesh& mesh, const AccelTree* tree,
+                                 const Receiver& receiver, const TraceConfig& config) {
+  std::optional<AccelTree> own;
+  if (tree == nullptr) own.emplace(build_tree(mesh));
+  const AccelTree& t = tree ? *tree : *own;
+  const std::size_t n = rays.size();
+  std::size_t cap = 1;
+  for (const Ray& r : rays) cap = std::max(cap, r.face_history.size() + 1);
+  std::vector<double> o(3 * n), d(3 * n), m(kNumBands * n), path(n);
+  std::vector<int32_t> alive(n), hist(n * cap, -1), nh(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    const Ray& r = rays[i];
+    for (int k = 0; k < 3; ++k) o[3 * i + k] = r.origin[k], d[3 * i + k] = r.dir[k];
+    for (int b = 0; b < kNumBands; ++b) m[kNumBands * i + b] = r.band_multiplier[b];
+    path[i] = r.path_length;
+    alive[i] = r.alive ? 1 : 0;
+    nh[i] = static_cast<int32_t>(r.face_history.size());
+    std::copy(r.face_history.begin(), r.face_history.end(), hist.begin() + i * cap);
+  }
+  rr_receiver rc{{receiver.center.x, receiver.center.y, receiver.center.z}, receiver.radius};
+  rr_trace_config cfg{};
+  cfg.max_iterations = config.max_iterations;
+  cfg.speed_of_sound = config.speed_of_sound;
+  cfg.max_range = config.max_range;
+  rr_trace_result* h = nullptr;
+  detail::check(rr_step(t.handle(), static_cast<int64_t>(n), o.data(), d.data(), m.data(), path.data(), alive.data(),
+                        hist.data(), nh.data(), static_cast<int32_t>(cap), &rc, &cfg, tree ? 0 : 1, &h));
+  detail::TraceHandle guard(h);
+  for (std::size_t i = 0; i < n; ++i) {
+    Ray& r = rays[i];
+    r.origin = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+    r.dir = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+    for (int b = 0; b < kNumBands; ++b) r.band_multiplier[b] = m[kNumBands * i + b];
+    r.path_length = path[i];
+    r.alive = alive[i] != 0;
+    r.face_history.assign(hist.begin() + i * cap, hist.begin() + i * cap + nh[i]);
+  }
+  rr_trace_stats st{};
+  detail::check(rr_trace_stats_get(h, &st));
+  const std::size_t nc = static_cast<std::size_t>(st.n_captures);
+  std::vector<int32_t> ray(nc), ch(std::max<int64_t>(st.total_history, 1));
+  std::vector<double> point(3 * nc), dir(3 * nc), cpath(nc), mult(kNumBands * nc);
+  std::vector<int64_t> off(nc + 1);
+  detail::check(rr_trace_captures(h, nullptr, ray.data(), point.data(), dir.data(), cpath.data(), mult.data(),
+                                  off.data(), ch.data()));
+  std::vector<Capture> caps(nc);
+  for (std::size_t i = 0; i < nc; ++i) {
+    Capture& c = caps[i];
+    c.ray_index = ray[i];
+    c.point = {point[3 * i], point[3 * i + 1], point[3 * i + 2]};
+    c.incoming_dir = {dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]};
+    c.path_length = cpath[i];
+    for (int b = 0; b < kNumBands; ++b) c.band_multiplier[b] = mult[kNumBands * i + b];
+    c.face_history.assign(ch.begin() + off[i], ch.begin() + off[i + 1]);
+  }
+  return caps;
 }
 
 // ------------------------------------------------------------------ air (air_absorption.hpp)

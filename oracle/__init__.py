@@ -337,6 +337,9 @@ class Ref:
         L.rref_nearest_hit.argtypes = [_vp, _f64p, _f64p, _i64, C.c_int, _i32p, _f64p, _f64p]
         L.rref_intersect_sphere.argtypes = [_f64p, _f64p, _f64p, C.c_double, C.POINTER(C.c_double)]
         L.rref_fibonacci.argtypes = [C.c_int, _f64p]
+        L.rref_bench_row.restype = C.c_double
+        L.rref_bench_row.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                     C.POINTER(_i32)]
         L.rref_trace.restype = _vp
         L.rref_trace.argtypes = [_vp, _f64p, _i32, _f64p, C.c_double, _i32, C.c_double, _i32, _i64, _i64, _i64]
         L.rref_trace_info.argtypes = [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64),
@@ -385,6 +388,15 @@ class Ref:
         if not h:
             self._err()
         return RefScene(self, h, mesh)
+
+    def bench_row(self, k, with_tree=True, threads=1, min_elapsed=0.25, max_repeats=50):
+        """The reference's complexity-benchmark row (bench.cpp:26-46, 71-102):
+        (seconds per step() iteration, build seconds, tree depth)."""
+        b, d = C.c_double(), _i32()
+        t = self.L.rref_bench_row(k, int(with_tree), threads, min_elapsed, max_repeats, C.byref(b), C.byref(d))
+        if t < 0:
+            self._err()
+        return t, b.value, d.value
 
     def fibonacci(self, n):
         out = np.empty((n, 3))

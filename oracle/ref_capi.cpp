@@ -17,6 +17,7 @@
 //   factors               metrics.hpp:56-60
 //   enumerate_images      shoebox.hpp:43
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <cstring>
@@ -563,6 +564,51 @@ void rref_mesh_free(void* h) { delete static_cast<TriangleMesh*>(h); }
 
 int rref_hardware_threads() {
   return static_cast<int>(std::thread::hardware_concurrency());
+}
+
+
+// The reference's complexity benchmark row (bench.cpp:71-102 with the timing
+// loop of bench.cpp:26-46): build the subdivided tetrahedron of 2^k faces
+// (mesh_gen.hpp:25), build_tree, then the per-iteration wall time of step()
+// over 2^k emitted rays (tree, or brute force when with_tree == 0).
+// Returns seconds per iteration (< 0 on error); build seconds and the tree
+// depth go to the out-pointers.
+double rref_bench_row(int k, int with_tree, int threads, double min_elapsed,
+                      int max_repeats, double* build_seconds, int32_t* depth) {
+  using Clock = std::chrono::steady_clock;
+  double per_iter = -1.0;
+  guarded([&] {
+    Material reflective;
+    reflective.name = "reflective";
+    reflective.absorption = BandArray::Zero();
+    const TriangleMesh mesh = make_subdivided_tetrahedron(k, reflective);
+    const auto b0 = Clock::now();
+    const AccelTree tree = build_tree(mesh);
+    *build_seconds = std::chrono::duration<double>(Clock::now() - b0).count();
+    *depth = tree.depth();
+    SourceConfig source;
+    source.position = Vec3::Zero();
+    source.ray_count = 1 << k;
+    auto rays = emit(source);
+    Receiver receiver;
+    receiver.center = Vec3(1e6, 1e6, 1e6);
+    receiver.radius = 1e-3;
+    TraceConfig config;
+    config.max_range = 1e30;
+    config.thread_count = threads;
+    const AccelTree* t = with_tree ? &tree : nullptr;
+    step(rays, mesh, t, receiver, config);
+    double elapsed = 0.0;
+    int repeats = 0;
+    while (repeats < max_repeats && (repeats < 1 || elapsed < min_elapsed)) {
+      const auto s0 = Clock::now();
+      step(rays, mesh, t, receiver, config);
+      elapsed += std::chrono::duration<double>(Clock::now() - s0).count();
+      ++repeats;
+    }
+    per_iter = elapsed / repeats;
+  });
+  return per_iter;
 }
 
 }  // extern "C"

@@ -205,3 +205,53 @@ def test_pipeline_matches_oracle(tmp_path, port, ref):
     wf = ref.factors(want.dist, want.energy, 343.0)
     assert np.array_equal(fac[:, :, 1], wf[:, :, 1])
     np.testing.assert_allclose(fac[:, :, 0], wf[:, :, 0], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_facade_step_matches_reference(tmp_path, ref):
+    """emit + step() through the facade (host lattice with the C library's
+    sin/cos, as emission.cpp evaluates it) reproduce the reference's own
+    trace() truncated to the same iteration count bit for bit, with the
+    tree and with tree == nullptr (brute force)."""
+    import oracle
+    src = os.path.join(ROOT, "tests", "native", "facade_step.cpp")
+    exe = str(tmp_path / "facade_step")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    src, "-L", os.path.join(ROOT, "paper_1811_05784_b200"), "-lroomray_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_1811_05784_b200"), "-o", exe], check=True)
+    s = scenes.config1()
+    n_rays, iters = 3000, 12
+    (rc, rr) = s.receivers[0]
+    inp, out = tmp_path / "in", tmp_path / "out"
+    inp.mkdir()
+    out.mkdir()
+    s.vertices.astype(np.float64).tofile(inp / "vertices.f64")
+    s.faces.astype(np.int32).tofile(inp / "faces.i32")
+    s.absorption.astype(np.float64).tofile(inp / "alpha.f64")
+    np.array([*s.source, *rc, rr], np.float64).tofile(inp / "params.f64")
+    r = subprocess.run([exe, str(inp), str(out), str(n_rays), str(iters)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr + r.stdout
+
+    cap, st = ref.scene(oracle.Mesh(s.vertices, s.faces, s.absorption)).trace(s.source, n_rays, rc, rr, iters, 0.0)
+    assert len(cap) > 0
+    for tag in ("tree", "brute"):
+        ray = np.fromfile(out / f"{tag}_cap_ray.i32", np.int32)
+        cf = np.fromfile(out / f"{tag}_cap_f.f64").reshape(-1, 15)
+        off = np.fromfile(out / f"{tag}_cap_off.i64", np.int64)
+        hist = np.fromfile(out / f"{tag}_cap_hist.i32", np.int32)
+        assert len(ray) == len(cap), tag
+        order = np.lexsort((cf[:, 6], ray))  # trace() sorts by (ray, path), tracer.cpp:143-147
+        assert np.array_equal(ray[order], cap.ray)
+        assert np.array_equal(cf[order, 0:3], cap.point) and np.array_equal(cf[order, 3:6], cap.dir)
+        assert np.array_equal(cf[order, 6], cap.path) and np.array_equal(cf[order, 7:15], cap.mult)
+        lens = np.diff(off)[order]
+        assert np.array_equal(lens, np.diff(cap.hist_off))
+        got = np.concatenate([hist[off[i]:off[i + 1]] for i in order]) if len(order) else hist[:0]
+        assert np.array_equal(got, cap.hist[: cap.hist_off[-1]])
+    rays_t = np.fromfile(out / "tree_rays.f64").reshape(n_rays, -1)
+    rays_b = np.fromfile(out / "brute_rays.f64").reshape(n_rays, -1)
+    assert np.array_equal(rays_t, rays_b)
+    alive, n_hist = rays_t[:, 7] == 1, rays_t[:, 8]
+    assert n_hist.max() <= iters and np.all(n_hist[alive] == iters)  # one face per surviving iteration
+    assert np.all(rays_t[~alive, 6] > st.max_range) or np.all(n_hist[~alive] < iters)
