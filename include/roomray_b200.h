@@ -32,6 +32,8 @@ typedef struct rr_ctx rr_ctx;
 typedef struct rr_scene rr_scene;
 typedef struct rr_trace_result rr_trace_result;
 typedef struct rr_images rr_images;
+typedef struct rr_lattice rr_lattice;
+typedef struct rr_match rr_match;
 
 /* Reference-layout tree node (TreeNode, accel_tree.hpp:15-22): post-order,
  * root last, leaves hold one face. */
@@ -203,6 +205,50 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist,
                         int32_t* order, int32_t* has_proj, double* proj,
                         int64_t* path_off, int32_t* path);
 rr_status rr_images_destroy(rr_images* im);
+
+/* ---------------------------------------------------------------- shoebox
+ * The analytic mirror-lattice check of a rectangular room (shoebox.hpp).
+ * rr_shoebox_images = enumerate_images (shoebox.hpp:38-43,
+ * shoebox.cpp:43-116): box [0,L]^3 with walls x0,x1,y0,y1,z0,z1
+ * (BoxWall, shoebox.hpp:13), walls_alpha 6*8; every lattice image within
+ * max_distance of the receiver, sorted by (distance, lattice cell).  Errors
+ * as the reference: dimensions <= 0, source/receiver not strictly inside,
+ * max_distance or radius <= 0 -> RR_INVALID_ARGUMENT. */
+rr_status rr_shoebox_images(rr_ctx* ctx, const double* dims, const double* walls_alpha,
+                            const double* source, const double* receiver,
+                            double max_distance, double receiver_radius,
+                            const rr_air* air, rr_lattice** out);
+rr_status rr_lattice_info(rr_lattice* lat, int64_t* n);
+/* Any output may be NULL.  wall_hits 6 per image, energy 8 per image. */
+rr_status rr_lattice_get(rr_lattice* lat, double* pos, double* dist, int32_t* order,
+                         int32_t* wall_hits, double* energy);
+rr_status rr_lattice_destroy(rr_lattice* lat);
+
+/* compare (shoebox.hpp:67-70, shoebox.cpp:126-182): each traced image goes
+ * to the nearest oracle image within pos_tol (largest oracle index on
+ * ties); per matched oracle image the member list (traced order), the max
+ * position error and 10 log10(sum traced E / oracle E) per band.  Arrays are
+ * host or device memory; oracle order may be NULL (reported as 0). */
+rr_status rr_shoebox_compare(rr_ctx* ctx, int64_t n_oracle, const double* oracle_pos,
+                             const double* oracle_energy, const int32_t* oracle_order,
+                             int64_t n_traced, const double* traced_pos,
+                             const double* traced_energy, double pos_tol,
+                             double energy_tol_db, rr_match** out);
+/* The same on device-resident sets: a lattice against an image set. */
+rr_status rr_lattice_compare_images(rr_lattice* lat, rr_images* traced, double pos_tol,
+                                    double energy_tol_db, rr_match** out);
+/* MatchReport (shoebox.hpp:56-66): counts, max_position_error and the 8
+ * per-band rms energy errors (dB). */
+rr_status rr_match_info(rr_match* m, int64_t* n_matched, int64_t* n_members,
+                        int64_t* n_unmatched_oracle, int64_t* n_unmatched_traced,
+                        double* max_position_error, double* rms_energy_error_db);
+/* MatchedImage list in oracle order; member_off has n_matched+1 entries.
+ * Any output may be NULL. */
+rr_status rr_match_get(rr_match* m, int32_t* oracle_index, double* position_error,
+                       int32_t* order, double* energy_delta_db, int64_t* member_off,
+                       int32_t* members, int32_t* unmatched_oracle,
+                       int32_t* unmatched_traced);
+rr_status rr_match_destroy(rr_match* m);
 
 /* Measurement helper (no reference counterpart): sustained L2 read
  * bandwidth (GB/s) streaming an L2-resident buffer of `bytes`, `iters`

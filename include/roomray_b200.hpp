@@ -674,6 +674,137 @@ inline BandFactors factors(const PulseTrains& trains) {
   return bf;
 }
 
+// ------------------------------------------------------------------ shoebox lattice (shoebox.hpp)
+enum BoxWall { kWallX0 = 0, kWallX1, kWallY0, kWallY1, kWallZ0, kWallZ1 };  // shoebox.hpp:13
+
+/// Rectangular room [0,Lx] x [0,Ly] x [0,Lz], one material per wall
+/// (shoebox.hpp:16-22).
+struct ShoeBox {
+  Vec3 dimensions{1.0, 1.0, 1.0};
+  std::array<Material, 6> walls{};
+  void validate() const {
+    for (int a = 0; a < 3; ++a)
+      if (dimensions[a] <= 0.0) throw std::invalid_argument("box dimensions must be > 0");
+  }
+  bool inside(const Vec3& p) const {
+    for (int a = 0; a < 3; ++a)
+      if (!(p[a] > 0.0) || !(p[a] < dimensions[a])) return false;
+    return true;
+  }
+};
+
+/// OracleImageSource (shoebox.hpp:25-31).
+struct OracleImageSource {
+  Vec3 position{};
+  double distance = 0.0;
+  int order = 0;
+  std::array<int, 6> wall_hits{};
+  BandArray band_energy{};
+};
+
+/// enumerate_images (shoebox.hpp:38-43) on the GPU: every mirror-lattice
+/// image within max_distance of the receiver, sorted by (distance, cell).
+inline std::vector<OracleImageSource> enumerate_images(const ShoeBox& box, const Vec3& source, const Vec3& receiver,
+                                                       double max_distance, double receiver_radius,
+                                                       const AirModel& air) {
+  const double dims[3] = {box.dimensions.x, box.dimensions.y, box.dimensions.z};
+  double alpha[6 * kNumBands];
+  for (int w = 0; w < 6; ++w)
+    for (int b = 0; b < kNumBands; ++b) alpha[kNumBands * w + b] = box.walls[w].absorption[b];
+  const double s[3] = {source.x, source.y, source.z}, r[3] = {receiver.x, receiver.y, receiver.z};
+  rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
+  rr_lattice* h = nullptr;
+  detail::check(rr_shoebox_images(Device::get(0).handle(), dims, alpha, s, r, max_distance, receiver_radius, &a, &h));
+  std::unique_ptr<rr_lattice, rr_status (*)(rr_lattice*)> guard(h, rr_lattice_destroy);
+  int64_t n = 0;
+  detail::check(rr_lattice_info(h, &n));
+  std::vector<double> pos(3 * n), dist(n), energy(kNumBands * n);
+  std::vector<int32_t> order(n), hits(6 * n);
+  detail::check(rr_lattice_get(h, pos.data(), dist.data(), order.data(), hits.data(), energy.data()));
+  std::vector<OracleImageSource> out(static_cast<std::size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    OracleImageSource& o = out[i];
+    o.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    o.distance = dist[i];
+    o.order = order[i];
+    for (int w = 0; w < 6; ++w) o.wall_hits[w] = hits[6 * i + w];
+    for (int b = 0; b < kNumBands; ++b) o.band_energy[b] = energy[kNumBands * i + b];
+  }
+  return out;
+}
+
+/// MatchedImage / MatchReport (shoebox.hpp:47-66).
+struct MatchedImage {
+  int oracle_index = -1;
+  std::vector<int> traced_indices;
+  double position_error = 0.0;
+  int order = 0;
+  BandArray energy_delta_db{};
+};
+
+struct MatchReport {
+  std::vector<MatchedImage> matched;
+  std::vector<int> unmatched_oracle;  // beams the tracer missed
+  std::vector<int> unmatched_traced;  // should be empty
+  double max_position_error = 0.0;
+  BandArray rms_energy_error_db{};
+  double pos_tol = 0.0;
+  double energy_tol_db = 0.0;
+  bool energy_within(double tol_db, int max_order) const {  // shoebox.cpp:118-124
+    for (const MatchedImage& m : matched) {
+      if (m.order > max_order) continue;
+      for (double d : m.energy_delta_db)
+        if (std::abs(d) > tol_db) return false;
+    }
+    return true;
+  }
+};
+
+/// compare (shoebox.hpp:67-70) on the GPU: cells hashed at 2 * pos_tol
+/// instead of the reference's O(T * O) scan; same matches, same tie rule.
+inline MatchReport compare(const std::vector<OracleImageSource>& oracle, const std::vector<ImageSource>& traced,
+                           double pos_tol, double energy_tol_db) {
+  const std::size_t no = oracle.size(), nt = traced.size();
+  std::vector<double> opos(3 * no), oen(kNumBands * no), tpos(3 * nt), ten(kNumBands * nt);
+  std::vector<int32_t> oord(no);
+  for (std::size_t i = 0; i < no; ++i) {
+    for (int k = 0; k < 3; ++k) opos[3 * i + k] = oracle[i].position[k];
+    for (int b = 0; b < kNumBands; ++b) oen[kNumBands * i + b] = oracle[i].band_energy[b];
+    oord[i] = oracle[i].order;
+  }
+  for (std::size_t i = 0; i < nt; ++i) {
+    for (int k = 0; k < 3; ++k) tpos[3 * i + k] = traced[i].position[k];
+    for (int b = 0; b < kNumBands; ++b) ten[kNumBands * i + b] = traced[i].band_energy[b];
+  }
+  rr_match* h = nullptr;
+  detail::check(rr_shoebox_compare(Device::get(0).handle(), static_cast<int64_t>(no), opos.data(), oen.data(),
+                                   oord.data(), static_cast<int64_t>(nt), tpos.data(), ten.data(), pos_tol,
+                                   energy_tol_db, &h));
+  std::unique_ptr<rr_match, rr_status (*)(rr_match*)> guard(h, rr_match_destroy);
+  int64_t g = 0, nm = 0, nuo = 0, nut = 0;
+  MatchReport r;
+  r.pos_tol = pos_tol;
+  r.energy_tol_db = energy_tol_db;
+  detail::check(rr_match_info(h, &g, &nm, &nuo, &nut, &r.max_position_error, r.rms_energy_error_db.data()));
+  std::vector<int32_t> oi(g), ord(g), mem(nm);
+  std::vector<double> err(g), dd(kNumBands * g);
+  std::vector<int64_t> off(g + 1);
+  r.unmatched_oracle.resize(nuo);
+  r.unmatched_traced.resize(nut);
+  detail::check(rr_match_get(h, oi.data(), err.data(), ord.data(), dd.data(), off.data(), mem.data(),
+                             r.unmatched_oracle.data(), r.unmatched_traced.data()));
+  r.matched.resize(g);
+  for (int64_t i = 0; i < g; ++i) {
+    MatchedImage& m = r.matched[i];
+    m.oracle_index = oi[i];
+    m.position_error = err[i];
+    m.order = ord[i];
+    for (int b = 0; b < kNumBands; ++b) m.energy_delta_db[b] = dd[kNumBands * i + b];
+    m.traced_indices.assign(mem.begin() + off[i], mem.begin() + off[i + 1]);
+  }
+  return r;
+}
+
 }  // namespace roomray_b200
 
 #endif  // ROOMRAY_B200_HPP

@@ -511,6 +511,87 @@ inline RunArtifacts run_trace_pipeline(const RunConfig& config) {
   return a;
 }
 
+// ------------------------------------------------------------------ shoebox oracle run (pipeline.hpp:47-61)
+struct OracleConfig {
+  ShoeBox box;
+  Vec3 source_position{};
+  int ray_count = 1;
+  Receiver receiver;
+  AirModel air;
+  double max_distance = 0.0;  // 0 derives the tracer range (r/2)*sqrt(N) + r
+  std::string output_dir = "oracle_out";
+
+  /// pipeline.cpp:335-374: box.dimensions, materials (relative to the
+  /// config file), walls{x0..z1} by material name, source{position,
+  /// ray_count}, receiver{center, radius}; optional air{...}, max_distance,
+  /// output_dir.
+  static OracleConfig from_json_file(const std::string& path) {
+    using detail::Json;
+    const Json doc = detail::JsonReader(detail::read_file(path, "config")).parse();
+    auto at = [](const Json& o, const char* k) -> const Json& {
+      const Json* v = o.kind == Json::Obj ? o.get(k) : nullptr;
+      if (!v) throw std::runtime_error(std::string("oracle config: missing field '") + k + "'");
+      return *v;
+    };
+    auto num = [](const Json& v, const char* k) {
+      if (v.kind != Json::Num) throw std::runtime_error(std::string("oracle config: '") + k + "' must be a number");
+      return v.num;
+    };
+    auto str = [](const Json& v, const char* k) {
+      if (v.kind != Json::Str) throw std::runtime_error(std::string("oracle config: '") + k + "' must be a string");
+      return v.str;
+    };
+    auto vec3 = [&](const Json& v, const char* k) {
+      if (v.kind != Json::Arr || v.arr.size() != 3)
+        throw std::runtime_error(std::string("oracle config: '") + k + "' must be an array of 3 numbers");
+      return Vec3{num(v.arr[0], k), num(v.arr[1], k), num(v.arr[2], k)};
+    };
+    OracleConfig c;
+    c.box.dimensions = vec3(at(at(doc, "box"), "dimensions"), "dimensions");
+    std::string material_path = str(at(doc, "materials"), "materials");
+    if (std::filesystem::path(material_path).is_relative())
+      material_path = (std::filesystem::path(path).parent_path() / material_path).string();
+    const auto table = load_material_table(material_path);
+    const Json& walls = at(doc, "walls");
+    const char* slots[6] = {"x0", "x1", "y0", "y1", "z0", "z1"};
+    for (int w = 0; w < 6; ++w) {
+      const std::string name = str(at(walls, slots[w]), slots[w]);
+      const auto found = table.find(name);
+      if (found == table.end())
+        throw UnresolvedMaterialError("material '" + name + "' not found in the material table");
+      c.box.walls[w] = found->second;
+    }
+    const Json& src = at(doc, "source");
+    c.source_position = vec3(at(src, "position"), "position");
+    c.ray_count = static_cast<int>(num(at(src, "ray_count"), "ray_count"));
+    const Json& rec = at(doc, "receiver");
+    c.receiver.center = vec3(at(rec, "center"), "center");
+    c.receiver.radius = num(at(rec, "radius"), "radius");
+    if (const Json* air = doc.get("air")) {
+      if (const Json* v = air->get("enabled")) c.air.enabled = v->kind == Json::Bool ? v->b : true;
+      if (const Json* v = air->get("temperature_c")) c.air.temperature_c = num(*v, "temperature_c");
+      if (const Json* v = air->get("relative_humidity")) c.air.relative_humidity = num(*v, "relative_humidity");
+      if (const Json* v = air->get("pressure_kpa")) c.air.pressure_kpa = num(*v, "pressure_kpa");
+    }
+    if (const Json* v = doc.get("max_distance")) c.max_distance = num(*v, "max_distance");
+    if (const Json* v = doc.get("output_dir")) c.output_dir = str(*v, "output_dir");
+    return c;
+  }
+
+  /// pipeline.cpp:327-333.
+  double resolved_max_distance() const {
+    if (max_distance > 0.0) return max_distance;
+    return 0.5 * receiver.radius * std::sqrt(static_cast<double>(ray_count)) + receiver.radius;
+  }
+};
+
+/// run_oracle (pipeline.hpp:61, pipeline.cpp:376-381) on the GPU.
+inline std::vector<OracleImageSource> run_oracle(const OracleConfig& config) {
+  config.box.validate();
+  return enumerate_images(config.box, config.source_position, config.receiver.center,
+                          config.resolved_max_distance(), config.receiver.radius, config.air);
+}
+
 }  // namespace roomray_b200
 
 #endif  // ROOMRAY_B200_IO_HPP

@@ -371,6 +371,12 @@ class Ref:
         L.rref_lattice.argtypes = [_f64p, _f64p, _f64p, _f64p, C.c_double, C.c_double, _f64p, C.POINTER(_i64)]
         L.rref_lattice_get.argtypes = [_vp, _f64p, _f64p, _i32p, _f64p]
         L.rref_lattice_free.argtypes = [_vp]
+        L.rref_lattice_hits.argtypes = [_vp, _i32p]
+        L.rref_compare.restype = _vp
+        L.rref_compare.argtypes = [_i64, _f64p, _f64p, _i32p, _i64, _f64p, _f64p, C.c_double, C.c_double, _i64p,
+                                   C.POINTER(C.c_double), _f64p]
+        L.rref_compare_get.argtypes = [_vp, _i32p, _f64p, _i32p, _f64p, _i64p, _i32p, _i32p, _i32p]
+        L.rref_compare_free.argtypes = [_vp]
         L.rref_mesh_gen.restype = _vp
         L.rref_mesh_gen.argtypes = [C.c_int, _f64p, C.c_int, C.POINTER(_i64), C.POINTER(_i64)]
         L.rref_mesh_get.argtypes = [_vp, _f64p, _i32p]
@@ -476,8 +482,35 @@ class Ref:
         n = n.value
         pos, dist, order, energy = np.empty((n, 3)), np.empty(n), np.empty(n, np.int32), np.empty((n, 8))
         self.L.rref_lattice_get(h, pos.reshape(-1), dist, order, energy.reshape(-1))
+        hits = np.empty((n, 6), np.int32)
+        self.L.rref_lattice_hits(h, hits.reshape(-1))
         self.L.rref_lattice_free(h)
+        self.last_lattice_hits = hits
         return pos, dist, order, energy
+
+    def compare(self, opos, oenergy, oorder, tpos, tenergy, pos_tol, tol_db):
+        """The reference's compare (shoebox.cpp:126-182) -> dict of arrays."""
+        opos, oen = _c(opos, np.float64).reshape(-1), _c(oenergy, np.float64).reshape(-1)
+        tpos, ten = _c(tpos, np.float64).reshape(-1), _c(tenergy, np.float64).reshape(-1)
+        oorder = _c(oorder, np.int32)
+        counts, mx, rms = np.zeros(4, np.int64), C.c_double(), np.empty(8)
+        h = self.L.rref_compare(len(oorder), opos, oen, oorder, len(tpos) // 3, tpos, ten, pos_tol, tol_db, counts,
+                                C.byref(mx), rms)
+        if not h:
+            self._err()
+        g, nm, nuo, nut = (int(x) for x in counts)
+        r = dict(oracle_index=np.empty(g, np.int32), position_error=np.empty(g), order=np.empty(g, np.int32),
+                 energy_delta_db=np.empty((g, 8)), member_off=np.empty(g + 1, np.int64),
+                 members=np.empty(max(nm, 1), np.int32), unmatched_oracle=np.empty(max(nuo, 1), np.int32),
+                 unmatched_traced=np.empty(max(nut, 1), np.int32))
+        self.L.rref_compare_get(h, r["oracle_index"], r["position_error"], r["order"],
+                                r["energy_delta_db"].reshape(-1), r["member_off"], r["members"],
+                                r["unmatched_oracle"], r["unmatched_traced"])
+        self.L.rref_compare_free(h)
+        r["members"], r["unmatched_oracle"], r["unmatched_traced"] = (
+            r["members"][:nm], r["unmatched_oracle"][:nuo], r["unmatched_traced"][:nut])
+        r["max_position_error"], r["rms_energy_error_db"] = mx.value, rms
+        return r
 
     def mesh_gen(self, kind: str, dims=(1.0, 1.0, 1.0), level=0):
         k = {"box": 0, "icosphere": 1, "tetra": 2}[kind]

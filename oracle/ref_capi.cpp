@@ -525,6 +525,62 @@ void rref_lattice_get(void* h, double* pos, double* dist, int32_t* order,
   }
 }
 
+void rref_lattice_hits(void* h, int32_t* hits) {
+  auto* v = static_cast<std::vector<OracleImageSource>*>(h);
+  for (size_t i = 0; i < v->size(); ++i)
+    for (int w = 0; w < 6; ++w) hits[6 * i + w] = (*v)[i].wall_hits[w];
+}
+
+// compare (shoebox.cpp:126-182) on plain arrays.
+void* rref_compare(int64_t no, const double* opos, const double* oen, const int32_t* oorder, int64_t nt,
+                   const double* tpos, const double* ten, double pos_tol, double tol_db, int64_t* counts,
+                   double* max_err, double* rms) {
+  MatchReport* out = nullptr;
+  int rc = guarded([&] {
+    std::vector<OracleImageSource> oracle(static_cast<size_t>(no));
+    for (int64_t i = 0; i < no; ++i) {
+      oracle[i].position = Vec3(opos[3 * i], opos[3 * i + 1], opos[3 * i + 2]);
+      oracle[i].order = oorder[i];
+      for (int b = 0; b < kNumBands; ++b) oracle[i].band_energy[b] = oen[kNumBands * i + b];
+    }
+    std::vector<ImageSource> traced(static_cast<size_t>(nt));
+    for (int64_t i = 0; i < nt; ++i) {
+      traced[i].position = Vec3(tpos[3 * i], tpos[3 * i + 1], tpos[3 * i + 2]);
+      for (int b = 0; b < kNumBands; ++b) traced[i].band_energy[b] = ten[kNumBands * i + b];
+    }
+    out = new MatchReport(compare(oracle, traced, pos_tol, tol_db));
+    int64_t members = 0;
+    for (const auto& m : out->matched) members += static_cast<int64_t>(m.traced_indices.size());
+    counts[0] = static_cast<int64_t>(out->matched.size());
+    counts[1] = members;
+    counts[2] = static_cast<int64_t>(out->unmatched_oracle.size());
+    counts[3] = static_cast<int64_t>(out->unmatched_traced.size());
+    *max_err = out->max_position_error;
+    for (int b = 0; b < kNumBands; ++b) rms[b] = out->rms_energy_error_db[b];
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void rref_compare_get(void* h, int32_t* oracle_index, double* pos_err, int32_t* order, double* delta,
+                      int64_t* member_off, int32_t* members, int32_t* uo, int32_t* ut) {
+  auto* r = static_cast<MatchReport*>(h);
+  member_off[0] = 0;
+  int64_t k = 0;
+  for (size_t g = 0; g < r->matched.size(); ++g) {
+    const auto& m = r->matched[g];
+    oracle_index[g] = m.oracle_index;
+    pos_err[g] = m.position_error;
+    order[g] = m.order;
+    for (int b = 0; b < kNumBands; ++b) delta[kNumBands * g + b] = m.energy_delta_db[b];
+    for (int t : m.traced_indices) members[k++] = t;
+    member_off[g + 1] = k;
+  }
+  for (size_t i = 0; i < r->unmatched_oracle.size(); ++i) uo[i] = r->unmatched_oracle[i];
+  for (size_t i = 0; i < r->unmatched_traced.size(); ++i) ut[i] = r->unmatched_traced[i];
+}
+
+void rref_compare_free(void* h) { delete static_cast<MatchReport*>(h); }
+
 void rref_lattice_free(void* h) {
   delete static_cast<std::vector<OracleImageSource>*>(h);
 }

@@ -104,6 +104,16 @@ SIGNATURES = [
     ("rr_images_destroy", C.c_int, [_vp]),
     ("rr_images_device", C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     ("rr_air_beta_bands", C.c_int, [C.POINTER(Air), _f64p]),
+    ("rr_shoebox_images", C.c_int, [_vp, _f64p, _f64p, _f64p, _f64p, _d, _d, C.POINTER(Air), C.POINTER(_vp)]),
+    ("rr_lattice_info", C.c_int, [_vp, C.POINTER(_i64)]),
+    ("rr_lattice_get", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    ("rr_lattice_destroy", C.c_int, [_vp]),
+    ("rr_shoebox_compare", C.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _d, _d, C.POINTER(_vp)]),
+    ("rr_lattice_compare_images", C.c_int, [_vp, _vp, _d, _d, C.POINTER(_vp)]),
+    ("rr_match_info", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
+                                C.POINTER(_d), _f64p]),
+    ("rr_match_get", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("rr_match_destroy", C.c_int, [_vp]),
     ("rr_synthesize", C.c_int, [_vp, _i64, _f64p, _f64p, _d, _d, _i32, _i64, _vp, _vp]),
     ("rr_ir_bin_device", C.c_int, [_vp, _i64, _vp, _vp, _d, _d, _i64, _vp]),
     ("rr_ir_filter_device", C.c_int, [_vp, _vp, _d, _i32, _i64, _vp, _vp]),

@@ -673,6 +673,145 @@ rr_status rr_l2_read_gbs(rr_ctx* ctx, int64_t bytes, int32_t iters, double* gbs)
   });
 }
 
+// ---------------------------------------------------------------- shoebox lattice (rr_shoebox.cu)
+rr_status rr_shoebox_images(rr_ctx* ctx, const double* dims, const double* walls_alpha, const double* source,
+                            const double* receiver, double max_distance, double receiver_radius, const rr_air* air,
+                            rr_lattice** out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(dims, "dims");
+    check_ptr(walls_alpha, "walls_alpha");
+    check_ptr(source, "source");
+    check_ptr(receiver, "receiver");
+    check_ptr(air, "air");
+    check_ptr(out, "out");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    *out = rr::enumerate_lattice(ctx, dims, walls_alpha, source, receiver, max_distance, receiver_radius, *air);
+    ctx->refs++;
+  });
+}
+
+rr_status rr_lattice_info(rr_lattice* lat, int64_t* n) {
+  return guarded([&] {
+    check_ptr(lat, "lattice");
+    if (n) *n = lat->n;
+  });
+}
+
+rr_status rr_lattice_get(rr_lattice* lat, double* pos, double* dist, int32_t* order, int32_t* wall_hits,
+                         double* energy) {
+  return guarded([&] {
+    check_ptr(lat, "lattice");
+    RR_CUDA(cudaSetDevice(lat->ctx->device));
+    cudaStream_t st = lat->ctx->stream;
+    const int64_t n = lat->n;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+    };
+    cp(pos, lat->pos.p, sizeof(double) * 3 * n);
+    cp(dist, lat->dist.p, sizeof(double) * n);
+    cp(order, lat->order.p, sizeof(int32_t) * n);
+    cp(wall_hits, lat->hits.p, sizeof(int32_t) * 6 * n);
+    cp(energy, lat->energy.p, sizeof(double) * rr::kBands * n);
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+rr_status rr_lattice_destroy(rr_lattice* lat) {
+  return guarded([&] {
+    if (!lat) return;
+    rr_ctx* ctx = lat->ctx;
+    cudaSetDevice(ctx->device);
+    delete lat;
+    cudaStreamSynchronize(ctx->stream);
+    ctx_release(ctx);
+  });
+}
+
+rr_status rr_shoebox_compare(rr_ctx* ctx, int64_t n_oracle, const double* oracle_pos, const double* oracle_energy,
+                             const int32_t* oracle_order, int64_t n_traced, const double* traced_pos,
+                             const double* traced_energy, double pos_tol, double energy_tol_db, rr_match** out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(out, "out");
+    if (n_oracle > 0) {
+      check_ptr(oracle_pos, "oracle_pos");
+      check_ptr(oracle_energy, "oracle_energy");
+    }
+    if (n_traced > 0) {
+      check_ptr(traced_pos, "traced_pos");
+      check_ptr(traced_energy, "traced_energy");
+    }
+    RR_CUDA(cudaSetDevice(ctx->device));
+    *out = rr::compare_lattice(ctx, n_oracle, oracle_pos, oracle_energy, oracle_order, n_traced, traced_pos,
+                               traced_energy, pos_tol, energy_tol_db);
+    ctx->refs++;
+  });
+}
+
+rr_status rr_lattice_compare_images(rr_lattice* lat, rr_images* traced, double pos_tol, double energy_tol_db,
+                                    rr_match** out) {
+  return guarded([&] {
+    check_ptr(lat, "lattice");
+    check_ptr(traced, "images");
+    check_ptr(out, "out");
+    if (traced->scene->ctx != lat->ctx) rr::invalid("lattice and images belong to different contexts");
+    rr_ctx* ctx = lat->ctx;
+    RR_CUDA(cudaSetDevice(ctx->device));
+    *out = rr::compare_lattice(ctx, lat->n, lat->pos.p, lat->energy.p, lat->order.p, traced->n, traced->pos.p,
+                               traced->energy.p, pos_tol, energy_tol_db);
+    ctx->refs++;
+  });
+}
+
+rr_status rr_match_info(rr_match* m, int64_t* n_matched, int64_t* n_members, int64_t* n_unmatched_oracle,
+                        int64_t* n_unmatched_traced, double* max_position_error, double* rms_energy_error_db) {
+  return guarded([&] {
+    check_ptr(m, "match");
+    if (n_matched) *n_matched = m->n_matched;
+    if (n_members) *n_members = m->n_members;
+    if (n_unmatched_oracle) *n_unmatched_oracle = m->n_unmatched_oracle;
+    if (n_unmatched_traced) *n_unmatched_traced = m->n_unmatched_traced;
+    if (max_position_error) *max_position_error = m->max_position_error;
+    if (rms_energy_error_db)
+      for (int b = 0; b < rr::kBands; ++b) rms_energy_error_db[b] = m->rms_db[b];
+  });
+}
+
+rr_status rr_match_get(rr_match* m, int32_t* oracle_index, double* position_error, int32_t* order,
+                       double* energy_delta_db, int64_t* member_off, int32_t* members, int32_t* unmatched_oracle,
+                       int32_t* unmatched_traced) {
+  return guarded([&] {
+    check_ptr(m, "match");
+    RR_CUDA(cudaSetDevice(m->ctx->device));
+    cudaStream_t st = m->ctx->stream;
+    const int64_t g = m->n_matched;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+    };
+    cp(oracle_index, m->oracle_index.p, sizeof(int32_t) * g);
+    cp(position_error, m->pos_err.p, sizeof(double) * g);
+    cp(order, m->order.p, sizeof(int32_t) * g);
+    cp(energy_delta_db, m->delta_db.p, sizeof(double) * rr::kBands * g);
+    cp(member_off, m->member_off.p, sizeof(int64_t) * (g + 1));
+    cp(members, m->members.p, sizeof(int32_t) * m->n_members);
+    cp(unmatched_oracle, m->unmatched_oracle.p, sizeof(int32_t) * m->n_unmatched_oracle);
+    cp(unmatched_traced, m->unmatched_traced.p, sizeof(int32_t) * m->n_unmatched_traced);
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+rr_status rr_match_destroy(rr_match* m) {
+  return guarded([&] {
+    if (!m) return;
+    rr_ctx* ctx = m->ctx;
+    cudaSetDevice(ctx->device);
+    delete m;
+    cudaStreamSynchronize(ctx->stream);
+    ctx_release(ctx);
+  });
+}
+
 rr_status rr_air_beta_bands(const rr_air* air, double* beta) {
   return guarded([&] {
     check_ptr(air, "air");

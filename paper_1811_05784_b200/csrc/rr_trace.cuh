@@ -91,3 +91,29 @@ namespace rr {
 rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_rays, const rr_air& air,
                                const rr_cluster_options& opt);
 }  // namespace rr
+
+// Shoebox mirror-lattice oracle and matcher (rr_shoebox.cu).
+struct rr_lattice {
+  rr_ctx* ctx = nullptr;
+  int64_t n = 0;
+  rr::DevBuf<double> pos, dist, energy;
+  rr::DevBuf<int32_t> order, hits;
+};
+
+struct rr_match {
+  rr_ctx* ctx = nullptr;
+  int64_t n_matched = 0, n_members = 0, n_unmatched_oracle = 0, n_unmatched_traced = 0;
+  double max_position_error = 0.0, pos_tol = 0.0, energy_tol_db = 0.0;
+  double rms_db[rr::kBands] = {};
+  rr::DevBuf<int32_t> oracle_index, order, members, unmatched_oracle, unmatched_traced;
+  rr::DevBuf<int64_t> member_off;
+  rr::DevBuf<double> pos_err, delta_db;
+};
+
+namespace rr {
+rr_lattice* enumerate_lattice(rr_ctx* ctx, const double* dims, const double* walls_alpha, const double* source,
+                              const double* receiver, double max_distance, double receiver_radius, const rr_air& air);
+rr_match* compare_lattice(rr_ctx* ctx, int64_t no, const double* opos, const double* oenergy, const int32_t* oorder,
+                          int64_t nt, const double* tpos, const double* tenergy, double pos_tol, double energy_tol_db);
+void air_beta_bands(const rr_air& a, double* beta);
+}  // namespace rr

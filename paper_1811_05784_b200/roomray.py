@@ -447,6 +447,126 @@ def build_image_sources(trace_res: DeviceTrace, total_rays: int, air: AirModel =
     return build_image_sources_device(trace_res, total_rays, air, options, receiver).fetch()
 
 
+# ------------------------------------------------------------------ shoebox lattice (shoebox.hpp)
+@dataclass
+class OracleImages:
+    """OracleImageSource list (shoebox.hpp:25-31), sorted by (distance, cell)."""
+
+    position: np.ndarray
+    distance: np.ndarray
+    order: np.ndarray
+    wall_hits: np.ndarray
+    band_energy: np.ndarray
+
+    def __len__(self):
+        return len(self.distance)
+
+
+class Lattice:
+    """enumerate_images result resident on the device (rr_lattice)."""
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+        n = C.c_int64()
+        check(lib.rr_lattice_info(h, C.byref(n)))
+        self.n = n.value
+
+    def __len__(self):
+        return self.n
+
+    def __del__(self):
+        if getattr(self, "h", None) and not _SHUTDOWN:
+            self.lib.rr_lattice_destroy(self.h)
+            self.h = None
+
+    def fetch(self) -> OracleImages:
+        n = self.n
+        o = OracleImages(np.empty((n, 3)), np.empty(n), np.empty(n, np.int32), np.empty((n, 6), np.int32),
+                         np.empty((n, NUM_BANDS)))
+        check(self.lib.rr_lattice_get(self.h, ptr(o.position), ptr(o.distance), ptr(o.order), ptr(o.wall_hits),
+                                      ptr(o.band_energy)))
+        return o
+
+
+def enumerate_images(dimensions, walls_alpha, source, receiver, max_distance: float, receiver_radius: float,
+                     air: AirModel = AirModel(), ctx: Context | None = None) -> Lattice:
+    """enumerate_images (shoebox.hpp:38-43) on the device: every mirror image of
+    `source` in the box [0, L]^3 within max_distance of `receiver`; walls
+    x0, x1, y0, y1, z0, z1 with 8-band absorption walls_alpha (6, 8)."""
+    ctx = ctx or Context.default()
+    a = air.c()
+    h = C.c_void_p()
+    check(ctx.lib.rr_shoebox_images(ctx.h, _f64(dimensions, (3,)), _f64(walls_alpha, (6 * NUM_BANDS,)),
+                                    _f64(source, (3,)), _f64(receiver, (3,)), float(max_distance),
+                                    float(receiver_radius), C.byref(a), C.byref(h)))
+    return Lattice(ctx.lib, h)
+
+
+@dataclass
+class MatchReport:
+    """MatchReport (shoebox.hpp:56-66); matched images in oracle order."""
+
+    oracle_index: np.ndarray
+    position_error: np.ndarray
+    order: np.ndarray
+    energy_delta_db: np.ndarray
+    member_off: np.ndarray
+    members: np.ndarray
+    unmatched_oracle: np.ndarray
+    unmatched_traced: np.ndarray
+    max_position_error: float
+    rms_energy_error_db: np.ndarray
+    pos_tol: float
+    energy_tol_db: float
+
+    def traced_indices(self, i):
+        return self.members[self.member_off[i]:self.member_off[i + 1]]
+
+    def energy_within(self, tol_db: float, max_order: int) -> bool:
+        """MatchReport::energy_within (shoebox.cpp:118-124)."""
+        sel = self.order <= max_order
+        return not bool((np.abs(self.energy_delta_db[sel]) > tol_db).any())
+
+
+def compare(oracle, traced, pos_tol: float, energy_tol_db: float, ctx: Context | None = None) -> MatchReport:
+    """compare (shoebox.hpp:67-70) on the device.  `oracle` is a Lattice or
+    OracleImages; `traced` a DeviceImages, ImageSources or (position, energy)."""
+    h = C.c_void_p()
+    if isinstance(oracle, Lattice) and isinstance(traced, DeviceImages):
+        lib = oracle.lib
+        check(lib.rr_lattice_compare_images(oracle.h, traced.h, float(pos_tol), float(energy_tol_db), C.byref(h)))
+    else:
+        ctx = ctx or Context.default()
+        lib = ctx.lib
+        if isinstance(oracle, Lattice):
+            oracle = oracle.fetch()
+        if isinstance(traced, DeviceImages):
+            traced = traced.fetch()
+        if isinstance(traced, tuple):
+            tp, te = traced
+        else:
+            tp, te = traced.position, traced.band_energy
+        op, oe = _f64(oracle.position).reshape(-1, 3), _f64(oracle.band_energy).reshape(-1, NUM_BANDS)
+        oo = np.ascontiguousarray(oracle.order, np.int32)
+        tp, te = _f64(tp).reshape(-1, 3), _f64(te).reshape(-1, NUM_BANDS)
+        check(lib.rr_shoebox_compare(ctx.h, len(op), ptr(op), ptr(oe), ptr(oo), len(tp), ptr(tp), ptr(te),
+                                     float(pos_tol), float(energy_tol_db), C.byref(h)))
+    try:
+        g, nm, nuo, nut = (C.c_int64() for _ in range(4))
+        mx = C.c_double()
+        rms = np.empty(NUM_BANDS)
+        check(lib.rr_match_info(h, C.byref(g), C.byref(nm), C.byref(nuo), C.byref(nut), C.byref(mx), rms))
+        n = g.value
+        r = MatchReport(np.empty(n, np.int32), np.empty(n), np.empty(n, np.int32), np.empty((n, NUM_BANDS)),
+                        np.empty(n + 1, np.int64), np.empty(nm.value, np.int32), np.empty(nuo.value, np.int32),
+                        np.empty(nut.value, np.int32), mx.value, rms, float(pos_tol), float(energy_tol_db))
+        check(lib.rr_match_get(h, ptr(r.oracle_index), ptr(r.position_error), ptr(r.order), ptr(r.energy_delta_db),
+                               ptr(r.member_off), ptr(r.members), ptr(r.unmatched_oracle), ptr(r.unmatched_traced)))
+        return r
+    finally:
+        lib.rr_match_destroy(h)
+
+
 FACTOR_NAMES = ("edt_s", "t30_s", "spl_db", "c80_db", "d50_pct", "ts_ms")
 
 

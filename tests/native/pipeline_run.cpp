@@ -1,7 +1,12 @@
 // Driver for tests/test_gpu_facade.py::test_pipeline_matches_oracle: runs
 // roomray_b200::run_trace_pipeline on a run-config file (the reference's
 // pipeline.cpp:144-185 shape) and dumps images, the broadband RIR and the
-// factors as raw arrays.   pipeline_run <run.json> <out_dir>
+// factors as raw arrays.   pipeline_run <run.json> <out_dir> [oracle.json]
+// With an oracle config (pipeline.hpp:47-61) it also runs run_oracle and
+// compare(oracle, images, 1e-9, 1.5) — acceptance criterion 4
+// (acceptance_main.cpp:239-272) — and prints the report.
+#include <algorithm>
+#include <cmath>
 #include <fstream>
 #include <iostream>
 #include <string>
@@ -18,7 +23,7 @@ static void write_all(const std::string& path, const std::vector<T>& v) {
 }
 
 int main(int argc, char** argv) {
-  if (argc != 3) return 2;
+  if (argc != 3 && argc != 4) return 2;
   const std::string out = argv[2];
   try {
     const rb::RunConfig cfg = rb::RunConfig::from_json_file(argv[1]);
@@ -46,6 +51,19 @@ int main(int argc, char** argv) {
               << a.images.size() << " images, stages";
     for (const auto& t : a.timings) std::cout << " " << t.name << "=" << t.seconds;
     std::cout << "\n";
+    if (argc == 4) {
+      const rb::OracleConfig oc = rb::OracleConfig::from_json_file(argv[3]);
+      const auto lattice = rb::run_oracle(oc);
+      const rb::MatchReport rep = rb::compare(lattice, a.images, 1e-9, 1.5);
+      double worst = 0.0;
+      for (const rb::MatchedImage& m : rep.matched)
+        if (m.order <= 2)
+          for (double d : m.energy_delta_db) worst = std::max(worst, std::abs(d));
+      std::cout << "acceptance4 oracle=" << lattice.size() << " matched=" << rep.matched.size()
+                << " oracle_only=" << rep.unmatched_oracle.size() << " traced_only=" << rep.unmatched_traced.size()
+                << " max_pos_err=" << rep.max_position_error << " worst_db=" << worst
+                << " within=" << (rep.energy_within(1.5, 2) ? 1 : 0) << "\n";
+    }
   } catch (const std::invalid_argument& e) {
     std::cout << "invalid_argument: " << e.what() << "\n";
     return 3;

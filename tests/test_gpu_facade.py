@@ -255,3 +255,30 @@ def test_facade_step_matches_reference(tmp_path, ref):
     alive, n_hist = rays_t[:, 7] == 1, rays_t[:, 8]
     assert n_hist.max() <= iters and np.all(n_hist[alive] == iters)  # one face per surviving iteration
     assert np.all(rays_t[~alive, 6] > st.max_range) or np.all(n_hist[~alive] < iters)
+
+
+@pytest.mark.gpu
+def test_pipeline_shoebox_acceptance(tmp_path):
+    """Acceptance criterion 4 (acceptance_main.cpp:239-272) through the C++
+    facade: run_trace_pipeline on the 5x4x3 shoebox with 10^5 rays, then
+    run_oracle (OracleConfig from JSON, pipeline.cpp:335-381) and compare at
+    1e-9 m / 1.5 dB: no traced-only images, orders <= 2 within 1.5 dB."""
+    import json
+    exe = _compile_pipeline(str(tmp_path / "pipeline_run"))
+    out = tmp_path / "out"
+    out.mkdir()
+    run = _pipeline_files(tmp_path, source={"position": [4, 2, 1.7], "ray_count": 100000})
+    walls = {w: ("concrete_block_coarse" if w.endswith("0") else "hollow_wooden_podium")
+             for w in ("x0", "x1", "y0", "y1", "z0", "z1")}
+    (tmp_path / "oracle.json").write_text(json.dumps({
+        "box": {"dimensions": [5, 4, 3]}, "materials": "materials.json", "walls": walls,
+        "source": {"position": [4, 2, 1.7], "ray_count": 100000}, "receiver": {"center": [2, 2, 1.7], "radius": 0.2},
+        "air": {"enabled": True, "temperature_c": 20, "relative_humidity": 50, "pressure_kpa": 101.325},
+        "max_distance": 0}))
+    r = subprocess.run([exe, str(run), str(out), str(tmp_path / "oracle.json")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = [x for x in r.stdout.splitlines() if x.startswith("acceptance4")][0]
+    f = dict(kv.split("=") for kv in line.split()[1:])
+    assert int(f["matched"]) > 0 and int(f["traced_only"]) == 0, line
+    assert float(f["max_pos_err"]) <= 1e-9 and f["within"] == "1", line
