@@ -118,6 +118,8 @@ rr_status rr_ctx_create(int device, rr_ctx** out) {
     cudaDeviceProp prop;
     RR_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) rr::invalid("roomray_b200 needs an sm_100a (Blackwell) device");
+    RR_CUDA(cudaMallocHost(&c->pinned, sizeof(int64_t) * 64));
+    for (cudaEvent_t& e : c->level_ev) RR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
   });
 }
@@ -128,6 +130,9 @@ void ctx_release(rr_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
+  for (cudaEvent_t e : ctx->level_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
 }
 
@@ -239,6 +244,7 @@ rr_status rr_scene_tree(rr_scene* s, rr_tree_node* nodes) {
     check_ptr(s, "scene");
     check_ptr(nodes, "nodes");
     RR_CUDA(cudaSetDevice(s->ctx->device));
+    rr::ensure_reference_tree(s);  // built on first use (rr_build.cu)
     RR_CUDA(cudaMemcpyAsync(nodes, s->ref.p, s->ref.bytes(), cudaMemcpyDeviceToHost, s->ctx->stream));
     RR_CUDA(cudaStreamSynchronize(s->ctx->stream));
   });

@@ -356,13 +356,25 @@ __global__ void plane_key_kernel(const double* __restrict__ fb, int64_t nf, int 
 __device__ __forceinline__ int32_t plane_lookup(const unsigned long long* __restrict__ table,
                                                 const int64_t* __restrict__ off, int k, double c) {
   const unsigned long long key = ord_key(c);
-  int64_t lo = off[k], hi = off[k + 1];
+  int64_t lo = off[2 * k], hi = off[2 * k + 1];  // axis k's sorted unique planes: [off[2k], off[2k+1])
   while (lo < hi) {
     const int64_t mid = (lo + hi) / 2;
     if (table[mid] < key) lo = mid + 1; else hi = mid;
   }
-  if (lo < off[k + 1] && table[lo] == key) return static_cast<int32_t>((k << 29) | (lo - off[k]));
+  if (lo < off[2 * k + 1] && table[lo] == key) return static_cast<int32_t>((k << 29) | (lo - off[2 * k]));
   return -1;
+}
+
+// per-axis table ranges from the unique counts; the "not flat on k"
+// sentinel (~0) sorts last and is dropped
+__global__ void plane_range_kernel(const unsigned long long* __restrict__ table, const int* __restrict__ num,
+                                   int64_t nf, int64_t* __restrict__ off) {
+  const int k = threadIdx.x;
+  if (k >= 3) return;
+  int64_t n = num[k];
+  if (n > 0 && table[k * nf + n - 1] == ~0ull) --n;
+  off[2 * k] = k * nf;
+  off[2 * k + 1] = k * nf + n;
 }
 
 __global__ void face_plane_kernel(const double* __restrict__ fb, int64_t nf,
@@ -424,16 +436,17 @@ inline unsigned grid_for(int64_t n, int block = 256) {
 
 }  // namespace
 
-void build_scene_tree(rr_scene* s) {
-  cudaStream_t st = s->ctx->stream;
-  const int64_t nf = s->nf;
-  cudaEvent_t e0, e1;
-  RR_CUDA(cudaEventCreate(&e0));
-  RR_CUDA(cudaEventCreate(&e1));
-  RR_CUDA(cudaEventRecord(e0, st));
+namespace {
+// Host plan of the reference median tree: per-level segment size multisets
+// (they depend on nf only), the cached top-K node count and level bases.
+struct LevelPlan {
+  int n_levels = 0, D = 0;
+  int64_t K = 0, max_seg = 1;
+  std::vector<int64_t> seg_count, split_count;
+  std::vector<int32_t> level_base;
+};
 
-  StageTimer tm(st);
-  // ---- host plan: per-level segment size multisets (depend on nf only)
+LevelPlan plan_levels(int64_t nf) {
   std::vector<std::map<int64_t, int64_t>> levels;
   levels.push_back({{nf, 1}});
   for (;;) {
@@ -469,10 +482,123 @@ void build_scene_tree(rr_scene* s) {
   int64_t max_seg = 1;
   for (auto c : seg_count) max_seg = std::max(max_seg, c);
 
-  s->depth = n_levels - 1;
-  s->K = static_cast<int32_t>(K);
+  LevelPlan lp;
+  lp.n_levels = n_levels;
+  lp.D = D;
+  lp.K = K;
+  lp.max_seg = max_seg;
+  lp.seg_count = seg_count;
+  lp.split_count = split_count;
+  lp.level_base = level_base;
+  return lp;
+}
+}  // namespace
+
+// Scene build: face plane ids, the SAH traversal tree (rr_sah.cu) and the
+// mesh bounds.  The reference-layout median tree (accel_tree.cpp:19-87) is
+// built on first use only (ensure_reference_tree): traversal, projection
+// and nearest_hit run on the SAH tree, so run_trace_pipeline never needs it.
+void build_scene_tree(rr_scene* s) {
+  cudaStream_t st = s->ctx->stream;
+  const int64_t nf = s->nf;
+  cudaEvent_t e0, e1;
+  RR_CUDA(cudaEventCreate(&e0));
+  RR_CUDA(cudaEventCreate(&e1));
+  RR_CUDA(cudaEventRecord(e0, st));
+  StageTimer tm(st);
+  const LevelPlan lp = plan_levels(nf);
+  s->depth = lp.n_levels - 1;
+  s->K = static_cast<int32_t>(lp.K);
   s->root = static_cast<int32_t>(2 * nf - 2);
 
+  DevBuf<double> fb;
+  fb.alloc(6 * nf, st);
+  {
+    DevBuf<uint64_t> keys;
+    DevBuf<int32_t> ids;
+    keys.alloc(3 * nf, st);
+    ids.alloc(3 * nf, st);
+    face_prep_kernel<<<grid_for(nf), 256, 0, st>>>(s->verts.p, s->tris.p, nf, fb.p, keys.p, ids.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches++;
+  }
+  // ---- axis-aligned plane tables: per axis, the sorted unique plane
+  // coordinates of the flat faces; ids for faces and for tree children
+  DevBuf<unsigned long long>& table = s->plane_table;
+  DevBuf<int64_t>& doff = s->plane_off;
+  {
+    DevBuf<unsigned long long> pkeys, psorted;
+    DevBuf<int> dnum;
+    DevBuf<uint8_t> ptmp;
+    pkeys.alloc(nf, st);
+    psorted.alloc(nf, st);
+    table.alloc(3 * nf, st);
+    doff.alloc(6, st);
+    dnum.alloc(3, st);
+    size_t need = 0, need2 = 0;
+    RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+    RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p, dnum.p, static_cast<int>(nf), st));
+    ptmp.alloc(std::max(need, need2), st);
+    for (int k = 0; k < 3; ++k) {  // axis k's unique planes at table + k * nf
+      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
+      RR_LAUNCH_CHECK();
+      size_t t = ptmp.n;
+      RR_CUDA(cub::DeviceRadixSort::SortKeys(ptmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
+      t = ptmp.n;
+      RR_CUDA(cub::DeviceSelect::Unique(ptmp.p, t, psorted.p, table.p + k * nf, dnum.p + k, static_cast<int>(nf), st));
+      s->ctx->launches += 6;
+    }
+    plane_range_kernel<<<1, 32, 0, st>>>(table.p, dnum.p, nf, doff.p);
+    s->face_plane.alloc(nf, st);
+    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 2;
+  }
+
+  tm.mark("build: plane tables");
+  build_sah_tree(s, st);
+  tm.mark("build: SAH tree");
+  // ---- TriangleMesh::bounds over all vertices (image-source tolerance)
+  DevBuf<unsigned long long> vb;
+  vb.alloc(6, st);
+  RR_CUDA(cudaMemsetAsync(vb.p, 0xff, sizeof(unsigned long long) * 3, st));
+  RR_CUDA(cudaMemsetAsync(vb.p + 3, 0x00, sizeof(unsigned long long) * 3, st));
+  const int64_t nv = std::max<int64_t>(s->nv, 1);
+  vert_bounds_kernel<<<std::min<unsigned>(grid_for(nv), 1184u), 256, 0, st>>>(s->verts.p, s->nv, vb.p);
+  RR_LAUNCH_CHECK();
+  DevBuf<double> vbd;
+  vbd.alloc(6, st);
+  unmap_bounds_kernel<<<1, 32, 0, st>>>(vb.p, vbd.p);
+  RR_LAUNCH_CHECK();
+  s->ctx->launches += 2;
+  double hb[6];
+  RR_CUDA(cudaMemcpyAsync(hb, vbd.p, sizeof hb, cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaEventRecord(e1, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < 3; ++k) {
+    s->lo[k] = hb[k];
+    s->hi[k] = hb[3 + k];
+  }
+  RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// The reference median tree in its own layout (RefNode, for
+// AccelTree::nodes) and as TNodes / 4-wide QNodes for the diagnostic
+// traversals (RR_SAH=0, nearest_hit_batch brute = 3): level-synchronous
+// exact-median split of three presorted face lists (accel_tree.cpp:19-47).
+void ensure_reference_tree(rr_scene* s) {
+  if (s->ref_built) return;
+  cudaStream_t st = s->ctx->stream;
+  const int64_t nf = s->nf;
+  StageTimer tm(st);
+  const LevelPlan lp = plan_levels(nf);
+  const int n_levels = lp.n_levels, D = lp.D;
+  const int64_t K = lp.K, max_seg = lp.max_seg;
+  const std::vector<int64_t>& seg_count = lp.seg_count;
+  const std::vector<int64_t>& split_count = lp.split_count;
+  const std::vector<int32_t>& level_base = lp.level_base;
   // ---- buffers
   DevBuf<double> fb;
   fb.alloc(6 * nf, st);
@@ -512,92 +638,6 @@ void build_scene_tree(rr_scene* s) {
   face_prep_kernel<<<grid_for(nf), 256, 0, st>>>(s->verts.p, s->tris.p, nf, fb.p, keys.p, ids.p);
   RR_LAUNCH_CHECK();
   s->ctx->launches++;
-
-  // ---- axis-aligned plane tables: per axis, the sorted unique plane
-  // coordinates of the flat faces; ids for faces and for tree children
-  DevBuf<unsigned long long> table;
-  DevBuf<int64_t> doff;
-  {
-    DevBuf<unsigned long long> pkeys, psorted;
-    DevBuf<int> dnum;
-    DevBuf<uint8_t> ptmp;
-    pkeys.alloc(nf, st);
-    psorted.alloc(nf, st);
-    table.alloc(3 * nf, st);
-    doff.alloc(4, st);
-    dnum.alloc(1, st);
-    int64_t hoff[4] = {0, 0, 0, 0};
-    for (int k = 0; k < 3; ++k) {
-      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
-      RR_LAUNCH_CHECK();
-      size_t need = 0;
-      RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-      size_t need2 = 0;
-      RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf),
-                                        st));
-      if (std::max(need, need2) > ptmp.n) ptmp.alloc(std::max(need, need2), st);
-      size_t t = ptmp.n;
-      RR_CUDA(cub::DeviceRadixSort::SortKeys(ptmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-      t = ptmp.n;
-      RR_CUDA(cub::DeviceSelect::Unique(ptmp.p, t, psorted.p, table.p + hoff[k], dnum.p, static_cast<int>(nf), st));
-      int num = 0;
-      unsigned long long last = 0;
-      RR_CUDA(cudaMemcpyAsync(&num, dnum.p, sizeof num, cudaMemcpyDeviceToHost, st));
-      RR_CUDA(cudaStreamSynchronize(st));
-      if (num > 0)
-        RR_CUDA(cudaMemcpyAsync(&last, table.p + hoff[k] + num - 1, sizeof last, cudaMemcpyDeviceToHost, st));
-      RR_CUDA(cudaStreamSynchronize(st));
-      if (num > 0 && last == ~0ull) --num;  // the "not flat on k" sentinel
-      hoff[k + 1] = hoff[k] + num;
-      s->ctx->launches += 6;
-    }
-    RR_CUDA(cudaMemcpyAsync(doff.p, hoff, sizeof hoff, cudaMemcpyHostToDevice, st));
-    s->face_plane.alloc(nf, st);
-    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
-    RR_LAUNCH_CHECK();
-    s->ctx->launches += 1;
-    RR_CUDA(cudaStreamSynchronize(st));  // hoff is a stack array
-  }
-
-  // ---- the SAH traversal tree (rr_sah.cu) needs only the faces and their
-  // plane ids: build it on a second stream from a second host thread while
-  // this thread builds the reference tree
-  cudaStream_t st2 = nullptr;
-  RR_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  cudaEvent_t ready;
-  RR_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  RR_CUDA(cudaEventRecord(ready, st));
-  RR_CUDA(cudaStreamWaitEvent(st2, ready, 0));
-  cudaEventDestroy(ready);
-  std::exception_ptr sah_error;
-  float sah_ms = 0.f;
-  std::thread sah_thread([s, st2, &sah_error, &sah_ms] {
-    try {
-      RR_CUDA(cudaSetDevice(s->ctx->device));
-      cudaEvent_t a0, a1;
-      RR_CUDA(cudaEventCreate(&a0));
-      RR_CUDA(cudaEventCreate(&a1));
-      RR_CUDA(cudaEventRecord(a0, st2));
-      build_sah_tree(s, st2);
-      RR_CUDA(cudaEventRecord(a1, st2));
-      RR_CUDA(cudaEventSynchronize(a1));
-      RR_CUDA(cudaEventElapsedTime(&sah_ms, a0, a1));
-      cudaEventDestroy(a0);
-      cudaEventDestroy(a1);
-    } catch (...) {
-      sah_error = std::current_exception();
-    }
-  });
-  struct Joiner {  // join on every exit path (exceptions included)
-    std::thread& t;
-    ~Joiner() {
-      if (t.joinable()) t.join();
-    }
-  } joiner{sah_thread};
-  // large scenes keep the GPU busy with one build at a time (C5: 27 ms
-  // sequential vs 33 ms overlapped); small ones are launch-latency bound and
-  // overlap well (C2: 6.1 -> 4.8 ms)
-  if (nf > (int64_t(1) << 18)) sah_thread.join();
 
   // ---- CUB scratch
   size_t tmp_sort = 0, tmp_scan = 0, tmp_scan2 = 0;
@@ -655,9 +695,8 @@ void build_scene_tree(rr_scene* s) {
     std::swap(segs, nsegs);
   }
 
-  tm.mark("build: reference levels");
-  tm.mark("build: plane tables");
-  node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, table.p, doff.p,
+  tm.mark("reference tree: levels");
+  node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, s->plane_table.p, s->plane_off.p,
                                                          s->tnodes.p);
   RR_LAUNCH_CHECK();
   s->ctx->launches++;
@@ -690,46 +729,16 @@ void build_scene_tree(rr_scene* s) {
     k4 = std::min<int32_t>(counts[1], kMaxCachedQNodes);
   }
 
-  tm.mark("build: 4-wide collapse");
-  // ---- TriangleMesh::bounds over all vertices (image-source tolerance)
-  DevBuf<unsigned long long> vb;
-  vb.alloc(6, st);
-  RR_CUDA(cudaMemsetAsync(vb.p, 0xff, sizeof(unsigned long long) * 3, st));
-  RR_CUDA(cudaMemsetAsync(vb.p + 3, 0x00, sizeof(unsigned long long) * 3, st));
-  const int64_t nv = std::max<int64_t>(s->nv, 1);
-  vert_bounds_kernel<<<std::min<unsigned>(grid_for(nv), 1184u), 256, 0, st>>>(s->verts.p, s->nv, vb.p);
-  RR_LAUNCH_CHECK();
-  DevBuf<double> vbd;
-  vbd.alloc(6, st);
-  unmap_bounds_kernel<<<1, 32, 0, st>>>(vb.p, vbd.p);
-  RR_LAUNCH_CHECK();
-  s->ctx->launches += 2;
-  double hb[6];
-  RR_CUDA(cudaMemcpyAsync(hb, vbd.p, sizeof hb, cudaMemcpyDeviceToHost, st));
+  tm.mark("reference tree: 4-wide collapse");
   RR_CUDA(cudaMemcpyAsync(&s->hdr, s->dhdr.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
-  RR_CUDA(cudaEventRecord(e1, st));
   RR_CUDA(cudaStreamSynchronize(st));
-  for (int k = 0; k < 3; ++k) {
-    s->lo[k] = hb[k];
-    s->hi[k] = hb[3 + k];
-  }
   s->hdr.K = static_cast<int32_t>(K);
   s->hdr.K4 = k4;
   s->hdr.root4 = nf == 1 ? s->hdr.root_ref : 0;
   s->hdr.depth = s->depth;
   RR_CUDA(cudaMemcpyAsync(s->dhdr.p, &s->hdr, sizeof(TravHeader), cudaMemcpyHostToDevice, st));
-  RR_CUDA(cudaEventElapsedTime(&s->build_ms, e0, e1));
-  if (sah_thread.joinable()) sah_thread.join();
-  RR_CUDA(cudaStreamSynchronize(st2));
-  // the SAH buffers were allocated on st2: later frees go to the scene's stream
-  s->snodes.s = st;
-  s->s4nodes.s = st;
-  cudaStreamDestroy(st2);
-  if (sah_error) std::rethrow_exception(sah_error);
-  tm.mark("build: SAH tree (joined)");
-  s->build_ms = std::max(s->build_ms, sah_ms);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  RR_CUDA(cudaStreamSynchronize(st));
+  s->ref_built = true;
 }
 
 }  // namespace rr

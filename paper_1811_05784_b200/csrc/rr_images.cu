@@ -889,8 +889,11 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   }
   tm.mark("coplanar merge");
   EnergyParams ep;
-  ep.hdr = s->hdr;
-  ep.nodes = s->tnodes.p;
+  // projection (image_sources.cpp:142-152) on the SAH tree: closest hits do
+  // not depend on the tree (rr_geom.cuh), so this equals the reference's
+  if (!s->snodes.p) ensure_reference_tree(s);
+  ep.hdr = s->snodes.p ? s->shdr : s->hdr;
+  ep.nodes = s->snodes.p ? s->snodes.p : s->tnodes.p;
   ep.tri = s->tri.p;
   for (int k = 0; k < 3; ++k) ep.recv[k] = tr->recv_center[3 * recv + k];
   for (int b = 0; b < kBands; ++b) ep.beta[b] = beta[b];

@@ -151,6 +151,8 @@ struct rr_ctx {
   cudaStream_t stream = nullptr;
   std::atomic<int64_t> launches{0};  // the scene build counts from two host threads
   int sm_count = 0;
+  int64_t* pinned = nullptr;        // 64 pinned int64 slots for asynchronous read-backs
+  cudaEvent_t level_ev[64] = {};    // per-level events of the SAH build
 };
 
 struct rr_scene {
@@ -176,6 +178,9 @@ struct rr_scene {
   int32_t sah_depth = 0;
   int64_t n_qnodes = 0;
   rr::DevBuf<rr::TravHeader> dhdr;
+  rr::DevBuf<unsigned long long> plane_table;  // sorted unique axis-aligned plane coordinates
+  rr::DevBuf<int64_t> plane_off;               // per-axis offsets into plane_table (4)
+  bool ref_built = false;         // reference tree (ref, tnodes, qnodes, hdr) built on first use
   rr::TravHeader hdr{};
   int32_t root = -1, depth = 0, K = 0;
   double lo[3]{}, hi[3]{};        // TriangleMesh::bounds (geometry.cpp:41-45)
@@ -186,8 +191,10 @@ struct rr_scene {
 namespace rr {
 // rr_build.cu
 void build_scene_tree(rr_scene* s);
+void ensure_reference_tree(rr_scene* s);
 // rr_sah.cu (needs face_plane; runs on its own stream)
 void build_sah_tree(rr_scene* s, cudaStream_t st);
+void build_sah4(rr_scene* s);  // 4-wide collapse, on demand
 // rr_trace.cu
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
                        int64_t n, int brute, int32_t* d_face, double* d_delta,

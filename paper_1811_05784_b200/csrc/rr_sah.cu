@@ -58,6 +58,17 @@ struct SSeg {
   int32_t side;    // 0 left, 1 right
 };
 
+// Per-level counters kept on the device, so the host enqueues whole levels
+// without reading anything back: S segments at this level, the BFS index of
+// its first internal node, and this level's split / SAH segment counts.
+struct LevelState {
+  int64_t S;
+  int64_t n_split;
+  int64_t n_sah;
+  int32_t level_base;
+  int32_t pad;
+};
+
 __device__ __forceinline__ uint64_t okey(double x) {
   if (x == 0.0) x = 0.0;
   uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
@@ -253,15 +264,18 @@ __global__ void root_hdr_kernel(const unsigned long long* __restrict__ bb, TravH
 }
 
 // 3. node emission and split choice
-__global__ void split_kernel(const SSeg* __restrict__ segs, int64_t S, const int32_t* __restrict__ rank,
+__global__ void split_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls,
+                             const int32_t* __restrict__ rank,
                              const unsigned long long* __restrict__ bb, const unsigned long long* __restrict__ cb,
                              const int32_t* __restrict__ pl, const int32_t* __restrict__ sah_idx,
                              const int32_t* __restrict__ bcnt, const uint32_t* __restrict__ bbox,
-                             const int32_t* __restrict__ perm0, int32_t level_base, float eps, TNode* __restrict__ tn,
+                             const int32_t* __restrict__ perm0, TNode* __restrict__ tn,
                              TravHeader* __restrict__ hdr, int32_t* __restrict__ seg_axis,
                              int32_t* __restrict__ seg_split, int64_t* __restrict__ seg_nl, SSeg* __restrict__ next) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= S) return;
+  if (j >= ls->S) return;
+  const int32_t level_base = ls->level_base;
+  const float eps = hdr->eps;
   const SSeg sg = segs[j];
   if (sg.n >= 2 && sg.n <= kSmall) {  // finish_kernel's
     seg_axis[j] = -1;
@@ -383,12 +397,14 @@ __device__ void child_slot(TNode* p, int side, const double* lo, const double* h
   }
 }
 
-__global__ void finish_kernel(const SSeg* __restrict__ segs, int64_t S, const int32_t* __restrict__ perm0,
-                              const double* __restrict__ fb, const double* __restrict__ cen,
-                              const int32_t* __restrict__ face_plane, int64_t nf, float eps, TNode* __restrict__ tn,
-                              TravHeader* __restrict__ hdr, unsigned long long* __restrict__ top) {
+__global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls,
+                              const int32_t* __restrict__ perm0, const double* __restrict__ fb,
+                              const double* __restrict__ cen, const int32_t* __restrict__ face_plane, int64_t nf,
+                              TNode* __restrict__ tn, TravHeader* __restrict__ hdr,
+                              unsigned long long* __restrict__ top) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= S) return;
+  if (j >= ls->S) return;
+  const float eps = hdr->eps;
   const SSeg sg = segs[j];
   const int n = static_cast<int>(sg.n);
   if (n < 2 || n > kSmall) return;
@@ -529,10 +545,10 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* 
   if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
 }
 
-__global__ void seg_init_kernel(int64_t S, unsigned long long* __restrict__ bb, unsigned long long* __restrict__ cb,
-                                int32_t* __restrict__ pl) {
+__global__ void seg_init_kernel(const LevelState* __restrict__ ls, unsigned long long* __restrict__ bb,
+                                unsigned long long* __restrict__ cb, int32_t* __restrict__ pl) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= S) return;
+  if (j >= ls->S) return;
   for (int k = 0; k < 3; ++k) {  // ordered keys: min from ~0, max from 0
     bb[6 * j + k] = ~0ull;
     bb[6 * j + 3 + k] = 0ull;
@@ -544,11 +560,12 @@ __global__ void seg_init_kernel(int64_t S, unsigned long long* __restrict__ bb, 
 }
 
 // packed flags: split (>= kSmall + 1 faces) << 32 | SAH-eligible
-__global__ void split_flag_kernel(const SSeg* __restrict__ segs, int64_t S, int level,
-                                  unsigned long long* __restrict__ flags) {
+__global__ void split_flag_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls, int64_t s_max,
+                                  int level, unsigned long long* __restrict__ flags) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j > S) return;
-  if (j == S) {
+  const int64_t S = ls->S;
+  if (j > s_max) return;
+  if (j >= S) {  // the scan runs over the level's upper bound s_max + 1
     flags[j] = 0;
     return;
   }
@@ -562,9 +579,16 @@ __global__ void split_flag_kernel(const SSeg* __restrict__ segs, int64_t S, int 
 }
 
 __global__ void rank_kernel(const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ ranks,
-                            int64_t S, int32_t* __restrict__ srank, int32_t* __restrict__ sah_idx, int64_t n_bins,
+                            LevelState* __restrict__ ls, int32_t* __restrict__ srank, int32_t* __restrict__ sah_idx,
                             int32_t* __restrict__ bcnt, uint32_t* __restrict__ bbox) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t S = ls->S;
+  const unsigned long long both = ranks[S];  // exclusive scan at S = the level's totals
+  const int64_t n_bins = static_cast<int64_t>(both & 0xffffffffull) * 3 * kBins;
+  if (j == 0) {
+    ls->n_split = static_cast<int64_t>(both >> 32);
+    ls->n_sah = static_cast<int64_t>(both & 0xffffffffull);
+  }
   if (j < S) {
     srank[j] = static_cast<int32_t>(ranks[j] >> 32);
     sah_idx[j] = (flags[j] & 0xffffffffull) ? static_cast<int32_t>(ranks[j] & 0xffffffffull) : -1;
@@ -576,6 +600,14 @@ __global__ void rank_kernel(const unsigned long long* __restrict__ flags, const 
       bbox[6 * j + 3 + k] = 0u;
     }
   }
+}
+
+// end of a level: the next one has 2 * n_split segments, its nodes follow
+__global__ void advance_kernel(LevelState* __restrict__ ls, int64_t* __restrict__ s_out) {
+  if (threadIdx.x) return;
+  ls->level_base += static_cast<int32_t>(ls->n_split);
+  ls->S = 2 * ls->n_split;
+  *s_out = ls->S;
 }
 
 // ---- 4-wide collapse of the SAH tree: every internal node at even depth
@@ -690,7 +722,12 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   RR_CUDA(cudaMemsetAsync(dh.p, 0, sizeof(TravHeader), st));
   RR_CUDA(cudaMemsetAsync(posA.p, 0, sizeof(int32_t) * nf, st));
 
-  int64_t max_seg = nf;  // segments per level never exceed the face count
+  // Upper bounds for the device-resident level sizes: a level has at most
+  // 2^L segments, below the root at most 2 * nf / (kSmall + 1) (only
+  // segments of more than kSmall faces split), and at most nf / kSahMin
+  // SAH-binned segments.
+  const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(nf, 2 * (nf / (kSmall + 1)) + 2));
+  const int64_t max_sah = nf / kSahMin + 1;
   DevBuf<SSeg> segA, segB;
   DevBuf<int32_t> srank, sah_idx, axis, split, pl;
   DevBuf<unsigned long long> flags, franks;
@@ -710,58 +747,63 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   cb.alloc(6 * max_seg, st);
   DevBuf<int32_t> bcnt;
   DevBuf<uint32_t> bbox;
+  bcnt.alloc(max_sah * 3 * kBins, st);
+  bbox.alloc(max_sah * 3 * kBins * 6, st);
   const SSeg root{0, nf, -1, 0};
   RR_CUDA(cudaMemcpyAsync(segA.p, &root, sizeof root, cudaMemcpyHostToDevice, st));
+  DevBuf<LevelState> ls;
+  ls.alloc(1, st);
+  const LevelState ls0{1, 0, 0, 0, 0};
+  RR_CUDA(cudaMemcpyAsync(ls.p, &ls0, sizeof ls0, cudaMemcpyHostToDevice, st));
+  // the next level's segment count, per level, read back a few levels late
+  // (pinned slots and events owned by the context)
+  constexpr int kMaxLevels = 64;
+  int64_t* h_next = s->ctx->pinned;
+  DevBuf<int64_t> d_next;
+  d_next.alloc(kMaxLevels, st);
+  cudaEvent_t* lev_ev = s->ctx->level_ev;
+  int n_ev = 0;
   int32_t *perm = permA.p, *perm_o = permB.p, *pos = posA.p, *pos_o = posB.p;
   SSeg *segs = segA.p, *nsegs = segB.p;
-  int64_t S = 1;
-  int32_t level_base = 0;
   DevBuf<unsigned long long> top;  // internal nodes handed to finish_kernel (from the top)
   top.alloc(1, st);
   RR_CUDA(cudaMemsetAsync(top.p, 0, sizeof(unsigned long long), st));
-  int depth = 0;
-  float eps = 0.f;  // from the root box, read back with level 0's counts
   StageTimer tm(st);
-  for (int L = 0; S > 0; ++L) {
-    depth = L;
+  // Levels are enqueued without host round trips; the host learns that the
+  // tree is complete kLag levels later and stops.  Levels enqueued after the
+  // last split find no segments and change nothing.
+  constexpr int kLag = 2;
+  int depth = -1;
+  for (int L = 0; L < kMaxLevels && depth < 0; ++L) {
     if (tm.on) tm.mark(L < 64 ? kLevelNames[L] : "level");
+    const int64_t s_max = L == 0 ? 1 : std::min<int64_t>(max_seg, L < 62 ? (int64_t(1) << L) : max_seg);
+    const int64_t sah_max = std::min<int64_t>(s_max, max_sah);
     // 1. bounds (one init launch for the per-segment accumulators)
-    seg_init_kernel<<<grid(S), 256, 0, st>>>(S, bb.p, cb.p, pl.p);
+    seg_init_kernel<<<grid(s_max), 256, 0, st>>>(ls.p, bb.p, cb.p, pl.p);
     bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
     if (L == 0) root_hdr_kernel<<<1, 32, 0, st>>>(bb.p, dh.p);
     // 2. split flags and SAH flags, both ranks from one 64-bit scan
     //    (split flag in the high word, SAH flag in the low word)
-    split_flag_kernel<<<grid(S + 1), 256, 0, st>>>(segs, S, L, flags.p);
+    split_flag_kernel<<<grid(s_max + 1), 256, 0, st>>>(segs, ls.p, s_max, L, flags.p);
     RR_LAUNCH_CHECK();
     cub_run([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, flags.p, franks.p, static_cast<int>(S + 1), st);
+      return cub::DeviceScan::ExclusiveSum(t, b, flags.p, franks.p, static_cast<int>(s_max + 1), st);
     }, tmp, st);
-    unsigned long long both = 0;
-    RR_CUDA(cudaMemcpyAsync(&both, franks.p + S, sizeof both, cudaMemcpyDeviceToHost, st));
-    if (L == 0) RR_CUDA(cudaMemcpyAsync(&eps, &dh.p->eps, sizeof eps, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaStreamSynchronize(st));
-    const int64_t n_split = static_cast<int64_t>(both >> 32), n_sah = static_cast<int64_t>(both & 0xffffffffull);
     // srank[j] / sah_idx[j] (compact index, -1 for non-SAH segments), bins reset
-    if (n_sah > 0) {
-      bcnt.alloc(n_sah * 3 * kBins, st);
-      bbox.alloc(n_sah * 3 * kBins * 6, st);
-    }
-    rank_kernel<<<grid(std::max<int64_t>(S, n_sah * 3 * kBins)), 256, 0, st>>>(flags.p, franks.p, S, srank.p,
-                                                                               sah_idx.p, n_sah * 3 * kBins,
-                                                                               bcnt.p, bbox.p);
+    rank_kernel<<<grid(std::max<int64_t>(s_max, sah_max * 3 * kBins)), 256, 0, st>>>(flags.p, franks.p, ls.p,
+                                                                                    srank.p, sah_idx.p, bcnt.p,
+                                                                                    bbox.p);
     RR_LAUNCH_CHECK();
-    if (n_sah > 0) {
+    if (sah_max > 0) {
       bin_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, cb.p, sah_idx.p, nf, bcnt.p, bbox.p);
       RR_LAUNCH_CHECK();
     }
     // 3. nodes + splits
-    split_kernel<<<grid(S), 256, 0, st>>>(segs, S, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
-                                          level_base, eps, s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
-    finish_kernel<<<grid(S, 64), 64, 0, st>>>(segs, S, perm, fb.p, cen.p, s->face_plane.p, nf, eps, s->snodes.p,
-                                              dh.p, top.p);
+    split_kernel<<<grid(s_max), 256, 0, st>>>(segs, ls.p, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
+                                              s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
+    finish_kernel<<<grid(s_max, 64), 64, 0, st>>>(segs, ls.p, perm, fb.p, cen.p, s->face_plane.p, nf, s->snodes.p,
+                                                  dh.p, top.p);
     RR_LAUNCH_CHECK();
-    s->ctx->launches += 6;
-    if (n_split == 0) break;
     // 4. stable partition of the three lists
     flag_kernel<<<grid(nf), 256, 0, st>>>(pos, segs, axis.p, split.p, cb.p, cen.p, perm, nf, flag.p);
     gather_kernel<<<grid(3 * nf), 256, 0, st>>>(perm, flag.p, 3 * nf, fl.p);
@@ -771,43 +813,26 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
     }, tmp, st);
     scatter_kernel<<<grid(3 * nf), 256, 0, st>>>(pos, segs, axis.p, nl.p, srank.p, perm, fl.p, scan.p, nf, perm_o,
                                                   pos_o);
+    advance_kernel<<<1, 32, 0, st>>>(ls.p, d_next.p + L);
     RR_LAUNCH_CHECK();
-    s->ctx->launches += 4;
+    RR_CUDA(cudaMemcpyAsync(h_next + L, d_next.p + L, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    n_ev = L + 1;
+    RR_CUDA(cudaEventRecord(lev_ev[L], st));
+    s->ctx->launches += 12;
     std::swap(perm, perm_o);
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
-    level_base += static_cast<int32_t>(n_split);
-    S = 2 * n_split;
+    const int seen = L - kLag;  // the newest level the host waits for
+    if (seen >= 0) {
+      RR_CUDA(cudaEventSynchronize(lev_ev[seen]));
+      for (int q = 0; q <= seen && depth < 0; ++q)
+        if (h_next[q] == 0) depth = q;
+    }
   }
-  {  // 4-wide collapse (traversed by the wide kernel variant)
-    const int32_t n_int = static_cast<int32_t>(nf - 1);
-    TravHeader hh;
-    RR_CUDA(cudaMemcpyAsync(&hh, dh.p, sizeof hh, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaStreamSynchronize(st));
-    DevBuf<int32_t> depthb, qf, qi;
-    depthb.alloc(n_int, st);
-    qf.alloc(n_int + 1, st);
-    qi.alloc(n_int + 1, st);
-    RR_CUDA(cudaMemsetAsync(depthb.p, 0xff, depthb.bytes(), st));
-    if (hh.root_ref >= 0) RR_CUDA(cudaMemsetAsync(depthb.p + hh.root_ref, 0, sizeof(int32_t), st));
-    for (int d = 0; d <= depth + 6; ++d)
-      depth_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, d, depthb.p);
-    qflag_kernel<<<grid(n_int + 1), 256, 0, st>>>(depthb.p, n_int, qf.p);
-    cub_run([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, qf.p, qi.p, static_cast<int>(n_int + 1), st);
-    }, tmp, st);
-    int32_t nq = 0;
-    RR_CUDA(cudaMemcpyAsync(&nq, qi.p + n_int, sizeof nq, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaStreamSynchronize(st));
-    s->s4nodes.alloc(std::max(nq, 1), st);
-    qbuild_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, qf.p, qi.p, s->s4nodes.p);
-    RR_LAUNCH_CHECK();
-    int32_t root4 = hh.root_ref;
-    if (hh.root_ref >= 0) RR_CUDA(cudaMemcpyAsync(&root4, qi.p + hh.root_ref, sizeof root4, cudaMemcpyDeviceToHost, st));
-    RR_CUDA(cudaStreamSynchronize(st));
-    s->s4root = root4;
-    s->ctx->launches += depth + 10;
-  }
+  RR_CUDA(cudaStreamSynchronize(st));
+  for (int q = 0; q < n_ev && depth < 0; ++q)
+    if (h_next[q] == 0) depth = q;
+  if (depth < 0) throw Error(RR_RUNTIME, "SAH build did not terminate");
   RR_CUDA(cudaMemcpyAsync(&s->shdr, dh.p, sizeof(TravHeader), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
   s->shdr.K = 0;
@@ -815,6 +840,42 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   s->shdr.root4 = 0;
   s->sah_depth = depth;
   if (depth > kMaxDepth) throw Error(RR_RUNTIME, "SAH tree deeper than the traversal stack");
+  // the 4-wide collapse serves the deep-tree kernel only; smaller scenes
+  // build it on demand (build_sah4)
+  if (nf >= (int64_t(1) << 18)) build_sah4(s);
+}
+
+// 4-wide collapse of the SAH tree (traversed by trace_kernel<3, ...>).
+void build_sah4(rr_scene* s) {
+  if (s->s4nodes.p || !s->snodes.p) return;
+  cudaStream_t st = s->ctx->stream;
+  const int32_t n_int = static_cast<int32_t>(s->nf - 1);
+  const int depth = s->sah_depth;
+  DevBuf<uint8_t> tmp;
+  DevBuf<int32_t> depthb, qf, qi;
+  depthb.alloc(n_int, st);
+  qf.alloc(n_int + 1, st);
+  qi.alloc(n_int + 1, st);
+  RR_CUDA(cudaMemsetAsync(depthb.p, 0xff, depthb.bytes(), st));
+  const int32_t root_ref = s->shdr.root_ref;
+  if (root_ref >= 0) RR_CUDA(cudaMemsetAsync(depthb.p + root_ref, 0, sizeof(int32_t), st));
+  for (int d = 0; d <= depth + 6; ++d)
+    depth_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, d, depthb.p);
+  qflag_kernel<<<grid(n_int + 1), 256, 0, st>>>(depthb.p, n_int, qf.p);
+  cub_run([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, qf.p, qi.p, static_cast<int>(n_int + 1), st);
+  }, tmp, st);
+  int32_t nq = 0;
+  RR_CUDA(cudaMemcpyAsync(&nq, qi.p + n_int, sizeof nq, cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  s->s4nodes.alloc(std::max(nq, 1), st);
+  qbuild_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, qf.p, qi.p, s->s4nodes.p);
+  RR_LAUNCH_CHECK();
+  int32_t root4 = root_ref;
+  if (root_ref >= 0) RR_CUDA(cudaMemcpyAsync(&root4, qi.p + root_ref, sizeof root4, cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  s->s4root = root4;
+  s->ctx->launches += depth + 10;
 }
 
 }  // namespace rr

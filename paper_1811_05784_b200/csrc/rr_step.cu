@@ -169,6 +169,7 @@ rr_trace_result* step_rays(rr_scene* s, int64_t n, double* origin, double* dir, 
   if (!(recv->radius > 0.0)) invalid("receiver radius must be > 0");
   cudaStream_t st = s->ctx->stream;
   const bool sah = s->snodes.p != nullptr;
+  if (!sah) ensure_reference_tree(s);
   StepParams p{};
   p.hdr = sah ? s->shdr : s->hdr;
   p.nodes = sah ? s->snodes.p : s->tnodes.p;

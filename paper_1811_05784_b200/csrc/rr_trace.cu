@@ -647,10 +647,15 @@ void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d, int64_
                        double* d_delta, double* d_point) {
   if (n <= 0) return;
   const unsigned g = static_cast<unsigned>((n + 127) / 128);
+  // brute 0: the SAH tree; 2 / 3: diagnostics on the reference median tree
+  // (fp32 leaf classification, 4-wide nodes)
+  const bool sah = brute == 0 && s->snodes.p != nullptr;
+  if (brute != 1 && !sah) ensure_reference_tree(s);
   if (brute == 1)
     brute_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->tri.p, s->nf, d_o, d_d, n, d_face, d_delta, d_point);
   else
-    nearest_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(s->hdr, s->tnodes.p, brute == 3 ? s->qnodes.p : nullptr,
+    nearest_hit_kernel<<<g, 128, 0, s->ctx->stream>>>(sah ? s->shdr : s->hdr, sah ? s->snodes.p : s->tnodes.p,
+                                                       brute == 3 ? s->qnodes.p : nullptr,
                                                        brute == 2 ? s->tri32.p : nullptr, s->tri.p, d_o, d_d, n,
                                                        d_face, d_delta, d_point);
   RR_LAUNCH_CHECK();
@@ -679,6 +684,14 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     return e ? std::atoi(e) : 1;
   }();
   const bool sah = use_sah && s->snodes.p != nullptr;
+  if (!sah || (cfg->flags & RR_TRACE_WIDE)) ensure_reference_tree(s);
+  // kernel variant (RR_DF, see below); the 4-wide SAH collapse is built on
+  // first use by the variants that traverse it
+  static const int df_env = [] {
+    const char* e = std::getenv("RR_DF");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (sah && (df_env == 23 || df_env == 24 || (df_env < 0 && s->nf >= (1 << 18)))) build_sah4(s);
   p.nodes = sah ? s->snodes.p : s->tnodes.p;
   p.qnodes = s->qnodes.p;
   // default: binary nodes, fp64 test at every leaf (fastest measured); diagnostics: fp32 leaf classification, 4-wide nodes
@@ -776,10 +789,6 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // of the loop's lanes hold a leaf or enough lanes are stuck behind theirs
   // (default 16: >= half stuck; C2 25.7 -> 21.4 ms, C3 2.16 -> 1.88 ms,
   // C5 1415 -> 1170 ms against 0)
-  static const int df_env = [] {
-    const char* e = std::getenv("RR_DF");
-    return e ? std::atoi(e) : -1;
-  }();
   // default: per-ray loop with postponed leaf tests over the binary SAH tree;
   // deep trees (>= 2^18 faces) over its 4-wide collapse, which halves the
   // dependent node fetches (C3 -15 %, C5 -8 %; C2 100k +8 %, so not there)
