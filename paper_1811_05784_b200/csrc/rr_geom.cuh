@@ -260,10 +260,13 @@ struct RegRay {  // ray held in registers
 
 // CNT: count internal-node visits and leaf tests into *cnt (instrumented build)
 // UNR: internal nodes a lane may process per vote round (amortises the votes)
-template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1>  // STUCKT < 0: >= 1/|STUCKT| of lanes
+// SMS: the bottom SMS stack entries live in shared memory (sst: this
+// thread's column, stride 128), the rest in local memory
+template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1, int SMS = 0>  // STUCKT < 0: >= 1/|STUCKT| of lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
-                                                    int32_t rplane, unsigned long long* cnt = nullptr) {
+                                                    int32_t rplane, unsigned long long* cnt = nullptr,
+                                                    int2* sst = nullptr) {
   HitResult best{0.0, -1};
   RayF r;
   if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
@@ -276,14 +279,14 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     const float t = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest);
     node = (t == kInf) ? kDone : h.root_ref;
   }
-  int2 st[kStack];
+  int2 st[kStack - SMS];
   int sp = 0;
   int32_t leaf = 0;  // stashed leaf (< 0) or 0
   auto pop = [&]() {
     node = kDone;
     while (sp > 0) {
       --sp;
-      const int2 e = st[sp];
+      const int2 e = (SMS > 0 && sp < SMS) ? sst[sp * 128] : st[sp - SMS];
       if (__int_as_float(e.y) <= tbest) {
         node = e.x;
         break;
@@ -304,7 +307,9 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       const bool hl = tl != kInf, hr = tr != kInf;
       if (hl && hr) {
         const bool lf = tl <= tr;
-        st[sp] = make_int2(lf ? dd.y : dd.x, __float_as_int(lf ? tr : tl));
+        const int2 e = make_int2(lf ? dd.y : dd.x, __float_as_int(lf ? tr : tl));
+        if (SMS > 0 && sp < SMS) sst[sp * 128] = e;
+        else st[sp - SMS] = e;
         ++sp;
         node = lf ? dd.x : dd.y;
       } else if (hl) {

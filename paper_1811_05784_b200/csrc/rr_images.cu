@@ -31,6 +31,7 @@ struct ImgOut {
   double *pos, *dist, *energy, *mult, *proj;
   int32_t *ray_count, *order, *has_proj, *path;
   int64_t* path_off;
+  int64_t* path_src;  // per image: start of its path in the capture histories
 };
 
 namespace rr {
@@ -99,18 +100,19 @@ __global__ void retro_kernel(const double* __restrict__ point, const double* __r
   idx[i] = static_cast<int32_t>(c);
 }
 
-// Path sort, stage 1: radix key of the first three faces (21 bits each,
+// Path sort, stage 1: radix key of the first faces (as many as fit in 63 bits
+// at ceil(log2(nf + 1)) bits each, at least three;
 // face + 1, 0 past the end: a proper prefix sorts first, as in
 // std::lexicographical_compare).
-__global__ void prefix_key_kernel(const int32_t* __restrict__ idx, int64_t n, PathView pv,
+__global__ void prefix_key_kernel(const int32_t* __restrict__ idx, int64_t n, PathView pv, int bits, int faces,
                                   unsigned long long* __restrict__ keys) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t c = idx[i], a0 = pv.off[c], len = pv.off[c + 1] - a0;
   unsigned long long k = 0;
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < faces; ++j) {  // face + 1 (0: path ended), lexicographic
     const unsigned long long f = j < len ? static_cast<unsigned long long>(pv.hist[a0 + j]) + 1ull : 0ull;
-    k = (k << 21) | f;
+    k = (k << bits) | f;
   }
   keys[i] = k;
 }
@@ -164,6 +166,23 @@ __global__ void group_start_kernel(const int32_t* __restrict__ head, const int32
 __device__ __forceinline__ D3 ld3(const double* p, int64_t i) { return d3(p[3 * i], p[3 * i + 1], p[3 * i + 2]); }
 __device__ __forceinline__ double norm3(D3 a) { return sqrt(dot(a, a)); }
 
+// In-order fp64 sum of the points p[s, e): the loads of 8 iterations are
+// issued together, the additions keep the reference's order (same bits as a
+// plain loop, without one memory latency per element on long groups).
+__device__ __forceinline__ D3 sum_points(const double* __restrict__ p, int64_t s, int64_t e) {
+  D3 acc = d3(0, 0, 0);
+  int64_t i = s;
+  for (; i + 8 <= e; i += 8) {
+    D3 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ld3(p, i + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = acc + v[u];
+  }
+  for (; i < e; ++i) acc = acc + ld3(p, i);
+  return acc;
+}
+
 __device__ __forceinline__ bool pt_less(const double* retro, int64_t c0, int32_t a, int32_t b) {
   const D3 x = ld3(retro, a - c0), y = ld3(retro, b - c0);
   if (x.x != y.x) return x.x < y.x;
@@ -210,20 +229,118 @@ __global__ void gather_retro_kernel(const int32_t* __restrict__ idx, int64_t n, 
   for (int k = 0; k < 3; ++k) rs[3 * i + k] = retro[3 * j + k];
 }
 
+constexpr int64_t kBigGroup = 256;  // groups this large go to group_big_kernel (one block each)
+
+// split groups: sort by retro point and count the beams (split_group)
+__device__ void split_count(int32_t* idx, int64_t s, int64_t e, const double* retro, int64_t c0, double tol,
+                            int32_t* n_img_g) {
+  const int64_t m = e - s;
+  heap_sort(idx + s, m, retro, c0);
+  int32_t cnt = 1;
+  D3 anchor = ld3(retro, idx[s] - c0);
+  for (int64_t i = s + 1; i < e; ++i) {
+    const D3 p = ld3(retro, idx[i] - c0);
+    if (norm3(p - anchor) > tol) {
+      ++cnt;
+      anchor = p;
+    }
+  }
+  *n_img_g = cnt;
+}
+
+// Large groups, one block each (taken from a device list): the block stages
+// chunks of retro points in shared memory, thread 0 sums them in capture
+// order (the reference's bits), the spread is a block max.
+__global__ void __launch_bounds__(256) group_big_kernel(int32_t* __restrict__ idx, const int64_t* __restrict__ gstart,
+                                                        int64_t ng, int64_t n, const double* __restrict__ retro,
+                                                        const double* __restrict__ rs, int64_t c0, double tol,
+                                                        const int32_t* __restrict__ big, const int32_t* __restrict__ n_big,
+                                                        int32_t* __restrict__ n_img, int32_t* __restrict__ is_split,
+                                                        double* __restrict__ gmean) {
+  constexpr int kChunk = 1024;
+  __shared__ double sp[3 * kChunk];
+  __shared__ double red[256];
+  __shared__ double smean[3];
+  const int nb = *n_big;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t g = big[b];
+    const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n, m = e - s;
+    D3 acc = d3(0, 0, 0);
+    for (int64_t c = s; c < e; c += kChunk) {
+      const int64_t len = min(static_cast<int64_t>(kChunk), e - c);
+      __syncthreads();
+      for (int64_t k = threadIdx.x; k < 3 * len; k += blockDim.x) sp[k] = rs[3 * c + k];
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int64_t k = 0; k < len; ++k) acc = acc + d3(sp[3 * k], sp[3 * k + 1], sp[3 * k + 2]);
+    }
+    if (threadIdx.x == 0) {
+      smean[0] = acc.x / static_cast<double>(m);
+      smean[1] = acc.y / static_cast<double>(m);
+      smean[2] = acc.z / static_cast<double>(m);
+    }
+    __syncthreads();
+    const D3 mean = d3(smean[0], smean[1], smean[2]);
+    double spread2 = 0.0;
+    for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+      const D3 v = ld3(rs, i) - mean;
+      const double q = dot(v, v);
+      spread2 = (spread2 < q) ? q : spread2;
+    }
+    red[threadIdx.x] = spread2;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double spread = sqrt(red[0]);
+      if (spread <= tol) {
+        n_img[g] = 1;
+        is_split[g] = 0;
+        gmean[3 * g] = mean.x;
+        gmean[3 * g + 1] = mean.y;
+        gmean[3 * g + 2] = mean.z;
+      } else {
+        is_split[g] = 1;
+        split_count(idx, s, e, retro, c0, tol, n_img + g);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void group_count_kernel(int32_t* __restrict__ idx, const int64_t* __restrict__ gstart, int64_t ng,
                                    int64_t n, const double* __restrict__ retro, const double* __restrict__ rs,
                                    int64_t c0, double tol, int32_t* __restrict__ n_img,
-                                   int32_t* __restrict__ is_split, double* __restrict__ gmean) {
+                                   int32_t* __restrict__ is_split, double* __restrict__ gmean,
+                                   int32_t* __restrict__ big, int32_t* __restrict__ n_big) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t s = gstart[g], e = g + 1 < ng ? gstart[g + 1] : n, m = e - s;
-  D3 mean = d3(0, 0, 0);
-  for (int64_t i = s; i < e; ++i) mean = mean + ld3(rs, i);  // capture order, as the reference
+  if (m >= kBigGroup) {
+    big[atomicAdd(n_big, 1)] = static_cast<int32_t>(g);
+    return;
+  }
+  D3 mean = sum_points(rs, s, e);  // capture order, as the reference
   mean = d3(mean.x / static_cast<double>(m), mean.y / static_cast<double>(m), mean.z / static_cast<double>(m));
   // max of the norms = sqrt of the max squared norm (sqrt is monotone and
-  // correctly rounded): one square root per group, the same bits
+  // correctly rounded): one square root per group, the same bits; the max
+  // is order-free, so 8 loads go out together
   double spread2 = 0.0;
-  for (int64_t i = s; i < e; ++i) {
+  int64_t i = s;
+  for (; i + 8 <= e; i += 8) {
+    D3 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ld3(rs, i + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const D3 w = v[u] - mean;
+      const double q = dot(w, w);
+      spread2 = (spread2 < q) ? q : spread2;
+    }
+  }
+  for (; i < e; ++i) {
     const D3 v = ld3(rs, i) - mean;
     const double q = dot(v, v);
     spread2 = (spread2 < q) ? q : spread2;
@@ -238,17 +355,7 @@ __global__ void group_count_kernel(int32_t* __restrict__ idx, const int64_t* __r
     return;
   }
   is_split[g] = 1;
-  heap_sort(idx + s, m, retro, c0);
-  int32_t cnt = 1;
-  D3 anchor = ld3(retro, idx[s] - c0);
-  for (int64_t i = s + 1; i < e; ++i) {
-    const D3 p = ld3(retro, idx[i] - c0);
-    if (norm3(p - anchor) > tol) {
-      ++cnt;
-      anchor = p;
-    }
-  }
-  n_img[g] = cnt;
+  split_count(idx, s, e, retro, c0, tol, n_img + g);
 }
 
 struct ImgTmp {
@@ -262,7 +369,15 @@ struct ImgTmp {
 __device__ void emit_image(const int32_t* idx, int64_t b0, int64_t b1, const double* retro, int64_t c0,
                            const int64_t* off, ImgTmp t, int64_t slot) {
   D3 sum = d3(0, 0, 0);
-  for (int64_t i = b0; i < b1; ++i) sum = sum + ld3(retro, idx[i] - c0);
+  int64_t i = b0;
+  for (; i + 4 <= b1; i += 4) {
+    D3 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ld3(retro, idx[i + u] - c0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sum = sum + v[u];
+  }
+  for (; i < b1; ++i) sum = sum + ld3(retro, idx[i] - c0);
   const double m = static_cast<double>(b1 - b0);
   t.pos[3 * slot] = sum.x / m;
   t.pos[3 * slot + 1] = sum.y / m;
@@ -316,7 +431,9 @@ __device__ __forceinline__ unsigned long long cell_key(int32_t order, const long
     h *= 0xBF58476D1CE4E5B9ull;
     h ^= h >> 31;
   }
-  return h == ~0ull ? ~1ull : h;  // ~0 marks an empty hash slot
+  // 32 bits: runs of equal keys may merge two cells (harmless, see
+  // resolve_round_kernel) and the cell sort needs 4 radix passes
+  return h & 0xffffffffull;  // never ~0, which marks an empty hash slot
 }
 
 // Open-addressing table: sorted cell key -> first index of its run.
@@ -394,8 +511,10 @@ __global__ void owner_init_kernel(int32_t* __restrict__ owner, int64_t n) {
 // within 1e-12); it is an anchor when no pred is.  i is decided once every
 // pred below that anchor is decided.  Decisions only move from undecided to
 // final, so reading a neighbour's value while it is being written is safe.
-// Candidate cells: per axis those met by [p - tol, p + tol] (cell size
-// 2 tol, widened by 1 % against rounding of the cell index).
+// Candidate cells: per axis those met by [p - tol, p + tol] (widened by 1 %
+// against rounding of the cell index); cells of 16 tol, so a window mostly
+// meets a single cell (one hash probe) while the images of different
+// beams stay far apart.
 __global__ void resolve_round_kernel(ImgTmp t, const double* __restrict__ mult, int64_t n, double cs, double tol,
                                      const unsigned long long* __restrict__ skeys, Cand cand,
                                      const unsigned long long* __restrict__ tkey, const int32_t* __restrict__ tstart,
@@ -429,10 +548,9 @@ __global__ void resolve_round_kernel(ImgTmp t, const double* __restrict__ mult, 
           // smallest undecided pred seen, no later entry can change the outcome
           if (j >= i || j >= best_anchor || j >= min_undet) break;
           if (cand.order[q] != oi) continue;
+          // (a hash collision only adds entries of another cell, still in
+          // ascending id order; any that meet cond(j, i) are true preds)
           const D3 pj = ld3(cand.pos, q);
-          if (static_cast<long long>(floor(pj.x / cs)) != cx || static_cast<long long>(floor(pj.y / cs)) != cy ||
-              static_cast<long long>(floor(pj.z / cs)) != cz)
-            continue;  // hash collision
           // cond(j, i), j the anchor candidate (image_sources.cpp:111-116)
           if (norm3(pi - pj) > tol) continue;
           const double* mj = cand.mult + kBands * q;
@@ -452,49 +570,31 @@ __global__ void resolve_round_kernel(ImgTmp t, const double* __restrict__ mult, 
   progress[0] = 1;
 }
 
-// claims sorted by (owner, index): key owner << 32 | index, anchors ~0
-__global__ void claim_key_kernel(const int32_t* __restrict__ owner, int64_t n, unsigned long long* __restrict__ keys) {
+// claims sorted by (owner, index): key owner << cb | index (cb bits hold any
+// image index), anchors ~0
+__global__ void claim_key_kernel(const int32_t* __restrict__ owner, int64_t n, int cb,
+                                 unsigned long long* __restrict__ keys) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t o = owner[i];
-  keys[i] = o >= 0 ? (static_cast<unsigned long long>(static_cast<uint32_t>(o)) << 32) | static_cast<uint32_t>(i)
+  keys[i] = o >= 0 ? (static_cast<unsigned long long>(static_cast<uint32_t>(o)) << cb) | static_cast<uint32_t>(i)
                    : ~0ull;
 }
 
-__global__ void claim_start_kernel(const unsigned long long* __restrict__ skeys, int64_t n,
-                                   int32_t* __restrict__ claim_start) {
+__global__ void claim_start_kernel(const unsigned long long* __restrict__ skeys, int64_t n, int cb,
+                                   int32_t* __restrict__ claim_start, int32_t* __restrict__ claim_end) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= n || skeys[q] == ~0ull) return;
-  const uint32_t a = static_cast<uint32_t>(skeys[q] >> 32);
-  if (q == 0 || static_cast<uint32_t>(skeys[q - 1] >> 32) != a) claim_start[a] = static_cast<int32_t>(q);
+  const uint32_t a = static_cast<uint32_t>(skeys[q] >> cb);
+  if (q == 0 || static_cast<uint32_t>(skeys[q - 1] >> cb) != a) claim_start[a] = static_cast<int32_t>(q);
+  if (q + 1 == n || skeys[q + 1] == ~0ull || static_cast<uint32_t>(skeys[q + 1] >> cb) != a)
+    claim_end[a] = static_cast<int32_t>(q + 1);
 }
 
-// merged image per anchor: weighted mean over the anchor and its claims in
-// index order, lexicographically smallest path (image_sources.cpp:103-128)
-__global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict__ owner,
-                                  const unsigned long long* __restrict__ claims,
-                                  const int32_t* __restrict__ claim_start, const int32_t* __restrict__ anchor_rank,
-                                  PathView pv, ImgTmp out, int64_t n_out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || owner[i] != kAnchor) return;
-  int32_t cnt = t.count[i];
-  D3 w = d3(t.pos[3 * i] * static_cast<double>(cnt), t.pos[3 * i + 1] * static_cast<double>(cnt),
-            t.pos[3 * i + 2] * static_cast<double>(cnt));
-  int32_t rep = t.rep[i];
-  const int32_t q0 = claim_start[i];
-  if (q0 >= 0) {
-    // the reference keeps the lexicographically smallest face path
-    // (image_sources.cpp:121-123); images are indexed in path order and every
-    // claim j > i, so that is always the anchor's own path
-    for (int64_t q = q0; q < n && claims[q] != ~0ull &&
-                         static_cast<uint32_t>(claims[q] >> 32) == static_cast<uint32_t>(i);
-         ++q) {
-      const int32_t j = static_cast<int32_t>(claims[q] & 0xffffffffu);
-      const double cj = static_cast<double>(t.count[j]);
-      w = w + d3(t.pos[3 * j] * cj, t.pos[3 * j + 1] * cj, t.pos[3 * j + 2] * cj);
-      cnt += t.count[j];
-    }
-  }
+constexpr int64_t kBigClaims = 256;  // anchors with this many claims go to merge_big_kernel
+
+__device__ __forceinline__ void merge_write(ImgTmp t, int64_t i, D3 w, int32_t cnt, const int32_t* anchor_rank,
+                                            ImgTmp out, int64_t n_out) {
   const int64_t s = anchor_rank[i];
   const double m = static_cast<double>(cnt);
   out.pos[3 * s] = w.x / m;
@@ -502,8 +602,97 @@ __global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict
   out.pos[3 * s + 2] = w.z / m;
   out.count[s] = cnt;
   out.order[s] = t.order[i];
-  out.rep[s] = rep;               // path source (lexicographic minimum)
+  // the reference keeps the lexicographically smallest face path
+  // (image_sources.cpp:121-123); images are indexed in path order and every
+  // claim j > i, so that is always the anchor's own path
+  out.rep[s] = t.rep[i];          // path source (lexicographic minimum)
   out.rep[n_out + s] = t.rep[i];  // multiplier source (the anchor's, :113)
+}
+
+__device__ __forceinline__ D3 weighted(ImgTmp t, int64_t i) {
+  const double c = static_cast<double>(t.count[i]);
+  return d3(t.pos[3 * i] * c, t.pos[3 * i + 1] * c, t.pos[3 * i + 2] * c);
+}
+
+// merged image per anchor: weighted mean over the anchor and its claims in
+// index order (image_sources.cpp:103-128)
+__global__ void merge_emit_kernel(ImgTmp t, int64_t n, const int32_t* __restrict__ owner,
+                                  const unsigned long long* __restrict__ claims,
+                                  const int32_t* __restrict__ claim_start, const int32_t* __restrict__ claim_end,
+                                  const int32_t* __restrict__ anchor_rank, ImgTmp out, int64_t n_out,
+                                  unsigned long long cmask, int32_t* __restrict__ big, int32_t* __restrict__ n_big) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || owner[i] != kAnchor) return;
+  const int64_t q0 = claim_start[i], q1 = q0 >= 0 ? claim_end[i] : q0;
+  if (q1 - q0 >= kBigClaims) {
+    big[atomicAdd(n_big, 1)] = static_cast<int32_t>(i);
+    return;
+  }
+  int32_t cnt = t.count[i];
+  D3 w = weighted(t, i);
+  int64_t q = q0;
+  for (; q + 4 <= q1; q += 4) {  // gather 4 claims, then add them in index order
+    D3 pj[4];
+    int32_t cj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int32_t j = static_cast<int32_t>(claims[q + u] & cmask);
+      pj[u] = weighted(t, j);
+      cj[u] = t.count[j];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      w = w + pj[u];
+      cnt += cj[u];
+    }
+  }
+  for (; q < q1; ++q) {
+    const int32_t j = static_cast<int32_t>(claims[q] & cmask);
+    w = w + weighted(t, j);
+    cnt += t.count[j];
+  }
+  merge_write(t, i, w, cnt, anchor_rank, out, n_out);
+}
+
+// anchors with many claims, one block each: the claims' weighted positions
+// are staged in shared memory in parallel, thread 0 adds them in order
+__global__ void __launch_bounds__(256) merge_big_kernel(ImgTmp t, const unsigned long long* __restrict__ claims,
+                                                        const int32_t* __restrict__ claim_start,
+                                                        const int32_t* __restrict__ claim_end,
+                                                        const int32_t* __restrict__ anchor_rank, ImgTmp out,
+                                                        int64_t n_out, unsigned long long cmask,
+                                                        const int32_t* __restrict__ big,
+                                                        const int32_t* __restrict__ n_big) {
+  constexpr int kChunk = 1024;
+  __shared__ double sw[3 * kChunk];
+  __shared__ int32_t sc[kChunk];
+  const int nb = *n_big;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t i = big[b];
+    const int64_t q0 = claim_start[i], q1 = claim_end[i];
+    int32_t cnt = t.count[i];
+    D3 w = weighted(t, i);
+    for (int64_t c = q0; c < q1; c += kChunk) {
+      const int64_t len = min(static_cast<int64_t>(kChunk), q1 - c);
+      __syncthreads();
+      for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
+        const int32_t j = static_cast<int32_t>(claims[c + k] & cmask);
+        const D3 v = weighted(t, j);
+        sw[3 * k] = v.x;
+        sw[3 * k + 1] = v.y;
+        sw[3 * k + 2] = v.z;
+        sc[k] = t.count[j];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int64_t k = 0; k < len; ++k) {
+          w = w + d3(sw[3 * k], sw[3 * k + 1], sw[3 * k + 2]);
+          cnt += sc[k];
+        }
+    }
+    if (threadIdx.x == 0) merge_write(t, i, w, cnt, anchor_rank, out, n_out);
+    __syncthreads();
+  }
 }
 
 __global__ void flag_anchor_kernel(const int32_t* __restrict__ owner, int64_t n, int32_t* __restrict__ f) {
@@ -618,9 +807,19 @@ __global__ void final_gather_kernel(const int32_t* __restrict__ perm, int64_t n,
   im.has_proj[i] = has_proj[s];
   const int32_t r = t.rep[s];
   const int64_t a0 = pv.off[r], len = pv.off[r + 1] - a0, o = out_off[i];
-  for (int64_t k = 0; k < len; ++k) im.path[o + k] = pv.hist[a0 + k];
+  im.path_src[i] = a0;  // path elements are copied by final_path_kernel
   im.path_off[i] = o;
   if (i == n - 1) im.path_off[n] = o + len;
+}
+
+// one warp per image copies its face path (coalesced)
+__global__ void final_path_kernel(const int64_t* __restrict__ path_off, const int64_t* __restrict__ path_src,
+                                  int64_t n, const int32_t* __restrict__ hist, int32_t* __restrict__ path) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t o = path_off[i], len = path_off[i + 1] - o, a0 = path_src[i];
+  for (int64_t k = lane; k < len; k += 32) path[o + k] = hist[a0 + k];
 }
 
 inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>((n + b - 1) / b); }
@@ -706,10 +905,13 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     pk.alloc(n, st);
     pk_s.alloc(n, st);
     idx_s.alloc(n, st);
-    prefix_key_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, pv, pk.p);
+    int bits = 1;
+    while ((int64_t(1) << bits) <= s->nf) ++bits;  // face + 1 <= nf
+    const int faces = std::max(1, 63 / bits);
+    prefix_key_kernel<<<grid(n), 256, 0, st>>>(idx.p, n, pv, bits, faces, pk.p);
     RR_LAUNCH_CHECK();
     cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, pk.p, pk_s.p, idx.p, idx_s.p, n, 0, 63, st);
+      return cub::DeviceRadixSort::SortPairs(t, b, pk.p, pk_s.p, idx.p, idx_s.p, n, 0, bits * faces, st);
     }, st);
     DevBuf<int32_t> dirty;
     dirty.alloc(n, st);
@@ -753,9 +955,19 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   tm.mark("groups: heads");
   DevBuf<double> gmean;
   gmean.alloc(3 * ng, st);
-  group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, n_img.p,
-                                                    is_split.p, gmean.p);
-  RR_LAUNCH_CHECK();
+  {
+    DevBuf<int32_t> big, n_big;
+    big.alloc(std::max<int64_t>(n / kBigGroup + 1, 1), st);
+    n_big.alloc(1, st);
+    RR_CUDA(cudaMemsetAsync(n_big.p, 0, sizeof(int32_t), st));
+    group_count_kernel<<<grid(ng, 128), 128, 0, st>>>(idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, n_img.p,
+                                                      is_split.p, gmean.p, big.p, n_big.p);
+    RR_LAUNCH_CHECK();
+    group_big_kernel<<<static_cast<unsigned>(std::min<int64_t>(n / kBigGroup + 1, 2 * ctx->sm_count)), 256, 0, st>>>(
+        idx.p, gstart.p, ng, n, retro.p, rs.p, c0, tol, big.p, n_big.p, n_img.p, is_split.p, gmean.p);
+    RR_LAUNCH_CHECK();
+    ctx->launches += 1;
+  }
   tm.mark("groups: count");
   if (tm.on) {  // group statistics (development)
     std::vector<int64_t> gs(ng + 1);
@@ -801,7 +1013,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   ImgTmp M = T;
   const int32_t* mult_src = trep.p;
   if (opt.merge_coplanar && ni > 1) {
-    const double cs = 2.0 * tol;
+    const double cs = 16.0 * tol;
     DevBuf<unsigned long long> keys, skeys;
     DevBuf<int32_t> ids, sids;
     keys.alloc(ni, st);
@@ -811,7 +1023,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     cell_key_kernel<<<grid(ni), 256, 0, st>>>(T, ni, cs, keys.p, ids.p);
     RR_LAUNCH_CHECK();
     cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, keys.p, skeys.p, ids.p, sids.p, ni, 0, 64, st);
+      return cub::DeviceRadixSort::SortPairs(t, b, keys.p, skeys.p, ids.p, sids.p, ni, 0, 32, st);
     }, st);
     unsigned long long tsize = 1024;
     while (tsize < 2ull * static_cast<unsigned long long>(ni)) tsize <<= 1;
@@ -851,17 +1063,21 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     }
     tm.mark("merge: resolve");
     DevBuf<unsigned long long> ckeys, cskeys;
-    DevBuf<int32_t> claim_start;
+    DevBuf<int32_t> claim_start, claim_end;
     ckeys.alloc(ni, st);
     cskeys.alloc(ni, st);
     claim_start.alloc(ni, st);
-    claim_key_kernel<<<grid(ni), 256, 0, st>>>(owner.p, ni, ckeys.p);
+    claim_end.alloc(ni, st);
+    int cb = 1;
+    while ((int64_t(1) << cb) < ni) ++cb;  // bits of an image index
+    const unsigned long long cmask = (1ull << cb) - 1ull;
+    claim_key_kernel<<<grid(ni), 256, 0, st>>>(owner.p, ni, cb, ckeys.p);
     RR_LAUNCH_CHECK();
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, ckeys.p, cskeys.p, ni, 0, 64, st);
+    cub_call([&](void* t, size_t& b) {  // anchors' ~0 keys stay last: all-ones in the sorted bits
+      return cub::DeviceRadixSort::SortKeys(t, b, ckeys.p, cskeys.p, ni, 0, 2 * cb, st);
     }, st);
     RR_CUDA(cudaMemsetAsync(claim_start.p, 0xff, claim_start.bytes(), st));
-    claim_start_kernel<<<grid(ni), 256, 0, st>>>(cskeys.p, ni, claim_start.p);
+    claim_start_kernel<<<grid(ni), 256, 0, st>>>(cskeys.p, ni, cb, claim_start.p, claim_end.p);
     RR_LAUNCH_CHECK();
     tm.mark("merge: claims");
     DevBuf<int32_t> aflag, arank;
@@ -881,7 +1097,15 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     mrep.alloc(2 * static_cast<int64_t>(na), st);
     M = ImgTmp{mpos.p, mcount.p, morder.p, mrep.p};
     // path reps at [0, na), multiplier reps at [na, 2na)
-    merge_emit_kernel<<<grid(ni), 256, 0, st>>>(T, ni, owner.p, cskeys.p, claim_start.p, arank.p, pv, M, na);
+    DevBuf<int32_t> mbig, n_mbig;
+    mbig.alloc(ni / kBigClaims + 1, st);
+    n_mbig.alloc(1, st);
+    RR_CUDA(cudaMemsetAsync(n_mbig.p, 0, sizeof(int32_t), st));
+    merge_emit_kernel<<<grid(ni), 256, 0, st>>>(T, ni, owner.p, cskeys.p, claim_start.p, claim_end.p, arank.p, M, na,
+                                                cmask, mbig.p, n_mbig.p);
+    RR_LAUNCH_CHECK();
+    merge_big_kernel<<<static_cast<unsigned>(std::min<int64_t>(ni / kBigClaims + 1, 2 * ctx->sm_count)), 256, 0,
+                       st>>>(T, cskeys.p, claim_start.p, claim_end.p, arank.p, M, na, cmask, mbig.p, n_mbig.p);
     RR_LAUNCH_CHECK();
     ctx->launches += 3;
     ni = na;
@@ -963,13 +1187,19 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
   im->order.alloc(ni, st);
   im->has_proj.alloc(ni, st);
   im->path.alloc(std::max<int64_t>(tpath, 1), st);
+  DevBuf<int64_t> psrc;
+  psrc.alloc(std::max<int64_t>(ni, 1), st);
   final_gather_kernel<<<grid(ni), 256, 0, st>>>(perm.p, ni, M, dist.p, energy.p, mult.p, has_proj.p, proj.p, pv,
                                                 im->path_off.p,
                                                 ImgOut{im->pos.p, im->dist.p, im->energy.p, im->mult.p, im->proj.p,
                                                        im->ray_count.p, im->order.p, im->has_proj.p, im->path.p,
-                                                       im->path_off.p});
+                                                       im->path_off.p, psrc.p});
   RR_LAUNCH_CHECK();
-  ctx->launches += 6;
+  if (tpath > 0) {
+    final_path_kernel<<<grid(32 * ni), 256, 0, st>>>(im->path_off.p, psrc.p, ni, pv.hist, im->path.p);
+    RR_LAUNCH_CHECK();
+  }
+  ctx->launches += 7;
   tm.mark("gather");
   RR_CUDA(cudaStreamSynchronize(st));
   return im.release();

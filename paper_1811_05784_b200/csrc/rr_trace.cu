@@ -48,9 +48,10 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1>
+template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1, int SMS = 0>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
+  __shared__ int2 s_stack[SMS > 0 ? SMS * 128 : 1];  // bottom of the traversal stacks (SMS > 0)
   extern __shared__ TNode smem_nodes[];
   QNode* smem_q = reinterpret_cast<QNode*>(smem_nodes);
   const int32_t K = (p.use_smem && V != 0) ? (WIDE ? p.hdr.K4 : p.hdr.K) : 0;
@@ -118,7 +119,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     } else if (V == 3) {
       wall = closest_hit4_pl<16, -2, RegRay>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt);
+      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt,
+                                                            s_stack + threadIdx.x);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
@@ -807,6 +809,9 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 15) dfk = trace_kernel<1, 8, false, 16, -4>;  // >= 1/4 of the loop's lanes stuck
   if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
   if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
+  if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
+  if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
+  if (df == 32) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 16>;
   if (df == 23 && s->s4nodes.p) dfk = trace_kernel<3, 8>;
   if (df == 24 && s->s4nodes.p) dfk = trace_kernel<3, 6>;
   if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true>;
