@@ -102,7 +102,7 @@ __global__ void prep_kernel(const double* __restrict__ v, const int32_t* __restr
     fb[6 * f + k] = fmin(va, fmin(vb, vc));
     fb[6 * f + 3 + k] = fmax(va, fmax(vb, vc));
     cen[3 * f + k] = ce;
-    keys[k * nf + f] = okey(ce);
+    keys[k * nf + f] = okeyf(__double2float_rn(ce));  // 32-bit sort key: order only shapes the tree
     ids[k * nf + f] = static_cast<int32_t>(f);
   }
 }
@@ -263,7 +263,35 @@ __global__ void root_hdr_kernel(const unsigned long long* __restrict__ bb, TravH
   }
 }
 
-// 3. node emission and split choice
+// 3. node emission and split choice: one warp per segment.  For SAH
+// segments lane b holds bin b; prefix and suffix unions/counts come from warp
+// scans, every lane prices the split below its bin, and the warp takes the
+// cheapest (ties: lowest axis, then highest bin, as a sequential scan from
+// the top bin down with a strict < would).  Lane 0 writes the node.
+struct BinAcc {
+  float lo[3], hi[3];
+  int32_t c;
+};
+
+__device__ __forceinline__ BinAcc bin_union(BinAcc a, const BinAcc& b) {
+  for (int k = 0; k < 3; ++k) {
+    a.lo[k] = fminf(a.lo[k], b.lo[k]);
+    a.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+  }
+  a.c += b.c;
+  return a;
+}
+
+__device__ __forceinline__ BinAcc shfl_acc(const BinAcc& a, int src_delta, bool up) {
+  BinAcc r;
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = up ? __shfl_up_sync(0xffffffffu, a.lo[k], src_delta) : __shfl_down_sync(0xffffffffu, a.lo[k], src_delta);
+    r.hi[k] = up ? __shfl_up_sync(0xffffffffu, a.hi[k], src_delta) : __shfl_down_sync(0xffffffffu, a.hi[k], src_delta);
+  }
+  r.c = up ? __shfl_up_sync(0xffffffffu, a.c, src_delta) : __shfl_down_sync(0xffffffffu, a.c, src_delta);
+  return r;
+}
+
 __global__ void split_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls,
                              const int32_t* __restrict__ rank,
                              const unsigned long long* __restrict__ bb, const unsigned long long* __restrict__ cb,
@@ -272,89 +300,102 @@ __global__ void split_kernel(const SSeg* __restrict__ segs, const LevelState* __
                              const int32_t* __restrict__ perm0, TNode* __restrict__ tn,
                              TravHeader* __restrict__ hdr, int32_t* __restrict__ seg_axis,
                              int32_t* __restrict__ seg_split, int64_t* __restrict__ seg_nl, SSeg* __restrict__ next) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= ls->S) return;
-  const int32_t level_base = ls->level_base;
-  const float eps = hdr->eps;
+  static_assert(kBins == 32, "one lane per bin");
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= ls->S) return;  // warp-uniform
   const SSeg sg = segs[j];
   if (sg.n >= 2 && sg.n <= kSmall) {  // finish_kernel's
-    seg_axis[j] = -1;
+    if (lane == 0) seg_axis[j] = -1;
     return;
   }
-  double lo[3], hi[3];
-  for (int k = 0; k < 3; ++k) {
-    lo[k] = oval(bb[6 * j + k]);
-    hi[k] = oval(bb[6 * j + 3 + k]);
-  }
-  const int32_t my_ref = sg.n == 1 ? ~perm0[sg.b] : level_base + rank[j];
-  const int32_t plane = (pl[2 * j] == pl[2 * j + 1]) ? pl[2 * j] : -1;
-  if (sg.parent < 0) {
-    hdr->root_ref = my_ref;
-  } else {
-    TNode* p = tn + sg.parent;
-    const float lx = lo_f(lo[0], eps), ly = lo_f(lo[1], eps), lz = lo_f(lo[2], eps);
-    const float hx = hi_f(hi[0], eps), hy = hi_f(hi[1], eps), hz = hi_f(hi[2], eps);
-    if (sg.side == 0) {
-      p->a = make_float4(lx, hx, ly, hy);
-      reinterpret_cast<float2*>(&p->b)[0] = make_float2(lz, hz);
-      p->d.x = my_ref;
-      p->d.z = plane;
-    } else {
-      reinterpret_cast<float2*>(&p->b)[1] = make_float2(lx, hx);
-      p->c = make_float4(ly, hy, lz, hz);
-      p->d.y = my_ref;
-      p->d.w = plane;
+  const int32_t level_base = ls->level_base;
+  const float eps = hdr->eps;
+  if (lane == 0) {
+    double lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = oval(bb[6 * j + k]);
+      hi[k] = oval(bb[6 * j + 3 + k]);
     }
+    const int32_t my_ref = sg.n == 1 ? ~perm0[sg.b] : level_base + rank[j];
+    const int32_t plane = (pl[2 * j] == pl[2 * j + 1]) ? pl[2 * j] : -1;
+    if (sg.parent < 0) {
+      hdr->root_ref = my_ref;
+    } else {
+      TNode* p = tn + sg.parent;
+      const float lx = lo_f(lo[0], eps), ly = lo_f(lo[1], eps), lz = lo_f(lo[2], eps);
+      const float hx = hi_f(hi[0], eps), hy = hi_f(hi[1], eps), hz = hi_f(hi[2], eps);
+      if (sg.side == 0) {
+        p->a = make_float4(lx, hx, ly, hy);
+        reinterpret_cast<float2*>(&p->b)[0] = make_float2(lz, hz);
+        p->d.x = my_ref;
+        p->d.z = plane;
+      } else {
+        reinterpret_cast<float2*>(&p->b)[1] = make_float2(lx, hx);
+        p->c = make_float4(ly, hy, lz, hz);
+        p->d.y = my_ref;
+        p->d.w = plane;
+      }
+    }
+    if (sg.n == 1) seg_axis[j] = -1;
   }
-  if (sg.n == 1) {
-    seg_axis[j] = -1;
-    return;
-  }
+  if (sg.n == 1) return;
   int axis = -1, split = -1;
   int64_t nl = sg.n / 2;
   const int32_t q = sah_idx[j];
   if (q >= 0) {
     float best = 3.4e38f;
+    int best_axis = -1, best_split = -1;
+    int64_t best_nl = 0;
     for (int a = 0; a < 3; ++a) {
-      const int32_t* cnt = bcnt + (static_cast<int64_t>(q) * 3 + a) * kBins;
-      const uint32_t* box = bbox + 6 * (static_cast<int64_t>(q) * 3 + a) * kBins;
-      float la[kBins];
-      int64_t lc[kBins];
-      float alo[3] = {3.4e38f, 3.4e38f, 3.4e38f}, ahi[3] = {-3.4e38f, -3.4e38f, -3.4e38f};
-      int64_t c = 0;
-      for (int b = 0; b < kBins; ++b) {
-        if (cnt[b] > 0)
-          for (int k = 0; k < 3; ++k) {
-            alo[k] = fminf(alo[k], ovalf(box[6 * b + k]));
-            ahi[k] = fmaxf(ahi[k], ovalf(box[6 * b + 3 + k]));
-          }
-        c += cnt[b];
-        lc[b] = c;
-        la[b] = c > 0 ? half_area(alo, ahi) : 0.0f;
-      }
+      const int64_t slot = (static_cast<int64_t>(q) * 3 + a) * kBins + lane;
+      BinAcc mine;
+      mine.c = bcnt[slot];
       for (int k = 0; k < 3; ++k) {
-        alo[k] = 3.4e38f;
-        ahi[k] = -3.4e38f;
+        mine.lo[k] = mine.c > 0 ? ovalf(bbox[6 * slot + k]) : 3.4e38f;
+        mine.hi[k] = mine.c > 0 ? ovalf(bbox[6 * slot + 3 + k]) : -3.4e38f;
       }
-      c = 0;
-      for (int b = kBins - 1; b >= 1; --b) {
-        if (cnt[b] > 0)
-          for (int k = 0; k < 3; ++k) {
-            alo[k] = fminf(alo[k], ovalf(box[6 * b + k]));
-            ahi[k] = fmaxf(ahi[k], ovalf(box[6 * b + 3 + k]));
-          }
-        c += cnt[b];
-        if (c == 0 || lc[b - 1] == 0) continue;
-        const float cost = la[b - 1] * static_cast<float>(lc[b - 1]) + half_area(alo, ahi) * static_cast<float>(c);
-        if (cost < best) {
-          best = cost;
-          axis = a;
-          split = b;
-          nl = lc[b - 1];
+      BinAcc pre = mine, suf = mine;  // inclusive prefix (bins <= lane), suffix (bins >= lane)
+      for (int d = 1; d < 32; d <<= 1) {
+        const BinAcc up = shfl_acc(pre, d, true);
+        if (lane >= d) pre = bin_union(pre, up);
+        const BinAcc dn = shfl_acc(suf, d, false);
+        if (lane + d < 32) suf = bin_union(suf, dn);
+      }
+      // split below bin `lane` (lane >= 1): left = bins < lane, right = bins >= lane
+      const BinAcc left = shfl_acc(pre, 1, true);
+      float cost = 3.4e38f;
+      bool ok = lane >= 1 && suf.c > 0 && left.c > 0;
+      if (ok) {
+        const float la = half_area(left.lo, left.hi), ra = half_area(suf.lo, suf.hi);
+        cost = la * static_cast<float>(left.c) + ra * static_cast<float>(suf.c);
+      }
+      // warp argmin of (cost, -lane)
+      float c_best = ok ? cost : 3.4e38f;
+      int b_best = ok ? lane : -1;
+      for (int d = 16; d > 0; d >>= 1) {
+        const float oc = __shfl_xor_sync(0xffffffffu, c_best, d);
+        const int ob = __shfl_xor_sync(0xffffffffu, b_best, d);
+        if (ob >= 0 && (b_best < 0 || oc < c_best || (oc == c_best && ob > b_best))) {
+          c_best = oc;
+          b_best = ob;
         }
       }
+      const int32_t left_count = __shfl_sync(0xffffffffu, left.c, b_best < 0 ? 0 : b_best);
+      if (b_best >= 0 && c_best < best) {
+        best = c_best;
+        best_axis = a;
+        best_split = b_best;
+        best_nl = left_count;
+      }
+    }
+    if (best_axis >= 0) {
+      axis = best_axis;
+      split = best_split;
+      nl = best_nl;
     }
   }
+  if (lane != 0) return;
   if (axis < 0) {  // object median on the longest centroid extent
     double bestx = -1.0;
     for (int k = 0; k < 3; ++k) {
@@ -713,7 +754,7 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   for (int k = 0; k < 3; ++k)
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, keys.p + k * nf, keys_o.p + k * nf, ids.p + k * nf,
-                                             permA.p + k * nf, static_cast<int>(nf), 0, 64, st);
+                                             permA.p + k * nf, static_cast<int>(nf), 0, 32, st);
     }, tmp, st);
   s->snodes.alloc(nf - 1, st);
   RR_CUDA(cudaMemsetAsync(s->snodes.p, 0, s->snodes.bytes(), st));
@@ -799,7 +840,7 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
       RR_LAUNCH_CHECK();
     }
     // 3. nodes + splits
-    split_kernel<<<grid(s_max), 256, 0, st>>>(segs, ls.p, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
+    split_kernel<<<grid(32 * s_max), 256, 0, st>>>(segs, ls.p, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
                                               s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
     finish_kernel<<<grid(s_max, 64), 64, 0, st>>>(segs, ls.p, perm, fb.p, cen.p, s->face_plane.p, nf, s->snodes.p,
                                                   dh.p, top.p);
