@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   D3 o{}, d{};
   double path = 0.0;
   int32_t steps = 0, bounces = 0, rplane = -2;
-  unsigned long long st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
+  uint32_t st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;  // per thread: fits 32 bits
   unsigned long long st_cnt[2] = {0, 0};  // node visits, leaf tests (CNT)
   int32_t st_max = 0;
 
@@ -205,10 +205,10 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     st_max = max(st_max, __shfl_xor_sync(0xffffffffu, st_max, off));
   }
   if (lane == 0) {
-    atomicAdd(p.stats + 0, st_bounce);
-    atomicAdd(p.stats + 1, st_esc);
-    atomicAdd(p.stats + 2, st_oor);
-    atomicAdd(p.stats + 3, st_alive);
+    atomicAdd(p.stats + 0, (unsigned long long)st_bounce);
+    atomicAdd(p.stats + 1, (unsigned long long)st_esc);
+    atomicAdd(p.stats + 2, (unsigned long long)st_oor);
+    atomicAdd(p.stats + 3, (unsigned long long)st_alive);
     atomicMax(p.stats + 4, (unsigned long long)st_max);
   }
   if (CNT) {
@@ -809,6 +809,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 15) dfk = trace_kernel<1, 8, false, 16, -4>;  // >= 1/4 of the loop's lanes stuck
   if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
   if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
+  if (df == 33) dfk = trace_kernel<1, 9, false, 16, -2>;  // 56-register budget
   if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
   if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
   if (df == 32) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 16>;
