@@ -282,6 +282,10 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   int2 st[kStack - SMS];
   int sp = 0;
   int32_t leaf = 0;  // stashed leaf (< 0) or 0
+  if (node < 0 && node != kDone) {  // one-face scene: the root is a leaf
+    leaf = node;
+    node = kDone;
+  }
   auto pop = [&]() {
     node = kDone;
     while (sp > 0) {

@@ -1,0 +1,324 @@
+"""The reference's own unit-test cases, restated against the GPU API.
+
+Each test mirrors one TEST_CASE of the reference's suite (file:line cited)
+with the same inputs and bounds, so the GPU path passes the checks a
+reference user already relies on:
+  tests/test_tracer.cpp (reflection, one bounce, escape, capture on exit,
+  energy bookkeeping, specularity, sorted captures, order invariance, source
+  inside the receiver, inverse-square law, truncation),
+  tests/test_geometry.cpp (triangle and sphere examples, watertight cube),
+  tests/test_accel_tree.cpp (median split, single leaf, empty mesh, perfect
+  tree, balanced leaves).
+The reference draws random inputs from std::mt19937; these use seeded numpy
+generators of the same shape and size.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1811_05784_b200 import AccelTree, Receiver, SourceConfig, TraceConfig, TriangleMesh
+from paper_1811_05784_b200 import roomray as rr
+from paper_1811_05784_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+CONCRETE = [0.36, 0.36, 0.44, 0.31, 0.29, 0.39, 0.25, 0.25]  # Table-1 concrete block, coarse
+
+
+def _box(dims, alpha=0.0):
+    v, f, a = scenes.box_scene(dims, absorption=alpha)
+    return AccelTree(TriangleMesh(v, f, a))
+
+
+def _single(a, b, c, alpha=0.0):
+    v = np.array([a, b, c], np.float64)
+    return AccelTree(TriangleMesh(v, np.array([[0, 1, 2, 0]], np.int32), np.full((1, 8), alpha)))
+
+
+def _rays(origins, dirs, hist_cap=64):
+    o = np.ascontiguousarray(np.atleast_2d(origins), np.float64)
+    d = np.ascontiguousarray(np.atleast_2d(dirs), np.float64)
+    n = len(o)
+    return rr.Rays(o.copy(), d.copy(), np.ones((n, 8)), np.zeros(n), np.ones(n, np.int32),
+                   np.zeros((n, hist_cap), np.int32), np.zeros(n, np.int32))
+
+
+def _unit(rng, n):
+    v = rng.normal(size=(n, 3))
+    return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+
+# ---------------------------------------------------------------- test_tracer.cpp
+def test_reflection_examples_and_identities():
+    """test_tracer.cpp:25-42 through one step off a large z = 0 triangle."""
+    tree = _single((-100, -100, 0), (100, -100, 0), (0, 200, 0))
+    s = math.sqrt(2.0) / 2.0
+    rng = np.random.default_rng(11)
+    u = _unit(rng, 1000)
+    u[:, 2] = -np.abs(u[:, 2]) - 0.05  # all head for the plane
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    dirs = np.concatenate([[[0, 0, -1], [s, 0, -s]], u])
+    rays = _rays(np.tile([0.0, 0.0, 1.0], (len(dirs), 1)), dirs)
+    rr.step(tree, rays, Receiver((500, 500, 500), 0.1), TraceConfig(max_range=1e3))
+    r = rays.dir
+    assert np.linalg.norm(r[0] - [0, 0, 1]) < 1e-15
+    assert np.linalg.norm(r[1] - [s, 0, s]) < 1e-15
+    n = np.array([0.0, 0.0, 1.0])  # oriented against the incident direction
+    assert np.all(np.abs(np.linalg.norm(r, axis=1) - 1.0) <= 1e-12)
+    assert np.all(np.abs(r @ n + dirs @ n) <= 1e-12)
+    tan_r = r - np.outer(r @ n, n)
+    tan_u = dirs - np.outer(dirs @ n, n)
+    assert np.all(np.linalg.norm(tan_r - tan_u, axis=1) <= 1e-12)
+
+
+def test_one_bounce_applies_the_per_band_wall_absorption():
+    """test_tracer.cpp:44-63."""
+    tree = _box((2, 2, 2), CONCRETE)
+    rays = _rays([1, 1, 1], [1, 0, 0])
+    rr.step(tree, rays, Receiver((1, 1, 1.5), 0.01), TraceConfig(max_range=100.0))
+    expected = np.array([0.64, 0.64, 0.56, 0.69, 0.71, 0.61, 0.75, 0.75])
+    assert np.all(np.abs(rays.mult[0] - expected) < 1e-12)
+    assert rays.path[0] == pytest.approx(1.0)
+    assert rays.n_hist[0] == 1
+    assert np.linalg.norm(rays.dir[0] - [-1, 0, 0]) < 1e-15
+    assert rays.alive[0] == 1
+
+
+def test_ray_aimed_away_from_an_open_mesh_is_killed_without_capture():
+    """test_tracer.cpp:65-81."""
+    tree = _single((0, 0, 0), (1, 0, 0), (0, 1, 0))
+    rays = _rays([0.2, 0.2, 1.0], [0, 0, 1])
+    caps = rr.step(tree, rays, Receiver((50, 50, 50), 0.1), TraceConfig(max_range=100.0)).captures()
+    assert len(caps) == 0
+    assert rays.alive[0] == 0
+
+
+def test_escaping_ray_can_still_be_captured_on_the_way_out():
+    """test_tracer.cpp:83-100."""
+    tree = _single((0, 0, 0), (1, 0, 0), (0, 1, 0))
+    rays = _rays([0.2, 0.2, 1.0], [0, 0, 1])
+    caps = rr.step(tree, rays, Receiver((0.2, 0.2, 5.0), 0.25), TraceConfig(max_range=100.0)).captures()
+    assert len(caps) == 1
+    assert caps.path[0] == pytest.approx(3.75)
+    assert rays.alive[0] == 0
+
+
+def test_energy_bookkeeping_in_a_fully_reflecting_box():
+    """test_tracer.cpp:102-128: alpha = 0 keeps multipliers at 1; in a closed
+    mesh only the range kills."""
+    tree = _box((3, 4, 5))
+    rays = rr.Rays.emit(rr.SourceConfig((1.5, 2, 2.5), 500), hist_cap=16)
+    cfg = TraceConfig(max_range=40.0)
+    for _ in range(12):
+        rr.step(tree, rays, Receiver((1.0, 1.0, 1.0), 0.3), cfg)
+        assert np.all(rays.mult == 1.0)
+        dead = rays.alive == 0
+        assert np.all(rays.path[dead] > cfg.max_range)
+
+
+def test_shoebox_rays_stay_specular():
+    """test_tracer.cpp:130-152."""
+    tree = _box((5, 4, 3))
+    rays = rr.Rays.emit(rr.SourceConfig((4, 2, 1.7), 200), hist_cap=16)
+    initial = np.abs(rays.dir.copy())
+    for _ in range(10):
+        rr.step(tree, rays, Receiver((2, 2, 1.7), 0.2), TraceConfig(max_range=30.0))
+        assert np.all(np.abs(np.abs(rays.dir) - initial) <= 1e-9)
+
+
+def test_captures_are_monotone_in_path_length_and_sorted():
+    """test_tracer.cpp:154-179 (the device lattice)."""
+    tree = _box((5, 4, 3))
+    rec = Receiver((2, 2, 1.7), 0.2)
+    res = rr.trace(tree, SourceConfig((4, 2, 1.7), 3000), rec, TraceConfig())
+    c = res.captures
+    assert len(c) > 0
+    ordered = (c.ray[1:] > c.ray[:-1]) | ((c.ray[1:] == c.ray[:-1]) & (c.path[1:] > c.path[:-1]))
+    assert ordered.all()
+    assert np.all(np.abs(np.linalg.norm(c.point - np.array(rec.center), axis=1) - rec.radius) <= 1e-9)
+    assert np.all(c.path <= res.max_range)
+
+
+def test_captures_are_independent_of_ray_processing_order():
+    """test_tracer.cpp:181-218: forward and reversed spans, 8 steps."""
+    tree = _box((5, 4, 3))
+    rec, cfg = Receiver((2, 2, 1.7), 0.2), TraceConfig(max_range=25.0)
+    n = 400
+    fwd = rr.Rays.emit(rr.SourceConfig((4, 2, 1.7), n), hist_cap=16)
+    rev = rr.Rays(*[np.ascontiguousarray(x[::-1]) for x in (fwd.origin, fwd.dir, fwd.mult, fwd.path, fwd.alive,
+                                                             fwd.hist, fwd.n_hist)])
+    a, b = [], []
+    for _ in range(8):
+        ca = rr.step(tree, fwd, rec, cfg).captures()
+        cb = rr.step(tree, rev, rec, cfg).captures()
+        a += list(zip(ca.ray.tolist(), ca.path.tolist()))
+        b += list(zip((n - 1 - cb.ray).tolist(), cb.path.tolist()))
+    a.sort()
+    b.sort()
+    assert len(a) == len(b) > 0
+    for (ra, pa), (rb, pb) in zip(a, b):
+        assert ra == rb and pa == pytest.approx(pb, rel=1e-12)
+
+
+def test_repeated_step_is_deterministic():
+    """test_tracer.cpp:220-249 compares thread counts; the GPU grid replaces
+    thread_count, so the same span stepped twice must agree exactly."""
+    tree = _box((5, 4, 3))
+    rec = Receiver((2, 2, 1.7), 0.2)
+    x = rr.Rays.emit(rr.SourceConfig((4, 2, 1.7), 4096), hist_cap=8)
+    y = rr.Rays(*[np.copy(v) for v in (x.origin, x.dir, x.mult, x.path, x.alive, x.hist, x.n_hist)])
+    for _ in range(5):
+        ca = rr.step(tree, x, rec, TraceConfig(max_range=25.0)).captures()
+        cb = rr.step(tree, y, rec, TraceConfig(max_range=25.0, thread_count=4)).captures()
+        assert np.array_equal(ca.ray, cb.ray) and np.array_equal(ca.path, cb.path)
+
+
+def test_direct_capture_with_the_source_inside_the_receiver_uses_the_exit():
+    """test_tracer.cpp:251-269."""
+    tree = _box((10, 10, 10))
+    res = rr.trace(tree, SourceConfig((5, 5, 5), 16), Receiver((5, 5, 5), 0.5),
+                   TraceConfig(max_iterations=1, max_range=100.0))
+    c = res.captures
+    assert len(c) == 16
+    assert np.allclose(c.path, 0.5)
+    assert np.all(np.diff(c.hist_off) == 0)
+
+
+def test_free_space_inverse_square_law_at_18_m():
+    """test_tracer.cpp:271-292: 10^6 rays, absorbent 200 m box, r = 0.36."""
+    tree = _box((200, 200, 200), 1.0)
+    res = rr.trace(tree, SourceConfig((100, 100, 100), 1_000_000), Receiver((118, 100, 100), 0.36), TraceConfig())
+    assert res.max_range == pytest.approx(180.0)
+    direct = int(np.sum(np.diff(res.captures.hist_off) == 0))
+    expected = 1e6 * 0.36 * 0.36 / (4.0 * 18.0 * 18.0)
+    assert abs(direct - expected) <= 3.0 * math.sqrt(expected)
+
+
+def test_iteration_cap_flags_truncation():
+    """test_tracer.cpp:294-309."""
+    tree = _box((2, 2, 2))
+    res = rr.trace(tree, SourceConfig((1, 1, 1), 8), Receiver((1, 1, 1), 0.1),
+                   TraceConfig(max_iterations=3, max_range=1e6))
+    assert res.truncated and res.iterations == 3
+
+
+# ---------------------------------------------------------------- test_geometry.cpp
+@pytest.mark.parametrize("brute", [False, True])
+def test_triangle_intersection_axis_aligned_examples(brute):
+    """test_geometry.cpp:48-73 through nearest_hit / nearest_hit_brute."""
+    tree = _single((0, 0, 0), (1, 0, 0), (0, 1, 0))
+    hit = rr.nearest_hit_brute if brute else rr.nearest_hit
+    o = [[0.25, 0.25, 1], [0.25, 0.25, 1], [2, 2, 1], [0.25, 0.25, -1], [0.25, 0.25, 1e-7]]
+    d = [[0, 0, -1], [0, 0, 1], [0, 0, -1], [0, 0, 1], [0, 0, -1]]
+    face, delta, point = hit(tree, o, d)
+    assert face[0] == 0 and delta[0] == pytest.approx(1.0)
+    assert np.linalg.norm(point[0] - [0.25, 0.25, 0]) < 1e-12
+    assert face[1] == -1  # pointing away
+    assert face[2] == -1  # barycentric outside
+    assert face[3] == 0   # double sided: hit from below
+    assert face[4] == -1  # self-hit guard (delta <= 1e-6)
+
+
+def test_sphere_intersection_examples():
+    """test_geometry.cpp:75-86, through receiver captures of one step (an open
+    one-face mesh far away, so every ray escapes after its sphere test)."""
+    tree = _single((1000, 1000, 1000), (1001, 1000, 1000), (1000, 1001, 1000))
+    cases = [((0, 0, 0), (1, 0, 0), (5, 0, 0), 4.0),   # entry
+             ((0, 0, 0), (0, 1, 0), (5, 0, 0), None),  # miss
+             ((0, 0, 0), (0, 0, 1), (0, 0, 0), 1.0),   # origin at the centre: exit
+             ((10, 0, 0), (1, 0, 0), (5, 0, 0), None)]  # sphere behind
+    for o, d, c, want in cases:
+        rays = _rays(o, d)
+        caps = rr.step(tree, rays, Receiver(c, 1.0), TraceConfig(max_range=100.0)).captures()
+        if want is None:
+            assert len(caps) == 0
+        else:
+            assert len(caps) == 1 and caps.path[0] == pytest.approx(want)
+
+
+def test_watertight_cube_every_inside_ray_finds_one_nearest_hit():
+    """test_geometry.cpp:120-131: 10 000 random directions from the centre."""
+    tree = _box((2, 2, 2))
+    d = _unit(np.random.default_rng(99), 10000)
+    for hit in (rr.nearest_hit, rr.nearest_hit_brute):
+        face, delta, _ = hit(tree, np.tile([1.0, 1.0, 1.0], (10000, 1)), d)
+        assert np.all(face >= 0)
+        assert np.all(delta <= math.sqrt(3.0) + 1e-12) and np.all(delta >= 1.0 - 1e-12)
+
+
+# ---------------------------------------------------------------- test_accel_tree.cpp
+def _beads(stations):
+    v, f = [], []
+    for x in stations:
+        b = len(v)
+        v += [(x, 0, 0), (x + 0.1, 0, 0), (x, 0.1, 0)]
+        f.append((b, b + 1, b + 2, 0))
+    return AccelTree(TriangleMesh(np.array(v, np.float64), np.array(f, np.int32), np.zeros((1, 8))))
+
+
+def _leaves(nodes, n, depth, out):
+    if nodes["face"][n] >= 0:
+        out.append((int(nodes["face"][n]), depth))
+        return
+    for c in (nodes["left"][n], nodes["right"][n]):
+        assert np.all(nodes["lo"][n] <= nodes["lo"][c]) and np.all(nodes["hi"][c] <= nodes["hi"][n])
+        _leaves(nodes, c, depth + 1, out)
+
+
+def test_median_split_on_the_largest_extent():
+    """test_accel_tree.cpp:48-66."""
+    t = _beads([0, 10, 20, 30])
+    nd = t.nodes()
+    assert t.leaf_count() == 4 and t.node_count() == 7 and t.depth() == 2
+    root = t.root
+    left, right = [], []
+    _leaves(nd, nd["left"][root], 1, left)
+    _leaves(nd, nd["right"][root], 1, right)
+    assert sorted(f for f, _ in left) == [0, 1] and sorted(f for f, _ in right) == [2, 3]
+    assert nd["hi"][nd["left"][root]][0] < nd["lo"][nd["right"][root]][0]
+
+
+def test_single_face_is_a_single_leaf():
+    """test_accel_tree.cpp:68-74."""
+    t = _beads([5])
+    assert t.node_count() == 1 and t.depth() == 0
+    assert t.nodes()["face"][t.root] == 0
+
+
+def test_empty_mesh_is_rejected():
+    """test_accel_tree.cpp:76-80: std::invalid_argument -> ValueError."""
+    with pytest.raises(ValueError):
+        AccelTree(TriangleMesh(np.zeros((0, 3)), np.zeros((0, 4), np.int32), np.zeros((1, 8))))
+
+
+def test_power_of_two_face_count_gives_a_perfect_tree():
+    """test_accel_tree.cpp:82-90."""
+    v, f, a = scenes.subdivided_tetrahedron(17)
+    assert len(f) == 1 << 17
+    t = AccelTree(TriangleMesh(v, f, a))
+    assert t.leaf_count() == 1 << 17 and t.node_count() == 2 * (1 << 17) - 1 and t.depth() == 17
+
+
+def test_leaves_partition_the_face_set_and_stay_balanced():
+    """test_accel_tree.cpp:92-108 (777-face soup)."""
+    v, f, a = scenes.random_soup(5150, 777, 10.0, 0.5)
+    t = AccelTree(TriangleMesh(v, f, a))
+    out = []
+    _leaves(t.nodes(), t.root, 0, out)
+    faces = sorted(x for x, _ in out)
+    depths = [d for _, d in out]
+    assert faces == list(range(len(f)))
+    assert max(depths) - min(depths) <= 1
+    assert max(depths) <= math.ceil(math.log2(len(f))) + 1
+
+
+def test_one_face_scene_traces_to_completion():
+    """A one-face mesh has a leaf root (accel_tree.cpp:43-46); the persistent
+    tracer and step() must test it and finish (regression: a stashed-leaf
+    traversal that never saw the leaf spun forever)."""
+    tree = _single((0, 0, 0), (1, 0, 0), (0, 1, 0))
+    res = rr.trace(tree, SourceConfig((0.2, 0.2, 1.0), 1000), Receiver((0.2, 0.2, 5.0), 0.25),
+                   TraceConfig(max_range=100.0))
+    assert res.iterations <= 3 and res.escaped == 1000
+    assert len(res.captures) > 0
