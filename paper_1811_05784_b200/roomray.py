@@ -430,6 +430,27 @@ class DeviceImages:
         return d.value, e.value, n.value
 
 
+def import_captures(tree: AccelTree, ray, point, direction, path, histories, receiver: Receiver,
+                    mult=None) -> DeviceTrace:
+    """rr_captures_import: caller-held Capture records (tracer_types.hpp:27-34)
+    as a device trace for build_image_sources (image_sources.hpp:58-61).
+    ``histories`` is a list of face-index sequences; ``mult`` None rebuilds
+    the multipliers from the histories (the product of 1 - alpha)."""
+    n = len(ray)
+    r = np.ascontiguousarray(ray, np.int32).reshape(-1)
+    lens = np.array([len(h) for h in histories], np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    hist = np.ascontiguousarray(np.concatenate([np.asarray(h, np.int32) for h in histories]) if lens.sum()
+                                else np.zeros(1, np.int32), np.int32)
+    pt, di, pa = _f64(point).reshape(n, 3), _f64(direction).reshape(n, 3), _f64(path).reshape(n)
+    m = None if mult is None else _f64(mult).reshape(n, NUM_BANDS)
+    rec = _lib.Receiver((C.c_double * 3)(*map(float, receiver.center)), float(receiver.radius))
+    h = C.c_void_p()
+    check(tree.lib.rr_captures_import(tree.h, n, None, ptr(r), ptr(pt), ptr(di), ptr(pa), ptr(m), ptr(off),
+                                      ptr(hist), C.byref(rec), 1, C.byref(h)))
+    return DeviceTrace(tree, h)
+
+
 def build_image_sources_device(trace_res: DeviceTrace, total_rays: int, air: AirModel = AirModel(),
                                options: ClusterOptions = ClusterOptions(), receiver: int = 0) -> DeviceImages:
     a = air.c()

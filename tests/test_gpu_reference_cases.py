@@ -322,3 +322,225 @@ def test_one_face_scene_traces_to_completion():
                    TraceConfig(max_range=100.0))
     assert res.iterations <= 3 and res.escaped == 1000
     assert len(res.captures) > 0
+
+
+# ---------------------------------------------------------------- test_image_sources.cpp
+def _images(tree, caps, receiver, total_rays=1000, air=None, merge=False):
+    """caps: list of (point, dir, path, history) -> fetched image sources."""
+    pts = np.array([c[0] for c in caps], np.float64)
+    dirs = np.array([c[1] for c in caps], np.float64)
+    paths = np.array([c[2] for c in caps], np.float64)
+    dt = rr.import_captures(tree, np.arange(len(caps)), pts, dirs, paths, [c[3] for c in caps], receiver)
+    return rr.build_image_sources(dt, total_rays, air or rr.AirModel.off(), rr.ClusterOptions(1e-6, merge))
+
+
+def _toward(frm, to):
+    d = np.asarray(to, np.float64) - np.asarray(frm, np.float64)
+    return d / np.linalg.norm(d)
+
+
+def test_retro_propagation_unfolds_mirrors():
+    """test_image_sources.cpp:25-48: direct and first-order mirrors (walls
+    x = 0, face 0, and x = 5, face 2)."""
+    tree = _box((5, 4, 3))
+    source, rc = np.array([4, 2, 1.7]), np.array([2, 2, 1.7])
+    caps = []
+    for img, hist in ((source, []), (np.array([-4, 2, 1.7]), [0]), (np.array([6, 2, 1.7]), [2])):
+        d = _toward(img, rc)
+        entry = rc - 0.2 * d
+        caps.append((entry, d, np.linalg.norm(entry - img), hist))
+    im = _images(tree, caps, Receiver(tuple(rc), 0.2))
+    assert len(im) == 3
+    got = {tuple(im.face_path(i)): im.position[i] for i in range(len(im))}
+    assert np.linalg.norm(got[()] - source) < 1e-12
+    assert np.linalg.norm(got[(0,)] - [-4, 2, 1.7]) < 1e-12
+    assert np.linalg.norm(got[(2,)] - [6, 2, 1.7]) < 1e-12
+
+
+def test_clustering_keys_on_the_exact_face_path():
+    """test_image_sources.cpp:50-75: 250 captures of one path -> one image;
+    the same retro point under another path stays split unless merged."""
+    tree = _box((5, 4, 3))
+    target = np.array([1.0, 2.0, 3.0])
+    caps = []
+    for i in range(250):
+        d = np.array([1.0, 0.001 * i, 0.0])
+        d /= np.linalg.norm(d)
+        caps.append((target + 4.0 * d, d, 4.0, [7, 9]))
+    rec = Receiver((2, 2, 1.7), 0.2)
+    im = _images(tree, caps, rec)
+    assert len(im) == 1 and im.ray_count[0] == 250 and im.order[0] == 2
+    assert np.linalg.norm(im.position[0] - target) < 1e-12
+    caps.append((target + np.array([4.0, 0, 0]), np.array([1.0, 0, 0]), 4.0, [7, 10]))
+    assert len(_images(tree, caps, rec)) == 2
+    merged = _images(tree, caps, rec, merge=True)
+    assert len(merged) == 1 and merged.ray_count[0] == 251
+
+
+def test_divergent_retro_points_split_even_with_one_path():
+    """test_image_sources.cpp:77-83."""
+    tree = _box((5, 4, 3))
+    caps = [((0, 0, 0), (1, 0, 0), 2.0, [3]), ((5, 0, 0), (1, 0, 0), 2.0, [3])]
+    assert len(_images(tree, caps, Receiver((2, 2, 1.7), 0.2))) == 2
+
+
+def test_energy_attachment_follows_the_capture_units():
+    """test_image_sources.cpp:85-120: n/N, exact halving, an absorbent wall,
+    air absorption exp(-beta d); image 10 m from the receiver."""
+    per_wall = np.zeros((6, 8))
+    per_wall[0] = 1.0  # wall x0 (faces 0, 1) totally absorbent
+    v, f, a = scenes.box_scene((5, 4, 3), per_wall=per_wall)
+    tree = AccelTree(TriangleMesh(v, f, a))
+    rec = Receiver((0, 0, 0), 0.2)
+    direct = [((0, 0, 0.2), (0, 0, -1), 9.8, [])] * 25
+    lossless = _images(tree, direct, rec, 1000)
+    assert lossless.distance[0] == pytest.approx(10.0)
+    assert np.all(np.abs(lossless.band_energy[0] - 0.025) < 1e-15)
+    doubled = _images(tree, direct, rec, 2000)
+    assert np.all(np.abs(lossless.band_energy[0] - 2.0 * doubled.band_energy[0]) < 1e-18)
+    absorbed = _images(tree, [((0, 0, 0.2), (0, 0, -1), 9.8, [0])] * 25, rec, 1000)
+    assert np.all(absorbed.band_energy[0] == 0.0)
+    air = rr.AirModel()
+    damped = _images(tree, direct, rec, 1000, air)
+    beta = rr.air_beta_bands(air)
+    assert np.all(damped.band_energy[0] <= lossless.band_energy[0])
+    np.testing.assert_allclose(damped.band_energy[0], lossless.band_energy[0] * np.exp(-beta * 10.0), rtol=1e-12)
+
+
+def test_projection_lands_on_the_reflecting_wall():
+    """test_image_sources.cpp:122-139."""
+    tree = _box((5, 4, 3))
+    rc = np.array([2, 2, 1.7])
+    caps = []
+    for img, hist in ((np.array([-4, 2, 1.7]), [0]), (np.array([4, 2, 1.7]), [])):
+        d = _toward(img, rc)
+        entry = rc - 0.2 * d
+        caps.append((entry, d, np.linalg.norm(entry - img), hist))
+    im = _images(tree, caps, Receiver(tuple(rc), 0.2))
+    by_order = {int(im.order[i]): i for i in range(len(im))}
+    i1, i0 = by_order[1], by_order[0]
+    assert im.has_projection[i1] == 1
+    assert np.linalg.norm(im.projection[i1] - [0, 2, 1.7]) < 1e-12
+    assert im.has_projection[i0] == 0
+
+
+# ---------------------------------------------------------------- test_rir.cpp
+def test_empty_image_set_gives_an_empty_response():
+    """test_rir.cpp:37-42."""
+    res = rr.synthesize(np.zeros(0), np.zeros((0, 8)), 343.0, 44100.0)
+    assert len(res.samples) == 0
+
+
+def test_single_event_at_t0_reproduces_the_causal_kernel_half():
+    """test_rir.cpp:44-56: one unit event in band 4 at t = 0."""
+    e = np.zeros((1, 8))
+    e[0, 4] = 1.0
+    res = rr.synthesize(np.zeros(1), e, 343.0, 44100.0)
+    kernel = rr.design_band_filter(4, 44100.0)
+    delay = (len(kernel) - 1) // 2
+    assert len(res.samples) == delay + 1
+    np.testing.assert_allclose(res.samples, kernel[delay:], rtol=1e-15, atol=0)
+
+
+def test_two_identical_events_superpose_at_the_sample_offset():
+    """test_rir.cpp:58-79: band-3 events of amplitude 0.7 at 1 s and 2 s."""
+    fs = 44100.0
+    e = np.zeros((2, 8))
+    e[:, 3] = 0.49
+    two = rr.synthesize(np.array([343.0, 686.0]), e, 343.0, fs).samples
+    one = rr.synthesize(np.array([343.0]), e[:1], 343.0, fs).samples
+    off = int(fs)
+    expected = two.copy()
+    expected[:] = 0.0
+    expected[:len(one)] += one
+    expected[off:off + len(one)] += one[:len(expected) - off]
+    np.testing.assert_allclose(two, expected, rtol=1e-12, atol=1e-15)
+
+
+def test_band_edges_share_crossovers_so_the_summed_bank_is_flat():
+    """test_rir.cpp:81-94: summed bank within 1.5 dB over 88 Hz - 5.6 kHz."""
+    fs = 44100.0
+    total = sum(rr.design_band_filter(b, fs) for b in range(8))
+    n = np.arange(len(total))
+    for i in range(81):
+        f = 88.0 * (5600.0 / 88.0) ** (i / 80.0)
+        mag = abs(np.sum(total * np.exp(-2j * np.pi * f * n / fs)))
+        assert abs(20.0 * math.log10(mag)) <= 1.5
+
+
+def test_band_kernel_energy_against_the_brickwall_ideal():
+    """test_rir.cpp:96-114."""
+    fs = 44100.0
+    for b, fc in enumerate([62.5, 125.0, 250.0, 500.0, 1000.0, 2000.0, 4000.0, 8000.0]):
+        k = rr.design_band_filter(b, fs)
+        ratio = float(np.sum(k * k)) / (2.0 * fc * (math.sqrt(2.0) - 1.0 / math.sqrt(2.0)) / fs)
+        assert (0.25 if b == 0 else 0.5) <= ratio <= 1.5
+
+
+def test_sample_rate_must_cover_the_top_band_edge():
+    """test_rir.cpp:116-119."""
+    with pytest.raises(ValueError):
+        rr.design_band_filter(7, 16000.0)
+    rr.design_band_filter(7, 44100.0)
+
+
+# ---------------------------------------------------------------- test_metrics.cpp
+def _train_factors(band, events, c=343.0):
+    """factors() of one band's pulse train, the events given as (t, a)."""
+    d = np.array([t * c for t, _ in events], np.float64)
+    e = np.zeros((len(events), 8))
+    e[:, band] = [a * a for _, a in events]
+    return rr.factors(d, e, c)
+
+
+def test_two_equal_pulses_clarity_zero_definition_half_center_mid():
+    """test_metrics.cpp:81-89."""
+    f = _train_factors(4, [(0.0, 0.3), (0.1, 0.3)])["bands"][4]
+    assert f["c80_db"][1]
+    assert f["c80_db"][0] == pytest.approx(0.0, abs=1e-9)
+    assert f["d50_pct"][0] == pytest.approx(50.0, abs=1e-9)
+    assert f["ts_ms"][0] == pytest.approx(50.0, abs=1e-9)
+    assert f["spl_db"][0] == pytest.approx(10.0 * math.log10(0.18), rel=1e-12)
+
+
+def test_windows_are_measured_from_the_first_arrival():
+    """test_metrics.cpp:91-99."""
+    f = _train_factors(0, [(0.5, 0.3), (0.6, 0.3)])["bands"][0]
+    assert f["c80_db"][0] == pytest.approx(0.0, abs=1e-9)
+    assert f["d50_pct"][0] == pytest.approx(50.0, abs=1e-9)
+    assert f["ts_ms"][0] == pytest.approx(50.0, abs=1e-6)
+
+
+def test_a_lone_direct_pulse_has_all_energy_early():
+    """test_metrics.cpp:101-110."""
+    f = _train_factors(2, [(0.01, 0.5)])["bands"][2]
+    assert f["d50_pct"][0] == pytest.approx(100.0)
+    assert f["c80_db"][0] == pytest.approx(99.0)
+    assert f["ts_ms"][0] == pytest.approx(0.0, abs=1e-12)
+    assert not f["t30_s"][1]
+
+
+def test_insufficient_decay_flags_t30_unreliable_but_not_the_rest():
+    """test_metrics.cpp:112-121."""
+    f = _train_factors(1, [(0.0, 1.0), (0.05, 0.5), (0.1, 0.25), (0.15, 0.125)])["bands"][1]
+    assert not f["t30_s"][1] and f["spl_db"][1] and f["d50_pct"][1]
+
+
+def test_band_factors_aggregate_the_mid_bands():
+    """test_metrics.cpp:123-136."""
+    c = 343.0
+    d = np.array([0.0, 0.1 * c])
+    e = np.full((2, 8), 0.09)
+    e[:, 3] = 0.01
+    out = rr.factors(d, e, c)
+    assert out["mid"]["d50_pct"][0] == pytest.approx(50.0)
+    spl500, spl1k = out["bands"][3]["spl_db"][0], out["bands"][4]["spl_db"][0]
+    assert out["mid"]["spl_db"][0] == pytest.approx(0.5 * (spl500 + spl1k))
+
+
+def test_factors_of_an_empty_or_silent_train_are_unreliable():
+    """test_metrics.cpp:138-148."""
+    f = rr.factors(np.zeros(0), np.zeros((0, 8)))["bands"][0]
+    assert not f["spl_db"][1] and not f["t30_s"][1]
+    g = _train_factors(0, [(0.1, 0.0)])["bands"][0]
+    assert not g["spl_db"][1]

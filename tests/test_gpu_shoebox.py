@@ -120,3 +120,73 @@ def test_c2_images_sit_on_the_lattice(ctx):
     assert rep.energy_within(1.5, 2), np.abs(rep.energy_delta_db[rep.order <= 2]).max()
     # beams that merge_coplanar did not fold (split by range) still land on one image
     assert rep.member_off[-1] == im.n
+
+
+# ---- the reference's own shoebox cases (tests/test_shoebox.cpp), restated
+def _fixture(dmax, src=(4, 2, 1.7), recv=(2, 2, 1.7), walls=None):
+    w = np.zeros((6, 8)) if walls is None else walls
+    return rr.enumerate_images((5.0, 4.0, 3.0), w, src, recv, dmax, 0.2, rr.AirModel.off()).fetch()
+
+
+def test_order1_images_are_the_six_wall_mirrors(ctx):
+    """test_shoebox.cpp:23-40."""
+    o = _fixture(12.0)
+    got = {tuple(p) for p, k in zip(o.position.tolist(), o.order) if k == 1}
+    assert got == {(-4, 2, 1.7), (6, 2, 1.7), (4, -2, 1.7), (4, 6, 1.7), (4, 2, -1.7), (4, 2, 4.3)}
+
+
+def test_direct_image_is_the_source_itself(ctx):
+    """test_shoebox.cpp:42-51."""
+    o = _fixture(12.0)
+    assert o.order[0] == 0 and np.array_equal(o.position[0], [4, 2, 1.7])
+    assert o.distance[0] == pytest.approx(2.0)
+
+
+def test_image_count_grows_with_the_cube_of_the_range(ctx):
+    """test_shoebox.cpp:53-63."""
+    assert 7.0 <= len(_fixture(40.0)) / len(_fixture(20.0)) <= 9.0
+
+
+def test_wall_hit_counting_on_a_hand_unfolded_three_bounce_image(ctx):
+    """test_shoebox.cpp:65-97: cell (2, -1, 0) of source (4, 2, 1.5)."""
+    walls = np.repeat((0.1 * np.arange(1, 7))[:, None], 8, axis=1)
+    o = _fixture(20.0, (4, 2, 1.5), (2, 2, 1.5), walls)
+    i = int(np.nonzero(np.linalg.norm(o.position - [14, -2, 1.5], axis=1) < 1e-12)[0][0])
+    assert o.order[i] == 3 and list(o.wall_hits[i]) == [1, 1, 1, 0, 0, 0]
+    d = o.distance[i]
+    want = 0.2 * 0.2 / (4.0 * d * d) * (1.0 - 0.1) * (1.0 - 0.2) * (1.0 - 0.3)
+    assert o.band_energy[i, 0] == pytest.approx(want, rel=1e-12)
+
+
+def test_lossless_box_follows_the_pure_inverse_square_law(ctx):
+    """test_shoebox.cpp:99-108."""
+    o = _fixture(30.0)
+    want = 0.2 * 0.2 / (4.0 * o.distance ** 2)
+    assert np.all(np.abs(o.band_energy - want[:, None]) < 1e-15)
+
+
+def test_enumeration_is_sorted_and_deterministic(ctx):
+    """test_shoebox.cpp:123-139 (incl. truncation independence)."""
+    a, b, c = _fixture(25.0), _fixture(25.0), _fixture(35.0)
+    assert np.array_equal(a.position, b.position)
+    assert np.all(np.diff(a.distance) >= 0)
+    assert np.array_equal(a.position, c.position[:len(a)])
+
+
+def test_comparison_matches_aggregates_and_reports_misses(ctx):
+    """test_shoebox.cpp:141-182 with both subcases."""
+    o = _fixture(10.0)
+    tp, te, = o.position[:-1].copy(), o.band_energy[:-1].copy()  # drop the last one
+    te[0] *= 0.5  # split the first image into two half-energy beams
+    tp, te = np.concatenate([tp, tp[:1]]), np.concatenate([te, te[:1]])
+    rep = rr.compare(o, (tp, te), 1e-9, 1.5, ctx)
+    assert len(rep.oracle_index) == len(o) - 1 and len(rep.unmatched_oracle) == 1
+    assert len(rep.unmatched_traced) == 0 and rep.max_position_error <= 1e-12
+    assert rep.energy_within(0.01, 1000)
+    stray = rr.compare(o, (np.concatenate([tp, [[100, 100, 100]]]), np.concatenate([te, np.full((1, 8), 1e-6)])),
+                       1e-9, 1.5, ctx)
+    assert len(stray.unmatched_traced) == 1
+    te2 = te.copy()
+    te2[1] *= 2.0  # +3 dB
+    off = rr.compare(o, (tp, te2), 1e-9, 1.5, ctx)
+    assert not off.energy_within(1.5, 1000) and off.energy_within(3.2, 1000)
