@@ -172,6 +172,12 @@ rr_status rr_captures_import(rr_scene* scene, int64_t n, const int32_t* recv,
                              const double* mult, const int64_t* hist_off,
                              const int32_t* hist, const rr_receiver* receivers,
                              int32_t n_recv, rr_trace_result** out);
+/* fibonacci_directions (emission.cpp:17-29) as the tracer evaluates it on
+ * the device (correctly rounded fp64 sin/cos): directions of lattice
+ * indices first + i * stride, i < count, of an n-point lattice, into out
+ * (count*3, host or device).  n < 1 -> RR_INVALID_ARGUMENT. */
+rr_status rr_fibonacci_directions(rr_ctx* ctx, int64_t n, int64_t first, int64_t stride,
+                                  int64_t count, double* out);
 /* step (tracer.hpp:43-45): one iteration over n caller rays, in place —
  * the Ray span of the reference (tracer_types.hpp:11-18) as SoA arrays:
  * origin/dir n*3, mult n*8 (band multipliers), path n, alive n, hist
@@ -257,6 +263,12 @@ rr_status rr_l2_read_gbs(rr_ctx* ctx, int64_t bytes, int32_t iters, double* gbs)
 
 /* air_beta_bands (air_absorption.cpp:59-65), 8 values. */
 rr_status rr_air_beta_bands(const rr_air* air, double* beta);
+/* air_alpha_db_per_m (air_absorption.cpp:21-53): ISO 9613-1 level
+ * attenuation in dB/m at frequency f (0 when disabled). */
+rr_status rr_air_alpha_db_per_m(const rr_air* air, double f, double* alpha);
+/* AirModel::validate (air_absorption.cpp:8-19): RR_INVALID_ARGUMENT outside
+ * [-20, 50] C, [10, 100] %, [80, 120] kPa (an enabled model only). */
+rr_status rr_air_validate(const rr_air* air);
 
 /* ---------------------------------------------------------------- IR
  * build_pulse_trains + synthesize (rir.hpp:33-45), per band: events at

@@ -464,6 +464,20 @@ struct AirModel {
   bool enabled = true;
 };
 
+/// AirModel::validate (air_absorption.cpp:8-19).
+inline void validate(const AirModel& air) {
+  rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
+  detail::check(rr_air_validate(&a));
+}
+
+/// air_alpha_db_per_m (air_absorption.cpp:21-53): ISO 9613-1, dB/m.
+inline double air_alpha_db_per_m(const AirModel& air, double frequency_hz) {
+  rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
+  double out = 0.0;
+  detail::check(rr_air_alpha_db_per_m(&a, frequency_hz, &out));
+  return out;
+}
+
 /// air_beta_bands (air_absorption.hpp:35): energy attenuation per metre.
 inline BandArray air_beta_bands(const AirModel& air) {
   rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};

@@ -818,6 +818,33 @@ rr_status rr_match_destroy(rr_match* m) {
   });
 }
 
+rr_status rr_air_alpha_db_per_m(const rr_air* air, double f, double* alpha) {
+  return guarded([&] {
+    check_ptr(air, "air");
+    check_ptr(alpha, "alpha");
+    *alpha = rr::air_alpha(*air, f);
+  });
+}
+
+rr_status rr_air_validate(const rr_air* air) {
+  return guarded([&] {
+    check_ptr(air, "air");
+    rr::air_validate(*air);
+  });
+}
+
+rr_status rr_fibonacci_directions(rr_ctx* ctx, int64_t n, int64_t first, int64_t stride, int64_t count,
+                                  double* out) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    if (n < 1) rr::invalid("fibonacci_directions needs n >= 1");  // emission.cpp:18
+    if (count < 0 || first < 0 || stride < 1) rr::invalid("bad lattice subset");
+    if (count > 0) check_ptr(out, "out");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    rr::fibonacci_device(ctx, n, first, stride, count, out);
+  });
+}
+
 rr_status rr_air_beta_bands(const rr_air* air, double* beta) {
   return guarded([&] {
     check_ptr(air, "air");

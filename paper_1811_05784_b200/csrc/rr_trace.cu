@@ -645,6 +645,37 @@ __global__ void brute_hit_kernel(const FaceTri* __restrict__ tri, int64_t nf, co
   point[3 * i + 2] = pt.z;
 }
 
+__global__ void fib_kernel(int64_t n, int64_t first, int64_t stride, int64_t count, double az_step,
+                           double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const D3 d = fib_dir(first + i * stride, n, az_step);
+  out[3 * i] = d.x;
+  out[3 * i + 1] = d.y;
+  out[3 * i + 2] = d.z;
+}
+
+void fibonacci_device(rr_ctx* ctx, int64_t n, int64_t first, int64_t stride, int64_t count, double* out) {
+  if (count == 0) return;
+  cudaStream_t st = ctx->stream;
+  cudaPointerAttributes at{};
+  RR_CUDA(cudaPointerGetAttributes(&at, out));
+  const bool dev = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  DevBuf<double> tmp;
+  double* d_out = out;
+  if (!dev) {
+    tmp.alloc(3 * count, st);
+    d_out = tmp.p;
+  }
+  const double golden = (1.0 + std::sqrt(5.0)) / 2.0;  // emission.cpp:19-20, as run_trace
+  fib_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(n, first, stride, count,
+                                                                        2.0 * M_PI * (1.0 - 1.0 / golden), d_out);
+  RR_LAUNCH_CHECK();
+  ctx->launches++;
+  if (!dev) RR_CUDA(cudaMemcpyAsync(out, d_out, sizeof(double) * 3 * count, cudaMemcpyDeviceToHost, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+}
+
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d, int64_t n, int brute, int32_t* d_face,
                        double* d_delta, double* d_point) {
   if (n <= 0) return;

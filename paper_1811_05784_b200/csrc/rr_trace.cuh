@@ -117,3 +117,10 @@ rr_match* compare_lattice(rr_ctx* ctx, int64_t no, const double* opos, const dou
                           int64_t nt, const double* tpos, const double* tenergy, double pos_tol, double energy_tol_db);
 void air_beta_bands(const rr_air& a, double* beta);
 }  // namespace rr
+
+namespace rr {
+// rr_trace.cu: the tracer's own lattice evaluation, for rr_fibonacci_directions
+void fibonacci_device(rr_ctx* ctx, int64_t n, int64_t first, int64_t stride, int64_t count, double* out);
+double air_alpha(const rr_air& a, double f);
+void air_validate(const rr_air& a);
+}  // namespace rr

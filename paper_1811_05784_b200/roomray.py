@@ -313,6 +313,34 @@ class AirModel:
         return _lib.Air(int(self.enabled), self.temperature_c, self.relative_humidity, self.pressure_kpa)
 
 
+def air_alpha_db_per_m(air: AirModel, frequency: float) -> float:
+    """air_alpha_db_per_m (air_absorption.cpp:21-53), dB/m."""
+    lib = _lib.load()
+    out = C.c_double()
+    a = air.c()
+    check(lib.rr_air_alpha_db_per_m(C.byref(a), float(frequency), C.byref(out)))
+    return out.value
+
+
+def air_validate(air: AirModel) -> None:
+    """AirModel::validate (air_absorption.cpp:8-19): ValueError out of range."""
+    lib = _lib.load()
+    a = air.c()
+    check(lib.rr_air_validate(C.byref(a)))
+
+
+def fibonacci_directions(n: int, first: int = 0, stride: int = 1, count: int | None = None,
+                         ctx: Context | None = None) -> np.ndarray:
+    """fibonacci_directions (emission.cpp:17-29) evaluated on the device the
+    way the tracer emits its rays (correctly rounded sin/cos)."""
+    ctx = ctx or Context.default()
+    if count is None:
+        count = max(0, (n - first + stride - 1) // stride) if n >= 1 else 0
+    out = np.empty((count, 3))
+    check(ctx.lib.rr_fibonacci_directions(ctx.h, int(n), int(first), int(stride), int(count), ptr(out)))
+    return out
+
+
 def air_beta_bands(air: AirModel) -> np.ndarray:
     lib = _lib.load()
     out = np.empty(NUM_BANDS)

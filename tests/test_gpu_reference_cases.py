@@ -544,3 +544,92 @@ def test_factors_of_an_empty_or_silent_train_are_unreliable():
     assert not f["spl_db"][1] and not f["t30_s"][1]
     g = _train_factors(0, [(0.1, 0.0)])["bands"][0]
     assert not g["spl_db"][1]
+
+
+# ---------------------------------------------------------------- test_emission.cpp
+def test_single_direction_sits_on_the_equator():
+    """test_emission.cpp:10-15."""
+    d = rr.fibonacci_directions(1)
+    assert d.shape == (1, 3) and d[0, 2] == 0.0
+    assert np.linalg.norm(d[0]) == pytest.approx(1.0, rel=1e-12)
+
+
+def test_zero_rays_is_invalid():
+    """test_emission.cpp:17-22 (fibonacci_directions and trace's emission)."""
+    with pytest.raises(ValueError):
+        rr.fibonacci_directions(0, count=0)
+    with pytest.raises(ValueError):
+        rr.trace(_box((2, 2, 2)), SourceConfig((1, 1, 1), 0), Receiver((1, 1, 1), 0.1), TraceConfig())
+
+
+def test_lattice_is_unit_norm_and_balanced():
+    """test_emission.cpp:24-33."""
+    d = rr.fibonacci_directions(1000)
+    assert np.all(np.abs(np.linalg.norm(d, axis=1) - 1.0) <= 1e-12)
+    assert np.linalg.norm(d.mean(axis=0)) <= 0.01
+
+
+def test_cap_counting_matches_solid_angle_fractions_at_one_million_points():
+    """test_emission.cpp:35-52: 20 random caps over the 10^6 lattice."""
+    n = 1_000_000
+    d = rr.fibonacci_directions(n)
+    rng = np.random.default_rng(2024)
+    for _ in range(20):
+        axis = _unit(rng, 1)[0]
+        omega = rng.uniform(0.1, 4.0)
+        inside = np.count_nonzero(d @ axis >= 1.0 - omega / (2.0 * math.pi)) / n
+        expected = omega / (4.0 * math.pi)
+        assert abs(inside - expected) <= 0.01 * expected
+
+
+def test_emission_is_deterministic_and_matches_the_host_lattice():
+    """test_emission.cpp:54-81: bit-reproducible, ray k carries lattice
+    direction k; the device lattice equals the C library's to 1 ulp (the
+    correctly rounded sin/cos differ from glibc on ~0.3 % of azimuths)."""
+    a = rr.fibonacci_directions(4096)
+    b = rr.fibonacci_directions(4096)
+    assert np.array_equal(a, b)
+    sub = rr.fibonacci_directions(4096, first=5, stride=7)
+    assert np.array_equal(sub, a[5::7])
+    host = rr.Rays.emit(rr.SourceConfig((1, 2, 3), 4096), hist_cap=1).dir
+    np.testing.assert_allclose(a, host, rtol=0, atol=4e-16)
+    assert np.all(np.linalg.norm(a[:4, None] - a[None, :4], axis=2)[np.triu_indices(4, 1)] > 1e-6)
+
+
+# ---------------------------------------------------------------- test_air_absorption.cpp
+def test_attenuation_grows_with_frequency_at_room_conditions():
+    """test_air_absorption.cpp:9-17."""
+    air = rr.AirModel()
+    beta = rr.air_beta_bands(air)
+    assert np.all(beta >= 0.0) and np.all(np.diff(beta) > 0)
+    assert rr.air_alpha_db_per_m(air, 62.5) < rr.air_alpha_db_per_m(air, 8000.0)
+
+
+def test_disabled_model_is_lossless():
+    """test_air_absorption.cpp:19-23."""
+    assert np.all(rr.air_beta_bands(rr.AirModel.off()) == 0.0)
+    assert rr.air_alpha_db_per_m(rr.AirModel.off(), 1000.0) == 0.0
+
+
+def test_reference_value_at_1khz_20c_70rh():
+    """test_air_absorption.cpp:25-32: 4.978 dB/km within 2 %."""
+    alpha = rr.air_alpha_db_per_m(rr.AirModel(relative_humidity=70.0), 1000.0)
+    assert abs(alpha - 4.978e-3) <= 0.02 * 4.978e-3
+
+
+def test_energy_and_level_conventions_agree():
+    """test_air_absorption.cpp:34-46."""
+    air = rr.AirModel()
+    alpha = rr.air_alpha_db_per_m(air, 8000.0)
+    beta = rr.air_beta_bands(air)[7]
+    assert math.exp(-beta * 100.0) == pytest.approx(10.0 ** (-alpha * 100.0 / 10.0), rel=1e-12)
+    assert abs(alpha - 0.105291) <= 0.02 * 0.105291
+    assert math.exp(-beta * 100.0) == pytest.approx(0.08853, rel=0.02)
+
+
+def test_condition_range_is_validated():
+    """test_air_absorption.cpp:48-60."""
+    for bad in (dict(temperature_c=-30.0), dict(relative_humidity=5.0), dict(pressure_kpa=200.0)):
+        with pytest.raises(ValueError):
+            rr.air_validate(rr.AirModel(**bad))
+    rr.air_validate(rr.AirModel())
