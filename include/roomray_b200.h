@@ -321,6 +321,12 @@ rr_status rr_factors_from_images(rr_ctx* ctx, int64_t n, const double* dist,
                                  const double* energy, double c,
                                  rr_factors* out);
 rr_status rr_images_factors(rr_images* im, double c, rr_factors* out);
+/* schroeder(const BandPulseTrain&) (metrics.cpp:125-134) for the 8 trains
+ * (band_off 9 entries, amplitudes in train order, host or device): level in
+ * dB per event, 10 log10(remaining / total energy).  A band whose events
+ * carry no energy -> RR_INVALID_ARGUMENT (metrics.cpp:17-19). */
+rr_status rr_band_schroeder(rr_ctx* ctx, const int64_t* band_off,
+                            const double* amplitude, double* level_db);
 
 /* Length of the reference's response (rir.cpp:78-80): llround(t_last*fs) +
  * (taps-1)/2 + 1, or 0 without events. */

@@ -337,6 +337,8 @@ class Ref:
         L.rref_nearest_hit.argtypes = [_vp, _f64p, _f64p, _i64, C.c_int, _i32p, _f64p, _f64p]
         L.rref_intersect_sphere.argtypes = [_f64p, _f64p, _f64p, C.c_double, C.POINTER(C.c_double)]
         L.rref_fibonacci.argtypes = [C.c_int, _f64p]
+        if hasattr(L, "rref_run_artifacts"):
+            L.rref_run_artifacts.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p]
         L.rref_bench_row.restype = C.c_double
         L.rref_bench_row.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double),
                                      C.POINTER(_i32)]
@@ -394,6 +396,12 @@ class Ref:
         if not h:
             self._err()
         return RefScene(self, h, mesh)
+
+    def run_artifacts(self, run_json, out_dir, oracle_json=""):
+        """The reference's run_trace_pipeline + write_run_artifacts (and the
+        shoebox oracle files with oracle_json) into out_dir."""
+        if self.L.rref_run_artifacts(str(run_json).encode(), str(out_dir).encode(), str(oracle_json).encode()):
+            self._err()
 
     def bench_row(self, k, with_tree=True, threads=1, min_elapsed=0.25, max_repeats=50):
         """The reference's complexity-benchmark row (bench.cpp:26-46, 71-102):

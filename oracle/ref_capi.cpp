@@ -34,6 +34,7 @@
 #include "roomray/metrics.hpp"
 #ifdef RREF_HAVE_OBJ
 #include "roomray/obj_loader.hpp"
+#include "roomray/pipeline.hpp"
 #endif
 #include "roomray/rir.hpp"
 #include "roomray/shoebox.hpp"
@@ -666,5 +667,34 @@ double rref_bench_row(int k, int with_tree, int threads, double min_elapsed,
   });
   return per_iter;
 }
+
+
+#ifdef RREF_HAVE_OBJ
+// The reference's `roomray trace` file set (pipeline.cpp:144-325): run the
+// pipeline on a run config (deterministic: one thread) and write its
+// artifacts into out_dir; with an oracle config also run_oracle +
+// write_oracle_artifacts and the comparison report of the traced
+// image_sources.json (pipeline.cpp:327-514) into out_dir/oracle.
+int rref_run_artifacts(const char* run_json, const char* out_dir, const char* oracle_json) {
+  return guarded([&] {
+    RunConfig config = RunConfig::from_json_file(run_json);
+    config.output_dir = out_dir;
+    config.deterministic = true;
+    config.dump_captures = true;
+    config.dump_tree_stats = true;
+    const RunArtifacts artifacts = run_trace_pipeline(config);
+    write_run_artifacts(config, artifacts);
+    if (oracle_json && *oracle_json) {
+      OracleConfig oc = OracleConfig::from_json_file(oracle_json);
+      oc.output_dir = std::string(out_dir) + "/oracle";
+      const auto oracle = run_oracle(oc);
+      write_oracle_artifacts(oc, oracle);
+      const auto traced = load_image_sources_json(std::string(out_dir) + "/image_sources.json");
+      check_comparable(oc, traced);
+      write_comparison_report(oc.output_dir + "/comparison.json", compare(oracle, traced.images, 1e-9, 1.5));
+    }
+  });
+}
+#endif
 
 }  // extern "C"

@@ -104,6 +104,7 @@ SIGNATURES = [
     ("rr_images_destroy", C.c_int, [_vp]),
     ("rr_images_device", C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     ("rr_air_beta_bands", C.c_int, [C.POINTER(Air), _f64p]),
+    ("rr_band_schroeder", C.c_int, [_vp, _vp, _vp, _vp]),
     ("rr_air_alpha_db_per_m", C.c_int, [C.POINTER(Air), _d, C.POINTER(_d)]),
     ("rr_air_validate", C.c_int, [C.POINTER(Air)]),
     ("rr_fibonacci_directions", C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),

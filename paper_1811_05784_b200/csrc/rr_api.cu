@@ -548,6 +548,22 @@ void image_factors(rr_ctx* ctx, const double* d_dist, const double* d_energy, in
 }  // namespace rr
 extern "C" {
 
+rr_status rr_band_schroeder(rr_ctx* ctx, const int64_t* band_off, const double* amplitude, double* level_db) {
+  return guarded([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(band_off, "band_off");
+    if (band_off[0] != 0) rr::invalid("band_off[0] must be 0");
+    for (int b = 0; b < rr::kBands; ++b)
+      if (band_off[b + 1] < band_off[b]) rr::invalid("band_off must be non-decreasing");
+    if (band_off[rr::kBands] > 0) {
+      check_ptr(amplitude, "amplitude");
+      check_ptr(level_db, "level_db");
+    }
+    RR_CUDA(cudaSetDevice(ctx->device));
+    rr::band_schroeder(ctx, band_off, amplitude, level_db);
+  });
+}
+
 rr_status rr_band_factors(rr_ctx* ctx, const int64_t* band_off, const double* time, const double* amplitude,
                           rr_factors* out) {
   return guarded([&] {

@@ -15,7 +15,7 @@
 #include <algorithm>
 #include <cmath>
 
-#include "rr_internal.cuh"
+#include "rr_trace.cuh"
 
 namespace rr {
 namespace {
@@ -257,6 +257,70 @@ void band_factors(rr_ctx* ctx, const double* d_t, const double* d_a, int64_t n, 
   RR_LAUNCH_CHECK();
   ctx->launches += 14;
   RR_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
+}
+
+// schroeder(const BandPulseTrain&) (metrics.cpp:13-28, 125-134): per band,
+// in the train's event order, level_i = 10 log10(max(tail_i / total,
+// 1e-300)) with tail_i the energy of events i.. (one block per band: block
+// reduction for the total, chunked block scans for the tails).
+__global__ void __launch_bounds__(256) schroeder_kernel(const int64_t* __restrict__ off,
+                                                        const double* __restrict__ amp, double* __restrict__ level,
+                                                        int32_t* __restrict__ silent) {
+  using Reduce = cub::BlockReduce<double, 256>;
+  using Scan = cub::BlockScan<double, 256>;
+  __shared__ union {
+    typename Reduce::TempStorage r;
+    typename Scan::TempStorage s;
+  } tmp;
+  __shared__ double s_total, s_carry;
+  const int b = blockIdx.x;
+  const int64_t b0 = off[b], b1 = off[b + 1];
+  if (b1 == b0) return;
+  double part = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) part += amp[i] * amp[i];
+  const double total = Reduce(tmp.r).Sum(part);
+  if (threadIdx.x == 0) {
+    s_total = total;
+    s_carry = 0.0;
+    silent[b] = total <= 0.0 ? 1 : 0;
+  }
+  __syncthreads();
+  const double tot = s_total;
+  for (int64_t c = b0; c < b1; c += blockDim.x) {
+    const int64_t i = c + threadIdx.x;
+    const double e = i < b1 ? amp[i] * amp[i] : 0.0;
+    double before = 0.0, chunk = 0.0;
+    __syncthreads();
+    Scan(tmp.s).ExclusiveSum(e, before, chunk);
+    const double tail = tot - (s_carry + before);
+    if (i < b1) level[i] = 10.0 * log10(fmax(tail / tot, 1e-300));
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += chunk;
+  }
+}
+
+void band_schroeder(rr_ctx* ctx, const int64_t* band_off, const double* amplitude, double* level) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = band_off[kBands];
+  DevBuf<int64_t> off;
+  DevBuf<double> a, lv;
+  DevBuf<int32_t> silent;
+  off.alloc(kBands + 1, st);
+  a.alloc(std::max<int64_t>(n, 1), st);
+  lv.alloc(std::max<int64_t>(n, 1), st);
+  silent.alloc(kBands, st);
+  RR_CUDA(cudaMemcpyAsync(off.p, band_off, sizeof(int64_t) * (kBands + 1), cudaMemcpyHostToDevice, st));
+  RR_CUDA(cudaMemsetAsync(silent.p, 0, sizeof(int32_t) * kBands, st));
+  if (n > 0) RR_CUDA(cudaMemcpyAsync(a.p, amplitude, sizeof(double) * n, cudaMemcpyDefault, st));
+  schroeder_kernel<<<kBands, 256, 0, st>>>(off.p, a.p, lv.p, silent.p);
+  RR_LAUNCH_CHECK();
+  ctx->launches++;
+  int32_t h_silent[kBands];
+  RR_CUDA(cudaMemcpyAsync(h_silent, silent.p, sizeof h_silent, cudaMemcpyDeviceToHost, st));
+  if (n > 0) RR_CUDA(cudaMemcpyAsync(level, lv.p, sizeof(double) * n, cudaMemcpyDefault, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < kBands; ++b)
+    if (h_silent[b]) invalid("decay of an all-zero signal is undefined");  // metrics.cpp:17-19
 }
 
 // factors(const PulseTrains&) for trains given as images: t = d / c,

@@ -123,4 +123,6 @@ namespace rr {
 void fibonacci_device(rr_ctx* ctx, int64_t n, int64_t first, int64_t stride, int64_t count, double* out);
 double air_alpha(const rr_air& a, double f);
 void air_validate(const rr_air& a);
+// rr_metrics.cu
+void band_schroeder(rr_ctx* ctx, const int64_t* band_off, const double* amplitude, double* level);
 }  // namespace rr

@@ -282,3 +282,145 @@ def test_pipeline_shoebox_acceptance(tmp_path):
     f = dict(kv.split("=") for kv in line.split()[1:])
     assert int(f["matched"]) > 0 and int(f["traced_only"]) == 0, line
     assert float(f["max_pos_err"]) <= 1e-9 and f["within"] == "1", line
+
+
+def _upstream_layout(text):
+    """The oracle's writers are built against the nlohmann 3.11.3 copy inside
+    the cudnn-frontend wheel, which carries a local patch that prints integer
+    arrays on one line ("[10,9]"); upstream nlohmann (the reference's vendored
+    json.hpp) prints them one element per line, as the facade does.  Expand
+    the patched form back to the upstream layout."""
+    import re
+    out = []
+    pat = re.compile(r"^(\s*)(.*?)\[(-?\d+(?:,-?\d+)*)\](,?)$")
+    for line in text.splitlines():
+        m = pat.match(line)
+        if not m or "\"" in m.group(3):
+            out.append(line)
+            continue
+        ind, head, body, comma = m.groups()
+        vals = body.split(",")
+        out.append(f"{ind}{head}[")
+        out += [f"{ind}  {v}{',' if i + 1 < len(vals) else ''}" for i, v in enumerate(vals)]
+        out.append(f"{ind}]{comma}")
+    return "\n".join(out) + "\n"
+
+
+def _num_lines_equal_when_values_equal(a_text, b_text):
+    """Line-by-line: a line may differ only where a number differs in value
+    (so equal values are formatted identically, as nlohmann / %.17g do)."""
+    import re
+    b_text = _upstream_layout(b_text)
+    al, bl = a_text.splitlines(), b_text.splitlines()
+    assert len(al) == len(bl)
+    num = re.compile(r"-?\d+(?:\.\d+)?(?:e[+-]\d+)?")
+    for x, y in zip(al, bl):
+        if x == y:
+            continue
+        nx, ny = num.findall(x), num.findall(y)
+        assert num.sub("#", x) == num.sub("#", y), (x, y)
+        assert any(float(p) != float(q) for p, q in zip(nx, ny)), (x, y)
+
+
+@pytest.mark.gpu
+def test_run_artifacts_match_the_reference_writers(tmp_path, ref):
+    """`roomray trace` file set (pipeline.cpp:208-325) and the shoebox
+    oracle / comparison files (:327-514), written by the facade
+    (include/roomray_b200_artifacts.hpp) from GPU results, against the
+    reference's own writers run on the reference pipeline: same files, same
+    layout, values within the parity tolerances; equal values are formatted
+    identically; two runs are byte-identical (acceptance 10)."""
+    import json
+    import struct
+    if not hasattr(ref.L, "rref_run_artifacts"):
+        pytest.skip("reference writers not built")
+    exe = str(tmp_path / "artifacts_run")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "native", "artifacts_run.cpp"), "-L",
+                    os.path.join(ROOT, "paper_1811_05784_b200"), "-lroomray_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_1811_05784_b200"), "-o", exe], check=True)
+    run = _pipeline_files(tmp_path)
+    walls = {w: ("concrete_block_coarse" if w.endswith("0") else "hollow_wooden_podium")
+             for w in ("x0", "x1", "y0", "y1", "z0", "z1")}
+    (tmp_path / "oracle.json").write_text(json.dumps({
+        "box": {"dimensions": [5, 4, 3]}, "materials": "materials.json", "walls": walls,
+        "source": {"position": [4, 2, 1.7], "ray_count": 20000}, "receiver": {"center": [2, 2, 1.7], "radius": 0.2},
+        "max_distance": 0}))
+    ours, ours2, theirs = tmp_path / "ours", tmp_path / "ours2", tmp_path / "ref"
+    for out in (ours, ours2):
+        r = subprocess.run([exe, str(run), str(out), str(tmp_path / "oracle.json")], capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+    ref.run_artifacts(run, theirs, tmp_path / "oracle.json")
+
+    def files(d):
+        return sorted(str(p.relative_to(d)) for p in d.rglob("*") if p.is_file())
+    assert files(ours) == files(theirs)
+    for name in ("image_sources.json", "metrics.json", "rir.wav"):  # acceptance 10
+        assert (ours / name).read_bytes() == (ours2 / name).read_bytes(), name
+
+    a, b = json.loads((ours / "image_sources.json").read_text()), json.loads((theirs / "image_sources.json").read_text())
+    assert a["config"] == b["config"] and a["max_range_m"] == b["max_range_m"]
+    assert len(a["images"]) == len(b["images"]) > 10
+    for x, y in zip(a["images"], b["images"]):
+        assert (x["order"], x["ray_count"], x["face_path"]) == (y["order"], y["ray_count"], y["face_path"])
+        np.testing.assert_allclose(x["position"], y["position"], rtol=1e-10, atol=1e-10)
+        np.testing.assert_allclose(x["band_energy"], y["band_energy"], rtol=1e-9)
+        assert (x["projection"] is None) == (y["projection"] is None)
+        if x["projection"] is not None:
+            np.testing.assert_allclose(x["projection"], y["projection"], rtol=1e-9, atol=1e-9)
+    _num_lines_equal_when_values_equal((ours / "image_sources.json").read_text(),
+                                       (theirs / "image_sources.json").read_text())
+    for csv in ("image_sources.csv", "band_trains.csv"):
+        ta, tb = (ours / csv).read_text().splitlines(), (theirs / csv).read_text().splitlines()
+        assert ta[0] == tb[0] and len(ta) == len(tb)
+        fa = np.array([[float(v) if v else np.nan for v in line.split(",")] for line in ta[1:]])
+        fb = np.array([[float(v) if v else np.nan for v in line.split(",")] for line in tb[1:]])
+        np.testing.assert_allclose(fa, fb, rtol=1e-9, atol=1e-12, equal_nan=True)
+        _num_lines_equal_when_values_equal((ours / csv).read_text(), (theirs / csv).read_text())
+    wa, wb = (ours / "rir.wav").read_bytes(), (theirs / "rir.wav").read_bytes()
+    assert wa[:44] == wb[:44] and len(wa) == len(wb)
+    sa, sb = np.frombuffer(wa[44:], np.float32), np.frombuffer(wb[44:], np.float32)
+    assert np.abs(sa - sb).max() <= 1e-6 * np.abs(sb).max()
+    ma, mb = json.loads((ours / "metrics.json").read_text()), json.loads((theirs / "metrics.json").read_text())
+    assert list(ma) == list(mb)
+    for band in ma:
+        for k in ma[band]:
+            assert ma[band][k]["reliable"] == mb[band][k]["reliable"], (band, k)
+            assert ma[band][k]["value"] == pytest.approx(mb[band][k]["value"], rel=1e-6, abs=1e-9), (band, k)
+    for p in sorted(ours.glob("decay_*.csv")):
+        da = np.loadtxt(p, delimiter=",", skiprows=1, ndmin=2)
+        db = np.loadtxt(theirs / p.name, delimiter=",", skiprows=1, ndmin=2)
+        assert da.shape == db.shape and np.array_equal(da[:, 0], db[:, 0])
+        keep = db[:, 1] > -100.0  # the last events' tails cancel to rounding noise in both
+        np.testing.assert_allclose(da[keep, 1], db[keep, 1], rtol=0, atol=1e-6)
+    ca = [json.loads(x) for x in (ours / "captures.jsonl").read_text().splitlines()]
+    cb = [json.loads(x) for x in (theirs / "captures.jsonl").read_text().splitlines()]
+    assert [c["ray_index"] for c in ca] == [c["ray_index"] for c in cb]
+    assert [c["face_history"] for c in ca] == [c["face_history"] for c in cb]
+    np.testing.assert_allclose([c["point"] for c in ca], [c["point"] for c in cb], rtol=1e-10, atol=1e-10)
+    ta, tb = json.loads((ours / "tree_stats.json").read_text()), json.loads((theirs / "tree_stats.json").read_text())
+    assert [ta[k] for k in ("node_count", "leaf_count", "depth")] == [tb[k] for k in ("node_count", "leaf_count", "depth")]
+    ra, rb = json.loads((ours / "run_report.json").read_text()), json.loads((theirs / "run_report.json").read_text())
+    assert list(ra) == list(rb) and list(ra["timings_s"]) == list(rb["timings_s"])
+    for k in ("mesh", "trace", "image_sources"):
+        assert ra[k] == rb[k], k
+    assert (ra["tree"]["node_count"], ra["tree"]["depth"]) == (rb["tree"]["node_count"], rb["tree"]["depth"])
+    np.testing.assert_allclose(ra["air"]["alpha_db_per_m"], rb["air"]["alpha_db_per_m"], rtol=1e-14)
+    # shoebox oracle files and the comparison report
+    oa = (ours / "oracle" / "oracle_image_sources.json").read_text()
+    ob = (theirs / "oracle" / "oracle_image_sources.json").read_text()
+    ja, jb = json.loads(oa), json.loads(ob)
+    assert ja["config"] == jb["config"] and len(ja["images"]) == len(jb["images"])
+    for x, y in zip(ja["images"], jb["images"]):
+        assert (x["position"], x["distance_m"], x["order"], x["wall_hits"]) == (
+            y["position"], y["distance_m"], y["order"], y["wall_hits"])
+        np.testing.assert_allclose(x["band_energy"], y["band_energy"], rtol=1e-12)
+    _num_lines_equal_when_values_equal(oa, ob)
+    cpa = json.loads((ours / "oracle" / "comparison.json").read_text())
+    cpb = json.loads((theirs / "oracle" / "comparison.json").read_text())
+    for k in ("matched_count", "unmatched_oracle_count", "unmatched_traced_count", "unmatched_oracle",
+              "unmatched_traced"):
+        assert cpa[k] == cpb[k], k
+    assert [m["oracle_index"] for m in cpa["matched"]] == [m["oracle_index"] for m in cpb["matched"]]
+    assert [m["traced_indices"] for m in cpa["matched"]] == [m["traced_indices"] for m in cpb["matched"]]
