@@ -591,7 +591,25 @@ __global__ void capture_out_kernel(const Capture* __restrict__ caps, const int32
   for (int b = 0; b < kBands; ++b) m[b] = 1.0;
   const int32_t* h = p.hist + static_cast<int64_t>(c.ray) * p.H;
   const int64_t base = off[i];
-  for (int j = 0; j < order; ++j) {
+  // the product stays in path order (tracer.cpp:57-58); the history, material
+  // and (1 - alpha) loads of 8 bounces go out together
+  int j = 0;
+  for (; j + 8 <= order; j += 8) {
+    int32_t f[8], mt[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) f[u] = h[j + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      o_hist[base + j + u] = f[u];
+      mt[u] = mat[f[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double* a = oma + kBands * mt[u];
+      for (int b = 0; b < kBands; ++b) m[b] *= a[b];
+    }
+  }
+  for (; j < order; ++j) {
     const int32_t f = h[j];
     o_hist[base + j] = f;
     const double* a = oma + kBands * mat[f];
