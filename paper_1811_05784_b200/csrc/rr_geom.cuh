@@ -367,7 +367,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
 // are ordered by entry distance, the nearest taken next and the others
 // pushed (leaves included, so a popped entry may be a leaf); coplanar slots
 // culled via QNode.pad; same postponed, warp-batched leaf tests.
-template <int LEAFT, int STUCKT, typename RAY>
+template <int LEAFT, int STUCKT, typename RAY, int UNR = 1>
 __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const QNode* __restrict__ q4,
                                                      int32_t root4, const FaceTri* __restrict__ tri,
                                                      const RAY& ray, int32_t rplane) {
@@ -398,7 +398,8 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
     }
   };
   while (node != kDone || leaf != 0) {
-    if (node >= 0 && node != kDone) {
+#pragma unroll 1
+    for (int u = 0; u < UNR && node >= 0 && node != kDone && (u == 0 || leaf == 0); ++u) {
       const float4* p = reinterpret_cast<const float4*>(q4 + node);
       const float4 lx = __ldg(p), hx = __ldg(p + 1), ly = __ldg(p + 2), hy = __ldg(p + 3);
       const float4 lz = __ldg(p + 4), hz = __ldg(p + 5);
@@ -437,8 +438,13 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
       } else {
         pop();
       }
+      if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
+        leaf = node;
+        prefetch_l1(tri + ~leaf);
+        pop();
+      }
     }
-    if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
+    if (node < 0 && leaf == 0) {  // a popped leaf (or a leaf root) with no node visit
       leaf = node;
       prefetch_l1(tri + ~leaf);
       pop();

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 3) {
-      wall = closest_hit4_pl<16, -2, RegRay>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
+      wall = closest_hit4_pl<16, -2, RegRay, UNR>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
       wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt,
                                                             s_stack + threadIdx.x);
@@ -843,7 +843,9 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // default: per-ray loop with postponed leaf tests over the binary SAH tree;
   // deep trees (>= 2^18 faces) over its 4-wide collapse, which halves the
   // dependent node fetches (C3 -15 %, C5 -8 %; C2 100k +8 %, so not there)
-  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 16);
+  // (binary default: up to 16 internal nodes per lane between leaf votes,
+  // C1 0.46 -> 0.36 ms, C2 12.67 -> 12.20 ms against one per vote)
+  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 37);
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
@@ -859,12 +861,16 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 16) dfk = trace_kernel<1, 8, false, 16, -2>;
   if (df == 17) dfk = trace_kernel<1, 8, false, 16, -8>;
   if (df == 33) dfk = trace_kernel<1, 9, false, 16, -2>;  // 56-register budget
+  if (df == 34) dfk = trace_kernel<1, 8, false, 16, -2, false, 2>;  // 2 / 4 internal nodes per vote round
+  if (df == 35) dfk = trace_kernel<1, 8, false, 16, -2, false, 4>;
+  if (df == 36) dfk = trace_kernel<1, 8, false, 16, -2, false, 8>;
+  if (df == 37) dfk = trace_kernel<1, 8, false, 16, -2, false, 16>;
   if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
   if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
   if (df == 32) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 16>;
   if (df == 23 && s->s4nodes.p) dfk = trace_kernel<3, 8>;
   if (df == 24 && s->s4nodes.p) dfk = trace_kernel<3, 6>;
-  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true>;
+  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true, 16>;  // counts of the default
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
