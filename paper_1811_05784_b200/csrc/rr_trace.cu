@@ -549,15 +549,18 @@ __global__ void ray_order_key_kernel(const TraceParams p, uint32_t* __restrict__
 }
 
 // ---------------------------------------------------------------- captures
-__global__ void capture_keys_kernel(const Capture* __restrict__ caps, int64_t n, TraceParams p,
+// sort key (receiver, ray, order) packed into as few bits as the run needs
+// (b_ray bits of the local ray index, monotone in the global one; b_ord bits
+// of the order), so the radix sort makes only the passes it must
+__global__ void capture_keys_kernel(const Capture* __restrict__ caps, int64_t n, int b_ray, int b_ord,
                                     unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Capture c = caps[i];
-  const uint64_t k = static_cast<uint64_t>(global_ray(p, c.ray));
+  const uint64_t k = static_cast<uint64_t>(c.ray);
   const uint64_t order = static_cast<uint32_t>(c.meta) >> 8;
   const uint64_t recv = c.meta & 0xff;
-  keys[i] = (recv << 56) | (k << 20) | order;
+  keys[i] = (((recv << b_ray) | k) << b_ord) | order;
   idx[i] = static_cast<int32_t>(i);
 }
 
@@ -956,18 +959,26 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   res->c_off.alloc(nc + 1, st);
   if (nc > 0) {
     const unsigned g = static_cast<unsigned>((nc + 255) / 256);
-    capture_keys_kernel<<<g, 256, 0, st>>>(caps.p, nc, p, keys.p, idx.p);
+    auto bits = [](int64_t v) {  // bits to hold 0..v
+      int b = 0;
+      while (b < 63 && (int64_t(1) << b) <= v) ++b;
+      return b;
+    };
+    const int b_ray = bits(count - 1), b_ord = bits(std::max<int64_t>(cfg->max_iterations, 1)),
+              b_rec = bits(n_recv - 1);
+    const int end_bit = std::min(64, b_rec + b_ray + b_ord);
+    capture_keys_kernel<<<g, 256, 0, st>>>(caps.p, nc, b_ray, b_ord, keys.p, idx.p);
     RR_LAUNCH_CHECK();
     s->ctx->launches++;
     int32_t* order_idx = idx.p;
     if (sort) {
       size_t tb = 0;
       RR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_o.p, idx.p, idx_o.p, static_cast<int>(nc),
-                                              0, 64, st));
+                                              0, end_bit, st));
       DevBuf<uint8_t> tmp;
       tmp.alloc(tb, st);
       RR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_o.p, idx.p, idx_o.p, static_cast<int>(nc), 0,
-                                              64, st));
+                                              end_bit, st));
       s->ctx->launches += 4;
       order_idx = idx_o.p;
     }
