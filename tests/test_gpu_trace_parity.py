@@ -165,3 +165,30 @@ def test_trace_multi_receiver_and_subset(ctx, port):
                                686.0, first=3, stride=97, count=0)
     assert res.ray_bounces == ost.ray_bounces
     _compare_captures(res.captures, oc)
+
+
+@pytest.mark.parametrize("offset,scale", [((1000.0, -2000.0, 500.0), 1.0), ((0.0, 0.0, 0.0), 1e-3),
+                                          ((-3.0e4, 1.0e4, 2.0e3), 1.0), ((0.0, 0.0, 0.0), 250.0)])
+def test_trace_far_and_scaled_scenes(ctx, port, offset, scale):
+    """The conservative fp32 box filter (eps = scale * 2^-19 of the largest
+    coordinate, rr_geom.cuh) at other magnitudes: C1 moved 30 km off the
+    origin, shrunk to 8 mm, blown up to 2 km — the captures stay
+    bit-identical to the fp64 reference."""
+    s = scenes.config1()
+    v = s.vertices * scale + np.asarray(offset)
+    src = tuple(np.asarray(s.source) * scale + np.asarray(offset))
+    recvs = [(tuple(np.asarray(c) * scale + np.asarray(offset)), r * scale) for c, r in s.receivers]
+    res, oc, ost = _trace_both(ctx, port, v, s.faces, s.absorption, src, 4000, recvs, s.max_iterations,
+                               s.max_range * scale)
+    assert res.ray_bounces == ost.ray_bounces and len(oc) > 0
+    _compare_captures(res.captures, oc)
+
+
+def test_trace_soup_interior_rays(ctx, port):
+    """An unstructured soup (overlapping boxes, no planes to cull) with rays
+    from inside it: 20 000 rays, 30 bounces, escapes."""
+    v, f, a = scenes.random_soup(424242, 20000, 10.0, 0.6)
+    a = np.full_like(a, 0.05)
+    res, oc, ost = _trace_both(ctx, port, v, f, a, (5.0, 5.0, 5.0), 20000, [((4.0, 6.0, 5.5), 0.7)], 30, 200.0)
+    assert res.escaped == ost.escaped and res.ray_bounces == ost.ray_bounces
+    _compare_captures(res.captures, oc)
