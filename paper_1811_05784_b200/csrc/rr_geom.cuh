@@ -260,13 +260,19 @@ struct RegRay {  // ray held in registers
 
 // CNT: count internal-node visits and leaf tests into *cnt (instrumented build)
 // UNR: internal nodes a lane may process per vote round (amortises the votes)
+__device__ __forceinline__ int mt32(const float4* __restrict__ tri32, int32_t f, const RayF& r, float dx, float dy,
+                                    float dz, float S, float* tlo, float* tup);
+
 // SMS: the bottom SMS stack entries live in shared memory (sst: this
-// thread's column, stride 128), the rest in local memory
-template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1, int SMS = 0>  // STUCKT < 0: >= 1/|STUCKT| of lanes
+// thread's column, stride 128), the rest in local memory.  F32L: a batched
+// leaf first goes through the conservative fp32 classification (mt32) and
+// only leaves it cannot reject run the fp64 test.
+template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1, int SMS = 0,
+          bool F32L = false>  // STUCKT < 0: >= 1/|STUCKT| of lanes
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
                                                     int32_t rplane, unsigned long long* cnt = nullptr,
-                                                    int2* sst = nullptr) {
+                                                    int2* sst = nullptr, const float4* __restrict__ tri32 = nullptr) {
   HitResult best{0.0, -1};
   RayF r;
   if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
@@ -344,11 +350,20 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       if (leaf != 0) {
         const int32_t f = ~leaf;
         if (CNT) ++cnt[1];
-        const double t = mt_delta(tri, f, ray.org(), ray.dir());
-        if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
-          best.delta = t;
-          best.face = f;
-          tbest = prune_bound(t, r.shift);
+        bool test = true;
+        if (F32L) {
+          const D3 dd = ray.dir();
+          float lo, up;
+          test = mt32(tri32, f, r, __double2float_rn(dd.x), __double2float_rn(dd.y), __double2float_rn(dd.z),
+                      h.eps * 0x1p19f, &lo, &up) != 0;
+        }
+        if (test) {
+          const double t = mt_delta(tri, f, ray.org(), ray.dir());
+          if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+            best.delta = t;
+            best.face = f;
+            tbest = prune_bound(t, r.shift);
+          }
         }
         leaf = 0;
         if (node < 0) {  // the leaf that waited for the slot

@@ -48,7 +48,8 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
-template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1, int SMS = 0>
+template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1, int SMS = 0,
+          bool F32L = false>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   __shared__ int2 s_stack[SMS > 0 ? SMS * 128 : 1];  // bottom of the traversal stacks (SMS > 0)
@@ -119,8 +120,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     } else if (V == 3) {
       wall = closest_hit4_pl<16, -2, RegRay, UNR>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane, st_cnt,
-                                                            s_stack + threadIdx.x);
+      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS, F32L>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane,
+                                                                  st_cnt, s_stack + threadIdx.x, p.tri32);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
     } else {
@@ -867,6 +868,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 34) dfk = trace_kernel<1, 8, false, 16, -2, false, 2>;  // 2 / 4 internal nodes per vote round
   if (df == 35) dfk = trace_kernel<1, 8, false, 16, -2, false, 4>;
   if (df == 36) dfk = trace_kernel<1, 8, false, 16, -2, false, 8>;
+  if (df == 46) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, true>;  // fp32 leaf prefilter (C2 +3 %)
   if (df == 37) dfk = trace_kernel<1, 8, false, 16, -2, false, 16>;
   if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
   if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
