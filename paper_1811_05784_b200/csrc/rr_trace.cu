@@ -574,52 +574,55 @@ __global__ void capture_len_kernel(const Capture* __restrict__ caps, const int32
 
 // Sorted SoA captures + face paths + band multipliers (the ordered product
 // of (1 - alpha), tracer.cpp:57-58).
+// Materialise the sorted captures: 8 lanes per capture, lane b rebuilds band
+// b's multiplier as the ordered product of (1 - alpha) over the face history
+// (tracer.cpp:57-58, the same bits as the running product) and copies every
+// 8th history entry; lane 0 writes the fixed fields.
 __global__ void capture_out_kernel(const Capture* __restrict__ caps, const int32_t* __restrict__ idx, int64_t n,
                                    TraceParams p, const int32_t* __restrict__ mat, const double* __restrict__ oma,
                                    const int64_t* __restrict__ off, int32_t* __restrict__ o_recv,
                                    int32_t* __restrict__ o_ray, double* __restrict__ o_point,
                                    double* __restrict__ o_dir, double* __restrict__ o_path,
                                    double* __restrict__ o_mult, int32_t* __restrict__ o_hist) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = g >> 3;
+  const int b = static_cast<int>(g & 7);
   if (i >= n) return;
-  const Capture c = caps[idx[i]];
-  const int32_t order = static_cast<uint32_t>(c.meta) >> 8;
-  o_recv[i] = c.meta & 0xff;
-  o_ray[i] = static_cast<int32_t>(global_ray(p, c.ray));
-  for (int k = 0; k < 3; ++k) {
-    o_point[3 * i + k] = c.p[k];
-    o_dir[3 * i + k] = c.d[k];
+  const Capture& c = caps[idx[i]];
+  const int32_t meta = c.meta;
+  const int32_t order = static_cast<uint32_t>(meta) >> 8;
+  const int32_t ray = c.ray;
+  if (b == 0) {
+    o_recv[i] = meta & 0xff;
+    o_ray[i] = static_cast<int32_t>(global_ray(p, ray));
+    o_path[i] = c.path;
   }
-  o_path[i] = c.path;
-  double m[kBands];
-  for (int b = 0; b < kBands; ++b) m[b] = 1.0;
-  const int32_t* h = p.hist + static_cast<int64_t>(c.ray) * p.H;
+  if (b < 3) {
+    o_point[3 * i + b] = c.p[b];
+    o_dir[3 * i + b] = c.d[b];
+  }
+  const int32_t* h = p.hist + static_cast<int64_t>(ray) * p.H;
   const int64_t base = off[i];
-  // the product stays in path order (tracer.cpp:57-58); the history, material
-  // and (1 - alpha) loads of 8 bounces go out together
+  const int g0 = threadIdx.x & 24;              // first lane of this capture's group of 8
+  const unsigned gm = 0xffu << g0;              // the group runs its loops in lockstep
+  double m = 1.0;
   int j = 0;
   for (; j + 8 <= order; j += 8) {
-    int32_t f[8], mt[8];
+    const int32_t mine = h[j + b];  // each lane fetches one of the next 8 faces
+    o_hist[base + j + b] = mine;
+    const int32_t mt = mat[mine];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) f[u] = h[j + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      o_hist[base + j + u] = f[u];
-      mt[u] = mat[f[u]];
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const double* a = oma + kBands * mt[u];
-      for (int b = 0; b < kBands; ++b) m[b] *= a[b];
-    }
+    for (int u = 0; u < 8; ++u) m *= oma[kBands * __shfl_sync(gm, mt, g0 + u) + b];
   }
-  for (; j < order; ++j) {
-    const int32_t f = h[j];
-    o_hist[base + j] = f;
-    const double* a = oma + kBands * mat[f];
-    for (int b = 0; b < kBands; ++b) m[b] *= a[b];
+  const int rest = order - j;
+  int32_t mt = 0;
+  if (b < rest) {
+    const int32_t f = h[j + b];
+    o_hist[base + j + b] = f;
+    mt = mat[f];
   }
-  for (int b = 0; b < kBands; ++b) o_mult[kBands * i + b] = m[b];
+  for (int u = 0; u < rest; ++u) m *= oma[kBands * __shfl_sync(gm, mt, g0 + u) + b];
+  o_mult[kBands * i + b] = m;
 }
 
 // ---------------------------------------------------------------- queries
@@ -1004,7 +1007,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     res->c_path.alloc(nc, st);
     res->c_mult.alloc(kBands * nc, st);
     res->c_hist.alloc(std::max<int64_t>(total, 1), st);
-    capture_out_kernel<<<g, 256, 0, st>>>(caps.p, order_idx, nc, p, s->mat.p, s->oma.p, res->c_off.p,
+    capture_out_kernel<<<static_cast<unsigned>((8 * nc + 255) / 256), 256, 0, st>>>(
+        caps.p, order_idx, nc, p, s->mat.p, s->oma.p, res->c_off.p,
                                            res->c_recv.p, res->c_ray.p, res->c_point.p, res->c_dir.p,
                                            res->c_path.p, res->c_mult.p, res->c_hist.p);
     RR_LAUNCH_CHECK();
