@@ -268,7 +268,7 @@ __device__ __forceinline__ int mt32(const float4* __restrict__ tri32, int32_t f,
 // leaf first goes through the conservative fp32 classification (mt32) and
 // only leaves it cannot reject run the fp64 test.
 template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1, int SMS = 0,
-          bool F32L = false>  // STUCKT < 0: >= 1/|STUCKT| of lanes
+          bool F32L = false, int TOS = 0>  // STUCKT < 0: >= 1/|STUCKT| of lanes; TOS: newest entries in registers (0-2)
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
                                                     int32_t rplane, unsigned long long* cnt = nullptr,
@@ -287,6 +287,8 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   }
   int2 st[kStack - SMS];
   int sp = 0;
+  int2 top[TOS > 0 ? TOS : 1];  // TOS: the newest entries (top[0] newest), kept out of local memory
+  int n_top = 0;
   int32_t leaf = 0;  // stashed leaf (< 0) or 0
   if (node < 0 && node != kDone) {  // one-face scene: the root is a leaf
     leaf = node;
@@ -294,6 +296,16 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   }
   auto pop = [&]() {
     node = kDone;
+    while (TOS > 0 && n_top > 0) {
+      const int2 e = top[0];
+#pragma unroll
+      for (int k = 0; k + 1 < TOS; ++k) top[k] = top[k + 1];
+      --n_top;
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        return;
+      }
+    }
     while (sp > 0) {
       --sp;
       const int2 e = (SMS > 0 && sp < SMS) ? sst[sp * 128] : st[sp - SMS];
@@ -318,9 +330,17 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       if (hl && hr) {
         const bool lf = tl <= tr;
         const int2 e = make_int2(lf ? dd.y : dd.x, __float_as_int(lf ? tr : tl));
-        if (SMS > 0 && sp < SMS) sst[sp * 128] = e;
-        else st[sp - SMS] = e;
-        ++sp;
+        if (TOS > 0) {
+          if (n_top == TOS) st[sp++] = top[TOS - 1];  // the oldest register entry spills
+#pragma unroll
+          for (int k = TOS - 1; k > 0; --k) top[k] = top[k - 1];
+          top[0] = e;
+          n_top = min(n_top + 1, TOS);
+        } else {
+          if (SMS > 0 && sp < SMS) sst[sp * 128] = e;
+          else st[sp - SMS] = e;
+          ++sp;
+        }
         node = lf ? dd.x : dd.y;
       } else if (hl) {
         node = dd.x;
