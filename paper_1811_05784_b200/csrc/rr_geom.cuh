@@ -287,7 +287,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   }
   int2 st[kStack - SMS];
   int sp = 0;
-  int2 top[TOS > 0 ? TOS : 1];  // TOS: the newest entries (top[0] newest), kept out of local memory
+  int2 top[TOS > 0 ? TOS : 1] = {};  // TOS: the newest entries (top[0] newest), kept out of local memory
   int n_top = 0;
   int32_t leaf = 0;  // stashed leaf (< 0) or 0
   if (node < 0 && node != kDone) {  // one-face scene: the root is a leaf
@@ -402,7 +402,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
 // are ordered by entry distance, the nearest taken next and the others
 // pushed (leaves included, so a popped entry may be a leaf); coplanar slots
 // culled via QNode.pad; same postponed, warp-batched leaf tests.
-template <int LEAFT, int STUCKT, typename RAY, int UNR = 1>
+template <int LEAFT, int STUCKT, typename RAY, int UNR = 1, int TOS = 0>
 __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const QNode* __restrict__ q4,
                                                      int32_t root4, const FaceTri* __restrict__ tri,
                                                      const RAY& ray, int32_t rplane) {
@@ -420,9 +420,32 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
   }
   int2 st[kStack4];
   int sp = 0;
+  int2 top[TOS > 0 ? TOS : 1] = {};  // TOS: the newest entries in registers (top[0] newest)
+  int n_top = 0;
   int32_t leaf = 0;
+  auto push = [&](int2 e) {
+    if (TOS > 0) {
+      if (n_top == TOS) st[sp++] = top[TOS - 1];
+#pragma unroll
+      for (int k = TOS - 1; k > 0; --k) top[k] = top[k - 1];
+      top[0] = e;
+      n_top = min(n_top + 1, TOS);
+    } else {
+      st[sp++] = e;
+    }
+  };
   auto pop = [&]() {
     node = kDone;
+    while (TOS > 0 && n_top > 0) {
+      const int2 e = top[0];
+#pragma unroll
+      for (int k = 0; k + 1 < TOS; ++k) top[k] = top[k + 1];
+      --n_top;
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        return;
+      }
+    }
     while (sp > 0) {
       --sp;
       const int2 e = st[sp];
@@ -465,9 +488,9 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
       cx(t1, c1, t3, c3);
       cx(t1, c1, t2, c2);
       // push the far hits (descending), continue with the nearest
-      if (t3 != kInf) st[sp++] = make_int2(c3, __float_as_int(t3));
-      if (t2 != kInf) st[sp++] = make_int2(c2, __float_as_int(t2));
-      if (t1 != kInf) st[sp++] = make_int2(c1, __float_as_int(t1));
+      if (t3 != kInf) push(make_int2(c3, __float_as_int(t3)));
+      if (t2 != kInf) push(make_int2(c2, __float_as_int(t2)));
+      if (t1 != kInf) push(make_int2(c1, __float_as_int(t1)));
       if (t0 != kInf) {
         node = c0;
       } else {

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 3) {
-      wall = closest_hit4_pl<16, -2, RegRay, UNR>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
+      wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
       wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS, F32L, TOS>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane,
                                                                   st_cnt, s_stack + threadIdx.x, p.tri32);
