@@ -852,8 +852,9 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // dependent node fetches (C3 -15 %, C5 -8 %; C2 100k +8 %, so not there)
   // (binary default: up to 16 internal nodes per lane between leaf votes,
   // C1 0.46 -> 0.36 ms, C2 12.67 -> 12.20 ms against one per vote; the two
-  // newest stack entries in registers, C2 12.20 -> 11.68 ms)
-  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 48);
+  // newest stack entries in registers, C2 12.20 -> 11.68 ms; a 72-register
+  // budget, 11.62 ms)
+  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 54);
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
@@ -875,13 +876,14 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 46) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, true>;  // fp32 leaf prefilter (C2 +3 %)
   if (df == 47) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, false, 1>;  // top entry in registers
   if (df == 48) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, false, 2>;  // two top entries
+  if (df == 54) dfk = trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2>;  // 72-register budget
   if (df == 37) dfk = trace_kernel<1, 8, false, 16, -2, false, 16>;
   if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
   if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
   if (df == 32) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 16>;
   if (df == 23 && s->s4nodes.p) dfk = trace_kernel<3, 8>;
   if (df == 24 && s->s4nodes.p) dfk = trace_kernel<3, 6>;
-  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 8, false, 16, -2, true, 16, 0, false, 2>;  // counts of the default
+  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2>;  // counts of the default
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
