@@ -268,7 +268,7 @@ __device__ __forceinline__ int mt32(const float4* __restrict__ tri32, int32_t f,
 // leaf first goes through the conservative fp32 classification (mt32) and
 // only leaves it cannot reject run the fp64 test.
 template <int LEAFT, int STUCKT = 1, typename RAY = RegRay, bool CNT = false, int UNR = 1, int SMS = 0,
-          bool F32L = false, int TOS = 0>  // STUCKT < 0: >= 1/|STUCKT| of lanes; TOS: newest entries in registers (0-2)
+          bool F32L = false, int TOS = 0, bool PFL = true>  // STUCKT < 0: >= 1/|STUCKT| of lanes; TOS: newest entries in registers (0-2); PFL: prefetch stashed leaves
 __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const TNode* __restrict__ nodes,
                                                     const FaceTri* __restrict__ tri, const RAY& ray,
                                                     int32_t rplane, unsigned long long* cnt = nullptr,
@@ -351,7 +351,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       }
       if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
         leaf = node;
-        prefetch_l1(tri + ~leaf);
+        if (PFL) prefetch_l1(tri + ~leaf);
         pop();
       }
     }
@@ -388,7 +388,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
         leaf = 0;
         if (node < 0) {  // the leaf that waited for the slot
           leaf = node;
-          prefetch_l1(tri + ~leaf);
+          if (PFL) prefetch_l1(tri + ~leaf);
           pop();
         }
       }

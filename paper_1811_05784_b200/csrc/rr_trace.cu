@@ -49,7 +49,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 // V = 1: binary nodes, fp64 test at every leaf (default)
 // V = 2: 4-wide nodes, fp64 test at every leaf (diagnostic)
 template <int V, int MINB, bool PF = false, int PL = 0, int ST = 1, bool CNT = false, int UNR = 1, int SMS = 0,
-          bool F32L = false, int TOS = 0>
+          bool F32L = false, int TOS = 0, bool PFL = true>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
   constexpr bool WIDE = V == 2;
   __shared__ int2 s_stack[SMS > 0 ? SMS * 128 : 1];  // bottom of the traversal stacks (SMS > 0)
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     } else if (V == 3) {
       wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
-      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS, F32L, TOS>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane,
+      wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS, F32L, TOS, PFL>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane,
                                                                   st_cnt, s_stack + threadIdx.x, p.tri32);
     } else if (V == 1) {
       wall = closest_hit<PF>(p.hdr, p.nodes, smem_nodes, K, p.tri, o, d, nullptr, rplane);
@@ -853,8 +853,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // (binary default: up to 16 internal nodes per lane between leaf votes,
   // C1 0.46 -> 0.36 ms, C2 12.67 -> 12.20 ms against one per vote; the two
   // newest stack entries in registers, C2 12.20 -> 11.68 ms; a 72-register
-  // budget, 11.62 ms)
-  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 54);
+  // budget, 11.62 ms; no L1 prefetch of stashed leaves, 11.53 ms)
+  const int df = df_env >= 0 ? df_env : (s->nf >= (1 << 18) && s->s4nodes.p ? 23 : 59);
   auto dfk = df == 2 ? trace_kernel_df<8, 16, 8, true> : df == 3 ? trace_kernel_df<8, 16, 10, true>
            : df == 4 ? trace_kernel_df<8, 16, 12, true> : df == 5 ? trace_kernel_df<16, 16, 10, true>
            : df == 6 ? trace_kernel_df<4, 16, 10, true> : trace_kernel_df<8, 16, 8, false>;
@@ -877,13 +877,14 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (df == 47) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, false, 1>;  // top entry in registers
   if (df == 48) dfk = trace_kernel<1, 8, false, 16, -2, false, 16, 0, false, 2>;  // two top entries
   if (df == 54) dfk = trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2>;  // 72-register budget
+  if (df == 59) dfk = trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;  // no leaf prefetch
   if (df == 37) dfk = trace_kernel<1, 8, false, 16, -2, false, 16>;
   if (df == 30) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 4>;   // shared-memory stack bottom
   if (df == 31) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 8>;
   if (df == 32) dfk = trace_kernel<1, 8, false, 16, -2, false, 1, 16>;
   if (df == 23 && s->s4nodes.p) dfk = trace_kernel<3, 8>;
   if (df == 24 && s->s4nodes.p) dfk = trace_kernel<3, 6>;
-  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2>;  // counts of the default
+  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;  // counts of the default
   auto kernel = variant == 0 ? (df ? dfk : fast) : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
