@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128, 8) step_kernel(const StepParams p) {
       }
     }
   } else {
-    wall = closest_hit_pl<16, -2, RegRay>(p.hdr, p.nodes, p.tri, RegRay{o, d}, -2);
+    wall = closest_hit_pl<16, -2, RegRay>(p.hdr, p.nodes, p.tri, RegRay{o, d}, -2);  // (the tracer's 16-node / register-stack tuning is slower here: one query per thread)
   }
   const int32_t nh = p.n_hist[i];
   const double sd = sphere_delta(o, d, d3(p.rc[0], p.rc[1], p.rc[2]), p.rr);
