@@ -84,7 +84,7 @@ __device__ __forceinline__ float inv_dir(double dk) {
   float f = __double2float_rn(dk);
   float a = fabsf(f);
   if (a < 1e-30f) f = copysignf(1e-30f, dk);
-  return 1.0f / f;
+  return __frcp_rn(f);  // correctly rounded, as 1.0f / f
 }
 
 // Origins farther than 4*scale from 0 are moved (in fp64) to the root box
