@@ -32,6 +32,8 @@ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
 
 constexpr int32_t kPop = 0x7fffffff;
 constexpr int32_t kDone = 0x7ffffffe;
+// an internal node to visit (not a leaf, not kDone / kPop): one unsigned compare
+__device__ __forceinline__ bool is_inner(int32_t n) { return static_cast<uint32_t>(n) < static_cast<uint32_t>(kDone); }
 constexpr int kStack = 32;   // BVH2: one push per level, depth <= 30
 constexpr int kStack4 = 48;  // 4-wide: <= 3 pushes per level, depth <= 15
 
@@ -317,7 +319,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
   };
   while (node != kDone || leaf != 0) {
 #pragma unroll 1
-    for (int u = 0; u < UNR && node >= 0 && node != kDone && (u == 0 || leaf == 0); ++u) {
+    for (int u = 0; u < UNR && is_inner(node) && (u == 0 || leaf == 0); ++u) {
       if (CNT) ++cnt[0];
       const float4* q = reinterpret_cast<const float4*>(nodes + node);
       const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -360,7 +362,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     const unsigned act = __activemask();
     const unsigned hv = __ballot_sync(act, leaf != 0);
     if (hv == 0) continue;
-    const bool can = node >= 0 && node != kDone;
+    const bool can = is_inner(node);
     const bool must = leaf != 0 && !can;
     const unsigned mv = __ballot_sync(act, must);
     const unsigned cv = __ballot_sync(act, can);
