@@ -9,8 +9,9 @@
 //
 // Differences from the reference, all outside the hot path:
 //  * Vec3 is {x, y, z} with operator[]; BandArray is std::array<double, 8>.
-//  * AccelTree holds the device scene; its reference-layout node table is
-//    downloaded on first use through nodes() (a method, not a field).
+//  * AccelTree holds the device scene (traversed through a device SAH tree);
+//    its reference-layout median tree is built and downloaded on first use
+//    through nodes() (a method, not a field).
 //  * Hit carries delta, point and face_index (lambda / mu are not reported).
 //  * RoomImpulseResponse additionally holds the 8 per-band responses.
 //  * step() takes std::vector<Ray>& (the reference takes std::span<Ray>);
