@@ -92,7 +92,8 @@ class TriangleMesh:
 
 
 class AccelTree:
-    """Device scene + median-split tree (rr_scene)."""
+    """Device scene (rr_scene): faces, a device SAH traversal tree, and the
+    reference-layout median-split tree, built on first use of nodes()."""
 
     def __init__(self, mesh: TriangleMesh, ctx: Context | None = None, validate: bool = True):
         self.ctx = ctx or Context.default()
@@ -140,7 +141,7 @@ class AccelTree:
 
 
 def build_tree(mesh: TriangleMesh, ctx: Context | None = None, validate: bool = True) -> AccelTree:
-    """build_tree (accel_tree.hpp:38): device median-split build."""
+    """build_tree (accel_tree.hpp:38): the device scene and its trees."""
     return AccelTree(mesh, ctx, validate)
 
 
