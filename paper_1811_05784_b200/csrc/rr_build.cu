@@ -345,50 +345,54 @@ __device__ __forceinline__ int flat_axis(const double* lo, const double* hi) {
   return -1;
 }
 
-__global__ void plane_key_kernel(const double* __restrict__ fb, int64_t nf, int axis,
-                                 unsigned long long* __restrict__ keys) {
+// Axis-aligned plane ids: the flat faces' plane coordinates go into one
+// open-addressing hash table per axis (size T, a power of two, ~0 = empty);
+// a plane's id is (axis << 29) | its slot.  Ids are only compared for
+// equality (coplanar culling), so no order is needed.
+__device__ __forceinline__ uint64_t plane_slot0(uint64_t key, uint64_t mask) {
+  key ^= key >> 33;
+  key *= 0xff51afd7ed558ccdull;
+  key ^= key >> 33;
+  return key & mask;
+}
+
+__global__ void plane_insert_kernel(const double* __restrict__ fb, int64_t nf, unsigned long long* __restrict__ table,
+                                    int64_t T) {
   const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const int k = flat_axis(fb + 6 * f, fb + 6 * f + 3);
-  keys[f] = k == axis ? ord_key(fb[6 * f + k]) : ~0ull;
-}
-
-__device__ __forceinline__ int32_t plane_lookup(const unsigned long long* __restrict__ table,
-                                                const int64_t* __restrict__ off, int k, double c) {
-  const unsigned long long key = ord_key(c);
-  int64_t lo = off[2 * k], hi = off[2 * k + 1];  // axis k's sorted unique planes: [off[2k], off[2k+1])
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (table[mid] < key) lo = mid + 1; else hi = mid;
+  if (k < 0) return;
+  const unsigned long long key = ord_key(fb[6 * f + k]);
+  unsigned long long* t = table + k * T;
+  for (uint64_t h = plane_slot0(key, T - 1);; h = (h + 1) & (T - 1)) {
+    const unsigned long long prev = atomicCAS(t + h, ~0ull, key);
+    if (prev == ~0ull || prev == key) return;
   }
-  if (lo < off[2 * k + 1] && table[lo] == key) return static_cast<int32_t>((k << 29) | (lo - off[2 * k]));
-  return -1;
 }
 
-// per-axis table ranges from the unique counts; the "not flat on k"
-// sentinel (~0) sorts last and is dropped
-__global__ void plane_range_kernel(const unsigned long long* __restrict__ table, const int* __restrict__ num,
-                                   int64_t nf, int64_t* __restrict__ off) {
-  const int k = threadIdx.x;
-  if (k >= 3) return;
-  int64_t n = num[k];
-  if (n > 0 && table[k * nf + n - 1] == ~0ull) --n;
-  off[2 * k] = k * nf;
-  off[2 * k + 1] = k * nf + n;
+__device__ __forceinline__ int32_t plane_lookup(const unsigned long long* __restrict__ table, int64_t T, int k,
+                                                double c) {
+  const unsigned long long key = ord_key(c);
+  const unsigned long long* t = table + k * T;
+  for (uint64_t h = plane_slot0(key, T - 1);; h = (h + 1) & (T - 1)) {
+    const unsigned long long v = t[h];
+    if (v == key) return static_cast<int32_t>((k << 29) | static_cast<int32_t>(h));
+    if (v == ~0ull) return -1;
+  }
 }
 
 __global__ void face_plane_kernel(const double* __restrict__ fb, int64_t nf,
-                                  const unsigned long long* __restrict__ table, const int64_t* __restrict__ off,
+                                  const unsigned long long* __restrict__ table, int64_t T,
                                   int32_t* __restrict__ face_plane) {
   const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const int k = flat_axis(fb + 6 * f, fb + 6 * f + 3);
-  face_plane[f] = k < 0 ? -1 : plane_lookup(table, off, k, fb[6 * f + k]);
+  face_plane[f] = k < 0 ? -1 : plane_lookup(table, T, k, fb[6 * f + k]);
 }
 
 __global__ void node_plane_kernel(const RefNode* __restrict__ ref, const int32_t* __restrict__ tidx,
                                   int64_t n_nodes, const unsigned long long* __restrict__ table,
-                                  const int64_t* __restrict__ off, TNode* __restrict__ tn) {
+                                  int64_t T, TNode* __restrict__ tn) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n_nodes || ref[i].face >= 0) return;
   int32_t pl[2];
@@ -396,7 +400,7 @@ __global__ void node_plane_kernel(const RefNode* __restrict__ ref, const int32_t
   for (int s = 0; s < 2; ++s) {
     const RefNode& c = ref[kids[s]];
     const int k = flat_axis(c.lo, c.hi);
-    pl[s] = k < 0 ? -1 : plane_lookup(table, off, k, c.lo[k]);
+    pl[s] = k < 0 ? -1 : plane_lookup(table, T, k, c.lo[k]);
   }
   tn[tidx[i]].d.z = pl[0];
   tn[tidx[i]].d.w = pl[1];
@@ -522,39 +526,23 @@ void build_scene_tree(rr_scene* s) {
     RR_LAUNCH_CHECK();
     s->ctx->launches++;
   }
-  // ---- axis-aligned plane tables: per axis, the sorted unique plane
-  // coordinates of the flat faces; ids for faces and for tree children
+  // ---- axis-aligned plane ids: one hash table of plane coordinates per
+  // axis; ids for faces (here) and for tree children (reference tree)
   DevBuf<unsigned long long>& table = s->plane_table;
-  DevBuf<int64_t>& doff = s->plane_off;
   {
-    DevBuf<unsigned long long> pkeys, psorted;
-    DevBuf<int> dnum;
-    DevBuf<uint8_t> ptmp;
-    pkeys.alloc(nf, st);
-    psorted.alloc(nf, st);
-    table.alloc(3 * nf, st);
-    doff.alloc(6, st);
-    dnum.alloc(3, st);
-    size_t need = 0, need2 = 0;
-    RR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-    RR_CUDA(cub::DeviceSelect::Unique(nullptr, need2, psorted.p, table.p, dnum.p, static_cast<int>(nf), st));
-    ptmp.alloc(std::max(need, need2), st);
-    for (int k = 0; k < 3; ++k) {  // axis k's unique planes at table + k * nf
-      plane_key_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, k, pkeys.p);
-      RR_LAUNCH_CHECK();
-      size_t t = ptmp.n;
-      RR_CUDA(cub::DeviceRadixSort::SortKeys(ptmp.p, t, pkeys.p, psorted.p, static_cast<int>(nf), 0, 64, st));
-      t = ptmp.n;
-      RR_CUDA(cub::DeviceSelect::Unique(ptmp.p, t, psorted.p, table.p + k * nf, dnum.p + k, static_cast<int>(nf), st));
-      s->ctx->launches += 6;
-    }
-    plane_range_kernel<<<1, 32, 0, st>>>(table.p, dnum.p, nf, doff.p);
+    int64_t T = 1024;
+    while (T < 2 * nf) T <<= 1;  // load factor <= 1/2 per axis
+    if (T > (int64_t(1) << 29)) invalid("too many faces for 29-bit plane slots");
+    s->plane_T = T;
+    table.alloc(3 * T, st);
+    RR_CUDA(cudaMemsetAsync(table.p, 0xff, table.bytes(), st));
+    plane_insert_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, T);
+    RR_LAUNCH_CHECK();
     s->face_plane.alloc(nf, st);
-    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, doff.p, s->face_plane.p);
+    face_plane_kernel<<<grid_for(nf), 256, 0, st>>>(fb.p, nf, table.p, T, s->face_plane.p);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 2;
   }
-
   tm.mark("build: plane tables");
   build_sah_tree(s, st);
   tm.mark("build: SAH tree");
@@ -696,7 +684,7 @@ void ensure_reference_tree(rr_scene* s) {
   }
 
   tm.mark("reference tree: levels");
-  node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, s->plane_table.p, s->plane_off.p,
+  node_plane_kernel<<<grid_for(2 * nf - 1), 256, 0, st>>>(s->ref.p, ntidx.p, 2 * nf - 1, s->plane_table.p, s->plane_T,
                                                          s->tnodes.p);
   RR_LAUNCH_CHECK();
   s->ctx->launches++;

@@ -178,8 +178,8 @@ struct rr_scene {
   int32_t sah_depth = 0;
   int64_t n_qnodes = 0;
   rr::DevBuf<rr::TravHeader> dhdr;
-  rr::DevBuf<unsigned long long> plane_table;  // sorted unique axis-aligned plane coordinates
-  rr::DevBuf<int64_t> plane_off;               // per-axis offsets into plane_table (4)
+  rr::DevBuf<unsigned long long> plane_table;  // 3 hash tables of axis-aligned plane coordinates
+  int64_t plane_T = 0;                          // slots per axis table
   bool ref_built = false;         // reference tree (ref, tnodes, qnodes, hdr) built on first use
   rr::TravHeader hdr{};
   int32_t root = -1, depth = 0, K = 0;
