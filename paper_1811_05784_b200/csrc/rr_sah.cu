@@ -566,8 +566,14 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* 
                                const int32_t* __restrict__ seg_axis, const int64_t* __restrict__ seg_nl,
                                const int32_t* __restrict__ rank, const int32_t* __restrict__ perm,
                                const int32_t* __restrict__ fl, const int32_t* __restrict__ scan, int64_t nf,
-                               int32_t* __restrict__ perm_out, int32_t* __restrict__ pos_seg_out) {
+                               int32_t* __restrict__ perm_out, int32_t* __restrict__ pos_seg_out,
+                               LevelState* __restrict__ ls, int64_t* __restrict__ s_out) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g == 0) {  // end of the level (nothing in this kernel reads ls): the next has 2 n_split segments
+    ls->level_base += static_cast<int32_t>(ls->n_split);
+    ls->S = 2 * ls->n_split;
+    *s_out = ls->S;
+  }
   if (g >= 3 * nf) return;
   const int k = static_cast<int>(g / nf);
   const int64_t i = g - k * nf;
@@ -586,10 +592,18 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* 
   if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
 }
 
+__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level);
+
+// per-segment accumulator reset and the packed split / SAH flags (positions
+// S .. s_max get flag 0 so the scan can run over the level's upper bound)
 __global__ void seg_init_kernel(const LevelState* __restrict__ ls, unsigned long long* __restrict__ bb,
-                                unsigned long long* __restrict__ cb, int32_t* __restrict__ pl) {
+                                unsigned long long* __restrict__ cb, int32_t* __restrict__ pl,
+                                const SSeg* __restrict__ segs, int64_t s_max, int level,
+                                unsigned long long* __restrict__ flags) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= ls->S) return;
+  const int64_t S = ls->S;
+  if (j <= s_max) flags[j] = j < S ? split_flags(segs, j, level) : 0ull;
+  if (j >= S) return;
   for (int k = 0; k < 3; ++k) {  // ordered keys: min from ~0, max from 0
     bb[6 * j + k] = ~0ull;
     bb[6 * j + 3 + k] = 0ull;
@@ -601,22 +615,14 @@ __global__ void seg_init_kernel(const LevelState* __restrict__ ls, unsigned long
 }
 
 // packed flags: split (>= kSmall + 1 faces) << 32 | SAH-eligible
-__global__ void split_flag_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls, int64_t s_max,
-                                  int level, unsigned long long* __restrict__ flags) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t S = ls->S;
-  if (j > s_max) return;
-  if (j >= S) {  // the scan runs over the level's upper bound s_max + 1
-    flags[j] = 0;
-    return;
-  }
+__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level) {
   const int64_t n = segs[j].n;
   const unsigned long long split = n > kSmall ? 1ull : 0ull;  // 2..kSmall: finish_kernel
   // SAH only while the depth budget allows a median finish below
   int lg = 0;
   while ((int64_t(1) << lg) < n) ++lg;
   const unsigned long long sah = (n >= kSahMin && level + 1 + lg + 2 <= kMaxDepth) ? 1ull : 0ull;
-  flags[j] = (split << 32) | sah;
+  return (split << 32) | sah;
 }
 
 __global__ void rank_kernel(const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ ranks,
@@ -643,13 +649,6 @@ __global__ void rank_kernel(const unsigned long long* __restrict__ flags, const 
   }
 }
 
-// end of a level: the next one has 2 * n_split segments, its nodes follow
-__global__ void advance_kernel(LevelState* __restrict__ ls, int64_t* __restrict__ s_out) {
-  if (threadIdx.x) return;
-  ls->level_base += static_cast<int32_t>(ls->n_split);
-  ls->S = 2 * ls->n_split;
-  *s_out = ls->S;
-}
 
 // ---- 4-wide collapse of the SAH tree: every internal node at even depth
 // becomes a QNode whose slots are its grandchildren (or a child leaf); slot
@@ -820,12 +819,11 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
     const int64_t s_max = L == 0 ? 1 : std::min<int64_t>(max_seg, L < 62 ? (int64_t(1) << L) : max_seg);
     const int64_t sah_max = std::min<int64_t>(s_max, max_sah);
     // 1. bounds (one init launch for the per-segment accumulators)
-    seg_init_kernel<<<grid(s_max), 256, 0, st>>>(ls.p, bb.p, cb.p, pl.p);
+    seg_init_kernel<<<grid(s_max + 1), 256, 0, st>>>(ls.p, bb.p, cb.p, pl.p, segs, s_max, L, flags.p);
     bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
     if (L == 0) root_hdr_kernel<<<1, 32, 0, st>>>(bb.p, dh.p);
     // 2. split flags and SAH flags, both ranks from one 64-bit scan
     //    (split flag in the high word, SAH flag in the low word)
-    split_flag_kernel<<<grid(s_max + 1), 256, 0, st>>>(segs, ls.p, s_max, L, flags.p);
     RR_LAUNCH_CHECK();
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, flags.p, franks.p, static_cast<int>(s_max + 1), st);
@@ -853,13 +851,12 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
       return cub::DeviceScan::ExclusiveSum(t, b, fl.p, scan.p, static_cast<int>(3 * nf), st);
     }, tmp, st);
     scatter_kernel<<<grid(3 * nf), 256, 0, st>>>(pos, segs, axis.p, nl.p, srank.p, perm, fl.p, scan.p, nf, perm_o,
-                                                  pos_o);
-    advance_kernel<<<1, 32, 0, st>>>(ls.p, d_next.p + L);
+                                                  pos_o, ls.p, d_next.p + L);
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaMemcpyAsync(h_next + L, d_next.p + L, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     n_ev = L + 1;
     RR_CUDA(cudaEventRecord(lev_ev[L], st));
-    s->ctx->launches += 12;
+    s->ctx->launches += 10;
     std::swap(perm, perm_o);
     std::swap(pos, pos_o);
     std::swap(segs, nsegs);
