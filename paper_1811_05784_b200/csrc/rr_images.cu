@@ -229,7 +229,7 @@ __global__ void gather_retro_kernel(const int32_t* __restrict__ idx, int64_t n, 
   for (int k = 0; k < 3; ++k) rs[3 * i + k] = retro[3 * j + k];
 }
 
-constexpr int64_t kBigGroup = 256;  // groups this large go to group_big_kernel (one block each)
+constexpr int64_t kBigGroup = 64;  // groups this large go to group_big_kernel (one block each)
 
 // split groups: sort by retro point and count the beams (split_group)
 __device__ void split_count(int32_t* idx, int64_t s, int64_t e, const double* retro, int64_t c0, double tol,
@@ -591,7 +591,7 @@ __global__ void claim_start_kernel(const unsigned long long* __restrict__ skeys,
     claim_end[a] = static_cast<int32_t>(q + 1);
 }
 
-constexpr int64_t kBigClaims = 256;  // anchors with this many claims go to merge_big_kernel
+constexpr int64_t kBigClaims = 48;  // anchors with this many claims go to merge_big_kernel
 
 __device__ __forceinline__ void merge_write(ImgTmp t, int64_t i, D3 w, int32_t cnt, const int32_t* anchor_rank,
                                             ImgTmp out, int64_t n_out) {
