@@ -919,6 +919,29 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     prefix_run_flag_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, idx_s.p, dirty.p);
     prefix_run_sort_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, dirty.p, idx_s.p);
     RR_LAUNCH_CHECK();
+    if (tm.on) {  // dirty-run statistics (development)
+      std::vector<unsigned long long> hk(n);
+      std::vector<int32_t> hd(n);
+      RR_CUDA(cudaMemcpyAsync(hk.data(), pk_s.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaMemcpyAsync(hd.data(), dirty.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      int64_t runs = 0, dirty_runs = 0, dirty_elems = 0, max_dirty = 0, max_run = 0;
+      for (int64_t a = 0; a < n;) {
+        int64_t b = a + 1;
+        while (b < n && hk[b] == hk[a]) ++b;
+        ++runs;
+        max_run = std::max(max_run, b - a);
+        if (hd[a]) {
+          ++dirty_runs;
+          dirty_elems += b - a;
+          max_dirty = std::max(max_dirty, b - a);
+        }
+        a = b;
+      }
+      std::fprintf(stderr, "[rr timing] prefix runs %lld (max %lld), dirty %lld with %lld captures (max %lld)\n",
+                   (long long)runs, (long long)max_run, (long long)dirty_runs, (long long)dirty_elems,
+                   (long long)max_dirty);
+    }
     idx = std::move(idx_s);
     ctx->launches += 6;
   } else {
