@@ -633,3 +633,41 @@ def test_condition_range_is_validated():
         with pytest.raises(ValueError):
             rr.air_validate(rr.AirModel(**bad))
     rr.air_validate(rr.AirModel())
+
+
+def test_triangle_intersection_agrees_with_a_direct_linear_solve():
+    """test_geometry.cpp:88-118: 10 000 random triangles in [-1, 1]^3, origins
+    in [-2, 2]^3, half the rays aimed near the centroid; delta against a
+    linear solve of o + t d = a + u e1 + v e2 to 1e-9.  The triangles sit in
+    cells 100 m apart in one mesh, so a ray's own triangle, when hit, is its
+    nearest."""
+    rng = np.random.default_rng(7041)
+    n = 10000
+    tri = rng.uniform(-1.0, 1.0, (n, 3, 3))
+    area = 0.5 * np.linalg.norm(np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]), axis=1)
+    tri = tri[area >= 1e-6]
+    n = len(tri)
+    cell = np.stack(np.unravel_index(np.arange(n), (22, 22, 22)), 1).astype(np.float64) * 100.0
+    o = rng.uniform(-2.0, 2.0, (n, 3))
+    d = _unit(rng, n)
+    aimed = tri.mean(axis=1) + 0.3 * rng.uniform(-1.0, 1.0, (n, 3)) - o
+    even = np.arange(n) % 2 == 0
+    d[even] = aimed[even] / np.linalg.norm(aimed[even], axis=1, keepdims=True)
+    v = (tri + cell[:, None, :]).reshape(-1, 3)
+    f = np.stack([np.arange(n) * 3, np.arange(n) * 3 + 1, np.arange(n) * 3 + 2, np.zeros(n, int)], 1).astype(np.int32)
+    tree = AccelTree(TriangleMesh(v, f, np.zeros((1, 8))))
+    face, delta, point = rr.nearest_hit(tree, o + cell, d)
+    # linear solve per triangle: [d, -e1, -e2] (t, u, v) = a - o
+    e1, e2 = tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]
+    A = np.stack([d, -e1, -e2], 2)
+    sol = np.linalg.solve(A, (tri[:, 0] - o)[..., None])[..., 0]
+    t, uu, vv = sol[:, 0], sol[:, 1], sol[:, 2]
+    slow = (uu >= 0) & (vv >= 0) & (uu + vv <= 1) & (t > 1e-6)
+    own = face == np.arange(n)
+    edge = (np.abs(uu) < 1e-9) | (np.abs(vv) < 1e-9) | (np.abs(uu + vv - 1) < 1e-9) | (np.abs(t - 1e-6) < 1e-9)
+    assert np.all((own == slow) | edge)  # same decision away from the boundaries
+    hit = own & slow
+    assert hit.sum() > 1000
+    assert np.all(np.abs(delta[hit] - t[hit]) <= 1e-9 * np.maximum(1.0, np.abs(t[hit])))
+    assert np.all(np.linalg.norm(point[hit] - (o + cell + delta[:, None] * d)[hit], axis=1)
+                  <= 1e-9 * np.maximum(1.0, delta[hit]))
