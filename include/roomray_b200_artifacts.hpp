@@ -451,6 +451,62 @@ inline void write_wav(const std::string& path, const std::vector<double>& sample
   if (!out) throw std::runtime_error("write failed: " + path);
 }
 
+/// WavData / read_wav (wav.hpp:13-18, wav.cpp:68-115): mono 32-bit float
+/// files as written above; std::runtime_error for anything else.
+struct WavData {
+  std::vector<double> samples;
+  double sample_rate = 0.0;
+};
+
+inline WavData read_wav(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open: " + path);
+  auto u32 = [&]() {
+    unsigned char b[4] = {0, 0, 0, 0};
+    in.read(reinterpret_cast<char*>(b), 4);
+    return static_cast<uint32_t>(b[0] | (b[1] << 8) | (b[2] << 16) | (static_cast<uint32_t>(b[3]) << 24));
+  };
+  auto u16 = [&]() {
+    unsigned char b[2] = {0, 0};
+    in.read(reinterpret_cast<char*>(b), 2);
+    return static_cast<uint16_t>(b[0] | (b[1] << 8));
+  };
+  char tag[5] = {};
+  in.read(tag, 4);
+  if (std::strncmp(tag, "RIFF", 4) != 0) throw std::runtime_error("not a RIFF file: " + path);
+  u32();
+  in.read(tag, 4);
+  if (std::strncmp(tag, "WAVE", 4) != 0) throw std::runtime_error("not a WAVE file: " + path);
+  WavData wav;
+  uint16_t format = 0, channels = 0, bits = 0;
+  while (in.read(tag, 4)) {
+    const uint32_t size = u32();
+    if (std::strncmp(tag, "fmt ", 4) == 0) {
+      format = u16();
+      channels = u16();
+      wav.sample_rate = u32();
+      u32();
+      u16();
+      bits = u16();
+      if (size > 16) in.seekg(size - 16, std::ios::cur);
+    } else if (std::strncmp(tag, "data", 4) == 0) {
+      if (format != 3 || channels != 1 || bits != 32)
+        throw std::runtime_error("unsupported WAV layout (need mono 32-bit float): " + path);
+      const std::size_t count = size / sizeof(float);
+      wav.samples.resize(count);
+      for (std::size_t i = 0; i < count; ++i) {
+        float f = 0.0f;
+        in.read(reinterpret_cast<char*>(&f), 4);
+        wav.samples[i] = f;
+      }
+      return wav;
+    } else {
+      in.seekg(size + (size & 1), std::ios::cur);
+    }
+  }
+  throw std::runtime_error("no data chunk in " + path);
+}
+
 // ------------------------------------------------------------------ decay curves (metrics.hpp)
 struct DecayPoint {
   double time_s = 0.0;
@@ -474,6 +530,50 @@ inline std::array<std::vector<DecayPoint>, kNumBands> schroeder_bands(const Puls
     for (std::size_t i = 0; i < ev.size(); ++i) out[b].push_back({ev[i].time_s, level[off[b] + i]});
   }
   return out;
+}
+
+// ------------------------------------------------------------------ trains and metrics files (pipeline.hpp:84-87)
+/// write_band_trains_csv (pipeline.cpp:516-526): "band,time_s,amplitude".
+inline void write_band_trains_csv(const std::string& path, const PulseTrains& trains) {
+  std::string csv = "band,time_s,amplitude\n";
+  for (const BandPulseTrain& t : trains)
+    for (const PulseEvent& e : t.events)
+      csv += std::to_string(t.band) + ',' + detail::format_double(e.time_s) + ',' + detail::format_double(e.amplitude) +
+             '\n';
+  detail::write_text(path, csv);
+}
+
+/// load_band_trains_csv (pipeline.cpp:528-553): the file back into trains;
+/// std::runtime_error naming the line for malformed rows or bad bands.
+inline PulseTrains load_band_trains_csv(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open: " + path);
+  PulseTrains trains;
+  for (int b = 0; b < kNumBands; ++b) trains[b].band = b;
+  std::string line;
+  std::getline(in, line);  // header
+  int line_no = 1;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (line.empty()) continue;
+    std::istringstream ls(line);
+    std::string band_text, time_text, amp_text;
+    if (!std::getline(ls, band_text, ',') || !std::getline(ls, time_text, ',') || !std::getline(ls, amp_text))
+      throw std::runtime_error("band_trains.csv line " + std::to_string(line_no) + " is malformed");
+    const int band = std::stoi(band_text);
+    if (band < 0 || band >= kNumBands)
+      throw std::runtime_error("band_trains.csv line " + std::to_string(line_no) + ": bad band index");
+    trains[band].events.push_back({std::stod(time_text), std::stod(amp_text)});
+  }
+  return trains;
+}
+
+/// write_metrics_json (pipeline.cpp:555-565): per band centre and "mid".
+inline void write_metrics_json(const std::string& path, const BandFactors& factors) {
+  detail::JOut j = detail::JOut::object();
+  for (int b = 0; b < kNumBands; ++b) j.set(detail::band_name(kBandCentersHz[b]), detail::factors_json(factors.bands[b]));
+  j.set("mid", detail::factors_json(factors.mid));
+  detail::write_text(path, j.dump(2) + "\n");
 }
 
 // ------------------------------------------------------------------ run artifacts (pipeline.hpp:40-45)
@@ -524,21 +624,13 @@ inline std::vector<std::string> write_run_artifacts(const RunConfig& config, con
       outputs.note(p);
     }
     {
-      std::string csv = "band,time_s,amplitude\n";
-      for (const BandPulseTrain& t : a.trains)
-        for (const PulseEvent& e : t.events)
-          csv += std::to_string(t.band) + ',' + detail::format_double(e.time_s) + ',' +
-                 detail::format_double(e.amplitude) + '\n';
       const std::string p = out_path("band_trains.csv");
-      detail::write_text(p, csv);
+      write_band_trains_csv(p, a.trains);
       outputs.note(p);
     }
     {
-      JOut j = JOut::object();
-      for (int b = 0; b < kNumBands; ++b) j.set(detail::band_name(kBandCentersHz[b]), detail::factors_json(a.metrics.bands[b]));
-      j.set("mid", detail::factors_json(a.metrics.mid));
       const std::string p = out_path("metrics.json");
-      detail::write_text(p, j.dump(2) + "\n");
+      write_metrics_json(p, a.metrics);
       outputs.note(p);
     }
     {
