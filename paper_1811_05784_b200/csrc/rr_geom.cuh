@@ -176,6 +176,33 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// Leaf refs: ~f holds face f; in the SAH tree ~(f | kPairBit) holds faces f
+// and f + 1 together (a quad's two triangles share one box, so the node
+// over them only cost a dependent fetch; rr_sah.cu finish_kernel).
+__device__ __forceinline__ int32_t leaf_face(int32_t leaf) { return ~leaf & (kPairBit - 1); }
+__device__ __forceinline__ int leaf_faces(int32_t leaf) { return (~leaf & kPairBit) ? 2 : 1; }
+
+// fp64 test of a leaf's faces into best (lexicographic (delta, face)
+// minimum, accel_tree.cpp:148-153); true if best changed
+__device__ __forceinline__ bool test_leaf(const FaceTri* __restrict__ tri, int32_t leaf, D3 o, D3 d,
+                                          HitResult& best) {
+  const int32_t f0 = leaf_face(leaf);
+  const int nfc = leaf_faces(leaf);
+  if (nfc == 2) prefetch_l1(tri + f0 + 1);
+  bool better = false;
+#pragma unroll 1
+  for (int k = 0; k < nfc; ++k) {
+    const int32_t f = f0 + k;
+    const double t = mt_delta(tri, f, o, d);
+    if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+      best.delta = t;
+      best.face = f;
+      better = true;
+    }
+  }
+  return better;
+}
+
 template <bool PF = false>
 __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNode* __restrict__ nodes,
                                                  const TNode* smem, int32_t K, const FaceTri* __restrict__ tri,
@@ -200,8 +227,10 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
       ++visits;
       const TNode nd = load_node(nodes, smem, node, K);
       if (PF) {  // start fetching both children while the boxes are tested
-        prefetch_l1(nd.d.x >= 0 ? static_cast<const void*>(nodes + nd.d.x) : static_cast<const void*>(tri + ~nd.d.x));
-        prefetch_l1(nd.d.y >= 0 ? static_cast<const void*>(nodes + nd.d.y) : static_cast<const void*>(tri + ~nd.d.y));
+        prefetch_l1(nd.d.x >= 0 ? static_cast<const void*>(nodes + nd.d.x)
+                                : static_cast<const void*>(tri + leaf_face(nd.d.x)));
+        prefetch_l1(nd.d.y >= 0 ? static_cast<const void*>(nodes + nd.d.y)
+                                : static_cast<const void*>(tri + leaf_face(nd.d.y)));
       }
       float tl = box_enter(r, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y, tbest);
       float tr = box_enter(r, nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w, tbest);
@@ -222,13 +251,7 @@ __device__ __forceinline__ HitResult closest_hit(const TravHeader& h, const TNod
         node = kPop;
       }
     } else if (node < 0) {
-      const int32_t f = ~node;
-      const double t = mt_delta(tri, f, o, d);
-      if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
-        best.delta = t;
-        best.face = f;
-        tbest = prune_bound(t, r.shift);
-      }
+      if (test_leaf(tri, node, o, d, best)) tbest = prune_bound(best.delta, r.shift);
       node = kPop;
     }
     if (node == kPop) {
@@ -353,7 +376,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
       }
       if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
         leaf = node;
-        if (PFL) prefetch_l1(tri + ~leaf);
+        if (PFL) prefetch_l1(tri + leaf_face(leaf));
         pop();
       }
     }
@@ -370,27 +393,19 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
     const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
     if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
-        const int32_t f = ~leaf;
-        if (CNT) ++cnt[1];
+        if (CNT) cnt[1] += leaf_faces(leaf);
         bool test = true;
-        if (F32L) {
+        if (F32L && leaf_faces(leaf) == 1) {
           const D3 dd = ray.dir();
           float lo, up;
-          test = mt32(tri32, f, r, __double2float_rn(dd.x), __double2float_rn(dd.y), __double2float_rn(dd.z),
-                      h.eps * 0x1p19f, &lo, &up) != 0;
+          test = mt32(tri32, leaf_face(leaf), r, __double2float_rn(dd.x), __double2float_rn(dd.y),
+                      __double2float_rn(dd.z), h.eps * 0x1p19f, &lo, &up) != 0;
         }
-        if (test) {
-          const double t = mt_delta(tri, f, ray.org(), ray.dir());
-          if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
-            best.delta = t;
-            best.face = f;
-            tbest = prune_bound(t, r.shift);
-          }
-        }
+        if (test && test_leaf(tri, leaf, ray.org(), ray.dir(), best)) tbest = prune_bound(best.delta, r.shift);
         leaf = 0;
         if (node < 0) {  // the leaf that waited for the slot
           leaf = node;
-          if (PFL) prefetch_l1(tri + ~leaf);
+          if (PFL) prefetch_l1(tri + leaf_face(leaf));
           pop();
         }
       }
@@ -500,13 +515,13 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
       }
       if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
         leaf = node;
-        prefetch_l1(tri + ~leaf);
+        prefetch_l1(tri + leaf_face(leaf));
         pop();
       }
     }
     if (node < 0 && leaf == 0) {  // a popped leaf (or a leaf root) with no node visit
       leaf = node;
-      prefetch_l1(tri + ~leaf);
+      prefetch_l1(tri + leaf_face(leaf));
       pop();
     }
     const unsigned act = __activemask();
@@ -520,17 +535,11 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
     const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
     if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
-        const int32_t f = ~leaf;
-        const double t = mt_delta(tri, f, ray.org(), ray.dir());
-        if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
-          best.delta = t;
-          best.face = f;
-          tbest = prune_bound(t, r.shift);
-        }
+        if (test_leaf(tri, leaf, ray.org(), ray.dir(), best)) tbest = prune_bound(best.delta, r.shift);
         leaf = 0;
         if (node < 0) {  // the leaf that waited for the slot
           leaf = node;
-          prefetch_l1(tri + ~leaf);
+          prefetch_l1(tri + leaf_face(leaf));
           pop();
         }
       }

@@ -123,6 +123,8 @@ struct __align__(16) QNode {
   int4 pad;
 };
 constexpr int32_t kEmpty = static_cast<int32_t>(0x80000000);
+// leaf ref flag: ~(f | kPairBit) holds faces f and f + 1 (SAH tree, rr_geom.cuh test_leaf)
+constexpr int32_t kPairBit = 1 << 30;
 
 struct TravHeader {
   float lo[3], hi[3];  // conservative root box

@@ -96,11 +96,27 @@ __global__ void prep_kernel(const double* __restrict__ v, const int32_t* __restr
   const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const int32_t a = t[4 * f], b = t[4 * f + 1], c = t[4 * f + 2];
+  // twins: faces 2k and 2k + 1 with the same AABB (a quad's two triangles)
+  // get the box centre as their common centroid, so every sorted list keeps
+  // them adjacent and SAH bins never separate them (pair leaves, below)
+  const int64_t g = f ^ 1;
+  bool twin = g < nf;
+  double lo[3], hi[3];
   for (int k = 0; k < 3; ++k) {
     const double va = v[3 * a + k], vb = v[3 * b + k], vc = v[3 * c + k];
-    const double ce = ((va + vb) + vc) / 3.0;
-    fb[6 * f + k] = fmin(va, fmin(vb, vc));
-    fb[6 * f + 3 + k] = fmax(va, fmax(vb, vc));
+    lo[k] = fmin(va, fmin(vb, vc));
+    hi[k] = fmax(va, fmax(vb, vc));
+    if (twin) {
+      const int32_t* tg = t + 4 * g;
+      const double wa = v[3 * tg[0] + k], wb = v[3 * tg[1] + k], wc = v[3 * tg[2] + k];
+      twin = fmin(wa, fmin(wb, wc)) == lo[k] && fmax(wa, fmax(wb, wc)) == hi[k];
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    const double va = v[3 * a + k], vb = v[3 * b + k], vc = v[3 * c + k];
+    const double ce = twin ? 0.5 * (lo[k] + hi[k]) : ((va + vb) + vc) / 3.0;
+    fb[6 * f + k] = lo[k];
+    fb[6 * f + 3 + k] = hi[k];
     cen[3 * f + k] = ce;
     keys[k * nf + f] = okeyf(__double2float_rn(ce));  // 32-bit sort key: order only shapes the tree
     ids[k * nf + f] = static_cast<int32_t>(f);
@@ -292,12 +308,19 @@ __device__ __forceinline__ BinAcc shfl_acc(const BinAcc& a, int src_delta, bool 
   return r;
 }
 
+// faces p (left of a median cut) and q (right of it) are twins (prep_kernel)
+__device__ __forceinline__ bool twins_at(int32_t p, int32_t q, const double* __restrict__ cen) {
+  return (p ^ 1) == q && cen[3 * p] == cen[3 * q] && cen[3 * p + 1] == cen[3 * q + 1] &&
+         cen[3 * p + 2] == cen[3 * q + 2];
+}
+
 __global__ void split_kernel(const SSeg* __restrict__ segs, const LevelState* __restrict__ ls,
                              const int32_t* __restrict__ rank,
                              const unsigned long long* __restrict__ bb, const unsigned long long* __restrict__ cb,
                              const int32_t* __restrict__ pl, const int32_t* __restrict__ sah_idx,
                              const int32_t* __restrict__ bcnt, const uint32_t* __restrict__ bbox,
-                             const int32_t* __restrict__ perm0, TNode* __restrict__ tn,
+                             const int32_t* __restrict__ perm0, const double* __restrict__ cen, int64_t nf,
+                             TNode* __restrict__ tn,
                              TravHeader* __restrict__ hdr, int32_t* __restrict__ seg_axis,
                              int32_t* __restrict__ seg_split, int64_t* __restrict__ seg_nl, SSeg* __restrict__ next) {
   static_assert(kBins == 32, "one lane per bin");
@@ -407,6 +430,8 @@ __global__ void split_kernel(const SSeg* __restrict__ segs, const LevelState* __
     }
     split = -1;
     nl = sg.n / 2;
+    const int32_t* lst = perm0 + axis * nf + sg.b;
+    if (twins_at(lst[nl - 1], lst[nl], cen)) ++nl;  // keep twins together
   }
   seg_axis[j] = axis;
   seg_split[j] = split;
@@ -471,12 +496,39 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
     }
     *plane = pmin == pmax ? pmin : -1;
   };
+  // A two-face range [a, a + 2) of consecutive faces (f, f + 1) becomes one
+  // pair leaf when a node over it cannot pay: with equal node and face test
+  // costs the SAH splits only if A(left) + A(right) < A(union), and a quad's
+  // two triangles share one box (the node cost a dependent fetch for no cull).
+  auto half_area = [](const double* lo, const double* hi) {
+    const double x = hi[0] - lo[0], y = hi[1] - lo[1], z = hi[2] - lo[2];
+    return x * y + y * z + z * x;
+  };
+  auto pair_ref = [&](int a, int32_t* ref) -> bool {
+    const int32_t g0 = min(f[a], f[a + 1]);
+    if (max(f[a], f[a + 1]) != g0 + 1) return false;
+    double lo[3], hi[3], l0[3], h0[3], l1[3], h1[3];
+    int32_t pdummy;
+    range_box(a, a + 2, lo, hi, &pdummy);
+    range_box(a, a + 1, l0, h0, &pdummy);
+    range_box(a + 1, a + 2, l1, h1, &pdummy);
+    if (half_area(l0, h0) + half_area(l1, h1) < half_area(lo, hi)) return false;
+    *ref = ~(g0 | kPairBit);
+    return true;
+  };
   {  // the segment itself, in its parent's slot (or as the root)
     double lo[3], hi[3];
     int32_t plane;
     range_box(0, n, lo, hi, &plane);
-    if (sg.parent < 0) hdr->root_ref = base;
-    else child_slot(tn + sg.parent, sg.side, lo, hi, eps, base, plane);
+    int32_t pref;
+    if (sg.parent < 0) {
+      hdr->root_ref = base;
+    } else if (n == 2 && pair_ref(0, &pref)) {
+      child_slot(tn + sg.parent, sg.side, lo, hi, eps, pref, plane);  // its node id stays unused
+      return;
+    } else {
+      child_slot(tn + sg.parent, sg.side, lo, hi, eps, base, plane);
+    }
   }
   // explicit stack of ranges still to split: (a, b, node index)
   int sa[kSmall], sb[kSmall], sn[kSmall];
@@ -508,24 +560,26 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
       }
       f[y + 1] = v;
     }
-    const int m = a + (b - a) / 2;
+    int m = a + (b - a) / 2;
+    if (b - a > 2 && twins_at(f[m - 1], f[m], cen)) m = (m + 1 < b) ? m + 1 : m - 1;  // keep twins together
     const int rng[2][2] = {{a, m}, {m, b}};
     // preorder ids: the subtree of `me` (range size s) owns [me, me + s - 1);
     // left child me + 1, right child me + (m - a)
-    const int32_t ref[2] = {(m - a) >= 2 ? me + 1 : ~f[a], (b - m) >= 2 ? me + (m - a) : ~f[m]};
+    int32_t ref[2] = {(m - a) >= 2 ? me + 1 : ~f[a], (b - m) >= 2 ? me + (m - a) : ~f[m]};
+    bool leafpair[2] = {m - a == 2 && pair_ref(a, &ref[0]), b - m == 2 && pair_ref(m, &ref[1])};
     for (int side = 0; side < 2; ++side) {
       double lo[3], hi[3];
       int32_t plane;
       range_box(rng[side][0], rng[side][1], lo, hi, &plane);
       child_slot(tn + me, side, lo, hi, eps, ref[side], plane);
     }
-    if (b - m >= 2) {
+    if (b - m >= 2 && !leafpair[1]) {
       sa[sp] = m;
       sb[sp] = b;
       sn[sp] = ref[1];
       ++sp;
     }
-    if (m - a >= 2) {
+    if (m - a >= 2 && !leafpair[0]) {
       sa[sp] = a;
       sb[sp] = m;
       sn[sp] = ref[0];
@@ -537,7 +591,7 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
 // 4a. left/right flag per face
 __global__ void flag_kernel(const int32_t* __restrict__ pos_seg, const SSeg* __restrict__ segs,
                             const int32_t* __restrict__ seg_axis, const int32_t* __restrict__ seg_split,
-                            const unsigned long long* __restrict__ cb, const double* __restrict__ cen,
+                            const int64_t* __restrict__ seg_nl, const unsigned long long* __restrict__ cb, const double* __restrict__ cen,
                             const int32_t* __restrict__ perm, int64_t nf, uint8_t* __restrict__ flag) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nf) return;
@@ -548,7 +602,7 @@ __global__ void flag_kernel(const int32_t* __restrict__ pos_seg, const SSeg* __r
   const SSeg sg = segs[s];
   const int32_t f = perm[axis * nf + i];  // position i of the axis list
   if (seg_split[s] < 0) {
-    flag[f] = (i - sg.b) < sg.n / 2 ? 1 : 0;
+    flag[f] = (i - sg.b) < seg_nl[s] ? 1 : 0;
   } else {
     const double clo = oval(cb[6 * s + axis]), ext = oval(cb[6 * s + 3 + axis]) - clo;
     flag[f] = bin_of(cen[3 * f + axis], clo, ext) < seg_split[s] ? 1 : 0;
@@ -839,12 +893,12 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
     }
     // 3. nodes + splits
     split_kernel<<<grid(32 * s_max), 256, 0, st>>>(segs, ls.p, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
-                                              s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
+                                              cen.p, nf, s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
     finish_kernel<<<grid(s_max, 64), 64, 0, st>>>(segs, ls.p, perm, fb.p, cen.p, s->face_plane.p, nf, s->snodes.p,
                                                   dh.p, top.p);
     RR_LAUNCH_CHECK();
     // 4. stable partition of the three lists
-    flag_kernel<<<grid(nf), 256, 0, st>>>(pos, segs, axis.p, split.p, cb.p, cen.p, perm, nf, flag.p);
+    flag_kernel<<<grid(nf), 256, 0, st>>>(pos, segs, axis.p, split.p, nl.p, cb.p, cen.p, perm, nf, flag.p);
     gather_kernel<<<grid(3 * nf), 256, 0, st>>>(perm, flag.p, 3 * nf, fl.p);
     RR_LAUNCH_CHECK();
     cub_run([&](void* t, size_t& b) {

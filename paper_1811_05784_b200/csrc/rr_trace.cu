@@ -392,13 +392,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_df(const TraceParams p
       const unsigned lm = __ballot_sync(0xffffffffu, busy && leaf != kNoLeaf);
       if (__any_sync(0xffffffffu, stuck) || __popc(lm) >= LEAFT) {
         if (busy && leaf != kNoLeaf) {
-          const int32_t f = ~leaf;
           const LaneRay x = load_ray();
-          const double t = mt_delta(p.tri, f, x.o, x.d);
-          if (t > 0.0 && (best_face < 0 || t < best_delta || (t == best_delta && f < best_face))) {
-            best_delta = t;
-            best_face = f;
-            tbest = prune_bound(t, rf.shift);
+          HitResult hb{best_delta, best_face};
+          if (test_leaf(p.tri, leaf, x.o, x.d, hb)) {
+            best_delta = hb.delta;
+            best_face = hb.face;
+            tbest = prune_bound(hb.delta, rf.shift);
           }
           leaf = kNoLeaf;
           if (node < 0) {  // the leaf that was waiting for the slot
@@ -741,7 +740,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_SAH");
     return e ? std::atoi(e) : 1;
   }();
-  const bool sah = use_sah && s->snodes.p != nullptr;
+  // (the fp32-leaf diagnostic classifies single-face leaves: reference tree)
+  const bool sah = use_sah && s->snodes.p != nullptr && !(cfg->flags & RR_TRACE_F32_LEAVES);
   if (!sah || (cfg->flags & RR_TRACE_WIDE)) ensure_reference_tree(s);
   // kernel variant (RR_DF, see below); the 4-wide SAH collapse is built on
   // first use by the variants that traverse it
@@ -889,7 +889,19 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
   static thread_local const void* occ_cache_fn = nullptr;
   if (occ_cache_smem != static_cast<int>(smem) || occ_cache_fn != reinterpret_cast<const void*>(kernel)) {
-    RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    // RR_CARVE (dev A/B): preferred shared-memory carveout in percent; -1
+    // leaves the driver's choice
+    static const int carve = [] {
+      const char* e = std::getenv("RR_CARVE");
+      return e ? std::atoi(e) : -1;
+    }();
+    if (carve >= 0) {
+      RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      if (smem > 0)
+        RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    } else {
+      RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    }
     RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache_blocks, kernel, 128, smem));
     occ_cache_smem = static_cast<int>(smem);
     occ_cache_fn = reinterpret_cast<const void*>(kernel);
