@@ -236,16 +236,7 @@ def run_ours(args):
     taps = 1023
     h2d = pv.numel() * 8 + pt.numel() * 4 + pa.numel() * 8
     e2e_ms, d2h, breakdown = [], 0, {}
-    pool = {}
 
-    def pinned(key, t):
-        """Device tensor -> reused pinned host buffer (async copy)."""
-        buf = pool.get(key)
-        if buf is None or buf.numel() < t.numel() or buf.dtype != t.dtype:
-            buf = pool[key] = torch.empty(max(t.numel(), 1), dtype=t.dtype, pin_memory=True)
-        out = buf[: t.numel()].view(t.shape)
-        out.copy_(t, non_blocking=True)
-        return out
     lib = _lib.load()
     import ctypes as C
 
@@ -262,30 +253,38 @@ def run_ours(args):
         sc = rr.AccelTree.__new__(rr.AccelTree)
         sc.ctx, sc.lib, sc.mesh, sc.h = ctx, lib, mesh, h
         marks = []
+        host = [("start", w0)]
 
         def mark(name):
             ev = torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
                 ev.record()
             marks.append((name, ev))
+            if os.environ.get("RR_E2E_DEBUG"):
+                host.append((name, time.perf_counter()))
 
         mark("scene")
         res = run_sharded(sc, src, recv, cfg, air=rr.AirModel(), options=rr.ClusterOptions(1e-6, True),
-                          sample_rate=scene.sample_rate, length=L, taps=taps, mark=mark)
-        # results to pinned host memory: the 8 band IRs (every rank) and the
-        # merged image list (rank 0)
+                          sample_rate=scene.sample_rate, length=L, taps=taps, mark=mark, host=True)
+        # run_sharded(host=True) returns the results in pinned host memory:
+        # the 8 band IRs and the broadband IR (every rank) and the merged image
+        # list (rank 0); the image list's D2H overlaps the IR stage
         fetched = []
         for r, band in enumerate(res.band_ir):
-            fetched.append(pinned(("ir", r), band.reshape(-1)))
+            fetched += [band, res.broadband[r]]
             if res.images[r] is not None:
-                for f in res.images[r].__dataclass_fields__:
-                    fetched.append(pinned((f, r), getattr(res.images[r], f)))
+                fetched += [getattr(res.images[r], f) for f in res.images[r].__dataclass_fields__]
+        assert all(not t.is_cuda for t in fetched)
         with torch.cuda.stream(stream):
             e1.record()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
         if it >= args.warmup:
             e2e_ms.append(max(e0.elapsed_time(e1), (w1 - w0) * 1e3))
+            if os.environ.get("RR_E2E_DEBUG"):
+                print("e2e dbg: event %.3f wall %.3f host marks %s" % (
+                    e0.elapsed_time(e1), (w1 - w0) * 1e3,
+                    [(n, round((t - w0) * 1e3, 3)) for n, t in host]), file=sys.stderr)
             prev = e0
             for name, ev in marks + [("fetch", e1)]:
                 breakdown[name] = breakdown.get(name, 0.0) + prev.elapsed_time(ev) / args.steps

@@ -210,6 +210,16 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist,
                         double* energy, double* mult, int32_t* ray_count,
                         int32_t* order, int32_t* has_proj, double* proj,
                         int64_t* path_off, int32_t* path);
+/* rr_images_get without the host synchronization: the copies are enqueued on
+ * `stream` (a cudaStream_t; 0 = the legacy default stream) after the work
+ * enqueued so far on the context's stream, so a D2H into pinned memory can
+ * overlap later device work (the IR stage).  The caller synchronizes
+ * `stream` before reading the outputs or destroying `im`. */
+rr_status rr_images_get_async(rr_images* im, void* stream, double* pos,
+                              double* dist, double* energy, double* mult,
+                              int32_t* ray_count, int32_t* order,
+                              int32_t* has_proj, double* proj,
+                              int64_t* path_off, int32_t* path);
 rr_status rr_images_destroy(rr_images* im);
 
 /* ---------------------------------------------------------------- shoebox

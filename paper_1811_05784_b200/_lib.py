@@ -101,6 +101,7 @@ SIGNATURES = [
                                          C.POINTER(_vp)]),
     ("rr_images_info", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
     ("rr_images_get", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("rr_images_get_async", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("rr_images_destroy", C.c_int, [_vp]),
     ("rr_images_device", C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     ("rr_air_beta_bands", C.c_int, [C.POINTER(Air), _f64p]),

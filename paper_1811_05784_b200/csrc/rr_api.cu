@@ -916,6 +916,38 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist, double* energy
   });
 }
 
+rr_status rr_images_get_async(rr_images* im, void* stream, double* pos, double* dist, double* energy, double* mult,
+                              int32_t* ray_count, int32_t* order, int32_t* has_proj, double* proj, int64_t* path_off,
+                              int32_t* path) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    RR_CUDA(cudaSetDevice(im->scene->ctx->device));
+    cudaStream_t ctx = im->scene->ctx->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st != ctx) {  // the side stream starts after the image build
+      cudaEvent_t ev;
+      RR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      RR_CUDA(cudaEventRecord(ev, ctx));
+      RR_CUDA(cudaStreamWaitEvent(st, ev, 0));
+      RR_CUDA(cudaEventDestroy(ev));
+    }
+    const int64_t n = im->n;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+    };
+    cp(pos, im->pos.p, sizeof(double) * 3 * n);
+    cp(dist, im->dist.p, sizeof(double) * n);
+    cp(energy, im->energy.p, sizeof(double) * rr::kBands * n);
+    cp(mult, im->mult.p, sizeof(double) * rr::kBands * n);
+    cp(ray_count, im->ray_count.p, sizeof(int32_t) * n);
+    cp(order, im->order.p, sizeof(int32_t) * n);
+    cp(has_proj, im->has_proj.p, sizeof(int32_t) * n);
+    cp(proj, im->proj.p, sizeof(double) * 3 * n);
+    cp(path_off, im->path_off.p, sizeof(int64_t) * (n + 1));
+    cp(path, im->path.p, sizeof(int32_t) * im->total_path);
+  });
+}
+
 rr_status rr_images_destroy(rr_images* im) {
   return guarded([&] {
     if (!im) return;

@@ -331,12 +331,18 @@ class ShardedResult:
 
 
 def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: float, length: int, taps: int = 1023,
-                block: int = 4096, group=None, mark=None, exchange: bool | None = None) -> ShardedResult:
+                block: int = 4096, group=None, mark=None, exchange: bool | None = None,
+                host: bool = False) -> ShardedResult:
     """trace -> exchange -> image sources -> IR for every receiver, the ranks
     of `group` each tracing a block-cyclic shard of the N-ray lattice (one
     trace serves all receivers: a receiver never alters a ray,
     tracer.cpp:27-29).  With a single rank it is the plain single-GPU
-    pipeline."""
+    pipeline.
+
+    host=True returns the image lists and IRs in pinned host memory: a
+    single rank's image list is copied to the host on a side stream while the
+    IR stage runs on the context stream (the copy is PCIe bound, ~1 ms for
+    C2's 56 MB, and the IR stage does not read it)."""
     import ctypes as C
 
     from . import _lib
@@ -373,25 +379,106 @@ def run_sharded(tree, source, receivers, config, *, air, options, sample_rate: f
             dt_local, ridx = dt, r
         dimg = build_image_sources_device(dt_local, source.ray_count, air, options, receiver=ridx)
         mark("images")
+        early = None
+        if host and not xch:  # start the image list's D2H now, overlapping the IR stage
+            early = images_to_host_async(dimg, dev)
+            mark("gather")
         d_dist, d_en, n_img = dimg.device_arrays()
         hist = torch.empty(NUM_BANDS * (length + taps), dtype=torch.float64, device=dev)
         _lib.check(lib.rr_ir_bin_device(tree.ctx.h, n_img, C.c_void_p(d_dist), C.c_void_p(d_en),
                                         config.speed_of_sound, sample_rate, length + taps,
                                         C.c_void_p(hist.data_ptr())))
-        torch.cuda.synchronize(dev)
+        # stream-level ordering only (a device-wide synchronize would also
+        # wait for the side stream's image copy)
+        _order(tree.ctx.stream, dev, ctx_first=True)
         reduce_histogram(hist, group)
-        torch.cuda.synchronize(dev)
         band = torch.empty(NUM_BANDS * length, dtype=torch.float64, device=dev)
         bb = torch.empty(length, dtype=torch.float64, device=dev)
+        _order(tree.ctx.stream, dev, ctx_first=False)
         _lib.check(lib.rr_ir_filter_device(tree.ctx.h, C.c_void_p(hist.data_ptr()), sample_rate, taps, length,
                                            C.c_void_p(band.data_ptr()), C.c_void_p(bb.data_ptr())))
-        torch.cuda.synchronize(dev)
+        _order(tree.ctx.stream, dev, ctx_first=True)
         mark("ir")
-        local = images_to_tensors(dimg)
-        out.local_images += len(local)
-        out.images.append(gather_images(local, group) if xch else local)
-        out.band_ir.append(band.view(NUM_BANDS, length))
+        if early is not None:
+            local, side, _ = early  # (dimg stays referenced until the copy ran)
+            out.local_images += len(local)
+            out.images.append(local)
+        else:
+            local = images_to_tensors(dimg)
+            out.local_images += len(local)
+            merged = gather_images(local, group) if xch else local
+            if host and merged is not None:
+                merged, side = imageset_to_host_async(merged, dev, tree.ctx.stream)
+                side.synchronize()
+            out.images.append(merged)
+        band = band.view(NUM_BANDS, length)
+        if host:
+            band, bb = _pinned_copy(band), _pinned_copy(bb)
+        out.band_ir.append(band)
         out.broadband.append(bb)
         torch.cuda.synchronize(dev)
-        mark("gather")
+        mark("gather" if early is None else "host")
     return out
+
+
+def _order(ctx_stream: int, dev, ctx_first: bool) -> None:
+    """Make torch's current stream wait for the context stream (ctx_first)
+    or the other way round."""
+    if not ctx_stream:
+        return
+    ctx = torch.cuda.ExternalStream(ctx_stream, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    a, b = (ctx, cur) if ctx_first else (cur, ctx)
+    if a != b:
+        ev = torch.cuda.Event()
+        ev.record(a)
+        b.wait_event(ev)
+
+
+def _pinned_copy(t: torch.Tensor) -> torch.Tensor:
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
+
+
+def images_to_host_async(dimages, dev):
+    """A device image set (rr_images) straight into pinned host tensors,
+    copied on a side stream that starts after the image build
+    (rr_images_get_async); returns (host set, stream, dimages).  The caller
+    synchronizes the stream before reading the set or dropping dimages."""
+    import ctypes as C
+
+    from ._lib import check
+
+    n, tp = dimages.n, dimages.total_path
+    f = dict(dtype=torch.float64, pin_memory=True)
+    i = dict(dtype=torch.int32, pin_memory=True)
+    im = ImageSet(torch.empty((n, 3), **f), torch.empty(n, **f), torch.empty((n, NUM_BANDS), **f),
+                  torch.empty((n, NUM_BANDS), **f), torch.empty(n, **i), torch.empty(n, **i), torch.empty(n, **i),
+                  torch.empty((n, 3), **f), torch.empty(n + 1, dtype=torch.int64, pin_memory=True),
+                  torch.empty(max(tp, 1), **i))
+    side = torch.cuda.Stream(device=dev)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    check(dimages.lib.rr_images_get_async(dimages.h, C.c_void_p(side.cuda_stream), vp(im.position), vp(im.distance),
+                                          vp(im.band_energy), vp(im.band_multiplier), vp(im.ray_count), vp(im.order),
+                                          vp(im.has_projection), vp(im.projection), vp(im.path_off), vp(im.path)))
+    im.path = im.path[:tp]
+    return im, side, dimages
+
+
+def imageset_to_host_async(im: ImageSet, dev, ctx_stream: int):
+    """Copy a device ImageSet into pinned host tensors on a side stream that
+    waits for the context stream's work so far; returns (host set, stream)."""
+    ctx = torch.cuda.ExternalStream(ctx_stream, device=dev) if ctx_stream else torch.cuda.current_stream(dev)
+    ready = torch.cuda.Event()
+    ready.record(ctx)
+    ready_cur = torch.cuda.Event()
+    ready_cur.record(torch.cuda.current_stream(dev))  # torch.empty / D2D copies of images_to_tensors
+    side = torch.cuda.Stream(device=dev)
+    side.wait_event(ready)
+    side.wait_event(ready_cur)
+    with torch.cuda.stream(side):
+        fields = {k: _pinned_copy(getattr(im, k)) for k in im.__dataclass_fields__}
+    for k in im.__dataclass_fields__:  # the device tensors stay alive until the copy ran
+        getattr(im, k).record_stream(side)
+    return ImageSet(**fields), side

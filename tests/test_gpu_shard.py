@@ -163,3 +163,29 @@ def test_nccl_exchange_path_single_rank():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "exchange ok" in r.stdout
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c3"])
+def test_host_fetch_equals_device_results(ctx, cfg_name):
+    """run_sharded(host=True) (image list copied to pinned host memory on a
+    side stream while the IR stage runs) returns exactly the device results,
+    for one receiver (C1) and five (C3)."""
+    s = scenes.CONFIGS[cfg_name]()
+    tree = rr.AccelTree(rr.TriangleMesh(s.vertices, s.faces, s.absorption), ctx)
+    src = rr.SourceConfig(s.source, 20000)
+    recv = [rr.Receiver(*r) for r in s.receivers]
+    cfg = rr.TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range)
+    L = int(round(0.25 * s.sample_rate))
+    kw = dict(air=rr.AirModel(), options=rr.ClusterOptions(1e-6, True), sample_rate=s.sample_rate, length=L)
+    dev = shard.run_sharded(tree, src, recv, cfg, **kw)
+    host = shard.run_sharded(tree, src, recv, cfg, host=True, **kw)
+    torch.cuda.synchronize()
+    assert len(host.images) == len(dev.images) == len(recv)
+    for r in range(len(recv)):
+        assert len(host.images[r]) == len(dev.images[r]) > 0
+        for f in FIELDS:
+            h, d = getattr(host.images[r], f), getattr(dev.images[r], f)
+            assert not h.is_cuda and h.is_pinned()
+            assert torch.equal(h, d.cpu()), (r, f)
+        assert not host.band_ir[r].is_cuda and torch.equal(host.band_ir[r], dev.band_ir[r].cpu())
+        assert torch.equal(host.broadband[r], dev.broadband[r].cpu())
