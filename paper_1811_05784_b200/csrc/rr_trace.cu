@@ -606,12 +606,29 @@ __global__ void capture_out_kernel(const Capture* __restrict__ caps, const int32
   const unsigned gm = 0xffu << g0;              // the group runs its loops in lockstep
   double m = 1.0;
   int j = 0;
-  for (; j + 8 <= order; j += 8) {
-    const int32_t mine = h[j + b];  // each lane fetches one of the next 8 faces
-    o_hist[base + j + b] = mine;
-    const int32_t mt = mat[mine];
+  // up to four chunks of 8 faces per iteration: the history and material
+  // loads of all of them are issued before the (ordered) products
+  for (; j + 8 <= order; j += 32) {
+    const int nc = min(4, (order - j) >> 3);  // full chunks in this round (uniform over the group)
+    int32_t mt[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) m *= oma[kBands * __shfl_sync(gm, mt, g0 + u) + b];
+    for (int c = 0; c < 4; ++c) mt[c] = c < nc ? h[j + 8 * c + b] : 0;  // each lane fetches one face per chunk
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < nc) o_hist[base + j + 8 * c + b] = mt[c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) mt[c] = c < nc ? mat[mt[c]] : 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < nc) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m *= oma[kBands * __shfl_sync(gm, mt[c], g0 + u) + b];
+      }
+    }
+    if (nc < 4) {
+      j += 8 * nc;
+      break;
+    }
   }
   const int rest = order - j;
   int32_t mt = 0;
