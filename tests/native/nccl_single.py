@@ -27,12 +27,16 @@ def main():
     kw = dict(air=rr.AirModel(), options=rr.ClusterOptions(1e-6, True), sample_rate=48000.0, length=48000)
     a = shard.run_sharded(tree, src, recv, cfg, exchange=False, **kw)
     b = shard.run_sharded(tree, src, recv, cfg, exchange=True, **kw)
+    h = shard.run_sharded(tree, src, recv, cfg, exchange=True, host=True, **kw)  # pinned host results
     total = 0
     for r in range(len(recv)):
         for f in a.images[r].__dataclass_fields__:
             x, y = getattr(a.images[r], f).cpu().numpy(), getattr(b.images[r], f).cpu().numpy()
             assert np.array_equal(x, y), (r, f)
+            z = getattr(h.images[r], f)
+            assert not z.is_cuda and np.array_equal(x, z.numpy()), (r, f)
         assert torch.equal(a.band_ir[r], b.band_ir[r]), r
+        assert torch.equal(a.band_ir[r].cpu(), h.band_ir[r]), r
         total += len(a.images[r])
     assert total > 20, total
     dist.destroy_process_group()
