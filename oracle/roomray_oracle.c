@@ -493,14 +493,20 @@ int ro_intersect_sphere(const double* o, const double* d, const double* c,
   return sphere(mk(o[0], o[1], o[2]), mk(d[0], d[1], d[2]), mk(c[0], c[1], c[2]), r, out);
 }
 
-/* fibonacci_directions emission.cpp:17-29 */
+/* fibonacci_directions emission.cpp:17-29.  The reference's
+ * rho*std::cos(phi), rho*std::sin(phi) compiles (g++ -O2, objdump of
+ * oracle/_ref/obj/emission.o) to ONE glibc sincos() call, whose results can
+ * differ from separate sin()/cos() calls, so the restatement calls sincos
+ * explicitly rather than relying on gcc to merge the pair. */
 static inline v3 fib_dir(int64_t k, int64_t n) {
   const double golden = (1.0 + sqrt(5.0)) / 2.0;
   const double step = 2.0 * M_PI * (1.0 - 1.0 / golden);
   double z = 1.0 - (2.0 * (double)k + 1.0) / (double)n;
   double rho = sqrt(smax(0.0, 1.0 - z * z));
   double phi = step * (double)k;
-  return mk(rho * cos(phi), rho * sin(phi), z);
+  double s, c;
+  sincos(phi, &s, &c);
+  return mk(rho * c, rho * s, z);
 }
 
 void ro_fibonacci(int64_t n, int64_t first, int64_t stride, int64_t count, double* out) {

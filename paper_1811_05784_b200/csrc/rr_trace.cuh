@@ -40,7 +40,9 @@ struct TraceParams {
   double rc[kMaxRecv][3];
   double rr[kMaxRecv];
   int32_t max_iter;
-  double max_range;
+  double rng[kMaxRecv];  // capture range per receiver: resolved_max_range (tracer.cpp:10-15) of each
+  double max_range;      // kill range: the largest of rng (a receiver never alters a ray)
+  double cull_min;       // coplanar-subtree cull only when |d_axis| exceeds this (see run_trace)
   int32_t* hist;  // count * H
   int64_t H;
   Capture* caps;

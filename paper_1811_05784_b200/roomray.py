@@ -333,7 +333,8 @@ def air_validate(air: AirModel) -> None:
 def fibonacci_directions(n: int, first: int = 0, stride: int = 1, count: int | None = None,
                          ctx: Context | None = None) -> np.ndarray:
     """fibonacci_directions (emission.cpp:17-29) evaluated on the device the
-    way the tracer emits its rays (correctly rounded sin/cos)."""
+    way the tracer emits its rays (glibc's sincos restated bit for bit,
+    rr_sincos.cuh)."""
     ctx = ctx or Context.default()
     if count is None:
         count = max(0, (n - first + stride - 1) // stride) if n >= 1 else 0

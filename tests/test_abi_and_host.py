@@ -4,8 +4,10 @@
   declares, and the ctypes signature table covers them all;
 * scene generators are deterministic and have the BASELINE.json sizes;
 * the device emission's sin/cos (rr_sincos.cuh, compiled for the host here)
-  is correctly rounded, and its disagreement with glibc is the documented
-  sub-0.3 % one-ulp set.
+  is bit-identical to the installed glibc sincos() -- the call the
+  reference's fibonacci_directions makes -- on every lattice azimuth of every
+  config and on random arguments in each branch; its correctly rounded
+  fallback (beyond 1.05e8 rad) is checked against decimal sin.
 """
 import ctypes
 import os
@@ -94,18 +96,32 @@ def sincos_check():
     return exe
 
 
-def test_emission_sincos_vs_glibc(sincos_check):
-    out = subprocess.run([sincos_check, "1000000"], capture_output=True, text=True).stdout
-    m = re.search(r"mismatches (\d+) of (\d+)", out)
-    bad, n = int(m.group(1)), int(m.group(2))
-    # glibc's sin/cos are not correctly rounded on ~0.28 % of the lattice
-    # azimuths (<= 1 ulp); rr_sincos.cuh is (see the decimal check below)
-    assert bad / n < 0.005
+def _sincos_run(exe, *args):
+    out = subprocess.run([exe, *map(str, args)], capture_output=True, text=True).stdout
+    m = re.search(r"mismatches (\d+) of (\d+) fallback (\d+)", out)
+    assert m, out
+    return int(m.group(1)), int(m.group(2)), int(m.group(3)), out
+
+
+def test_emission_sincos_bit_identical_to_glibc_on_every_lattice(sincos_check):
+    """Every azimuth of C1 (10^4 rays), C2/C3 (10^6) and C5 (8*10^6)."""
+    bad, n, fb, out = _sincos_run(sincos_check, "lattice", 10_000, 1_000_000, 8_000_000)
+    assert n == 9_010_000 and fb == 0
+    assert bad == 0, out
+
+
+def test_emission_sincos_bit_identical_to_glibc_random(sincos_check):
+    """Random arguments in every branch of glibc's routine (tiny, Taylor,
+    table, pi/2 - |x|, Cody-Waite up to 1.05e8 rad), both signs."""
+    bad, n, fb, out = _sincos_run(sincos_check, "random", 4_000_000, 11)
+    assert n > 3_900_000 and fb > 0
+    assert bad == 0, out
 
 
 def test_emission_sincos_correctly_rounded():
-    """Spot-check rr::sincos_cr against 60-digit decimal sin/cos on the
-    azimuths where it disagrees with glibc."""
+    """Spot-check rr::sincos_cr (the fallback beyond 1.05e8 rad) against
+    60-digit decimal sin/cos on azimuths where glibc is not correctly
+    rounded."""
     from decimal import Decimal, getcontext
     getcontext().prec = 60
     exe_src = os.path.join(ROOT, "tests", "native", "sincos_check.cpp")

@@ -1,0 +1,164 @@
+"""GPU parity of the DEFAULT product path at config scale.
+
+No test here passes `directions=`: the device evaluates the Fibonacci lattice
+itself (rr_sincos.cuh, glibc's sincos restated bit for bit), exactly as the
+bench, the facade's trace() and run_trace_pipeline do.  Compared against the
+CPU oracle on all host threads:
+
+* the full lattices of C1, C2/C3 and C5 (10^4, 10^6, 8*10^6 rays) against
+  glibc's sincos through the oracle, every component bit-identical;
+* full C2 (10^6 rays, 50 reflections): every capture, face path, multiplier
+  and counter bit-identical to the oracle's trace; then the full image-source
+  set (coplanar merge off) against the oracle's build_image_sources;
+* full C3 (10^6 rays, 30 reflections, 5 receivers): one device trace serves
+  all five receivers; each receiver's captures are compared with its own
+  single-receiver run of the UNMODIFIED reference (oracle/_ref), which emits
+  its rays with its own emit() (emission.cpp:31-43);
+* C5 (2*10^6 triangles, 100 reflections): 65 536 rays of the 8*10^6 lattice
+  (stride 122) bit-identical to the oracle;
+* the restatement against the reference (the chain the CPU suite pins),
+  repeated here so the GPU run sees it: C1 traced by the oracle port and by
+  oracle/_ref, identical.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1811_05784_b200 import AccelTree, Receiver, SourceConfig, TraceConfig, TriangleMesh, trace
+from paper_1811_05784_b200 import roomray as rr
+from paper_1811_05784_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+AIR = (1.0, 20.0, 50.0, 101.325)
+
+
+def _captures_equal(g, o, recv=None):
+    if recv is not None:
+        assert (g.recv == recv).all()
+    assert len(g) == len(o), (len(g), len(o))
+    for k in ("ray", "hist_off", "path", "point", "dir", "mult"):
+        np.testing.assert_array_equal(getattr(g, k), getattr(o, k), err_msg=k)
+    np.testing.assert_array_equal(g.hist, o.hist[: o.hist_off[-1]])
+
+
+def _select(c, r):
+    """Captures of receiver r, with their own history offsets."""
+    m = c.recv == r
+    idx = np.nonzero(m)[0]
+    lens = c.hist_off[idx + 1] - c.hist_off[idx]
+    off = np.zeros(len(idx) + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    hist = np.concatenate([c.hist[c.hist_off[i]:c.hist_off[i + 1]] for i in idx]) if len(idx) else c.hist[:0]
+    return oracle.Captures(c.recv[m], c.ray[m], c.point[m], c.dir[m], c.path[m], c.mult[m], off, hist)
+
+
+@pytest.mark.parametrize("n", [10_000, 1_000_000, 8_000_000])
+def test_device_lattice_bit_identical_to_glibc(ctx, port, n):
+    got = rr.fibonacci_directions(n, ctx=ctx)
+    want = port.fibonacci(n)
+    assert got.shape == want.shape == (n, 3)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.fixture(scope="module")
+def c2():
+    return scenes.config2()
+
+
+@pytest.fixture(scope="module")
+def c2_runs(ctx, port, c2):
+    s = c2
+    rc, rad = s.receivers[0]
+    tree = AccelTree(TriangleMesh(s.vertices, s.faces, s.absorption), ctx)
+    dt = rr.trace_device(tree, SourceConfig(s.source, s.ray_count), Receiver(rc, rad),
+                         TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range))
+    ps = port.scene(oracle.Mesh(s.vertices, s.faces, s.absorption))
+    oc, ost = ps.trace(s.source, s.ray_count, [rc], [rad], s.max_iterations, s.max_range, THREADS)
+    return tree, dt, ps, oc, ost
+
+
+def test_c2_full_trace_default_path(c2_runs):
+    tree, dt, ps, oc, ost = c2_runs
+    res = dt.result()
+    assert res.n_rays == 1_000_000
+    assert res.ray_bounces == ost.ray_bounces > 40_000_000
+    assert (res.escaped, res.out_of_range, res.iterations, res.truncated) == \
+        (ost.escaped, ost.out_of_range, ost.iterations, ost.truncated)
+    assert len(oc) > 500_000
+    _captures_equal(res.captures, oc)
+
+
+def test_c2_full_image_sources_default_path(c2, c2_runs):
+    tree, dt, ps, oc, ost = c2_runs
+    rc, _ = c2.receivers[0]
+    gi = rr.build_image_sources(dt, c2.ray_count, rr.AirModel(), rr.ClusterOptions(1e-6, False))
+    oi = ps.image_sources(oc, c2.ray_count, AIR, rc, 1e-6, False)
+    assert len(gi) == len(oi) > 100_000
+    np.testing.assert_array_equal(gi.order, oi.order)
+    np.testing.assert_array_equal(gi.ray_count, oi.ray_count)
+    np.testing.assert_array_equal(gi.path_off, oi.path_off)
+    np.testing.assert_array_equal(gi.path, oi.path)
+    np.testing.assert_array_equal(gi.position, oi.pos)
+    np.testing.assert_array_equal(gi.distance, oi.dist)
+    np.testing.assert_array_equal(gi.band_multiplier, oi.mult)
+    np.testing.assert_allclose(gi.band_energy, oi.energy, rtol=1e-12, atol=0)
+    np.testing.assert_array_equal(gi.has_projection, oi.has_proj)
+    np.testing.assert_array_equal(gi.projection, oi.proj)
+
+
+def test_c3_full_trace_five_receivers_vs_reference(ctx, ref):
+    s = scenes.config3()
+    tree = AccelTree(TriangleMesh(s.vertices, s.faces, s.absorption), ctx)
+    recvs = [Receiver(c, r) for c, r in s.receivers]
+    res = trace(tree, SourceConfig(s.source, s.ray_count), recvs,
+                TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range))
+    rs = ref.scene(oracle.Mesh(s.vertices, s.faces, s.absorption))
+    total = 0
+    for r, (c, rad) in enumerate(s.receivers):
+        oc, ost = rs.trace(s.source, s.ray_count, c, rad, s.max_iterations, s.max_range, THREADS)
+        _captures_equal(_select(res.captures, r), oc)
+        assert (res.escaped, res.out_of_range, res.iterations, res.truncated) == \
+            (ost.escaped, ost.out_of_range, ost.iterations, ost.truncated)
+        total += len(oc)
+    assert total == len(res.captures) > 1000
+    assert res.escaped > 0
+
+
+def test_c5_65536_rays_default_path(ctx, port):
+    s = scenes.config5()
+    stride = s.ray_count // 65_536  # 122
+    first = 3
+    cnt = 65_536
+    tree = AccelTree(TriangleMesh(s.vertices, s.faces, s.absorption), ctx)
+    rc, rad = s.receivers[0]
+    res = trace(tree, SourceConfig(s.source, s.ray_count), Receiver(rc, rad),
+                TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range), first=first, stride=stride,
+                count=cnt)
+    ps = port.scene(oracle.Mesh(s.vertices, s.faces, s.absorption))
+    oc, ost = ps.trace(s.source, s.ray_count, [rc], [rad], s.max_iterations, s.max_range, THREADS, first, stride,
+                       cnt)
+    assert res.n_rays == cnt
+    assert res.ray_bounces == ost.ray_bounces
+    assert (res.escaped, res.out_of_range, res.truncated) == (ost.escaped, ost.out_of_range, ost.truncated)
+    assert len(oc) > 1000
+    _captures_equal(res.captures, oc)
+
+
+def test_restatement_equals_reference_c1(port, ref):
+    """oracle/roomray_oracle.c against the unmodified reference on C1 (the
+    pin tests/test_oracle_vs_ref.py holds in the CPU suite)."""
+    s = scenes.config1()
+    rc, rad = s.receivers[0]
+    pc, pst = port.scene(oracle.Mesh(s.vertices, s.faces, s.absorption)).trace(
+        s.source, s.ray_count, [rc], [rad], s.max_iterations, s.max_range, THREADS)
+    oc, ost = ref.scene(oracle.Mesh(s.vertices, s.faces, s.absorption)).trace(
+        s.source, s.ray_count, rc, rad, s.max_iterations, s.max_range, THREADS)
+    _captures_equal(pc, oc)
+    assert (pst.escaped, pst.out_of_range, pst.iterations, pst.truncated) == \
+        (ost.escaped, ost.out_of_range, ost.iterations, ost.truncated)
