@@ -77,6 +77,9 @@ typedef struct {
 #define RR_TRACE_F32_LEAVES 4    /* diagnostic: fp32 leaf classification + fp64 resolution */
 #define RR_TRACE_WIDE 8          /* diagnostic: traverse the 4-wide collapse */
 #define RR_TRACE_COUNT 16        /* instrumented kernel: count node visits and leaf tests */
+#define RR_TRACE_TREE8 32        /* traverse the 8-wide compressed tree at any scene size
+                                    (the default from 2^18 faces up) */
+#define RR_TRACE_TREE2 64        /* traverse the binary SAH tree at any scene size */
 
 /* Statistics of a trace (TraceResult, tracer.hpp:22-29). */
 typedef struct {

@@ -154,6 +154,9 @@ class Port:
         L.ro_fibonacci.argtypes = [_i64, _i64, _i64, _i64, _f64p]
         L.ro_trace_run.restype = _vp
         L.ro_trace_run.argtypes = [_vp, _f64p, _i64, _f64p, _f64p, _i32, _i32, C.c_double, _i32, _i64, _i64, _i64]
+        L.ro_trace_run_dirs.restype = _vp
+        L.ro_trace_run_dirs.argtypes = [_vp, _f64p, _i64, _f64p, _f64p, _i32, _i32, C.c_double, _i32, _i64, _i64,
+                                        _i64, _vp]
         L.ro_trace_info.argtypes = [_vp, C.POINTER(_i32), C.POINTER(_i32)] + [C.POINTER(_i64)] * 2 + [
             C.POINTER(C.c_double)] + [C.POINTER(_i64)] * 5
         L.ro_trace_captures.argtypes = [_vp, _i32p, _i32p, _f64p, _f64p, _f64p, _f64p, _i64p, _i32p]
@@ -265,11 +268,15 @@ class PortScene:
         return face, delta, point
 
     def trace(self, src, ray_count, recv_centers, recv_radii, max_iterations=1000, max_range=0.0,
-              threads=1, first=0, stride=0, count=0):
+              threads=1, first=0, stride=0, count=0, directions=None):
+        """trace() over the lattice subset, or over caller `directions`
+        (count x 3, ray ids first + i*stride) when given."""
         rc = _c(recv_centers, np.float64).reshape(-1, 3)
         rr = _c(np.atleast_1d(recv_radii), np.float64)
-        h = self.p.L.ro_trace_run(self.h, _c(src, np.float64), ray_count, rc.reshape(-1), rr, len(rr),
-                                  max_iterations, max_range, threads, first, stride, count)
+        dirs = None if directions is None else _c(directions, np.float64).reshape(-1)
+        h = self.p.L.ro_trace_run_dirs(self.h, _c(src, np.float64), ray_count, rc.reshape(-1), rr, len(rr),
+                                       max_iterations, max_range, threads, first, stride, count,
+                                       None if dirs is None else dirs.ctypes.data)
         if not h:
             self.p._err()
         try:

@@ -569,9 +569,11 @@ typedef struct {
   int64_t n;
   const double* rc;
   const double* rr;
+  const double* rng; /* capture range per receiver */
+  const double* dirs; /* optional caller directions (count x 3), else the lattice */
   int32_t n_recv;
   int32_t max_it;
-  double max_range;
+  double max_range; /* kill range: the largest of rng */
   int64_t first, stride, begin, end;
   /* outputs */
   capbuf buf;
@@ -589,7 +591,8 @@ static void* trace_worker(void* arg) {
   int32_t* hist = (int32_t*)malloc(sizeof(int32_t) * (w->max_it > 0 ? w->max_it : 1));
   for (int64_t i = w->begin; i < w->end; ++i) {
     int64_t k = w->first + i * w->stride;
-    v3 o = w->src, d = fib_dir(k, w->n);
+    v3 o = w->src;
+    v3 d = w->dirs ? mk(w->dirs[3 * i], w->dirs[3 * i + 1], w->dirs[3 * i + 2]) : fib_dir(k, w->n);
     double path = 0.0;
     double mult[RO_BANDS];
     for (int b = 0; b < RO_BANDS; ++b) mult[b] = 1.0;
@@ -605,7 +608,7 @@ static void* trace_worker(void* arg) {
         v3 c = mk(w->rc[3 * r], w->rc[3 * r + 1], w->rc[3 * r + 2]);
         if (sphere(o, d, c, w->rr[r], &sd) && (!wall.ok || sd < wall.delta)) {
           double L = path + sd;
-          if (L <= w->max_range) {
+          if (L <= w->rng[r]) {
             cap_t cp;
             cp.recv = r;
             cp.ray = (int32_t)k;
@@ -666,11 +669,30 @@ ro_trace* ro_trace_run(const ro_scene* s, const double* src, int64_t ray_count,
                        int32_t n_recv, int32_t max_iterations, double max_range,
                        int32_t threads, int64_t first, int64_t stride,
                        int64_t count) {
+  return ro_trace_run_dirs(s, src, ray_count, recv_centers, recv_radii, n_recv, max_iterations, max_range,
+                           threads, first, stride, count, NULL);
+}
+
+/* Several receivers on one set of trajectories (a receiver never alters a
+ * ray, tracer.cpp:27-29): receiver r captures while L <= its own
+ * resolved_max_range (tracer.cpp:10-15), rays die past the largest, which
+ * reproduces one reference trace() per receiver.  dirs (count x 3, may be
+ * NULL) replaces the lattice directions of the traced rays (the Ray span of
+ * step(), tracer.hpp:43). */
+ro_trace* ro_trace_run_dirs(const ro_scene* s, const double* src, int64_t ray_count,
+                            const double* recv_centers, const double* recv_radii,
+                            int32_t n_recv, int32_t max_iterations, double max_range,
+                            int32_t threads, int64_t first, int64_t stride,
+                            int64_t count, const double* dirs) {
   for (int32_t r = 0; r < n_recv; ++r)
     if (recv_radii[r] <= 0.0) {
       set_err("receiver radius must be > 0");
       return NULL;
     }
+  if (n_recv < 1 || n_recv > 64) {
+    set_err("n_recv must be in [1, 64]");
+    return NULL;
+  }
   if (ray_count < 1) {
     set_err("source ray_count must be >= 1");
     return NULL;
@@ -682,8 +704,13 @@ ro_trace* ro_trace_run(const ro_scene* s, const double* src, int64_t ray_count,
   }
   if (count <= 0 || first + (count - 1) * stride >= ray_count)
     count = (ray_count - first + stride - 1) / stride;
-  /* resolved_max_range tracer.cpp:10-15 (first receiver's radius) */
-  double mr = max_range > 0.0 ? max_range : 0.5 * recv_radii[0] * sqrt((double)ray_count);
+  /* resolved_max_range tracer.cpp:10-15, per receiver */
+  double rng[64];
+  double mr = 0.0;
+  for (int32_t r = 0; r < n_recv; ++r) {
+    rng[r] = max_range > 0.0 ? max_range : 0.5 * recv_radii[r] * sqrt((double)ray_count);
+    if (rng[r] > mr) mr = rng[r];
+  }
   if (threads < 1) threads = 1;
   if (count < threads) threads = count > 0 ? (int32_t)count : 1;
   worker* ws = (worker*)calloc(threads, sizeof(worker));
@@ -696,6 +723,8 @@ ro_trace* ro_trace_run(const ro_scene* s, const double* src, int64_t ray_count,
     w->n = ray_count;
     w->rc = recv_centers;
     w->rr = recv_radii;
+    w->rng = rng;
+    w->dirs = dirs;
     w->n_recv = n_recv;
     w->max_it = max_iterations;
     w->max_range = mr;

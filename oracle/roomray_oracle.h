@@ -54,6 +54,11 @@ ro_trace* ro_trace_run(const ro_scene* s, const double* src, int64_t ray_count,
                        int32_t n_recv, int32_t max_iterations, double max_range,
                        int32_t threads, int64_t first, int64_t stride,
                        int64_t count);
+ro_trace* ro_trace_run_dirs(const ro_scene* s, const double* src, int64_t ray_count,
+                            const double* recv_centers, const double* recv_radii,
+                            int32_t n_recv, int32_t max_iterations, double max_range,
+                            int32_t threads, int64_t first, int64_t stride,
+                            int64_t count, const double* dirs);
 void ro_trace_info(const ro_trace* t, int32_t* iterations, int32_t* truncated,
                    int64_t* escaped, int64_t* out_of_range, double* max_range,
                    int64_t* n_captures, int64_t* total_hist,

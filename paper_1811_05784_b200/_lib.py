@@ -20,6 +20,8 @@ RR_TRACE_KEEP_UNSORTED = 2
 RR_TRACE_F32_LEAVES = 4
 RR_TRACE_WIDE = 8
 RR_TRACE_COUNT = 16
+RR_TRACE_TREE8 = 32
+RR_TRACE_TREE2 = 64
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")

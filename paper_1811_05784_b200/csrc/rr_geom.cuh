@@ -809,4 +809,203 @@ __device__ __forceinline__ HitResult closest_hit4(const TravHeader& h, const QNo
   return best;
 }
 
+
+// ---------------------------------------------------------------------------
+// 8-wide compressed traversal (WNode, rr_wide.cu).  Leaf refs index the
+// leaf-ordered face copy: ~(t | kPairBit) holds wtri[t] and wtri[t + 1];
+// the face id travels in FaceTri.pad.
+
+// Moller-Trumbore on a leaf-ordered face (mt_delta's operations), face id out
+__device__ __forceinline__ double mt_delta_w(const FaceTri* __restrict__ wtri, int32_t t, D3 o, D3 d, int32_t* face) {
+  const double2* p = reinterpret_cast<const double2*>(wtri + t);
+  const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3), q4 = __ldg(p + 4);
+  *face = static_cast<int32_t>(__double_as_longlong(q4.y));
+  const D3 va = d3(q0.x, q0.y, q1.x);
+  const D3 e1 = d3(q1.y, q2.x, q2.y);
+  const D3 e2 = d3(q3.x, q3.y, q4.x);
+  const D3 pv = cross(d, e2);
+  const double det = dot(e1, pv);
+  if (det == 0.0) return -1.0;
+  const double inv = 1.0 / det;
+  const D3 tv = o - va;
+  const double lambda = dot(tv, pv) * inv;
+  if (lambda < 0.0 || lambda > 1.0) return -1.0;
+  const D3 qv = cross(tv, e1);
+  const double mu = dot(d, qv) * inv;
+  if (mu < 0.0 || lambda + mu > 1.0) return -1.0;
+  const double delta = dot(e2, qv) * inv;
+  if (delta <= 1e-6) return -1.0;
+  return delta;
+}
+
+__device__ __forceinline__ bool test_leaf_w(const FaceTri* __restrict__ wtri, int32_t leaf, D3 o, D3 d,
+                                            HitResult& best) {
+  const int32_t t0 = leaf_face(leaf);
+  const int nfc = leaf_faces(leaf);
+  bool better = false;
+#pragma unroll 1
+  for (int k = 0; k < nfc; ++k) {
+    int32_t f;
+    const double t = mt_delta_w(wtri, t0 + k, o, d, &f);
+    if (t > 0.0 && (best.face < 0 || t < best.delta || (t == best.delta && f < best.face))) {
+      best.delta = t;
+      best.face = f;
+      better = true;
+    }
+  }
+  return better;
+}
+
+// byte k of the (w0, w1) pair as an exact fp32 integer: 2^23 + b built by one
+// byte permute, then 2^23 subtracted (exact)
+__device__ __forceinline__ float qbyte(uint32_t w0, uint32_t w1, int k) {
+  const uint32_t w = k < 4 ? w0 : w1;
+  return __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440u | static_cast<uint32_t>(k & 3))) - 8388608.0f;
+}
+
+// Same contract as closest_hit_pl (postponed, warp-batched leaf tests;
+// pruning by the best hit so far; coplanar cull), over 8-wide nodes: the
+// hit slots are pushed farthest first and the nearest is continued.  STK
+// bounds the stack (the builder's occupancy bound s->wstack must fit).
+template <int LEAFT, int STUCKT, typename RAY, int UNR, int TOS, int STK, bool CNT = false>
+__device__ __forceinline__ HitResult closest_hit8_pl(const TravHeader& h, const WNode* __restrict__ wn,
+                                                     const FaceTri* __restrict__ wtri, const RAY& ray,
+                                                     int32_t rplane, unsigned long long* cnt = nullptr) {
+  HitResult best{0.0, -1};
+  RayF r;
+  if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
+  const float kInf = __int_as_float(0x7f800000);
+  float tbest = FLT_MAX;
+  int32_t node = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest) == kInf ? kDone : 0;
+  const bool px = r.ix >= 0.0f, py = r.iy >= 0.0f, pz = r.iz >= 0.0f;
+  int2 st[STK];
+  int sp = 0;
+  int2 top[TOS > 0 ? TOS : 1] = {};
+  int n_top = 0;
+  int32_t leaf = 0;
+  auto push = [&](int2 e) {
+    if (TOS > 0) {
+      if (n_top == TOS) st[sp++] = top[TOS - 1];
+#pragma unroll
+      for (int k = TOS - 1; k > 0; --k) top[k] = top[k - 1];
+      top[0] = e;
+      n_top = min(n_top + 1, TOS);
+    } else {
+      st[sp++] = e;
+    }
+  };
+  auto pop = [&]() {
+    node = kDone;
+    while (TOS > 0 && n_top > 0) {
+      const int2 e = top[0];
+#pragma unroll
+      for (int k = 0; k + 1 < TOS; ++k) top[k] = top[k + 1];
+      --n_top;
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        return;
+      }
+    }
+    while (sp > 0) {
+      --sp;
+      const int2 e = st[sp];
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        break;
+      }
+    }
+  };
+  while (node != kDone || leaf != 0) {
+#pragma unroll 1
+    for (int u = 0; u < UNR && is_inner(node) && (u == 0 || leaf == 0); ++u) {
+      if (CNT) ++cnt[0];
+      const float4* q = reinterpret_cast<const float4*>(wn + node);
+      const float4 hh = __ldg(q);
+      const int4 mm = __ldg(reinterpret_cast<const int4*>(q + 1));
+      const uint4 qx = __ldg(reinterpret_cast<const uint4*>(q + 2));
+      const uint4 qy = __ldg(reinterpret_cast<const uint4*>(q + 3));
+      const uint4 qz = __ldg(reinterpret_cast<const uint4*>(q + 4));
+      const uint32_t hw = __float_as_uint(hh.w);
+      const float ax = __uint_as_float((hw & 0xffu) << 23) * r.ix;
+      const float ay = __uint_as_float(((hw >> 8) & 0xffu) << 23) * r.iy;
+      const float az = __uint_as_float(((hw >> 16) & 0xffu) << 23) * r.iz;
+      const float bx = __fmaf_rn(hh.x, r.ix, r.nx), by = __fmaf_rn(hh.y, r.iy, r.ny), bz = __fmaf_rn(hh.z, r.iz, r.nz);
+      // near / far planes per axis from the ray's octant
+      const uint32_t nx0 = px ? qx.x : qx.z, nx1 = px ? qx.y : qx.w, fx0 = px ? qx.z : qx.x, fx1 = px ? qx.w : qx.y;
+      const uint32_t ny0 = py ? qy.x : qy.z, ny1 = py ? qy.y : qy.w, fy0 = py ? qy.z : qy.x, fy1 = py ? qy.w : qy.y;
+      const uint32_t nz0 = pz ? qz.x : qz.z, nz1 = pz ? qz.y : qz.w, fz0 = pz ? qz.z : qz.x, fz1 = pz ? qz.w : qz.y;
+      const uint32_t bits = static_cast<uint32_t>(mm.w);
+      const uint32_t cull = mm.z == rplane ? (bits >> 16) & 0xffu : 0u;
+      const uint32_t valid = bits & 0xffu & ~cull;
+      float tk[8];
+      uint32_t hitm = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float tnx = __fmaf_rn(qbyte(nx0, nx1, k), ax, bx), tfx = __fmaf_rn(qbyte(fx0, fx1, k), ax, bx);
+        const float tny = __fmaf_rn(qbyte(ny0, ny1, k), ay, by), tfy = __fmaf_rn(qbyte(fy0, fy1, k), ay, by);
+        const float tnz = __fmaf_rn(qbyte(nz0, nz1, k), az, bz), tfz = __fmaf_rn(qbyte(fz0, fz1, k), az, bz);
+        const float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, 0.0f));
+        const float tf = fminf(fminf(tfx, tfy), fminf(tfz, tbest));
+        tk[k] = tn;
+        if (tn <= tf) hitm |= 1u << k;
+      }
+      hitm &= valid;
+      const uint32_t imask = hw >> 24;
+      const uint32_t leafm = (bits & 0xffu) & ~imask, pairm = (bits >> 8) & 0xffu;
+      auto ref_of = [&](int k) -> int32_t {
+        const uint32_t below = (1u << k) - 1u;
+        if ((imask >> k) & 1u) return mm.x + __popc(imask & below);
+        const int32_t t = mm.y + __popc(leafm & below) + __popc(pairm & leafm & below);
+        return ~(t | (((pairm >> k) & 1u) ? kPairBit : 0));
+      };
+      if (hitm == 0) {
+        pop();
+      } else {
+        while (hitm & (hitm - 1u)) {  // two or more: push the farthest
+          float tmx = -1.0f;
+          int kmx = 0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (((hitm >> k) & 1u) && tk[k] > tmx) {
+              tmx = tk[k];
+              kmx = k;
+            }
+          push(make_int2(ref_of(kmx), __float_as_int(tmx)));
+          hitm &= ~(1u << kmx);
+        }
+        node = ref_of(__ffs(hitm) - 1);
+      }
+      if (node < 0 && node != kDone && leaf == 0) {  // stash a reached leaf and keep traversing
+        leaf = node;
+        pop();
+      }
+    }
+    if (node < 0 && node != kDone && leaf == 0) {  // a popped leaf with no node visit
+      leaf = node;
+      pop();
+    }
+    const unsigned act = __activemask();
+    const unsigned hv = __ballot_sync(act, leaf != 0);
+    if (hv == 0) continue;
+    const bool can = is_inner(node);
+    const bool must = leaf != 0 && !can;
+    const unsigned mv = __ballot_sync(act, must);
+    const unsigned cv = __ballot_sync(act, can);
+    const int na = __popc(act);
+    const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
+    if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
+      if (leaf != 0) {
+        if (CNT) cnt[1] += leaf_faces(leaf);
+        if (test_leaf_w(wtri, leaf, ray.org(), ray.dir(), best)) tbest = prune_bound(best.delta, r.shift);
+        leaf = 0;
+        if (node < 0 && node != kDone) {  // the leaf that waited for the slot
+          leaf = node;
+          pop();
+        }
+      }
+    }
+  }
+  return best;
+}
+
 }  // namespace rr

@@ -123,6 +123,27 @@ struct __align__(16) QNode {
   int4 pad;
 };
 constexpr int32_t kEmpty = static_cast<int32_t>(0x80000000);
+
+// 8-wide compressed traversal node (rr_wide.cu), 80 B = five 16-B loads.
+// Child boxes are quantized to 8 bits per plane on a per-node grid
+// p + q * 2^e (p fp32, e a power-of-two exponent per axis), rounded outward
+// beyond the binary node's conservative fp32 boxes (see rr_wide.cu for the
+// error budget), so the filter stays a superset of the fp64 reference's.
+//   h  = (px, py, pz, bits: ex | ey << 8 | ez << 16 | imask << 24)
+//        e: the biased fp32 exponent of the scale; imask bit k: slot k internal
+//   m  = (child_base, tri_base, plane, valid | pair << 8 | cull << 16)
+//        internal slot k -> node child_base + popc(imask & ((1 << k) - 1));
+//        leaf slot k -> its 1 (or 2, pair bit) faces at tri_base + (faces of
+//        the leaf slots before k); cull bit k: slot k's subtree lies in
+//        axis-aligned plane `plane` (coplanar-subtree cull)
+//   qx = (lo bytes 0-3, lo bytes 4-7, hi bytes 0-3, hi bytes 4-7) of slot k,
+//   qy, qz likewise.
+struct __align__(16) WNode {
+  float4 h;
+  int4 m;
+  uint4 qx, qy, qz;
+};
+static_assert(sizeof(WNode) == 80, "WNode");
 // leaf ref flag: ~(f | kPairBit) holds faces f and f + 1 (SAH tree, rr_geom.cuh test_leaf)
 constexpr int32_t kPairBit = 1 << 30;
 
@@ -176,6 +197,11 @@ struct rr_scene {
   rr::DevBuf<rr::TNode> snodes;   // SAH traversal tree (rr_sah.cu), nf-1 nodes, BFS order
   rr::TravHeader shdr{};          // its header (root box, root ref, eps)
   rr::DevBuf<rr::QNode> s4nodes;  // 4-wide collapse of the SAH tree (pad = slot plane ids)
+  rr::DevBuf<rr::WNode> wnodes;   // 8-wide compressed collapse of the SAH tree (rr_wide.cu)
+  rr::DevBuf<rr::FaceTri> wtri;   // faces in its leaf order, pad = the face id (int64 bits)
+  int32_t wroot = -1;             // WNode root (0) when built
+  int32_t wstack = 0;             // bound on the traversal stack occupancy over the 8-wide tree
+  int32_t wdepth = 0;
   int32_t s4root = -1;
   int32_t sah_depth = 0;
   int64_t n_qnodes = 0;
@@ -197,6 +223,8 @@ void ensure_reference_tree(rr_scene* s);
 // rr_sah.cu (needs face_plane; runs on its own stream)
 void build_sah_tree(rr_scene* s, cudaStream_t st);
 void build_sah4(rr_scene* s);  // 4-wide collapse, on demand
+// rr_wide.cu
+void build_wide(rr_scene* s);  // 8-wide compressed collapse, on demand
 // rr_trace.cu
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
                        int64_t n, int brute, int32_t* d_face, double* d_delta,

@@ -932,9 +932,9 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   s->shdr.root4 = 0;
   s->sah_depth = depth;
   if (depth > kMaxDepth) throw Error(RR_RUNTIME, "SAH tree deeper than the traversal stack");
-  // the 4-wide collapse serves the deep-tree kernel only; smaller scenes
-  // build it on demand (build_sah4)
-  if (nf >= (int64_t(1) << 18)) build_sah4(s);
+  // the 8-wide collapse serves the deep-tree kernel only; smaller scenes
+  // build it on demand (build_wide, rr_trace.cu)
+  if (nf >= (int64_t(1) << 18)) build_wide(s);
 }
 
 // 4-wide collapse of the SAH tree (traversed by trace_kernel<3, ...>).

@@ -23,7 +23,16 @@
 #include "rr_sincos.cuh"
 #include "rr_trace.cuh"
 
+#ifndef RR_W8_MINB
+#define RR_W8_MINB 6  // blocks of 128 per SM the 8-wide kernel's register budget targets
+#endif
+#ifndef RR_W8_UNR
+#define RR_W8_UNR 8  // internal nodes a lane may visit between leaf votes
+#endif
+
 namespace rr {
+
+constexpr int kStack8 = 96;  // 8-wide traversal stack (entries); the tree's bound must fit
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
   if (p.block > 0) {
@@ -117,6 +126,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     HitResult wall;
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
+    } else if (V == 4) {
+      wall = closest_hit8_pl<PL, ST, RegRay, UNR, TOS, kStack8, CNT>(p.hdr, p.wnodes, p.wtri, RegRay{o, d}, rplane,
+                                                                   st_cnt);
     } else if (V == 3) {
       wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
@@ -493,7 +505,18 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  if (sah && (df_env0 == 23 || df_env0 == 24 || (df_env0 < 0 && s->nf >= (1 << 18)))) build_sah4(s);
+  if (sah && (df_env0 == 23 || df_env0 == 24)) build_sah4(s);
+  // 8-wide compressed tree for deep scenes (RR_WIDE: face-count threshold,
+  // default 2^18; the 8-wide kernel needs the builder's stack bound to fit)
+  static const int64_t wide_min = [] {
+    const char* e = std::getenv("RR_WIDE");
+    return e ? std::atoll(e) : int64_t(1) << 18;
+  }();
+  const bool want8 = sah && !(cfg->flags & RR_TRACE_TREE2) && !(cfg->flags & RR_TRACE_WIDE) &&
+                     ((cfg->flags & RR_TRACE_TREE8) || (df_env0 < 0 && s->nf >= wide_min));
+  if (want8) build_wide(s);
+  p.wnodes = s->wnodes.p;
+  p.wtri = s->wtri.p;
   p.nodes = sah ? s->snodes.p : s->tnodes.p;
   p.qnodes = s->qnodes.p;
   // default: binary nodes, fp64 test at every leaf (fastest measured); diagnostics: fp32 leaf classification, 4-wide nodes
@@ -610,12 +633,16 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  const bool wide4 = s->s4nodes.p != nullptr && (df_env == 23 || (df_env < 0 && s->nf >= (1 << 18)));
-  auto dfk = wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
+  const bool wide4 = s->s4nodes.p != nullptr && df_env == 23;
+  const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8;
+  auto dfk = wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, false, RR_W8_UNR, 0, false, 2, false>
+           : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
-  if (cfg->flags & RR_TRACE_COUNT) dfk = trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;  // counts of the default
+  if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
+    dfk = wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, true, RR_W8_UNR, 0, false, 2, false>
+                : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;

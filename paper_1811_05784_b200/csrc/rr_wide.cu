@@ -1,0 +1,268 @@
+// K1'' — 8-wide compressed collapse of the SAH traversal tree (rr_sah.cu).
+//
+// Deep scenes (C3, C5: 4.4e5 - 2e6 faces) make the binary traversal a chain
+// of ~50 dependent node fetches per ray-bounce against a 128 MB node array
+// that does not fit in the 126 MB L2 (the round-1 C5 tracer: 1.2 KB of DRAM
+// traffic per ray-bounce at 20 % of HBM bandwidth).  Collapsing the binary
+// tree into 8-wide nodes with 8-bit quantized child boxes (the compressed
+// wide BVH layout of Ylitie, Karras and Laine, HPG 2017, restated for this
+// tracer's exactness contract) cuts the chain to ~1/3 and the node array to
+// ~80 B per 7 binary nodes, which keeps it L2-resident; the faces are copied
+// into leaf order so a node's leaf faces are contiguous.
+//
+// Build, level-synchronous from the root (one thread per wide node):
+//   expand: start from the binary node's two children and repeatedly open
+//           the internal child of largest surface area until 8 slots are
+//           used or only leaves remain (leaves are the SAH tree's own 1- or
+//           2-face leaves);
+//   scan:   exclusive sum of (internal children, leaf faces) per node, so a
+//           node's internal children are contiguous one level down and its
+//           leaf faces contiguous in `wtri`;
+//   write:  the WNode (quantized boxes, masks, plane cull bits), the next
+//           frontier, the leaf faces (FaceTri with the face id in `pad`).
+//
+// Exactness.  The traversal only filters; the closest hit is still the
+// lexicographic (delta, face) minimum of the fp64 tests of every admitted
+// face (accel_tree.cpp:148-153), so any superset of the reference's boxes
+// gives identical results.  Each slot's box is the binary node's
+// conservative fp32 child box (exact box + eps, rounded outward; eps =
+// scale * 2^-19 bounds the fp32 slab error, rr_geom.cuh box_enter) widened
+// by another eps/4 and rounded outward onto the grid: q_lo = floor, q_hi =
+// ceil, evaluated in fp64 on the exact grid values p + q * 2^e.  The node
+// traversal evaluates a plane as fma(q, 2^e * inv, fma(p, inv, -o * inv)):
+// two roundings more than box_enter's fma(l, inv, -o * inv), each below
+// 6 * scale * 2^-24 in space units (|q * 2^e|, |p - o| <= 6 scale), so
+// < 0.2 eps altogether, inside the extra eps/4.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "rr_geom.cuh"
+
+namespace rr {
+namespace {
+
+constexpr int kW = 8;
+
+struct Slot {
+  float b[6];  // lo x, hi x, lo y, hi y, lo z, hi z (the TNode child box)
+  int32_t ref;  // binary ref: >= 0 internal, < 0 leaf (~f or ~(f | kPairBit))
+  int32_t plane;
+};
+
+__device__ __forceinline__ void tnode_slot(const TNode& t, int side, Slot& s) {
+  if (side == 0) {
+    s.b[0] = t.a.x; s.b[1] = t.a.y; s.b[2] = t.a.z; s.b[3] = t.a.w; s.b[4] = t.b.x; s.b[5] = t.b.y;
+    s.ref = t.d.x;
+    s.plane = t.d.z;
+  } else {
+    s.b[0] = t.b.z; s.b[1] = t.b.w; s.b[2] = t.c.x; s.b[3] = t.c.y; s.b[4] = t.c.z; s.b[5] = t.c.w;
+    s.ref = t.d.y;
+    s.plane = t.d.w;
+  }
+}
+
+__device__ __forceinline__ float half_area(const Slot& s) {
+  const float dx = s.b[1] - s.b[0], dy = s.b[3] - s.b[2], dz = s.b[5] - s.b[4];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+// expand frontier node i into <= 8 slots; packed (internal << 32 | faces)
+__global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __restrict__ frontier, int32_t n,
+                              Slot* __restrict__ slots, int32_t* __restrict__ nslot,
+                              unsigned long long* __restrict__ packed) {
+  const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= n) return;
+  Slot s[kW];
+  const TNode t = tn[frontier[i]];
+  tnode_slot(t, 0, s[0]);
+  tnode_slot(t, 1, s[1]);
+  int cnt = 2;
+  while (cnt < kW) {
+    int best = -1;
+    float ba = -1.f;
+    for (int k = 0; k < cnt; ++k)
+      if (s[k].ref >= 0) {
+        const float a = half_area(s[k]);
+        if (a > ba) {
+          ba = a;
+          best = k;
+        }
+      }
+    if (best < 0) break;
+    const TNode c = tn[s[best].ref];
+    tnode_slot(c, 0, s[best]);
+    tnode_slot(c, 1, s[cnt]);
+    ++cnt;
+  }
+  unsigned long long ni = 0, nfc = 0;
+  for (int k = 0; k < cnt; ++k) {
+    slots[static_cast<int64_t>(i) * kW + k] = s[k];
+    if (s[k].ref >= 0) ++ni;
+    else nfc += leaf_faces(s[k].ref);
+  }
+  nslot[i] = cnt;
+  packed[i] = (ni << 32) | nfc;
+}
+
+// exact grid values: plane = p + q * 2^(e-127); returns the biased exponent
+__device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, double m, float* p_out,
+                                               uint32_t* lo8, uint32_t* hi8) {
+  double lo = 1e300, hi = -1e300;
+  for (int k = 0; k < cnt; ++k) {
+    lo = fmin(lo, static_cast<double>(s[k].b[2 * ax]) - m);
+    hi = fmax(hi, static_cast<double>(s[k].b[2 * ax + 1]) + m);
+  }
+  const float p = __double2float_rd(lo);
+  const double pd = static_cast<double>(p);
+  // smallest power of two with (hi - p) <= 255 * scale
+  int e = static_cast<int>(ceil(log2((hi - pd) / 255.0)));
+  while (ldexp(255.0, e) < hi - pd) ++e;
+  while (e > -126 && ldexp(255.0, e - 1) >= hi - pd) --e;
+  e = max(e, -126);
+  const double sc = ldexp(1.0, e);
+  lo8[0] = lo8[1] = hi8[0] = hi8[1] = 0;
+  for (int k = 0; k < cnt; ++k) {
+    double ql = floor((static_cast<double>(s[k].b[2 * ax]) - m - pd) / sc);
+    double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc);
+    ql = fmin(fmax(ql, 0.0), 255.0);
+    qh = fmin(fmax(qh, 0.0), 255.0);
+    lo8[k >> 2] |= static_cast<uint32_t>(ql) << (8 * (k & 3));
+    hi8[k >> 2] |= static_cast<uint32_t>(qh) << (8 * (k & 3));
+  }
+  *p_out = p;
+  return static_cast<uint32_t>(e + 127);
+}
+
+__global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __restrict__ nslot,
+                             const unsigned long long* __restrict__ offs, int32_t n, int32_t level_base,
+                             int32_t next_base, const int32_t* __restrict__ acc, const FaceTri* __restrict__ tri,
+                             double margin, WNode* __restrict__ out, FaceTri* __restrict__ wtri,
+                             int32_t* __restrict__ next_frontier, int32_t* __restrict__ next_acc,
+                             int32_t* __restrict__ bound) {
+  const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= n) return;
+  Slot s[kW];
+  const int cnt = nslot[i];
+  for (int k = 0; k < cnt; ++k) s[k] = slots[static_cast<int64_t>(i) * kW + k];
+  const unsigned long long o = offs[i];
+  const int32_t ci = static_cast<int32_t>(o >> 32);  // rank of my first internal child in the next level
+  const int32_t ti = static_cast<int32_t>(o & 0xffffffffu);
+  WNode w;
+  float p[3];
+  uint32_t e[3], lo8[3][2], hi8[3][2];
+  for (int ax = 0; ax < 3; ++ax) e[ax] = quant_axis(s, cnt, ax, margin, &p[ax], lo8[ax], hi8[ax]);
+  uint32_t imask = 0, valid = 0, pair = 0, cull = 0;
+  // plane for the cull: the first slot plane (a subtree inside an axis-aligned
+  // wall usually has all its slots in that wall)
+  int32_t plane = -1;
+  for (int k = 0; k < cnt; ++k)
+    if (s[k].plane >= 0) {
+      plane = s[k].plane;
+      break;
+    }
+  const int32_t a = acc[i] + cnt - 1;  // stack entries while visiting this node's subtree
+  int ni = 0, nfc = 0;
+  for (int k = 0; k < cnt; ++k) {
+    valid |= 1u << k;
+    if (plane >= 0 && s[k].plane == plane) cull |= 1u << k;
+    if (s[k].ref >= 0) {
+      imask |= 1u << k;
+      next_frontier[ci + ni] = s[k].ref;
+      next_acc[ci + ni] = a;
+      ++ni;
+    } else {
+      const int32_t f0 = leaf_face(s[k].ref);
+      const int nl = leaf_faces(s[k].ref);
+      if (nl == 2) pair |= 1u << k;
+      for (int j = 0; j < nl; ++j) {
+        FaceTri ft = tri[f0 + j];
+        ft.pad = __longlong_as_double(static_cast<long long>(f0 + j));
+        wtri[ti + nfc + j] = ft;
+      }
+      nfc += nl;
+    }
+  }
+  atomicMax(bound, a);
+  w.h = make_float4(p[0], p[1], p[2], __int_as_float(static_cast<int>(e[0] | (e[1] << 8) | (e[2] << 16) |
+                                                                       (imask << 24))));
+  w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16)));
+  w.qx = make_uint4(lo8[0][0], lo8[0][1], hi8[0][0], hi8[0][1]);
+  w.qy = make_uint4(lo8[1][0], lo8[1][1], hi8[1][0], hi8[1][1]);
+  w.qz = make_uint4(lo8[2][0], lo8[2][1], hi8[2][0], hi8[2][1]);
+  out[level_base + i] = w;
+}
+
+inline unsigned grid(int64_t n, int b = 256) { return static_cast<unsigned>(std::max<int64_t>(1, (n + b - 1) / b)); }
+
+}  // namespace
+
+void build_wide(rr_scene* s) {
+  if (s->wnodes.p || !s->snodes.p || s->shdr.root_ref < 0 || s->nf < 3) return;
+  cudaStream_t st = s->ctx->stream;
+  const int64_t nf = s->nf;
+  const int32_t n_int = static_cast<int32_t>(nf - 1);
+  // every wide node consumes >= 1 binary internal node
+  DevBuf<WNode> nodes;
+  nodes.alloc(n_int, st);
+  s->wtri.alloc(nf, st);
+  DevBuf<int32_t> fr[2], ac[2], nslot, bound;
+  DevBuf<Slot> slots;
+  DevBuf<unsigned long long> packed, offs;
+  DevBuf<uint8_t> tmp;
+  bound.alloc(1, st);
+  RR_CUDA(cudaMemsetAsync(bound.p, 0, sizeof(int32_t), st));
+  fr[0].alloc(1, st);
+  ac[0].alloc(1, st);
+  const int32_t root = s->shdr.root_ref, zero = 0;
+  RR_CUDA(cudaMemcpyAsync(fr[0].p, &root, sizeof root, cudaMemcpyHostToDevice, st));
+  RR_CUDA(cudaMemcpyAsync(ac[0].p, &zero, sizeof zero, cudaMemcpyHostToDevice, st));
+  const double margin = 0.25 * static_cast<double>(s->shdr.eps);
+  int32_t n = 1, base = 0, depth = 0;
+  int64_t tri_done = 0;
+  while (n > 0) {
+    slots.alloc(static_cast<int64_t>(n) * kW, st);
+    nslot.alloc(n, st);
+    packed.alloc(n + 1, st);
+    offs.alloc(n + 1, st);
+    expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p);
+    RR_LAUNCH_CHECK();
+    RR_CUDA(cudaMemsetAsync(packed.p + n, 0, sizeof(unsigned long long), st));
+    size_t need = 0;
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, packed.p, offs.p, n + 1, st));
+    if (need > tmp.n) tmp.alloc(need, st);
+    RR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, need, packed.p, offs.p, n + 1, st));
+    unsigned long long tot = 0;
+    RR_CUDA(cudaMemcpyAsync(&tot, offs.p + n, sizeof tot, cudaMemcpyDeviceToHost, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+    const int32_t n_next = static_cast<int32_t>(tot >> 32);
+    const int64_t n_tri = static_cast<int64_t>(tot & 0xffffffffu);
+    if (base + n + n_next > n_int) throw Error(RR_RUNTIME, "8-wide collapse: node count bound exceeded");
+    fr[1].alloc(std::max(n_next, 1), st);
+    ac[1].alloc(std::max(n_next, 1), st);
+    write_kernel<<<grid(n), 256, 0, st>>>(slots.p, nslot.p, offs.p, n, base, base + n, ac[0].p, s->tri.p, margin,
+                                          nodes.p, s->wtri.p + tri_done, fr[1].p, ac[1].p, bound.p);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 5;
+    tri_done += n_tri;
+    base += n;
+    n = n_next;
+    ++depth;
+    std::swap(fr[0], fr[1]);
+    std::swap(ac[0], ac[1]);
+  }
+  if (tri_done != nf) throw Error(RR_RUNTIME, "8-wide collapse: leaf faces do not cover the mesh");
+  int32_t h_bound = 0;
+  RR_CUDA(cudaMemcpyAsync(&h_bound, bound.p, sizeof h_bound, cudaMemcpyDeviceToHost, st));
+  // compact copy of the node array
+  s->wnodes.alloc(base, st);
+  RR_CUDA(cudaMemcpyAsync(s->wnodes.p, nodes.p, sizeof(WNode) * base, cudaMemcpyDeviceToDevice, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  s->wroot = 0;
+  s->wstack = h_bound + 1;
+  s->wdepth = depth;
+  s->ctx->launches += 1;
+}
+
+}  // namespace rr

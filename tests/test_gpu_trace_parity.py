@@ -10,7 +10,7 @@ import pytest
 import oracle
 from paper_1811_05784_b200 import (AccelTree, Receiver, SourceConfig, TraceConfig, TriangleMesh, nearest_hit,
                                    nearest_hit_brute, trace)
-from paper_1811_05784_b200 import scenes
+from paper_1811_05784_b200 import _lib, scenes
 
 pytestmark = pytest.mark.gpu
 
@@ -116,30 +116,32 @@ def _compare_captures(g, o, recv_filter=None):
     np.testing.assert_array_equal(g.mult, o.mult)
 
 
-def _trace_both(ctx, port, v, f, a, src, n, recvs, max_it, max_range, **subset):
+# traversal trees: the default for the scene size, the 8-wide compressed
+# tree (default from 2^18 faces), the binary SAH tree
+TREES = [0, _lib.RR_TRACE_TREE8, _lib.RR_TRACE_TREE2]
+
+
+def _trace_both(ctx, port, v, f, a, src, n, recvs, max_it, max_range, flags=0, **subset):
     gm, om = _mesh(v, f, a)
     tree = AccelTree(gm, ctx)
-    # host-lattice directions from the oracle (glibc sin/cos in this process),
-    # so trajectories are compared bit for bit; device emission is tested in
-    # test_gpu_emission.py
-    first, stride = subset.get("first", 0), subset.get("stride", 0)
-    cnt = n if stride <= 0 else (n - first + stride - 1) // stride
-    dirs = port.fibonacci(n, first if stride > 0 else 0, max(stride, 1), cnt)
+    # the device evaluates the lattice itself (glibc's sincos restated,
+    # rr_sincos.cuh), so trajectories are compared bit for bit
     res = trace(tree, SourceConfig(src, n), [Receiver(c, r) for c, r in recvs],
-                TraceConfig(max_iterations=max_it, max_range=max_range), directions=dirs, **subset)
+                TraceConfig(max_iterations=max_it, max_range=max_range), flags=flags, **subset)
     oc, ost = port.scene(om).trace(src, n, [c for c, _ in recvs], [r for _, r in recvs], max_it, max_range,
                                    first=subset.get("first", 0), stride=subset.get("stride", 0),
                                    count=subset.get("count", 0))
     return res, oc, ost
 
 
-def test_trace_shoebox_fixture(ctx, port):
+@pytest.mark.parametrize("flags", TREES)
+def test_trace_shoebox_fixture(ctx, port, flags):
     """The section-4.2 fixture (tests/fixtures/shoebox_run_small.json): [5,4,3]
     box, concrete/podium walls, 20 000 rays, receiver r=0.2."""
     concrete = [0.36, 0.36, 0.44, 0.31, 0.29, 0.39, 0.25, 0.25]
     podium = [0.4, 0.4, 0.3, 0.2, 0.17, 0.15, 0.1, 0.1]
     v, f, a = scenes.box_scene((5, 4, 3), per_wall=[concrete, podium] * 3)
-    res, oc, ost = _trace_both(ctx, port, v, f, a, (4, 2, 1.7), 20000, [((2, 2, 1.7), 0.2)], 1000, 0.0)
+    res, oc, ost = _trace_both(ctx, port, v, f, a, (4, 2, 1.7), 20000, [((2, 2, 1.7), 0.2)], 1000, 0.0, flags)
     assert res.iterations == ost.iterations
     assert res.truncated == ost.truncated
     assert res.escaped == ost.escaped and res.out_of_range == ost.out_of_range
@@ -148,28 +150,31 @@ def test_trace_shoebox_fixture(ctx, port):
     _compare_captures(res.captures, oc)
 
 
-def test_trace_config1_full(ctx, port):
+@pytest.mark.parametrize("flags", TREES)
+def test_trace_config1_full(ctx, port, flags):
     s = scenes.config1()
     res, oc, ost = _trace_both(ctx, port, s.vertices, s.faces, s.absorption, s.source, s.ray_count, s.receivers,
-                               s.max_iterations, s.max_range)
+                               s.max_iterations, s.max_range, flags)
     assert (res.iterations, res.truncated, res.escaped, res.out_of_range) == (
         ost.iterations, ost.truncated, ost.escaped, ost.out_of_range)
     assert res.ray_bounces == ost.ray_bounces
     _compare_captures(res.captures, oc)
 
 
-def test_trace_multi_receiver_and_subset(ctx, port):
+@pytest.mark.parametrize("flags", TREES)
+def test_trace_multi_receiver_and_subset(ctx, port, flags):
     s = scenes.config2()
     recvs = [((6.0, 2.0, 1.2), 0.5), ((1.0, 1.0, 1.0), 0.3), ((4.0, 5.0, 2.5), 0.4)]
     res, oc, ost = _trace_both(ctx, port, s.vertices, s.faces, s.absorption, s.source, s.ray_count, recvs, 50,
-                               686.0, first=3, stride=97, count=0)
+                               686.0, flags, first=3, stride=97, count=0)
     assert res.ray_bounces == ost.ray_bounces
     _compare_captures(res.captures, oc)
 
 
+@pytest.mark.parametrize("flags", TREES)
 @pytest.mark.parametrize("offset,scale", [((1000.0, -2000.0, 500.0), 1.0), ((0.0, 0.0, 0.0), 1e-3),
                                           ((-3.0e4, 1.0e4, 2.0e3), 1.0), ((0.0, 0.0, 0.0), 250.0)])
-def test_trace_far_and_scaled_scenes(ctx, port, offset, scale):
+def test_trace_far_and_scaled_scenes(ctx, port, offset, scale, flags):
     """The conservative fp32 box filter (eps = scale * 2^-19 of the largest
     coordinate, rr_geom.cuh) at other magnitudes: C1 moved 30 km off the
     origin, shrunk to 8 mm, blown up to 2 km — the captures stay
@@ -179,16 +184,18 @@ def test_trace_far_and_scaled_scenes(ctx, port, offset, scale):
     src = tuple(np.asarray(s.source) * scale + np.asarray(offset))
     recvs = [(tuple(np.asarray(c) * scale + np.asarray(offset)), r * scale) for c, r in s.receivers]
     res, oc, ost = _trace_both(ctx, port, v, s.faces, s.absorption, src, 4000, recvs, s.max_iterations,
-                               s.max_range * scale)
+                               s.max_range * scale, flags)
     assert res.ray_bounces == ost.ray_bounces and len(oc) > 0
     _compare_captures(res.captures, oc)
 
 
-def test_trace_soup_interior_rays(ctx, port):
+@pytest.mark.parametrize("flags", TREES)
+def test_trace_soup_interior_rays(ctx, port, flags):
     """An unstructured soup (overlapping boxes, no planes to cull) with rays
     from inside it: 20 000 rays, 30 bounces, escapes."""
     v, f, a = scenes.random_soup(424242, 20000, 10.0, 0.6)
     a = np.full_like(a, 0.05)
-    res, oc, ost = _trace_both(ctx, port, v, f, a, (5.0, 5.0, 5.0), 20000, [((4.0, 6.0, 5.5), 0.7)], 30, 200.0)
+    res, oc, ost = _trace_both(ctx, port, v, f, a, (5.0, 5.0, 5.0), 20000, [((4.0, 6.0, 5.5), 0.7)], 30, 200.0,
+                               flags)
     assert res.escaped == ost.escaped and res.ray_bounces == ost.ray_bounces
     _compare_captures(res.captures, oc)
