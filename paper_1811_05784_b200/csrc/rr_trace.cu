@@ -26,13 +26,17 @@
 #ifndef RR_W8_MINB
 #define RR_W8_MINB 6  // blocks of 128 per SM the 8-wide kernel's register budget targets
 #endif
+#ifndef RR_G8_MINB
+#define RR_G8_MINB 8  // blocks of 128 per SM for the cooperative 8-wide kernel
+#endif
 #ifndef RR_W8_UNR
 #define RR_W8_UNR 8  // internal nodes a lane may visit between leaf votes
 #endif
 
 namespace rr {
 
-constexpr int kStack8 = 96;  // 8-wide traversal stack (entries); the tree's bound must fit
+constexpr int kStack8 = 96;   // 8-wide traversal stack (entries); the tree's bound must fit
+constexpr int kStackG8 = 48;  // cooperative kernel: shared-memory stack per group (16 groups per block)
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
   if (p.block > 0) {
@@ -53,6 +57,10 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
   sincos_emit(phi, &s, &c);
   return d3(rho * c, rho * s, z);
 }
+
+}  // namespace rr
+#include "rr_trace_g8.cuh"
+namespace rr {
 
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
 // V = 1: binary nodes, fp64 test at every leaf (default)
@@ -634,15 +642,24 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     return e ? std::atoi(e) : -1;
   }();
   const bool wide4 = s->s4nodes.p != nullptr && df_env == 23;
-  const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8;
-  auto dfk = wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, false, RR_W8_UNR, 0, false, 2, false>
+  // 8-wide: the cooperative kernel (8 lanes per ray, rr_trace_g8.cuh); RR_G8=0
+  // selects the one-lane-per-ray variant (closest_hit8_pl) for A/B timing
+  static const int g8_env = [] {
+    const char* e = std::getenv("RR_G8");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool coop8 = want8 && s->wnodes.p != nullptr && g8_env != 0 && s->wstack_int <= kStackG8;
+  const bool wide8 = want8 && s->wnodes.p != nullptr && !coop8 && s->wstack <= kStack8;
+  auto dfk = coop8 ? trace_kernel_g8<RR_G8_MINB, kStackG8>
+           : wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, false, RR_W8_UNR, 0, false, 2, false>
            : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, true, RR_W8_UNR, 0, false, 2, false>
-                : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
+    dfk = coop8   ? trace_kernel_g8<RR_G8_MINB, kStackG8, true>
+          : wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, true, RR_W8_UNR, 0, false, 2, false>
+                  : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;

@@ -137,10 +137,11 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, d
 
 __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __restrict__ nslot,
                              const unsigned long long* __restrict__ offs, int32_t n, int32_t level_base,
-                             int32_t next_base, const int32_t* __restrict__ acc, const FaceTri* __restrict__ tri,
+                             int32_t next_base, int32_t tri_base, const int32_t* __restrict__ acc,
+                             const FaceTri* __restrict__ tri,
                              double margin, WNode* __restrict__ out, FaceTri* __restrict__ wtri,
                              int32_t* __restrict__ next_frontier, int32_t* __restrict__ next_acc,
-                             int32_t* __restrict__ bound) {
+                             int32_t* __restrict__ bound, int32_t* __restrict__ bound_int) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
@@ -148,7 +149,7 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
   for (int k = 0; k < cnt; ++k) s[k] = slots[static_cast<int64_t>(i) * kW + k];
   const unsigned long long o = offs[i];
   const int32_t ci = static_cast<int32_t>(o >> 32);  // rank of my first internal child in the next level
-  const int32_t ti = static_cast<int32_t>(o & 0xffffffffu);
+  const int32_t ti = tri_base + static_cast<int32_t>(o & 0xffffffffu);
   WNode w;
   float p[3];
   uint32_t e[3], lo8[3][2], hi8[3][2];
@@ -162,7 +163,15 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       plane = s[k].plane;
       break;
     }
-  const int32_t a = acc[i] + cnt - 1;  // stack entries while visiting this node's subtree
+  // stack occupancy bounds below this node: every slot but the one taken
+  // pushed (closest_hit8_pl pushes leaves too), or every internal slot but
+  // one (the cooperative kernel tests leaves at once, rr_trace_g8.cuh); acc
+  // carries the former in the low and the latter in the high 16 bits
+  int n_int = 0;
+  for (int k = 0; k < cnt; ++k) n_int += s[k].ref >= 0;
+  const int32_t a_all = (acc[i] & 0xffff) + cnt - 1;
+  const int32_t a_int = (acc[i] >> 16) + max(n_int - 1, 0);
+  const int32_t a = a_all | (a_int << 16);
   int ni = 0, nfc = 0;
   for (int k = 0; k < cnt; ++k) {
     valid |= 1u << k;
@@ -184,7 +193,8 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       nfc += nl;
     }
   }
-  atomicMax(bound, a);
+  atomicMax(bound, a_all);
+  atomicMax(bound_int, a_int);
   w.h = make_float4(p[0], p[1], p[2], __int_as_float(static_cast<int>(e[0] | (e[1] << 8) | (e[2] << 16) |
                                                                        (imask << 24))));
   w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16)));
@@ -207,12 +217,12 @@ void build_wide(rr_scene* s) {
   DevBuf<WNode> nodes;
   nodes.alloc(n_int, st);
   s->wtri.alloc(nf, st);
-  DevBuf<int32_t> fr[2], ac[2], nslot, bound;
+  DevBuf<int32_t> fr[2], ac[2], nslot, bound;  // bound: [all slots, internal slots]
   DevBuf<Slot> slots;
   DevBuf<unsigned long long> packed, offs;
   DevBuf<uint8_t> tmp;
-  bound.alloc(1, st);
-  RR_CUDA(cudaMemsetAsync(bound.p, 0, sizeof(int32_t), st));
+  bound.alloc(2, st);
+  RR_CUDA(cudaMemsetAsync(bound.p, 0, 2 * sizeof(int32_t), st));
   fr[0].alloc(1, st);
   ac[0].alloc(1, st);
   const int32_t root = s->shdr.root_ref, zero = 0;
@@ -241,8 +251,9 @@ void build_wide(rr_scene* s) {
     if (base + n + n_next > n_int) throw Error(RR_RUNTIME, "8-wide collapse: node count bound exceeded");
     fr[1].alloc(std::max(n_next, 1), st);
     ac[1].alloc(std::max(n_next, 1), st);
-    write_kernel<<<grid(n), 256, 0, st>>>(slots.p, nslot.p, offs.p, n, base, base + n, ac[0].p, s->tri.p, margin,
-                                          nodes.p, s->wtri.p + tri_done, fr[1].p, ac[1].p, bound.p);
+    write_kernel<<<grid(n), 256, 0, st>>>(slots.p, nslot.p, offs.p, n, base, base + n,
+                                          static_cast<int32_t>(tri_done), ac[0].p, s->tri.p, margin, nodes.p,
+                                          s->wtri.p, fr[1].p, ac[1].p, bound.p, bound.p + 1);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 5;
     tri_done += n_tri;
@@ -253,14 +264,15 @@ void build_wide(rr_scene* s) {
     std::swap(ac[0], ac[1]);
   }
   if (tri_done != nf) throw Error(RR_RUNTIME, "8-wide collapse: leaf faces do not cover the mesh");
-  int32_t h_bound = 0;
-  RR_CUDA(cudaMemcpyAsync(&h_bound, bound.p, sizeof h_bound, cudaMemcpyDeviceToHost, st));
+  int32_t h_bound[2] = {0, 0};
+  RR_CUDA(cudaMemcpyAsync(h_bound, bound.p, sizeof h_bound, cudaMemcpyDeviceToHost, st));
   // compact copy of the node array
   s->wnodes.alloc(base, st);
   RR_CUDA(cudaMemcpyAsync(s->wnodes.p, nodes.p, sizeof(WNode) * base, cudaMemcpyDeviceToDevice, st));
   RR_CUDA(cudaStreamSynchronize(st));
   s->wroot = 0;
-  s->wstack = h_bound + 1;
+  s->wstack = h_bound[0] + 1;
+  s->wstack_int = h_bound[1] + 1;
   s->wdepth = depth;
   s->ctx->launches += 1;
 }
