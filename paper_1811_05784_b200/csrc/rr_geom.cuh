@@ -856,156 +856,84 @@ __device__ __forceinline__ bool test_leaf_w(const FaceTri* __restrict__ wtri, in
   return better;
 }
 
-// byte k of the (w0, w1) pair as an exact fp32 integer: 2^23 + b built by one
-// byte permute, then 2^23 subtracted (exact)
-__device__ __forceinline__ float qbyte(uint32_t w0, uint32_t w1, int k) {
-  const uint32_t w = k < 4 ? w0 : w1;
-  return __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440u | static_cast<uint32_t>(k & 3))) - 8388608.0f;
+// One 8-wide node visit (WNode, rr_wide.cu) for one lane's ray: entry
+// distances of the 8 slots, the mask of slots hit within tmax and not
+// culled, and the slot refs.  A plane of slot k is p + (q - 1) * 2^e; with
+// F = 2^23 + q (one byte permute builds its fp32 bits) the slab distance is
+// fma(F, A, C), A = 2^e * inv (exact: a power of two times inv),
+// C = fl(B - (2^23 + 1) * A), B = fma(p, inv, -o * inv).  The builder's
+// extra grid step on each side covers C's rounding (<= |A| / 2).
+struct WVisit {
+  float t[8];
+  uint32_t hit;      // slots hit
+  uint32_t imask;    // internal slots
+  int32_t child;     // first internal child
+  int32_t tri;       // first leaf face
+  uint32_t leafm, pairm;
+};
+
+__device__ __forceinline__ float wbyte(uint32_t w, int k) {
+  return __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440u | static_cast<uint32_t>(k & 3)));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
 }
 
-// Same contract as closest_hit_pl (postponed, warp-batched leaf tests;
-// pruning by the best hit so far; coplanar cull), over 8-wide nodes: the
-// hit slots are pushed farthest first and the nearest is continued.  STK
-// bounds the stack (the builder's occupancy bound s->wstack must fit).
-template <int LEAFT, int STUCKT, typename RAY, int UNR, int TOS, int STK, bool CNT = false>
-__device__ __forceinline__ HitResult closest_hit8_pl(const TravHeader& h, const WNode* __restrict__ wn,
-                                                     const FaceTri* __restrict__ wtri, const RAY& ray,
-                                                     int32_t rplane, unsigned long long* cnt = nullptr) {
-  HitResult best{0.0, -1};
-  RayF r;
-  if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
-  const float kInf = __int_as_float(0x7f800000);
-  float tbest = FLT_MAX;
-  int32_t node = box_enter(r, h.lo[0], h.hi[0], h.lo[1], h.hi[1], h.lo[2], h.hi[2], tbest) == kInf ? kDone : 0;
-  const bool px = r.ix >= 0.0f, py = r.iy >= 0.0f, pz = r.iz >= 0.0f;
-  int2 st[STK];
-  int sp = 0;
-  int2 top[TOS > 0 ? TOS : 1] = {};
-  int n_top = 0;
-  int32_t leaf = 0;
-  auto push = [&](int2 e) {
-    if (TOS > 0) {
-      if (n_top == TOS) st[sp++] = top[TOS - 1];
+__device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t node, const RayF& r, bool px, bool py,
+                                         bool pz, float tmax, int32_t rplane, WVisit& v) {
+  const float4* q = reinterpret_cast<const float4*>(wn + node);
+  const float4 hh = __ldg(q);
+  const int4 mm = __ldg(reinterpret_cast<const int4*>(q + 1));
+  const uint4 qx = __ldg(reinterpret_cast<const uint4*>(q + 2));
+  const uint4 qy = __ldg(reinterpret_cast<const uint4*>(q + 3));
+  const uint4 qz = __ldg(reinterpret_cast<const uint4*>(q + 4));
+  const uint32_t hw = __float_as_uint(hh.w);
+  const float ax = __uint_as_float((hw & 0xffu) << 23) * r.ix;
+  const float ay = __uint_as_float(((hw >> 8) & 0xffu) << 23) * r.iy;
+  const float az = __uint_as_float(((hw >> 16) & 0xffu) << 23) * r.iz;
+  const float cx = __fmaf_rn(-8388609.0f, ax, __fmaf_rn(hh.x, r.ix, r.nx));
+  const float cy = __fmaf_rn(-8388609.0f, ay, __fmaf_rn(hh.y, r.iy, r.ny));
+  const float cz = __fmaf_rn(-8388609.0f, az, __fmaf_rn(hh.z, r.iz, r.nz));
+  // near / far plane words per axis from the ray's octant
+  const uint32_t nx0 = px ? qx.x : qx.z, nx1 = px ? qx.y : qx.w, fx0 = px ? qx.z : qx.x, fx1 = px ? qx.w : qx.y;
+  const uint32_t ny0 = py ? qy.x : qy.z, ny1 = py ? qy.y : qy.w, fy0 = py ? qy.z : qy.x, fy1 = py ? qy.w : qy.y;
+  const uint32_t nz0 = pz ? qz.x : qz.z, nz1 = pz ? qz.y : qz.w, fz0 = pz ? qz.z : qz.x, fz1 = pz ? qz.w : qz.y;
+  const uint32_t bits = static_cast<uint32_t>(mm.w);
+  const uint32_t cull = mm.z == rplane ? (bits >> 16) & 0xffu : 0u;
+  uint32_t hit = 0;
 #pragma unroll
-      for (int k = TOS - 1; k > 0; --k) top[k] = top[k - 1];
-      top[0] = e;
-      n_top = min(n_top + 1, TOS);
-    } else {
-      st[sp++] = e;
-    }
-  };
-  auto pop = [&]() {
-    node = kDone;
-    while (TOS > 0 && n_top > 0) {
-      const int2 e = top[0];
-#pragma unroll
-      for (int k = 0; k + 1 < TOS; ++k) top[k] = top[k + 1];
-      --n_top;
-      if (__int_as_float(e.y) <= tbest) {
-        node = e.x;
-        return;
-      }
-    }
-    while (sp > 0) {
-      --sp;
-      const int2 e = st[sp];
-      if (__int_as_float(e.y) <= tbest) {
-        node = e.x;
-        break;
-      }
-    }
-  };
-  while (node != kDone || leaf != 0) {
-#pragma unroll 1
-    for (int u = 0; u < UNR && is_inner(node) && (u == 0 || leaf == 0); ++u) {
-      if (CNT) ++cnt[0];
-      const float4* q = reinterpret_cast<const float4*>(wn + node);
-      const float4 hh = __ldg(q);
-      const int4 mm = __ldg(reinterpret_cast<const int4*>(q + 1));
-      const uint4 qx = __ldg(reinterpret_cast<const uint4*>(q + 2));
-      const uint4 qy = __ldg(reinterpret_cast<const uint4*>(q + 3));
-      const uint4 qz = __ldg(reinterpret_cast<const uint4*>(q + 4));
-      const uint32_t hw = __float_as_uint(hh.w);
-      const float ax = __uint_as_float((hw & 0xffu) << 23) * r.ix;
-      const float ay = __uint_as_float(((hw >> 8) & 0xffu) << 23) * r.iy;
-      const float az = __uint_as_float(((hw >> 16) & 0xffu) << 23) * r.iz;
-      const float bx = __fmaf_rn(hh.x, r.ix, r.nx), by = __fmaf_rn(hh.y, r.iy, r.ny), bz = __fmaf_rn(hh.z, r.iz, r.nz);
-      // near / far planes per axis from the ray's octant
-      const uint32_t nx0 = px ? qx.x : qx.z, nx1 = px ? qx.y : qx.w, fx0 = px ? qx.z : qx.x, fx1 = px ? qx.w : qx.y;
-      const uint32_t ny0 = py ? qy.x : qy.z, ny1 = py ? qy.y : qy.w, fy0 = py ? qy.z : qy.x, fy1 = py ? qy.w : qy.y;
-      const uint32_t nz0 = pz ? qz.x : qz.z, nz1 = pz ? qz.y : qz.w, fz0 = pz ? qz.z : qz.x, fz1 = pz ? qz.w : qz.y;
-      const uint32_t bits = static_cast<uint32_t>(mm.w);
-      const uint32_t cull = mm.z == rplane ? (bits >> 16) & 0xffu : 0u;
-      const uint32_t valid = bits & 0xffu & ~cull;
-      float tk[8];
-      uint32_t hitm = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float tnx = __fmaf_rn(qbyte(nx0, nx1, k), ax, bx), tfx = __fmaf_rn(qbyte(fx0, fx1, k), ax, bx);
-        const float tny = __fmaf_rn(qbyte(ny0, ny1, k), ay, by), tfy = __fmaf_rn(qbyte(fy0, fy1, k), ay, by);
-        const float tnz = __fmaf_rn(qbyte(nz0, nz1, k), az, bz), tfz = __fmaf_rn(qbyte(fz0, fz1, k), az, bz);
-        const float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, 0.0f));
-        const float tf = fminf(fminf(tfx, tfy), fminf(tfz, tbest));
-        tk[k] = tn;
-        if (tn <= tf) hitm |= 1u << k;
-      }
-      hitm &= valid;
-      const uint32_t imask = hw >> 24;
-      const uint32_t leafm = (bits & 0xffu) & ~imask, pairm = (bits >> 8) & 0xffu;
-      auto ref_of = [&](int k) -> int32_t {
-        const uint32_t below = (1u << k) - 1u;
-        if ((imask >> k) & 1u) return mm.x + __popc(imask & below);
-        const int32_t t = mm.y + __popc(leafm & below) + __popc(pairm & leafm & below);
-        return ~(t | (((pairm >> k) & 1u) ? kPairBit : 0));
-      };
-      if (hitm == 0) {
-        pop();
-      } else {
-        while (hitm & (hitm - 1u)) {  // two or more: push the farthest
-          float tmx = -1.0f;
-          int kmx = 0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (((hitm >> k) & 1u) && tk[k] > tmx) {
-              tmx = tk[k];
-              kmx = k;
-            }
-          push(make_int2(ref_of(kmx), __float_as_int(tmx)));
-          hitm &= ~(1u << kmx);
-        }
-        node = ref_of(__ffs(hitm) - 1);
-      }
-      if (node < 0 && node != kDone && leaf == 0) {  // stash a reached leaf and keep traversing
-        leaf = node;
-        pop();
-      }
-    }
-    if (node < 0 && node != kDone && leaf == 0) {  // a popped leaf with no node visit
-      leaf = node;
-      pop();
-    }
-    const unsigned act = __activemask();
-    const unsigned hv = __ballot_sync(act, leaf != 0);
-    if (hv == 0) continue;
-    const bool can = is_inner(node);
-    const bool must = leaf != 0 && !can;
-    const unsigned mv = __ballot_sync(act, must);
-    const unsigned cv = __ballot_sync(act, can);
-    const int na = __popc(act);
-    const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
-    if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
-      if (leaf != 0) {
-        if (CNT) cnt[1] += leaf_faces(leaf);
-        if (test_leaf_w(wtri, leaf, ray.org(), ray.dir(), best)) tbest = prune_bound(best.delta, r.shift);
-        leaf = 0;
-        if (node < 0 && node != kDone) {  // the leaf that waited for the slot
-          leaf = node;
-          pop();
-        }
-      }
-    }
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t wnx = k < 4 ? nx0 : nx1, wfx = k < 4 ? fx0 : fx1;
+    const uint32_t wny = k < 4 ? ny0 : ny1, wfy = k < 4 ? fy0 : fy1;
+    const uint32_t wnz = k < 4 ? nz0 : nz1, wfz = k < 4 ? fz0 : fz1;
+    const float tn = fmax3(__fmaf_rn(wbyte(wnx, k), ax, cx), __fmaf_rn(wbyte(wny, k), ay, cy),
+                           __fmaf_rn(wbyte(wnz, k), az, cz));
+    const float tf = fmin3(__fmaf_rn(wbyte(wfx, k), ax, cx), __fmaf_rn(wbyte(wfy, k), ay, cy),
+                           __fmaf_rn(wbyte(wfz, k), az, cz));
+    v.t[k] = tn;
+    if (tn <= fminf(tf, tmax) && tf >= 0.0f) hit |= 1u << k;
   }
-  return best;
+  v.hit = hit & bits & 0xffu & ~cull;
+  v.imask = hw >> 24;
+  v.child = mm.x;
+  v.tri = mm.y;
+  v.leafm = (bits & 0xffu) & ~v.imask;
+  v.pairm = (bits >> 8) & 0xffu;
+}
+
+// ref of slot k: internal -> WNode index; leaf -> ~(first face | kPairBit if 2)
+__device__ __forceinline__ int32_t wref(const WVisit& v, int k) {
+  const uint32_t below = (1u << k) - 1u;
+  if ((v.imask >> k) & 1u) return v.child + __popc(v.imask & below);
+  const int32_t t = v.tri + __popc(v.leafm & below) + __popc(v.pairm & v.leafm & below);
+  return ~(t | (((v.pairm >> k) & 1u) ? kPairBit : 0));
 }
 
 }  // namespace rr

@@ -201,7 +201,7 @@ struct rr_scene {
   rr::DevBuf<rr::FaceTri> wtri;   // faces in its leaf order, pad = the face id (int64 bits)
   int32_t wroot = -1;             // WNode root (0) when built
   int32_t wstack = 0;             // bound on the traversal stack occupancy over the 8-wide tree
-  int32_t wstack_int = 0;         // the same when only internal slots are pushed (cooperative kernel)
+  bool wide_ok = false;           // every grid step <= 16 (no fp32 overflow in the slab form)
   int32_t wdepth = 0;
   int32_t s4root = -1;
   int32_t sah_depth = 0;

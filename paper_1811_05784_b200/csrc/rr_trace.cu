@@ -23,20 +23,9 @@
 #include "rr_sincos.cuh"
 #include "rr_trace.cuh"
 
-#ifndef RR_W8_MINB
-#define RR_W8_MINB 6  // blocks of 128 per SM the 8-wide kernel's register budget targets
-#endif
-#ifndef RR_G8_MINB
-#define RR_G8_MINB 8  // blocks of 128 per SM for the cooperative 8-wide kernel
-#endif
-#ifndef RR_W8_UNR
-#define RR_W8_UNR 8  // internal nodes a lane may visit between leaf votes
-#endif
-
 namespace rr {
 
-constexpr int kStack8 = 96;   // 8-wide traversal stack (entries); the tree's bound must fit
-constexpr int kStackG8 = 48;  // cooperative kernel: shared-memory stack per group (16 groups per block)
+constexpr int kStack8 = 96;  // 8-wide traversal stack (entries); the tree's bound must fit
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
   if (p.block > 0) {
@@ -59,7 +48,7 @@ __device__ __forceinline__ D3 fib_dir(int64_t k, int64_t n, double az_step) {
 }
 
 }  // namespace rr
-#include "rr_trace_g8.cuh"
+#include "rr_trace_w8.cuh"
 namespace rr {
 
 // V = 0: binary nodes, fp32 leaf classification + fp64 resolution (diagnostic)
@@ -134,9 +123,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     HitResult wall;
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
-    } else if (V == 4) {
-      wall = closest_hit8_pl<PL, ST, RegRay, UNR, TOS, kStack8, CNT>(p.hdr, p.wnodes, p.wtri, RegRay{o, d}, rplane,
-                                                                   st_cnt);
     } else if (V == 3) {
       wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
     } else if (V == 1 && PL > 0) {
@@ -642,24 +628,24 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     return e ? std::atoi(e) : -1;
   }();
   const bool wide4 = s->s4nodes.p != nullptr && df_env == 23;
-  // 8-wide: the cooperative kernel (8 lanes per ray, rr_trace_g8.cuh); RR_G8=0
-  // selects the one-lane-per-ray variant (closest_hit8_pl) for A/B timing
-  static const int g8_env = [] {
-    const char* e = std::getenv("RR_G8");
-    return e ? std::atoi(e) : 1;
+  // 8-wide compressed tree: trace_kernel_w8 (rr_trace_w8.cuh); RR_W8V
+  // selects an A/B variant (MINB, DONET, UNR)
+  static const int w8v = [] {
+    const char* e = std::getenv("RR_W8V");
+    return e ? std::atoi(e) : 0;
   }();
-  const bool coop8 = want8 && s->wnodes.p != nullptr && g8_env != 0 && s->wstack_int <= kStackG8;
-  const bool wide8 = want8 && s->wnodes.p != nullptr && !coop8 && s->wstack <= kStack8;
-  auto dfk = coop8 ? trace_kernel_g8<RR_G8_MINB, kStackG8>
-           : wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, false, RR_W8_UNR, 0, false, 2, false>
-           : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
+  const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8 && s->wide_ok;
+  using KFn = void (*)(const TraceParams);
+  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 16, 8, kStack8> : w8v == 2 ? trace_kernel_w8<6, 8, 8, kStack8>
+          : w8v == 3 ? trace_kernel_w8<6, 24, 8, kStack8> : w8v == 4 ? trace_kernel_w8<6, 16, 4, kStack8>
+          : w8v == 5 ? trace_kernel_w8<6, 16, 16, kStack8> : w8v == 6 ? trace_kernel_w8<5, 16, 8, kStack8>
+                     : trace_kernel_w8<6, 16, 8, kStack8>;
+  auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = coop8   ? trace_kernel_g8<RR_G8_MINB, kStackG8, true>
-          : wide8 ? trace_kernel<4, RR_W8_MINB, false, 16, -2, true, RR_W8_UNR, 0, false, 2, false>
-                  : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
+    dfk = wide8 ? trace_kernel_w8<6, 16, 8, kStack8, true> : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;

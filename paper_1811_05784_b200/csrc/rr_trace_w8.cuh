@@ -1,0 +1,298 @@
+// K3w — the tracer over the 8-wide compressed tree (rr_wide.cu), for deep
+// scenes (default from 2^18 faces: C3, C5).  Included by rr_trace.cu.
+//
+// Same contract as trace_kernel (tracer.cpp:19-149: step_ray per bounce,
+// receiver captures, reflection, range / iteration termination, statistics),
+// restructured so that lanes do not idle behind the slowest traversal of
+// their warp:
+//  * every lane owns one ray and keeps its traversal state (node, stack,
+//    stashed leaf, best hit) across loop iterations;
+//  * traversal phase: lanes still searching visit up to UNR 8-wide nodes
+//    (visit_w8: 8 quantized slab tests; hit slots pushed farthest first, the
+//    nearest continued), reached leaves are stashed and tested in warp-voted
+//    batches (as in closest_hit_pl), until at least DONET lanes of the warp
+//    have finished their closest-hit query (or none is searching);
+//  * shading phase: the finished lanes together do the receiver tests and
+//    the warp-aggregated capture append, reflect, write the face history,
+//    terminate, take new rays from the global counter and start their next
+//    query.
+// Without the batching a warp's bounce lasts as long as its slowest lane's
+// query: on C5 (17 node visits per ray-bounce on average) only ~7 of 32
+// lanes were active per node visit.
+#pragma once
+
+namespace rr {
+
+template <int MINB, int DONET, int UNR, int STK, bool CNT = false>
+__global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const float kInf = __int_as_float(0x7f800000);
+  // ray
+  int64_t ray = -1;
+  bool exhausted = false;
+  D3 o{}, d{};
+  double path = 0.0;
+  int32_t steps = 0, bounces = 0, rplane = -2;
+  // traversal of the current step
+  bool searching = false;  // a closest-hit query is in progress
+  RayF r{};
+  bool px = true, py = true, pz = true;
+  float tbest = FLT_MAX;
+  HitResult best{0.0, -1};
+  int32_t node = kDone, leaf = 0;
+  int2 st[STK];
+  int sp = 0;
+  int2 top[2] = {};
+  int n_top = 0;
+  uint32_t st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
+  unsigned long long st_cnt[2] = {0, 0};
+  int32_t st_max = 0;
+
+  auto push = [&](int2 e) {
+    if (n_top == 2) st[sp++] = top[1];
+    top[1] = top[0];
+    top[0] = e;
+    n_top = min(n_top + 1, 2);
+  };
+  auto pop = [&]() {
+    node = kDone;
+    while (n_top > 0) {
+      const int2 e = top[0];
+      top[0] = top[1];
+      --n_top;
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        return;
+      }
+    }
+    while (sp > 0) {
+      --sp;
+      const int2 e = st[sp];
+      if (__int_as_float(e.y) <= tbest) {
+        node = e.x;
+        break;
+      }
+    }
+  };
+  // start the closest-hit query of the next step_ray
+  auto begin_query = [&]() {
+    ++steps;
+    best = HitResult{0.0, -1};
+    tbest = FLT_MAX;
+    sp = 0;
+    n_top = 0;
+    leaf = 0;
+    node = kDone;
+    if (make_rayf(p.hdr, o, d, r)) {
+      const float t0 = box_enter(r, p.hdr.lo[0], p.hdr.hi[0], p.hdr.lo[1], p.hdr.hi[1], p.hdr.lo[2], p.hdr.hi[2],
+                                 tbest);
+      node = t0 == kInf ? kDone : 0;
+    }
+    px = r.ix >= 0.0f;
+    py = r.iy >= 0.0f;
+    pz = r.iz >= 0.0f;
+    searching = true;
+  };
+
+  for (;;) {
+    // ---------------- shading: rays whose query finished, and new rays
+    const bool shade = ray >= 0 && !searching;
+    if (shade) {
+      const bool has_wall = best.face >= 0;
+      for (int rc = 0; rc < p.n_recv; ++rc) {
+        const double sd = sphere_delta(o, d, d3(p.rc[rc][0], p.rc[rc][1], p.rc[rc][2]), p.rr[rc]);
+        bool cap = sd > 0.0 && (!has_wall || sd < best.delta);
+        double L = 0.0;
+        if (cap) {
+          L = path + sd;
+          cap = L <= p.rng[rc];  // resolved_max_range of receiver rc
+        }
+        const unsigned act = __activemask();
+        const unsigned cm = __ballot_sync(act, cap);
+        if (cm) {
+          const int leader = __ffs(cm) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(p.cap_count, (unsigned long long)__popc(cm));
+          base = __shfl_sync(act, base, leader);
+          if (cap) {
+            const unsigned long long slot = base + __popc(cm & lt_mask);
+            if (slot < static_cast<unsigned long long>(p.cap_capacity)) {
+              Capture c;
+              const D3 pt = o + sd * d;
+              c.p[0] = pt.x; c.p[1] = pt.y; c.p[2] = pt.z;
+              c.d[0] = d.x; c.d[1] = d.y; c.d[2] = d.z;
+              c.path = L;
+              c.ray = static_cast<int32_t>(ray);
+              c.meta = (bounces << 8) | rc;
+              p.caps[slot] = c;
+            }
+          }
+        }
+      }
+      bool dead = false;
+      if (!has_wall) {
+        dead = true;
+        st_esc++;
+      } else {
+        const double* nn = p.normal + 3 * static_cast<int64_t>(best.face);
+        D3 n = d3(__ldg(nn), __ldg(nn + 1), __ldg(nn + 2));
+        if (dot(n, d) > 0.0) n = d3(-n.x, -n.y, -n.z);
+        const D3 pt = o + best.delta * d;
+        const double s2 = 2.0 * dot(d, n);
+        d = d - s2 * n;  // reflect, tracer.hpp:33-37
+        o = pt;
+        // the next segment leaves this face's plane: cull coplanar subtrees
+        // (p.cull_min: see run_trace)
+        const int32_t pid = __ldg(p.face_plane + best.face);
+        if (pid >= 0) {
+          const int k = pid >> 29;
+          const double dk = k == 0 ? d.x : (k == 1 ? d.y : d.z);
+          rplane = fabs(dk) > p.cull_min ? pid : -2;
+        } else {
+          rplane = -2;
+        }
+        path += best.delta;
+        p.hist[ray * p.H + bounces] = best.face;
+        ++bounces;
+        if (path > p.max_range) {
+          dead = true;
+          st_oor++;
+        }
+      }
+      if (!dead && steps >= p.max_iter) {
+        dead = true;
+        st_alive++;
+      }
+      if (dead) {
+        st_bounce += steps;
+        st_max = max(st_max, steps);
+        ray = -1;
+      } else {
+        begin_query();
+      }
+    }
+    // new rays (warp-aggregated fetch from the global counter)
+    const bool need = ray < 0 && !exhausted;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(p.ray_counter, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int64_t c = static_cast<int64_t>(base) + __popc(m & lt_mask);
+        if (c < p.count) {
+          const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + c)) : c;
+          ray = i;
+          o = d3(p.src[0], p.src[1], p.src[2]);
+          d = p.dirs ? d3(p.dirs[3 * i], p.dirs[3 * i + 1], p.dirs[3 * i + 2])
+                     : fib_dir(global_ray(p, i), p.N, p.az_step);
+          path = 0.0;
+          steps = 0;
+          bounces = 0;
+          rplane = -2;
+          if (p.max_iter <= 0) {  // trace() with a zero cap: nothing runs
+            st_alive++;
+            ray = -1;
+          } else {
+            begin_query();
+          }
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, ray < 0 && exhausted)) break;
+
+    // ---------------- traversal until DONET lanes wait for shading
+    for (;;) {
+      if (searching) {
+#pragma unroll 1
+        for (int u = 0; u < UNR && is_inner(node) && (u == 0 || leaf == 0); ++u) {
+          if (CNT) ++st_cnt[0];
+          WVisit v;
+          visit_w8(p.wnodes, node, r, px, py, pz, tbest, rplane, v);
+          uint32_t hm = v.hit;
+          if (hm == 0) {
+            pop();
+          } else {
+            while (hm & (hm - 1u)) {  // two or more: push the farthest
+              float tmx = -kInf;
+              int kmx = 0;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (((hm >> k) & 1u) && v.t[k] > tmx) {
+                  tmx = v.t[k];
+                  kmx = k;
+                }
+              push(make_int2(wref(v, kmx), __float_as_int(tmx)));
+              hm &= ~(1u << kmx);
+            }
+            node = wref(v, __ffs(hm) - 1);
+          }
+          if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
+            leaf = node;
+            pop();
+          }
+        }
+        if (node < 0 && leaf == 0) {  // a popped leaf with no node visit
+          leaf = node;
+          pop();
+        }
+        // batched fp64 leaf tests (closest_hit_pl's vote)
+        const unsigned act = __activemask();
+        const unsigned hv = __ballot_sync(act, leaf != 0);
+        if (hv != 0) {
+          const bool can = is_inner(node);
+          const bool must = leaf != 0 && !can;
+          const unsigned mv = __ballot_sync(act, must);
+          const unsigned cv = __ballot_sync(act, can);
+          const int na = __popc(act);
+          if (2 * __popc(mv) >= na || cv == 0 || 2 * __popc(hv) >= na) {
+            if (leaf != 0) {
+              if (CNT) st_cnt[1] += leaf_faces(leaf);
+              if (test_leaf_w(p.wtri, leaf, o, d, best)) tbest = prune_bound(best.delta, r.shift);
+              leaf = 0;
+              if (node < 0) {  // the leaf that waited for the slot
+                leaf = node;
+                pop();
+              }
+            }
+          }
+        }
+        if (node == kDone && leaf == 0) searching = false;  // query done: best holds the hit
+      }
+      const unsigned sv = __ballot_sync(0xffffffffu, searching);
+      const unsigned wv = __ballot_sync(0xffffffffu, ray >= 0 && !searching);
+      if (sv == 0 || __popc(wv) >= DONET) break;
+    }
+  }
+  // ---- statistics
+  for (int off = 16; off > 0; off >>= 1) {
+    st_bounce += __shfl_xor_sync(0xffffffffu, st_bounce, off);
+    st_esc += __shfl_xor_sync(0xffffffffu, st_esc, off);
+    st_oor += __shfl_xor_sync(0xffffffffu, st_oor, off);
+    st_alive += __shfl_xor_sync(0xffffffffu, st_alive, off);
+    st_max = max(st_max, __shfl_xor_sync(0xffffffffu, st_max, off));
+  }
+  if (lane == 0) {
+    atomicAdd(p.stats + 0, (unsigned long long)st_bounce);
+    atomicAdd(p.stats + 1, (unsigned long long)st_esc);
+    atomicAdd(p.stats + 2, (unsigned long long)st_oor);
+    atomicAdd(p.stats + 3, (unsigned long long)st_alive);
+    atomicMax(p.stats + 4, (unsigned long long)st_max);
+  }
+  if (CNT) {
+    for (int off = 16; off > 0; off >>= 1) {
+      st_cnt[0] += __shfl_xor_sync(0xffffffffu, st_cnt[0], off);
+      st_cnt[1] += __shfl_xor_sync(0xffffffffu, st_cnt[1], off);
+    }
+    if (lane == 0) {
+      atomicAdd(p.stats + 5, st_cnt[0]);
+      atomicAdd(p.stats + 6, st_cnt[1]);
+    }
+  }
+}
+
+}  // namespace rr

@@ -27,12 +27,13 @@
 // gives identical results.  Each slot's box is the binary node's
 // conservative fp32 child box (exact box + eps, rounded outward; eps =
 // scale * 2^-19 bounds the fp32 slab error, rr_geom.cuh box_enter) widened
-// by another eps/4 and rounded outward onto the grid: q_lo = floor, q_hi =
-// ceil, evaluated in fp64 on the exact grid values p + q * 2^e.  The node
-// traversal evaluates a plane as fma(q, 2^e * inv, fma(p, inv, -o * inv)):
-// two roundings more than box_enter's fma(l, inv, -o * inv), each below
-// 6 * scale * 2^-24 in space units (|q * 2^e|, |p - o| <= 6 scale), so
-// < 0.2 eps altogether, inside the extra eps/4.
+// by another eps/4 and rounded outward onto the grid, one more grid step
+// on each side (quant_axis), evaluated in fp64 on the exact grid values.  The
+// node traversal evaluates a plane as fma(2^23 + q, A, C) (rr_geom.cuh
+// wslab): its rounding of C is at most half a grid step (covered by the
+// extra step), the other two roundings (B = fma(p, inv, -o * inv) and the
+// final fma) are below 6 * scale * 2^-24 each in space units (|q * 2^e|,
+// |p - o| <= 6 scale), < 0.2 eps together, inside the extra eps/4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -106,7 +107,12 @@ __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __res
   packed[i] = (ni << 32) | nfc;
 }
 
-// exact grid values: plane = p + q * 2^(e-127); returns the biased exponent
+// Grid of one axis: plane(q) = p + (q - 1) * 2^(e-127), q in [0, 255]
+// (p fp32, exact in fp64).  Each slot gets q_lo one step below the floor and
+// q_hi one step above the ceiling of its margin-widened box: the traversal
+// evaluates t = fma(2^23 + q, A, C) with A = 2^(e-127) * inv (exact) and
+// C = fl(B - (2^23 + 1) A), whose rounding is at most |A| / 2, i.e. half a
+// grid step in space units (rr_geom.cuh wslab).  Returns the biased exponent.
 __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, double m, float* p_out,
                                                uint32_t* lo8, uint32_t* hi8) {
   double lo = 1e300, hi = -1e300;
@@ -116,16 +122,18 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, d
   }
   const float p = __double2float_rd(lo);
   const double pd = static_cast<double>(p);
-  // smallest power of two with (hi - p) <= 255 * scale
-  int e = static_cast<int>(ceil(log2((hi - pd) / 255.0)));
-  while (ldexp(255.0, e) < hi - pd) ++e;
-  while (e > -126 && ldexp(255.0, e - 1) >= hi - pd) --e;
+  // smallest power of two with (hi - p) <= 253 * scale (q = plane step + 1,
+  // one step of slack below and above)
+  int e = static_cast<int>(ceil(log2((hi - pd) / 253.0)));
+  while (ldexp(253.0, e) < hi - pd) ++e;
+  while (e > -126 && ldexp(253.0, e - 1) >= hi - pd) --e;
   e = max(e, -126);
   const double sc = ldexp(1.0, e);
   lo8[0] = lo8[1] = hi8[0] = hi8[1] = 0;
   for (int k = 0; k < cnt; ++k) {
+    // q - 1 = floor(..) - 1 and ceil(..) + 1
     double ql = floor((static_cast<double>(s[k].b[2 * ax]) - m - pd) / sc);
-    double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc);
+    double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc) + 2.0;
     ql = fmin(fmax(ql, 0.0), 255.0);
     qh = fmin(fmax(qh, 0.0), 255.0);
     lo8[k >> 2] |= static_cast<uint32_t>(ql) << (8 * (k & 3));
@@ -141,7 +149,7 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
                              const FaceTri* __restrict__ tri,
                              double margin, WNode* __restrict__ out, FaceTri* __restrict__ wtri,
                              int32_t* __restrict__ next_frontier, int32_t* __restrict__ next_acc,
-                             int32_t* __restrict__ bound, int32_t* __restrict__ bound_int) {
+                             int32_t* __restrict__ bound, int32_t* __restrict__ emax) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
@@ -163,15 +171,9 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       plane = s[k].plane;
       break;
     }
-  // stack occupancy bounds below this node: every slot but the one taken
-  // pushed (closest_hit8_pl pushes leaves too), or every internal slot but
-  // one (the cooperative kernel tests leaves at once, rr_trace_g8.cuh); acc
-  // carries the former in the low and the latter in the high 16 bits
-  int n_int = 0;
-  for (int k = 0; k < cnt; ++k) n_int += s[k].ref >= 0;
-  const int32_t a_all = (acc[i] & 0xffff) + cnt - 1;
-  const int32_t a_int = (acc[i] >> 16) + max(n_int - 1, 0);
-  const int32_t a = a_all | (a_int << 16);
+  // stack occupancy bound below this node: every slot but the one taken
+  // pushed (trace_kernel_w8 pushes leaf slots too)
+  const int32_t a = acc[i] + cnt - 1;
   int ni = 0, nfc = 0;
   for (int k = 0; k < cnt; ++k) {
     valid |= 1u << k;
@@ -193,8 +195,8 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       nfc += nl;
     }
   }
-  atomicMax(bound, a_all);
-  atomicMax(bound_int, a_int);
+  atomicMax(bound, a);
+  atomicMax(emax, static_cast<int32_t>(max(e[0], max(e[1], e[2]))));
   w.h = make_float4(p[0], p[1], p[2], __int_as_float(static_cast<int>(e[0] | (e[1] << 8) | (e[2] << 16) |
                                                                        (imask << 24))));
   w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16)));
@@ -217,7 +219,7 @@ void build_wide(rr_scene* s) {
   DevBuf<WNode> nodes;
   nodes.alloc(n_int, st);
   s->wtri.alloc(nf, st);
-  DevBuf<int32_t> fr[2], ac[2], nslot, bound;  // bound: [all slots, internal slots]
+  DevBuf<int32_t> fr[2], ac[2], nslot, bound;  // bound: [stack bound, largest grid exponent]
   DevBuf<Slot> slots;
   DevBuf<unsigned long long> packed, offs;
   DevBuf<uint8_t> tmp;
@@ -272,7 +274,9 @@ void build_wide(rr_scene* s) {
   RR_CUDA(cudaStreamSynchronize(st));
   s->wroot = 0;
   s->wstack = h_bound[0] + 1;
-  s->wstack_int = h_bound[1] + 1;
+  // fma(2^23 + q, A, C) with |A| = 2^e |inv| <= 2^e * 1e30 stays finite for
+  // grid steps 2^e <= 16 (scenes up to ~2 km); larger scenes use the binary tree
+  s->wide_ok = h_bound[1] <= 127 + 4;
   s->wdepth = depth;
   s->ctx->launches += 1;
 }
