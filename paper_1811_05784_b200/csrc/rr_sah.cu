@@ -932,9 +932,10 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   s->shdr.root4 = 0;
   s->sah_depth = depth;
   if (depth > kMaxDepth) throw Error(RR_RUNTIME, "SAH tree deeper than the traversal stack");
-  // the 8-wide collapse serves the deep-tree kernel only; smaller scenes
-  // build it on demand (build_wide, rr_trace.cu)
-  if (nf >= (int64_t(1) << 18)) build_wide(s);
+  // the wide collapses serve the deep-tree kernels (rr_trace.cu run_trace
+  // picks the tree by face count); forced choices build theirs on demand
+  if (nf >= (int64_t(1) << 20)) build_wide(s);
+  else if (nf >= (int64_t(1) << 18)) build_sah4(s);
 }
 
 // 4-wide collapse of the SAH tree (traversed by trace_kernel<3, ...>).

@@ -499,13 +499,18 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  if (sah && (df_env0 == 23 || df_env0 == 24)) build_sah4(s);
-  // 8-wide compressed tree for deep scenes (RR_WIDE: face-count threshold,
-  // default 2^18; the 8-wide kernel needs the builder's stack bound to fit)
+  // Trees by scene size (measured): the binary SAH tree
+  // below 2^18 faces; its 4-wide fp32 collapse from 2^18 (C3: 1.06 ms vs
+  // 1.39 binary, 2.09 8-wide); the 8-wide compressed tree from 2^20, where
+  // the binary node array (64 B per face) no longer fits the 126 MB L2
+  // (C5: 657 ms vs 724 4-wide, 997 binary).  RR_WIDE moves the 8-wide threshold.
   static const int64_t wide_min = [] {
     const char* e = std::getenv("RR_WIDE");
-    return e ? std::atoll(e) : int64_t(1) << 18;
+    return e ? std::atoll(e) : int64_t(1) << 20;
   }();
+  const bool want4 = sah && !(cfg->flags & (RR_TRACE_TREE2 | RR_TRACE_TREE8 | RR_TRACE_WIDE)) &&
+                     ((df_env0 < 0 && s->nf >= (1 << 18) && s->nf < wide_min) || df_env0 == 23 || df_env0 == 24);
+  if (want4) build_sah4(s);
   const bool want8 = sah && !(cfg->flags & RR_TRACE_TREE2) && !(cfg->flags & RR_TRACE_WIDE) &&
                      ((cfg->flags & RR_TRACE_TREE8) || (df_env0 < 0 && s->nf >= wide_min));
   if (want8) build_wide(s);
@@ -627,7 +632,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     const char* e = std::getenv("RR_DF");
     return e ? std::atoi(e) : -1;
   }();
-  const bool wide4 = s->s4nodes.p != nullptr && df_env == 23;
+  const bool wide4 = want4 && s->s4nodes.p != nullptr && (df_env < 0 || df_env == 23);
   // 8-wide compressed tree: trace_kernel_w8 (rr_trace_w8.cuh); RR_W8V
   // selects an A/B variant (MINB, DONET, UNR)
   static const int w8v = [] {
@@ -636,16 +641,15 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   }();
   const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8 && s->wide_ok;
   using KFn = void (*)(const TraceParams);
-  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 16, 8, kStack8> : w8v == 2 ? trace_kernel_w8<6, 8, 8, kStack8>
-          : w8v == 3 ? trace_kernel_w8<6, 24, 8, kStack8> : w8v == 4 ? trace_kernel_w8<6, 16, 4, kStack8>
-          : w8v == 5 ? trace_kernel_w8<6, 16, 16, kStack8> : w8v == 6 ? trace_kernel_w8<5, 16, 8, kStack8>
-                     : trace_kernel_w8<6, 16, 8, kStack8>;
+  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8, false, false>
+          : w8v == 2 ? trace_kernel_w8<8, 6, 1, kStack8>
+                     : trace_kernel_w8<8, 8, 1, kStack8>;
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8 ? trace_kernel_w8<6, 16, 8, kStack8, true> : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
+    dfk = wide8 ? trace_kernel_w8<8, 8, 1, kStack8, true> : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;

@@ -23,7 +23,7 @@
 
 namespace rr {
 
-template <int MINB, int DONET, int UNR, int STK, bool CNT = false>
+template <int MINB, int DONET, int UNR, int STK, bool CNT = false, bool SORT = true>
 __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -213,23 +213,44 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           if (CNT) ++st_cnt[0];
           WVisit v;
           visit_w8(p.wnodes, node, r, px, py, pz, tbest, rplane, v);
-          uint32_t hm = v.hit;
+          const uint32_t hm = v.hit;
           if (hm == 0) {
             pop();
           } else {
-            while (hm & (hm - 1u)) {  // two or more: push the farthest
-              float tmx = -kInf;
-              int kmx = 0;
+            // continue into the nearest hit slot; push the others (SORT: in
+            // descending entry distance, else in slot order, branch-free)
+            float tmn = kInf;
+            int kmn = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (((hm >> k) & 1u) && v.t[k] < tmn) {
+                tmn = v.t[k];
+                kmn = k;
+              }
+            uint32_t rest = hm & ~(1u << kmn);
+            if (SORT) {
+              while (rest & (rest - 1u)) {  // two or more left: push the farthest
+                float tmx = -kInf;
+                int kmx = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (((rest >> k) & 1u) && v.t[k] > tmx) {
+                    tmx = v.t[k];
+                    kmx = k;
+                  }
+                push(make_int2(wref(v, kmx), __float_as_int(tmx)));
+                rest &= ~(1u << kmx);
+              }
+              if (rest) {
+                const int k = __ffs(rest) - 1;
+                push(make_int2(wref(v, k), __float_as_int(v.t[k])));
+              }
+            } else if (rest) {
 #pragma unroll
               for (int k = 0; k < 8; ++k)
-                if (((hm >> k) & 1u) && v.t[k] > tmx) {
-                  tmx = v.t[k];
-                  kmx = k;
-                }
-              push(make_int2(wref(v, kmx), __float_as_int(tmx)));
-              hm &= ~(1u << kmx);
+                if ((rest >> k) & 1u) push(make_int2(wref(v, k), __float_as_int(v.t[k])));
             }
-            node = wref(v, __ffs(hm) - 1);
+            node = wref(v, kmn);
           }
           if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
             leaf = node;
