@@ -62,7 +62,7 @@ def brb_model(config):
         return json.load(f)[config]
 
 
-UNIT_SCALE = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12,
+UNIT_SCALE = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
               "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
 
 
@@ -191,13 +191,17 @@ def cpu_reference_sample(scene, seconds, threads):
             _, st = sc.trace(scene.source, scene.ray_count, [scene.receivers[0][0]], [scene.receivers[0][1]],
                              scene.max_iterations, scene.max_range, threads, 0, stride, 0)
             return st.ray_bounces, time.perf_counter() - t
-    probe = max(1, scene.ray_count // 2000)
-    rb, dt = run(probe)
-    rate = rb / max(dt, 1e-9)
-    per_ray = rb / ((scene.ray_count + probe - 1) // probe)
-    want_rays = max(threads * 64, int(rate * seconds / max(per_ray, 1)))
-    stride = max(1, scene.ray_count // max(want_rays, 1))
+    # size the strided sample to ~`seconds` (the first probes underestimate
+    # the rate: thread start-up and tail imbalance on few rays)
+    stride = max(1, scene.ray_count // 2000)
     rb, dt = run(stride)
+    for _ in range(3):
+        if dt >= 0.5 * seconds or stride == 1:
+            break
+        rays_now = (scene.ray_count + stride - 1) // stride
+        want = rays_now * seconds / max(dt, 1e-3)
+        stride = max(1, int(scene.ray_count // max(want, 1)))
+        rb, dt = run(stride)
     rays = (scene.ray_count + stride - 1) // stride
     return rb / dt, f"{rays} of {scene.ray_count} lattice rays (k = 0 mod {stride}), {rb} ray*bounces, {dt:.2f} s", \
         kind, rb, dt
@@ -359,7 +363,7 @@ def run_ours(args):
     cnt = rr.trace_device(tree, src, recv, cfg, flags=_lib.RR_TRACE_COUNT, **shard).stats
     b_bar = cnt.ray_bounces / max(cnt.n_rays, 1)
     v_rb, l_rb = cnt.node_visits / cnt.ray_bounces, cnt.leaf_tests / cnt.ray_bounces
-    b_kernel = 64 * v_rb + 80 * l_rb + 48 + 4 + 128 / b_bar
+    b_kernel = cnt.node_bytes * v_rb + 80 * l_rb + 48 + 4 + 128 / b_bar
     ref_model_gbs = model["B_rb"] * bounces / kern_s / 1e9
     l2 = C.c_double()
     _lib.check(lib.rr_l2_read_gbs(ctx.h, 48 << 20, 40, C.byref(l2)))
@@ -384,6 +388,7 @@ def run_ours(args):
         "reference_tree_equiv_frac": round(ref_model_gbs / peak, 4),
         "note": "SURVEY 8(d) B_rb prices the reference median tree's node visits (n_int, n_leaf counted by the "
                 "oracle); the SAH/wide traversal here visits fewer nodes, so this is a throughput equivalent",
+        "kernel_tree_width": cnt.tree_width, "kernel_node_bytes": cnt.node_bytes,
         "kernel_node_visits_per_rb": round(v_rb, 2), "kernel_leaf_tests_per_rb": round(l_rb, 2),
         "kernel_bytes_per_rb": round(b_kernel, 1),
         "kernel_equiv_gbs": round(b_kernel * bounces / kern_s / 1e9, 1),

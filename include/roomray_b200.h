@@ -78,8 +78,9 @@ typedef struct {
 #define RR_TRACE_WIDE 8          /* diagnostic: traverse the 4-wide collapse */
 #define RR_TRACE_COUNT 16        /* instrumented kernel: count node visits and leaf tests */
 #define RR_TRACE_TREE8 32        /* traverse the 8-wide compressed tree at any scene size
-                                    (the default from 2^18 faces up) */
-#define RR_TRACE_TREE2 64        /* traverse the binary SAH tree at any scene size */
+                                    (the default from 2^20 faces up) */
+#define RR_TRACE_TREE2 64        /* traverse the binary SAH tree at any scene size (the default
+                                    below 2^18 faces; 2^18..2^20: its 4-wide collapse) */
 
 /* Statistics of a trace (TraceResult, tracer.hpp:22-29). */
 typedef struct {
@@ -94,6 +95,8 @@ typedef struct {
   int64_t n_rays;        /* rays traced by this call */
   int64_t node_visits;   /* internal-node visits (RR_TRACE_COUNT), else -1 */
   int64_t leaf_tests;    /* fp64 triangle tests (RR_TRACE_COUNT), else -1 */
+  int32_t tree_width;    /* children per node of the traversed tree: 2, 4 or 8 */
+  int32_t node_bytes;    /* bytes per node of that tree: 64 (binary), 128 (4-wide), 80 (8-wide) */
 } rr_trace_stats;
 
 /* AirModel (air_absorption.hpp:10-23). */

@@ -54,7 +54,8 @@ class TraceConfig(C.Structure):
 class TraceStats(C.Structure):
     _fields_ = [("iterations", _i32), ("truncated", _i32), ("escaped", _i64), ("out_of_range", _i64),
                 ("max_range", _d), ("n_captures", _i64), ("total_history", _i64), ("ray_bounces", _i64),
-                ("n_rays", _i64), ("node_visits", _i64), ("leaf_tests", _i64)]
+                ("n_rays", _i64), ("node_visits", _i64), ("leaf_tests", _i64), ("tree_width", _i32),
+                ("node_bytes", _i32)]
 
 
 class Air(C.Structure):

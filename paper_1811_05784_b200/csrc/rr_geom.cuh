@@ -419,10 +419,11 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
 // are ordered by entry distance, the nearest taken next and the others
 // pushed (leaves included, so a popped entry may be a leaf); coplanar slots
 // culled via QNode.pad; same postponed, warp-batched leaf tests.
-template <int LEAFT, int STUCKT, typename RAY, int UNR = 1, int TOS = 0>
+template <int LEAFT, int STUCKT, typename RAY, int UNR = 1, int TOS = 0, bool CNT = false>
 __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const QNode* __restrict__ q4,
                                                      int32_t root4, const FaceTri* __restrict__ tri,
-                                                     const RAY& ray, int32_t rplane) {
+                                                     const RAY& ray, int32_t rplane,
+                                                     unsigned long long* cnt = nullptr) {
   HitResult best{0.0, -1};
   RayF r;
   if (!make_rayf(h, ray.org(), ray.dir(), r)) return best;
@@ -475,6 +476,7 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
   while (node != kDone || leaf != 0) {
 #pragma unroll 1
     for (int u = 0; u < UNR && node >= 0 && node != kDone && (u == 0 || leaf == 0); ++u) {
+      if (CNT) ++cnt[0];
       const float4* p = reinterpret_cast<const float4*>(q4 + node);
       const float4 lx = __ldg(p), hx = __ldg(p + 1), ly = __ldg(p + 2), hy = __ldg(p + 3);
       const float4 lz = __ldg(p + 4), hz = __ldg(p + 5);
@@ -535,6 +537,7 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
     const bool enough_stuck = STUCKT > 0 ? __popc(mv) >= STUCKT : __popc(mv) * (-STUCKT) >= na;
     if (enough_stuck || cv == 0 || __popc(hv) * LEAFT >= 32 * na) {
       if (leaf != 0) {
+        if (CNT) cnt[1] += leaf_faces(leaf);
         if (test_leaf(tri, leaf, ray.org(), ray.dir(), best)) tbest = prune_bound(best.delta, r.shift);
         leaf = 0;
         if (node < 0) {  // the leaf that waited for the slot

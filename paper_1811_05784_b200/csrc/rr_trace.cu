@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
     if (V == 0) {
       wall = closest_hit_f(p.hdr, p.nodes, p.tri32, p.tri, o, d);
     } else if (V == 3) {
-      wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane);
+      wall = closest_hit4_pl<16, -2, RegRay, UNR, TOS, CNT>(p.hdr, p.q4, p.root4, p.tri, RegRay{o, d}, rplane, st_cnt);
     } else if (V == 1 && PL > 0) {
       wall = closest_hit_pl<PL, ST, RegRay, CNT, UNR, SMS, F32L, TOS, PFL>(p.hdr, p.nodes, p.tri, RegRay{o, d}, rplane,
                                                                   st_cnt, s_stack + threadIdx.x, p.tri32);
@@ -641,15 +641,20 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   }();
   const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8 && s->wide_ok;
   using KFn = void (*)(const TraceParams);
+  // A/B (C5, ms): default (MINB 8, DONET 8, UNR 1, sorted pushes) 657;
+  // unsorted pushes 667; 12 stack entries in shared memory 658; MINB 7 666;
+  // DONET 16 / UNR 4 at MINB 6 716; UNR 8 810; no batching (per-ray loop) 1074
   KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8, false, false>
-          : w8v == 2 ? trace_kernel_w8<8, 6, 1, kStack8>
+          : w8v == 2 ? trace_kernel_w8<8, 8, 1, kStack8, false, true, 12>
                      : trace_kernel_w8<8, 8, 1, kStack8>;
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8 ? trace_kernel_w8<8, 8, 1, kStack8, true> : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
+    dfk = wide8   ? trace_kernel_w8<8, 8, 1, kStack8, true>
+          : wide4 ? trace_kernel<3, 8, false, 0, 1, true>
+                  : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
@@ -735,6 +740,9 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   S.n_rays = count;
   S.node_visits = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[7]) : -1;
   S.leaf_tests = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[8]) : -1;
+  S.tree_width = wide8 ? 8 : (wide4 || variant == 2) ? 4 : 2;
+  S.node_bytes = wide8 ? static_cast<int32_t>(sizeof(WNode)) : (wide4 || variant == 2) ? static_cast<int32_t>(sizeof(QNode))
+                                                                                      : static_cast<int32_t>(sizeof(TNode));
   s->caps_per_ray = static_cast<double>(nc) / static_cast<double>(std::max<int64_t>(count, 1) * n_recv);
 
   // ---- sort captures by (receiver, ray, order) and materialise

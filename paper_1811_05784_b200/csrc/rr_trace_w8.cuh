@@ -23,8 +23,12 @@
 
 namespace rr {
 
-template <int MINB, int DONET, int UNR, int STK, bool CNT = false, bool SORT = true>
+template <int MINB, int DONET, int UNR, int STK, bool CNT = false, bool SORT = true, int SMS = 0>
 __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p) {
+  // the SMS oldest stack entries of each lane in shared memory (column tid:
+  // lane i always in bank i, conflict-free), deeper ones in local memory
+  __shared__ int2 s_st[SMS > 0 ? SMS * 128 : 1];
+  int2* sst = s_st + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const float kInf = __int_as_float(0x7f800000);
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   float tbest = FLT_MAX;
   HitResult best{0.0, -1};
   int32_t node = kDone, leaf = 0;
-  int2 st[STK];
+  int2 st[STK - SMS];
   int sp = 0;
   int2 top[2] = {};
   int n_top = 0;
@@ -49,8 +53,13 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   unsigned long long st_cnt[2] = {0, 0};
   int32_t st_max = 0;
 
+  auto st_put = [&](int i, int2 e) {
+    if (SMS > 0 && i < SMS) sst[i * 128] = e;
+    else st[i - SMS] = e;
+  };
+  auto st_get = [&](int i) -> int2 { return (SMS > 0 && i < SMS) ? sst[i * 128] : st[i - SMS]; };
   auto push = [&](int2 e) {
-    if (n_top == 2) st[sp++] = top[1];
+    if (n_top == 2) st_put(sp++, top[1]);
     top[1] = top[0];
     top[0] = e;
     n_top = min(n_top + 1, 2);
@@ -68,7 +77,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
     }
     while (sp > 0) {
       --sp;
-      const int2 e = st[sp];
+      const int2 e = st_get(sp);
       if (__int_as_float(e.y) <= tbest) {
         node = e.x;
         break;
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
               }
             uint32_t rest = hm & ~(1u << kmn);
             if (SORT) {
-              while (rest & (rest - 1u)) {  // two or more left: push the farthest
+              while (rest) {  // push the farthest first
                 float tmx = -kInf;
                 int kmx = 0;
 #pragma unroll
@@ -240,10 +249,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
                   }
                 push(make_int2(wref(v, kmx), __float_as_int(tmx)));
                 rest &= ~(1u << kmx);
-              }
-              if (rest) {
-                const int k = __ffs(rest) - 1;
-                push(make_int2(wref(v, k), __float_as_int(v.t[k])));
               }
             } else if (rest) {
 #pragma unroll
