@@ -34,6 +34,8 @@ typedef struct rr_trace_result rr_trace_result;
 typedef struct rr_images rr_images;
 typedef struct rr_lattice rr_lattice;
 typedef struct rr_match rr_match;
+typedef struct rr_comm rr_comm;
+typedef struct rr_sharded rr_sharded;
 
 /* Reference-layout tree node (TreeNode, accel_tree.hpp:15-22): post-order,
  * root last, leaves hold one face. */
@@ -353,6 +355,41 @@ rr_status rr_band_filter(int32_t band, double fs, int32_t taps, double* out);
 /* Image arrays of a device image set (for rr_ir_bin_device). */
 rr_status rr_images_device(rr_images* im, const double** d_dist,
                            const double** d_energy, int64_t* n);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * run_trace_pipeline's trace -> image sources -> impulse responses
+ * (pipeline.cpp:163-175) over the ranks of an NCCL communicator, one process
+ * or thread per GPU.  Each rank traces a block-cyclic shard of the lattice
+ * (`block` rays per block) on its replicated scene; captures go to the owner
+ * of their order class (ncclSend/ncclRecv), owners build the image sources,
+ * the 8-band pulse histograms are summed exactly (64-bit fixed point,
+ * ncclAllReduce) and every rank runs the FIR; image lists are gathered to
+ * rank 0.  Results equal the single-GPU pipeline's bit for bit.  With comm ==
+ * NULL the plain single-GPU pipeline runs, still device resident.  NCCL
+ * failures return RR_NCCL.  (The reference has no multi-process path; its
+ * trace() splits rays over host threads, tracer.cpp:82-105.) */
+#define RR_NCCL_ID_BYTES 128
+rr_status rr_comm_unique_id(uint8_t* id); /* ncclGetUniqueId, RR_NCCL_ID_BYTES bytes, rank 0 */
+rr_status rr_comm_init(rr_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
+                       rr_comm** out); /* ncclCommInitRank on ctx's device */
+rr_status rr_comm_info(rr_comm* comm, int32_t* rank, int32_t* nranks);
+rr_status rr_comm_destroy(rr_comm* comm);
+rr_status rr_pipeline_sharded(rr_scene* scene, rr_comm* comm, const rr_source* source,
+                              const rr_receiver* receivers, int32_t n_recv,
+                              const rr_trace_config* cfg, const rr_air* air,
+                              const rr_cluster_options* opt, double fs, int64_t length,
+                              int32_t taps, int32_t block, rr_sharded** out);
+/* this rank's ray*bounces / rays, image sources built here (all receivers),
+ * and stage times in ms [trace, exchange, images, ir, gather] (may be NULL) */
+rr_status rr_sharded_info(rr_sharded* sh, int64_t* ray_bounces, int64_t* n_rays,
+                          int64_t* local_images, float* stage_ms);
+/* hands out receiver recv's image list (rank 0: all ranks' images in the
+ * reference order; other ranks: empty); destroy it with rr_images_destroy */
+rr_status rr_sharded_take_images(rr_sharded* sh, int32_t recv, rr_images** out);
+/* receiver recv's band IRs (8 x length) and broadband IR (length); host or
+ * device pointers, either may be NULL */
+rr_status rr_sharded_ir(rr_sharded* sh, int32_t recv, double* band_ir, double* broadband);
+rr_status rr_sharded_destroy(rr_sharded* sh);
 
 #ifdef __cplusplus
 }

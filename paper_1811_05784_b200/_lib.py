@@ -132,7 +132,19 @@ SIGNATURES = [
     ("rr_band_factors", C.c_int, [_vp, _i64p, _vp, _vp, _vp]),
     ("rr_factors_from_images", C.c_int, [_vp, _i64, _vp, _vp, _d, _vp]),
     ("rr_images_factors", C.c_int, [_vp, _d, _vp]),
+    ("rr_comm_unique_id", C.c_int, [_vp]),
+    ("rr_comm_init", C.c_int, [_vp, _vp, _i32, _i32, C.POINTER(_vp)]),
+    ("rr_comm_info", C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    ("rr_comm_destroy", C.c_int, [_vp]),
+    ("rr_pipeline_sharded", C.c_int, [_vp, _vp, C.POINTER(Source), C.POINTER(Receiver), _i32,
+                                      C.POINTER(TraceConfig), C.POINTER(Air), C.POINTER(ClusterOptions), _d, _i64,
+                                      _i32, _i32, C.POINTER(_vp)]),
+    ("rr_sharded_info", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    ("rr_sharded_take_images", C.c_int, [_vp, _i32, C.POINTER(_vp)]),
+    ("rr_sharded_ir", C.c_int, [_vp, _i32, _vp, _vp]),
+    ("rr_sharded_destroy", C.c_int, [_vp]),
 ]
+RR_NCCL_ID_BYTES = 128
 
 _LIB = None
 

@@ -1,6 +1,7 @@
 // C ABI entry points (include/roomray_b200.h): argument checks, uploads,
 // error mapping.  All compute runs in the kernels of rr_build.cu,
 // rr_trace.cu, rr_images.cu and rr_ir.cu.
+#include <functional>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -969,3 +970,10 @@ rr_status rr_images_device(rr_images* im, const double** d_dist, const double** 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- helpers for rr_shard.cu
+namespace rr {
+rr_status abi_guard_nccl(const std::function<void()>& f) { return guarded(f); }
+void scene_retain(rr_scene* s) { s->refs++; }
+void scene_drop(rr_scene* s) { scene_release(s); }
+}  // namespace rr

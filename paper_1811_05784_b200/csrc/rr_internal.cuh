@@ -226,6 +226,16 @@ void build_sah_tree(rr_scene* s, cudaStream_t st);
 void build_sah4(rr_scene* s);  // 4-wide collapse, on demand
 // rr_wide.cu
 void build_wide(rr_scene* s);  // 8-wide compressed collapse, on demand
+// rr_ir.cu
+void ir_bin(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy, double c, double fs, int64_t lh,
+            double* d_hist);
+void ir_filter(rr_ctx* ctx, const double* d_hist, int64_t lh, double fs, int taps, int64_t L, double* d_band_ir,
+               double* d_broadband);
+void ir_max_amp(rr_ctx* ctx, int64_t n, const double* d_energy, unsigned long long* d_max);
+void ir_bin_fixed(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy, double c, double fs,
+                  int64_t lh, const unsigned long long* d_max, int64_t n_scale, unsigned long long* d_acc);
+void ir_unfix(rr_ctx* ctx, const unsigned long long* d_acc, int64_t total, int64_t n_scale,
+              const unsigned long long* d_max, double* d_hist);
 // rr_trace.cu
 void nearest_hit_batch(rr_scene* s, const double* d_o, const double* d_d,
                        int64_t n, int brute, int32_t* d_face, double* d_delta,

@@ -37,12 +37,15 @@ __device__ __forceinline__ double fixed_scale(unsigned long long max_bits, int64
 
 // K6: pulse histogram (build_pulse_trains + the lround(t*fs) centring of
 // synthesize rir.cpp:86).
+// The fixed-point scale depends on (max amplitude, n_scale) only: ranks that
+// bin their shares with the global values produce integer histograms whose
+// exact sum equals the single-GPU histogram (rr_shard.cu).
 __global__ void bin_kernel(const double* __restrict__ dist, const double* __restrict__ energy, int64_t n, double c,
-                           double fs, int64_t lh, const unsigned long long* __restrict__ max_bits,
+                           double fs, int64_t lh, const unsigned long long* __restrict__ max_bits, int64_t n_scale,
                            unsigned long long* __restrict__ acc) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double scale = fixed_scale(*max_bits, n);
+  const double scale = fixed_scale(*max_bits, n_scale);
   const double t = dist[i] / c;
   const long long center = llround(t * fs);
   if (center < 0 || center >= lh) return;
@@ -184,16 +187,34 @@ void ir_bin(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy
   mx.alloc(1, st);
   RR_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes(), st));
   RR_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
-  if (n > 0) {
-    max_amp_kernel<<<592, 256, 0, st>>>(d_energy, kBands * n, mx.p);
-    RR_LAUNCH_CHECK();
-    bin_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(d_dist, d_energy, n, c, fs, lh, mx.p, acc.p);
-    RR_LAUNCH_CHECK();
-    ctx->launches += 2;
-  }
-  unfix_kernel<<<static_cast<unsigned>((kBands * lh + 255) / 256), 256, 0, st>>>(acc.p, kBands * lh,
-                                                                                  std::max<int64_t>(n, 1), mx.p,
-                                                                                  d_hist);
+  ir_max_amp(ctx, n, d_energy, mx.p);
+  ir_bin_fixed(ctx, n, d_dist, d_energy, c, fs, lh, mx.p, std::max<int64_t>(n, 1), acc.p);
+  ir_unfix(ctx, acc.p, kBands * lh, std::max<int64_t>(n, 1), mx.p, d_hist);
+}
+
+// The three phases of ir_bin, for the multi-GPU pipeline: the max amplitude
+// (max-reduced over ranks), the fixed-point binning with the global scale
+// (sum-reduced over ranks, exact), the conversion back to fp64.
+void ir_max_amp(rr_ctx* ctx, int64_t n, const double* d_energy, unsigned long long* d_max) {
+  if (n <= 0) return;
+  max_amp_kernel<<<592, 256, 0, ctx->stream>>>(d_energy, kBands * n, d_max);
+  RR_LAUNCH_CHECK();
+  ctx->launches++;
+}
+
+void ir_bin_fixed(rr_ctx* ctx, int64_t n, const double* d_dist, const double* d_energy, double c, double fs,
+                  int64_t lh, const unsigned long long* d_max, int64_t n_scale, unsigned long long* d_acc) {
+  if (n <= 0) return;
+  bin_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(d_dist, d_energy, n, c, fs, lh, d_max,
+                                                                              n_scale, d_acc);
+  RR_LAUNCH_CHECK();
+  ctx->launches++;
+}
+
+void ir_unfix(rr_ctx* ctx, const unsigned long long* d_acc, int64_t total, int64_t n_scale,
+              const unsigned long long* d_max, double* d_hist) {
+  unfix_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(d_acc, total, n_scale, d_max,
+                                                                                     d_hist);
   RR_LAUNCH_CHECK();
   ctx->launches++;
 }

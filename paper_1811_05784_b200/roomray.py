@@ -697,3 +697,89 @@ def step(tree: AccelTree, rays: Rays, receiver: Receiver, config: TraceConfig = 
                            _vptr(rays.alive), _vptr(rays.hist), _vptr(rays.n_hist), int(hist_cap), C.byref(rec),
                            C.byref(cfg), int(brute), C.byref(h)))
     return DeviceTrace(tree, h)
+
+
+# ------------------------------------------------------------------ multi-GPU through the C ABI
+class Comm:
+    """An NCCL communicator bound to a Context (rr_comm): one per rank.  The
+    unique id (rr_comm_unique_id, 128 bytes) comes from rank 0 and reaches
+    the others out of band (e.g. torch.distributed.broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = _lib.load()
+        buf = (C.c_uint8 * _lib.RR_NCCL_ID_BYTES)()
+        check(lib.rr_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, uid: bytes, nranks: int, rank: int):
+        self.ctx, self.lib = ctx, ctx.lib
+        buf = (C.c_uint8 * _lib.RR_NCCL_ID_BYTES).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(self.lib.rr_comm_init(ctx.h, buf, int(nranks), int(rank), C.byref(h)))
+        self.h, self.rank, self.nranks = h, rank, nranks
+
+    def __del__(self):
+        if getattr(self, "h", None) and not _SHUTDOWN:
+            self.lib.rr_comm_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class PipelineResult:
+    """Per receiver: images[r] (rank 0: every rank's image sources in the
+    reference order; other ranks: empty), band_ir[r] (8, L), broadband[r]
+    (L,); this rank's ray_bounces / n_rays, image sources built here, and
+    stage times (ms) trace / exchange / images / ir / gather."""
+
+    images: list
+    band_ir: list
+    broadband: list
+    ray_bounces: int
+    n_rays: int
+    local_images: int
+    stage_ms: dict
+
+
+def pipeline_sharded(tree: AccelTree, source: SourceConfig, receivers, config: TraceConfig = TraceConfig(), *,
+                     comm: Comm | None = None, air: AirModel = AirModel(), options: ClusterOptions = ClusterOptions(),
+                     sample_rate: float = 48000.0, length: int | None = None, taps: int = 1023, block: int = 4096,
+                     device_images: bool = False) -> PipelineResult:
+    """run_trace_pipeline's trace -> image sources -> IRs (pipeline.cpp:163-175)
+    on the device, over the ranks of `comm` (rr_pipeline_sharded); comm=None
+    is the single-GPU pipeline.  Captures never leave the GPU."""
+    recs = receivers if isinstance(receivers, (list, tuple)) else [receivers]
+    src = _lib.Source((C.c_double * 3)(*map(float, source.position)), int(source.ray_count))
+    rarr = (_lib.Receiver * len(recs))(*[_lib.Receiver((C.c_double * 3)(*map(float, r.center)), float(r.radius))
+                                         for r in recs])
+    cfg = _lib.TraceConfig(int(config.max_iterations), float(config.speed_of_sound), float(config.max_range), 0, 0, 0,
+                           0, 0, None)
+    a = air.c()
+    o = _lib.ClusterOptions(float(options.tol_scale), int(options.merge_coplanar))
+    if length is None:
+        length = int(round(2.0 * sample_rate))
+    h = C.c_void_p()
+    lib = tree.lib
+    check(lib.rr_pipeline_sharded(tree.h, comm.h if comm is not None else None, C.byref(src), rarr, len(recs),
+                                  C.byref(cfg), C.byref(a), C.byref(o), float(sample_rate), int(length), int(taps),
+                                  int(block), C.byref(h)))
+    try:
+        rb, nr, li = C.c_int64(), C.c_int64(), C.c_int64()
+        ms = (C.c_float * 5)()
+        check(lib.rr_sharded_info(h, C.byref(rb), C.byref(nr), C.byref(li), ms))
+        images, bands, bbs = [], [], []
+        for r in range(len(recs)):
+            ih = C.c_void_p()
+            check(lib.rr_sharded_take_images(h, r, C.byref(ih)))
+            di = DeviceImages(lib, ih)
+            images.append(di if device_images else di.fetch())
+            band = np.empty((NUM_BANDS, length))
+            bb = np.empty(length)
+            check(lib.rr_sharded_ir(h, r, band.ctypes.data, bb.ctypes.data))
+            bands.append(band)
+            bbs.append(bb)
+        names = ("trace", "exchange", "images", "ir", "gather")
+        return PipelineResult(images, bands, bbs, rb.value, nr.value, li.value,
+                              {k: float(v) for k, v in zip(names, ms)})
+    finally:
+        lib.rr_sharded_destroy(h)
