@@ -15,10 +15,12 @@ such mesh).  It is the only HBM-resident scene (C1-C3 fit in the 126 MB L2).
 One step = one trace of the whole lattice (device emission, persistent
 traversal kernel, capture compaction + sort) on the device-resident scene:
 `value` counts the nearest-hit queries executed (ray*bounces) per second.
-`e2e` is the same metric through the C ABI from pinned host arrays: scene
-upload + validation + device tree build + trace + image sources (coplanar
-merge on, RunConfig default) + 8-band IR synthesis + download of the images
-and IRs, every step.
+`e2e` is the same metric through the C ABI from pinned host arrays, every
+step: scene upload + device validation + tree build (rr_scene_create), then
+rr_pipeline_sharded -- trace, the NCCL capture exchange when N > 1, image
+sources (coplanar merge on, RunConfig default), exact multi-GPU 8-band IR --
+and the download of every image list and IR.  `e2e_native_cpp` times the C++
+facade's run_trace_pipeline stages (tests/native/pipeline_bench.cpp).
 
 Multi-GPU: strong scaling of the fixed 8 * 10^6-ray lattice, each rank
 tracing a block-cyclic shard (4 096-ray blocks), time = max over ranks.
@@ -207,6 +209,33 @@ def cpu_reference_sample(scene, seconds, threads):
         kind, rb, dt
 
 
+def native_pipeline(scene, steps, warmup):
+    """The C++ facade's run_trace_pipeline stages (tests/native/pipeline_bench.cpp:
+    tree build, trace, image sources, pulse trains + IR, factors; host mesh
+    in, host artifacts out), compiled here with g++ against the library."""
+    import tempfile
+    exe = os.path.join(ROOT, "build", "pipeline_bench")
+    src = os.path.join(ROOT, "tests", "native", "pipeline_bench.cpp")
+    lib_dir = os.path.join(ROOT, "paper_1811_05784_b200")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-L", lib_dir,
+                    "-lroomray_b200", "-Wl,-rpath," + lib_dir, "-o", exe], check=True)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "scene.bin")
+        (c, r), = scene.receivers[:1]
+        with open(path, "wb") as f:
+            f.write(np.array([len(scene.vertices), len(scene.faces), len(scene.absorption)], np.int64).tobytes())
+            f.write(np.ascontiguousarray(scene.vertices, np.float64).tobytes())
+            f.write(np.ascontiguousarray(scene.faces, np.int32).tobytes())
+            f.write(np.ascontiguousarray(scene.absorption, np.float64).tobytes())
+            f.write(np.array(scene.source, np.float64).tobytes())
+            f.write(np.array([scene.ray_count], np.int64).tobytes())
+            f.write(np.array([*c, r, scene.max_range, scene.sample_rate], np.float64).tobytes())
+            f.write(np.array([scene.max_iterations, 1], np.int64).tobytes())
+        out = subprocess.run([exe, path, str(steps), str(warmup)], capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -215,7 +244,6 @@ def run_ours(args):
     from paper_1811_05784_b200 import Context, Receiver, SourceConfig, TraceConfig, TriangleMesh
     from paper_1811_05784_b200 import roomray as rr
     from paper_1811_05784_b200 import _lib
-    from paper_1811_05784_b200.shard import run_sharded
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -289,59 +317,52 @@ def run_ours(args):
     lib = _lib.load()
     import ctypes as C
 
+    # the multi-GPU pipeline behind the C ABI (rr_pipeline_sharded): its own
+    # NCCL communicator, the unique id from rank 0 over torch.distributed
+    comm = None
+    if world > 1:
+        uid = [rr.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = rr.Comm(ctx, uid[0], world, rank)
     for it in range(args.warmup + args.steps):
         barrier()
         w0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1, e_sc = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         with torch.cuda.stream(stream):
             e0.record()
         h = C.c_void_p()
         _lib.check(lib.rr_scene_create(ctx.h, C.c_void_p(pv.data_ptr()), len(scene.vertices),
                                        C.c_void_p(pt.data_ptr()), len(scene.faces), C.c_void_p(pa.data_ptr()),
                                        len(scene.absorption), 1, C.byref(h)))
+        with torch.cuda.stream(stream):
+            e_sc.record()
         sc = rr.AccelTree.__new__(rr.AccelTree)
         sc.ctx, sc.lib, sc.mesh, sc.h = ctx, lib, mesh, h
-        marks = []
-        host = [("start", w0)]
-
-        def mark(name):
-            ev = torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                ev.record()
-            marks.append((name, ev))
-            if os.environ.get("RR_E2E_DEBUG"):
-                host.append((name, time.perf_counter()))
-
-        mark("scene")
-        res = run_sharded(sc, src, recv, cfg, air=rr.AirModel(), options=rr.ClusterOptions(1e-6, True),
-                          sample_rate=scene.sample_rate, length=L, taps=taps, mark=mark, host=True)
-        # run_sharded(host=True) returns the results in pinned host memory:
-        # the 8 band IRs and the broadband IR (every rank) and the merged image
-        # list (rank 0); the image list's D2H overlaps the IR stage
+        res = rr.pipeline_sharded(sc, src, recv, cfg, comm=comm, air=rr.AirModel(),
+                                  options=rr.ClusterOptions(1e-6, True), sample_rate=scene.sample_rate, length=L,
+                                  taps=taps, block=4096)
+        # results in host memory: every receiver's 8 band IRs and broadband IR
+        # (every rank), the merged image list (rank 0)
         fetched = []
         for r, band in enumerate(res.band_ir):
             fetched += [band, res.broadband[r]]
-            if res.images[r] is not None:
-                fetched += [getattr(res.images[r], f) for f in res.images[r].__dataclass_fields__]
-        assert all(not t.is_cuda for t in fetched)
+            im = res.images[r]
+            fetched += [getattr(im, f) for f in im.__dataclass_fields__]
         with torch.cuda.stream(stream):
             e1.record()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
         if it >= args.warmup:
             e2e_ms.append(max(e0.elapsed_time(e1), (w1 - w0) * 1e3))
-            if os.environ.get("RR_E2E_DEBUG"):
-                print("e2e dbg: event %.3f wall %.3f host marks %s" % (
-                    e0.elapsed_time(e1), (w1 - w0) * 1e3,
-                    [(n, round((t - w0) * 1e3, 3)) for n, t in host]), file=sys.stderr)
-            prev = e0
-            for name, ev in marks + [("fetch", e1)]:
-                breakdown[name] = breakdown.get(name, 0.0) + prev.elapsed_time(ev) / args.steps
-                prev = ev
-            d2h = sum(t.numel() * t.element_size() for t in fetched)
+            stages = {"scene": e0.elapsed_time(e_sc), **res.stage_ms}
+            stages["fetch+host"] = e2e_ms[-1] - sum(stages.values())
+            for k, v in stages.items():
+                breakdown[k] = breakdown.get(k, 0.0) + v / args.steps
+            d2h = sum(np.asarray(x).nbytes for x in fetched)
         del res
         lib.rr_scene_destroy(h)
         sc.h = None
+    del comm
     e2e_local = sum(e2e_ms)
     t = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -401,6 +422,14 @@ def run_ours(args):
             threads = os.cpu_count() or 1
             rate, sample, kind, _, _ = cpu_reference_sample(scene, args.cpu_seconds, threads)
             cpu = {"value": round(rate, 1), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+        native = None
+        if world == 1 and not args.no_native:
+            nat = native_pipeline(scene, max(2, args.steps // 3), 1)
+            native = {"value": round(nat["ray_bounces_per_step"] / nat["seconds_per_step"], 1), "unit": UNIT,
+                      "seconds_per_step": nat["seconds_per_step"], "stage_s": nat["stage_s"], "steps": nat["steps"],
+                      "images": nat["images"], "captures": nat["captures"],
+                      "what": "C++ facade run_trace_pipeline stages (tree build .. factors), host mesh in, host "
+                              "artifacts out (captures, images, pulse trains, IR, factors), wall clock"}
         out = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
@@ -413,6 +442,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": round(t.item() / args.steps, 3),
                     "stage_ms": {k: round(v, 3) for k, v in breakdown.items()}},
+            "e2e_native_cpp": native,
             "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches), "nccl": nccl,
             "clocks": clk.summary(),
             "ray_bounces_per_step": int(total_bounces / args.steps),
@@ -531,6 +561,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-native", action="store_true", help="skip the C++ facade pipeline timing")
     ap.add_argument("--dry-run", action="store_true", help="gloo/CPU launcher check, no kernels")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

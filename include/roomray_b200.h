@@ -356,6 +356,19 @@ rr_status rr_band_filter(int32_t band, double fs, int32_t taps, double* out);
 rr_status rr_images_device(rr_images* im, const double** d_dist,
                            const double** d_energy, int64_t* n);
 
+/* build_pulse_trains (rir.cpp:9-30) of a device image set: band b's events
+ * (t = d / c, amplitude sqrt(E_b)) sorted by (time, amplitude) at
+ * [band_off[b], band_off[b+1]) of time / amplitude (8 * n each, host or
+ * device; band_off 9 entries, may be NULL).  No host sort. */
+rr_status rr_images_pulse_trains(rr_images* im, double c, int64_t* band_off,
+                                 double* time, double* amplitude);
+/* synthesize (rir.cpp:60-96) of a device image set.  With band_ir and
+ * broadband both NULL: *length = the reference length llround(t_last*fs) +
+ * (taps-1)/2 + 1 (0 without images).  Otherwise fills band_ir (8 x *length)
+ * and / or broadband (*length), host or device buffers. */
+rr_status rr_images_synthesize(rr_images* im, double c, double fs, int32_t taps,
+                               int64_t* length, double* band_ir, double* broadband);
+
 /* ---------------------------------------------------------------- multi-GPU
  * run_trace_pipeline's trace -> image sources -> impulse responses
  * (pipeline.cpp:163-175) over the ranks of an NCCL communicator, one process

@@ -312,26 +312,17 @@ struct TraceHandle {
 };
 }  // namespace detail
 
-/// trace (tracer.hpp:50-52): the whole Fibonacci lattice on the GPU.
-inline TraceResult trace(const TriangleMesh& /*mesh*/, const AccelTree& tree, const SourceConfig& source,
-                         const Receiver& receiver, const TraceConfig& config) {
-  rr_source src{{source.position.x, source.position.y, source.position.z}, source.ray_count};
-  rr_receiver rc{{receiver.center.x, receiver.center.y, receiver.center.z}, receiver.radius};
-  rr_trace_config cfg{};
-  cfg.max_iterations = config.max_iterations;
-  cfg.speed_of_sound = config.speed_of_sound;
-  cfg.max_range = config.max_range;
-  rr_trace_result* h = nullptr;
-  detail::check(rr_trace(tree.handle(), &src, &rc, 1, &cfg, &h));
-  detail::TraceHandle guard(h);
+namespace detail {
+// host copy of a device trace (TraceResult, tracer.hpp:22-29)
+inline TraceResult trace_result_from(rr_trace_result* h) {
   rr_trace_stats st{};
-  detail::check(rr_trace_stats_get(h, &st));
+  check(rr_trace_stats_get(h, &st));
   const std::size_t n = static_cast<std::size_t>(st.n_captures);
   std::vector<int32_t> ray(n), hist(std::max<int64_t>(st.total_history, 1));
   std::vector<double> point(3 * n), dir(3 * n), path(n), mult(kNumBands * n);
   std::vector<int64_t> off(n + 1);
-  detail::check(rr_trace_captures(h, nullptr, ray.data(), point.data(), dir.data(), path.data(), mult.data(),
-                                  off.data(), hist.data()));
+  check(rr_trace_captures(h, nullptr, ray.data(), point.data(), dir.data(), path.data(), mult.data(), off.data(),
+                          hist.data()));
   TraceResult r;
   r.iterations = st.iterations;
   r.truncated = st.truncated != 0;
@@ -351,6 +342,28 @@ inline TraceResult trace(const TriangleMesh& /*mesh*/, const AccelTree& tree, co
     c.face_history.assign(hist.begin() + off[i], hist.begin() + off[i + 1]);
   }
   return r;
+}
+
+// the device trace of the whole lattice for one receiver (caller destroys)
+inline rr_trace_result* trace_device(const AccelTree& tree, const SourceConfig& source, const Receiver& receiver,
+                                     const TraceConfig& config) {
+  rr_source src{{source.position.x, source.position.y, source.position.z}, source.ray_count};
+  rr_receiver rc{{receiver.center.x, receiver.center.y, receiver.center.z}, receiver.radius};
+  rr_trace_config cfg{};
+  cfg.max_iterations = config.max_iterations;
+  cfg.speed_of_sound = config.speed_of_sound;
+  cfg.max_range = config.max_range;
+  rr_trace_result* h = nullptr;
+  check(rr_trace(tree.handle(), &src, &rc, 1, &cfg, &h));
+  return h;
+}
+}  // namespace detail
+
+/// trace (tracer.hpp:50-52): the whole Fibonacci lattice on the GPU.
+inline TraceResult trace(const TriangleMesh& /*mesh*/, const AccelTree& tree, const SourceConfig& source,
+                         const Receiver& receiver, const TraceConfig& config) {
+  detail::TraceHandle guard(detail::trace_device(tree, source, receiver, config));
+  return detail::trace_result_from(guard.h);
 }
 
 /// Ray (tracer_types.hpp:11-18).
@@ -512,6 +525,35 @@ inline Vec3 retro_propagate(const Capture& c) {
 
 /// build_image_sources (image_sources.hpp:58-61): cluster + attach_energy +
 /// project on the GPU, sorted by (order, distance, face path).
+namespace detail {
+// host copy of a device image set (ImageSource list, image_sources.hpp:14-23)
+inline std::vector<ImageSource> images_from(rr_images* im) {
+  int64_t ni = 0, tp = 0;
+  check(rr_images_info(im, &ni, &tp));
+  const std::size_t m = static_cast<std::size_t>(ni);
+  std::vector<double> pos(3 * m), dist(m), en(kNumBands * m), mu(kNumBands * m), proj(3 * m);
+  std::vector<int32_t> cnt(m), order(m), hp(m), pth(std::max<int64_t>(tp, 1));
+  std::vector<int64_t> poff(m + 1);
+  check(rr_images_get(im, pos.data(), dist.data(), en.data(), mu.data(), cnt.data(), order.data(), hp.data(),
+                      proj.data(), poff.data(), pth.data()));
+  std::vector<ImageSource> out(m);
+  for (std::size_t i = 0; i < m; ++i) {
+    ImageSource& s = out[i];
+    s.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    s.distance = dist[i];
+    for (int b = 0; b < kNumBands; ++b) {
+      s.band_energy[b] = en[kNumBands * i + b];
+      s.band_multiplier[b] = mu[kNumBands * i + b];
+    }
+    s.ray_count = cnt[i];
+    s.order = order[i];
+    s.face_path.assign(pth.begin() + poff[i], pth.begin() + poff[i + 1]);
+    if (hp[i]) s.projection = Vec3{proj[3 * i], proj[3 * i + 1], proj[3 * i + 2]};
+  }
+  return out;
+}
+}  // namespace detail
+
 inline std::vector<ImageSource> build_image_sources(const std::vector<Capture>& captures, int total_rays,
                                                     const AirModel& air, const Vec3& receiver_center,
                                                     const TriangleMesh& /*mesh*/, const AccelTree& tree,
@@ -543,29 +585,7 @@ inline std::vector<ImageSource> build_image_sources(const std::vector<Capture>& 
   rr_images* im = nullptr;
   detail::check(rr_build_image_sources(h, 0, total_rays, &a, &o, &im));
   std::unique_ptr<rr_images, void (*)(rr_images*)> img(im, [](rr_images* p) { rr_images_destroy(p); });
-  int64_t ni = 0, tp = 0;
-  detail::check(rr_images_info(im, &ni, &tp));
-  const std::size_t m = static_cast<std::size_t>(ni);
-  std::vector<double> pos(3 * m), dist(m), en(kNumBands * m), mu(kNumBands * m), proj(3 * m);
-  std::vector<int32_t> cnt(m), order(m), hp(m), pth(std::max<int64_t>(tp, 1));
-  std::vector<int64_t> poff(m + 1);
-  detail::check(rr_images_get(im, pos.data(), dist.data(), en.data(), mu.data(), cnt.data(), order.data(), hp.data(),
-                              proj.data(), poff.data(), pth.data()));
-  std::vector<ImageSource> out(m);
-  for (std::size_t i = 0; i < m; ++i) {
-    ImageSource& s = out[i];
-    s.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-    s.distance = dist[i];
-    for (int b = 0; b < kNumBands; ++b) {
-      s.band_energy[b] = en[kNumBands * i + b];
-      s.band_multiplier[b] = mu[kNumBands * i + b];
-    }
-    s.ray_count = cnt[i];
-    s.order = order[i];
-    s.face_path.assign(pth.begin() + poff[i], pth.begin() + poff[i + 1]);
-    if (hp[i]) s.projection = Vec3{proj[3 * i], proj[3 * i + 1], proj[3 * i + 2]};
-  }
-  return out;
+  return detail::images_from(im);
 }
 
 // ------------------------------------------------------------------ RIR (rir.hpp)
@@ -688,6 +708,51 @@ inline BandFactors factors(const PulseTrains& trains) {
   bf.mid = detail::to_factors(out[kNumBands]);
   return bf;
 }
+
+namespace detail {
+// build_pulse_trains of a device image set, sorted on the device (no host sort)
+inline PulseTrains trains_from(rr_images* im, double speed_of_sound) {
+  if (speed_of_sound <= 0.0) throw std::invalid_argument("speed of sound must be > 0");
+  int64_t n = 0, tp = 0;
+  check(rr_images_info(im, &n, &tp));
+  std::vector<int64_t> off(kNumBands + 1);
+  std::vector<double> t(kNumBands * std::max<int64_t>(n, 1)), a(kNumBands * std::max<int64_t>(n, 1));
+  check(rr_images_pulse_trains(im, speed_of_sound, off.data(), t.data(), a.data()));
+  PulseTrains trains;
+  for (int b = 0; b < kNumBands; ++b) {
+    trains[b].band = b;
+    trains[b].events.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
+  }
+  return trains;
+}
+
+// synthesize(trains) of a device image set (the trains' events are the images')
+inline RoomImpulseResponse rir_from(rr_images* im, const PulseTrains& trains, double speed_of_sound,
+                                    double sample_rate, int taps = kBandFilterTaps) {
+  RoomImpulseResponse rir;
+  rir.sample_rate = sample_rate;
+  rir.band_trains = trains;
+  int64_t length = 0;
+  check(rr_images_synthesize(im, speed_of_sound, sample_rate, taps, &length, nullptr, nullptr));
+  if (length == 0) return rir;
+  std::vector<double> band(static_cast<std::size_t>(kNumBands * length));
+  rir.samples.assign(static_cast<std::size_t>(length), 0.0);
+  check(rr_images_synthesize(im, speed_of_sound, sample_rate, taps, &length, band.data(), rir.samples.data()));
+  for (int b = 0; b < kNumBands; ++b)
+    rir.band_samples[b].assign(band.begin() + b * length, band.begin() + (b + 1) * length);
+  return rir;
+}
+
+inline BandFactors factors_from(rr_images* im, double speed_of_sound) {
+  rr_factors out[kNumBands + 1];
+  check(rr_images_factors(im, speed_of_sound, out));
+  BandFactors bf;
+  for (int b = 0; b < kNumBands; ++b) bf.bands[b] = to_factors(out[b]);
+  bf.mid = to_factors(out[kNumBands]);
+  return bf;
+}
+}  // namespace detail
 
 // ------------------------------------------------------------------ shoebox lattice (shoebox.hpp)
 enum BoxWall { kWallX0 = 0, kWallX1, kWallY0, kWallY1, kWallZ0, kWallZ1 };  // shoebox.hpp:13

@@ -473,20 +473,20 @@ struct RunArtifacts {
   double tree_build_seconds = 0.0;
 };
 
-/// run_trace_pipeline (pipeline.cpp:144-185) with every stage on the GPU.
-inline RunArtifacts run_trace_pipeline(const RunConfig& config) {
-  config.validate();
-  RunArtifacts a;
+/// The stages of run_trace_pipeline after loading (pipeline.cpp:154-183),
+/// device resident: the trace's captures are copied to the host once (they
+/// are an artifact) while the image sources are built from the device trace,
+/// and the pulse trains (sorted on the device), the impulse response and the
+/// perceptive factors come from the device image set: no capture re-upload,
+/// no host sort.  a.mesh must be loaded; fills the rest of a.
+inline void run_trace_pipeline_on(RunArtifacts& a, const RunConfig& config) {
   using clock = std::chrono::steady_clock;
-  const auto start = clock::now();
-  auto last = start;
+  auto last = clock::now();
   auto mark = [&](const char* name) {
     const auto now = clock::now();
     a.timings.push_back({name, std::chrono::duration<double>(now - last).count()});
     last = now;
   };
-  a.mesh = load_obj(config.mesh_path, load_material_table(config.material_path), &a.load_report);
-  mark("load");
   a.tree = build_tree(a.mesh);
   mark("tree_build");
   a.tree_build_seconds = a.timings.back().seconds;
@@ -495,18 +495,33 @@ inline RunArtifacts run_trace_pipeline(const RunConfig& config) {
   tc.speed_of_sound = config.speed_of_sound;
   tc.max_range = config.max_range;
   tc.thread_count = config.deterministic ? 1 : config.thread_count;
-  a.trace = trace(a.mesh, a.tree, config.source, config.receiver, tc);
+  detail::TraceHandle th(detail::trace_device(a.tree, config.source, config.receiver, tc));
+  a.trace = detail::trace_result_from(th.h);
   mark("trace");
-  ClusterOptions co;
-  co.merge_coplanar = config.merge_coplanar;
-  a.images = build_image_sources(a.trace.captures, config.source.ray_count, config.air, config.receiver.center,
-                                 a.mesh, a.tree, co);
+  rr_air air{config.air.enabled ? 1 : 0, config.air.temperature_c, config.air.relative_humidity,
+             config.air.pressure_kpa};
+  rr_cluster_options co{ClusterOptions{}.tol_scale, config.merge_coplanar ? 1 : 0};
+  rr_images* im = nullptr;
+  detail::check(rr_build_image_sources(th.h, 0, config.source.ray_count, &air, &co, &im));
+  std::unique_ptr<rr_images, void (*)(rr_images*)> img(im, [](rr_images* p) { rr_images_destroy(p); });
+  a.images = detail::images_from(im);
   mark("image_sources");
-  a.trains = build_pulse_trains(a.images, config.speed_of_sound);
-  a.rir = synthesize(a.trains, config.sample_rate);
+  a.trains = detail::trains_from(im, config.speed_of_sound);
+  a.rir = detail::rir_from(im, a.trains, config.speed_of_sound, config.sample_rate);
   mark("rir");
-  a.metrics = factors(a.trains);
+  a.metrics = detail::factors_from(im, config.speed_of_sound);
   mark("metrics");
+}
+
+/// run_trace_pipeline (pipeline.cpp:144-185) with every stage on the GPU.
+inline RunArtifacts run_trace_pipeline(const RunConfig& config) {
+  config.validate();
+  RunArtifacts a;
+  using clock = std::chrono::steady_clock;
+  const auto start = clock::now();
+  a.mesh = load_obj(config.mesh_path, load_material_table(config.material_path), &a.load_report);
+  a.timings.push_back({"load", std::chrono::duration<double>(clock::now() - start).count()});
+  run_trace_pipeline_on(a, config);
   a.total_seconds = std::chrono::duration<double>(clock::now() - start).count();
   return a;
 }

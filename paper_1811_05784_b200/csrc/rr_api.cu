@@ -473,8 +473,8 @@ rr_status rr_synthesize(rr_ctx* ctx, int64_t n, const double* dist, const double
     dd.alloc(std::max<int64_t>(n, 1), st);
     de.alloc(rr::kBands * std::max<int64_t>(n, 1), st);
     if (n > 0) {
-      RR_CUDA(cudaMemcpyAsync(dd.p, dist, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-      RR_CUDA(cudaMemcpyAsync(de.p, energy, sizeof(double) * rr::kBands * n, cudaMemcpyHostToDevice, st));
+      RR_CUDA(cudaMemcpyAsync(dd.p, dist, sizeof(double) * n, cudaMemcpyDefault, st));
+      RR_CUDA(cudaMemcpyAsync(de.p, energy, sizeof(double) * rr::kBands * n, cudaMemcpyDefault, st));
       rr::DevBuf<int> bad;
       bad.alloc(1, st);
       RR_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
@@ -977,3 +977,79 @@ rr_status abi_guard_nccl(const std::function<void()>& f) { return guarded(f); }
 void scene_retain(rr_scene* s) { s->refs++; }
 void scene_drop(rr_scene* s) { scene_release(s); }
 }  // namespace rr
+
+// ---------------------------------------------------------------- pulse trains / IR of a device image set
+namespace rr {
+void image_trains(rr_ctx* ctx, const double* d_dist, const double* d_energy, int64_t n, double c, double* time,
+                  double* amp);
+}
+namespace {
+__global__ void max_dist_kernel(const double* __restrict__ d, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, d[i]);
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+}  // namespace
+
+extern "C" {
+
+rr_status rr_images_pulse_trains(rr_images* im, double c, int64_t* band_off, double* time, double* amplitude) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");  // rir.cpp:11-13
+    rr_ctx* ctx = im->scene->ctx;
+    RR_CUDA(cudaSetDevice(ctx->device));
+    if (band_off)
+      for (int b = 0; b <= rr::kBands; ++b) band_off[b] = b * im->n;
+    if (im->n > 0) {
+      check_ptr(time, "time");
+      check_ptr(amplitude, "amplitude");
+      rr::image_trains(ctx, im->dist.p, im->energy.p, im->n, c, time, amplitude);
+    }
+  });
+}
+
+rr_status rr_images_synthesize(rr_images* im, double c, double fs, int32_t taps, int64_t* length, double* band_ir,
+                               double* broadband) {
+  return guarded([&] {
+    check_ptr(im, "images");
+    check_ptr(length, "length");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");
+    if (taps < 3) rr::invalid("taps must be >= 3");
+    rr_ctx* ctx = im->scene->ctx;
+    RR_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    if (!band_ir && !broadband) {  // the reference length (rir.cpp:78-80)
+      *length = 0;
+      if (im->n == 0) return;
+      rr::DevBuf<unsigned long long> mx;
+      mx.alloc(1, st);
+      RR_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
+      max_dist_kernel<<<148, 256, 0, st>>>(im->dist.p, im->n, mx.p);
+      RR_LAUNCH_CHECK();
+      ctx->launches++;
+      unsigned long long bits = 0;
+      RR_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof bits, cudaMemcpyDeviceToHost, st));
+      RR_CUDA(cudaStreamSynchronize(st));
+      double last;
+      std::memcpy(&last, &bits, sizeof last);
+      *length = static_cast<int64_t>(std::llround(last / c * fs)) + (taps - 1) / 2 + 1;
+      return;
+    }
+    if (*length <= 0) rr::invalid("length must be > 0");
+    const int64_t L = *length, lh = L + taps;
+    rr::DevBuf<double> hist, band, bb;
+    hist.alloc(rr::kBands * lh, st);
+    band.alloc(rr::kBands * L, st);
+    bb.alloc(L, st);
+    rr::ir_bin(ctx, im->n, im->dist.p, im->energy.p, c, fs, lh, hist.p);
+    rr::ir_filter(ctx, hist.p, lh, fs, taps, L, band.p, bb.p);
+    if (band_ir) RR_CUDA(cudaMemcpyAsync(band_ir, band.p, sizeof(double) * rr::kBands * L, cudaMemcpyDefault, st));
+    if (broadband) RR_CUDA(cudaMemcpyAsync(broadband, bb.p, sizeof(double) * L, cudaMemcpyDefault, st));
+    RR_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

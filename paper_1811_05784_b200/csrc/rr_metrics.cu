@@ -54,6 +54,15 @@ __global__ void energy_kernel(const double* __restrict__ t, const double* __rest
   es[i] = a[j] * a[j];  // metrics.cpp:121
 }
 
+__global__ void gather_pair_kernel(const double* __restrict__ t, const double* __restrict__ a,
+                                   const int32_t* __restrict__ perm, int64_t n, double* __restrict__ ts,
+                                   double* __restrict__ as) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ts[i] = t[perm[i]];
+  as[i] = a[perm[i]];
+}
+
 // pass 1: per-block (sum e, min time over e > 0)
 __global__ void pass1_kernel(const double* __restrict__ ts, const double* __restrict__ es, int64_t n,
                              double* __restrict__ part) {
@@ -321,6 +330,48 @@ void band_schroeder(rr_ctx* ctx, const int64_t* band_off, const double* amplitud
   RR_CUDA(cudaStreamSynchronize(st));
   for (int b = 0; b < kBands; ++b)
     if (h_silent[b]) invalid("decay of an all-zero signal is undefined");  // metrics.cpp:17-19
+}
+
+// build_pulse_trains (rir.cpp:9-30) of an image set on the device: band b's
+// events (t = d / c, amplitude sqrt(E_b)) sorted by (time, amplitude)
+// (rir.cpp:22-28, the two stable radix passes of band_factors), copied to
+// time / amp at [b * n, (b + 1) * n) (host or device buffers).
+void image_trains(rr_ctx* ctx, const double* d_dist, const double* d_energy, int64_t n, double c, double* time,
+                  double* amp) {
+  if (n <= 0) return;
+  cudaStream_t st = ctx->stream;
+  DevBuf<uint8_t> tmp;
+  DevBuf<double> t, a, ts, as;
+  DevBuf<unsigned long long> k, ko;
+  DevBuf<int32_t> i1, i2;
+  t.alloc(n, st);
+  a.alloc(n, st);
+  ts.alloc(n, st);
+  as.alloc(n, st);
+  k.alloc(n, st);
+  ko.alloc(n, st);
+  i1.alloc(n, st);
+  i2.alloc(n, st);
+  const unsigned g = static_cast<unsigned>((n + 255) / 256);
+  for (int b = 0; b < kBands; ++b) {
+    events_kernel<<<g, 256, 0, st>>>(d_dist, d_energy, n, c, b, t.p, a.p);
+    keys_kernel<<<g, 256, 0, st>>>(a.p, nullptr, n, k.p);
+    iota_kernel<<<g, 256, 0, st>>>(i2.p, n);
+    RR_LAUNCH_CHECK();
+    cub_do([&](void* tt, size_t& bb) {
+      return cub::DeviceRadixSort::SortPairs(tt, bb, k.p, ko.p, i2.p, i1.p, static_cast<int>(n), 0, 64, st);
+    }, tmp, st);
+    keys_kernel<<<g, 256, 0, st>>>(t.p, i1.p, n, k.p);
+    cub_do([&](void* tt, size_t& bb) {
+      return cub::DeviceRadixSort::SortPairs(tt, bb, k.p, ko.p, i1.p, i2.p, static_cast<int>(n), 0, 64, st);
+    }, tmp, st);
+    gather_pair_kernel<<<g, 256, 0, st>>>(t.p, a.p, i2.p, n, ts.p, as.p);
+    RR_LAUNCH_CHECK();
+    RR_CUDA(cudaMemcpyAsync(time + b * n, ts.p, sizeof(double) * n, cudaMemcpyDefault, st));
+    RR_CUDA(cudaMemcpyAsync(amp + b * n, as.p, sizeof(double) * n, cudaMemcpyDefault, st));
+    ctx->launches += 12;
+  }
+  RR_CUDA(cudaStreamSynchronize(st));
 }
 
 // factors(const PulseTrains&) for trains given as images: t = d / c,
