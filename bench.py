@@ -319,6 +319,12 @@ def run_ours(args):
 
     # the multi-GPU pipeline behind the C ABI (rr_pipeline_sharded): its own
     # NCCL communicator, the unique id from rank 0 over torch.distributed
+    _torch_dt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32,
+                 np.dtype(np.int64): torch.int64}
+
+    def pinned(shape, dtype):  # page-locked host outputs (full PCIe bandwidth)
+        return torch.empty(shape, dtype=_torch_dt[np.dtype(dtype)], pin_memory=True).numpy()
+
     comm = None
     if world > 1:
         uid = [rr.Comm.unique_id() if rank == 0 else None]
@@ -340,7 +346,7 @@ def run_ours(args):
         sc.ctx, sc.lib, sc.mesh, sc.h = ctx, lib, mesh, h
         res = rr.pipeline_sharded(sc, src, recv, cfg, comm=comm, air=rr.AirModel(),
                                   options=rr.ClusterOptions(1e-6, True), sample_rate=scene.sample_rate, length=L,
-                                  taps=taps, block=4096)
+                                  taps=taps, block=4096, alloc=pinned)
         # results in host memory: every receiver's 8 band IRs and broadband IR
         # (every rank), the merged image list (rank 0)
         fetched = []

@@ -442,11 +442,14 @@ class DeviceImages:
             self.lib.rr_images_destroy(self.h)
             self.h = None
 
-    def fetch(self) -> ImageSources:
+    def fetch(self, alloc=np.empty) -> ImageSources:
+        """Copy to host arrays made by alloc(shape, dtype) (numpy's by default;
+        pass a pinned-memory allocator for full-bandwidth copies)."""
         n = self.n
-        im = ImageSources(np.empty((n, 3)), np.empty(n), np.empty((n, NUM_BANDS)), np.empty((n, NUM_BANDS)),
-                          np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32), np.empty((n, 3)),
-                          np.empty(n + 1, np.int64), np.empty(max(self.total_path, 1), np.int32))
+        f8, i4 = np.float64, np.int32
+        im = ImageSources(alloc((n, 3), f8), alloc((n,), f8), alloc((n, NUM_BANDS), f8), alloc((n, NUM_BANDS), f8),
+                          alloc((n,), i4), alloc((n,), i4), alloc((n,), i4), alloc((n, 3), f8),
+                          alloc((n + 1,), np.int64), alloc((max(self.total_path, 1),), i4))
         check(self.lib.rr_images_get(self.h, ptr(im.position), ptr(im.distance), ptr(im.band_energy),
                                      ptr(im.band_multiplier), ptr(im.ray_count), ptr(im.order),
                                      ptr(im.has_projection), ptr(im.projection), ptr(im.path_off), ptr(im.path)))
@@ -744,10 +747,11 @@ class PipelineResult:
 def pipeline_sharded(tree: AccelTree, source: SourceConfig, receivers, config: TraceConfig = TraceConfig(), *,
                      comm: Comm | None = None, air: AirModel = AirModel(), options: ClusterOptions = ClusterOptions(),
                      sample_rate: float = 48000.0, length: int | None = None, taps: int = 1023, block: int = 4096,
-                     device_images: bool = False) -> PipelineResult:
+                     device_images: bool = False, alloc=np.empty) -> PipelineResult:
     """run_trace_pipeline's trace -> image sources -> IRs (pipeline.cpp:163-175)
     on the device, over the ranks of `comm` (rr_pipeline_sharded); comm=None
-    is the single-GPU pipeline.  Captures never leave the GPU."""
+    is the single-GPU pipeline.  Captures never leave the GPU.  Host outputs
+    go to arrays made by alloc(shape, dtype) (e.g. pinned memory)."""
     recs = receivers if isinstance(receivers, (list, tuple)) else [receivers]
     src = _lib.Source((C.c_double * 3)(*map(float, source.position)), int(source.ray_count))
     rarr = (_lib.Receiver * len(recs))(*[_lib.Receiver((C.c_double * 3)(*map(float, r.center)), float(r.radius))
@@ -772,9 +776,9 @@ def pipeline_sharded(tree: AccelTree, source: SourceConfig, receivers, config: T
             ih = C.c_void_p()
             check(lib.rr_sharded_take_images(h, r, C.byref(ih)))
             di = DeviceImages(lib, ih)
-            images.append(di if device_images else di.fetch())
-            band = np.empty((NUM_BANDS, length))
-            bb = np.empty(length)
+            images.append(di if device_images else di.fetch(alloc))
+            band = alloc((NUM_BANDS, length), np.float64)
+            bb = alloc((length,), np.float64)
             check(lib.rr_sharded_ir(h, r, band.ctypes.data, bb.ctypes.data))
             bands.append(band)
             bbs.append(bb)
