@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libroomray_b200.so")
+# RR_LIB_PATH selects another build of the same ABI, e.g. the checked one
+# (libroomray_b200_checked.so: device-side bounds checks, tests/test_gpu_checked.py)
+LIB_PATH = os.environ.get("RR_LIB_PATH") or os.path.join(HERE, "libroomray_b200.so")
 
 RR_OK, RR_INVALID_ARGUMENT, RR_RUNTIME, RR_CUDA, RR_NCCL = range(5)
 RR_TRACE_NO_SMEM_CACHE = 1

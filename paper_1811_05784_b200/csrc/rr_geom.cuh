@@ -356,6 +356,7 @@ __device__ __forceinline__ HitResult closest_hit_pl(const TravHeader& h, const T
         const bool lf = tl <= tr;
         const int2 e = make_int2(lf ? dd.y : dd.x, __float_as_int(lf ? tr : tl));
         if (TOS > 0) {
+          RR_DCHECK(n_top < TOS || sp < kStack - SMS);
           if (n_top == TOS) st[sp++] = top[TOS - 1];  // the oldest register entry spills
 #pragma unroll
           for (int k = TOS - 1; k > 0; --k) top[k] = top[k - 1];
@@ -442,6 +443,7 @@ __device__ __forceinline__ HitResult closest_hit4_pl(const TravHeader& h, const 
   int n_top = 0;
   int32_t leaf = 0;
   auto push = [&](int2 e) {
+    RR_DCHECK(sp < kStack4);
     if (TOS > 0) {
       if (n_top == TOS) st[sp++] = top[TOS - 1];
 #pragma unroll

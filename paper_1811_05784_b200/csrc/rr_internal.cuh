@@ -37,6 +37,24 @@ struct Error : std::runtime_error {
 
 #define RR_LAUNCH_CHECK() RR_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the checked build (libroomray_b200_checked.so,
+// -DRR_CHECKED; tests/test_gpu_checked.py): stack depths, node / face /
+// history indices.  A failed check prints and traps (the launch fails with
+// an error instead of touching memory it must not).  Compiled out otherwise.
+#ifdef RR_CHECKED
+#define RR_DCHECK(c)                                                               \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("RR_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define RR_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 // Device buffer, stream-ordered allocation on the owning context's stream.
 template <typename T>
 struct DevBuf {

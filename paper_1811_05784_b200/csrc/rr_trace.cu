@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const TraceParams p) {
         rplane = -2;
       }
       path += wall.delta;
+      RR_DCHECK(ray < p.count && bounces < p.H && wall.face < p.nf);
       p.hist[ray * p.H + bounces] = wall.face;
       ++bounces;
       if (path > p.max_range) {
@@ -516,6 +517,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (want8) build_wide(s);
   p.wnodes = s->wnodes.p;
   p.wtri = s->wtri.p;
+  p.n_wnodes = static_cast<int32_t>(s->wnodes.n);
+  p.nf = s->nf;
   p.nodes = sah ? s->snodes.p : s->tnodes.p;
   p.qnodes = s->qnodes.p;
   // default: binary nodes, fp64 test at every leaf (fastest measured); diagnostics: fp32 leaf classification, 4-wide nodes

@@ -23,6 +23,8 @@ struct TraceParams {
   int32_t root4;
   const WNode* wnodes;  // 8-wide compressed collapse of the SAH tree (rr_wide.cu)
   const FaceTri* wtri;  // faces in its leaf order
+  int32_t n_wnodes;     // (bounds checks of the checked build)
+  int64_t nf;
   int32_t wide;  // 1: traverse the 4-wide QNodes, 0: the binary TNodes
   const FaceTri* tri;
   const float4* tri32;

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   int32_t st_max = 0;
 
   auto st_put = [&](int i, int2 e) {
+    RR_DCHECK(i < STK);
     if (SMS > 0 && i < SMS) sst[i * 128] = e;
     else st[i - SMS] = e;
   };
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           rplane = -2;
         }
         path += best.delta;
+        RR_DCHECK(ray < p.count && bounces < p.H && best.face < p.nf);
         p.hist[ray * p.H + bounces] = best.face;
         ++bounces;
         if (path > p.max_range) {
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         for (int u = 0; u < UNR && is_inner(node) && (u == 0 || leaf == 0); ++u) {
           if (CNT) ++st_cnt[0];
           WVisit v;
+          RR_DCHECK(node < p.n_wnodes);
           visit_w8(p.wnodes, node, r, px, py, pz, tbest, rplane, v);
           const uint32_t hm = v.hit;
           if (hm == 0) {
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           if (2 * __popc(mv) >= na || cv == 0 || 2 * __popc(hv) >= na) {
             if (leaf != 0) {
               if (CNT) st_cnt[1] += leaf_faces(leaf);
+              RR_DCHECK(leaf_face(leaf) + leaf_faces(leaf) <= p.nf);
               if (test_leaf_w(p.wtri, leaf, o, d, best)) tbest = prune_bound(best.delta, r.shift);
               leaf = 0;
               if (node < 0) {  // the leaf that waited for the slot

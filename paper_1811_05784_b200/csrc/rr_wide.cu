@@ -149,7 +149,7 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
                              const FaceTri* __restrict__ tri,
                              double margin, WNode* __restrict__ out, FaceTri* __restrict__ wtri,
                              int32_t* __restrict__ next_frontier, int32_t* __restrict__ next_acc,
-                             int32_t* __restrict__ bound, int32_t* __restrict__ emax) {
+                             int32_t* __restrict__ bound, int32_t* __restrict__ emax, int64_t n_faces) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
@@ -188,6 +188,7 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       const int nl = leaf_faces(s[k].ref);
       if (nl == 2) pair |= 1u << k;
       for (int j = 0; j < nl; ++j) {
+        RR_DCHECK(ti + nfc + j < n_faces && f0 + j < n_faces);
         FaceTri ft = tri[f0 + j];
         ft.pad = __longlong_as_double(static_cast<long long>(f0 + j));
         wtri[ti + nfc + j] = ft;
@@ -255,7 +256,7 @@ void build_wide(rr_scene* s) {
     ac[1].alloc(std::max(n_next, 1), st);
     write_kernel<<<grid(n), 256, 0, st>>>(slots.p, nslot.p, offs.p, n, base, base + n,
                                           static_cast<int32_t>(tri_done), ac[0].p, s->tri.p, margin, nodes.p,
-                                          s->wtri.p, fr[1].p, ac[1].p, bound.p, bound.p + 1);
+                                          s->wtri.p, fr[1].p, ac[1].p, bound.p, bound.p + 1, nf);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 5;
     tri_done += n_tri;
