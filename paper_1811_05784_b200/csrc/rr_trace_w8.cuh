@@ -23,7 +23,7 @@
 
 namespace rr {
 
-template <int MINB, int DONET, int UNR, int STK, bool CNT = false, bool SORT = true, int SMS = 0>
+template <int MINB, int DONET, int UNR, int STK, bool CNT = false, int SMS = 0>
 __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p) {
   // the SMS oldest stack entries of each lane in shared memory (column tid:
   // lane i always in bank i, conflict-free), deeper ones in local memory
@@ -229,34 +229,33 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           if (hm == 0) {
             pop();
           } else {
-            // continue into the nearest hit slot; push the others (SORT: in
-            // descending entry distance, else in slot order, branch-free)
-            float tmn = kInf;
-            int kmn = 0;
+            // continue into the nearest hit slot; push the others farthest
+            // first.  Sort keys pack the entry distance (clamped at 0, low 3
+            // mantissa bits replaced by the slot, top bit set so no hit key
+            // is 0) into one u32: t >= 0 orders like its bits, so min / max
+            // are integer min / max; a pushed entry keeps t rounded down by
+            // < 8 ulps (pruning stays conservative).
+            uint32_t key[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              if (((hm >> k) & 1u) && v.t[k] < tmn) {
-                tmn = v.t[k];
-                kmn = k;
-              }
-            uint32_t rest = hm & ~(1u << kmn);
-            if (SORT) {
-              while (rest) {  // push the farthest first
-                float tmx = -kInf;
-                int kmx = 0;
+              key[k] = ((hm >> k) & 1u) ? (0x80000000u | (__float_as_uint(fmaxf(v.t[k], 0.0f)) & ~7u) | k) : 0u;
+            uint32_t mn = 0xffffffffu;
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  if (((rest >> k) & 1u) && v.t[k] > tmx) {
-                    tmx = v.t[k];
-                    kmx = k;
-                  }
-                push(make_int2(wref(v, kmx), __float_as_int(tmx)));
-                rest &= ~(1u << kmx);
-              }
-            } else if (rest) {
+            for (int k = 0; k < 8; ++k) mn = min(mn, key[k] ? key[k] : 0xffffffffu);
+            const int kmn = static_cast<int>(mn & 7u);
+            if (hm & (hm - 1u)) {
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if ((rest >> k) & 1u) push(make_int2(wref(v, k), __float_as_int(v.t[k])));
+              for (int k = 0; k < 8; ++k) key[k] = k == kmn ? 0u : key[k];
+              for (;;) {
+                uint32_t mx = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mx = max(mx, key[k]);
+                if (mx == 0) break;
+                const int kmx = static_cast<int>(mx & 7u);
+                push(make_int2(wref(v, kmx), static_cast<int>(mx & 0x7ffffff8u)));
+#pragma unroll
+                for (int k = 0; k < 8; ++k) key[k] = k == kmx ? 0u : key[k];
+              }
             }
             node = wref(v, kmn);
           }
