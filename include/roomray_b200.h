@@ -222,7 +222,8 @@ rr_status rr_images_get(rr_images* im, double* pos, double* dist,
  * `stream` (a cudaStream_t; 0 = the legacy default stream) after the work
  * enqueued so far on the context's stream, so a D2H into pinned memory can
  * overlap later device work (the IR stage).  The caller synchronizes
- * `stream` before reading the outputs or destroying `im`. */
+ * `stream` before reading the outputs; rr_images_destroy may come earlier
+ * (its stream-ordered frees wait for the copies). */
 rr_status rr_images_get_async(rr_images* im, void* stream, double* pos,
                               double* dist, double* energy, double* mult,
                               int32_t* ray_count, int32_t* order,

@@ -946,6 +946,10 @@ rr_status rr_images_get_async(rr_images* im, void* stream, double* pos, double* 
     cp(proj, im->proj.p, sizeof(double) * 3 * n);
     cp(path_off, im->path_off.p, sizeof(int64_t) * (n + 1));
     cp(path, im->path.p, sizeof(int32_t) * im->total_path);
+    if (st != ctx) {  // rr_images_destroy orders its frees after these copies
+      if (!im->copies_done) RR_CUDA(cudaEventCreateWithFlags(&im->copies_done, cudaEventDisableTiming));
+      RR_CUDA(cudaEventRecord(im->copies_done, st));
+    }
   });
 }
 
@@ -954,6 +958,10 @@ rr_status rr_images_destroy(rr_images* im) {
     if (!im) return;
     rr_scene* sc = im->scene;
     cudaSetDevice(sc->ctx->device);
+    if (im->copies_done) {  // copies on a caller stream (rr_images_get_async) before the stream-ordered frees
+      cudaStreamWaitEvent(sc->ctx->stream, im->copies_done, 0);
+      cudaEventDestroy(im->copies_done);
+    }
     delete im;
     cudaStreamSynchronize(sc->ctx->stream);
     scene_release(sc);

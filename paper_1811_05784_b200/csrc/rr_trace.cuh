@@ -91,6 +91,7 @@ struct rr_images {
   rr::DevBuf<double> pos, dist, energy, mult, proj;
   rr::DevBuf<int32_t> ray_count, order, has_proj, path;
   rr::DevBuf<int64_t> path_off;
+  cudaEvent_t copies_done = nullptr;  // last rr_images_get_async on a caller stream
 };
 
 namespace rr {
