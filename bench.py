@@ -168,10 +168,11 @@ def load_scene(name):
     return scenes.CONFIGS[name]()
 
 
-def cpu_reference_sample(scene, seconds, threads):
+def cpu_reference_sample(scene, seconds, threads, stride=None):
     """The reference's own trace loop (oracle/_ref: unmodified tracer.cpp,
     step() with thread_count = threads) on a strided subset of the lattice,
-    sized to ~`seconds` of work.  Returns (rate, sample description, kind)."""
+    sized to ~`seconds` of work (or the given stride).  Returns (rate,
+    sample description, kind, ray*bounces, seconds, stride)."""
     import oracle
     if oracle.ref_available():
         lib = oracle.Ref()
@@ -195,9 +196,10 @@ def cpu_reference_sample(scene, seconds, threads):
             return st.ray_bounces, time.perf_counter() - t
     # size the strided sample to ~`seconds` (the first probes underestimate
     # the rate: thread start-up and tail imbalance on few rays)
-    stride = max(1, scene.ray_count // 2000)
+    fixed = stride is not None
+    stride = stride if fixed else max(1, scene.ray_count // 2000)
     rb, dt = run(stride)
-    for _ in range(3):
+    for _ in range(0 if fixed else 3):
         if dt >= 0.5 * seconds or stride == 1:
             break
         rays_now = (scene.ray_count + stride - 1) // stride
@@ -206,7 +208,7 @@ def cpu_reference_sample(scene, seconds, threads):
         rb, dt = run(stride)
     rays = (scene.ray_count + stride - 1) // stride
     return rb / dt, f"{rays} of {scene.ray_count} lattice rays (k = 0 mod {stride}), {rb} ray*bounces, {dt:.2f} s", \
-        kind, rb, dt
+        kind, rb, dt, stride
 
 
 def native_pipeline(scene, steps, warmup):
@@ -426,7 +428,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
-            rate, sample, kind, _, _ = cpu_reference_sample(scene, args.cpu_seconds, threads)
+            rate, sample, kind, _, _, _ = cpu_reference_sample(scene, args.cpu_seconds, threads)
             cpu = {"value": round(rate, 1), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
         native = None
         if world == 1 and not args.no_native:
@@ -467,10 +469,13 @@ def run_reference(args):
         return None
     scene = load_scene(args.config)
     threads = os.cpu_count() or 1
-    per_step = max(2.0, args.cpu_seconds / 3)
+    # the sample size (lattice stride) is fixed once, ~cpu_seconds / 2 of
+    # work per step; every step then traces that same subset
+    per_step = max(2.0, args.cpu_seconds / 2)
+    stride = None
     rates = []
     for i in range(args.warmup + args.steps):
-        rate, sample, kind, rb, dt = cpu_reference_sample(scene, per_step, threads)
+        rate, sample, kind, rb, dt, stride = cpu_reference_sample(scene, per_step, threads, stride)
         if i >= args.warmup:
             rates.append((rb, dt, sample, kind))
     rb = sum(r[0] for r in rates)

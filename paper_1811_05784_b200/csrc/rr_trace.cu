@@ -644,11 +644,13 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   }();
   const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8 && s->wide_ok;
   using KFn = void (*)(const TraceParams);
-  // A/B (C5, ms): default (MINB 8, DONET 8, UNR 1, sorted pushes) 657;
-  // unsorted pushes 667; 12 stack entries in shared memory 658 (RR_W8V=1);
-  // MINB 7 666; DONET 16 / UNR 4 at MINB 6 716; UNR 8 810; no batching
-  // (the per-ray loop) 1074
-  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8, false, 12> : trace_kernel_w8<8, 8, 1, kStack8>;
+  // A/B (C5, ms; before the ray state moved to shared memory): MINB 8,
+  // DONET 8, UNR 1, sorted pushes 657; unsorted pushes 667; 12 stack
+  // entries in shared memory 658; MINB 7 666; DONET 16 / UNR 4 at MINB 6
+  // 716; UNR 8 810; no batching (the per-ray loop) 1074.  After: 587
+  // (RR_W8V=1: MINB 9 592; 10: 620; 12: 692)
+  KFn w8k = w8v == 1 ? trace_kernel_w8<9, 8, 1, kStack8> : w8v == 2 ? trace_kernel_w8<8, 8, 1, kStack8, false, 12>
+                     : trace_kernel_w8<8, 8, 1, kStack8>;
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);

@@ -32,26 +32,43 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const float kInf = __int_as_float(0x7f800000);
-  // ray
-  int64_t ray = -1;
+  // the fp64 ray state (origin, direction, best hit so far, path length, ray
+  // index, step and bounce counts) lives in shared memory: the node visits,
+  // the bulk of the work, need only the fp32 slab data in registers; the
+  // leaf tests and the shading read it from shared memory.  Each register
+  // moved out of the 64-register budget of 8 blocks per SM removed spill
+  // traffic (C5: statistics 645 -> 628 ms, path / counters 610, origin /
+  // direction / best hit 587; 9 or 10 blocks per SM spill more, 592 / 620).
+  struct LaneState {
+    D3 o, d;
+    HitResult best;
+    double path;
+    int32_t ray, steps, bounces, pad;
+  };
+  __shared__ LaneState s_lane[128];
+  LaneState& ls = s_lane[threadIdx.x];
+  D3& o = ls.o;
+  D3& d = ls.d;
+  HitResult& best = ls.best;
+  bool has_ray = false;
   bool exhausted = false;
-  D3 o{}, d{};
-  double path = 0.0;
-  int32_t steps = 0, bounces = 0, rplane = -2;
+  int32_t rplane = -2;
   // traversal of the current step
   bool searching = false;  // a closest-hit query is in progress
   RayF r{};
   bool px = true, py = true, pz = true;
   float tbest = FLT_MAX;
-  HitResult best{0.0, -1};
   int32_t node = kDone, leaf = 0;
   int2 st[STK - SMS];
   int sp = 0;
   int2 top[2] = {};
   int n_top = 0;
-  uint32_t st_bounce = 0, st_esc = 0, st_oor = 0, st_alive = 0;
+  // termination statistics in shared memory (updated once per ray, rare),
+  // which keeps five counters out of the register budget
+  __shared__ unsigned long long s_stat[5];  // bounces, escaped, out of range, alive, max steps
+  if (threadIdx.x < 5) s_stat[threadIdx.x] = 0;
+  __syncthreads();
   unsigned long long st_cnt[2] = {0, 0};
-  int32_t st_max = 0;
 
   auto st_put = [&](int i, int2 e) {
     RR_DCHECK(i < STK);
@@ -87,7 +104,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   };
   // start the closest-hit query of the next step_ray
   auto begin_query = [&]() {
-    ++steps;
+    ++ls.steps;
     best = HitResult{0.0, -1};
     tbest = FLT_MAX;
     sp = 0;
@@ -107,7 +124,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
 
   for (;;) {
     // ---------------- shading: rays whose query finished, and new rays
-    const bool shade = ray >= 0 && !searching;
+    const bool shade = has_ray && !searching;
     if (shade) {
       const bool has_wall = best.face >= 0;
       for (int rc = 0; rc < p.n_recv; ++rc) {
@@ -115,7 +132,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         bool cap = sd > 0.0 && (!has_wall || sd < best.delta);
         double L = 0.0;
         if (cap) {
-          L = path + sd;
+          L = ls.path + sd;
           cap = L <= p.rng[rc];  // resolved_max_range of receiver rc
         }
         const unsigned act = __activemask();
@@ -133,8 +150,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
               c.p[0] = pt.x; c.p[1] = pt.y; c.p[2] = pt.z;
               c.d[0] = d.x; c.d[1] = d.y; c.d[2] = d.z;
               c.path = L;
-              c.ray = static_cast<int32_t>(ray);
-              c.meta = (bounces << 8) | rc;
+              c.ray = ls.ray;
+              c.meta = (ls.bounces << 8) | rc;
               p.caps[slot] = c;
             }
           }
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
       bool dead = false;
       if (!has_wall) {
         dead = true;
-        st_esc++;
+        atomicAdd(s_stat + 1, 1ull);
       } else {
         const double* nn = p.normal + 3 * static_cast<int64_t>(best.face);
         D3 n = d3(__ldg(nn), __ldg(nn + 1), __ldg(nn + 2));
@@ -162,29 +179,29 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         } else {
           rplane = -2;
         }
-        path += best.delta;
-        RR_DCHECK(ray < p.count && bounces < p.H && best.face < p.nf);
-        p.hist[ray * p.H + bounces] = best.face;
-        ++bounces;
-        if (path > p.max_range) {
+        ls.path += best.delta;
+        RR_DCHECK(ls.ray < p.count && ls.bounces < p.H && best.face < p.nf);
+        p.hist[static_cast<int64_t>(ls.ray) * p.H + ls.bounces] = best.face;
+        ++ls.bounces;
+        if (ls.path > p.max_range) {
           dead = true;
-          st_oor++;
+          atomicAdd(s_stat + 2, 1ull);
         }
       }
-      if (!dead && steps >= p.max_iter) {
+      if (!dead && ls.steps >= p.max_iter) {
         dead = true;
-        st_alive++;
+        atomicAdd(s_stat + 3, 1ull);
       }
       if (dead) {
-        st_bounce += steps;
-        st_max = max(st_max, steps);
-        ray = -1;
+        atomicAdd(s_stat + 0, static_cast<unsigned long long>(ls.steps));
+        atomicMax(s_stat + 4, static_cast<unsigned long long>(ls.steps));
+        has_ray = false;
       } else {
         begin_query();
       }
     }
     // new rays (warp-aggregated fetch from the global counter)
-    const bool need = ray < 0 && !exhausted;
+    const bool need = !has_ray && !exhausted;
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m) {
       const int leader = __ffs(m) - 1;
@@ -195,17 +212,18 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         const int64_t c = static_cast<int64_t>(base) + __popc(m & lt_mask);
         if (c < p.count) {
           const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + c)) : c;
-          ray = i;
+          has_ray = true;
+          ls.ray = static_cast<int32_t>(i);
           o = d3(p.src[0], p.src[1], p.src[2]);
           d = p.dirs ? d3(p.dirs[3 * i], p.dirs[3 * i + 1], p.dirs[3 * i + 2])
                      : fib_dir(global_ray(p, i), p.N, p.az_step);
-          path = 0.0;
-          steps = 0;
-          bounces = 0;
+          ls.path = 0.0;
+          ls.steps = 0;
+          ls.bounces = 0;
           rplane = -2;
           if (p.max_iter <= 0) {  // trace() with a zero cap: nothing runs
-            st_alive++;
-            ray = -1;
+            atomicAdd(s_stat + 3, 1ull);
+            has_ray = false;
           } else {
             begin_query();
           }
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         }
       }
     }
-    if (__all_sync(0xffffffffu, ray < 0 && exhausted)) break;
+    if (__all_sync(0xffffffffu, !has_ray && exhausted)) break;
 
     // ---------------- traversal until DONET lanes wait for shading
     for (;;) {
@@ -293,25 +311,14 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         if (node == kDone && leaf == 0) searching = false;  // query done: best holds the hit
       }
       const unsigned sv = __ballot_sync(0xffffffffu, searching);
-      const unsigned wv = __ballot_sync(0xffffffffu, ray >= 0 && !searching);
+      const unsigned wv = __ballot_sync(0xffffffffu, has_ray && !searching);
       if (sv == 0 || __popc(wv) >= DONET) break;
     }
   }
   // ---- statistics
-  for (int off = 16; off > 0; off >>= 1) {
-    st_bounce += __shfl_xor_sync(0xffffffffu, st_bounce, off);
-    st_esc += __shfl_xor_sync(0xffffffffu, st_esc, off);
-    st_oor += __shfl_xor_sync(0xffffffffu, st_oor, off);
-    st_alive += __shfl_xor_sync(0xffffffffu, st_alive, off);
-    st_max = max(st_max, __shfl_xor_sync(0xffffffffu, st_max, off));
-  }
-  if (lane == 0) {
-    atomicAdd(p.stats + 0, (unsigned long long)st_bounce);
-    atomicAdd(p.stats + 1, (unsigned long long)st_esc);
-    atomicAdd(p.stats + 2, (unsigned long long)st_oor);
-    atomicAdd(p.stats + 3, (unsigned long long)st_alive);
-    atomicMax(p.stats + 4, (unsigned long long)st_max);
-  }
+  __syncthreads();
+  if (threadIdx.x < 4) atomicAdd(p.stats + threadIdx.x, s_stat[threadIdx.x]);
+  if (threadIdx.x == 4) atomicMax(p.stats + 4, s_stat[4]);
   if (CNT) {
     for (int off = 16; off > 0; off >>= 1) {
       st_cnt[0] += __shfl_xor_sync(0xffffffffu, st_cnt[0], off);
