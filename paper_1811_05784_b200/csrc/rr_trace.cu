@@ -649,14 +649,15 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // entries in shared memory 658; MINB 7 666; DONET 16 / UNR 4 at MINB 6
   // 716; UNR 8 810; no batching (the per-ray loop) 1074.  After: 587
   // (RR_W8V=1: MINB 9 592; 10: 620; 12: 692)
-  KFn w8k = w8v == 1 ? trace_kernel_w8<9, 8, 1, kStack8> : w8v == 2 ? trace_kernel_w8<8, 8, 1, kStack8, false, 12>
-                     : trace_kernel_w8<8, 8, 1, kStack8>;
+  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8> : w8v == 2 ? trace_kernel_w8<8, 6, 1, kStack8, false, 12>
+          : w8v == 3 ? trace_kernel_w8<8, 8, 1, kStack8, false, 8>
+                     : trace_kernel_w8<8, 8, 1, kStack8, false, 12>;
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8   ? trace_kernel_w8<8, 8, 1, kStack8, true>
+    dfk = wide8   ? trace_kernel_w8<8, 8, 1, kStack8, true, 12>
           : wide4 ? trace_kernel<3, 8, false, 0, 1, true>
                   : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
@@ -675,7 +676,10 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
       if (smem > 0)
         RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     } else {
-      RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      cudaFuncAttributes fa{};
+      RR_CUDA(cudaFuncGetAttributes(&fa, kernel));
+      const int dyn = std::min<int>(200 * 1024, 227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
+      RR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     }
     RR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache_blocks, kernel, 128, smem));
     occ_cache_smem = static_cast<int>(smem);
