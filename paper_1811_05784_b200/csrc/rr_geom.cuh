@@ -891,6 +891,20 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
   return r;
 }
 
+#ifndef RR_FFMA2
+#define RR_FFMA2 1
+#endif
+// (f0, f1) * a + c in one packed fp32x2 FMA (Blackwell FFMA2), each lane
+// rounded like __fmaf_rn
+__device__ __forceinline__ float2 fma2(float f0, float f1, float a, float c) {
+  float2 r;
+  asm("{\n\t.reg .b64 F, A, C, D;\n\tmov.b64 F, {%2, %3};\n\tmov.b64 A, {%4, %4};\n\tmov.b64 C, {%5, %5};\n\t"
+      "fma.rn.f32x2 D, F, A, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(f0), "f"(f1), "f"(a), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t node, const RayF& r, bool px, bool py,
                                          bool pz, float tmax, int32_t rplane, WVisit& v) {
   const float4* q = reinterpret_cast<const float4*>(wn + node);
@@ -913,6 +927,27 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
   const uint32_t bits = static_cast<uint32_t>(mm.w);
   const uint32_t cull = mm.z == rplane ? (bits >> 16) & 0xffu : 0u;
   uint32_t hit = 0;
+#if RR_FFMA2
+  // two slots per packed FFMA2 (fma.rn.f32x2: each lane rounds like FFMA)
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t wnx = k < 4 ? nx0 : nx1, wfx = k < 4 ? fx0 : fx1;
+    const uint32_t wny = k < 4 ? ny0 : ny1, wfy = k < 4 ? fy0 : fy1;
+    const uint32_t wnz = k < 4 ? nz0 : nz1, wfz = k < 4 ? fz0 : fz1;
+    const float2 nx = fma2(wbyte(wnx, k), wbyte(wnx, k + 1), ax, cx);
+    const float2 ny = fma2(wbyte(wny, k), wbyte(wny, k + 1), ay, cy);
+    const float2 nz = fma2(wbyte(wnz, k), wbyte(wnz, k + 1), az, cz);
+    const float2 fx = fma2(wbyte(wfx, k), wbyte(wfx, k + 1), ax, cx);
+    const float2 fy = fma2(wbyte(wfy, k), wbyte(wfy, k + 1), ay, cy);
+    const float2 fz = fma2(wbyte(wfz, k), wbyte(wfz, k + 1), az, cz);
+    const float tn0 = fmax3(nx.x, ny.x, nz.x), tf0 = fmin3(fx.x, fy.x, fz.x);
+    const float tn1 = fmax3(nx.y, ny.y, nz.y), tf1 = fmin3(fx.y, fy.y, fz.y);
+    v.t[k] = tn0;
+    v.t[k + 1] = tn1;
+    if (tn0 <= fminf(tf0, tmax) && tf0 >= 0.0f) hit |= 1u << k;
+    if (tn1 <= fminf(tf1, tmax) && tf1 >= 0.0f) hit |= 2u << k;
+  }
+#else
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t wnx = k < 4 ? nx0 : nx1, wfx = k < 4 ? fx0 : fx1;
@@ -925,6 +960,7 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
     v.t[k] = tn;
     if (tn <= fminf(tf, tmax) && tf >= 0.0f) hit |= 1u << k;
   }
+#endif
   v.hit = hit & bits & 0xffu & ~cull;
   v.imask = hw >> 24;
   v.child = mm.x;
