@@ -147,6 +147,20 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
   return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
+#ifndef RR_FFMA2
+#define RR_FFMA2 1
+#endif
+// (f0, f1) * a + c in one packed fp32x2 FMA (Blackwell FFMA2), each lane
+// rounded like __fmaf_rn
+__device__ __forceinline__ float2 fma2(float f0, float f1, float a, float c) {
+  float2 r;
+  asm("{\n\t.reg .b64 F, A, C, D;\n\tmov.b64 F, {%2, %3};\n\tmov.b64 A, {%4, %4};\n\tmov.b64 C, {%5, %5};\n\t"
+      "fma.rn.f32x2 D, F, A, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(f0), "f"(f1), "f"(a), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ TNode load_node(const TNode* __restrict__ g, const TNode* s, int32_t n, int32_t K) {
   if (n < K) return s[n];
   const float4* p = reinterpret_cast<const float4*>(g + n);
@@ -888,20 +902,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float r;
   asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
-#ifndef RR_FFMA2
-#define RR_FFMA2 1
-#endif
-// (f0, f1) * a + c in one packed fp32x2 FMA (Blackwell FFMA2), each lane
-// rounded like __fmaf_rn
-__device__ __forceinline__ float2 fma2(float f0, float f1, float a, float c) {
-  float2 r;
-  asm("{\n\t.reg .b64 F, A, C, D;\n\tmov.b64 F, {%2, %3};\n\tmov.b64 A, {%4, %4};\n\tmov.b64 C, {%5, %5};\n\t"
-      "fma.rn.f32x2 D, F, A, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
-      : "=f"(r.x), "=f"(r.y)
-      : "f"(f0), "f"(f1), "f"(a), "f"(c));
   return r;
 }
 
