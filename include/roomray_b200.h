@@ -36,6 +36,7 @@ typedef struct rr_lattice rr_lattice;
 typedef struct rr_match rr_match;
 typedef struct rr_comm rr_comm;
 typedef struct rr_sharded rr_sharded;
+typedef struct rr_hub rr_hub;
 
 /* Reference-layout tree node (TreeNode, accel_tree.hpp:15-22): post-order,
  * root last, leaves hold one face. */
@@ -387,6 +388,14 @@ rr_status rr_comm_unique_id(uint8_t* id); /* ncclGetUniqueId, RR_NCCL_ID_BYTES b
 rr_status rr_comm_init(rr_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
                        rr_comm** out); /* ncclCommInitRank on ctx's device */
 rr_status rr_comm_info(rr_comm* comm, int32_t* rank, int32_t* nranks);
+/* Testing aid: an in-process loopback hub of nranks ranks on ONE GPU, each
+ * rank a host thread with its own rr_ctx; rr_pipeline_sharded's collectives
+ * then rendezvous on the hub and move data by device copies instead of NCCL,
+ * so the multi-rank exchange (sharding, ownership, packing, all-to-all,
+ * exact IR reduction, gather) runs where only one GPU exists. */
+rr_status rr_hub_create(int32_t nranks, rr_hub** out);
+rr_status rr_hub_destroy(rr_hub* hub);
+rr_status rr_comm_init_loopback(rr_ctx* ctx, rr_hub* hub, int32_t rank, rr_comm** out);
 rr_status rr_comm_destroy(rr_comm* comm);
 rr_status rr_pipeline_sharded(rr_scene* scene, rr_comm* comm, const rr_source* source,
                               const rr_receiver* receivers, int32_t n_recv,

@@ -139,6 +139,9 @@ SIGNATURES = [
     ("rr_comm_unique_id", C.c_int, [_vp]),
     ("rr_comm_init", C.c_int, [_vp, _vp, _i32, _i32, C.POINTER(_vp)]),
     ("rr_comm_info", C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    ("rr_hub_create", C.c_int, [_i32, C.POINTER(_vp)]),
+    ("rr_hub_destroy", C.c_int, [_vp]),
+    ("rr_comm_init_loopback", C.c_int, [_vp, _vp, _i32, C.POINTER(_vp)]),
     ("rr_comm_destroy", C.c_int, [_vp]),
     ("rr_pipeline_sharded", C.c_int, [_vp, _vp, C.POINTER(Source), C.POINTER(Receiver), _i32,
                                       C.POINTER(TraceConfig), C.POINTER(Air), C.POINTER(ClusterOptions), _d, _i64,

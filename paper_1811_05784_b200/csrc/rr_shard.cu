@@ -34,18 +34,51 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
+#include <tuple>
 #include <numeric>
 #include <vector>
 
 #include "rr_trace.cuh"
 
+// In-process loopback "communicator" for testing the multi-rank exchange on
+// one GPU: every rank is a host thread with its own context (same device);
+// the collectives rendezvous on the hub and move data with device copies.
+// Only the NCCL calls themselves are bypassed (rr_comm_init_loopback).
+struct rr_hub {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const void*> ptr;                                      // per rank: published buffer
+  std::vector<std::vector<std::tuple<int, const void*, size_t>>> sends;  // per rank: (peer, buf, bytes)
+  explicit rr_hub(int ranks) : n(ranks), ptr(ranks, nullptr), sends(ranks) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct rr_comm {
   rr_ctx* ctx = nullptr;
   ncclComm_t nccl = nullptr;
+  rr_hub* hub = nullptr;  // loopback ranks (tests) instead of NCCL
   int rank = 0, nranks = 1;
+  // a loopback group's pending point-to-point operations
+  std::vector<std::tuple<int, const void*, size_t>> g_send;
+  std::vector<std::tuple<int, void*, size_t>> g_recv;
 };
 
 struct rr_sharded {
@@ -218,6 +251,114 @@ ncclDataType_t nccl_type<int32_t>() { return ncclInt32; }
 template <>
 ncclDataType_t nccl_type<int64_t>() { return ncclInt64; }
 
+// ---- collectives: NCCL, or the loopback hub (tests)
+__global__ void u64_reduce_kernel(const unsigned long long* const* __restrict__ src, int n_src, int64_t count,
+                                  int op_max, unsigned long long* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  unsigned long long v = src[0][i];
+  for (int r = 1; r < n_src; ++r) v = op_max ? max(v, src[r][i]) : v + src[r][i];
+  out[i] = v;
+}
+
+void allreduce_u64(rr_comm* cm, unsigned long long* buf, int64_t count, bool op_max, cudaStream_t st) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclAllReduce(buf, buf, count, ncclUint64, op_max ? ncclMax : ncclSum, cm->nccl, st));
+    return;
+  }
+  rr_hub* h = cm->hub;
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->ptr[cm->rank] = buf;
+  h->barrier();
+  DevBuf<unsigned long long> tmp;
+  DevBuf<const unsigned long long*> srcs;
+  tmp.alloc(std::max<int64_t>(count, 1), st);
+  srcs.alloc(h->n, st);
+  std::vector<const unsigned long long*> hs(h->n);
+  for (int r = 0; r < h->n; ++r) hs[r] = static_cast<const unsigned long long*>(h->ptr[r]);
+  RR_CUDA(cudaMemcpyAsync(srcs.p, hs.data(), sizeof(void*) * h->n, cudaMemcpyHostToDevice, st));
+  u64_reduce_kernel<<<grid(count), 256, 0, st>>>(srcs.p, h->n, count, op_max ? 1 : 0, tmp.p);
+  RR_LAUNCH_CHECK();
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->barrier();  // every rank has read every buffer
+  RR_CUDA(cudaMemcpyAsync(buf, tmp.p, sizeof(unsigned long long) * count, cudaMemcpyDeviceToDevice, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->barrier();
+}
+
+void allgather_u64(rr_comm* cm, const unsigned long long* send, unsigned long long* recv, int64_t count,
+                   cudaStream_t st) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclAllGather(send, recv, count, ncclUint64, cm->nccl, st));
+    return;
+  }
+  rr_hub* h = cm->hub;
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->ptr[cm->rank] = send;
+  h->barrier();
+  for (int r = 0; r < h->n; ++r)
+    RR_CUDA(cudaMemcpyAsync(recv + r * count, h->ptr[r], sizeof(unsigned long long) * count,
+                            cudaMemcpyDeviceToDevice, st));
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->barrier();
+}
+
+void group_start(rr_comm* cm) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclGroupStart());
+    return;
+  }
+  cm->g_send.clear();
+  cm->g_recv.clear();
+}
+
+template <typename T>
+void p2p_send(rr_comm* cm, const T* buf, size_t n, int peer, cudaStream_t st) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclSend(buf, n, nccl_type<T>(), peer, cm->nccl, st));
+    return;
+  }
+  cm->g_send.emplace_back(peer, buf, n * sizeof(T));
+}
+
+template <typename T>
+void p2p_recv(rr_comm* cm, T* buf, size_t n, int peer, cudaStream_t st) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclRecv(buf, n, nccl_type<T>(), peer, cm->nccl, st));
+    return;
+  }
+  cm->g_recv.emplace_back(peer, buf, n * sizeof(T));
+}
+
+// the k-th receive from rank q matches q's k-th send to this rank
+void group_end(rr_comm* cm, cudaStream_t st) {
+  if (!cm->hub) {
+    RR_NCCL_CHECK(ncclGroupEnd());
+    return;
+  }
+  rr_hub* h = cm->hub;
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->sends[cm->rank] = cm->g_send;
+  h->barrier();
+  std::vector<int> used(h->n, 0);
+  for (const auto& rv : cm->g_recv) {
+    const int q = std::get<0>(rv);
+    int k = -1;
+    for (int seen = 0, j = 0; j < static_cast<int>(h->sends[q].size()); ++j)
+      if (std::get<0>(h->sends[q][j]) == cm->rank && seen++ == used[q]) {
+        k = j;
+        break;
+      }
+    if (k < 0) throw Error(RR_NCCL, "loopback: receive without a matching send");
+    ++used[q];
+    const auto& sd = h->sends[q][k];
+    if (std::get<2>(sd) != std::get<2>(rv)) throw Error(RR_NCCL, "loopback: send / receive sizes differ");
+    RR_CUDA(cudaMemcpyAsync(std::get<1>(rv), std::get<1>(sd), std::get<2>(rv), cudaMemcpyDeviceToDevice, st));
+  }
+  RR_CUDA(cudaStreamSynchronize(st));
+  h->barrier();
+}
+
 // rows of `w` elements: send `sn[q]` rows to rank q from consecutive blocks,
 // receive `rn[q]` rows from rank q into consecutive blocks (caller groups)
 template <typename T>
@@ -230,8 +371,8 @@ void a2a_rows(rr_comm* cm, const T* send, const std::vector<int64_t>& sn, T* rec
       if (sn[q])
         RR_CUDA(cudaMemcpyAsync(recv + ro * w, send + so * w, sizeof(T) * sn[q] * w, cudaMemcpyDeviceToDevice, st));
     } else {
-      if (sn[q]) RR_NCCL_CHECK(ncclSend(send + so * w, static_cast<size_t>(sn[q] * w), nccl_type<T>(), q, cm->nccl, st));
-      if (rn[q]) RR_NCCL_CHECK(ncclRecv(recv + ro * w, static_cast<size_t>(rn[q] * w), nccl_type<T>(), q, cm->nccl, st));
+      if (sn[q]) p2p_send<T>(cm, send + so * w, static_cast<size_t>(sn[q] * w), q, st);
+      if (rn[q]) p2p_recv<T>(cm, recv + ro * w, static_cast<size_t>(rn[q] * w), q, st);
     }
     so += sn[q];
     ro += rn[q];
@@ -298,7 +439,7 @@ std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result*
   RR_CUDA(cudaMemsetAsync(counts.p, 0, counts.bytes(), st));
   if (n) order_hist_kernel<<<grid(n), 256, 0, st>>>(tr->c_off.p, c0, n, max_order, counts.p);
   RR_LAUNCH_CHECK();
-  RR_NCCL_CHECK(ncclAllReduce(counts.p, counts.p, max_order + 1, ncclUint64, ncclSum, cm->nccl, st));
+  allreduce_u64(cm, counts.p, max_order + 1, false, st);
   std::vector<unsigned long long> h_counts(max_order + 1);
   RR_CUDA(cudaMemcpyAsync(h_counts.data(), counts.p, counts.bytes(), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
@@ -330,7 +471,7 @@ std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result*
   // counts of every rank to every rank
   DevBuf<unsigned long long> all_sc;
   all_sc.alloc(2 * world * world, st);
-  RR_NCCL_CHECK(ncclAllGather(sc.p, all_sc.p, 2 * world, ncclUint64, cm->nccl, st));
+  allgather_u64(cm, sc.p, all_sc.p, 2 * world, st);
   std::vector<unsigned long long> h_all(2 * world * world);
   RR_CUDA(cudaMemcpyAsync(h_all.data(), all_sc.p, all_sc.bytes(), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
@@ -375,7 +516,7 @@ std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result*
   r_path.alloc(std::max<int64_t>(m, 1), st);
   r_mult.alloc(kBands * std::max<int64_t>(m, 1), st);
   r_hist.alloc(std::max<int64_t>(mh, 1), st);
-  RR_NCCL_CHECK(ncclGroupStart());
+  group_start(cm);
   a2a_rows<int32_t>(cm, s_ray.p, sn, r_ray.p, rn, 1, st);
   a2a_rows<int32_t>(cm, s_ord.p, sn, r_ord.p, rn, 1, st);
   a2a_rows<double>(cm, s_point.p, sn, r_point.p, rn, 3, st);
@@ -383,7 +524,7 @@ std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result*
   a2a_rows<double>(cm, s_path.p, sn, r_path.p, rn, 1, st);
   a2a_rows<double>(cm, s_mult.p, sn, r_mult.p, rn, kBands, st);
   a2a_rows<int32_t>(cm, s_hist.p, sh, r_hist.p, rh, 1, st);
-  RR_NCCL_CHECK(ncclGroupEnd());
+  group_end(cm, st);
   // 4. history offsets of the received records, then the reference order
   DevBuf<int64_t> r_len, r_off;
   r_len.alloc(m + 1, st);
@@ -414,7 +555,7 @@ rr_images* gather_images(rr_comm* cm, rr_images* local) {
   const unsigned long long h_mine[2] = {static_cast<unsigned long long>(n),
                                         static_cast<unsigned long long>(local->total_path)};
   RR_CUDA(cudaMemcpyAsync(mine.p, h_mine, sizeof h_mine, cudaMemcpyHostToDevice, st));
-  RR_NCCL_CHECK(ncclAllGather(mine.p, all.p, 2, ncclUint64, cm->nccl, st));
+  allgather_u64(cm, mine.p, all.p, 2, st);
   std::vector<unsigned long long> h_all(2 * world);
   RR_CUDA(cudaMemcpyAsync(h_all.data(), all.p, all.bytes(), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
@@ -442,7 +583,7 @@ rr_images* gather_images(rr_comm* cm, rr_images* local) {
   has_proj.alloc(m1, st);
   len.alloc(m1, st);
   path.alloc(std::max<int64_t>(mh, 1), st);
-  RR_NCCL_CHECK(ncclGroupStart());
+  group_start(cm);
   a2a_rows<double>(cm, local->pos.p, sn, pos.p, rn, 3, st);
   a2a_rows<double>(cm, local->dist.p, sn, dist.p, rn, 1, st);
   a2a_rows<double>(cm, local->energy.p, sn, energy.p, rn, kBands, st);
@@ -453,7 +594,7 @@ rr_images* gather_images(rr_comm* cm, rr_images* local) {
   a2a_rows<int32_t>(cm, local->has_proj.p, sn, has_proj.p, rn, 1, st);
   a2a_rows<int64_t>(cm, plen.p, sn, len.p, rn, 1, st);
   a2a_rows<int32_t>(cm, local->path.p, sh, path.p, rh, 1, st);
-  RR_NCCL_CHECK(ncclGroupEnd());
+  group_end(cm, st);
   if (cm->rank != 0) {
     RR_CUDA(cudaStreamSynchronize(st));
     return nullptr;
@@ -577,10 +718,8 @@ rr_sharded* pipeline_sharded(rr_scene* s, rr_comm* cm, const rr_source* src, con
       dn.alloc(1, st);
       const unsigned long long hn = static_cast<unsigned long long>(local->n);
       RR_CUDA(cudaMemcpyAsync(dn.p, &hn, sizeof hn, cudaMemcpyHostToDevice, st));
-      RR_NCCL_CHECK(ncclGroupStart());
-      RR_NCCL_CHECK(ncclAllReduce(mx.p, mx.p, 1, ncclUint64, ncclMax, cm->nccl, st));
-      RR_NCCL_CHECK(ncclAllReduce(dn.p, dn.p, 1, ncclUint64, ncclSum, cm->nccl, st));
-      RR_NCCL_CHECK(ncclGroupEnd());
+      allreduce_u64(cm, mx.p, 1, true, st);
+      allreduce_u64(cm, dn.p, 1, false, st);
       unsigned long long h = 0;
       RR_CUDA(cudaMemcpyAsync(&h, dn.p, sizeof h, cudaMemcpyDeviceToHost, st));
       RR_CUDA(cudaStreamSynchronize(st));
@@ -588,7 +727,7 @@ rr_sharded* pipeline_sharded(rr_scene* s, rr_comm* cm, const rr_source* src, con
     }
     const int64_t n_scale = std::max<int64_t>(n_all, 1);
     ir_bin_fixed(ctx, local->n, local->dist.p, local->energy.p, cfg->speed_of_sound, fs, lh, mx.p, n_scale, acc.p);
-    if (cm) RR_NCCL_CHECK(ncclAllReduce(acc.p, acc.p, kBands * lh, ncclUint64, ncclSum, cm->nccl, st));
+    if (cm) allreduce_u64(cm, acc.p, kBands * lh, false, st);
     DevBuf<double> hist;
     hist.alloc(kBands * lh, st);
     ir_unfix(ctx, acc.p, kBands * lh, n_scale, mx.p, hist.p);
@@ -654,6 +793,31 @@ rr_status rr_comm_init(rr_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t r
   });
 }
 
+rr_status rr_hub_create(int32_t nranks, rr_hub** out) {
+  return rr::abi_guard_nccl([&] {
+    if (!out || nranks < 1) rr::invalid("nranks must be >= 1");
+    *out = new rr_hub(nranks);
+  });
+}
+
+rr_status rr_hub_destroy(rr_hub* hub) {
+  return rr::abi_guard_nccl([&] { delete hub; });
+}
+
+rr_status rr_comm_init_loopback(rr_ctx* ctx, rr_hub* hub, int32_t rank, rr_comm** out) {
+  return rr::abi_guard_nccl([&] {
+    if (!ctx || !hub || !out) rr::invalid("ctx, hub and out must not be null");
+    if (rank < 0 || rank >= hub->n) rr::invalid("rank out of range");
+    auto c = std::make_unique<rr_comm>();
+    c->ctx = ctx;
+    c->hub = hub;
+    c->rank = rank;
+    c->nranks = hub->n;
+    ctx->refs++;
+    *out = c.release();
+  });
+}
+
 rr_status rr_comm_info(rr_comm* comm, int32_t* rank, int32_t* nranks) {
   return rr::abi_guard_nccl([&] {
     if (!comm) rr::invalid("comm must not be null");
@@ -668,7 +832,7 @@ rr_status rr_comm_destroy(rr_comm* comm) {
     rr_ctx* ctx = comm->ctx;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    const ncclResult_t r = ncclCommDestroy(comm->nccl);
+    const ncclResult_t r = comm->nccl ? ncclCommDestroy(comm->nccl) : ncclSuccess;
     delete comm;
     rr_ctx_destroy(ctx);  // drops the reference taken by rr_comm_init
     if (r != ncclSuccess) throw rr::Error(RR_NCCL, std::string("ncclCommDestroy: ") + ncclGetErrorString(r));

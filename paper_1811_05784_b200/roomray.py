@@ -722,9 +722,35 @@ class Comm:
         check(self.lib.rr_comm_init(ctx.h, buf, int(nranks), int(rank), C.byref(h)))
         self.h, self.rank, self.nranks = h, rank, nranks
 
+    @classmethod
+    def loopback(cls, ctx: Context, hub: "Hub", rank: int) -> "Comm":
+        """Rank `rank` of an in-process loopback hub (testing the multi-rank
+        exchange on one GPU: one thread and one Context per rank)."""
+        c = cls.__new__(cls)
+        c.ctx, c.lib = ctx, ctx.lib
+        h = C.c_void_p()
+        check(c.lib.rr_comm_init_loopback(ctx.h, hub.h, int(rank), C.byref(h)))
+        c.h, c.rank, c.nranks, c.hub = h, rank, hub.nranks, hub
+        return c
+
     def __del__(self):
         if getattr(self, "h", None) and not _SHUTDOWN:
             self.lib.rr_comm_destroy(self.h)
+            self.h = None
+
+
+class Hub:
+    """rr_hub: the rendezvous of in-process loopback ranks (see Comm.loopback)."""
+
+    def __init__(self, nranks: int):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.rr_hub_create(int(nranks), C.byref(h)))
+        self.h, self.nranks = h, nranks
+
+    def __del__(self):
+        if getattr(self, "h", None) and not _SHUTDOWN:
+            self.lib.rr_hub_destroy(self.h)
             self.h = None
 
 

@@ -1,15 +1,18 @@
 """rr_pipeline_sharded: the multi-GPU pipeline behind the C ABI
 (run_trace_pipeline's trace -> image sources -> IRs, pipeline.cpp:163-175).
 
-Only one GPU is available to the tests, so the exchange path runs on a
-one-rank NCCL communicator: order-class histogram all-reduce, LPT ownership,
-destination sort, packing and the grouped send/recv all-to-all (self copies
-on one rank), capture import in the reference order, the global fixed-point
-scale of the pulse histograms (max / sum all-reduce), the exact integer
-all-reduce, and the image gather to rank 0.  Its results must equal the
-plain device pipeline (comm=None) and the step-by-step API bit for bit, and
-the oracle's images / impulse responses (BASELINE tolerance for the IR band
-energies, 1e-4 relative).
+Only one GPU is available to the tests, so the exchange runs (1) on a
+one-rank NCCL communicator -- the NCCL calls themselves -- and (2) on 2-4
+in-process loopback ranks (rr_hub: one thread, context and replicated scene
+per rank on the same GPU; the collectives rendezvous on the hub and copy on
+the device), which exercises the multi-rank logic proper: block-cyclic
+shards, the summed order histogram, LPT ownership, the cross-rank
+all-to-all of capture records, capture import in the reference order, the
+global fixed-point scale of the pulse histograms and their exact integer
+sum, and the image gather to rank 0.  Results must equal the plain device
+pipeline (comm=None) and the step-by-step API bit for bit, and the oracle's
+images / impulse responses (BASELINE tolerance for the IR band energies,
+1e-4 relative).
 """
 from __future__ import annotations
 
@@ -98,3 +101,59 @@ def test_pipeline_against_oracle(ctx, comm1, port):
 def test_comm_errors(ctx):
     with pytest.raises(ValueError):
         rr.Comm(ctx, rr.Comm.unique_id(), 2, 5)  # rank out of range
+
+
+# ---------------------------------------------------------------- several ranks on one GPU
+def _run_ranks(s, world, merge, block):
+    """world loopback ranks (one thread + one context + one replicated scene
+    each) through rr_pipeline_sharded; returns every rank's result."""
+    import threading
+
+    from paper_1811_05784_b200 import Context
+    hub = rr.Hub(world)
+    ctxs = [Context(0) for _ in range(world)]
+    trees = [AccelTree(TriangleMesh(s.vertices, s.faces, s.absorption), c) for c in ctxs]
+    comms = [rr.Comm.loopback(c, hub, r) for r, c in enumerate(ctxs)]
+    recvs = [Receiver(c, r) for c, r in s.receivers]
+    L = int(round(s.ir_seconds * s.sample_rate))
+    out, err = [None] * world, []
+
+    def rank(r):
+        try:
+            out[r] = rr.pipeline_sharded(trees[r], SourceConfig(s.source, s.ray_count), recvs,
+                                         TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range),
+                                         comm=comms[r], options=rr.ClusterOptions(1e-6, merge),
+                                         sample_rate=s.sample_rate, length=L, block=block)
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not err, err
+    return out
+
+
+@pytest.mark.parametrize("cfg,world,merge,block", [("c1", 2, True, 512), ("c1", 3, True, 4096),
+                                                   ("c2", 2, False, 4096), ("c3", 4, True, 4096)])
+def test_multi_rank_exchange_equals_one_gpu(ctx, cfg, world, merge, block):
+    """The multi-rank path proper -- block-cyclic shards, summed order
+    histograms, LPT ownership over several ranks, cross-rank all-to-all of the
+    capture records, the global fixed-point IR scale and integer sum, the
+    image gather -- on loopback ranks, against one GPU, bit for bit."""
+    s = scenes.CONFIGS[cfg]()
+    _, one = _run(ctx, s, None, merge)
+    res = _run_ranks(s, world, merge, block)
+    assert sum(r.n_rays for r in res) == s.ray_count
+    assert sum(r.ray_bounces for r in res) == one.ray_bounces
+    assert sum(r.local_images for r in res) == one.local_images
+    assert sum(r.local_images > 0 for r in res) > 1  # the image work really was split
+    for rcv in range(len(s.receivers)):
+        _images_equal(res[0].images[rcv], one.images[rcv])
+        for r in range(world):
+            np.testing.assert_array_equal(res[r].band_ir[rcv], one.band_ir[rcv])
+            np.testing.assert_array_equal(res[r].broadband[rcv], one.broadband[rcv])
+            if r:
+                assert len(res[r].images[rcv].distance) == 0
