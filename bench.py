@@ -370,6 +370,13 @@ def run_ours(args):
         del res
         lib.rr_scene_destroy(h)
         sc.h = None
+        if os.environ.get("RR_E2E_DEBUG"):
+            from cuda.bindings import runtime as crt
+            _, pool = crt.cudaDeviceGetDefaultMemPool(local)
+            _, rsv = crt.cudaMemPoolGetAttribute(pool, crt.cudaMemPoolAttr.cudaMemPoolAttrReservedMemCurrent)
+            _, used = crt.cudaMemPoolGetAttribute(pool, crt.cudaMemPoolAttr.cudaMemPoolAttrUsedMemHigh)
+            print(f"e2e dbg step {it}: {e2e_ms[-1] if it >= args.warmup else 0:.1f} ms, pool reserved "
+                  f"{int(rsv) / 2**30:.2f} GiB, used high {int(used) / 2**30:.2f} GiB", file=sys.stderr)
     del comm
     e2e_local = sum(e2e_ms)
     t = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")

@@ -1045,9 +1045,11 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     sids.alloc(ni, st);
     cell_key_kernel<<<grid(ni), 256, 0, st>>>(T, ni, cs, keys.p, ids.p);
     RR_LAUNCH_CHECK();
+    tm.mark("merge: cell keys");
     cub_call([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, keys.p, skeys.p, ids.p, sids.p, ni, 0, 32, st);
     }, st);
+    tm.mark("merge: cell sort");
     unsigned long long tsize = 1024;
     while (tsize < 2ull * static_cast<unsigned long long>(ni)) tsize <<= 1;
     DevBuf<unsigned long long> tkey;
@@ -1055,7 +1057,9 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     tkey.alloc(tsize, st);
     tstart.alloc(tsize, st);
     RR_CUDA(cudaMemsetAsync(tkey.p, 0xff, tkey.bytes(), st));
+    tm.mark("merge: table alloc");
     ht_insert_kernel<<<grid(ni), 256, 0, st>>>(skeys.p, ni, tkey.p, tstart.p, tsize - 1);
+    tm.mark("merge: table insert");
     DevBuf<double> cpos, cmult;
     DevBuf<int32_t> corder, owner, progress;
     cpos.alloc(3 * ni, st);

@@ -6,6 +6,7 @@
 #include <atomic>
 
 #include <cstdint>
+#include <ctime>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -93,13 +94,20 @@ struct StageTimer {
   cudaStream_t s;
   bool on;
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> host_ms;  // host wall clock at each mark
   explicit StageTimer(cudaStream_t st) : s(st), on(std::getenv("RR_TIMING") != nullptr) { mark("start"); }
+  static double now_ms() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return 1e3 * static_cast<double>(ts.tv_sec) + 1e-6 * static_cast<double>(ts.tv_nsec);
+  }
   void mark(const char* name) {
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
     ev.emplace_back(name, e);
+    host_ms.push_back(now_ms());
   }
   ~StageTimer() {
     if (!on) return;
@@ -107,7 +115,8 @@ struct StageTimer {
     for (size_t i = 1; i < ev.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-      std::fprintf(stderr, "[rr timing] %-24s %9.3f ms\n", ev[i].first, ms);
+      std::fprintf(stderr, "[rr timing] %-24s %9.3f ms (host enqueue %8.3f ms)\n", ev[i].first, ms,
+                   host_ms[i] - host_ms[i - 1]);
     }
     for (auto& p : ev) cudaEventDestroy(p.second);
   }
