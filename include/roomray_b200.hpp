@@ -24,6 +24,7 @@
 #define ROOMRAY_B200_HPP
 
 #include <algorithm>
+#include <thread>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -313,6 +314,27 @@ struct TraceHandle {
 }  // namespace detail
 
 namespace detail {
+// f(i) for i in [0, n) on the host's hardware threads (the conversions of
+// device results into the reference's per-record std::vector types are
+// allocation bound); serial below 2^14 records
+template <typename F>
+inline void parallel_for(std::size_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = n < (std::size_t(1) << 14) ? 1 : std::min<std::size_t>(hw, 32);
+  if (nt <= 1) {
+    for (std::size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::size_t chunk = (n + nt - 1) / nt;
+  for (std::size_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const std::size_t a = t * chunk, b = std::min(n, a + chunk);
+      for (std::size_t i = a; i < b; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
 // host copy of a device trace (TraceResult, tracer.hpp:22-29)
 inline TraceResult trace_result_from(rr_trace_result* h) {
   rr_trace_stats st{};
@@ -332,7 +354,7 @@ inline TraceResult trace_result_from(rr_trace_result* h) {
   r.ray_bounces = st.ray_bounces;
   r.kernel_ms = rr_trace_kernel_ms(h);
   r.captures.resize(n);
-  for (std::size_t i = 0; i < n; ++i) {
+  parallel_for(n, [&](std::size_t i) {
     Capture& c = r.captures[i];
     c.ray_index = ray[i];
     c.point = {point[3 * i], point[3 * i + 1], point[3 * i + 2]};
@@ -340,7 +362,7 @@ inline TraceResult trace_result_from(rr_trace_result* h) {
     c.path_length = path[i];
     for (int b = 0; b < kNumBands; ++b) c.band_multiplier[b] = mult[kNumBands * i + b];
     c.face_history.assign(hist.begin() + off[i], hist.begin() + off[i + 1]);
-  }
+  });
   return r;
 }
 
@@ -537,7 +559,7 @@ inline std::vector<ImageSource> images_from(rr_images* im) {
   check(rr_images_get(im, pos.data(), dist.data(), en.data(), mu.data(), cnt.data(), order.data(), hp.data(),
                       proj.data(), poff.data(), pth.data()));
   std::vector<ImageSource> out(m);
-  for (std::size_t i = 0; i < m; ++i) {
+  parallel_for(m, [&](std::size_t i) {
     ImageSource& s = out[i];
     s.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
     s.distance = dist[i];
@@ -549,7 +571,7 @@ inline std::vector<ImageSource> images_from(rr_images* im) {
     s.order = order[i];
     s.face_path.assign(pth.begin() + poff[i], pth.begin() + poff[i + 1]);
     if (hp[i]) s.projection = Vec3{proj[3 * i], proj[3 * i + 1], proj[3 * i + 2]};
-  }
+  });
   return out;
 }
 }  // namespace detail
@@ -722,8 +744,11 @@ inline PulseTrains trains_from(rr_images* im, double speed_of_sound) {
   for (int b = 0; b < kNumBands; ++b) {
     trains[b].band = b;
     trains[b].events.resize(static_cast<std::size_t>(n));
-    for (int64_t i = 0; i < n; ++i) trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
   }
+  parallel_for(static_cast<std::size_t>(kNumBands) * n, [&](std::size_t j) {
+    const std::size_t b = j / n, i = j - b * n;
+    trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
+  });
   return trains;
 }
 
