@@ -744,11 +744,8 @@ inline PulseTrains trains_from(rr_images* im, double speed_of_sound) {
   for (int b = 0; b < kNumBands; ++b) {
     trains[b].band = b;
     trains[b].events.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
   }
-  parallel_for(static_cast<std::size_t>(kNumBands) * n, [&](std::size_t j) {
-    const std::size_t b = j / n, i = j - b * n;
-    trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
-  });
   return trains;
 }
 
