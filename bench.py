@@ -83,20 +83,28 @@ def ncu_trace_counters(config):
     head = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     names, units = rows[head], rows[head + 1]
     want = ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "gpu__time_duration.sum")
+    opt = ("smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "smsp__thread_inst_executed_per_inst_executed.ratio")
     col = {w: names.index(w) for w in want}
+    col.update({w: names.index(w) for w in opt if w in names})
     kcol = names.index("Kernel Name")
-    acc = {w: [] for w in want}
+    acc = {w: [] for w in col}
     for r in rows[head + 2:]:
         if len(r) != len(names) or "trace_kernel" not in r[kcol]:
             continue
-        for w in want:
-            acc[w].append(float(r[col[w]].replace(",", "")) * UNIT_SCALE.get(units[col[w]].lower(), 1.0))
+        for w in col:
+            scale = UNIT_SCALE.get(units[col[w]].lower(), 1.0) if w in want else 1.0
+            acc[w].append(float(r[col[w]].replace(",", "")) * scale)
     if not acc[want[0]]:
         return None
     mean = {w: sum(v) / len(v) for w, v in acc.items()}
-    return {"dram_bytes": mean[want[0]] + mean[want[1]], "dram_read": mean[want[0]], "dram_write": mean[want[1]],
-            "l2_bytes": mean[want[2]], "ncu_ms": mean[want[3]] * 1e3, "launches": len(acc[want[0]]),
-            "source": os.path.relpath(path, ROOT)}
+    out = {"dram_bytes": mean[want[0]] + mean[want[1]], "dram_read": mean[want[0]], "dram_write": mean[want[1]],
+           "l2_bytes": mean[want[2]], "ncu_ms": mean[want[3]] * 1e3, "launches": len(acc[want[0]]),
+           "source": os.path.relpath(path, ROOT)}
+    if opt[0] in mean:
+        out.update({"warp_inst": mean[opt[0]], "issue_active_pct": mean.get(opt[1]),
+                    "threads_per_inst": mean.get(opt[2])})
+    return out
 
 
 # ---------------------------------------------------------------- clocks
@@ -415,6 +423,14 @@ def run_ours(args):
                      "l2_bytes_per_launch": round(ncu["l2_bytes"]),
                      "l2_achieved": round(ncu["l2_bytes"] / (kern_ms_launch / 1e3) / 1e9, 1),
                      "ncu_ms_per_launch": round(ncu["ncu_ms"], 3)})
+        if ncu.get("issue_active_pct") is not None:
+            # what does bound the kernel: the SM issue slots (ncu, same capture)
+            busy = ncu["issue_active_pct"] >= 65.0
+            roof["limiter"] = {"what": "SM instruction issue (not DRAM bandwidth)" if busy else
+                               "latency of dependent node fetches (issue slots idle, not DRAM bandwidth)",
+                               "issue_active_frac": round(ncu["issue_active_pct"] / 100.0, 4),
+                               "warp_instructions_per_launch": round(ncu["warp_inst"]),
+                               "threads_per_instruction": round(ncu["threads_per_inst"], 2)}
     else:
         roof.update({"achieved": None, "frac": None, "traffic": None,
                      "basis": "no committed ncu export for this config / world size"})
