@@ -649,15 +649,14 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // entries in shared memory 658; MINB 7 666; DONET 16 / UNR 4 at MINB 6
   // 716; UNR 8 810; no batching (the per-ray loop) 1074.  After: 587
   // (RR_W8V=1: MINB 9 592; 10: 620; 12: 692)
-  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8> : w8v == 2 ? trace_kernel_w8<8, 6, 1, kStack8, false, 12>
-          : w8v == 3 ? trace_kernel_w8<8, 8, 1, kStack8, false, 8>
-                     : trace_kernel_w8<8, 8, 1, kStack8, false, 12>;
+  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8, false, 12, 2, 2>
+                     : trace_kernel_w8<8, 6, 1, kStack8, false, 12, 4, 2>;
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
   if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8   ? trace_kernel_w8<8, 8, 1, kStack8, true, 12>
+    dfk = wide8   ? trace_kernel_w8<8, 6, 1, kStack8, true, 12, 4, 2>
           : wide4 ? trace_kernel<3, 8, false, 0, 1, true>
                   : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree

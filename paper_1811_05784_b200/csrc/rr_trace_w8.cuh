@@ -16,6 +16,9 @@
 //    the warp-aggregated capture append, reflect, write the face history,
 //    terminate, take new rays from the global counter and start their next
 //    query.
+// Leaves are tested (one batch, all lanes holding one) once a quarter of
+// the searching lanes are stuck behind their stashed leaf or half hold one
+// (STUCKD 4, HOLDD 2: C5 562 -> 549 ms against a half / a half).
 // Without the batching a warp's bounce lasts as long as its slowest lane's
 // query: on C5 (17 node visits per ray-bounce on average) only ~7 of 32
 // lanes were active per node visit.
@@ -23,7 +26,7 @@
 
 namespace rr {
 
-template <int MINB, int DONET, int UNR, int STK, bool CNT = false, int SMS = 0>
+template <int MINB, int DONET, int UNR, int STK, bool CNT = false, int SMS = 0, int STUCKD = 2, int HOLDD = 2>
 __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p) {
   // the SMS oldest stack entries of each lane in shared memory (column tid:
   // lane i always in bank i, conflict-free), deeper ones in local memory
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           const unsigned mv = __ballot_sync(act, must);
           const unsigned cv = __ballot_sync(act, can);
           const int na = __popc(act);
-          if (2 * __popc(mv) >= na || cv == 0 || 2 * __popc(hv) >= na) {
+          if (STUCKD * __popc(mv) >= na || cv == 0 || HOLDD * __popc(hv) >= na) {
             if (leaf != 0) {
               if (CNT) st_cnt[1] += leaf_faces(leaf);
               RR_DCHECK(leaf_face(leaf) + leaf_faces(leaf) <= p.nf);
