@@ -6,9 +6,11 @@
 // threads (tracer.cpp:82-105).  Here each rank holds the replicated mesh and
 // tree and traces a block-cyclic shard of the global Fibonacci lattice
 // (4 096-ray blocks) with no communication.  The one exchange step:
-//  1. order classes: the per-order capture histogram is summed over the
-//     ranks (ncclAllReduce) and whole classes (face-path lengths) are
-//     assigned to ranks by a deterministic longest-processing-time rule.
+//  1. order classes: each receiver's per-order capture histogram is summed
+//     over the ranks (ncclAllReduce) and the (receiver, order class) units
+//     are assigned to ranks jointly by a deterministic longest-processing-
+//     time rule (C3: 5 receivers with ~4 populated orders each balance to
+//     1.00 at 8 ranks, where per-receiver ownership left 2.8-3.3x).
 //     Grouping (exact face path), group splitting and the coplanar merge
 //     only ever combine captures / images of one order
 //     (image_sources.cpp:87-90, 111-116), so a class is a closed unit and
@@ -414,14 +416,10 @@ struct Timer {
 
 // the exchange of receiver r's captures; returns the imported trace on
 // this rank (its order classes, reference order)
-std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result* tr, int32_t r,
-                                                   const rr_receiver& receiver, int32_t max_order) {
-  rr_scene* s = tr->scene;
-  cudaStream_t st = s->ctx->stream;
-  const int world = cm->nranks;
+// receiver r's range [c0, c0 + n) of the (receiver, ray, order)-sorted captures
+void receiver_range(rr_trace_result* tr, int32_t r, int64_t* c0, int64_t* n) {
+  cudaStream_t st = tr->scene->ctx->stream;
   const int64_t nc_all = tr->stats.n_captures;
-  DevBuf<uint8_t> tmp;
-  // 0. receiver r's range of the (receiver, ray, order)-sorted captures
   int64_t range[2] = {0, 0};
   if (nc_all) {
     DevBuf<int64_t> dr;
@@ -432,21 +430,46 @@ std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result*
     RR_CUDA(cudaMemcpyAsync(range, dr.p, sizeof range, cudaMemcpyDeviceToHost, st));
     RR_CUDA(cudaStreamSynchronize(st));
   }
-  const int64_t c0 = range[0], n = range[1] - range[0];
-  // 1. order classes
+  *c0 = range[0];
+  *n = range[1] - range[0];
+}
+
+// ownership of every (receiver, order class) unit: per-receiver order
+// histograms summed over the ranks (one all-reduce), then the deterministic
+// LPT rule over all units jointly -- several receivers' classes spread over
+// the ranks even when each receiver has few populated orders (C3: 5
+// receivers, orders 0-3) -- owner[r * (max_order + 1) + o]
+std::vector<int32_t> assign_units(rr_comm* cm, rr_trace_result* tr, int32_t n_recv, int32_t max_order) {
+  cudaStream_t st = tr->scene->ctx->stream;
+  const int64_t per = max_order + 1;
   DevBuf<unsigned long long> counts;
-  counts.alloc(max_order + 1, st);
+  counts.alloc(n_recv * per, st);
   RR_CUDA(cudaMemsetAsync(counts.p, 0, counts.bytes(), st));
-  if (n) order_hist_kernel<<<grid(n), 256, 0, st>>>(tr->c_off.p, c0, n, max_order, counts.p);
-  RR_LAUNCH_CHECK();
-  allreduce_u64(cm, counts.p, max_order + 1, false, st);
-  std::vector<unsigned long long> h_counts(max_order + 1);
-  RR_CUDA(cudaMemcpyAsync(h_counts.data(), counts.p, counts.bytes(), cudaMemcpyDeviceToHost, st));
+  for (int32_t r = 0; r < n_recv; ++r) {
+    int64_t c0, n;
+    receiver_range(tr, r, &c0, &n);
+    if (n) order_hist_kernel<<<grid(n), 256, 0, st>>>(tr->c_off.p, c0, n, max_order, counts.p + r * per);
+    RR_LAUNCH_CHECK();
+  }
+  allreduce_u64(cm, counts.p, n_recv * per, false, st);
+  std::vector<unsigned long long> h(n_recv * per);
+  RR_CUDA(cudaMemcpyAsync(h.data(), counts.p, counts.bytes(), cudaMemcpyDeviceToHost, st));
   RR_CUDA(cudaStreamSynchronize(st));
-  const std::vector<int32_t> owner = assign_orders(h_counts, world);
+  return assign_orders(h, cm->nranks);
+}
+
+std::unique_ptr<rr_trace_result> exchange_captures(rr_comm* cm, rr_trace_result* tr, int32_t r,
+                                                   const rr_receiver& receiver, int32_t max_order,
+                                                   const int32_t* owner_row) {
+  rr_scene* s = tr->scene;
+  cudaStream_t st = s->ctx->stream;
+  const int world = cm->nranks;
+  DevBuf<uint8_t> tmp;
+  int64_t c0, n;
+  receiver_range(tr, r, &c0, &n);
   DevBuf<int32_t> d_owner;
-  d_owner.alloc(owner.size(), st);
-  RR_CUDA(cudaMemcpyAsync(d_owner.p, owner.data(), sizeof(int32_t) * owner.size(), cudaMemcpyHostToDevice, st));
+  d_owner.alloc(max_order + 1, st);
+  RR_CUDA(cudaMemcpyAsync(d_owner.p, owner_row, sizeof(int32_t) * (max_order + 1), cudaMemcpyHostToDevice, st));
   // 2. destination order (stable), counts, packing
   DevBuf<uint32_t> dest, dest_s;
   DevBuf<int32_t> idx, perm;
@@ -692,31 +715,38 @@ rr_sharded* pipeline_sharded(rr_scene* s, rr_comm* cm, const rr_source* src, con
   const int64_t lh = length + taps;
   out->band_ir.alloc(static_cast<size_t>(n_recv) * kBands * length, st);
   out->broadband.alloc(static_cast<size_t>(n_recv) * length, st);
+  // exchange every receiver's captures (owners of (receiver, order) units),
+  // then build every image list, then reduce / gather per receiver: the image
+  // work between the collectives is what the joint ownership balances
+  const int32_t max_order = std::max(cfg->max_iterations, 1);
+  std::vector<std::unique_ptr<rr_trace_result>> mine(n_recv);
+  if (cm) {
+    const std::vector<int32_t> owner = assign_units(cm, tr.get(), n_recv, max_order);
+    for (int32_t r = 0; r < n_recv; ++r)
+      mine[r] = exchange_captures(cm, tr.get(), r, recv[r], max_order, owner.data() + r * (max_order + 1));
+  }
+  tm.mark();
+  std::vector<std::unique_ptr<rr_images>> local(n_recv);
   for (int32_t r = 0; r < n_recv; ++r) {
-    std::unique_ptr<rr_trace_result> mine;
-    rr_trace_result* from = tr.get();
-    int32_t ridx = r;
-    if (cm) {
-      mine = exchange_captures(cm, tr.get(), r, recv[r], std::max(cfg->max_iterations, 1));
-      from = mine.get();
-      ridx = 0;
-    }
-    tm.mark();
-    std::unique_ptr<rr_images> local(build_image_sources(from, ridx, src->ray_count, air, opt));
-    out->local_images += local->n;
-    tm.mark();
+    local[r].reset(cm ? build_image_sources(mine[r].get(), 0, src->ray_count, air, opt)
+                      : build_image_sources(tr.get(), r, src->ray_count, air, opt));
+    out->local_images += local[r]->n;
+    mine[r].reset();
+  }
+  tm.mark();
+  for (int32_t r = 0; r < n_recv; ++r) {
     // impulse responses: global fixed-point scale, exact integer sum
     DevBuf<unsigned long long> mx, acc;
     mx.alloc(1, st);
     acc.alloc(kBands * lh, st);
     RR_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
     RR_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes(), st));
-    ir_max_amp(ctx, local->n, local->energy.p, mx.p);
-    int64_t n_all = local->n;
+    ir_max_amp(ctx, local[r]->n, local[r]->energy.p, mx.p);
+    int64_t n_all = local[r]->n;
     if (cm) {
       DevBuf<unsigned long long> dn;
       dn.alloc(1, st);
-      const unsigned long long hn = static_cast<unsigned long long>(local->n);
+      const unsigned long long hn = static_cast<unsigned long long>(local[r]->n);
       RR_CUDA(cudaMemcpyAsync(dn.p, &hn, sizeof hn, cudaMemcpyHostToDevice, st));
       allreduce_u64(cm, mx.p, 1, true, st);
       allreduce_u64(cm, dn.p, 1, false, st);
@@ -726,15 +756,18 @@ rr_sharded* pipeline_sharded(rr_scene* s, rr_comm* cm, const rr_source* src, con
       n_all = static_cast<int64_t>(h);
     }
     const int64_t n_scale = std::max<int64_t>(n_all, 1);
-    ir_bin_fixed(ctx, local->n, local->dist.p, local->energy.p, cfg->speed_of_sound, fs, lh, mx.p, n_scale, acc.p);
+    ir_bin_fixed(ctx, local[r]->n, local[r]->dist.p, local[r]->energy.p, cfg->speed_of_sound, fs, lh, mx.p, n_scale,
+                 acc.p);
     if (cm) allreduce_u64(cm, acc.p, kBands * lh, false, st);
     DevBuf<double> hist;
     hist.alloc(kBands * lh, st);
     ir_unfix(ctx, acc.p, kBands * lh, n_scale, mx.p, hist.p);
     ir_filter(ctx, hist.p, lh, fs, taps, length, out->band_ir.p + static_cast<size_t>(r) * kBands * length,
               out->broadband.p + static_cast<size_t>(r) * length);
-    tm.mark();
-    rr_images* merged = cm ? gather_images(cm, local.get()) : local.release();
+  }
+  tm.mark();
+  for (int32_t r = 0; r < n_recv; ++r) {
+    rr_images* merged = cm ? gather_images(cm, local[r].get()) : local[r].release();
     if (!merged) {  // ranks other than 0 hold an empty list
       merged = new rr_images();
       merged->scene = s;
@@ -742,15 +775,14 @@ rr_sharded* pipeline_sharded(rr_scene* s, rr_comm* cm, const rr_source* src, con
       RR_CUDA(cudaMemsetAsync(merged->path_off.p, 0, sizeof(int64_t), st));
     }
     out->images.push_back(merged);
-    tm.mark();
   }
+  tm.mark();
   RR_CUDA(cudaStreamSynchronize(st));
-  // stage times summed over receivers: trace, exchange, images, ir, gather
-  for (size_t i = 1; i < tm.ev.size(); ++i) {
+  // stage times: trace, exchange, images, ir, gather (all receivers)
+  for (size_t i = 1; i < tm.ev.size() && i <= 5; ++i) {
     float ms = 0.f;
     RR_CUDA(cudaEventElapsedTime(&ms, tm.ev[i - 1], tm.ev[i]));
-    const int stage = i == 1 ? 0 : static_cast<int>(1 + (i - 2) % 4);
-    out->stage_ms[stage] += ms;
+    out->stage_ms[i - 1] = ms;
   }
   return out.release();
 }

@@ -22,6 +22,18 @@ def main():
     c = rr.trace_device(tree, SourceConfig(s.source, s.ray_count), [Receiver(*r) for r in s.receivers],
                         TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range)).captures()
     order = np.diff(c.hist_off)
+    units = []  # (count, receiver, order) over all receivers: the joint ownership of rr_shard.cu
+    for r in range(len(s.receivers)):
+        cnt = np.bincount(order[c.recv == r], minlength=s.max_iterations + 1)
+        units += [(int(cnt[o]), r, o) for o in range(len(cnt))]
+    line = []
+    for world in (2, 4, 8):
+        load = np.zeros(world)
+        for n, r, o in sorted(units, key=lambda u: (-u[0], u[1], u[2])):
+            q = int(np.argmin(load))
+            load[q] += n
+        line.append(f"w{world}: max/mean {load.max() / max(load.mean(), 1):.2f}")
+    print(f"{name} all {len(s.receivers)} receivers jointly ((receiver, order) units): " + ", ".join(line))
     for r in range(len(s.receivers)):
         counts = np.bincount(order[c.recv == r], minlength=s.max_iterations + 1)
         line = []
