@@ -33,3 +33,20 @@ def test_world_size_mismatch_refused():
     p = subprocess.run([sys.executable, BENCH, "--gpus", "4", "--dry-run"], capture_output=True, text=True,
                        timeout=300, env=env)
     assert p.returncode != 0 and "WORLD_SIZE" in p.stderr
+
+
+def test_roofline_counters_from_committed_ncu_exports():
+    """bench.py's roofline reads the committed raw ncu exports of the trace
+    kernel (profiles/ncu_trace_<cfg>.csv): DRAM read + write bytes, L2 bytes,
+    duration, and the issue-slot counters, per launch."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for cfg in ("c5", "c3", "c2"):
+        c = bench.ncu_trace_counters(cfg)
+        assert c is not None and c["launches"] == 1, cfg
+        assert c["dram_bytes"] == c["dram_read"] + c["dram_write"] > 0
+        assert c["l2_bytes"] > c["dram_bytes"]
+        assert 0.1 < c["ncu_ms"] < 5000.0
+        assert 0.0 < c["issue_active_pct"] <= 100.0 and 1.0 <= c["threads_per_inst"] <= 32.0
+    c5 = bench.ncu_trace_counters("c5")
+    assert 300 < c5["dram_bytes"] / 799_998_849 < 2000  # bytes per C5 ray*bounce
