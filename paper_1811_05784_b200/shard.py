@@ -1,4 +1,10 @@
-"""Multi-GPU sharding of the trace and the exchange step.
+"""Multi-GPU sharding of the trace and the exchange step,
+over torch.distributed: the Python mirror of the library's rr_pipeline_sharded
+(csrc/rr_shard.cu), kept for the world-size-2 gloo tests on CPU
+(tests/test_shard_gloo.py, the oracle as per-rank compute).  The product
+path is rr_pipeline_sharded; this mirror assigns order classes per receiver
+(the library assigns (receiver, order) units jointly) and sums fp64 pulse
+histograms (the library sums 64-bit fixed-point ones, bit-exactly).
 
 Rays shard (the reference already chunks them, tracer.cpp:82-105): every
 rank holds the replicated mesh + tree and traces a block-cyclic shard of
