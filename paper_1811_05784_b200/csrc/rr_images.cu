@@ -919,7 +919,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     prefix_run_flag_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, idx_s.p, dirty.p);
     prefix_run_sort_kernel<<<grid(n), 256, 0, st>>>(pk_s.p, n, pv, dirty.p, idx_s.p);
     RR_LAUNCH_CHECK();
-    if (tm.on) {  // dirty-run statistics (development)
+    if (tm.stats) {  // dirty-run statistics (development)
       std::vector<unsigned long long> hk(n);
       std::vector<int32_t> hd(n);
       RR_CUDA(cudaMemcpyAsync(hk.data(), pk_s.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
@@ -992,7 +992,7 @@ rr_images* build_image_sources(rr_trace_result* tr, int32_t recv, int64_t total_
     ctx->launches += 1;
   }
   tm.mark("groups: count");
-  if (tm.on) {  // group statistics (development)
+  if (tm.stats) {  // group statistics (development)
     std::vector<int64_t> gs(ng + 1);
     std::vector<int32_t> sp(ng);
     RR_CUDA(cudaMemcpyAsync(gs.data(), gstart.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToHost, st));

@@ -92,10 +92,13 @@ struct DevBuf {
 // Stage timing for development (RR_TIMING=1 prints CUDA-event intervals).
 struct StageTimer {
   cudaStream_t s;
-  bool on;
+  bool on, stats;  // RR_TIMING set: stage events; RR_TIMING=2: also host-side statistics (slow)
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
   std::vector<double> host_ms;  // host wall clock at each mark
-  explicit StageTimer(cudaStream_t st) : s(st), on(std::getenv("RR_TIMING") != nullptr) { mark("start"); }
+  explicit StageTimer(cudaStream_t st)
+      : s(st), on(std::getenv("RR_TIMING") != nullptr), stats(on && std::getenv("RR_TIMING")[0] == '2') {
+    mark("start");
+  }
   static double now_ms() {
     timespec ts;
     clock_gettime(CLOCK_MONOTONIC, &ts);

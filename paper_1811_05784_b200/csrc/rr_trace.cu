@@ -483,6 +483,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   if (cfg->max_iterations > (1 << 20) - 1) invalid("max_iterations must be < 2^20");
   if (src->ray_count >= (int64_t(1) << 36)) invalid("ray_count must be < 2^36");
   cudaStream_t st = s->ctx->stream;
+  StageTimer tm(st);
   auto res = std::make_unique<rr_trace_result>();
   res->scene = s;
   TraceParams& p = res->params;
@@ -713,6 +714,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     s->ctx->launches += 5;
     p.order = order.p;
   }
+  tm.mark("trace: setup");
   cudaEvent_t e0, e1;
   RR_CUDA(cudaEventCreate(&e0));
   RR_CUDA(cudaEventCreate(&e1));
@@ -732,6 +734,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     if (static_cast<int64_t>(hc[0]) <= capacity) break;
     capacity = static_cast<int64_t>(hc[0]);  // exact re-run with the measured size
   }
+  tm.mark("trace: kernel");
   RR_CUDA(cudaEventElapsedTime(&res->kernel_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -815,6 +818,7 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   } else {
     RR_CUDA(cudaMemsetAsync(res->c_off.p, 0, sizeof(int64_t), st));
   }
+  tm.mark("trace: captures");
   RR_CUDA(cudaStreamSynchronize(st));
   return res.release();
 }
