@@ -57,6 +57,21 @@ struct Error : std::runtime_error {
 #endif
 
 // Device buffer, stream-ordered allocation on the owning context's stream.
+// RR_ALLOC_TRACE=1 (development): report stream-ordered allocation calls
+// that block the host for more than 2 ms
+inline bool alloc_trace() {
+  static const bool on = std::getenv("RR_ALLOC_TRACE") != nullptr;
+  return on;
+}
+inline double wall_ms() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return 1e3 * static_cast<double>(ts.tv_sec) + 1e-6 * static_cast<double>(ts.tv_nsec);
+}
+inline void slow_call(const char* what, size_t bytes, double ms) {
+  if (ms > 2.0) std::fprintf(stderr, "[rr alloc] %s %zu bytes blocked %.1f ms\n", what, bytes, ms);
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -79,10 +94,18 @@ struct DevBuf {
     release();
     s = stream;
     n = count;
-    if (count) RR_CUDA(cudaMallocAsync(&p, sizeof(T) * count, stream));
+    if (count) {
+      const double t0 = alloc_trace() ? wall_ms() : 0.0;
+      RR_CUDA(cudaMallocAsync(&p, sizeof(T) * count, stream));
+      if (alloc_trace()) slow_call("cudaMallocAsync", sizeof(T) * count, wall_ms() - t0);
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      const double t0 = alloc_trace() ? wall_ms() : 0.0;
+      cudaFreeAsync(p, s);
+      if (alloc_trace()) slow_call("cudaFreeAsync", sizeof(T) * n, wall_ms() - t0);
+    }
     p = nullptr;
     n = 0;
   }

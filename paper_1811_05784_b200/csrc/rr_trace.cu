@@ -26,6 +26,7 @@
 namespace rr {
 
 constexpr int kStack8 = 96;  // 8-wide traversal stack (entries); the tree's bound must fit
+constexpr int kStack8G = 32;  // 8-wide group traversal: one entry per level
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
   if (p.block > 0) {
@@ -637,29 +638,37 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
     return e ? std::atoi(e) : -1;
   }();
   const bool wide4 = want4 && s->s4nodes.p != nullptr && (df_env < 0 || df_env == 23);
-  // 8-wide compressed tree: trace_kernel_w8 (rr_trace_w8.cuh); RR_W8V
-  // selects an A/B variant (MINB, DONET, UNR)
+  // 8-wide compressed tree: trace_kernel_w8 (rr_trace_w8.cuh), the group
+  // traversal when the tree's depth fits its stack, else the sorted-push
+  // traversal.  RR_W8V (A/B): 1 the sorted-push kernel, 2 the group kernel
+  // in pure octant order (C5: 527 / 547 / 538 ms for 0 / 1 / 2).
   static const int w8v = [] {
     const char* e = std::getenv("RR_W8V");
     return e ? std::atoi(e) : 0;
   }();
   const bool wide8 = want8 && s->wnodes.p != nullptr && s->wstack <= kStack8 && s->wide_ok;
+  const bool grp8 = wide8 && w8v != 1 && s->wdepth < kStack8G;
+  const bool cnt = (cfg->flags & RR_TRACE_COUNT) != 0;
   using KFn = void (*)(const TraceParams);
-  // A/B (C5, ms; before the ray state moved to shared memory): MINB 8,
-  // DONET 8, UNR 1, sorted pushes 657; unsorted pushes 667; 12 stack
-  // entries in shared memory 658; MINB 7 666; DONET 16 / UNR 4 at MINB 6
-  // 716; UNR 8 810; no batching (the per-ray loop) 1074.  After: 587
-  // (RR_W8V=1: MINB 9 592; 10: 620; 12: 692)
-  KFn w8k = w8v == 1 ? trace_kernel_w8<8, 8, 1, kStack8, false, 12, 2, 2>
-                     : trace_kernel_w8<8, 6, 1, kStack8, false, 12, 4, 2>;
+  // A/B of the sorted-push kernel (C5, ms; before the ray state moved to
+  // shared memory): MINB 8, DONET 8, UNR 1, sorted pushes 657; unsorted
+  // pushes 667; 12 stack entries in shared memory 658; MINB 7 666; DONET 16 /
+  // UNR 4 at MINB 6 716; UNR 8 810; no batching (the per-ray loop) 1074.
+  // After: 587 (MINB 9 592; 10: 620; 12: 692).  Group kernel: DONET 4 / 8
+  // 535 / 527, STUCKD 2 / 8 529 / 547, HOLDD 4 547, MINB 9 (56 registers)
+  // 833, 16 stack entries all in shared memory (7 blocks per SM) 752.
+  KFn w8k = cnt ? trace_kernel_w8<8, 6, 1, kStack8, true, 12, 4, 2> : trace_kernel_w8<8, 6, 1, kStack8, false, 12, 4, 2>;
+  if (grp8)
+    w8k = w8v == 2 ? (cnt ? trace_kernel_w8<8, 6, 1, kStack8G, true, 12, 4, 2, true, false>
+                          : trace_kernel_w8<8, 6, 1, kStack8G, false, 12, 4, 2, true, false>)
+                   : (cnt ? trace_kernel_w8<8, 6, 1, kStack8G, true, 12, 4, 2, true, true>
+                          : trace_kernel_w8<8, 6, 1, kStack8G, false, 12, 4, 2, true, true>);
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);
 #endif
-  if (cfg->flags & RR_TRACE_COUNT)  // counts of the default
-    dfk = wide8   ? trace_kernel_w8<8, 6, 1, kStack8, true, 12, 4, 2>
-          : wide4 ? trace_kernel<3, 8, false, 0, 1, true>
-                  : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
+  if (cnt && !wide8)  // counts of the default
+    dfk = wide4 ? trace_kernel<3, 8, false, 0, 1, true> : trace_kernel<1, 7, false, 16, -2, true, 16, 0, false, 2, false>;
   // diagnostics: fp32 leaf classification / 4-wide nodes over the reference tree
   auto kernel = variant == 0 ? dfk : variant == 1 ? trace_kernel<0, 8> : trace_kernel<2, 1>;
   static thread_local int occ_cache_smem = -1, occ_cache_blocks = 0;
@@ -750,6 +759,8 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   S.n_rays = count;
   S.node_visits = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[7]) : -1;
   S.leaf_tests = (cfg->flags & RR_TRACE_COUNT) ? static_cast<int64_t>(hc[8]) : -1;
+  if ((cfg->flags & RR_TRACE_COUNT) && std::getenv("RR_TIMING"))
+    std::fprintf(stderr, "[rr timing] node visits hitting no slot: %llu of %llu\n", hc[9], hc[7]);
   S.tree_width = wide8 ? 8 : (wide4 || variant == 2) ? 4 : 2;
   S.node_bytes = wide8 ? static_cast<int32_t>(sizeof(WNode)) : (wide4 || variant == 2) ? static_cast<int32_t>(sizeof(QNode))
                                                                                       : static_cast<int32_t>(sizeof(TNode));

@@ -37,7 +37,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cfloat>
+#include <climits>
 #include <cmath>
+#include <cstdint>
 
 #include "rr_geom.cuh"
 
@@ -69,10 +72,19 @@ __device__ __forceinline__ float half_area(const Slot& s) {
   return dx * dy + dy * dz + dz * dx;
 }
 
-// expand frontier node i into <= 8 slots; packed (internal << 32 | faces)
+constexpr int32_t kEmptySlot = INT32_MIN;  // an unused slot of the 8 (ref)
+
+// expand frontier node i into <= 8 slots; packed (internal << 32 | faces).
+// order: place the children in the 8 slots by direction (Ylitie, Karras and
+// Laine 2017): slot s stands for the ray octant s (bit a set: negative
+// direction along axis a) and takes the child nearest to that octant's
+// rays' entry side, i.e. the one minimising dot(centroid - centre, sign(s)),
+// chosen greedily by cost; a ray of octant o then meets the children roughly
+// front to back in the slot order s = j ^ o, j = 0..7 (trace_kernel_w8's
+// group traversal).  Any slot order gives the same closest hits.
 __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __restrict__ frontier, int32_t n,
                               Slot* __restrict__ slots, int32_t* __restrict__ nslot,
-                              unsigned long long* __restrict__ packed) {
+                              unsigned long long* __restrict__ packed, int order) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
@@ -99,10 +111,46 @@ __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __res
   }
   unsigned long long ni = 0, nfc = 0;
   for (int k = 0; k < cnt; ++k) {
-    slots[static_cast<int64_t>(i) * kW + k] = s[k];
     if (s[k].ref >= 0) ++ni;
     else nfc += leaf_faces(s[k].ref);
   }
+  int at[kW];  // slot of child k
+  for (int k = 0; k < cnt; ++k) at[k] = k;
+  if (order) {
+    float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int k = 0; k < cnt; ++k)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fminf(lo[a], s[k].b[2 * a]);
+        hi[a] = fmaxf(hi[a], s[k].b[2 * a + 1]);
+      }
+    float c[kW][3];
+    for (int k = 0; k < cnt; ++k)
+      for (int a = 0; a < 3; ++a) c[k][a] = 0.5f * (s[k].b[2 * a] + s[k].b[2 * a + 1]) - 0.5f * (lo[a] + hi[a]);
+    uint32_t free_child = (1u << cnt) - 1u, free_slot = 0xffu;
+    for (int it = 0; it < cnt; ++it) {
+      float best = FLT_MAX;
+      int bk = -1, bs = -1;
+      for (int k = 0; k < cnt; ++k) {
+        if (!((free_child >> k) & 1u)) continue;
+        for (int sl = 0; sl < kW; ++sl) {
+          if (!((free_slot >> sl) & 1u)) continue;
+          const float cost = ((sl & 1) ? -c[k][0] : c[k][0]) + ((sl & 2) ? -c[k][1] : c[k][1]) +
+                             ((sl & 4) ? -c[k][2] : c[k][2]);
+          if (cost < best || bk < 0) {
+            best = cost;
+            bk = k;
+            bs = sl;
+          }
+        }
+      }
+      at[bk] = bs;
+      free_child &= ~(1u << bk);
+      free_slot &= ~(1u << bs);
+    }
+  }
+  Slot* out = slots + static_cast<int64_t>(i) * kW;
+  for (int k = 0; k < kW; ++k) out[k].ref = kEmptySlot;
+  for (int k = 0; k < cnt; ++k) out[at[k]] = s[k];
   nslot[i] = cnt;
   packed[i] = (ni << 32) | nfc;
 }
@@ -113,10 +161,11 @@ __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __res
 // evaluates t = fma(2^23 + q, A, C) with A = 2^(e-127) * inv (exact) and
 // C = fl(B - (2^23 + 1) A), whose rounding is at most |A| / 2, i.e. half a
 // grid step in space units (rr_geom.cuh wslab).  Returns the biased exponent.
-__device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, double m, float* p_out,
-                                               uint32_t* lo8, uint32_t* hi8) {
+__device__ __forceinline__ uint32_t quant_axis(const Slot* s, int ax, double m, float* p_out, uint32_t* lo8,
+                                               uint32_t* hi8) {
   double lo = 1e300, hi = -1e300;
-  for (int k = 0; k < cnt; ++k) {
+  for (int k = 0; k < kW; ++k) {
+    if (s[k].ref == kEmptySlot) continue;
     lo = fmin(lo, static_cast<double>(s[k].b[2 * ax]) - m);
     hi = fmax(hi, static_cast<double>(s[k].b[2 * ax + 1]) + m);
   }
@@ -130,7 +179,8 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int cnt, int ax, d
   e = max(e, -126);
   const double sc = ldexp(1.0, e);
   lo8[0] = lo8[1] = hi8[0] = hi8[1] = 0;
-  for (int k = 0; k < cnt; ++k) {
+  for (int k = 0; k < kW; ++k) {
+    if (s[k].ref == kEmptySlot) continue;
     // q - 1 = floor(..) - 1 and ceil(..) + 1
     double ql = floor((static_cast<double>(s[k].b[2 * ax]) - m - pd) / sc);
     double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc) + 2.0;
@@ -154,20 +204,20 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
   if (i >= n) return;
   Slot s[kW];
   const int cnt = nslot[i];
-  for (int k = 0; k < cnt; ++k) s[k] = slots[static_cast<int64_t>(i) * kW + k];
+  for (int k = 0; k < kW; ++k) s[k] = slots[static_cast<int64_t>(i) * kW + k];
   const unsigned long long o = offs[i];
   const int32_t ci = static_cast<int32_t>(o >> 32);  // rank of my first internal child in the next level
   const int32_t ti = tri_base + static_cast<int32_t>(o & 0xffffffffu);
   WNode w;
   float p[3];
   uint32_t e[3], lo8[3][2], hi8[3][2];
-  for (int ax = 0; ax < 3; ++ax) e[ax] = quant_axis(s, cnt, ax, margin, &p[ax], lo8[ax], hi8[ax]);
+  for (int ax = 0; ax < 3; ++ax) e[ax] = quant_axis(s, ax, margin, &p[ax], lo8[ax], hi8[ax]);
   uint32_t imask = 0, valid = 0, pair = 0, cull = 0;
   // plane for the cull: the first slot plane (a subtree inside an axis-aligned
   // wall usually has all its slots in that wall)
   int32_t plane = -1;
-  for (int k = 0; k < cnt; ++k)
-    if (s[k].plane >= 0) {
+  for (int k = 0; k < kW; ++k)
+    if (s[k].ref != kEmptySlot && s[k].plane >= 0) {
       plane = s[k].plane;
       break;
     }
@@ -175,7 +225,8 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
   // pushed (trace_kernel_w8 pushes leaf slots too)
   const int32_t a = acc[i] + cnt - 1;
   int ni = 0, nfc = 0;
-  for (int k = 0; k < cnt; ++k) {
+  for (int k = 0; k < kW; ++k) {
+    if (s[k].ref == kEmptySlot) continue;
     valid |= 1u << k;
     if (plane >= 0 && s[k].plane == plane) cull |= 1u << k;
     if (s[k].ref >= 0) {
@@ -200,7 +251,9 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
   atomicMax(emax, static_cast<int32_t>(max(e[0], max(e[1], e[2]))));
   w.h = make_float4(p[0], p[1], p[2], __int_as_float(static_cast<int>(e[0] | (e[1] << 8) | (e[2] << 16) |
                                                                        (imask << 24))));
-  w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16)));
+  // bits: valid | pair << 8 | cull << 16 | internal << 24 (the internal mask
+  // also in h.w, next to the exponents)
+  w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16) | (imask << 24)));
   w.qx = make_uint4(lo8[0][0], lo8[0][1], hi8[0][0], hi8[0][1]);
   w.qy = make_uint4(lo8[1][0], lo8[1][1], hi8[1][0], hi8[1][1]);
   w.qz = make_uint4(lo8[2][0], lo8[2][1], hi8[2][0], hi8[2][1]);
@@ -232,6 +285,11 @@ void build_wide(rr_scene* s) {
   RR_CUDA(cudaMemcpyAsync(fr[0].p, &root, sizeof root, cudaMemcpyHostToDevice, st));
   RR_CUDA(cudaMemcpyAsync(ac[0].p, &zero, sizeof zero, cudaMemcpyHostToDevice, st));
   const double margin = 0.25 * static_cast<double>(s->shdr.eps);
+  // RR_W8_ORDER=0: children in expansion order (A/B)
+  static const int slot_order = [] {
+    const char* e = std::getenv("RR_W8_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
   int32_t n = 1, base = 0, depth = 0;
   int64_t tri_done = 0;
   while (n > 0) {
@@ -239,7 +297,7 @@ void build_wide(rr_scene* s) {
     nslot.alloc(n, st);
     packed.alloc(n + 1, st);
     offs.alloc(n + 1, st);
-    expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p);
+    expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p, slot_order);
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaMemsetAsync(packed.p + n, 0, sizeof(unsigned long long), st));
     size_t need = 0;
