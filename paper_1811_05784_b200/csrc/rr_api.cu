@@ -4,9 +4,118 @@
 #include <functional>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "rr_trace.cuh"
+
+// Block cache of the context streams (rr_internal.cuh DevBuf).
+namespace rr {
+namespace {
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+  cudaStream_t s;
+  uint64_t tick;  // release order (oldest evicted first)
+};
+struct BlockCache {
+  std::mutex m;
+  std::vector<CachedBlock> blocks;
+  std::vector<cudaStream_t> streams;
+  size_t held = 0, limit = 0;
+  uint64_t tick = 0;
+  BlockCache() {
+    const char* e = std::getenv("RR_BLOCK_CACHE_MB");
+    limit = static_cast<size_t>(e ? std::atoll(e) : 16384) << 20;
+  }
+  bool known(cudaStream_t s) const {
+    for (cudaStream_t t : streams)
+      if (t == s) return true;
+    return false;
+  }
+};
+BlockCache& cache() {
+  static BlockCache* c = new BlockCache;  // never destroyed: DevBufs may outlive static destruction
+  return *c;
+}
+}  // namespace
+
+void* cache_take(size_t bytes, cudaStream_t s, size_t* got) {
+  BlockCache& c = cache();
+  if (c.limit == 0) return nullptr;
+  std::lock_guard<std::mutex> g(c.m);
+  // best fit among the stream's blocks of [bytes, bytes * 1.25 + 2 MB]
+  const size_t hi = bytes + bytes / 4 + (size_t{2} << 20);
+  size_t best = c.blocks.size();
+  for (size_t i = 0; i < c.blocks.size(); ++i) {
+    const CachedBlock& b = c.blocks[i];
+    if (b.s == s && b.bytes >= bytes && b.bytes <= hi && (best == c.blocks.size() || b.bytes < c.blocks[best].bytes))
+      best = i;
+  }
+  if (best == c.blocks.size()) return nullptr;
+  void* p = c.blocks[best].p;
+  *got = c.blocks[best].bytes;
+  c.held -= *got;
+  c.blocks[best] = c.blocks.back();
+  c.blocks.pop_back();
+  return p;
+}
+
+bool cache_give(void* p, size_t bytes, cudaStream_t s) {
+  BlockCache& c = cache();
+  if (c.limit == 0 || bytes > c.limit) return false;
+  std::lock_guard<std::mutex> g(c.m);
+  if (!c.known(s)) return false;
+  while (c.held + bytes > c.limit && !c.blocks.empty()) {  // evict the oldest
+    size_t o = 0;
+    for (size_t i = 1; i < c.blocks.size(); ++i)
+      if (c.blocks[i].tick < c.blocks[o].tick) o = i;
+    cudaFreeAsync(c.blocks[o].p, c.blocks[o].s);
+    c.held -= c.blocks[o].bytes;
+    c.blocks[o] = c.blocks.back();
+    c.blocks.pop_back();
+  }
+  c.blocks.push_back(CachedBlock{p, bytes, s, ++c.tick});
+  c.held += bytes;
+  return true;
+}
+
+void cache_register(cudaStream_t s) {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> g(c.m);
+  if (!c.known(s)) c.streams.push_back(s);
+}
+
+void cache_drop(cudaStream_t s) {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> g(c.m);
+  for (size_t i = 0; i < c.blocks.size();) {
+    if (c.blocks[i].s == s) {
+      cudaFreeAsync(c.blocks[i].p, s);
+      c.held -= c.blocks[i].bytes;
+      c.blocks[i] = c.blocks.back();
+      c.blocks.pop_back();
+    } else {
+      ++i;
+    }
+  }
+  for (size_t i = 0; i < c.streams.size(); ++i)
+    if (c.streams[i] == s) {
+      c.streams[i] = c.streams.back();
+      c.streams.pop_back();
+      break;
+    }
+}
+
+void cache_trim() {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> g(c.m);
+  for (const CachedBlock& b : c.blocks) cudaFreeAsync(b.p, b.s);
+  for (cudaStream_t s : c.streams) cudaStreamSynchronize(s);  // the frees reach the pool
+  c.blocks.clear();
+  c.held = 0;
+}
+}  // namespace rr
 
 namespace {
 
@@ -109,6 +218,7 @@ rr_status rr_ctx_create(int device, rr_ctx** out) {
     auto c = std::make_unique<rr_ctx>();
     c->device = device;
     RR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    rr::cache_register(c->stream);
     // keep freed stream-ordered allocations cached in the pool, so the
     // per-call buffers of rr_trace & co. cost no driver round trips
     cudaMemPool_t pool;
@@ -129,6 +239,7 @@ namespace {
 void ctx_release(rr_ctx* ctx) {
   if (--ctx->refs > 0) return;
   cudaSetDevice(ctx->device);
+  rr::cache_drop(ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
   for (cudaEvent_t e : ctx->level_ev)

@@ -72,20 +72,37 @@ inline void slow_call(const char* what, size_t bytes, double ms) {
   if (ms > 2.0) std::fprintf(stderr, "[rr alloc] %s %zu bytes blocked %.1f ms\n", what, bytes, ms);
 }
 
+// Block cache of the context streams (rr_api.cu).  A released block goes
+// to its stream's cache instead of cudaFreeAsync and a later allocation on
+// the same stream takes it back: everything that touches the block is
+// ordered on that one stream, exactly as with cudaFreeAsync ->
+// cudaMallocAsync, but with no driver call.  The driver's pool does the same
+// in principle, yet on the GPU boxes a steady-state C5 pipeline step saw
+// 2-300 ms host stalls inside cudaMallocAsync of sizes the pool had just
+// freed (gpurun_out/alloc_trace.log), which the end-to-end time pays.
+// Only streams registered by rr_ctx_create are cached; RR_BLOCK_CACHE_MB
+// caps the cached bytes (default 16384; 0 turns the cache off).
+void* cache_take(size_t bytes, cudaStream_t s, size_t* got);
+bool cache_give(void* p, size_t bytes, cudaStream_t s);
+void cache_register(cudaStream_t s);
+void cache_drop(cudaStream_t s);  // free the stream's blocks (before destroying it)
+void cache_trim();                // free every cached block (allocation failure)
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;  // bytes of the block (>= sizeof(T) * n when it came from the cache)
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap), s(o.s) { o.p = nullptr; o.n = 0; o.cap = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; cap = o.cap; s = o.s;
+      o.p = nullptr; o.n = 0; o.cap = 0;
     }
     return *this;
   }
@@ -95,19 +112,34 @@ struct DevBuf {
     s = stream;
     n = count;
     if (count) {
+      const size_t want = sizeof(T) * count;
+      p = static_cast<T*>(cache_take(want, stream, &cap));
+      if (p) return;
       const double t0 = alloc_trace() ? wall_ms() : 0.0;
-      RR_CUDA(cudaMallocAsync(&p, sizeof(T) * count, stream));
-      if (alloc_trace()) slow_call("cudaMallocAsync", sizeof(T) * count, wall_ms() - t0);
+      cudaError_t e = cudaMallocAsync(&p, want, stream);
+      if (e == cudaErrorMemoryAllocation) {  // cached blocks may hold the memory
+        cudaGetLastError();
+        cache_trim();
+        e = cudaMallocAsync(&p, want, stream);
+      }
+      if (e != cudaSuccess) {
+        p = nullptr;
+        n = 0;
+        RR_CUDA(e);
+      }
+      cap = want;
+      if (alloc_trace()) slow_call("cudaMallocAsync", want, wall_ms() - t0);
     }
   }
   void release() {
-    if (p) {
+    if (p && !cache_give(p, cap, s)) {
       const double t0 = alloc_trace() ? wall_ms() : 0.0;
       cudaFreeAsync(p, s);
-      if (alloc_trace()) slow_call("cudaFreeAsync", sizeof(T) * n, wall_ms() - t0);
+      if (alloc_trace()) slow_call("cudaFreeAsync", cap, wall_ms() - t0);
     }
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   size_t bytes() const { return sizeof(T) * n; }
 };
