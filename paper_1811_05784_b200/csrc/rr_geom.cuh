@@ -147,6 +147,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
   return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
+#ifndef RR_HBUF
+#define RR_HBUF 0  // 8-wide tracer: face history buffered per 32-B sector (rr_trace_w8.cuh; A/B)
+#endif
 #ifndef RR_FFMA2
 #define RR_FFMA2 1
 #endif

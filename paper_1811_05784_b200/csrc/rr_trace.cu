@@ -27,6 +27,23 @@ namespace rr {
 
 constexpr int kStack8 = 96;  // 8-wide traversal stack (entries); the tree's bound must fit
 constexpr int kStack8G = 32;  // 8-wide group traversal: one entry per level
+// stack entries per lane in shared memory (8-wide tracers).  The shared
+// memory per SM sets the L1 size (256 KB - the carveout the driver picks for
+// 8 blocks): C5 with 12 entries (196 KB carveout, 60 KB L1) 516 ms, 8 (164 KB,
+// 92 KB L1) 508, 4 (132 KB) 510, 0 (100 KB, the stack in local memory) 523;
+// the face-history sector buffer (RR_HBUF, +4 KB per block) at 12 entries
+// forced the 228 KB carveout (28 KB L1, L1 hit rate 34 -> 24 %): 728 ms; at
+// equal carveouts it is neutral (8 entries 511, 4 entries 509).
+#ifndef RR_SMS8
+#define RR_SMS8 (RR_HBUF ? 4 : 8)
+#endif
+constexpr int kSms8 = RR_SMS8;
+#ifndef RR_MINB8
+#define RR_MINB8 8  // blocks of 128 per SM (64 registers)
+#endif
+#ifndef RR_DONET8
+#define RR_DONET8 6  // lanes done before a warp leaves traversal for shading
+#endif
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
   if (p.block > 0) {
@@ -657,12 +674,12 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // After: 587 (MINB 9 592; 10: 620; 12: 692).  Group kernel: DONET 4 / 8
   // 535 / 527, STUCKD 2 / 8 529 / 547, HOLDD 4 547, MINB 9 (56 registers)
   // 833, 16 stack entries all in shared memory (7 blocks per SM) 752.
-  KFn w8k = cnt ? trace_kernel_w8<8, 6, 1, kStack8, true, 12, 4, 2> : trace_kernel_w8<8, 6, 1, kStack8, false, 12, 4, 2>;
+  KFn w8k = cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, true, kSms8, 4, 2> : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, false, kSms8, 4, 2>;
   if (grp8)
-    w8k = w8v == 2 ? (cnt ? trace_kernel_w8<8, 6, 1, kStack8G, true, 12, 4, 2, true, false>
-                          : trace_kernel_w8<8, 6, 1, kStack8G, false, 12, 4, 2, true, false>)
-                   : (cnt ? trace_kernel_w8<8, 6, 1, kStack8G, true, 12, 4, 2, true, true>
-                          : trace_kernel_w8<8, 6, 1, kStack8G, false, 12, 4, 2, true, true>);
+    w8k = w8v == 2 ? (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, 4, 2, true, false>
+                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, 4, 2, true, false>)
+                   : (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, 4, 2, true, true>
+                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, 4, 2, true, true>);
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);

@@ -70,6 +70,20 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   };
   __shared__ LaneState s_lane[128];
   LaneState& ls = s_lane[threadIdx.x];
+#if RR_HBUF
+  // face history: each lane's current 32-B sector of hist[] in shared memory
+  // (column tid), written out as two 16-B stores when the sector fills and
+  // lies inside the ray's own history, else word by word (the ray's first
+  // and last sectors).  One 4-B store per bounce made every bounce a partial
+  // sector in L2; with the L2 streaming triangles most were evicted before
+  // the next bounce filled them (C5: 31.7 GB of DRAM writes per trace for a
+  // 3.2 GB history).
+  __shared__ int32_t s_hist[8 * 128];
+  int32_t* shb = s_hist + threadIdx.x;
+  auto hist_words = [&](int64_t from, int64_t to) {  // hist[from..to] from the sector buffer
+    for (int64_t j = from; j <= to; ++j) p.hist[j] = shb[(j & 7) * 128];
+  };
+#endif
   D3& o = ls.o;
   D3& d = ls.d;
   HitResult& best = ls.best;
@@ -242,7 +256,22 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         }
         ls.path += best.delta;
         RR_DCHECK(ls.ray < p.count && ls.bounces < p.H && best.face < p.nf);
-        p.hist[static_cast<int64_t>(ls.ray) * p.H + ls.bounces] = best.face;
+        const int64_t g = static_cast<int64_t>(ls.ray) * p.H + ls.bounces;
+#if RR_HBUF
+        shb[(g & 7) * 128] = best.face;
+        if ((g & 7) == 7) {
+          const int64_t g0 = static_cast<int64_t>(ls.ray) * p.H;
+          if (g - 7 >= g0) {
+            int4* dst = reinterpret_cast<int4*>(p.hist + (g - 7));
+            dst[0] = make_int4(shb[0], shb[128], shb[256], shb[384]);
+            dst[1] = make_int4(shb[512], shb[640], shb[768], shb[896]);
+          } else {
+            hist_words(g0, g);
+          }
+        }
+#else
+        p.hist[g] = best.face;
+#endif
         ++ls.bounces;
         if (ls.path > p.max_range) {
           dead = true;
@@ -254,6 +283,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         atomicAdd(s_stat + 3, 1ull);
       }
       if (dead) {
+#if RR_HBUF
+        if (ls.bounces > 0) {  // the ray's last, partial sector
+          const int64_t g0 = static_cast<int64_t>(ls.ray) * p.H, gl = g0 + ls.bounces - 1;
+          if ((gl & 7) != 7) hist_words(max(g0, gl & ~static_cast<int64_t>(7)), gl);
+        }
+#endif
         atomicAdd(s_stat + 0, static_cast<unsigned long long>(ls.steps));
         atomicMax(s_stat + 4, static_cast<unsigned long long>(ls.steps));
         has_ray = false;
