@@ -34,6 +34,26 @@ __device__ __forceinline__ uint32_t xperm8(uint32_t m, uint32_t o) {
   return m;
 }
 
+#ifndef RR_PF8
+#define RR_PF8 1  // prefetch a stashed leaf's faces into L2 (C5 -0.5 %; 2: into L1, 0: none)
+#endif
+#ifndef RR_HCS
+#define RR_HCS 0  // A/B: face-history stores with the streaming (evict-first) hint
+#endif
+// start fetching the faces of a leaf stashed for the next batched test
+__device__ __forceinline__ void prefetch_leaf(const FaceTri* wtri, int32_t leaf) {
+  if (RR_PF8 == 0) return;
+  const char* a = reinterpret_cast<const char*>(wtri + leaf_face(leaf));
+  const char* b = a + leaf_faces(leaf) * sizeof(FaceTri) - 1;
+  if (RR_PF8 == 1) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
+  } else {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(b));
+  }
+}
+
 // GRP: group traversal.  The stack holds one entry per visited node with
 // more than one hit slot -- the node and the mask of its remaining hit slots
 // -- instead of one entry per pushed child: the visit continues into the
@@ -269,6 +289,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
             hist_words(g0, g);
           }
         }
+#elif RR_HCS
+        __stcs(p.hist + g, best.face);
 #else
         p.hist[g] = best.face;
 #endif
@@ -351,7 +373,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
                 uint32_t mn = 0xffffffffu;
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
-                  mn = min(mn, ((hm >> q) & 1u) ? ((__float_as_uint(fmaxf(v.t[q], 0.0f)) & ~7u) | q) : 0xffffffffu);
+                  mn = min(mn, ((hm >> q) & 1u) ? ((__float_as_uint(RR_HIT2 ? v.t[q] : fmaxf(v.t[q], 0.0f)) & ~7u) | q)
+                                                : 0xffffffffu);
                 k = static_cast<int>(mn & 7u);
                 pm = gperm(hm & ~(1u << k));
               } else {
@@ -405,11 +428,13 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           }
           if (node < 0 && leaf == 0) {  // stash a reached leaf and keep traversing
             leaf = node;
+            prefetch_leaf(p.wtri, leaf);
             if constexpr (GRP) gtake(); else pop();
           }
         }
         if (node < 0 && leaf == 0) {  // a popped leaf with no node visit
           leaf = node;
+          prefetch_leaf(p.wtri, leaf);
           if constexpr (GRP) gtake(); else pop();
         }
         // batched fp64 leaf tests (closest_hit_pl's vote)
@@ -429,6 +454,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
               leaf = 0;
               if (node < 0) {  // the leaf that waited for the slot
                 leaf = node;
+                prefetch_leaf(p.wtri, leaf);
                 if constexpr (GRP) gtake(); else pop();
               }
             }
