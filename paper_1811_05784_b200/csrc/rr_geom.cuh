@@ -147,11 +147,21 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
   return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
+// 8-wide tracer options (rr_trace_w8.cuh)
+#ifndef RR_PF8
+#define RR_PF8 1  // prefetch a stashed leaf's faces into L2 (C5 -0.5 %; 2: into L1, 0: none)
+#endif
+#ifndef RR_GST
+#define RR_GST 1  // group entries hold the node's child / face bases: no refetch at the pop (0: A/B)
+#endif
+#ifndef RR_HCS
+#define RR_HCS 0  // A/B: face-history stores with the streaming (evict-first) hint (neutral)
+#endif
 #ifndef RR_HIT2
 #define RR_HIT2 1  // 8-wide slot test with the clamps folded into the 3-input min / max (C5 506 -> 493 ms; 0: A/B)
 #endif
 #ifndef RR_FCG
-#define RR_FCG 0
+#define RR_FCG 0  // A/B: face loads cached in L2 only (C5 508 -> 511 ms)
 #endif
 #ifndef RR_HBUF
 #define RR_HBUF 0  // 8-wide tracer: face history buffered per 32-B sector (rr_trace_w8.cuh; A/B)

@@ -33,9 +33,11 @@ constexpr int kStack8G = 32;  // 8-wide group traversal: one entry per level
 // 92 KB L1) 508, 4 (132 KB) 510, 0 (100 KB, the stack in local memory) 523;
 // the face-history sector buffer (RR_HBUF, +4 KB per block) at 12 entries
 // forced the 228 KB carveout (28 KB L1, L1 hit rate 34 -> 24 %): 728 ms; at
-// equal carveouts it is neutral (8 entries 511, 4 entries 509).
+// equal carveouts it is neutral (8 entries 511, 4 entries 509).  Group
+// entries with the child / face bases (RR_GST, 12 B): 5 entries (164 KB)
+// 486.6 ms, 4 490, 2 503, 0 502, 8 (196 KB) 491; without, 8 entries 491.
 #ifndef RR_SMS8
-#define RR_SMS8 (RR_HBUF ? 4 : 8)
+#define RR_SMS8 (RR_HBUF ? 4 : RR_GST ? 5 : 8)
 #endif
 constexpr int kSms8 = RR_SMS8;
 #ifndef RR_MINB8

@@ -34,12 +34,6 @@ __device__ __forceinline__ uint32_t xperm8(uint32_t m, uint32_t o) {
   return m;
 }
 
-#ifndef RR_PF8
-#define RR_PF8 1  // prefetch a stashed leaf's faces into L2 (C5 -0.5 %; 2: into L1, 0: none)
-#endif
-#ifndef RR_HCS
-#define RR_HCS 0  // A/B: face-history stores with the streaming (evict-first) hint
-#endif
 // start fetching the faces of a leaf stashed for the next batched test
 __device__ __forceinline__ void prefetch_leaf(const FaceTri* wtri, int32_t leaf) {
   if (RR_PF8 == 0) return;
@@ -72,6 +66,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   // lane i always in bank i, conflict-free), deeper ones in local memory
   __shared__ int2 s_st[SMS > 0 ? SMS * 128 : 1];
   int2* sst = s_st + threadIdx.x;
+#if RR_GST
+  // group entries: (first child, first face) in s_st / st, the node's slot
+  // bits with the remaining-slot mask in bits 16-23 here
+  __shared__ uint32_t s_st2[SMS > 0 ? SMS * 128 : 1];
+  uint32_t* sst2 = s_st2 + threadIdx.x;
+#endif
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const float kInf = __int_as_float(0x7f800000);
@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
   float tbest = FLT_MAX;
   int32_t node = kDone, leaf = 0;
   int2 st[STK > SMS ? STK - SMS : 1];
+#if RR_GST
+  uint32_t st2[STK > SMS ? STK - SMS : 1];
+#endif
   int sp = 0;
   int2 top[2] = {};
   int n_top = 0;
@@ -141,6 +144,13 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
     else st[i - SMS] = e;
   };
   auto st_get = [&](int i) -> int2 { return (SMS > 0 && (SMS >= STK || i < SMS)) ? sst[i * 128] : st[i - SMS]; };
+#if RR_GST
+  auto st_put2 = [&](int i, uint32_t b) {
+    if (SMS > 0 && (SMS >= STK || i < SMS)) sst2[i * 128] = b;
+    else st2[i - SMS] = b;
+  };
+  auto st_get2 = [&](int i) -> uint32_t { return (SMS > 0 && (SMS >= STK || i < SMS)) ? sst2[i * 128] : st2[i - SMS]; };
+#endif
   auto push = [&](int2 e) {
     if (n_top == 2) st_put(sp++, top[1]);
     top[1] = top[0];
@@ -183,6 +193,14 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
         node = kDone;
         return;
       }
+#if RR_GST
+      --sp;
+      const int2 e = st_get(sp);
+      g_child = e.x;
+      g_tri = e.y;
+      g_bits = st_get2(sp);
+      g_mask = (g_bits >> 16) & 0xffu;
+#else
       const int2 e = st_get(--sp);
       g_node = e.x;
       g_mask = static_cast<uint32_t>(e.y);
@@ -190,6 +208,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
       g_child = mm.x;
       g_tri = mm.y;
       g_bits = static_cast<uint32_t>(mm.w);
+#endif
     }
     const int j = __ffs(g_mask) - 1;
     g_mask &= g_mask - 1u;
@@ -384,7 +403,14 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
               }
               const int32_t next = wref(v, k);
               if (pm) {  // the node's other hit slots become the current group
+#if RR_GST
+                if (g_mask != 0) {
+                  st_put2(sp, (g_bits & 0xff00ffffu) | (g_mask << 16));
+                  st_put(sp++, make_int2(g_child, g_tri));
+                }
+#else
                 if (g_mask != 0) st_put(sp++, make_int2(g_node, static_cast<int>(g_mask)));
+#endif
                 g_node = node;
                 g_mask = pm;
                 g_child = v.child;
