@@ -157,6 +157,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #ifndef RR_HCS
 #define RR_HCS 0  // A/B: face-history stores with the streaming (evict-first) hint (neutral)
 #endif
+#ifndef RR_OCT
+#define RR_OCT 1  // octant flags re-derived from the octant word at each visit: 7 -> 3 spill reloads per visit (C5 486.5 -> 482.8 ms; 0: A/B)
+#endif
 #ifndef RR_HIT2
 #define RR_HIT2 1  // 8-wide slot test with the clamps folded into the 3-input min / max (C5 506 -> 493 ms; 0: A/B)
 #endif

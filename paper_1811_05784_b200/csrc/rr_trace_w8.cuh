@@ -379,7 +379,11 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           if (CNT) ++st_cnt[0];
           WVisit v;
           RR_DCHECK(node < p.n_wnodes);
+#if RR_OCT  // the octant flags from the one octant word (fewer live registers)
+          visit_w8(p.wnodes, node, r, (oct & 1u) == 0u, (oct & 2u) == 0u, (oct & 4u) == 0u, tbest, rplane, v);
+#else
           visit_w8(p.wnodes, node, r, px, py, pz, tbest, rplane, v);
+#endif
           const uint32_t hm = v.hit;
           if (CNT && hm == 0) ++st_cnt[2];
           if constexpr (GRP) {
