@@ -37,9 +37,12 @@ namespace rr {
 namespace {
 
 constexpr int kBins = 32;
-constexpr int64_t kSahMin = 64;
+constexpr int64_t kSahMin = 17;  // binned SAH from 17 faces (64: C5 468.8 -> 477.0 ms, C2 9.26 -> 10.0 with the exact finish)
 constexpr int kMaxDepth = 30;
-constexpr int kSmall = 16;  // segments this small are built in one go by one thread
+#ifndef RR_KSMALL
+#define RR_KSMALL 16
+#endif
+constexpr int kSmall = RR_KSMALL;  // segments this small are built in one go by one thread
 const char* const kLevelNames[64] = {
     "sah level 0",  "sah level 1",  "sah level 2",  "sah level 3",  "sah level 4",  "sah level 5",  "sah level 6",
     "sah level 7",  "sah level 8",  "sah level 9",  "sah level 10", "sah level 11", "sah level 12", "sah level 13",
@@ -467,7 +470,7 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
                               const int32_t* __restrict__ perm0, const double* __restrict__ fb,
                               const double* __restrict__ cen, const int32_t* __restrict__ face_plane, int64_t nf,
                               TNode* __restrict__ tn, TravHeader* __restrict__ hdr,
-                              unsigned long long* __restrict__ top) {
+                              unsigned long long* __restrict__ top, int level, int fin_sah) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= ls->S) return;
   const float eps = hdr->eps;
@@ -530,26 +533,8 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
       child_slot(tn + sg.parent, sg.side, lo, hi, eps, base, plane);
     }
   }
-  // explicit stack of ranges still to split: (a, b, node index)
-  int sa[kSmall], sb[kSmall], sn[kSmall];
-  int sp = 0;
-  sa[0] = 0;
-  sb[0] = n;
-  sn[0] = base;
-  sp = 1;
-  while (sp > 0) {
-    --sp;
-    const int a = sa[sp], b = sb[sp], me = sn[sp];
-    // longest centroid extent, then insertion sort of f[a, b) on that axis
-    double clo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, chi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
-    for (int i = a; i < b; ++i)
-      for (int k = 0; k < 3; ++k) {
-        clo[k] = fmin(clo[k], cen[3 * f[i] + k]);
-        chi[k] = fmax(chi[k], cen[3 * f[i] + k]);
-      }
-    int ax = 0;
-    for (int k = 1; k < 3; ++k)
-      if (chi[k] - clo[k] > chi[ax] - clo[ax]) ax = k;
+  // insertion sort of f[a, b) by centroid on axis ax (ties by face id)
+  auto sort_axis = [&](int a, int b, int ax) {
     for (int x = a + 1; x < b; ++x) {
       const int32_t v = f[x];
       const double cv = cen[3 * v + ax];
@@ -560,8 +545,81 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
       }
       f[y + 1] = v;
     }
-    int m = a + (b - a) / 2;
-    if (b - a > 2 && twins_at(f[m - 1], f[m], cen)) m = (m + 1 < b) ? m + 1 : m - 1;  // keep twins together
+  };
+  // exact SAH over the sorted centroid orders of the three axes (fin_sah):
+  // the split position m of [a, b) minimising A(left) |left| + A(right)
+  // |right|, twins kept together; f[a, b) left sorted on the chosen axis.
+  // Returns false when no position qualifies.
+  auto sah_exact = [&](int a, int b, int* m_out) -> bool {
+    double best = HUGE_VAL;
+    int bax = -1, bm = -1;
+    for (int ax = 0; ax < 3; ++ax) {
+      sort_axis(a, b, ax);
+      double ra[kSmall];
+      double lo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, hi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+      for (int i = b - 1; i > a; --i) {  // ra[i - a]: area of f[i, b)
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = fmin(lo[k], fb[6 * f[i] + k]);
+          hi[k] = fmax(hi[k], fb[6 * f[i] + 3 + k]);
+        }
+        ra[i - a] = half_area(lo, hi);
+      }
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = HUGE_VAL;
+        hi[k] = -HUGE_VAL;
+      }
+      for (int i = a + 1; i < b; ++i) {  // split before position i
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = fmin(lo[k], fb[6 * f[i - 1] + k]);
+          hi[k] = fmax(hi[k], fb[6 * f[i - 1] + 3 + k]);
+        }
+        if (twins_at(f[i - 1], f[i], cen)) continue;
+        const double c = half_area(lo, hi) * (i - a) + ra[i - a] * (b - i);
+        if (c < best) {
+          best = c;
+          bax = ax;
+          bm = i;
+        }
+      }
+    }
+    if (bax < 0) return false;
+    if (bax != 2) sort_axis(a, b, bax);
+    *m_out = bm;
+    return true;
+  };
+  // explicit stack of ranges still to split: (a, b, node index, depth below
+  // the segment)
+  int sa[kSmall], sb[kSmall], sn[kSmall], sd[kSmall];
+  int sp = 0;
+  sa[0] = 0;
+  sb[0] = n;
+  sn[0] = base;
+  sd[0] = 0;
+  sp = 1;
+  while (sp > 0) {
+    --sp;
+    const int a = sa[sp], b = sb[sp], me = sn[sp], dep = sd[sp];
+    int m = -1;
+    // SAH while the depth budget leaves room for a median finish below
+    // either child (the level kernels' rule, split_flags)
+    int lg = 0;
+    while ((1 << lg) < b - a) ++lg;
+    const bool sah_ok = fin_sah && level + dep + lg + 2 <= kMaxDepth;
+    if (!(sah_ok && b - a > 2 && sah_exact(a, b, &m))) {
+      // longest centroid extent, then insertion sort of f[a, b) on that axis
+      double clo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, chi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+      for (int i = a; i < b; ++i)
+        for (int k = 0; k < 3; ++k) {
+          clo[k] = fmin(clo[k], cen[3 * f[i] + k]);
+          chi[k] = fmax(chi[k], cen[3 * f[i] + k]);
+        }
+      int ax = 0;
+      for (int k = 1; k < 3; ++k)
+        if (chi[k] - clo[k] > chi[ax] - clo[ax]) ax = k;
+      sort_axis(a, b, ax);
+      m = a + (b - a) / 2;
+      if (b - a > 2 && twins_at(f[m - 1], f[m], cen)) m = (m + 1 < b) ? m + 1 : m - 1;  // keep twins together
+    }
     const int rng[2][2] = {{a, m}, {m, b}};
     // preorder ids: the subtree of `me` (range size s) owns [me, me + s - 1);
     // left child me + 1, right child me + (m - a)
@@ -577,12 +635,14 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
       sa[sp] = m;
       sb[sp] = b;
       sn[sp] = ref[1];
+      sd[sp] = dep + 1;
       ++sp;
     }
     if (m - a >= 2 && !leafpair[0]) {
       sa[sp] = a;
       sb[sp] = m;
       sn[sp] = ref[0];
+      sd[sp] = dep + 1;
       ++sp;
     }
   }
@@ -646,17 +706,18 @@ __global__ void scatter_kernel(const int32_t* __restrict__ pos_seg, const SSeg* 
   if (k == 0) pos_seg_out[np] = 2 * rank[sj] + (left ? 0 : 1);
 }
 
-__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level);
+__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level,
+                                                          int64_t sah_min);
 
 // per-segment accumulator reset and the packed split / SAH flags (positions
 // S .. s_max get flag 0 so the scan can run over the level's upper bound)
 __global__ void seg_init_kernel(const LevelState* __restrict__ ls, unsigned long long* __restrict__ bb,
                                 unsigned long long* __restrict__ cb, int32_t* __restrict__ pl,
                                 const SSeg* __restrict__ segs, int64_t s_max, int level,
-                                unsigned long long* __restrict__ flags) {
+                                unsigned long long* __restrict__ flags, int64_t sah_min) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t S = ls->S;
-  if (j <= s_max) flags[j] = j < S ? split_flags(segs, j, level) : 0ull;
+  if (j <= s_max) flags[j] = j < S ? split_flags(segs, j, level, sah_min) : 0ull;
   if (j >= S) return;
   for (int k = 0; k < 3; ++k) {  // ordered keys: min from ~0, max from 0
     bb[6 * j + k] = ~0ull;
@@ -669,13 +730,14 @@ __global__ void seg_init_kernel(const LevelState* __restrict__ ls, unsigned long
 }
 
 // packed flags: split (>= kSmall + 1 faces) << 32 | SAH-eligible
-__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level) {
+__device__ __forceinline__ unsigned long long split_flags(const SSeg* __restrict__ segs, int64_t j, int level,
+                                                          int64_t sah_min) {
   const int64_t n = segs[j].n;
   const unsigned long long split = n > kSmall ? 1ull : 0ull;  // 2..kSmall: finish_kernel
   // SAH only while the depth budget allows a median finish below
   int lg = 0;
   while ((int64_t(1) << lg) < n) ++lg;
-  const unsigned long long sah = (n >= kSahMin && level + 1 + lg + 2 <= kMaxDepth) ? 1ull : 0ull;
+  const unsigned long long sah = (n >= sah_min && level + 1 + lg + 2 <= kMaxDepth) ? 1ull : 0ull;
   return (split << 32) | sah;
 }
 
@@ -821,7 +883,17 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
   // segments of more than kSmall faces split), and at most nf / kSahMin
   // SAH-binned segments.
   const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(nf, 2 * (nf / (kSmall + 1)) + 2));
-  const int64_t max_sah = nf / kSahMin + 1;
+  // RR_SAH_MIN / RR_SAH_FIN (A/B): the smallest binned-SAH segment, and
+  // exact SAH (1) or object medians (0) inside finish_kernel's segments
+  static const int64_t sah_min = [] {
+    const char* e = std::getenv("RR_SAH_MIN");
+    return std::max<int64_t>(kSmall + 1, e ? std::atoll(e) : kSahMin);
+  }();
+  static const int fin_sah = [] {
+    const char* e = std::getenv("RR_SAH_FIN");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int64_t max_sah = nf / sah_min + 1;
   DevBuf<SSeg> segA, segB;
   DevBuf<int32_t> srank, sah_idx, axis, split, pl;
   DevBuf<unsigned long long> flags, franks;
@@ -873,7 +945,7 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
     const int64_t s_max = L == 0 ? 1 : std::min<int64_t>(max_seg, L < 62 ? (int64_t(1) << L) : max_seg);
     const int64_t sah_max = std::min<int64_t>(s_max, max_sah);
     // 1. bounds (one init launch for the per-segment accumulators)
-    seg_init_kernel<<<grid(s_max + 1), 256, 0, st>>>(ls.p, bb.p, cb.p, pl.p, segs, s_max, L, flags.p);
+    seg_init_kernel<<<grid(s_max + 1), 256, 0, st>>>(ls.p, bb.p, cb.p, pl.p, segs, s_max, L, flags.p, sah_min);
     bounds_kernel<<<grid(nf), 256, 0, st>>>(pos, perm, fb.p, cen.p, s->face_plane.p, nf, bb.p, cb.p, pl.p);
     if (L == 0) root_hdr_kernel<<<1, 32, 0, st>>>(bb.p, dh.p);
     // 2. split flags and SAH flags, both ranks from one 64-bit scan
@@ -895,7 +967,7 @@ void build_sah_tree(rr_scene* s, cudaStream_t st) {
     split_kernel<<<grid(32 * s_max), 256, 0, st>>>(segs, ls.p, srank.p, bb.p, cb.p, pl.p, sah_idx.p, bcnt.p, bbox.p, perm,
                                               cen.p, nf, s->snodes.p, dh.p, axis.p, split.p, nl.p, nsegs);
     finish_kernel<<<grid(s_max, 64), 64, 0, st>>>(segs, ls.p, perm, fb.p, cen.p, s->face_plane.p, nf, s->snodes.p,
-                                                  dh.p, top.p);
+                                                  dh.p, top.p, L, fin_sah);
     RR_LAUNCH_CHECK();
     // 4. stable partition of the three lists
     flag_kernel<<<grid(nf), 256, 0, st>>>(pos, segs, axis.p, split.p, nl.p, cb.p, cen.p, perm, nf, flag.p);

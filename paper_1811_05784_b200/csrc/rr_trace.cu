@@ -747,13 +747,51 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   RR_CUDA(cudaEventCreate(&e0));
   RR_CUDA(cudaEventCreate(&e1));
   unsigned long long hc[10];
+  static const int l2p = [] {
+    const char* e = std::getenv("RR_L2P");
+    return e ? std::atoi(e) : 0;
+  }();
   for (int attempt = 0; attempt < 2; ++attempt) {
     caps.alloc(capacity, st);
     p.caps = caps.p;
     p.cap_capacity = capacity;
     RR_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * 10, st));
     RR_CUDA(cudaEventRecord(e0, st));
-    kernel<<<grid, 128, smem, st>>>(p);
+    if (l2p > 0 && wide8) {
+      // A/B (RR_L2P): an L2 persisting window over the 8-wide nodes (1) or
+      // the leaf-ordered faces (2) for this launch
+      static bool limit_set = false;
+      cudaDeviceProp prop;
+      RR_CUDA(cudaGetDeviceProperties(&prop, s->ctx->device));
+      if (!limit_set) {
+        RR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize));
+        limit_set = true;
+      }
+      const void* base = l2p == 1 ? static_cast<const void*>(s->wnodes.p) : static_cast<const void*>(s->wtri.p);
+      const size_t bytes = l2p == 1 ? s->wnodes.n * sizeof(WNode) : s->wtri.n * sizeof(FaceTri);
+      const size_t win = std::min<size_t>(bytes, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+      at[0].val.accessPolicyWindow.num_bytes = win;
+      at[0].val.accessPolicyWindow.hitRatio =
+          std::min(1.0f, static_cast<float>(prop.persistingL2CacheMaxSize) / static_cast<float>(win));
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(128);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = st;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      if (attempt == 0 && std::getenv("RR_TIMING"))
+        std::fprintf(stderr, "[rr timing] L2 window %zu B (persisting max %d B, hit ratio %.3f)\n", win,
+                     prop.persistingL2CacheMaxSize, at[0].val.accessPolicyWindow.hitRatio);
+      RR_CUDA(cudaLaunchKernelEx(&lc, kernel, p));
+    } else {
+      kernel<<<grid, 128, smem, st>>>(p);
+    }
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaEventRecord(e1, st));
     s->ctx->launches++;
