@@ -10,11 +10,13 @@
 // ~80 B per 7 binary nodes, which keeps it L2-resident; the faces are copied
 // into leaf order so a node's leaf faces are contiguous.
 //
-// Build, level-synchronous from the root (one thread per wide node):
-//   expand: start from the binary node's two children and repeatedly open
-//           the internal child of largest surface area until 8 slots are
-//           used or only leaves remain (leaves are the SAH tree's own 1- or
-//           2-face leaves);
+// Build: a bottom-up SAH-optimal distribution pass over the binary tree
+// (dp_up_kernel), then level-synchronous from the root (one thread per wide
+// node):
+//   expand: the slots of the node's optimal distribution (dp_unfold; the
+//           A/B alternative opens the internal child of largest surface area
+//           until 8 slots are used); leaves are the SAH tree's own 1- or
+//           2-face leaves;
 //   scan:   exclusive sum of (internal children, leaf faces) per node, so a
 //           node's internal children are contiguous one level down and its
 //           leaf faces contiguous in `wtri`;
@@ -74,6 +76,142 @@ __device__ __forceinline__ float half_area(const Slot& s) {
 
 constexpr int32_t kEmptySlot = INT32_MIN;  // an unused slot of the 8 (ref)
 
+// ---- SAH-optimal collapse (RR_W8_DP; Ylitie, Karras and Laine 2017, sec.
+// 4.1, restated for fixed 1-2-face leaves).  For every binary node n and
+// i = 1..8, G(n, i) is the least SAH cost of covering n's subtree with at
+// most i slots of one wide node, n itself never a slot:
+//   F(c, k) = cost of child c as <= k slots = min(S(c), G(c, k)), with
+//             S(c) = A(c) c_node + G(c, 8) (c its own wide node) or
+//             A(c) c_face nfaces(c) (a leaf slot), G(c, 1) = inf;
+//   D(n, j) = min over k of F(left, k) + F(right, j - k);
+//   G(n, i) = min over 2 <= j <= i of D(n, j).
+// Bottom-up (the second child to finish processes its parent), then each
+// wide node unfolds G(n, 8) through the recorded choices (expand_kernel).
+constexpr float kInfCost = 3.0e38f;
+
+struct alignas(16) DpRec {
+  float g[8];       // G(n, 1..8)
+  uint32_t bestj;   // nibble i-1: the j <= i achieving G(n, i)
+  uint32_t argk;    // nibble j-1: the k of D(n, j)
+  uint32_t pad[2];
+};
+
+__global__ void dp_init_kernel(const TNode* __restrict__ tn, int32_t n_int, int32_t* __restrict__ parent,
+                               int32_t* __restrict__ need, int32_t* __restrict__ arrived) {
+  const int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= n_int) return;
+  const TNode t = tn[n];
+  int c = 0;
+  if (t.d.x >= 0) { parent[t.d.x] = n; ++c; }
+  if (t.d.y >= 0) { parent[t.d.y] = n; ++c; }
+  need[n] = c;
+  arrived[n] = 0;
+}
+
+// F(c, k), k = 1..8, of slot s (its box from the parent's TNode)
+__device__ __forceinline__ void dp_child(const Slot& s, const DpRec* __restrict__ rec, float c_node, float c_face,
+                                         float* F) {
+  const float A = half_area(s);
+  if (s.ref < 0) {
+    const float v = A * c_face * static_cast<float>(leaf_faces(s.ref));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) F[k] = v;
+    return;
+  }
+  float g[8];
+  const float4* r = reinterpret_cast<const float4*>(rec + s.ref);
+  const float4 g0 = __ldcg(r), g1 = __ldcg(r + 1);  // written by another thread of this launch
+  g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+  const float S = A * c_node + g[7];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) F[k] = fminf(S, g[k]);
+}
+
+// single slot for child s given k slots (the choice dp_child's min made)
+__device__ __forceinline__ bool dp_single(const Slot& s, const DpRec* __restrict__ rec, float c_node, int k) {
+  if (s.ref < 0 || k == 1) return true;
+  const float S = half_area(s) * c_node + rec[s.ref].g[7];
+  return S <= rec[s.ref].g[k - 1];
+}
+
+__global__ void dp_up_kernel(const TNode* __restrict__ tn, int32_t n_int, const int32_t* __restrict__ parent,
+                             const int32_t* __restrict__ need, int32_t* __restrict__ arrived, DpRec* __restrict__ rec,
+                             float c_node, float c_face) {
+  int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (n >= n_int || need[n] != 0) return;
+  for (;;) {
+    const TNode t = tn[n];
+    Slot sl, sr;
+    tnode_slot(t, 0, sl);
+    tnode_slot(t, 1, sr);
+    float FL[8], FR[8];
+    dp_child(sl, rec, c_node, c_face, FL);
+    dp_child(sr, rec, c_node, c_face, FR);
+    DpRec o;
+    o.g[0] = kInfCost;
+    o.bestj = 0;
+    o.argk = 0;
+    float gi = kInfCost;
+    uint32_t bj = 1;
+    for (int j = 2; j <= 8; ++j) {
+      float d = kInfCost;
+      int bk = 1;
+      for (int k = 1; k < j; ++k) {
+        const float v = FL[k - 1] + FR[j - k - 1];
+        if (v < d) {
+          d = v;
+          bk = k;
+        }
+      }
+      o.argk |= static_cast<uint32_t>(bk) << (4 * (j - 1));
+      if (d < gi) {
+        gi = d;
+        bj = static_cast<uint32_t>(j);
+      }
+      o.g[j - 1] = gi;
+      o.bestj |= bj << (4 * (j - 1));
+    }
+    rec[n] = o;
+    __threadfence();
+    const int32_t p = parent[n];
+    if (p < 0) return;
+    if (atomicAdd(arrived + p, 1) + 1 < need[p]) return;
+    __threadfence();
+    n = p;
+  }
+}
+
+// the slots of binary node n as one wide node: G(n, 8) unfolded
+__device__ __forceinline__ int dp_unfold(const TNode* __restrict__ tn, const DpRec* __restrict__ rec, int32_t root,
+                                         float c_node, Slot* s) {
+  int32_t st_n[8];
+  int st_i[8];
+  int sp = 0, cnt = 0;
+  st_n[sp] = root;
+  st_i[sp++] = 8;
+  while (sp > 0) {
+    --sp;
+    const int32_t n = st_n[sp];
+    const int i = st_i[sp];
+    const DpRec& r = rec[n];
+    const int j = static_cast<int>((r.bestj >> (4 * (i - 1))) & 0xfu);
+    const int k = static_cast<int>((r.argk >> (4 * (j - 1))) & 0xfu);
+    const TNode t = tn[n];
+    for (int side = 0; side < 2; ++side) {
+      Slot c;
+      tnode_slot(t, side, c);
+      const int kk = side == 0 ? k : j - k;
+      if (dp_single(c, rec, c_node, kk)) {
+        s[cnt++] = c;
+      } else {
+        st_n[sp] = c.ref;
+        st_i[sp++] = kk;
+      }
+    }
+  }
+  return cnt;
+}
+
 // expand frontier node i into <= 8 slots; packed (internal << 32 | faces).
 // order: place the children in the 8 slots by direction (Ylitie, Karras and
 // Laine 2017): slot s stands for the ray octant s (bit a set: negative
@@ -84,15 +222,20 @@ constexpr int32_t kEmptySlot = INT32_MIN;  // an unused slot of the 8 (ref)
 // group traversal).  Any slot order gives the same closest hits.
 __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __restrict__ frontier, int32_t n,
                               Slot* __restrict__ slots, int32_t* __restrict__ nslot,
-                              unsigned long long* __restrict__ packed, int order) {
+                              unsigned long long* __restrict__ packed, int order, const DpRec* __restrict__ rec,
+                              float c_node) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
-  const TNode t = tn[frontier[i]];
-  tnode_slot(t, 0, s[0]);
-  tnode_slot(t, 1, s[1]);
   int cnt = 2;
-  while (cnt < kW) {
+  if (rec) {
+    cnt = dp_unfold(tn, rec, frontier[i], c_node, s);
+  } else {
+    const TNode t = tn[frontier[i]];
+    tnode_slot(t, 0, s[0]);
+    tnode_slot(t, 1, s[1]);
+  }
+  while (!rec && cnt < kW) {
     int best = -1;
     float ba = -1.f;
     for (int k = 0; k < cnt; ++k)
@@ -290,6 +433,30 @@ void build_wide(rr_scene* s) {
     const char* e = std::getenv("RR_W8_ORDER");
     return e ? std::atoi(e) : 1;
   }();
+  // RR_W8_DP (A/B): SAH-optimal collapse (1; C5 visits per ray-bounce
+  // 19.73 -> 18.89, trace 468.2 -> 458.0 ms) or the greedy largest-area
+  // expansion (0).  The leaves are fixed, so the face-test cost only adds a
+  // constant: c_face 0.5 .. 3 built the same tree.
+  static const int use_dp = [] {
+    const char* e = std::getenv("RR_W8_DP");
+    return e ? std::atoi(e) : 1;
+  }();
+  const float c_node = 1.0f, c_face = 1.0f;
+  DevBuf<DpRec> rec;
+  if (use_dp) {
+    DevBuf<int32_t> parent, need, arrived;
+    parent.alloc(n_int, st);
+    need.alloc(n_int, st);
+    arrived.alloc(n_int, st);
+    rec.alloc(n_int, st);
+    RR_CUDA(cudaMemsetAsync(parent.p, 0xff, sizeof(int32_t) * n_int, st));
+    dp_init_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, parent.p, need.p, arrived.p);
+    RR_LAUNCH_CHECK();
+    dp_up_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, parent.p, need.p, arrived.p, rec.p, c_node,
+                                              c_face);
+    RR_LAUNCH_CHECK();
+    s->ctx->launches += 3;
+  }
   int32_t n = 1, base = 0, depth = 0;
   int64_t tri_done = 0;
   while (n > 0) {
@@ -297,7 +464,8 @@ void build_wide(rr_scene* s) {
     nslot.alloc(n, st);
     packed.alloc(n + 1, st);
     offs.alloc(n + 1, st);
-    expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p, slot_order);
+    expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p, slot_order,
+                                           use_dp ? rec.p : nullptr, c_node);
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaMemsetAsync(packed.p + n, 0, sizeof(unsigned long long), st));
     size_t need = 0;
