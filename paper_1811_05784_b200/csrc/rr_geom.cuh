@@ -169,6 +169,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #ifndef RR_HBUF
 #define RR_HBUF 0  // 8-wide tracer: face history buffered per 32-B sector (rr_trace_w8.cuh; A/B)
 #endif
+#ifndef RR_QEXACT
+#define RR_QEXACT 1  // 8-wide planes as fma(q - 1, A, B), no extra grid step (C5 458 -> 436 ms; 0: A/B)
+#endif
 #ifndef RR_FFMA2
 #define RR_FFMA2 1
 #endif
@@ -180,6 +183,17 @@ __device__ __forceinline__ float2 fma2(float f0, float f1, float a, float c) {
       "fma.rn.f32x2 D, F, A, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
       : "=f"(r.x), "=f"(r.y)
       : "f"(f0), "f"(f1), "f"(a), "f"(c));
+  return r;
+}
+
+// (f0 - (2^23 + 1), f1 - (2^23 + 1)) * a + c, two slots per packed FADD +
+// FFMA: f = 2^23 + q from the byte permute, so f - (2^23 + 1) = q - 1 exactly
+__device__ __forceinline__ float2 fma2q(float f0, float f1, float a, float c) {
+  float2 r;
+  asm("{\n\t.reg .b64 F, K, A, C, D;\n\tmov.b64 F, {%2, %3};\n\tmov.b64 K, {%6, %6};\n\tmov.b64 A, {%4, %4};\n\t"
+      "mov.b64 C, {%5, %5};\n\tadd.rn.f32x2 F, F, K;\n\tfma.rn.f32x2 D, F, A, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(f0), "f"(f1), "f"(a), "f"(c), "f"(-8388609.0f));
   return r;
 }
 
@@ -904,10 +918,13 @@ __device__ __forceinline__ bool test_leaf_w(const FaceTri* __restrict__ wtri, in
 // One 8-wide node visit (WNode, rr_wide.cu) for one lane's ray: entry
 // distances of the 8 slots, the mask of slots hit within tmax and not
 // culled, and the slot refs.  A plane of slot k is p + (q - 1) * 2^e; with
-// F = 2^23 + q (one byte permute builds its fp32 bits) the slab distance is
-// fma(F, A, C), A = 2^e * inv (exact: a power of two times inv),
-// C = fl(B - (2^23 + 1) * A), B = fma(p, inv, -o * inv).  The builder's
-// extra grid step on each side covers C's rounding (<= |A| / 2).
+// F = 2^23 + q (one byte permute builds its fp32 bits), q - 1 = F - (2^23 +
+// 1) exactly (one packed FADD per two slots) and the slab distance is
+// fma(q - 1, A, B), A = 2^e * inv (exact: a power of two times inv),
+// B = fma(p, inv, -o * inv); the builder's margin covers the two roundings.
+// (RR_QEXACT 0: fma(F, A, C), C = fl(B - (2^23 + 1) * A), one FADD less per
+// two slots but C's rounding of up to half a grid step needs an extra grid
+// step on each side of every slot box: 5 % slower on C5.)
 struct WVisit {
   float t[8];
   uint32_t hit;      // slots hit
@@ -943,9 +960,17 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
   const float ax = __uint_as_float((hw & 0xffu) << 23) * r.ix;
   const float ay = __uint_as_float(((hw >> 8) & 0xffu) << 23) * r.iy;
   const float az = __uint_as_float(((hw >> 16) & 0xffu) << 23) * r.iz;
+#if RR_QEXACT
+  const float cx = __fmaf_rn(hh.x, r.ix, r.nx);
+  const float cy = __fmaf_rn(hh.y, r.iy, r.ny);
+  const float cz = __fmaf_rn(hh.z, r.iz, r.nz);
+#define RR_WFMA2 fma2q
+#else
   const float cx = __fmaf_rn(-8388609.0f, ax, __fmaf_rn(hh.x, r.ix, r.nx));
   const float cy = __fmaf_rn(-8388609.0f, ay, __fmaf_rn(hh.y, r.iy, r.ny));
   const float cz = __fmaf_rn(-8388609.0f, az, __fmaf_rn(hh.z, r.iz, r.nz));
+#define RR_WFMA2 fma2
+#endif
   // near / far plane words per axis from the ray's octant
   const uint32_t nx0 = px ? qx.x : qx.z, nx1 = px ? qx.y : qx.w, fx0 = px ? qx.z : qx.x, fx1 = px ? qx.w : qx.y;
   const uint32_t ny0 = py ? qy.x : qy.z, ny1 = py ? qy.y : qy.w, fy0 = py ? qy.z : qy.x, fy1 = py ? qy.w : qy.y;
@@ -960,12 +985,12 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
     const uint32_t wnx = k < 4 ? nx0 : nx1, wfx = k < 4 ? fx0 : fx1;
     const uint32_t wny = k < 4 ? ny0 : ny1, wfy = k < 4 ? fy0 : fy1;
     const uint32_t wnz = k < 4 ? nz0 : nz1, wfz = k < 4 ? fz0 : fz1;
-    const float2 nx = fma2(wbyte(wnx, k), wbyte(wnx, k + 1), ax, cx);
-    const float2 ny = fma2(wbyte(wny, k), wbyte(wny, k + 1), ay, cy);
-    const float2 nz = fma2(wbyte(wnz, k), wbyte(wnz, k + 1), az, cz);
-    const float2 fx = fma2(wbyte(wfx, k), wbyte(wfx, k + 1), ax, cx);
-    const float2 fy = fma2(wbyte(wfy, k), wbyte(wfy, k + 1), ay, cy);
-    const float2 fz = fma2(wbyte(wfz, k), wbyte(wfz, k + 1), az, cz);
+    const float2 nx = RR_WFMA2(wbyte(wnx, k), wbyte(wnx, k + 1), ax, cx);
+    const float2 ny = RR_WFMA2(wbyte(wny, k), wbyte(wny, k + 1), ay, cy);
+    const float2 nz = RR_WFMA2(wbyte(wnz, k), wbyte(wnz, k + 1), az, cz);
+    const float2 fx = RR_WFMA2(wbyte(wfx, k), wbyte(wfx, k + 1), ax, cx);
+    const float2 fy = RR_WFMA2(wbyte(wfy, k), wbyte(wfy, k + 1), ay, cy);
+    const float2 fz = RR_WFMA2(wbyte(wfz, k), wbyte(wfz, k + 1), az, cz);
 #if RR_HIT2
     // entry clamped at 0 and exit at tmax (>= 0) inside the 3-input min / max:
     // max(tn, 0) <= min(tf, tmax) is the test below, one compare per slot
@@ -990,14 +1015,16 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
     const uint32_t wnx = k < 4 ? nx0 : nx1, wfx = k < 4 ? fx0 : fx1;
     const uint32_t wny = k < 4 ? ny0 : ny1, wfy = k < 4 ? fy0 : fy1;
     const uint32_t wnz = k < 4 ? nz0 : nz1, wfz = k < 4 ? fz0 : fz1;
-    const float tn = fmax3(__fmaf_rn(wbyte(wnx, k), ax, cx), __fmaf_rn(wbyte(wny, k), ay, cy),
-                           __fmaf_rn(wbyte(wnz, k), az, cz));
-    const float tf = fmin3(__fmaf_rn(wbyte(wfx, k), ax, cx), __fmaf_rn(wbyte(wfy, k), ay, cy),
-                           __fmaf_rn(wbyte(wfz, k), az, cz));
+    const float q0 = RR_QEXACT ? 8388609.0f : 0.0f;
+    const float tn = fmax3(__fmaf_rn(wbyte(wnx, k) - q0, ax, cx), __fmaf_rn(wbyte(wny, k) - q0, ay, cy),
+                           __fmaf_rn(wbyte(wnz, k) - q0, az, cz));
+    const float tf = fmin3(__fmaf_rn(wbyte(wfx, k) - q0, ax, cx), __fmaf_rn(wbyte(wfy, k) - q0, ay, cy),
+                           __fmaf_rn(wbyte(wfz, k) - q0, az, cz));
     v.t[k] = tn;
     if (tn <= fminf(tf, tmax) && tf >= 0.0f) hit |= 1u << k;
   }
 #endif
+#undef RR_WFMA2
   v.hit = hit & bits & 0xffu & ~cull;
   v.imask = hw >> 24;
   v.child = mm.x;

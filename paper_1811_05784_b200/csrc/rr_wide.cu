@@ -29,13 +29,13 @@
 // gives identical results.  Each slot's box is the binary node's
 // conservative fp32 child box (exact box + eps, rounded outward; eps =
 // scale * 2^-19 bounds the fp32 slab error, rr_geom.cuh box_enter) widened
-// by another eps/4 and rounded outward onto the grid, one more grid step
-// on each side (quant_axis), evaluated in fp64 on the exact grid values.  The
-// node traversal evaluates a plane as fma(2^23 + q, A, C) (rr_geom.cuh
-// wslab): its rounding of C is at most half a grid step (covered by the
-// extra step), the other two roundings (B = fma(p, inv, -o * inv) and the
-// final fma) are below 6 * scale * 2^-24 each in space units (|q * 2^e|,
-// |p - o| <= 6 scale), < 0.2 eps together, inside the extra eps/4.
+// by another eps/4 and rounded outward onto the grid (quant_axis),
+// evaluated in fp64 on the exact grid values.  The node traversal evaluates
+// a plane as fma(q - 1, A, B) (rr_geom.cuh visit_w8; q - 1 is exact, one
+// packed FADD from the byte-permuted 2^23 + q), so two roundings remain,
+// B = fma(p, inv, -o * inv) and the final fma, each below 6 * scale * 2^-24
+// in space units (|q * 2^e|, |p - o| <= 6 scale): < 0.2 eps together,
+// inside the extra eps/4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -299,11 +299,14 @@ __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __res
 }
 
 // Grid of one axis: plane(q) = p + (q - 1) * 2^(e-127), q in [0, 255]
-// (p fp32, exact in fp64).  Each slot gets q_lo one step below the floor and
-// q_hi one step above the ceiling of its margin-widened box: the traversal
-// evaluates t = fma(2^23 + q, A, C) with A = 2^(e-127) * inv (exact) and
-// C = fl(B - (2^23 + 1) A), whose rounding is at most |A| / 2, i.e. half a
-// grid step in space units (rr_geom.cuh wslab).  Returns the biased exponent.
+// (p fp32, exact in fp64).  Each slot gets the floor / ceiling of its
+// margin-widened box on the grid: the traversal evaluates t = fma(q - 1, A,
+// B) with A = 2^(e-127) * inv (exact), whose error the margin covers.
+// RR_QEXACT 0 (A/B, round 2 before): t = fma(2^23 + q, A, C) with
+// C = fl(B - (2^23 + 1) A), whose rounding is up to half a grid step, so
+// each slot got one more grid step below and above (C5: 18.9 instead of
+// 18.0 node visits and 4.7 instead of 4.4 face tests per ray-bounce,
+// 458 instead of 436 ms).  Returns the biased exponent.
 __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int ax, double m, float* p_out, uint32_t* lo8,
                                                uint32_t* hi8) {
   double lo = 1e300, hi = -1e300;
@@ -314,19 +317,20 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int ax, double m, 
   }
   const float p = __double2float_rd(lo);
   const double pd = static_cast<double>(p);
-  // smallest power of two with (hi - p) <= 253 * scale (q = plane step + 1,
-  // one step of slack below and above)
-  int e = static_cast<int>(ceil(log2((hi - pd) / 253.0)));
-  while (ldexp(253.0, e) < hi - pd) ++e;
-  while (e > -126 && ldexp(253.0, e - 1) >= hi - pd) --e;
+  // smallest power of two with (hi - p) <= 254 * scale (q = plane step + 1;
+  // RR_QEXACT 0: 253, one step of slack below and above)
+  const double span = RR_QEXACT ? 254.0 : 253.0;
+  int e = static_cast<int>(ceil(log2((hi - pd) / span)));
+  while (ldexp(span, e) < hi - pd) ++e;
+  while (e > -126 && ldexp(span, e - 1) >= hi - pd) --e;
   e = max(e, -126);
   const double sc = ldexp(1.0, e);
   lo8[0] = lo8[1] = hi8[0] = hi8[1] = 0;
   for (int k = 0; k < kW; ++k) {
     if (s[k].ref == kEmptySlot) continue;
-    // q - 1 = floor(..) - 1 and ceil(..) + 1
-    double ql = floor((static_cast<double>(s[k].b[2 * ax]) - m - pd) / sc);
-    double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc) + 2.0;
+    // q - 1 = floor(..) - 1 and ceil(..) + 1 (RR_QEXACT: floor(..) and ceil(..))
+    double ql = floor((static_cast<double>(s[k].b[2 * ax]) - m - pd) / sc) + (RR_QEXACT ? 1.0 : 0.0);
+    double qh = ceil((static_cast<double>(s[k].b[2 * ax + 1]) + m - pd) / sc) + (RR_QEXACT ? 1.0 : 2.0);
     ql = fmin(fmax(ql, 0.0), 255.0);
     qh = fmin(fmax(qh, 0.0), 255.0);
     lo8[k >> 2] |= static_cast<uint32_t>(ql) << (8 * (k & 3));
