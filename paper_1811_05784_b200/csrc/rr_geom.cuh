@@ -172,6 +172,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #ifndef RR_QEXACT
 #define RR_QEXACT 1  // 8-wide planes as fma(q - 1, A, B), no extra grid step (C5 458 -> 436 ms; 0: A/B)
 #endif
+#ifndef RR_QMANT
+#define RR_QMANT 2  // 8-wide grid scales with 2 mantissa bits (0: powers of two; A/B)
+#endif
 #ifndef RR_FFMA2
 #define RR_FFMA2 1
 #endif
@@ -920,8 +923,10 @@ __device__ __forceinline__ bool test_leaf_w(const FaceTri* __restrict__ wtri, in
 // culled, and the slot refs.  A plane of slot k is p + (q - 1) * 2^e; with
 // F = 2^23 + q (one byte permute builds its fp32 bits), q - 1 = F - (2^23 +
 // 1) exactly (one packed FADD per two slots) and the slab distance is
-// fma(q - 1, A, B), A = 2^e * inv (exact: a power of two times inv),
-// B = fma(p, inv, -o * inv); the builder's margin covers the two roundings.
+// fma(q - 1, A, B), A = scale * inv, B = fma(p, inv, -o * inv); the
+// builder's margin covers the three roundings.  The per-axis grid scale is
+// 2^e (1 + j / 4) (RR_QMANT 2 mantissa bits in a 10-bit field whose shift
+// is the fp32 bits; powers of two: C5 17.9 -> 18.0 visits, 434 -> 437 ms).
 // (RR_QEXACT 0: fma(F, A, C), C = fl(B - (2^23 + 1) * A), one FADD less per
 // two slots but C's rounding of up to half a grid step needs an extra grid
 // step on each side of every slot box: 5 % slower on C5.)
@@ -957,9 +962,12 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
   const uint4 qy = __ldg(reinterpret_cast<const uint4*>(q + 3));
   const uint4 qz = __ldg(reinterpret_cast<const uint4*>(q + 4));
   const uint32_t hw = __float_as_uint(hh.w);
-  const float ax = __uint_as_float((hw & 0xffu) << 23) * r.ix;
-  const float ay = __uint_as_float(((hw >> 8) & 0xffu) << 23) * r.iy;
-  const float az = __uint_as_float(((hw >> 16) & 0xffu) << 23) * r.iz;
+  // grid scales: (8 + RR_QMANT)-bit fields = the fp32 bits of 2^(e-127) (1 + j / 2^M)
+  constexpr int kF = 8 + RR_QMANT;
+  constexpr uint32_t kFM = (1u << kF) - 1u;
+  const float ax = __uint_as_float((hw & kFM) << (23 - RR_QMANT)) * r.ix;
+  const float ay = __uint_as_float(((hw >> kF) & kFM) << (23 - RR_QMANT)) * r.iy;
+  const float az = __uint_as_float(((hw >> (2 * kF)) & kFM) << (23 - RR_QMANT)) * r.iz;
 #if RR_QEXACT
   const float cx = __fmaf_rn(hh.x, r.ix, r.nx);
   const float cy = __fmaf_rn(hh.y, r.iy, r.ny);
@@ -1026,7 +1034,7 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
 #endif
 #undef RR_WFMA2
   v.hit = hit & bits & 0xffu & ~cull;
-  v.imask = hw >> 24;
+  v.imask = bits >> 24;
   v.child = mm.x;
   v.tri = mm.y;
   v.leafm = (bits & 0xffu) & ~v.imask;

@@ -32,10 +32,12 @@
 // by another eps/4 and rounded outward onto the grid (quant_axis),
 // evaluated in fp64 on the exact grid values.  The node traversal evaluates
 // a plane as fma(q - 1, A, B) (rr_geom.cuh visit_w8; q - 1 is exact, one
-// packed FADD from the byte-permuted 2^23 + q), so two roundings remain,
-// B = fma(p, inv, -o * inv) and the final fma, each below 6 * scale * 2^-24
-// in space units (|q * 2^e|, |p - o| <= 6 scale): < 0.2 eps together,
-// inside the extra eps/4.
+// packed FADD from the byte-permuted 2^23 + q): three roundings, A = grid *
+// inv, B = fma(p, inv, -o * inv) and the final fma, each below 6 * scale *
+// 2^-24 = 0.19 eps in space units (|(q - 1) * grid|, |p - o| <= 6 scale),
+// where box_enter has one.  The binary box's eps covers box_enter's error
+// (o, inv, o * inv and the fma: below eps / 2, rr_geom.cuh), so the two
+// extra roundings (0.38 eps) stay inside the rest of eps plus the eps/4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -324,7 +326,20 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int ax, double m, 
   while (ldexp(span, e) < hi - pd) ++e;
   while (e > -126 && ldexp(span, e - 1) >= hi - pd) --e;
   e = max(e, -126);
-  const double sc = ldexp(1.0, e);
+  // RR_QMANT mantissa bits: the smallest 2^(e-1) (1 + j / 2^M) that still
+  // spans the box (a finer grid than the power of two, same decode cost)
+  uint32_t field = static_cast<uint32_t>(e + 127) << RR_QMANT;
+  double sc = ldexp(1.0, e);
+  if (RR_QMANT > 0 && e - 1 >= -126) {
+    for (int j = 1; j < (1 << RR_QMANT); ++j) {
+      const double c = ldexp(1.0 + static_cast<double>(j) / (1 << RR_QMANT), e - 1);
+      if (c * span >= hi - pd) {
+        sc = c;
+        field = (static_cast<uint32_t>(e - 1 + 127) << RR_QMANT) | static_cast<uint32_t>(j);
+        break;
+      }
+    }
+  }
   lo8[0] = lo8[1] = hi8[0] = hi8[1] = 0;
   for (int k = 0; k < kW; ++k) {
     if (s[k].ref == kEmptySlot) continue;
@@ -337,7 +352,7 @@ __device__ __forceinline__ uint32_t quant_axis(const Slot* s, int ax, double m, 
     hi8[k >> 2] |= static_cast<uint32_t>(qh) << (8 * (k & 3));
   }
   *p_out = p;
-  return static_cast<uint32_t>(e + 127);
+  return field;
 }
 
 __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __restrict__ nslot,
@@ -395,9 +410,13 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
     }
   }
   atomicMax(bound, a);
-  atomicMax(emax, static_cast<int32_t>(max(e[0], max(e[1], e[2]))));
-  w.h = make_float4(p[0], p[1], p[2], __int_as_float(static_cast<int>(e[0] | (e[1] << 8) | (e[2] << 16) |
-                                                                       (imask << 24))));
+  atomicMax(emax, static_cast<int32_t>(max(e[0], max(e[1], e[2])) >> RR_QMANT));
+  // h.w: the three (8 + RR_QMANT)-bit scale fields (RR_QMANT 0: the
+  // internal mask in the top byte too)
+  constexpr int kF = 8 + RR_QMANT;
+  w.h = make_float4(p[0], p[1], p[2],
+                    __int_as_float(static_cast<int>(e[0] | (e[1] << kF) | (e[2] << (2 * kF)) |
+                                                    (RR_QMANT == 0 ? imask << 24 : 0u))));
   // bits: valid | pair << 8 | cull << 16 | internal << 24 (the internal mask
   // also in h.w, next to the exponents)
   w.m = make_int4(next_base + ci, ti, plane, static_cast<int>(valid | (pair << 8) | (cull << 16) | (imask << 24)));
