@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <vector>
 
@@ -479,6 +480,19 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
   if (n < 2 || n > kSmall) return;
   int32_t f[kSmall];
   for (int i = 0; i < n; ++i) f[i] = perm0[sg.b + i];
+  // fp32 copies of the faces' centroids and boxes by local slot (sl[i] is
+  // the slot of f[i]): the split choice only shapes the tree, the node boxes
+  // are still the exact fp64 ones (range_box)
+  float lc[kSmall][3], lb[kSmall][6];
+  uint8_t sl[kSmall];
+  for (int i = 0; i < n; ++i) {
+    sl[i] = static_cast<uint8_t>(i);
+    for (int k = 0; k < 3; ++k) {
+      lc[i][k] = static_cast<float>(cen[3 * f[i] + k]);
+      lb[i][k] = static_cast<float>(fb[6 * f[i] + k]);
+      lb[i][3 + k] = static_cast<float>(fb[6 * f[i] + 3 + k]);
+    }
+  }
   const int32_t base = static_cast<int32_t>(nf - 1 - static_cast<int64_t>(atomicAdd(top, (unsigned long long)(n - 1))) -
                                             (n - 1));
   // range [a, b) of f -> AABB (exact, fp64) and common plane id
@@ -533,48 +547,55 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
       child_slot(tn + sg.parent, sg.side, lo, hi, eps, base, plane);
     }
   }
-  // insertion sort of f[a, b) by centroid on axis ax (ties by face id)
+  // insertion sort of f[a, b) by (fp32) centroid on axis ax (ties by face id)
   auto sort_axis = [&](int a, int b, int ax) {
     for (int x = a + 1; x < b; ++x) {
       const int32_t v = f[x];
-      const double cv = cen[3 * v + ax];
+      const uint8_t vs = sl[x];
+      const float cv = lc[vs][ax];
       int y = x - 1;
-      while (y >= a && (cen[3 * f[y] + ax] > cv || (cen[3 * f[y] + ax] == cv && f[y] > v))) {
+      while (y >= a && (lc[sl[y]][ax] > cv || (lc[sl[y]][ax] == cv && f[y] > v))) {
         f[y + 1] = f[y];
+        sl[y + 1] = sl[y];
         --y;
       }
       f[y + 1] = v;
+      sl[y + 1] = vs;
     }
+  };
+  auto half_area_f = [](const float* lo, const float* hi) {
+    const float x = hi[0] - lo[0], y = hi[1] - lo[1], z = hi[2] - lo[2];
+    return x * y + y * z + z * x;
   };
   // exact SAH over the sorted centroid orders of the three axes (fin_sah):
   // the split position m of [a, b) minimising A(left) |left| + A(right)
   // |right|, twins kept together; f[a, b) left sorted on the chosen axis.
   // Returns false when no position qualifies.
   auto sah_exact = [&](int a, int b, int* m_out) -> bool {
-    double best = HUGE_VAL;
+    float best = FLT_MAX;
     int bax = -1, bm = -1;
     for (int ax = 0; ax < 3; ++ax) {
       sort_axis(a, b, ax);
-      double ra[kSmall];
-      double lo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, hi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+      float ra[kSmall];
+      float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
       for (int i = b - 1; i > a; --i) {  // ra[i - a]: area of f[i, b)
         for (int k = 0; k < 3; ++k) {
-          lo[k] = fmin(lo[k], fb[6 * f[i] + k]);
-          hi[k] = fmax(hi[k], fb[6 * f[i] + 3 + k]);
+          lo[k] = fminf(lo[k], lb[sl[i]][k]);
+          hi[k] = fmaxf(hi[k], lb[sl[i]][3 + k]);
         }
-        ra[i - a] = half_area(lo, hi);
+        ra[i - a] = half_area_f(lo, hi);
       }
       for (int k = 0; k < 3; ++k) {
-        lo[k] = HUGE_VAL;
-        hi[k] = -HUGE_VAL;
+        lo[k] = FLT_MAX;
+        hi[k] = -FLT_MAX;
       }
       for (int i = a + 1; i < b; ++i) {  // split before position i
         for (int k = 0; k < 3; ++k) {
-          lo[k] = fmin(lo[k], fb[6 * f[i - 1] + k]);
-          hi[k] = fmax(hi[k], fb[6 * f[i - 1] + 3 + k]);
+          lo[k] = fminf(lo[k], lb[sl[i - 1]][k]);
+          hi[k] = fmaxf(hi[k], lb[sl[i - 1]][3 + k]);
         }
         if (twins_at(f[i - 1], f[i], cen)) continue;
-        const double c = half_area(lo, hi) * (i - a) + ra[i - a] * (b - i);
+        const float c = half_area_f(lo, hi) * (i - a) + ra[i - a] * (b - i);
         if (c < best) {
           best = c;
           bax = ax;
@@ -607,11 +628,11 @@ __global__ void finish_kernel(const SSeg* __restrict__ segs, const LevelState* _
     const bool sah_ok = fin_sah && level + dep + lg + 2 <= kMaxDepth;
     if (!(sah_ok && b - a > 2 && sah_exact(a, b, &m))) {
       // longest centroid extent, then insertion sort of f[a, b) on that axis
-      double clo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, chi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+      float clo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, chi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
       for (int i = a; i < b; ++i)
         for (int k = 0; k < 3; ++k) {
-          clo[k] = fmin(clo[k], cen[3 * f[i] + k]);
-          chi[k] = fmax(chi[k], cen[3 * f[i] + k]);
+          clo[k] = fminf(clo[k], lc[sl[i]][k]);
+          chi[k] = fmaxf(chi[k], lc[sl[i]][k]);
         }
       int ax = 0;
       for (int k = 1; k < 3; ++k)
