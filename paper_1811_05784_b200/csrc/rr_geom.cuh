@@ -172,6 +172,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #ifndef RR_QEXACT
 #define RR_QEXACT 1  // 8-wide planes as fma(q - 1, A, B), no extra grid step (C5 458 -> 436 ms; 0: A/B)
 #endif
+#ifndef RR_COOP
+#define RR_COOP 1  // 8-wide tracer: batched leaf tests spread over the whole warp (C5 434.7 -> 428.8 ms; 0: A/B)
+#endif
 #ifndef RR_QMANT
 #define RR_QMANT 2  // 8-wide grid scales with 2 mantissa bits (0: powers of two; A/B)
 #endif

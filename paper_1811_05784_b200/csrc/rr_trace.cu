@@ -43,6 +43,13 @@ constexpr int kSms8 = RR_SMS8;
 #ifndef RR_MINB8
 #define RR_MINB8 8  // blocks of 128 per SM (64 registers)
 #endif
+#ifndef RR_STUCKD8
+#define RR_STUCKD8 4  // leaf batch when 1/STUCKD of the searching lanes wait on their stashed leaf
+#endif
+#ifndef RR_HOLDD8
+#define RR_HOLDD8 1  // ... or 1/HOLDD of them hold one (with RR_COOP, STUCKD / HOLDD 4 / 1 427.5 ms,
+                     // 4 / 2 428.8, 4 / 4 437.6, 2 / 2 435.9, 8 / 2 440.8, 3 / 1 431.3, 5 / 1 428.5, 6 / 1 431.2)
+#endif
 #ifndef RR_DONET8
 #define RR_DONET8 6  // lanes done before a warp leaves traversal for shading
 #endif
@@ -676,12 +683,12 @@ rr_trace_result* run_trace(rr_scene* s, const rr_source* src, const rr_receiver*
   // After: 587 (MINB 9 592; 10: 620; 12: 692).  Group kernel: DONET 4 / 8
   // 535 / 527, STUCKD 2 / 8 529 / 547, HOLDD 4 547, MINB 9 (56 registers)
   // 833, 16 stack entries all in shared memory (7 blocks per SM) 752.
-  KFn w8k = cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, true, kSms8, 4, 2> : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, false, kSms8, 4, 2>;
+  KFn w8k = cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, true, kSms8, RR_STUCKD8, RR_HOLDD8> : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8, false, kSms8, RR_STUCKD8, RR_HOLDD8>;
   if (grp8)
-    w8k = w8v == 2 ? (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, 4, 2, true, false>
-                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, 4, 2, true, false>)
-                   : (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, 4, 2, true, true>
-                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, 4, 2, true, true>);
+    w8k = w8v == 2 ? (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, RR_STUCKD8, RR_HOLDD8, true, false>
+                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, RR_STUCKD8, RR_HOLDD8, true, false>)
+                   : (cnt ? trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, true, kSms8, RR_STUCKD8, RR_HOLDD8, true, true>
+                          : trace_kernel_w8<RR_MINB8, RR_DONET8, 1, kStack8G, false, kSms8, RR_STUCKD8, RR_HOLDD8, true, true>);
   auto dfk = wide8 ? w8k : wide4 ? trace_kernel<3, 8> : trace_kernel<1, 7, false, 16, -2, false, 16, 0, false, 2, false>;
 #ifdef RR_DIAG
   dfk = diag_trace_kernel(df_env, s->s4nodes.p != nullptr, dfk);

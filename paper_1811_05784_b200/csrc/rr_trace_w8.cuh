@@ -16,9 +16,9 @@
 //    the warp-aggregated capture append, reflect, write the face history,
 //    terminate, take new rays from the global counter and start their next
 //    query.
-// Leaves are tested (one batch, all lanes holding one) once a quarter of
-// the searching lanes are stuck behind their stashed leaf or half hold one
-// (STUCKD 4, HOLDD 2: C5 562 -> 549 ms against a half / a half).
+// Leaves are tested (one batch, all stashed faces spread over the warp,
+// RR_COOP) once a quarter of the searching lanes are stuck behind their
+// stashed leaf (STUCKD 4; HOLDD 1: or all of them hold one).
 // Without the batching a warp's bounce lasts as long as its slowest lane's
 // query: on C5 (17 node visits per ray-bounce on average) only ~7 of 32
 // lanes were active per node visit.
@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
     int32_t ray, steps, bounces, pad;
   };
   __shared__ LaneState s_lane[128];
+#if RR_COOP
+  __shared__ uint8_t s_item[128];  // per warp: lane (| 32 for a second face) of each stashed face
+#endif
   LaneState& ls = s_lane[threadIdx.x];
 #if RR_HBUF
   // face history: each lane's current 32-B sector of hist[] in shared memory
@@ -467,6 +470,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           prefetch_leaf(p.wtri, leaf);
           if constexpr (GRP) gtake(); else pop();
         }
+#if !RR_COOP
         // batched fp64 leaf tests (closest_hit_pl's vote)
         const unsigned act = __activemask();
         const unsigned hv = __ballot_sync(act, leaf != 0);
@@ -491,7 +495,79 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           }
         }
         if (node == kDone && leaf == 0) searching = false;  // query done: best holds the hit
+#endif
       }
+#if RR_COOP
+      // batched fp64 leaf tests (closest_hit_pl's vote), spread over the
+      // whole warp: the stashed leaves' faces are numbered (first faces of
+      // the holding lanes in lane order, then the second faces of the pair
+      // leaves), lane j tests face j against its owner's ray (read from
+      // the owner's shared-memory lane state) and the owners collect their
+      // results by shuffles, in the leaf's face order (test_leaf_w's rule).
+      // Before, only the holding lanes ran the fp64 tests (a quarter to a
+      // half of the warp, one loop trip per face of the largest leaf).
+      {
+        const unsigned hv = __ballot_sync(0xffffffffu, leaf != 0);
+        if (hv != 0) {
+          const bool can = searching && is_inner(node);
+          const bool must = leaf != 0 && !can;
+          const unsigned mv = __ballot_sync(0xffffffffu, must);
+          const unsigned cv = __ballot_sync(0xffffffffu, can);
+          const int na = __popc(__ballot_sync(0xffffffffu, searching));
+          if (STUCKD * __popc(mv) >= na || cv == 0 || HOLDD * __popc(hv) >= na) {
+            const bool two = leaf != 0 && leaf_faces(leaf) == 2;
+            const unsigned h2 = __ballot_sync(0xffffffffu, two);
+            const int c1 = __popc(hv), c2 = __popc(h2);
+            const int ia = __popc(hv & lt_mask), ib = c1 + __popc(h2 & lt_mask);
+            if (CNT && leaf != 0) st_cnt[1] += leaf_faces(leaf);
+            if (c1 + c2 <= 32) {
+              uint8_t* it = s_item + (threadIdx.x & ~31u);
+              if (leaf != 0) it[ia] = static_cast<uint8_t>(lane);
+              if (two) it[ib] = static_cast<uint8_t>(lane | 32);
+              __syncwarp();
+              const int own = lane < c1 + c2 ? it[lane] : 0;
+              const int32_t ol = __shfl_sync(0xffffffffu, leaf, own & 31);
+              double t = -1.0;
+              int32_t f = -1;
+              if (lane < c1 + c2) {
+                const LaneState& os = s_lane[(threadIdx.x & ~31u) + (own & 31)];
+                RR_DCHECK(leaf_face(ol) + leaf_faces(ol) <= p.nf);
+                t = mt_delta_w(p.wtri, leaf_face(ol) + (own >> 5), os.o, os.d, &f);
+              }
+              const double ta = __shfl_sync(0xffffffffu, t, ia & 31), tb = __shfl_sync(0xffffffffu, t, ib & 31);
+              const int32_t fa = __shfl_sync(0xffffffffu, f, ia & 31), fb = __shfl_sync(0xffffffffu, f, ib & 31);
+              __syncwarp();
+              if (leaf != 0) {
+                bool better = false;
+                if (ta > 0.0 && (best.face < 0 || ta < best.delta || (ta == best.delta && fa < best.face))) {
+                  best.delta = ta;
+                  best.face = fa;
+                  better = true;
+                }
+                if (two && tb > 0.0 && (best.face < 0 || tb < best.delta || (tb == best.delta && fb < best.face))) {
+                  best.delta = tb;
+                  best.face = fb;
+                  better = true;
+                }
+                if (better) tbest = prune_bound(best.delta, r.shift);
+              }
+            } else if (leaf != 0) {  // more than 32 faces: every lane its own leaf
+              RR_DCHECK(leaf_face(leaf) + leaf_faces(leaf) <= p.nf);
+              if (test_leaf_w(p.wtri, leaf, o, d, best)) tbest = prune_bound(best.delta, r.shift);
+            }
+            if (leaf != 0) {
+              leaf = 0;
+              if (node < 0) {  // the leaf that waited for the slot
+                leaf = node;
+                prefetch_leaf(p.wtri, leaf);
+                if constexpr (GRP) gtake(); else pop();
+              }
+            }
+          }
+        }
+        if (searching && node == kDone && leaf == 0) searching = false;  // query done: best holds the hit
+      }
+#endif
       const unsigned sv = __ballot_sync(0xffffffffu, searching);
       const unsigned wv = __ballot_sync(0xffffffffu, has_ray && !searching);
       if (sv == 0 || __popc(wv) >= DONET) break;
