@@ -466,10 +466,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 conservative box filter)",
             "data": "synthetic (seeded splitmix64 scene; no dataset)",
-            "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {n_total} rays, "
-                                   f"{scene.max_iterations} refl, {len(scene.receivers)} receiver(s)",
-                       "rays_per_gpu": -(-scene.ray_count // world), "parallelism": f"rays block-cyclic x{world}",
-                       "l2": "flushed between timed steps (512 MB write)"},
+            "config": bench_config(args, scene),
+            "run": {"rays_per_gpu": -(-scene.ray_count // world), "parallelism": f"rays block-cyclic x{world}",
+                    "l2": "flushed between timed steps (512 MB write)"},
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": round(t.item() / args.steps, 3),
                     "stage_ms": {k: round(v, 3) for k, v in breakdown.items()}},
@@ -483,6 +482,14 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return out
+
+
+def bench_config(args, scene):
+    """The workload both arms report (identical dicts, so the driver can
+    match the lines); how each arm ran it goes under "run"."""
+    return {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {scene.ray_count} rays, "
+                        f"{scene.max_iterations} refl, {len(scene.receivers)} receiver(s)",
+            "l2": "GPU arm: flushed between timed steps (512 MB write); CPU arm: n/a"}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -508,8 +515,7 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
            "data": "synthetic (seeded splitmix64 scene; no dataset)",
-           "config": {"workload": f"{args.config}: {scene.name}, {scene.n_faces} tri, {scene.ray_count} rays, "
-                                  f"{scene.max_iterations} refl, {len(scene.receivers)} receiver(s)", "parallelism": f"{threads} CPU threads"},
+           "config": bench_config(args, scene), "run": {"parallelism": f"{threads} CPU threads"},
            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": rates[0][3],
                             "sample": rates[0][2] + " per step"},
            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
