@@ -175,6 +175,17 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #ifndef RR_COOP
 #define RR_COOP 1  // 8-wide tracer: batched leaf tests spread over the whole warp (C5 434.7 -> 428.8 ms; 0: A/B)
 #endif
+#ifndef RR_PIPE
+// 8-wide visit: ALU-pipe work moved to the FMA pipe (bit mask; see wbyte,
+// visit_w8).  ncu (C5): ALU pipe 63 % busy, FMA pipe 22 %, issue 70 %: the
+// ALU pipe (one warp instruction per 2 cycles per SMSP, like the FMA pipe)
+// took the byte permutes, min / max, selects and compares.  1: near / far
+// planes by IMADs (427.3 -> 423.3 ms), 2: top bytes by IMAD.HI (425.6; 1|2
+// 421.8), 8: hit mask from FADD2 sign bits (1|2|8 417.0).  Tried and slower:
+// byte 2 by two IMADs (427.0), the nearest-slot keys by IMADs (421.6), the
+// octant permutation of the group mask as an L1 table (427.1).
+#define RR_PIPE 11
+#endif
 #ifndef RR_QMANT
 #define RR_QMANT 2  // 8-wide grid scales with 2 mantissa bits (0: powers of two; A/B)
 #endif
@@ -942,7 +953,31 @@ struct WVisit {
   uint32_t leafm, pairm;
 };
 
+// integer multiply-adds on the FMA pipe (the node visit is heavy on the ALU
+// pipe: byte permutes, min / max, selects, compares)
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// (a0 - b0, a1 - b1), one packed FADD
+__device__ __forceinline__ float2 fsub2(float a0, float a1, float b0, float b1) {
+  float2 r;
+  asm("{\n\t.reg .b64 A, B, D;\n\tmov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "sub.rn.f32x2 D, A, B;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  return r;
+}
 __device__ __forceinline__ float wbyte(uint32_t w, int k) {
+  // byte k & 3 of w as the fp32 2^23 + byte.  RR_PIPE & 2: the top byte as
+  // hi32(w * 2^8) + 0x4b000000 (one IMAD.HI; byte 2 by two IMADs too: slower)
+  if ((RR_PIPE & 2) && (k & 3) == 3) return __uint_as_float(imad_hi(w, 256u, 0x4b000000u));
   return __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440u | static_cast<uint32_t>(k & 3)));
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -983,9 +1018,24 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
 #define RR_WFMA2 fma2
 #endif
   // near / far plane words per axis from the ray's octant
+#if RR_PIPE & 1
+  // RR_PIPE & 1: near = lo + b (hi - lo), far = hi - b (hi - lo), b = 1 for
+  // a negative direction, as IMADs (FMA pipe) instead of 12 SELs (ALU pipe)
+  const uint32_t bx = px ? 0u : 1u, by = py ? 0u : 1u, bz = pz ? 0u : 1u;
+  const uint32_t dx0 = imad(qx.x, 0xffffffffu, qx.z), dx1 = imad(qx.y, 0xffffffffu, qx.w);
+  const uint32_t dy0 = imad(qy.x, 0xffffffffu, qy.z), dy1 = imad(qy.y, 0xffffffffu, qy.w);
+  const uint32_t dz0 = imad(qz.x, 0xffffffffu, qz.z), dz1 = imad(qz.y, 0xffffffffu, qz.w);
+  const uint32_t nx0 = imad(bx, dx0, qx.x), nx1 = imad(bx, dx1, qx.y), fx0 = imad(0u - bx, dx0, qx.z),
+                 fx1 = imad(0u - bx, dx1, qx.w);
+  const uint32_t ny0 = imad(by, dy0, qy.x), ny1 = imad(by, dy1, qy.y), fy0 = imad(0u - by, dy0, qy.z),
+                 fy1 = imad(0u - by, dy1, qy.w);
+  const uint32_t nz0 = imad(bz, dz0, qz.x), nz1 = imad(bz, dz1, qz.y), fz0 = imad(0u - bz, dz0, qz.z),
+                 fz1 = imad(0u - bz, dz1, qz.w);
+#else
   const uint32_t nx0 = px ? qx.x : qx.z, nx1 = px ? qx.y : qx.w, fx0 = px ? qx.z : qx.x, fx1 = px ? qx.w : qx.y;
   const uint32_t ny0 = py ? qy.x : qy.z, ny1 = py ? qy.y : qy.w, fy0 = py ? qy.z : qy.x, fy1 = py ? qy.w : qy.y;
   const uint32_t nz0 = pz ? qz.x : qz.z, nz1 = pz ? qz.y : qz.w, fz0 = pz ? qz.z : qz.x, fz1 = pz ? qz.w : qz.y;
+#endif
   const uint32_t bits = static_cast<uint32_t>(mm.w);
   const uint32_t cull = mm.z == rplane ? (bits >> 16) & 0xffu : 0u;
   uint32_t hit = 0;
@@ -1009,8 +1059,17 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
     const float tn1 = fmax3(nx.y, ny.y, fmaxf(nz.y, 0.0f)), tf1 = fmin3(fx.y, fy.y, fminf(fz.y, tmax));
     v.t[k] = tn0;
     v.t[k + 1] = tn1;
+#if RR_PIPE & 8
+    // RR_PIPE & 8: the misses from the sign bits of tf - tn (one packed FADD,
+    // sign bit = hi32(bits * 2)) gathered by IMADs, all on the FMA pipe:
+    // fl(tf - tn) < 0 exactly when tn > tf (a NaN counts as a hit)
+    const float2 dd = fsub2(tf0, tf1, tn0, tn1);
+    hit = imad(imad_hi(__float_as_uint(dd.x), 2u, 0u), 1u << k, hit);
+    hit = imad(imad_hi(__float_as_uint(dd.y), 2u, 0u), 2u << k, hit);
+#else
     hit |= (tn0 <= tf0 ? 1u : 0u) << k;
     hit |= (tn1 <= tf1 ? 2u : 0u) << k;
+#endif
 #else
     const float tn0 = fmax3(nx.x, ny.x, nz.x), tf0 = fmin3(fx.x, fy.x, fz.x);
     const float tn1 = fmax3(nx.y, ny.y, nz.y), tf1 = fmin3(fx.y, fy.y, fz.y);
@@ -1036,6 +1095,7 @@ __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t n
   }
 #endif
 #undef RR_WFMA2
+  if (RR_PIPE & 8) hit = ~hit;  // the misses gathered above
   v.hit = hit & bits & 0xffu & ~cull;
   v.imask = bits >> 24;
   v.child = mm.x;
