@@ -186,6 +186,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 // octant permutation of the group mask as an L1 table (427.1).
 #define RR_PIPE 11
 #endif
+#ifndef RR_RSM
+#define RR_RSM 1  // 8-wide tracer: the fp32 ray terms in shared memory (C5 417.9 -> 415.3 ms at the 196 KB carveout; 0: A/B)
+#endif
 #ifndef RR_QMANT
 #define RR_QMANT 2  // 8-wide grid scales with 2 mantissa bits (0: powers of two; A/B)
 #endif

@@ -36,6 +36,9 @@ constexpr int kStack8G = 32;  // 8-wide group traversal: one entry per level
 // equal carveouts it is neutral (8 entries 511, 4 entries 509).  Group
 // entries with the child / face bases (RR_GST, 12 B): 5 entries (164 KB)
 // 486.6 ms, 4 490, 2 503, 0 502, 8 (196 KB) 491; without, 8 entries 491.
+// With the fp32 ray terms in shared memory too (RR_RSM, +3 KB per block):
+// 5 entries (196 KB carveout) 415.3 ms, 3 (164 KB) 417.2; without RR_RSM 5
+// entries 417.9, 3 entries 425.9.
 #ifndef RR_SMS8
 #define RR_SMS8 (RR_HBUF ? 4 : RR_GST ? 5 : 8)
 #endif

@@ -89,6 +89,13 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
     int32_t ray, steps, bounces, pad;
   };
   __shared__ LaneState s_lane[128];
+#if RR_RSM
+  // the fp32 slab terms of the lane's ray (inv, -o * inv), column tid: read
+  // at every node visit from shared memory instead of spill slots (local
+  // memory, 22 % L1 hit rate under the node / face streams)
+  __shared__ float s_ray[6 * 128];
+  float* sry = s_ray + threadIdx.x;
+#endif
 #if RR_COOP
   __shared__ uint8_t s_item[128];  // per warp: lane (| 32 for a second face) of each stashed face
 #endif
@@ -231,6 +238,14 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
                                  tbest);
       node = t0 == kInf ? kDone : 0;
     }
+#if RR_RSM
+    sry[0] = r.ix;
+    sry[128] = r.iy;
+    sry[256] = r.iz;
+    sry[384] = r.nx;
+    sry[512] = r.ny;
+    sry[640] = r.nz;
+#endif
     px = r.ix >= 0.0f;
     py = r.iy >= 0.0f;
     pz = r.iz >= 0.0f;
@@ -383,7 +398,18 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel_w8(const TraceParams p
           WVisit v;
           RR_DCHECK(node < p.n_wnodes);
 #if RR_OCT  // the octant flags from the one octant word (fewer live registers)
+#if RR_RSM
+          RayF rs;
+          rs.ix = sry[0];
+          rs.iy = sry[128];
+          rs.iz = sry[256];
+          rs.nx = sry[384];
+          rs.ny = sry[512];
+          rs.nz = sry[640];
+          visit_w8(p.wnodes, node, rs, (oct & 1u) == 0u, (oct & 2u) == 0u, (oct & 4u) == 0u, tbest, rplane, v);
+#else
           visit_w8(p.wnodes, node, r, (oct & 1u) == 0u, (oct & 2u) == 0u, (oct & 4u) == 0u, tbest, rplane, v);
+#endif
 #else
           visit_w8(p.wnodes, node, r, px, py, pz, tbest, rplane, v);
 #endif
