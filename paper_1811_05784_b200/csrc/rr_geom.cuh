@@ -180,8 +180,10 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 // visit_w8).  ncu (C5): ALU pipe 63 % busy, FMA pipe 22 %, issue 70 %: the
 // ALU pipe (one warp instruction per 2 cycles per SMSP, like the FMA pipe)
 // took the byte permutes, min / max, selects and compares.  1: near / far
-// planes by IMADs (427.3 -> 423.3 ms), 2: top bytes by IMAD.HI (425.6; 1|2
-// 421.8), 8: hit mask from FADD2 sign bits (1|2|8 417.0).  Tried and slower:
+// planes by IMADs (427.3 -> 423.3 ms), 2: top bytes as mad.hi (ptxas emits
+// one LEA.HI with the 2^23 bits folded in: 425.6; 1|2 421.8), 8: hit mask
+// from FADD2 sign bits (LEA.HI) gathered by IMADs (1|2|8 417.0); forcing
+// IMAD.HI instead of LEA.HI costs 19 %.  Tried and slower:
 // byte 2 by two IMADs (427.0), the nearest-slot keys by IMADs (421.6), the
 // octant permutation of the group mask as an L1 table (427.1).
 #define RR_PIPE 11
@@ -979,7 +981,7 @@ __device__ __forceinline__ float2 fsub2(float a0, float a1, float b0, float b1) 
 }
 __device__ __forceinline__ float wbyte(uint32_t w, int k) {
   // byte k & 3 of w as the fp32 2^23 + byte.  RR_PIPE & 2: the top byte as
-  // hi32(w * 2^8) + 0x4b000000 (one IMAD.HI; byte 2 by two IMADs too: slower)
+  // hi32(w * 2^8) + 0x4b000000 (one LEA.HI; byte 2 by two IMADs too: slower)
   if ((RR_PIPE & 2) && (k & 3) == 3) return __uint_as_float(imad_hi(w, 256u, 0x4b000000u));
   return __uint_as_float(__byte_perm(w, 0x4b000000u, 0x7440u | static_cast<uint32_t>(k & 3)));
 }
