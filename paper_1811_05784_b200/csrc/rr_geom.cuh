@@ -149,7 +149,7 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 
 // 8-wide tracer options (rr_trace_w8.cuh)
 #ifndef RR_PF8
-#define RR_PF8 1  // prefetch a stashed leaf's faces into L2 (C5 -0.5 %; 2: into L1, 0: none)
+#define RR_PF8 0  // prefetch a stashed leaf's faces: 1 into L2, 2 into L1 (with the evict-first face loads: 0 406.5 ms, 1 409.0)
 #endif
 #ifndef RR_GST
 #define RR_GST 1  // group entries hold the node's child / face bases: no refetch at the pop (0: A/B)
@@ -164,7 +164,8 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #define RR_HIT2 1  // 8-wide slot test with the clamps folded into the 3-input min / max (C5 506 -> 493 ms; 0: A/B)
 #endif
 #ifndef RR_FCG
-#define RR_FCG 0  // A/B: face loads cached in L2 only (C5 508 -> 511 ms)
+#define RR_FCG 2  // face loads L1 evict-first, so the nodes and spill slots keep L1 (C5 414.3 -> 409.0 ms; 0: default
+                  // caching, 1: L2 only 429.0, 3: L1 no-allocate 414.9)
 #endif
 #ifndef RR_HBUF
 #define RR_HBUF 0  // 8-wide tracer: face history buffered per 32-B sector (rr_trace_w8.cuh; A/B)
@@ -190,6 +191,9 @@ __device__ __forceinline__ float box_enter(const RayF& r, float lx, float hx, fl
 #endif
 #ifndef RR_RSM
 #define RR_RSM 1  // 8-wide tracer: the fp32 ray terms in shared memory (C5 417.9 -> 415.3 ms at the 196 KB carveout; 0: A/B)
+#endif
+#ifndef RR_NEL
+#define RR_NEL 0  // A/B: 8-wide node loads with the L1 evict-last hint
 #endif
 #ifndef RR_QMANT
 #define RR_QMANT 2  // 8-wide grid scales with 2 mantissa bits (0: powers of two; A/B)
@@ -895,7 +899,21 @@ __device__ __forceinline__ HitResult closest_hit4(const TravHeader& h, const QNo
 // Moller-Trumbore on a leaf-ordered face (mt_delta's operations), face id out
 __device__ __forceinline__ double mt_delta_w(const FaceTri* __restrict__ wtri, int32_t t, D3 o, D3 d, int32_t* face) {
   const double2* p = reinterpret_cast<const double2*>(wtri + t);
-#if RR_FCG  // A/B: face loads cached in L2 only (L1 left to the nodes)
+#if RR_FCG == 2  // A/B: face loads marked L1 evict-first
+  double2 q0, q1, q2, q3, q4;
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(q0.x), "=d"(q0.y) : "l"(p));
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(q1.x), "=d"(q1.y) : "l"(p + 1));
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(q2.x), "=d"(q2.y) : "l"(p + 2));
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(q3.x), "=d"(q3.y) : "l"(p + 3));
+  asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(q4.x), "=d"(q4.y) : "l"(p + 4));
+#elif RR_FCG == 3  // A/B: face loads not allocated in L1
+  double2 q0, q1, q2, q3, q4;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(q0.x), "=d"(q0.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(q1.x), "=d"(q1.y) : "l"(p + 1));
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(q2.x), "=d"(q2.y) : "l"(p + 2));
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(q3.x), "=d"(q3.y) : "l"(p + 3));
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(q4.x), "=d"(q4.y) : "l"(p + 4));
+#elif RR_FCG  // A/B: face loads cached in L2 only (L1 left to the nodes)
   const double2 q0 = __ldcg(p), q1 = __ldcg(p + 1), q2 = __ldcg(p + 2), q3 = __ldcg(p + 3), q4 = __ldcg(p + 4);
 #else
   const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3), q4 = __ldg(p + 4);
@@ -999,11 +1017,27 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 __device__ __forceinline__ void visit_w8(const WNode* __restrict__ wn, int32_t node, const RayF& r, bool px, bool py,
                                          bool pz, float tmax, int32_t rplane, WVisit& v) {
   const float4* q = reinterpret_cast<const float4*>(wn + node);
+#if RR_NEL  // A/B: node loads marked L1 evict-last (the faces stream through)
+  float4 hh;
+  int4 mm;
+  uint4 qx, qy, qz;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(hh.x), "=f"(hh.y), "=f"(hh.z), "=f"(hh.w) : "l"(q));
+  asm("ld.global.nc.L1::evict_last.v4.s32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "l"(q + 1));
+  asm("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(qx.x), "=r"(qx.y), "=r"(qx.z), "=r"(qx.w) : "l"(q + 2));
+  asm("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(qy.x), "=r"(qy.y), "=r"(qy.z), "=r"(qy.w) : "l"(q + 3));
+  asm("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(qz.x), "=r"(qz.y), "=r"(qz.z), "=r"(qz.w) : "l"(q + 4));
+#else
   const float4 hh = __ldg(q);
   const int4 mm = __ldg(reinterpret_cast<const int4*>(q + 1));
   const uint4 qx = __ldg(reinterpret_cast<const uint4*>(q + 2));
   const uint4 qy = __ldg(reinterpret_cast<const uint4*>(q + 3));
   const uint4 qz = __ldg(reinterpret_cast<const uint4*>(q + 4));
+#endif
   const uint32_t hw = __float_as_uint(hh.w);
   // grid scales: (8 + RR_QMANT)-bit fields = the fp32 bits of 2^(e-127) (1 + j / 2^M)
   constexpr int kF = 8 + RR_QMANT;
