@@ -104,3 +104,29 @@ def test_unequal_receivers_auto_range_vs_reference(ctx, ref):
         total += len(oc)
     assert total == len(g)
     assert res.max_range == 0.5 * 1.0 * np.sqrt(n)  # rays die past the largest range
+
+
+@pytest.mark.parametrize("flags", TREES)
+def test_double_sided_walls_pair_leaves(ctx, port, flags):
+    """Every face duplicated with reversed winding at the next id (twins:
+    same centroid, ids 2i and 2i + 1), so every leaf of the SAH tree is a
+    2-face pair leaf and every closest hit is a tie broken by the face id.
+    On the 8-wide tree a warp then often stashes more than 32 faces at once,
+    which takes the per-lane fallback of the warp-cooperative leaf test
+    (rr_trace_w8.cuh, RR_COOP)."""
+    s = scenes.config1()
+    f = np.asarray(s.faces)  # (v0, v1, v2, material)
+    faces = np.empty((2 * len(f), f.shape[1]), dtype=f.dtype)
+    faces[0::2] = f
+    faces[1::2] = f
+    faces[1::2, 0], faces[1::2, 2] = f[:, 2], f[:, 0]
+    absorption = s.absorption
+    n = 20000
+    tree = AccelTree(TriangleMesh(s.vertices, faces, absorption), ctx)
+    res = trace(tree, SourceConfig(s.source, n), [Receiver(*s.receivers[0])],
+                TraceConfig(max_iterations=s.max_iterations, max_range=s.max_range), flags=flags)
+    oc, ost = port.scene(oracle.Mesh(s.vertices, faces, absorption)).trace(
+        s.source, n, [s.receivers[0][0]], [s.receivers[0][1]], s.max_iterations, s.max_range, THREADS)
+    assert res.ray_bounces == ost.ray_bounces and res.escaped == ost.escaped
+    assert len(res.captures) > 0
+    _captures_equal(res.captures, oc)
