@@ -54,7 +54,8 @@ constexpr int kSms8 = RR_SMS8;
                      // 4 / 2 428.8, 4 / 4 437.6, 2 / 2 435.9, 8 / 2 440.8, 3 / 1 431.3, 5 / 1 428.5, 6 / 1 431.2)
 #endif
 #ifndef RR_DONET8
-#define RR_DONET8 6  // lanes done before a warp leaves traversal for shading
+#define RR_DONET8 8  // lanes done before a warp leaves traversal for shading (final kernel: 5 / 6 / 7 / 8 / 9 / 10:
+                   // 409.8 / 406.4 / 404.8 / 404.4 / 404.7 / 405.7 ms)
 #endif
 
 __device__ __forceinline__ int64_t global_ray(const TraceParams& p, int64_t i) {
