@@ -15,8 +15,9 @@
 // node):
 //   expand: the slots of the node's optimal distribution (dp_unfold; the
 //           A/B alternative opens the internal child of largest surface area
-//           until 8 slots are used); leaves are the SAH tree's own 1- or
-//           2-face leaves;
+//           until 8 slots are used); leaf slots are the SAH tree's own 1- or
+//           2-face leaves, or two sibling single-face leaves as one pair
+//           slot over their parent's box;
 //   scan:   exclusive sum of (internal children, leaf faces) per node, so a
 //           node's internal children are contiguous one level down and its
 //           leaf faces contiguous in `wtri`;
@@ -57,6 +58,7 @@ struct Slot {
   float b[6];  // lo x, hi x, lo y, hi y, lo z, hi z (the TNode child box)
   int32_t ref;  // binary ref: >= 0 internal, < 0 leaf (~f or ~(f | kPairBit))
   int32_t plane;
+  int32_t ref2;  // >= 0: a pair slot of faces leaf_face(ref) and ref2 (two sibling leaves, RR_W8_PAIRS)
 };
 
 __device__ __forceinline__ void tnode_slot(const TNode& t, int side, Slot& s) {
@@ -64,10 +66,12 @@ __device__ __forceinline__ void tnode_slot(const TNode& t, int side, Slot& s) {
     s.b[0] = t.a.x; s.b[1] = t.a.y; s.b[2] = t.a.z; s.b[3] = t.a.w; s.b[4] = t.b.x; s.b[5] = t.b.y;
     s.ref = t.d.x;
     s.plane = t.d.z;
+    s.ref2 = -1;
   } else {
     s.b[0] = t.b.z; s.b[1] = t.b.w; s.b[2] = t.c.x; s.b[3] = t.c.y; s.b[4] = t.c.z; s.b[5] = t.c.w;
     s.ref = t.d.y;
     s.plane = t.d.w;
+    s.ref2 = -1;
   }
 }
 
@@ -110,9 +114,21 @@ __global__ void dp_init_kernel(const TNode* __restrict__ tn, int32_t n_int, int3
   arrived[n] = 0;
 }
 
-// F(c, k), k = 1..8, of slot s (its box from the parent's TNode)
-__device__ __forceinline__ void dp_child(const Slot& s, const DpRec* __restrict__ rec, float c_node, float c_face,
-                                         float* F) {
+// internal node c whose two children are single-face leaves: the faces
+// (they can share one pair slot, RR_W8_PAIRS)
+__device__ __forceinline__ bool pair_faces(const TNode* __restrict__ tn, int32_t c, int32_t* f1, int32_t* f2) {
+  const int4 d = tn[c].d;
+  if (d.x >= 0 || d.y >= 0 || leaf_faces(d.x) != 1 || leaf_faces(d.y) != 1) return false;
+  *f1 = leaf_face(d.x);
+  *f2 = leaf_face(d.y);
+  return true;
+}
+
+// F(c, k), k = 1..8, of slot s (its box from the parent's TNode); an
+// internal child whose two children are single faces may also become one
+// pair slot, cost A(c) c_face 2 (pairs != 0)
+__device__ __forceinline__ void dp_child(const TNode* __restrict__ tn, const Slot& s, const DpRec* __restrict__ rec,
+                                         float c_node, float c_face, int pairs, float* F) {
   const float A = half_area(s);
   if (s.ref < 0) {
     const float v = A * c_face * static_cast<float>(leaf_faces(s.ref));
@@ -124,21 +140,29 @@ __device__ __forceinline__ void dp_child(const Slot& s, const DpRec* __restrict_
   const float4* r = reinterpret_cast<const float4*>(rec + s.ref);
   const float4 g0 = __ldcg(r), g1 = __ldcg(r + 1);  // written by another thread of this launch
   g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
-  const float S = A * c_node + g[7];
+  int32_t f1, f2;
+  const float Sp = (pairs && pair_faces(tn, s.ref, &f1, &f2)) ? A * c_face * 2.0f : kInfCost;
+  const float S = fminf(A * c_node + g[7], Sp);
 #pragma unroll
   for (int k = 0; k < 8; ++k) F[k] = fminf(S, g[k]);
 }
 
-// single slot for child s given k slots (the choice dp_child's min made)
-__device__ __forceinline__ bool dp_single(const Slot& s, const DpRec* __restrict__ rec, float c_node, int k) {
-  if (s.ref < 0 || k == 1) return true;
-  const float S = half_area(s) * c_node + rec[s.ref].g[7];
-  return S <= rec[s.ref].g[k - 1];
+// the choice dp_child's min made for child s given k slots: 0 split it
+// further, 1 one slot as it is, 2 one pair slot
+__device__ __forceinline__ int dp_single(const TNode* __restrict__ tn, const Slot& s, const DpRec* __restrict__ rec,
+                                         float c_node, float c_face, int pairs, int k) {
+  if (s.ref < 0) return 1;
+  int32_t f1, f2;
+  const float A = half_area(s);
+  const float Sp = (pairs && pair_faces(tn, s.ref, &f1, &f2)) ? A * c_face * 2.0f : kInfCost;
+  const float Sw = A * c_node + rec[s.ref].g[7];
+  if (k > 1 && fminf(Sw, Sp) > rec[s.ref].g[k - 1]) return 0;
+  return Sp < Sw ? 2 : 1;
 }
 
 __global__ void dp_up_kernel(const TNode* __restrict__ tn, int32_t n_int, const int32_t* __restrict__ parent,
                              const int32_t* __restrict__ need, int32_t* __restrict__ arrived, DpRec* __restrict__ rec,
-                             float c_node, float c_face) {
+                             float c_node, float c_face, int pairs) {
   int32_t n = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (n >= n_int || need[n] != 0) return;
   for (;;) {
@@ -147,8 +171,8 @@ __global__ void dp_up_kernel(const TNode* __restrict__ tn, int32_t n_int, const 
     tnode_slot(t, 0, sl);
     tnode_slot(t, 1, sr);
     float FL[8], FR[8];
-    dp_child(sl, rec, c_node, c_face, FL);
-    dp_child(sr, rec, c_node, c_face, FR);
+    dp_child(tn, sl, rec, c_node, c_face, pairs, FL);
+    dp_child(tn, sr, rec, c_node, c_face, pairs, FR);
     DpRec o;
     o.g[0] = kInfCost;
     o.bestj = 0;
@@ -185,7 +209,7 @@ __global__ void dp_up_kernel(const TNode* __restrict__ tn, int32_t n_int, const 
 
 // the slots of binary node n as one wide node: G(n, 8) unfolded
 __device__ __forceinline__ int dp_unfold(const TNode* __restrict__ tn, const DpRec* __restrict__ rec, int32_t root,
-                                         float c_node, Slot* s) {
+                                         float c_node, float c_face, int pairs, Slot* s) {
   int32_t st_n[8];
   int st_i[8];
   int sp = 0, cnt = 0;
@@ -203,7 +227,14 @@ __device__ __forceinline__ int dp_unfold(const TNode* __restrict__ tn, const DpR
       Slot c;
       tnode_slot(t, side, c);
       const int kk = side == 0 ? k : j - k;
-      if (dp_single(c, rec, c_node, kk)) {
+      const int how = dp_single(tn, c, rec, c_node, c_face, pairs, kk);
+      if (how == 2) {  // the two leaves of c as one pair slot over c's box
+        int32_t f1 = 0, f2 = 0;
+        pair_faces(tn, c.ref, &f1, &f2);
+        c.ref = ~(f1 | kPairBit);
+        c.ref2 = f2;
+        s[cnt++] = c;
+      } else if (how == 1) {
         s[cnt++] = c;
       } else {
         st_n[sp] = c.ref;
@@ -225,13 +256,13 @@ __device__ __forceinline__ int dp_unfold(const TNode* __restrict__ tn, const DpR
 __global__ void expand_kernel(const TNode* __restrict__ tn, const int32_t* __restrict__ frontier, int32_t n,
                               Slot* __restrict__ slots, int32_t* __restrict__ nslot,
                               unsigned long long* __restrict__ packed, int order, const DpRec* __restrict__ rec,
-                              float c_node) {
+                              float c_node, float c_face, int pairs) {
   const int32_t i = static_cast<int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= n) return;
   Slot s[kW];
   int cnt = 2;
   if (rec) {
-    cnt = dp_unfold(tn, rec, frontier[i], c_node, s);
+    cnt = dp_unfold(tn, rec, frontier[i], c_node, c_face, pairs, s);
   } else {
     const TNode t = tn[frontier[i]];
     tnode_slot(t, 0, s[0]);
@@ -401,9 +432,10 @@ __global__ void write_kernel(const Slot* __restrict__ slots, const int32_t* __re
       const int nl = leaf_faces(s[k].ref);
       if (nl == 2) pair |= 1u << k;
       for (int j = 0; j < nl; ++j) {
-        RR_DCHECK(ti + nfc + j < n_faces && f0 + j < n_faces);
-        FaceTri ft = tri[f0 + j];
-        ft.pad = __longlong_as_double(static_cast<long long>(f0 + j));
+        const int32_t fj = (j == 1 && s[k].ref2 >= 0) ? s[k].ref2 : f0 + j;
+        RR_DCHECK(ti + nfc + j < n_faces && fj < n_faces);
+        FaceTri ft = tri[fj];
+        ft.pad = __longlong_as_double(static_cast<long long>(fj));
         wtri[ti + nfc + j] = ft;
       }
       nfc += nl;
@@ -458,13 +490,27 @@ void build_wide(rr_scene* s) {
   }();
   // RR_W8_DP (A/B): SAH-optimal collapse (1; C5 visits per ray-bounce
   // 19.73 -> 18.89, trace 468.2 -> 458.0 ms) or the greedy largest-area
-  // expansion (0).  The leaves are fixed, so the face-test cost only adds a
-  // constant: c_face 0.5 .. 3 built the same tree.
+  // expansion (0).
   static const int use_dp = [] {
     const char* e = std::getenv("RR_W8_DP");
     return e ? std::atoi(e) : 1;
   }();
-  const float c_node = 1.0f, c_face = 1.0f;
+  // RR_W8_PAIRS: two sibling single-face leaves may share one slot (a pair
+  // leaf of arbitrary faces, copied next to each other in wtri); RR_W8_CFACE:
+  // the face-test cost in node visits.  The warp-cooperative leaf tests make
+  // a face test cheap, so pairs pay almost always (C5, node visits / face
+  // tests per ray-bounce, ms): no pairs 17.93 / 4.38 404.4; c_face 2: 17.93
+  // / 4.38 404.5, 1: 17.80 / 4.51 400.8, 0.5: 17.62 / 4.81 396.1, 0.25:
+  // 17.56 / 4.98 394.8, 0.1 394.8, 0.05: 17.55 / 5.05 394.6, 0.01 394.6.
+  static const int pairs = [] {
+    const char* e = std::getenv("RR_W8_PAIRS");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const float c_face = [] {
+    const char* e = std::getenv("RR_W8_CFACE");
+    return e ? static_cast<float>(std::atof(e)) : 0.05f;
+  }();
+  const float c_node = 1.0f;
   DevBuf<DpRec> rec;
   if (use_dp) {
     DevBuf<int32_t> parent, need, arrived;
@@ -476,7 +522,7 @@ void build_wide(rr_scene* s) {
     dp_init_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, parent.p, need.p, arrived.p);
     RR_LAUNCH_CHECK();
     dp_up_kernel<<<grid(n_int), 256, 0, st>>>(s->snodes.p, n_int, parent.p, need.p, arrived.p, rec.p, c_node,
-                                              c_face);
+                                              c_face, pairs);
     RR_LAUNCH_CHECK();
     s->ctx->launches += 3;
   }
@@ -488,7 +534,7 @@ void build_wide(rr_scene* s) {
     packed.alloc(n + 1, st);
     offs.alloc(n + 1, st);
     expand_kernel<<<grid(n), 256, 0, st>>>(s->snodes.p, fr[0].p, n, slots.p, nslot.p, packed.p, slot_order,
-                                           use_dp ? rec.p : nullptr, c_node);
+                                           use_dp ? rec.p : nullptr, c_node, c_face, pairs);
     RR_LAUNCH_CHECK();
     RR_CUDA(cudaMemsetAsync(packed.p + n, 0, sizeof(unsigned long long), st));
     size_t need = 0;
