@@ -219,6 +219,20 @@ def cpu_reference_sample(scene, seconds, threads, stride=None):
         kind, rb, dt, stride
 
 
+def write_scene_bin(scene, path):
+    """The scene as tests/native/pipeline_bench.cpp reads it (receiver 0)."""
+    (c, r), = scene.receivers[:1]
+    with open(path, "wb") as f:
+        f.write(np.array([len(scene.vertices), len(scene.faces), len(scene.absorption)], np.int64).tobytes())
+        f.write(np.ascontiguousarray(scene.vertices, np.float64).tobytes())
+        f.write(np.ascontiguousarray(scene.faces, np.int32).tobytes())
+        f.write(np.ascontiguousarray(scene.absorption, np.float64).tobytes())
+        f.write(np.array(scene.source, np.float64).tobytes())
+        f.write(np.array([scene.ray_count], np.int64).tobytes())
+        f.write(np.array([*c, r, scene.max_range, scene.sample_rate], np.float64).tobytes())
+        f.write(np.array([scene.max_iterations, 1], np.int64).tobytes())
+
+
 def native_pipeline(scene, steps, warmup):
     """The C++ facade's run_trace_pipeline stages (tests/native/pipeline_bench.cpp:
     tree build, trace, image sources, pulse trains + IR, factors; host mesh
@@ -232,16 +246,7 @@ def native_pipeline(scene, steps, warmup):
                     "-lroomray_b200", "-Wl,-rpath," + lib_dir, "-o", exe], check=True)
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "scene.bin")
-        (c, r), = scene.receivers[:1]
-        with open(path, "wb") as f:
-            f.write(np.array([len(scene.vertices), len(scene.faces), len(scene.absorption)], np.int64).tobytes())
-            f.write(np.ascontiguousarray(scene.vertices, np.float64).tobytes())
-            f.write(np.ascontiguousarray(scene.faces, np.int32).tobytes())
-            f.write(np.ascontiguousarray(scene.absorption, np.float64).tobytes())
-            f.write(np.array(scene.source, np.float64).tobytes())
-            f.write(np.array([scene.ray_count], np.int64).tobytes())
-            f.write(np.array([*c, r, scene.max_range, scene.sample_rate], np.float64).tobytes())
-            f.write(np.array([scene.max_iterations, 1], np.int64).tobytes())
+        write_scene_bin(scene, path)
         out = subprocess.run([exe, path, str(steps), str(warmup)], capture_output=True, text=True, check=True).stdout
     return json.loads(out.strip().splitlines()[-1])
 

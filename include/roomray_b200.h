@@ -125,6 +125,15 @@ void* rr_ctx_stream(rr_ctx* ctx);
 /* Number of this library's kernels launched on the context so far. */
 int64_t rr_ctx_launches(rr_ctx* ctx);
 
+/* Page-locked host memory (cudaMallocHost) for staging buffers a caller
+ * reuses across calls: the copies of rr_scene_create, rr_trace_captures,
+ * rr_images_get and rr_images_pulse_trains run at full host-link speed from /
+ * into it, where pageable buffers go through the driver's bounce buffer.
+ * Not a reference interface (the reference has no device); the C++ façade
+ * keeps one grow-only buffer per thread.  bytes == 0 returns NULL. */
+rr_status rr_host_alloc(int64_t bytes, void** out);
+rr_status rr_host_free(void* p);
+
 /* ---------------------------------------------------------------- scene
  * TriangleMesh (geometry.hpp:60-77) + build_tree (accel_tree.hpp:38).
  * verts: nv*3 f64; tris: nf*4 i32 (a, b, c, material); alpha: nmat*8 f64.

@@ -34,6 +34,10 @@
 #include <string>
 #include <vector>
 
+#ifdef __linux__
+#include <sys/mman.h>
+#endif
+
 #include "roomray_b200.h"
 
 namespace roomray_b200 {
@@ -66,6 +70,101 @@ inline void check(rr_status s) {
   const std::string msg = rr_last_error();
   if (s == RR_INVALID_ARGUMENT) throw std::invalid_argument(msg);  // as the reference
   throw std::runtime_error("roomray_b200: " + msg);
+}
+
+// f(t, a, b) for the t-th of up to min(hw, 32) contiguous chunks [a, b) of
+// [0, n); one chunk (serial) below `serial_below` items
+template <typename F>
+inline void parallel_chunks(std::size_t n, F&& f, std::size_t serial_below = std::size_t(1) << 14) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = n < serial_below ? 1 : std::min<std::size_t>({hw, 32, n});
+  if (nt <= 1) {
+    if (n) f(std::size_t(0), std::size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::size_t chunk = (n + nt - 1) / nt;
+  for (std::size_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const std::size_t a = std::min(n, t * chunk), b = std::min(n, a + chunk);
+      if (a < b) f(t, a, b);
+    });
+  for (auto& x : th) x.join();
+}
+
+// f(i) for i in [0, n) on the host's hardware threads (the conversions of
+// device results into the reference's per-record std::vector types are
+// allocation bound); serial below 2^14 records
+template <typename F>
+inline void parallel_for(std::size_t n, F&& f, std::size_t serial_below = std::size_t(1) << 14) {
+  parallel_chunks(
+      n, [&](std::size_t, std::size_t a, std::size_t b) {
+        for (std::size_t i = a; i < b; ++i) f(i);
+      },
+      serial_below);
+}
+
+// One grow-only page-locked buffer per host thread (rr_host_alloc): device
+// results are copied into it at full host-link speed and converted from it,
+// so no pageable temporaries are zero-filled and faulted in on every call.
+class Staging {
+ public:
+  Staging() = default;
+  Staging(const Staging&) = delete;
+  Staging& operator=(const Staging&) = delete;
+  ~Staging() {
+    if (p_) rr_host_free(p_);  // status ignored: may run after the runtime's teardown
+  }
+  char* get(std::size_t bytes) {
+    if (bytes > cap_) {
+      if (p_) check(rr_host_free(p_));
+      p_ = nullptr;
+      cap_ = 0;
+      const std::size_t want = bytes + bytes / 4;
+      void* q = nullptr;
+      check(rr_host_alloc(static_cast<int64_t>(want), &q));
+      p_ = static_cast<char*>(q);
+      cap_ = want;
+    }
+    return p_;
+  }
+
+ private:
+  char* p_ = nullptr;
+  std::size_t cap_ = 0;
+};
+inline Staging& staging() {
+  thread_local Staging s;
+  return s;
+}
+
+// byte offsets of 256-B aligned arrays carved out of one staging buffer
+struct Layout {
+  std::size_t bytes = 0;
+  template <typename T>
+  std::size_t add(std::size_t n) {
+    const std::size_t o = (bytes + 255) & ~std::size_t(255);
+    bytes = o + n * sizeof(T);
+    return o;
+  }
+};
+template <typename T>
+inline T* at(char* base, std::size_t off) {
+  return reinterpret_cast<T*>(base + off);
+}
+
+// v.reserve(n), with transparent huge pages requested for the new storage:
+// the reference's record vectors run to hundreds of MB, and faulting them in
+// 4-KB pages inside their serial value-initialisation dominated the copies.
+template <typename T>
+inline void reserve_huge(std::vector<T>& v, std::size_t n) {
+  v.reserve(n);
+#ifdef __linux__
+  constexpr std::uintptr_t kHuge = std::uintptr_t(1) << 21;
+  const std::uintptr_t a = (reinterpret_cast<std::uintptr_t>(v.data()) + kHuge - 1) & ~(kHuge - 1);
+  const std::uintptr_t e = reinterpret_cast<std::uintptr_t>(v.data() + v.capacity()) & ~(kHuge - 1);
+  if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advisory: errors ignored
+#endif
 }
 }  // namespace detail
 
@@ -180,31 +279,47 @@ class AccelTree {
 /// or degenerate faces throw std::invalid_argument.
 inline AccelTree build_tree(const TriangleMesh& mesh, int device = 0) {
   Device& dev = Device::get(device);
-  std::vector<double> v(3 * mesh.vertices.size());
-  Aabb box;
-  box.min = {HUGE_VAL, HUGE_VAL, HUGE_VAL};
-  box.max = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
-  for (std::size_t i = 0; i < mesh.vertices.size(); ++i) {
-    for (int k = 0; k < 3; ++k) {
-      v[3 * i + k] = mesh.vertices[i][k];
-      box.min[k] = std::min(box.min[k], mesh.vertices[i][k]);
-      box.max[k] = std::max(box.max[k], mesh.vertices[i][k]);
-    }
+  const std::size_t nv = mesh.vertices.size(), nf = mesh.faces.size(), nm = std::max<std::size_t>(mesh.materials.size(), 1);
+  detail::Layout L;
+  const std::size_t o_v = L.add<double>(3 * nv), o_f = L.add<int32_t>(4 * nf), o_al = L.add<double>(kNumBands * nm);
+  char* base = detail::staging().get(L.bytes);
+  double* v = detail::at<double>(base, o_v);
+  int32_t* f = detail::at<int32_t>(base, o_f);
+  double* alpha = detail::at<double>(base, o_al);
+  // repack into the page-locked staging buffer (and the bounds) on the host threads
+  std::array<Aabb, 32> part;
+  for (auto& p : part) {
+    p.min = {HUGE_VAL, HUGE_VAL, HUGE_VAL};
+    p.max = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
   }
-  std::vector<int32_t> f(4 * mesh.faces.size());
-  for (std::size_t i = 0; i < mesh.faces.size(); ++i) {
+  detail::parallel_chunks(nv, [&](std::size_t t, std::size_t a, std::size_t b) {
+    Aabb& p = part[t];
+    for (std::size_t i = a; i < b; ++i)
+      for (int k = 0; k < 3; ++k) {
+        const double x = mesh.vertices[i][k];
+        v[3 * i + k] = x;
+        p.min[k] = std::min(p.min[k], x);
+        p.max[k] = std::max(p.max[k], x);
+      }
+  });
+  Aabb box = part[0];
+  for (const Aabb& p : part)
+    for (int k = 0; k < 3; ++k) {
+      box.min[k] = std::min(box.min[k], p.min[k]);
+      box.max[k] = std::max(box.max[k], p.max[k]);
+    }
+  detail::parallel_for(nf, [&](std::size_t i) {
     f[4 * i] = mesh.faces[i].a;
     f[4 * i + 1] = mesh.faces[i].b;
     f[4 * i + 2] = mesh.faces[i].c;
     f[4 * i + 3] = mesh.faces[i].material_id;
-  }
-  std::vector<double> alpha(kNumBands * std::max<std::size_t>(mesh.materials.size(), 1), 0.0);
+  });
+  std::fill(alpha, alpha + kNumBands * nm, 0.0);
   for (std::size_t m = 0; m < mesh.materials.size(); ++m)
     for (int b = 0; b < kNumBands; ++b) alpha[kNumBands * m + b] = mesh.materials[m].absorption[b];
   rr_scene* s = nullptr;
-  detail::check(rr_scene_create(dev.handle(), v.data(), static_cast<int64_t>(mesh.vertices.size()), f.data(),
-                                static_cast<int64_t>(mesh.faces.size()), alpha.data(),
-                                static_cast<int32_t>(std::max<std::size_t>(mesh.materials.size(), 1)), 1, &s));
+  detail::check(rr_scene_create(dev.handle(), v, static_cast<int64_t>(nv), f, static_cast<int64_t>(nf), alpha,
+                                static_cast<int32_t>(nm), 1, &s));
   AccelTree t;
   t.scene_.reset(s, [](rr_scene* p) { rr_scene_destroy(p); });
   int32_t root = -1, depth = 0;
@@ -314,37 +429,24 @@ struct TraceHandle {
 }  // namespace detail
 
 namespace detail {
-// f(i) for i in [0, n) on the host's hardware threads (the conversions of
-// device results into the reference's per-record std::vector types are
-// allocation bound); serial below 2^14 records
-template <typename F>
-inline void parallel_for(std::size_t n, F&& f) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const std::size_t nt = n < (std::size_t(1) << 14) ? 1 : std::min<std::size_t>(hw, 32);
-  if (nt <= 1) {
-    for (std::size_t i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::vector<std::thread> th;
-  const std::size_t chunk = (n + nt - 1) / nt;
-  for (std::size_t t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      const std::size_t a = t * chunk, b = std::min(n, a + chunk);
-      for (std::size_t i = a; i < b; ++i) f(i);
-    });
-  for (auto& x : th) x.join();
-}
-
 // host copy of a device trace (TraceResult, tracer.hpp:22-29)
 inline TraceResult trace_result_from(rr_trace_result* h) {
   rr_trace_stats st{};
   check(rr_trace_stats_get(h, &st));
   const std::size_t n = static_cast<std::size_t>(st.n_captures);
-  std::vector<int32_t> ray(n), hist(std::max<int64_t>(st.total_history, 1));
-  std::vector<double> point(3 * n), dir(3 * n), path(n), mult(kNumBands * n);
-  std::vector<int64_t> off(n + 1);
-  check(rr_trace_captures(h, nullptr, ray.data(), point.data(), dir.data(), path.data(), mult.data(), off.data(),
-                          hist.data()));
+  Layout L;
+  const std::size_t o_ray = L.add<int32_t>(n), o_hist = L.add<int32_t>(std::max<int64_t>(st.total_history, 1)),
+                    o_pt = L.add<double>(3 * n), o_dir = L.add<double>(3 * n), o_path = L.add<double>(n),
+                    o_mult = L.add<double>(kNumBands * n), o_off = L.add<int64_t>(n + 1);
+  char* base = staging().get(L.bytes);
+  const int32_t* ray = at<int32_t>(base, o_ray);
+  const int32_t* hist = at<int32_t>(base, o_hist);
+  const double *point = at<double>(base, o_pt), *dir = at<double>(base, o_dir), *path = at<double>(base, o_path),
+               *mult = at<double>(base, o_mult);
+  const int64_t* off = at<int64_t>(base, o_off);
+  check(rr_trace_captures(h, nullptr, at<int32_t>(base, o_ray), at<double>(base, o_pt), at<double>(base, o_dir),
+                          at<double>(base, o_path), at<double>(base, o_mult), at<int64_t>(base, o_off),
+                          at<int32_t>(base, o_hist)));
   TraceResult r;
   r.iterations = st.iterations;
   r.truncated = st.truncated != 0;
@@ -353,6 +455,7 @@ inline TraceResult trace_result_from(rr_trace_result* h) {
   r.max_range = st.max_range;
   r.ray_bounces = st.ray_bounces;
   r.kernel_ms = rr_trace_kernel_ms(h);
+  reserve_huge(r.captures, n);
   r.captures.resize(n);
   parallel_for(n, [&](std::size_t i) {
     Capture& c = r.captures[i];
@@ -361,7 +464,7 @@ inline TraceResult trace_result_from(rr_trace_result* h) {
     c.incoming_dir = {dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]};
     c.path_length = path[i];
     for (int b = 0; b < kNumBands; ++b) c.band_multiplier[b] = mult[kNumBands * i + b];
-    c.face_history.assign(hist.begin() + off[i], hist.begin() + off[i + 1]);
+    c.face_history.assign(hist + off[i], hist + off[i + 1]);
   });
   return r;
 }
@@ -553,12 +656,21 @@ inline std::vector<ImageSource> images_from(rr_images* im) {
   int64_t ni = 0, tp = 0;
   check(rr_images_info(im, &ni, &tp));
   const std::size_t m = static_cast<std::size_t>(ni);
-  std::vector<double> pos(3 * m), dist(m), en(kNumBands * m), mu(kNumBands * m), proj(3 * m);
-  std::vector<int32_t> cnt(m), order(m), hp(m), pth(std::max<int64_t>(tp, 1));
-  std::vector<int64_t> poff(m + 1);
-  check(rr_images_get(im, pos.data(), dist.data(), en.data(), mu.data(), cnt.data(), order.data(), hp.data(),
-                      proj.data(), poff.data(), pth.data()));
-  std::vector<ImageSource> out(m);
+  Layout L;
+  const std::size_t o_pos = L.add<double>(3 * m), o_dist = L.add<double>(m), o_en = L.add<double>(kNumBands * m),
+                    o_mu = L.add<double>(kNumBands * m), o_proj = L.add<double>(3 * m), o_cnt = L.add<int32_t>(m),
+                    o_order = L.add<int32_t>(m), o_hp = L.add<int32_t>(m),
+                    o_pth = L.add<int32_t>(std::max<int64_t>(tp, 1)), o_poff = L.add<int64_t>(m + 1);
+  char* base = staging().get(L.bytes);
+  double *pos = at<double>(base, o_pos), *dist = at<double>(base, o_dist), *en = at<double>(base, o_en),
+         *mu = at<double>(base, o_mu), *proj = at<double>(base, o_proj);
+  int32_t *cnt = at<int32_t>(base, o_cnt), *order = at<int32_t>(base, o_order), *hp = at<int32_t>(base, o_hp),
+          *pth = at<int32_t>(base, o_pth);
+  int64_t* poff = at<int64_t>(base, o_poff);
+  check(rr_images_get(im, pos, dist, en, mu, cnt, order, hp, proj, poff, pth));
+  std::vector<ImageSource> out;
+  reserve_huge(out, m);
+  out.resize(m);
   parallel_for(m, [&](std::size_t i) {
     ImageSource& s = out[i];
     s.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
@@ -569,7 +681,7 @@ inline std::vector<ImageSource> images_from(rr_images* im) {
     }
     s.ray_count = cnt[i];
     s.order = order[i];
-    s.face_path.assign(pth.begin() + poff[i], pth.begin() + poff[i + 1]);
+    s.face_path.assign(pth + poff[i], pth + poff[i + 1]);
     if (hp[i]) s.projection = Vec3{proj[3 * i], proj[3 * i + 1], proj[3 * i + 2]};
   });
   return out;
@@ -737,15 +849,25 @@ inline PulseTrains trains_from(rr_images* im, double speed_of_sound) {
   if (speed_of_sound <= 0.0) throw std::invalid_argument("speed of sound must be > 0");
   int64_t n = 0, tp = 0;
   check(rr_images_info(im, &n, &tp));
-  std::vector<int64_t> off(kNumBands + 1);
-  std::vector<double> t(kNumBands * std::max<int64_t>(n, 1)), a(kNumBands * std::max<int64_t>(n, 1));
-  check(rr_images_pulse_trains(im, speed_of_sound, off.data(), t.data(), a.data()));
+  Layout L;
+  const std::size_t o_off = L.add<int64_t>(kNumBands + 1), o_t = L.add<double>(kNumBands * std::max<int64_t>(n, 1)),
+                    o_a = L.add<double>(kNumBands * std::max<int64_t>(n, 1));
+  char* base = staging().get(L.bytes);
+  const int64_t* off = at<int64_t>(base, o_off);
+  const double *t = at<double>(base, o_t), *a = at<double>(base, o_a);
+  check(rr_images_pulse_trains(im, speed_of_sound, at<int64_t>(base, o_off), at<double>(base, o_t),
+                               at<double>(base, o_a)));
   PulseTrains trains;
-  for (int b = 0; b < kNumBands; ++b) {
-    trains[b].band = b;
-    trains[b].events.resize(static_cast<std::size_t>(n));
-    for (int64_t i = 0; i < n; ++i) trains[b].events[i] = {t[off[b] + i], a[off[b] + i]};
-  }
+  parallel_for(  // one band per thread
+      kNumBands,
+      [&](std::size_t b) {
+        trains[b].band = static_cast<int>(b);
+        auto& ev = trains[b].events;
+        reserve_huge(ev, static_cast<std::size_t>(n));
+        ev.resize(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) ev[i] = {t[off[b] + i], a[off[b] + i]};
+      },
+      0);
   return trains;
 }
 
@@ -754,15 +876,27 @@ inline RoomImpulseResponse rir_from(rr_images* im, const PulseTrains& trains, do
                                     double sample_rate, int taps = kBandFilterTaps) {
   RoomImpulseResponse rir;
   rir.sample_rate = sample_rate;
-  rir.band_trains = trains;
   int64_t length = 0;
   check(rr_images_synthesize(im, speed_of_sound, sample_rate, taps, &length, nullptr, nullptr));
-  if (length == 0) return rir;
-  std::vector<double> band(static_cast<std::size_t>(kNumBands * length));
-  rir.samples.assign(static_cast<std::size_t>(length), 0.0);
-  check(rr_images_synthesize(im, speed_of_sound, sample_rate, taps, &length, band.data(), rir.samples.data()));
-  for (int b = 0; b < kNumBands; ++b)
-    rir.band_samples[b].assign(band.begin() + b * length, band.begin() + (b + 1) * length);
+  double* band = nullptr;
+  if (length > 0) {
+    Layout L;
+    const std::size_t o_band = L.add<double>(kNumBands * length), o_sum = L.add<double>(length);
+    char* base = staging().get(L.bytes);
+    band = at<double>(base, o_band);
+    double* sum = at<double>(base, o_sum);
+    check(rr_images_synthesize(im, speed_of_sound, sample_rate, taps, &length, band, sum));
+    rir.samples.assign(sum, sum + length);
+  }
+  parallel_for(  // one band per thread: the band's copy of the trains and its filtered samples
+      kNumBands,
+      [&](std::size_t b) {
+        rir.band_trains[b].band = trains[b].band;
+        reserve_huge(rir.band_trains[b].events, trains[b].events.size());
+        rir.band_trains[b].events = trains[b].events;
+        if (band) rir.band_samples[b].assign(band + b * length, band + (b + 1) * length);
+      },
+      0);
   return rir;
 }
 

@@ -85,6 +85,8 @@ SIGNATURES = [
     ("rr_ctx_destroy", C.c_int, [_vp]),
     ("rr_ctx_stream", _vp, [_vp]),
     ("rr_ctx_launches", _i64, [_vp]),
+    ("rr_host_alloc", C.c_int, [_i64, C.POINTER(_vp)]),
+    ("rr_host_free", C.c_int, [_vp]),
     ("rr_scene_create", C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i32, _i32, C.POINTER(_vp)]),
     ("rr_scene_destroy", C.c_int, [_vp]),
     ("rr_scene_tree_info", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)]),

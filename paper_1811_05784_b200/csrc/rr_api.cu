@@ -265,6 +265,21 @@ rr_status rr_ctx_destroy(rr_ctx* ctx) {
   });
 }
 
+rr_status rr_host_alloc(int64_t bytes, void** out) {
+  return guarded([&] {
+    check_ptr(out, "out");
+    *out = nullptr;
+    if (bytes < 0) throw std::invalid_argument("bytes must be >= 0");
+    if (bytes > 0) RR_CUDA(cudaMallocHost(out, static_cast<size_t>(bytes)));
+  });
+}
+
+rr_status rr_host_free(void* p) {
+  return guarded([&] {
+    if (p) RR_CUDA(cudaFreeHost(p));
+  });
+}
+
 void* rr_ctx_stream(rr_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->stream) : nullptr; }
 int64_t rr_ctx_launches(rr_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 

@@ -52,6 +52,16 @@ def test_version_string():
     assert b"sm_100a" in lib.rr_version()
 
 
+def test_host_alloc_argument_errors():
+    # no device needed: size 0 returns NULL, a negative size is RR_INVALID_ARGUMENT, free(NULL) is a no-op
+    lib = _lib.load()
+    p = ctypes.c_void_p(1)
+    assert lib.rr_host_alloc(0, ctypes.byref(p)) == 0 and p.value is None
+    assert lib.rr_host_alloc(-8, ctypes.byref(p)) == 1
+    assert b"bytes" in lib.rr_last_error()
+    assert lib.rr_host_free(None) == 0
+
+
 def test_splitmix_golden_values():
     # splitmix64 reference outputs for seed 0 (first three)
     z = scenes.splitmix64(0, 3)
