@@ -1,9 +1,10 @@
 """The C++ facade (include/roomray_b200.hpp) as a reference user would call
 it: tests/native/facade_parity.cpp runs build_tree -> nearest_hit -> trace ->
 build_image_sources -> build_pulse_trains -> synthesize on the GPU and dumps
-the results, which must match the oracle: face paths, ray ids and counts exactly; positions to 1e-10
-(the device lattice's sin/cos is correctly rounded, glibc's is not on ~0.3 %
-of azimuths); the broadband RIR to 1e-6 of its peak."""
+the results, which must match the oracle: face paths, ray ids and counts exactly; positions to 1e-10;
+the broadband RIR to 1e-6 of its peak.  tests/native/facade_reuse.cpp checks
+that the façade's per-thread page-locked staging buffer, reused across calls
+of different sizes, leaves no stale data in the artifacts."""
 from __future__ import annotations
 
 import os
@@ -424,3 +425,18 @@ def test_run_artifacts_match_the_reference_writers(tmp_path, ref):
         assert cpa[k] == cpb[k], k
     assert [m["oracle_index"] for m in cpa["matched"]] == [m["oracle_index"] for m in cpb["matched"]]
     assert [m["traced_indices"] for m in cpa["matched"]] == [m["traced_indices"] for m in cpb["matched"]]
+
+
+@pytest.mark.gpu
+def test_facade_staging_reuse(tmp_path):
+    """run_trace_pipeline on a large room, a small room, then the large room
+    again: the repeated run's artifacts are byte-identical to the first."""
+    exe = str(tmp_path / "facade_reuse")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "native", "facade_reuse.cpp"), "-L",
+                    os.path.join(ROOT, "paper_1811_05784_b200"), "-lroomray_b200",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_1811_05784_b200"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    words = out.stdout.split()
+    assert words[0] == "ok" and int(words[1]) > 0 and int(words[2]) > 0 and int(words[3]) > 0, out.stdout
