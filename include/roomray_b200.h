@@ -373,6 +373,12 @@ rr_status rr_images_device(rr_images* im, const double** d_dist,
  * device; band_off 9 entries, may be NULL).  No host sort. */
 rr_status rr_images_pulse_trains(rr_images* im, double c, int64_t* band_off,
                                  double* time, double* amplitude);
+/* build_pulse_trains (rir.cpp:9-30) of host (or device) image data: dist n
+ * f64 (ImageSource::distance), energy n*8 f64 (band_energy rows); outputs as
+ * rr_images_pulse_trains, sorted on the device (the façade's
+ * build_pulse_trains(images, c) calls this instead of a host sort). */
+rr_status rr_pulse_trains(rr_ctx* ctx, int64_t n, const double* dist, const double* energy, double c,
+                          int64_t* band_off, double* time, double* amplitude);
 /* synthesize (rir.cpp:60-96) of a device image set.  With band_ir and
  * broadband both NULL: *length = the reference length llround(t_last*fs) +
  * (taps-1)/2 + 1 (0 without images).  Otherwise fills band_ir (8 x *length)

@@ -692,11 +692,21 @@ inline std::vector<ImageSource> build_image_sources(const std::vector<Capture>& 
                                                     const AirModel& air, const Vec3& receiver_center,
                                                     const TriangleMesh& /*mesh*/, const AccelTree& tree,
                                                     const ClusterOptions& options = {}) {
+  // the captures as flat arrays in the staging buffer: history offsets by a
+  // serial prefix sum, then every record on the host threads
   const std::size_t n = captures.size();
-  std::vector<int32_t> ray(n), hist;
-  std::vector<double> point(3 * n), dir(3 * n), path(n), mult(kNumBands * n);
   std::vector<int64_t> off(n + 1, 0);
-  for (std::size_t i = 0; i < n; ++i) {
+  for (std::size_t i = 0; i < n; ++i) off[i + 1] = off[i] + static_cast<int64_t>(captures[i].face_history.size());
+  detail::Layout L;
+  const std::size_t o_ray = L.add<int32_t>(n), o_pt = L.add<double>(3 * n), o_dir = L.add<double>(3 * n),
+                    o_path = L.add<double>(n), o_mult = L.add<double>(kNumBands * n),
+                    o_hist = L.add<int32_t>(std::max<int64_t>(off[n], 1));
+  char* base = detail::staging().get(L.bytes);
+  int32_t *ray = detail::at<int32_t>(base, o_ray), *hist = detail::at<int32_t>(base, o_hist);
+  double *point = detail::at<double>(base, o_pt), *dir = detail::at<double>(base, o_dir),
+         *path = detail::at<double>(base, o_path), *mult = detail::at<double>(base, o_mult);
+  hist[0] = 0;
+  detail::parallel_for(n, [&](std::size_t i) {
     const Capture& c = captures[i];
     ray[i] = c.ray_index;
     for (int k = 0; k < 3; ++k) {
@@ -705,14 +715,12 @@ inline std::vector<ImageSource> build_image_sources(const std::vector<Capture>& 
     }
     path[i] = c.path_length;
     for (int b = 0; b < kNumBands; ++b) mult[kNumBands * i + b] = c.band_multiplier[b];
-    hist.insert(hist.end(), c.face_history.begin(), c.face_history.end());
-    off[i + 1] = static_cast<int64_t>(hist.size());
-  }
-  if (hist.empty()) hist.push_back(0);
+    std::copy(c.face_history.begin(), c.face_history.end(), hist + off[i]);
+  });
   rr_receiver rc{{receiver_center.x, receiver_center.y, receiver_center.z}, 1.0};
   rr_trace_result* h = nullptr;
-  detail::check(rr_captures_import(tree.handle(), static_cast<int64_t>(n), nullptr, ray.data(), point.data(),
-                                   dir.data(), path.data(), mult.data(), off.data(), hist.data(), &rc, 1, &h));
+  detail::check(rr_captures_import(tree.handle(), static_cast<int64_t>(n), nullptr, ray, point, dir, path, mult,
+                                   off.data(), hist, &rc, 1, &h));
   detail::TraceHandle guard(h);
   rr_air a{air.enabled ? 1 : 0, air.temperature_c, air.relative_humidity, air.pressure_kpa};
   rr_cluster_options o{options.tol_scale, options.merge_coplanar ? 1 : 0};
@@ -744,23 +752,76 @@ struct RoomImpulseResponse {
 
 /// build_pulse_trains (rir.cpp:9-30): one event per image per band at
 /// t = d / c with amplitude sqrt(E), each train sorted by (time, amplitude).
+namespace detail {
+// the 8 sorted trains of n events each at [off[b], off[b+1]) of t / a
+// (rr_pulse_trains, rr_images_pulse_trains) as PulseTrains, one band per thread
+inline PulseTrains trains_unpack(int64_t n, const int64_t* off, const double* t, const double* a) {
+  PulseTrains trains;
+  parallel_for(
+      kNumBands,
+      [&](std::size_t b) {
+        trains[b].band = static_cast<int>(b);
+        auto& ev = trains[b].events;
+        reserve_huge(ev, static_cast<std::size_t>(n));
+        ev.resize(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) ev[i] = {t[off[b] + i], a[off[b] + i]};
+      },
+      0);
+  return trains;
+}
+
+// the trains' events as flat arrays (band b at [off[b], off[b+1])) in the
+// staging buffer, one band per thread; `extra_doubles` more doubles are
+// reserved after them (returned through *extra)
+struct PackedTrains {
+  std::array<int64_t, kNumBands + 1> off{};
+  double *t = nullptr, *a = nullptr, *extra = nullptr;
+};
+inline PackedTrains pack_trains(const PulseTrains& trains, std::size_t extra_doubles = 0) {
+  PackedTrains p;
+  for (int b = 0; b < kNumBands; ++b) p.off[b + 1] = p.off[b] + static_cast<int64_t>(trains[b].events.size());
+  const std::size_t total = static_cast<std::size_t>(p.off[kNumBands]);
+  Layout L;
+  const std::size_t o_t = L.add<double>(std::max<std::size_t>(total, 1)),
+                    o_a = L.add<double>(std::max<std::size_t>(total, 1)), o_x = L.add<double>(extra_doubles);
+  char* base = staging().get(L.bytes);
+  p.t = at<double>(base, o_t);
+  p.a = at<double>(base, o_a);
+  p.extra = at<double>(base, o_x);
+  parallel_for(
+      kNumBands,
+      [&](std::size_t b) {
+        const auto& ev = trains[b].events;
+        for (std::size_t i = 0; i < ev.size(); ++i) {
+          p.t[p.off[b] + i] = ev[i].time_s;
+          p.a[p.off[b] + i] = ev[i].amplitude;
+        }
+      },
+      0);
+  return p;
+}
+}  // namespace detail
+
+/// build_pulse_trains (rir.cpp:9-30): t = d / c and sqrt(E_b) per image and
+/// band, sorted by (time, amplitude) on the device (rr_pulse_trains).
 inline PulseTrains build_pulse_trains(const std::vector<ImageSource>& images, double speed_of_sound) {
   if (speed_of_sound <= 0.0) throw std::invalid_argument("speed of sound must be > 0");
-  PulseTrains trains;
-  for (int b = 0; b < kNumBands; ++b) {
-    trains[b].band = b;
-    trains[b].events.reserve(images.size());
-  }
-  for (const ImageSource& im : images) {
-    const double t = im.distance / speed_of_sound;
-    for (int b = 0; b < kNumBands; ++b) trains[b].events.push_back({t, std::sqrt(im.band_energy[b])});
-  }
-  for (auto& tr : trains)
-    std::sort(tr.events.begin(), tr.events.end(), [](const PulseEvent& a, const PulseEvent& b) {
-      if (a.time_s != b.time_s) return a.time_s < b.time_s;
-      return a.amplitude < b.amplitude;
-    });
-  return trains;
+  const std::size_t n = images.size();
+  detail::Layout L;
+  const std::size_t o_d = L.add<double>(std::max<std::size_t>(n, 1)),
+                    o_e = L.add<double>(kNumBands * std::max<std::size_t>(n, 1)), o_off = L.add<int64_t>(kNumBands + 1),
+                    o_t = L.add<double>(kNumBands * std::max<std::size_t>(n, 1)),
+                    o_a = L.add<double>(kNumBands * std::max<std::size_t>(n, 1));
+  char* base = detail::staging().get(L.bytes);
+  double *dist = detail::at<double>(base, o_d), *en = detail::at<double>(base, o_e);
+  detail::parallel_for(n, [&](std::size_t i) {
+    dist[i] = images[i].distance;
+    for (int b = 0; b < kNumBands; ++b) en[kNumBands * i + b] = images[i].band_energy[b];
+  });
+  int64_t* off = detail::at<int64_t>(base, o_off);
+  double *t = detail::at<double>(base, o_t), *a = detail::at<double>(base, o_a);
+  detail::check(rr_pulse_trains(Device::get(0).handle(), static_cast<int64_t>(n), dist, en, speed_of_sound, off, t, a));
+  return detail::trains_unpack(static_cast<int64_t>(n), off, t, a);
 }
 
 /// design_band_filter (rir.cpp:32-58), `taps` taps (reference: 1023).
@@ -776,29 +837,38 @@ inline std::vector<double> design_band_filter(int band, double sample_rate, int 
 inline RoomImpulseResponse synthesize(const PulseTrains& trains, double sample_rate, int taps = kBandFilterTaps) {
   RoomImpulseResponse rir;
   rir.sample_rate = sample_rate;
-  rir.band_trains = trains;
-  std::vector<int64_t> off(kNumBands + 1, 0);
-  std::vector<double> t, a;
-  double last = 0.0;
-  bool any = false;
-  for (int b = 0; b < kNumBands; ++b) {
-    for (const PulseEvent& e : trains[b].events) {
-      if (e.time_s < 0.0) throw std::invalid_argument("pulse events cannot precede t = 0");
-      t.push_back(e.time_s);
-      a.push_back(e.amplitude);
-      last = std::max(last, e.time_s);
-      any = true;
-    }
-    off[b + 1] = static_cast<int64_t>(t.size());
-  }
-  if (!any) return rir;
-  const int64_t length = static_cast<int64_t>(std::llround(last * sample_rate)) + (taps - 1) / 2 + 1;
-  std::vector<double> band(static_cast<std::size_t>(kNumBands * length));
-  rir.samples.assign(static_cast<std::size_t>(length), 0.0);
-  detail::check(rr_synthesize_trains(Device::get(0).handle(), off.data(), t.data(), a.data(), sample_rate, taps,
-                                     length, band.data(), rir.samples.data()));
+  // per band (one thread each): the copy into rir.band_trains, the latest
+  // event and the t >= 0 check
+  std::array<double, kNumBands> last{};
+  std::array<int, kNumBands> negative{};
+  detail::parallel_for(
+      kNumBands,
+      [&](std::size_t b) {
+        rir.band_trains[b].band = trains[b].band;
+        detail::reserve_huge(rir.band_trains[b].events, trains[b].events.size());
+        rir.band_trains[b].events = trains[b].events;
+        double m = 0.0;
+        for (const PulseEvent& e : trains[b].events) {
+          if (e.time_s < 0.0) negative[b] = 1;
+          m = std::max(m, e.time_s);
+        }
+        last[b] = m;
+      },
+      0);
   for (int b = 0; b < kNumBands; ++b)
-    rir.band_samples[b].assign(band.begin() + b * length, band.begin() + (b + 1) * length);
+    if (negative[b]) throw std::invalid_argument("pulse events cannot precede t = 0");
+  std::size_t total = 0;
+  for (const auto& tr : trains) total += tr.events.size();
+  if (total == 0) return rir;
+  const double t_last = *std::max_element(last.begin(), last.end());
+  const int64_t length = static_cast<int64_t>(std::llround(t_last * sample_rate)) + (taps - 1) / 2 + 1;
+  const detail::PackedTrains p = detail::pack_trains(trains, static_cast<std::size_t>((kNumBands + 1) * length));
+  double *band = p.extra, *sum = p.extra + kNumBands * length;
+  detail::check(rr_synthesize_trains(Device::get(0).handle(), p.off.data(), p.t, p.a, sample_rate, taps, length, band,
+                                     sum));
+  rir.samples.assign(sum, sum + length);
+  detail::parallel_for(
+      kNumBands, [&](std::size_t b) { rir.band_samples[b].assign(band + b * length, band + (b + 1) * length); }, 0);
   return rir;
 }
 
@@ -826,17 +896,9 @@ inline PerceptiveFactors to_factors(const rr_factors& f) {
 
 /// factors(const PulseTrains&) (metrics.hpp:56-60) on the GPU.
 inline BandFactors factors(const PulseTrains& trains) {
-  std::vector<int64_t> off(kNumBands + 1, 0);
-  std::vector<double> t, a;
-  for (int b = 0; b < kNumBands; ++b) {
-    for (const PulseEvent& e : trains[b].events) {
-      t.push_back(e.time_s);
-      a.push_back(e.amplitude);
-    }
-    off[b + 1] = static_cast<int64_t>(t.size());
-  }
+  const detail::PackedTrains p = detail::pack_trains(trains);
   rr_factors out[kNumBands + 1];
-  detail::check(rr_band_factors(Device::get(0).handle(), off.data(), t.data(), a.data(), out));
+  detail::check(rr_band_factors(Device::get(0).handle(), p.off.data(), p.t, p.a, out));
   BandFactors bf;
   for (int b = 0; b < kNumBands; ++b) bf.bands[b] = detail::to_factors(out[b]);
   bf.mid = detail::to_factors(out[kNumBands]);
@@ -857,18 +919,7 @@ inline PulseTrains trains_from(rr_images* im, double speed_of_sound) {
   const double *t = at<double>(base, o_t), *a = at<double>(base, o_a);
   check(rr_images_pulse_trains(im, speed_of_sound, at<int64_t>(base, o_off), at<double>(base, o_t),
                                at<double>(base, o_a)));
-  PulseTrains trains;
-  parallel_for(  // one band per thread
-      kNumBands,
-      [&](std::size_t b) {
-        trains[b].band = static_cast<int>(b);
-        auto& ev = trains[b].events;
-        reserve_huge(ev, static_cast<std::size_t>(n));
-        ev.resize(static_cast<std::size_t>(n));
-        for (int64_t i = 0; i < n; ++i) ev[i] = {t[off[b] + i], a[off[b] + i]};
-      },
-      0);
-  return trains;
+  return trains_unpack(n, off, t, a);
 }
 
 // synthesize(trains) of a device image set (the trains' events are the images')

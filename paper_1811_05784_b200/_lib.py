@@ -137,6 +137,7 @@ SIGNATURES = [
     ("rr_factors_from_images", C.c_int, [_vp, _i64, _vp, _vp, _d, _vp]),
     ("rr_images_factors", C.c_int, [_vp, _d, _vp]),
     ("rr_images_pulse_trains", C.c_int, [_vp, _d, _vp, _vp, _vp]),
+    ("rr_pulse_trains", C.c_int, [_vp, _i64, _vp, _vp, _d, _vp, _vp, _vp]),
     ("rr_images_synthesize", C.c_int, [_vp, _d, _d, _i32, C.POINTER(_i64), _vp, _vp]),
     ("rr_comm_unique_id", C.c_int, [_vp]),
     ("rr_comm_init", C.c_int, [_vp, _vp, _i32, _i32, C.POINTER(_vp)]),

@@ -1145,6 +1145,30 @@ rr_status rr_images_pulse_trains(rr_images* im, double c, int64_t* band_off, dou
   });
 }
 
+rr_status rr_pulse_trains(rr_ctx* ctx, int64_t n, const double* dist, const double* energy, double c,
+                          int64_t* band_off, double* time, double* amplitude) {
+  return guarded([&] {
+    check_ptr(ctx, "context");
+    if (c <= 0.0) rr::invalid("speed of sound must be > 0");  // rir.cpp:11-13
+    if (n < 0) rr::invalid("n must be >= 0");
+    RR_CUDA(cudaSetDevice(ctx->device));
+    if (band_off)
+      for (int b = 0; b <= rr::kBands; ++b) band_off[b] = b * n;
+    if (n == 0) return;
+    check_ptr(dist, "dist");
+    check_ptr(energy, "energy");
+    check_ptr(time, "time");
+    check_ptr(amplitude, "amplitude");
+    cudaStream_t st = ctx->stream;
+    rr::DevBuf<double> d, e;
+    d.alloc(n, st);
+    e.alloc(rr::kBands * n, st);
+    RR_CUDA(cudaMemcpyAsync(d.p, dist, sizeof(double) * n, cudaMemcpyDefault, st));
+    RR_CUDA(cudaMemcpyAsync(e.p, energy, sizeof(double) * rr::kBands * n, cudaMemcpyDefault, st));
+    rr::image_trains(ctx, d.p, e.p, n, c, time, amplitude);  // synchronizes the stream
+  });
+}
+
 rr_status rr_images_synthesize(rr_images* im, double c, double fs, int32_t taps, int64_t* length, double* band_ir,
                                double* broadband) {
   return guarded([&] {

@@ -5,6 +5,7 @@
 //
 //   native_breakdown <scene.bin> <steps> <warmup>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <fstream>
 #include <map>
@@ -91,6 +92,39 @@ int main(int argc, char** argv) {
     a.metrics = rb::detail::factors_from(im, cfg.speed_of_sound);
     mark("5 metrics");
     rr_images_destroy(im);
+    // the same stages through the reference's stage-by-stage API (host
+    // vectors between the calls, pipeline.cpp:163-178's sequence)
+    last = clk::now();
+    const rb::TraceResult tr = rb::trace(a.mesh, a.tree, cfg.source, cfg.receiver, tc);
+    mark("s1 trace()");
+    const auto imgs = rb::build_image_sources(tr.captures, cfg.source.ray_count, cfg.air, cfg.receiver.center, a.mesh,
+                                              a.tree, rb::ClusterOptions{1e-6, cfg.merge_coplanar});
+    mark("s2 build_image_sources()");
+    const rb::PulseTrains trains = rb::build_pulse_trains(imgs, cfg.speed_of_sound);
+    mark("s3 build_pulse_trains()");
+    const rb::RoomImpulseResponse rir = rb::synthesize(trains, cfg.sample_rate);
+    mark("s4 synthesize()");
+    const rb::BandFactors bf = rb::factors(trains);
+    mark("s5 factors()");
+    if (imgs.size() != a.images.size() || rir.samples != a.rir.samples) {
+      std::size_t bad_img = imgs.size(), bad_s = rir.samples.size();
+      for (std::size_t i = 0; i < std::min(imgs.size(), a.images.size()); ++i)
+        if (imgs[i].distance != a.images[i].distance || imgs[i].face_path != a.images[i].face_path ||
+            imgs[i].band_energy != a.images[i].band_energy) {
+          bad_img = i;
+          break;
+        }
+      double md = 0.0, peak = 0.0;
+      for (std::size_t i = 0; i < std::min(rir.samples.size(), a.rir.samples.size()); ++i) {
+        md = std::max(md, std::fabs(rir.samples[i] - a.rir.samples[i]));
+        peak = std::max(peak, std::fabs(a.rir.samples[i]));
+        if (bad_s == rir.samples.size() && rir.samples[i] != a.rir.samples[i]) bad_s = i;
+      }
+      std::printf("stage-by-stage vs pipeline: images %zu / %zu, first differing image %zu; samples %zu / %zu, "
+                  "first differing %zu, max |diff| %.3g of peak %.3g\n",
+                  imgs.size(), a.images.size(), bad_img, rir.samples.size(), a.rir.samples.size(), bad_s, md, peak);
+    }
+    (void)bf;
     if (it >= warmup)
       for (auto& kv : st) acc[kv.first] += kv.second;
     const auto t0 = clk::now();

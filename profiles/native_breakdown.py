@@ -2,6 +2,8 @@
 on a bench config: device work vs device->host copies vs host-side struct building.
 
     python profiles/native_breakdown.py [c5] [steps] [warmup]
+
+RR_BREAKDOWN_INCLUDE=<dir> compiles against another copy of the façade headers (A/B).
 """
 import os
 import subprocess
@@ -19,9 +21,10 @@ def main():
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     warmup = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     lib_dir = os.path.join(ROOT, "paper_1811_05784_b200")
-    exe = os.path.join(ROOT, "build", "native_breakdown")
+    inc = os.environ.get("RR_BREAKDOWN_INCLUDE", os.path.join(ROOT, "include"))
+    exe = os.path.join(ROOT, "build", "native_breakdown_" + str(abs(hash(inc)) % 10**6))
     os.makedirs(os.path.dirname(exe), exist_ok=True)
-    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", inc,
                     os.path.join(ROOT, "profiles", "native_breakdown.cpp"), "-L", lib_dir, "-lroomray_b200",
                     "-Wl,-rpath," + lib_dir, "-o", exe], check=True)
     scene = bench.load_scene(cfg)
